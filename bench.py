@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""Benchmark: rendered receiver-query spectra/s (BASELINE.json metric).
+
+Workload (N=1, BASELINE.json configs[1]): synthetic scene of 100k Gaussians
+(l_max=2, C=1), one transmitter, a batch of 1024 unseen receiver positions,
+90x360 az/el spectrum + RSSI per receiver, receiver-conditioned (full mode,
+F=6 d=64 d_c=16 S=16, 32^3 occupancy).  One step = build the transmitter
+state (projection, basis, tile sort, FP64 blend walk) + render the receiver
+batch (conditioning fused with the FLE reduction, compositing, spectrum/RSSI
+epilogue).  Multi-GPU (torchrun): weak scaling, every rank renders its own
+1024-receiver shard of the query grid against the replicated scene; no
+data-path collective (timing uses a barrier and a max-reduce only).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rendered Rx-query spectra/sec at N Gaussians (1/2/4/8 B200) vs host-CPU ref"
+UNIT = "spectra/s"
+TX = (0.3, -0.2, 0.1)
+BOX_LO, BOX_HI = (-4.0, -3.0, -1.5), (4.0, 3.0, 1.5)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--gaussians", type=int, default=100_000)
+    ap.add_argument("--rx", type=int, default=1024, help="receivers per rank per step")
+    ap.add_argument("--n-theta", type=int, default=90)
+    ap.add_argument("--n-phi", type=int, default=360)
+    ap.add_argument("--cpu-sample", type=int, default=0, help="receivers in the CPU baseline sample (0=auto)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(args):
+    return {"workload": "config2: synthetic scene, 1 Tx x receiver batch, spectrum + RSSI",
+            "gaussians": args.gaussians, "l_max": 2, "channels": 1,
+            "grid": f"{args.n_theta}x{args.n_phi}", "tile": 8,
+            "rx_per_rank": args.rx, "conditioning": "full F6 d64 dc16 S16 R32",
+            "step": "build_tx_state + render_queries(batch)",
+            "l2": "flushed (256 MiB write) between timed steps",
+            "parallelism": "receiver shards, scene replicated"}
+
+
+def make_inputs(args, lib, rank):
+    sc = lib.synth_scene(args.gaussians, 2, 1, 7)
+    rx = lib.synth_points(args.rx, 11 + 1000 * rank, "bench.rx", BOX_LO, BOX_HI, 0.05)
+    return sc, rx
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{device}.csv")
+
+    def start(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU reference
+def cpu_reference_run(args, sample, threads):
+    """The reference's own CPU path (oracle/_ref: the unmodified reference
+    sources, see oracle/Makefile) on a bounded receiver sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O  # cpu_baseline leg: the one place bench.py executes oracle/
+    chk = O.reference()
+    kind = "reference"
+    if chk is None:
+        raise RuntimeError("oracle/_ref/librxgs_ref.so missing (build() compiles it where /root/reference exists)")
+    sc = chk.synth_scene(args.gaussians, 2, 1, 7)
+    h = chk.scene(sc, "spectrum")
+    lo, hi = chk.scene_bounds(h, 0.0)
+    cfg = O.cond_cfg()
+    params = chk.synth_cond(cfg, 2, 1, lo, hi, 3, True)
+    olo, ohi = chk.scene_bounds(h, 0.1)
+    occ = chk.build_occupancy(h, 32, olo, ohi)
+    cond = chk.cond(cfg, params, occ, olo, ohi)
+    rx = chk.synth_points(sample, 11, "bench.rx", BOX_LO, BOX_HI, 0.05)
+    grid = O.Grid(args.n_theta, args.n_phi, 8, 1.0)
+    secs, _, _ = chk.bench_queries(h, cond, grid, TX, rx, threads)
+    return secs, kind
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2605_24290_b200 import capi
+
+    dev = torch.device("cuda", local)
+    sc, rx_np = make_inputs(args, capi, rank)
+    ctx = capi.Context(local)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+    scene = ctx.scene(sc, "spectrum")
+    lo, hi = scene.bounds(0.0)
+    cfg = capi.cond_cfg()
+    params = capi.synth_cond(cfg, 2, 1, lo, hi, 3, True)
+    cond = ctx.cond(cfg, params)
+    olo, ohi = scene.bounds(0.1)
+    cond.build_occupancy(scene, 32, olo, ohi)
+    grid = capi.Grid(args.n_theta, args.n_phi, 8, 1.0)
+    tx = np.array(TX)
+    n = args.rx
+    P = grid.cells
+
+    rx_dev = torch.from_numpy(rx_np).to(dev)
+    spec_dev = torch.empty((n, args.n_theta, args.n_phi), dtype=torch.float32, device=dev)
+    rssi_dev = torch.empty(n, dtype=torch.float32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step_device():
+        st = scene.tx_state(tx, grid)
+        scene.render_queries(cond, st, rx_dev, spec_dev, rssi_dev)
+        return st
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step_device()
+    barrier()
+
+    # ---------------- device-resident timed region
+    ctx.reset_stats()
+    ctx.profile(True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = ctx.launch_count()
+    barrier()
+    keep = []
+    for i in range(args.steps):
+        flush.fill_(float(i))  # L2 flush between timed steps (outside the events)
+        starts[i].record(stream)
+        keep.append(step_device())
+        ends[i].record(stream)
+    barrier()
+    clk = clocks.stop()
+    launches = ctx.launch_count() - launches0
+    ms_steps = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms_local = sum(ms_steps) / len(ms_steps)
+    cond_ms, cond_n, cond_rows = ctx.kernel_stats("cond_signal")
+    comp_ms, comp_n, _ = ctx.kernel_stats("composite")
+    walk_ms, _, _ = ctx.kernel_stats("walk")
+    ctx.profile(False)
+    stats = keep[-1].stats()
+    del keep
+
+    ms = torch.tensor([ms_local], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_max = float(ms.item())
+    value = world * n / (ms_max / 1e3)
+
+    # ---------------- end-to-end through the C-ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        rx_host = torch.from_numpy(rx_np.copy()).pin_memory()
+        spec_host = torch.empty((n, args.n_theta, args.n_phi), dtype=torch.float32).pin_memory()
+        rssi_host = torch.empty(n, dtype=torch.float32).pin_memory()
+        rx_h, spec_h, rssi_h = rx_host.numpy(), spec_host.numpy(), rssi_host.numpy()
+        tx_h = np.array(TX)
+
+        def step_e2e():
+            st = scene.tx_state(tx_h, grid)
+            scene.render_queries(cond, st, rx_h, spec_h, rssi_h)
+
+        for _ in range(max(1, args.warmup)):
+            step_e2e()
+        barrier()
+        t_ms = []
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            torch.cuda.synchronize(dev)
+            s = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            t0 = time.perf_counter()
+            step_e2e()
+            e.record(stream)
+            torch.cuda.synchronize(dev)
+            t_ms.append(max((time.perf_counter() - t0) * 1e3, s.elapsed_time(e)))
+        em = torch.tensor([sum(t_ms) / len(t_ms)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(em, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * n / (float(em.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(n * 3 * 8 + 3 * 8),
+               "d2h_bytes_per_step": int(n * P * 4 + n * 4),
+               "ms_per_step": float(em.item())}
+
+    # ---------------- roofline of the dominant kernel (cond_signal)
+    d, S, L, C = 64, 16, 9, 1
+    flop_row = 2 * (6 * d + d * d + 4 * C * d) + S * 30 + 20 + L * C * 16
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peak, peak_src = 1590.0, "fallback (B200_PROFILING.md)"
+    if os.path.exists(peaks_path):
+        pk = json.load(open(peaks_path))
+        peak, peak_src = float(pk.get("bf16_tflops", 1590.0)), "measured bf16_tflops (MEASURED_PEAKS.json)"
+    roofline = None
+    if cond_n:
+        per_launch_rows = cond_rows / cond_n
+        avg_ms = cond_ms / cond_n
+        achieved = flop_row * per_launch_rows / (avg_ms / 1e3) / 1e12
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": None,
+                    "kernel": "k_cond_signal (local MLP + probe + FLE reduction)",
+                    "pipe": "fp32 SIMT (tcgen05 port pending)", "peak_source": peak_src,
+                    "flop_per_row": flop_row, "rows_per_launch": per_launch_rows,
+                    "kernel_ms": avg_ms,
+                    "share_of_step": (cond_ms / cond_n) / ms_local,
+                    "composite_ms": comp_ms / max(comp_n, 1), "walk_ms": walk_ms / max(comp_n, 1)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        sample = args.cpu_sample or 64
+        try:
+            secs, kind = cpu_reference_run(args, sample, threads)
+            cpu = {"value": sample / secs, "unit": UNIT, "cores": threads, "kind": kind,
+                   "sample": f"{sample} receivers of the same workload (K={args.gaussians}, "
+                             f"{args.n_theta}x{args.n_phi}), build_tx_state + condition_forward (fanned over "
+                             f"{threads} threads) + render_field (chunks of 16, {threads} threads) + "
+                             f"spectrum/RSSI aggregation; {secs:.1f} s wall"}
+        except Exception as ex:  # reported, never fatal
+            cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference", "error": str(ex)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32 (FP64 geometry/walk)", "data": "synthetic",
+                "config": workload(args), "e2e": e2e, "gpu_launches": int(launches),
+                "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
+                "tx_state": stats}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    sample = args.cpu_sample or 32
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        cpu_reference_run(args, min(sample, 4), threads)
+    t = []
+    for _ in range(args.steps):
+        secs, kind = cpu_reference_run(args, sample, threads)
+        t.append(secs)
+    v = sample / (sum(t) / len(t))
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * sum(t) / len(t), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload(args), "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": f"{sample} receivers per step of the same workload"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,182 @@
+/* include/rxgs_b200.h -- C-ABI of the B200-native RxGS render path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, int status codes,
+ * thread-local error text, no C++ or torch types.  Each entry point names the
+ * reference interface it replaces (paths relative to /root/reference/proj).
+ * The reference is a static C++ library with no FFI; the header-only C++
+ * shim include/rxgs_b200.hpp re-exposes these calls under the reference's
+ * own rxgs::raster / rxgs::cond / rxgs::train names and exception types.
+ *
+ * Pointers: every array argument may be HOST or DEVICE memory (detected with
+ * cudaPointerGetAttributes).  Host outputs are written before the call
+ * returns; device outputs are written in stream order on the context stream.
+ * Layouts follow the reference exactly:
+ *   scene coefficients   ((k*L + l)*C + c)*2 + {re,im}          scene.hpp:16-18
+ *   per-rx coefficients  (((j*K + k)*L + l)*C + c)*2 + {re,im}   sphraster.hpp:92-93
+ *   field values         [j][c][re/im][row][col]                 sphraster.hpp:83
+ *   transmittance        [j][row][col]                           sphraster.hpp:84
+ * Modality: 0 rssi, 1 csi, 2 spectrum (channelsim.hpp:79).
+ * Conditioning mode: 0 full, 1 global_only, 2 local_only, 3 additive_only,
+ * 4 no_occlusion (conditioning.hpp:55).
+ */
+#ifndef RXGS_B200_H
+#define RXGS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RXGS_OK 0
+#define RXGS_ERR_INVALID 1 /* reference: std::invalid_argument */
+#define RXGS_ERR_RUNTIME 2 /* reference: std::runtime_error    */
+#define RXGS_ERR_CUDA 3    /* device / driver failure          */
+
+typedef struct rxgs_ctx_s* rxgs_ctx;
+typedef struct rxgs_scene_s* rxgs_scene;
+typedef struct rxgs_txstate_s* rxgs_txstate;
+typedef struct rxgs_cond_s* rxgs_cond;
+
+/* raster::SphericalGrid (sphraster.hpp:15-32). */
+typedef struct rxgs_grid {
+    int32_t n_theta, n_phi, tile_size, reserved;
+    double radius, theta_min, theta_max;
+} rxgs_grid;
+
+/* Thread-local text of the last failing call on this thread ("" if none).
+ * Messages match the reference's exception text, e.g.
+ * "render_field: non-finite coefficient at rx 1, gaussian 0". */
+const char* rxgs_last_error(void);
+int rxgs_version(void);
+
+/* ------------------------------------------------------------ context */
+int rxgs_ctx_create(int device, rxgs_ctx* out);
+int rxgs_ctx_destroy(rxgs_ctx ctx);
+/* Use an external cudaStream_t (e.g. torch's current stream); NULL = own. */
+int rxgs_ctx_set_stream(rxgs_ctx ctx, void* cuda_stream);
+int rxgs_ctx_synchronize(rxgs_ctx ctx);
+/* Per-kernel CUDA-event timing of the hot kernels (off by default). */
+int rxgs_ctx_profile(rxgs_ctx ctx, int enable);
+/* Totals since the last reset for one kernel name ("cond_local", "composite",
+ * "walk", "tx_prep", "cond_global", "signal", ...).  Synchronizes. */
+int rxgs_ctx_kernel_stats(rxgs_ctx ctx, const char* name, double* total_ms, int64_t* launches,
+                          double* work_units);
+int rxgs_ctx_reset_stats(rxgs_ctx ctx);
+/* Number of kernels of this library launched since the last reset. */
+int64_t rxgs_ctx_launch_count(rxgs_ctx ctx);
+
+/* ------------------------------------------------------------ synthetic inputs
+ * DESIGN.md section 5 (bit-identical to oracle/ and to the reference-side
+ * harness; built on the reference RNG, rng.hpp:17-72). */
+int rxgs_synth_scene(int k, int l_max, int channels, uint64_t seed, double* positions,
+                     double* log_scales, double* quaternions, double* tau_logits,
+                     double* fle_coeffs);
+int rxgs_synth_points(int n, uint64_t seed, const char* tag, const double lo[3],
+                      const double hi[3], double margin, double* out);
+/* Returns the packed parameter count; params may be NULL to query it. */
+int64_t rxgs_synth_cond(const int32_t cfg[9], int l_max, int channels, const double lo[3],
+                        const double hi[3], uint64_t seed, int randomize, double* params);
+
+/* ------------------------------------------------------------ scene
+ * GaussianScene (scene.hpp:19-48) upload. */
+int rxgs_scene_create(rxgs_ctx ctx, int k, int l_max, int channels, int modality,
+                      const double* positions, const double* log_scales,
+                      const double* quaternions, const double* tau_logits,
+                      const double* fle_coeffs, rxgs_scene* out);
+int rxgs_scene_destroy(rxgs_scene scene);
+/* GaussianScene::position_bounds().inflated(f) (scene.cpp:18-30). */
+int rxgs_scene_bounds(rxgs_scene scene, double inflate, double lo[3], double hi[3]);
+
+/* ------------------------------------------------------------ transmitter state
+ * raster::build_tx_state (sphraster.cpp:150-172): projection
+ * (project_gaussian :22-83, FP64), FLE basis (radiance.cpp:79-92), per-tile
+ * depth-sorted lists (bin_and_sort :85-102) and the receiver-independent
+ * front-to-back blend weights of every cell (render_field :285-298). */
+int rxgs_tx_state_build(rxgs_ctx ctx, rxgs_scene scene, const double tx[3],
+                        const rxgs_grid* grid, rxgs_txstate* out);
+int rxgs_tx_state_destroy(rxgs_txstate st);
+int64_t rxgs_tx_state_entries(rxgs_txstate st);
+/* Materialise TxState fields (sphraster.hpp:52-61).  Any pointer may be NULL.
+ * geom per Gaussian = theta, phi, depth, cov a b c d, prec a b c d,
+ * weight_scale (12 f64); spans = t0 t1 p0 p1; basis K*L complex (2 f64);
+ * offsets n_tiles+1 (int64); indices = concatenated tile lists (int32). */
+int rxgs_tx_state_get(rxgs_txstate st, int32_t* culled, double* geom, int32_t* spans,
+                      double* basis, int64_t* offsets, int32_t* indices);
+/* Sort keys in list order: (tile << 32) | depth_rank, depth_rank = position
+ * of the Gaussian in the (depth, index) order of all Gaussians. */
+int rxgs_tx_state_keys(rxgs_txstate st, uint64_t* keys);
+/* Receiver-independent statistics: visible Gaussians, list entries,
+ * mean walk per cell, mean tile-walk per cell (roofline inputs). */
+int rxgs_tx_state_stats(rxgs_txstate st, int64_t* visible, int64_t* entries, double* walk_per_cell,
+                        double* tile_walk_per_cell);
+/* Per-cell final transmittance (cells f64); identical for every receiver. */
+int rxgs_tx_state_transmittance(rxgs_txstate st, double* out);
+
+/* raster::bin_and_sort on caller-supplied projections (sphraster.cpp:85-102):
+ * culled[k], depth[k], spans[k*4].  Writes offsets (n_tiles+1) and, when
+ * cap >= entries, indices; *entries receives the total. */
+int rxgs_bin_and_sort(rxgs_ctx ctx, int k, const int32_t* culled, const double* depth,
+                      const int32_t* spans, const rxgs_grid* grid, int64_t* offsets,
+                      int32_t* indices, int64_t cap, int64_t* entries);
+
+/* ------------------------------------------------------------ render
+ * raster::render_field(TxState, scene, coeffs, n_rx) (sphraster.cpp:255-315)
+ * with the reference's materialised per-receiver coefficient tensor
+ * (n_rx*K*L*C*2 f64).  values / transmittance in the reference layouts. */
+int rxgs_render_field(rxgs_ctx ctx, rxgs_txstate st, rxgs_scene scene, const double* coeffs,
+                      int n_rx, double* values, double* transmittance);
+
+/* raster::aggregate_modality (sphraster.cpp:323-381).  out: rssi n_rx f64;
+ * csi n_rx*C*2; spectrum n_rx*H*W. */
+int rxgs_aggregate_modality(rxgs_ctx ctx, const rxgs_grid* grid, int modality, int n_rx,
+                            int channels, const double* values, double* out);
+
+/* ------------------------------------------------------------ conditioning
+ * cond::ConditioningState (conditioning.hpp:72-92).  cfg = {F, hidden, d_c,
+ * S, R, nearest_lookup, mode, l_max, C}; params packed as
+ * freqs | global l1.w l1.b l2.w l2.b l3.w l3.b | embed | local (same six).
+ * occupancy: R^3 f64 (index (ix*R+iy)*R+iz) or NULL for an empty grid. */
+int rxgs_cond_create(rxgs_ctx ctx, const int32_t cfg[9], const double* params,
+                     const double* occupancy, const double occ_lo[3], const double occ_hi[3],
+                     rxgs_cond* out);
+int rxgs_cond_destroy(rxgs_cond c);
+int64_t rxgs_cond_param_count(rxgs_cond c);
+/* Per-branch MLP invocation counters (conditioning.hpp:81-82). */
+int rxgs_cond_calls(rxgs_cond c, int64_t* global_calls, int64_t* local_calls);
+/* cond::build_occupancy (conditioning.cpp:114-161) on device; out R^3 f64 may
+ * be NULL.  If attach_to is non-NULL the grid becomes its occupancy. */
+int rxgs_build_occupancy(rxgs_ctx ctx, rxgs_scene scene, int resolution, const double lo[3],
+                         const double hi[3], double* out, rxgs_cond attach_to);
+/* cond::probe_segment (conditioning.cpp:163-178) for n segments against the
+ * conditioning state's occupancy (device FP32): out n*2 = (T, mean). */
+int rxgs_probe_segments(rxgs_ctx ctx, rxgs_cond c, int n, const double* from, const double* to,
+                        double* out);
+/* cond::condition_forward (conditioning.cpp:284-423) for one receiver:
+ * out K*L*C*2.  local_in (K*6) may be NULL (ConditionWorkspace::local_in). */
+int rxgs_condition_forward(rxgs_ctx ctx, rxgs_cond c, rxgs_scene scene, const double rx[3],
+                           double* out, double* local_in);
+/* cond::condition_batch (conditioning.cpp:425-435): out n_rx*K*L*C*2. */
+int rxgs_condition_batch(rxgs_ctx ctx, rxgs_cond c, rxgs_scene scene, const double* rx, int n_rx,
+                         double* out);
+
+/* ------------------------------------------------------------ batched queries
+ * The hot path: train::predict (trainer.cpp:147-154) batched over receivers
+ * (paper Algorithm 1) without materialising N*K*L*C*2 coefficients:
+ * conditioning (global + local branch) fused with the FLE basis reduction,
+ * then front-to-back compositing with the spectrum / RSSI epilogue.
+ * rx: n_rx*3 f64.  out_spectrum: n_rx*H*W f32 (may be NULL); out_rssi: n_rx
+ * f32 dB (may be NULL).  cond may be NULL (unconditioned model). */
+int rxgs_render_queries(rxgs_ctx ctx, rxgs_scene scene, rxgs_cond c, rxgs_txstate st,
+                        const double* rx, int n_rx, float* out_spectrum, float* out_rssi);
+
+/* train::predict for one (tx, rx): builds the TxState internally; out is the
+ * scene modality's measurement (spectrum H*W, rssi 1, csi C*2) in f64. */
+int rxgs_predict(rxgs_ctx ctx, rxgs_scene scene, rxgs_cond c, const rxgs_grid* grid,
+                 const double tx[3], const double rx[3], double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RXGS_B200_H */

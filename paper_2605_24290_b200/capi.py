@@ -1,0 +1,417 @@
+"""ctypes binding of the C-ABI in include/rxgs_b200.h (librxgs_b200.so).
+
+This is plumbing for Python callers (tests, bench.py): every call goes
+straight to the native library; there is no Python or CPU compute path.  If
+the shared library is missing the import fails loudly.
+
+Arrays may be numpy (host) or anything exposing ``data_ptr()`` (a CUDA torch
+tensor, passed as a device pointer).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "librxgs_b200.so")
+
+RXGS_OK, RXGS_ERR_INVALID, RXGS_ERR_RUNTIME, RXGS_ERR_CUDA = 0, 1, 2, 3
+MODALITY = {"rssi": 0, "csi": 1, "spectrum": 2}
+MODE = {"full": 0, "global_only": 1, "local_only": 2, "additive_only": 3, "no_occlusion": 4}
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (the B200 path has no fallback)")
+
+_lib = C.CDLL(LIB_PATH)
+_vp = C.c_void_p
+_i32 = C.c_int32
+_i64 = C.c_int64
+
+
+class Grid(C.Structure):
+    """raster::SphericalGrid (sphraster.hpp:15-32) as rxgs_grid."""
+    _fields_ = [("n_theta", _i32), ("n_phi", _i32), ("tile_size", _i32), ("reserved", _i32),
+                ("radius", C.c_double), ("theta_min", C.c_double), ("theta_max", C.c_double)]
+
+    def __init__(self, n_theta=1, n_phi=1, tile_size=8, radius=1.0, theta_min=0.0,
+                 theta_max=3.14159265358979323846):
+        super().__init__(int(n_theta), int(n_phi), int(tile_size), 0, float(radius), float(theta_min),
+                         float(theta_max))
+
+    @property
+    def tiles_theta(self):
+        return (self.n_theta + self.tile_size - 1) // self.tile_size
+
+    @property
+    def tiles_phi(self):
+        return (self.n_phi + self.tile_size - 1) // self.tile_size
+
+    @property
+    def n_tiles(self):
+        return self.tiles_theta * self.tiles_phi
+
+    @property
+    def cells(self):
+        return self.n_theta * self.n_phi
+
+
+_SIG = {
+    "rxgs_last_error": (C.c_char_p, []),
+    "rxgs_version": (C.c_int, []),
+    "rxgs_ctx_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
+    "rxgs_ctx_destroy": (C.c_int, [_vp]),
+    "rxgs_ctx_set_stream": (C.c_int, [_vp, _vp]),
+    "rxgs_ctx_synchronize": (C.c_int, [_vp]),
+    "rxgs_ctx_profile": (C.c_int, [_vp, C.c_int]),
+    "rxgs_ctx_kernel_stats": (C.c_int, [_vp, C.c_char_p, C.POINTER(C.c_double), C.POINTER(_i64),
+                                        C.POINTER(C.c_double)]),
+    "rxgs_ctx_reset_stats": (C.c_int, [_vp]),
+    "rxgs_ctx_launch_count": (_i64, [_vp]),
+    "rxgs_synth_scene": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint64, _vp, _vp, _vp, _vp, _vp]),
+    "rxgs_synth_points": (C.c_int, [C.c_int, C.c_uint64, C.c_char_p, _vp, _vp, C.c_double, _vp]),
+    "rxgs_synth_cond": (_i64, [_vp, C.c_int, C.c_int, _vp, _vp, C.c_uint64, C.c_int, _vp]),
+    "rxgs_scene_create": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp,
+                                    C.POINTER(_vp)]),
+    "rxgs_scene_destroy": (C.c_int, [_vp]),
+    "rxgs_scene_bounds": (C.c_int, [_vp, C.c_double, _vp, _vp]),
+    "rxgs_tx_state_build": (C.c_int, [_vp, _vp, _vp, C.POINTER(Grid), C.POINTER(_vp)]),
+    "rxgs_tx_state_destroy": (C.c_int, [_vp]),
+    "rxgs_tx_state_entries": (_i64, [_vp]),
+    "rxgs_tx_state_get": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "rxgs_tx_state_keys": (C.c_int, [_vp, _vp]),
+    "rxgs_tx_state_stats": (C.c_int, [_vp, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double)]),
+    "rxgs_tx_state_transmittance": (C.c_int, [_vp, _vp]),
+    "rxgs_bin_and_sort": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, C.POINTER(Grid), _vp, _vp, _i64,
+                                    C.POINTER(_i64)]),
+    "rxgs_render_field": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int, _vp, _vp]),
+    "rxgs_aggregate_modality": (C.c_int, [_vp, C.POINTER(Grid), C.c_int, C.c_int, C.c_int, _vp, _vp]),
+    "rxgs_cond_create": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(_vp)]),
+    "rxgs_cond_destroy": (C.c_int, [_vp]),
+    "rxgs_cond_param_count": (_i64, [_vp]),
+    "rxgs_cond_calls": (C.c_int, [_vp, C.POINTER(_i64), C.POINTER(_i64)]),
+    "rxgs_build_occupancy": (C.c_int, [_vp, _vp, C.c_int, _vp, _vp, _vp, _vp]),
+    "rxgs_probe_segments": (C.c_int, [_vp, _vp, C.c_int, _vp, _vp, _vp]),
+    "rxgs_condition_forward": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "rxgs_condition_batch": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int, _vp]),
+    "rxgs_render_queries": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp]),
+    "rxgs_predict": (C.c_int, [_vp, _vp, _vp, C.POINTER(Grid), _vp, _vp, _vp]),
+}
+for _name, (_res, _args) in _SIG.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTED = tuple(_SIG)
+
+
+class RxgsError(Exception):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+class InvalidArgument(RxgsError, ValueError):
+    """The reference's std::invalid_argument."""
+
+
+def _check(rc):
+    if rc != RXGS_OK:
+        msg = _lib.rxgs_last_error().decode()
+        if rc == RXGS_ERR_INVALID:
+            raise InvalidArgument(rc, msg)
+        raise RxgsError(rc, msg)
+
+
+_keep: list = []
+
+
+def ptr(a, dtype=None):
+    """Raw pointer of a numpy array (converted to a contiguous `dtype`) or a torch tensor."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return C.c_void_p(a.data_ptr())
+    arr = np.ascontiguousarray(a, dtype=dtype) if dtype is not None else np.ascontiguousarray(a)
+    _keep.append(arr)
+    if len(_keep) > 64:
+        del _keep[:32]
+    return C.c_void_p(arr.ctypes.data)
+
+
+def _out(shape, dtype=np.float64):
+    return np.empty(shape, dtype)
+
+
+# ------------------------------------------------------------------ synthetic inputs
+def synth_scene(k, l_max=2, channels=1, seed=7):
+    L = (l_max + 1) ** 2
+    pos, ls, q, tau = _out((k, 3)), _out((k, 3)), _out((k, 4)), _out(k)
+    co = _out((k, L, channels, 2))
+    _check(_lib.rxgs_synth_scene(k, l_max, channels, seed, pos.ctypes.data, ls.ctypes.data, q.ctypes.data,
+                                 tau.ctypes.data, co.ctypes.data))
+    return dict(positions=pos, log_scales=ls, quaternions=q, tau_logits=tau, fle_coeffs=co, l_max=l_max,
+                channels=channels)
+
+
+def synth_points(n, seed, tag, lo, hi, margin=0.05):
+    out = _out((n, 3))
+    lo = np.asarray(lo, np.float64)
+    hi = np.asarray(hi, np.float64)
+    _check(_lib.rxgs_synth_points(n, seed, tag.encode(), lo.ctypes.data, hi.ctypes.data, margin, out.ctypes.data))
+    return out
+
+
+def cond_cfg(F=6, hidden=64, dc=16, S=16, R=32, nearest=0, mode="full", l_max=2, C_=1):
+    return np.array([F, hidden, dc, S, R, nearest, MODE[mode] if isinstance(mode, str) else mode, l_max, C_],
+                    np.int32)
+
+
+def synth_cond(cfg, l_max, channels, lo, hi, seed=3, randomize=True):
+    cfg = np.asarray(cfg, np.int32)
+    lo = np.asarray(lo, np.float64)
+    hi = np.asarray(hi, np.float64)
+    n = _lib.rxgs_synth_cond(cfg.ctypes.data, l_max, channels, lo.ctypes.data, hi.ctypes.data, seed,
+                             int(randomize), None)
+    out = _out(n)
+    _lib.rxgs_synth_cond(cfg.ctypes.data, l_max, channels, lo.ctypes.data, hi.ctypes.data, seed, int(randomize),
+                         out.ctypes.data)
+    return out
+
+
+# ------------------------------------------------------------------ handles
+class Context:
+    def __init__(self, device=0):
+        h = _vp()
+        _check(_lib.rxgs_ctx_create(device, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.rxgs_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def set_stream(self, stream_handle):
+        _check(_lib.rxgs_ctx_set_stream(self.h, C.c_void_p(stream_handle) if stream_handle else None))
+
+    def synchronize(self):
+        _check(_lib.rxgs_ctx_synchronize(self.h))
+
+    def profile(self, enable=True):
+        _check(_lib.rxgs_ctx_profile(self.h, int(enable)))
+
+    def kernel_stats(self, name):
+        ms, n, w = C.c_double(), _i64(), C.c_double()
+        _check(_lib.rxgs_ctx_kernel_stats(self.h, name.encode(), C.byref(ms), C.byref(n), C.byref(w)))
+        return ms.value, n.value, w.value
+
+    def reset_stats(self):
+        _check(_lib.rxgs_ctx_reset_stats(self.h))
+
+    def launch_count(self):
+        return int(_lib.rxgs_ctx_launch_count(self.h))
+
+    # ---------------------------------------------------------- objects
+    def scene(self, sc, modality="spectrum"):
+        return Scene(self, sc, modality)
+
+    def cond(self, cfg, params, occ=None, lo=None, hi=None):
+        return Cond(self, cfg, params, occ, lo, hi)
+
+    def bin_and_sort(self, culled, depth, spans, grid: Grid):
+        k = len(culled)
+        offs = np.empty(grid.n_tiles + 1, np.int64)
+        n = _i64()
+        cul = np.ascontiguousarray(culled, np.int32)
+        dep = np.ascontiguousarray(depth, np.float64)
+        sp = np.ascontiguousarray(spans, np.int32)
+        _check(_lib.rxgs_bin_and_sort(self.h, k, cul.ctypes.data, dep.ctypes.data, sp.ctypes.data, C.byref(grid),
+                                      offs.ctypes.data, None, 0, C.byref(n)))
+        idx = np.empty(max(n.value, 1), np.int32)
+        _check(_lib.rxgs_bin_and_sort(self.h, k, cul.ctypes.data, dep.ctypes.data, sp.ctypes.data, C.byref(grid),
+                                      offs.ctypes.data, idx.ctypes.data, n.value, C.byref(n)))
+        return offs, idx[:n.value]
+
+    def aggregate(self, values, grid: Grid, modality):
+        values = np.ascontiguousarray(values, np.float64)
+        n_rx, ch = values.shape[0], values.shape[1]
+        m = MODALITY[modality]
+        shape = (n_rx,) if m == 0 else ((n_rx, ch, 2) if m == 1 else (n_rx, grid.n_theta, grid.n_phi))
+        out = _out(shape)
+        _check(_lib.rxgs_aggregate_modality(self.h, C.byref(grid), m, n_rx, ch, values.ctypes.data,
+                                            out.ctypes.data))
+        return out
+
+
+class Scene:
+    """GaussianScene upload (scene.hpp:19-48)."""
+
+    def __init__(self, ctx: Context, sc, modality="spectrum"):
+        self.ctx = ctx
+        self.data = sc
+        self.k = len(sc["tau_logits"])
+        self.l_max = sc["l_max"]
+        self.channels = sc["channels"]
+        self.L = (self.l_max + 1) ** 2
+        self.modality = modality
+        h = _vp()
+        _check(_lib.rxgs_scene_create(ctx.h, self.k, self.l_max, self.channels, MODALITY[modality],
+                                      ptr(sc["positions"], np.float64), ptr(sc["log_scales"], np.float64),
+                                      ptr(sc["quaternions"], np.float64), ptr(sc["tau_logits"], np.float64),
+                                      ptr(sc["fle_coeffs"], np.float64), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib.rxgs_scene_destroy(self.h)
+            self.h = None
+
+    def bounds(self, inflate=0.0):
+        lo, hi = _out(3), _out(3)
+        _check(_lib.rxgs_scene_bounds(self.h, inflate, lo.ctypes.data, hi.ctypes.data))
+        return lo, hi
+
+    def tx_state(self, tx, grid: Grid):
+        return TxState(self, tx, grid)
+
+    def render_field(self, st, coeffs, n_rx, values=None, transmittance=None):
+        own = values is None
+        if own:
+            values = _out((n_rx, self.channels, 2, st.grid.n_theta, st.grid.n_phi))
+            transmittance = _out((n_rx, st.grid.n_theta, st.grid.n_phi))
+        _check(_lib.rxgs_render_field(self.ctx.h, st.h, self.h, ptr(coeffs, np.float64), n_rx, ptr(values),
+                                      ptr(transmittance)))
+        return values, transmittance
+
+    def render_queries(self, cond, st, rx, spectrum=None, rssi=None, want=("spectrum", "rssi")):
+        """Fused batched query path; numpy in -> numpy out unless torch tensors are passed."""
+        n = int(rx.shape[0])
+        if spectrum is None and "spectrum" in want:
+            spectrum = np.empty((n, st.grid.n_theta, st.grid.n_phi), np.float32)
+        if rssi is None and "rssi" in want:
+            rssi = np.empty(n, np.float32)
+        _check(_lib.rxgs_render_queries(self.ctx.h, self.h, None if cond is None else cond.h, st.h,
+                                        ptr(rx, np.float64), n, ptr(spectrum), ptr(rssi)))
+        return spectrum, rssi
+
+    def predict(self, cond, grid: Grid, tx, rx):
+        m = MODALITY[self.modality]
+        out = _out(grid.cells if m == 2 else (1 if m == 0 else 2 * self.channels))
+        _check(_lib.rxgs_predict(self.ctx.h, self.h, None if cond is None else cond.h, C.byref(grid),
+                                 ptr(tx, np.float64), ptr(rx, np.float64), out.ctypes.data))
+        return out
+
+
+class TxState:
+    """raster::TxState (sphraster.hpp:52-61), device resident."""
+
+    def __init__(self, scene: Scene, tx, grid: Grid):
+        self.scene = scene
+        self.grid = grid
+        h = _vp()
+        _check(_lib.rxgs_tx_state_build(scene.ctx.h, scene.h, ptr(tx, np.float64), C.byref(grid), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib.rxgs_tx_state_destroy(self.h)
+            self.h = None
+
+    @property
+    def entries(self):
+        return int(_lib.rxgs_tx_state_entries(self.h))
+
+    def get(self):
+        k, L = self.scene.k, self.scene.L
+        n = self.entries
+        culled = np.empty(k, np.int32)
+        geom = _out((k, 12))
+        spans = np.empty((k, 4), np.int32)
+        basis = _out((k, L, 2))
+        offs = np.empty(self.grid.n_tiles + 1, np.int64)
+        idx = np.empty(max(n, 1), np.int32)
+        _check(_lib.rxgs_tx_state_get(self.h, culled.ctypes.data, geom.ctypes.data, spans.ctypes.data,
+                                      basis.ctypes.data, offs.ctypes.data, idx.ctypes.data))
+        return dict(culled=culled, geom=geom, spans=spans, basis=basis, offsets=offs, indices=idx[:n])
+
+    def keys(self):
+        out = np.empty(max(self.entries, 1), np.uint64)
+        _check(_lib.rxgs_tx_state_keys(self.h, out.ctypes.data))
+        return out[:self.entries]
+
+    def stats(self):
+        v, e, w, tw = _i64(), _i64(), C.c_double(), C.c_double()
+        _check(_lib.rxgs_tx_state_stats(self.h, C.byref(v), C.byref(e), C.byref(w), C.byref(tw)))
+        return dict(visible=v.value, entries=e.value, walk_per_cell=w.value, tile_walk_per_cell=tw.value)
+
+    def transmittance(self):
+        out = _out((self.grid.n_theta, self.grid.n_phi))
+        _check(_lib.rxgs_tx_state_transmittance(self.h, out.ctypes.data))
+        return out
+
+
+class Cond:
+    """cond::ConditioningState (conditioning.hpp:72-92), device resident."""
+
+    def __init__(self, ctx: Context, cfg, params, occ=None, lo=None, hi=None):
+        self.ctx = ctx
+        self.cfg = np.asarray(cfg, np.int32)
+        h = _vp()
+        _check(_lib.rxgs_cond_create(ctx.h, ptr(self.cfg, np.int32), ptr(params, np.float64),
+                                     ptr(occ, np.float64) if occ is not None else None,
+                                     ptr(lo, np.float64) if lo is not None else None,
+                                     ptr(hi, np.float64) if hi is not None else None, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib.rxgs_cond_destroy(self.h)
+            self.h = None
+
+    @property
+    def param_count(self):
+        return int(_lib.rxgs_cond_param_count(self.h))
+
+    def calls(self):
+        g, l_ = _i64(), _i64()
+        _check(_lib.rxgs_cond_calls(self.h, C.byref(g), C.byref(l_)))
+        return g.value, l_.value
+
+    def build_occupancy(self, scene: Scene, R, lo, hi, attach=True):
+        out = _out((R, R, R))
+        _check(_lib.rxgs_build_occupancy(self.ctx.h, scene.h, R, ptr(lo, np.float64), ptr(hi, np.float64),
+                                         out.ctypes.data, self.h if attach else None))
+        return out
+
+    def probe(self, frm, to):
+        frm = np.ascontiguousarray(frm, np.float64).reshape(-1, 3)
+        to = np.ascontiguousarray(to, np.float64).reshape(-1, 3)
+        out = _out((frm.shape[0], 2))
+        _check(_lib.rxgs_probe_segments(self.ctx.h, self.h, frm.shape[0], frm.ctypes.data, to.ctypes.data,
+                                        out.ctypes.data))
+        return out
+
+    def forward(self, scene: Scene, rx, workspace=False):
+        out = _out((scene.k, scene.L, scene.channels, 2))
+        lin = _out((scene.k, 6)) if workspace else None
+        _check(_lib.rxgs_condition_forward(self.ctx.h, self.h, scene.h, ptr(rx, np.float64), out.ctypes.data,
+                                           None if lin is None else lin.ctypes.data))
+        return (out, lin) if workspace else out
+
+    def batch(self, scene: Scene, rx):
+        rx = np.ascontiguousarray(rx, np.float64).reshape(-1, 3)
+        out = _out((rx.shape[0], scene.k, scene.L, scene.channels, 2))
+        _check(_lib.rxgs_condition_batch(self.ctx.h, self.h, scene.h, rx.ctypes.data, rx.shape[0], out.ctypes.data))
+        return out
+
+
+def build_occupancy(ctx: Context, scene: Scene, R, lo, hi):
+    out = _out((R, R, R))
+    _check(_lib.rxgs_build_occupancy(ctx.h, scene.h, R, ptr(lo, np.float64), ptr(hi, np.float64), out.ctypes.data,
+                                     None))
+    return out

@@ -1,0 +1,977 @@
+// C-ABI layer: handles, validation with the reference's error text, host /
+// device pointer handling, stream-ordered orchestration of the kernels.
+// See include/rxgs_b200.h for the contract and DESIGN.md for the data flow.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "rxgs_internal.cuh"
+
+using namespace rxgs_b200;
+
+namespace rxgs_b200 {
+
+namespace {
+thread_local std::string g_err;
+}
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    g_err = std::string("CUDA error: ") + cudaGetErrorString(e) + " (" + what + ")";
+    return RXGS_ERR_CUDA;
+}
+
+void timing_begin(rxgs_ctx ctx, const char* name, cudaEvent_t* a) {
+    (void)name;
+    *a = nullptr;
+    if (!ctx->profile) return;
+    if (ctx->event_pool.empty()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        ctx->event_pool.push_back(e);
+    }
+    *a = ctx->event_pool.back();
+    ctx->event_pool.pop_back();
+    cudaEventRecord(*a, ctx->stream);
+}
+
+void timing_end(rxgs_ctx ctx, const char* name, cudaEvent_t a, double work) {
+    if (!ctx->profile || !a) return;
+    cudaEvent_t b;
+    if (ctx->event_pool.empty()) {
+        cudaEventCreate(&b);
+    } else {
+        b = ctx->event_pool.back();
+        ctx->event_pool.pop_back();
+    }
+    cudaEventRecord(b, ctx->stream);
+    ctx->pending.push_back({name, a, b, work});
+}
+
+}  // namespace rxgs_b200
+
+namespace {
+
+void resolve_timings(rxgs_ctx ctx) {
+    if (ctx->pending.empty()) return;
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& p : ctx->pending) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, p.a, p.b);
+        auto& st = ctx->stats[p.name];
+        st.ms += ms;
+        st.launches += 1;
+        st.work += p.work;
+        ctx->event_pool.push_back(p.a);
+        ctx->event_pool.push_back(p.b);
+    }
+    ctx->pending.clear();
+}
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Device view of a caller array: the pointer itself if it is device memory,
+// otherwise a stream-ordered copy into `tmp`.
+template <typename T>
+int dev_in(rxgs_ctx ctx, const T* p, size_t n, DevBuf& tmp, const T** out) {
+    if (!p || n == 0) {
+        *out = p;
+        return RXGS_OK;
+    }
+    if (is_device_ptr(p)) {
+        *out = p;
+        return RXGS_OK;
+    }
+    RXGS_CUDA(tmp.ensure(n * sizeof(T)));
+    RXGS_CUDA(cudaMemcpyAsync(tmp.p, p, n * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+    *out = tmp.as<T>();
+    return RXGS_OK;
+}
+
+template <typename T>
+int dev_out(T* p, size_t n, DevBuf& tmp, T** out) {
+    if (!p) {
+        *out = nullptr;
+        return RXGS_OK;
+    }
+    if (is_device_ptr(p)) {
+        *out = p;
+        return RXGS_OK;
+    }
+    RXGS_CUDA(tmp.ensure(std::max<size_t>(n, 1) * sizeof(T)));
+    *out = tmp.as<T>();
+    return RXGS_OK;
+}
+
+template <typename T>
+int finish_out(rxgs_ctx ctx, T* user, const T* dev, size_t n) {
+    if (!user || user == dev || n == 0) return RXGS_OK;
+    RXGS_CUDA(cudaMemcpyAsync(user, dev, n * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+    return RXGS_OK;
+}
+
+template <typename T>
+std::vector<T> to_host(const T* p, size_t n) {
+    std::vector<T> v(n);
+    if (n == 0 || !p) return v;
+    if (is_device_ptr(p))
+        cudaMemcpy(v.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost);
+    else
+        std::memcpy(v.data(), p, n * sizeof(T));
+    return v;
+}
+
+int set_device(rxgs_ctx ctx) {
+    RXGS_CUDA(cudaSetDevice(ctx->device));
+    return RXGS_OK;
+}
+
+int validate_grid(const rxgs_grid* g) {  // SphericalGrid::validate, sphraster.cpp:14-20
+    if (!g) return fail(RXGS_ERR_INVALID, "grid: null");
+    if (g->n_theta < 1 || g->n_phi < 1) return fail(RXGS_ERR_INVALID, "grid: n_theta * n_phi must be >= 1");
+    if (g->tile_size < 1) return fail(RXGS_ERR_INVALID, "grid: tile_size must be >= 1");
+    if (!(g->radius > 0.0)) return fail(RXGS_ERR_INVALID, "grid: radius must be > 0");
+    if (!(g->theta_min >= 0.0 && g->theta_max <= kPi && g->theta_min < g->theta_max))
+        return fail(RXGS_ERR_INVALID, "grid: elevation span must satisfy 0 <= min < max <= pi");
+    return RXGS_OK;
+}
+
+DevGrid make_grid(const rxgs_grid* g) {
+    DevGrid d{};
+    d.nt = g->n_theta;
+    d.np = g->n_phi;
+    d.ts = g->tile_size;
+    d.tiles_t = (d.nt + d.ts - 1) / d.ts;
+    d.tiles_p = (d.np + d.ts - 1) / d.ts;
+    d.n_tiles = d.tiles_t * d.tiles_p;
+    d.cpt = d.ts * d.ts;
+    d.cell_blocks = (d.cpt + kMaxCellsPerBlock - 1) / kMaxCellsPerBlock;
+    d.radius = g->radius;
+    d.tmin = g->theta_min;
+    d.tmax = g->theta_max;
+    d.dth = (g->theta_max - g->theta_min) / g->n_theta;
+    d.dph = kTwoPi / g->n_phi;
+    return d;
+}
+
+int check_err_flag(rxgs_ctx ctx, int* d_err, int* host_val) {
+    RXGS_CUDA(cudaMemcpyAsync(host_val, d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RXGS_OK;
+}
+
+int reset_err_flag(rxgs_ctx ctx) {
+    RXGS_CUDA(ctx->err_flag.ensure(sizeof(int) * 4));
+    const int v = INT_MAX;
+    RXGS_CUDA(cudaMemcpyAsync(ctx->err_flag.p, &v, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    return RXGS_OK;
+}
+
+#define RX_TRY(expr)                 \
+    do {                             \
+        const int rc__ = (expr);     \
+        if (rc__ != RXGS_OK) return rc__; \
+    } while (0)
+
+#define API_BEGIN try {
+#define API_END                                                         \
+    }                                                                   \
+    catch (const std::bad_alloc&) {                                     \
+        return fail(RXGS_ERR_RUNTIME, "host allocation failed");        \
+    }                                                                   \
+    catch (const std::exception& e) {                                   \
+        return fail(RXGS_ERR_RUNTIME, e.what());                        \
+    }
+
+// Layout offsets of the packed conditioning parameters.
+void layout_cond(rxgs_cond_s& c) {
+    c.L = (c.l_max + 1) * (c.l_max + 1);
+    c.gin = 6 * c.F + 2 + c.dc;
+    size_t o = 0;
+    const size_t d = c.hidden;
+    c.o_freq = o; o += static_cast<size_t>(c.F) * 3;
+    c.o_gw1 = o; o += d * c.gin;
+    c.o_gb1 = o; o += d;
+    c.o_gw2 = o; o += d * d;
+    c.o_gb2 = o; o += d;
+    c.o_gw3 = o; o += 4 * c.C * d;
+    c.o_gb3 = o; o += 4 * c.C;
+    c.o_emb = o; o += static_cast<size_t>(c.L) * c.dc;
+    c.o_lw1 = o; o += d * 6;
+    c.o_lb1 = o; o += d;
+    c.o_lw2 = o; o += d * d;
+    c.o_lb2 = o; o += d;
+    c.o_lw3 = o; o += 4 * c.C * d;
+    c.o_lb3 = o; o += 4 * c.C;
+    c.n_params = static_cast<int64_t>(o);
+}
+
+// Signals for a receiver chunk: fused conditioning (or the bare base
+// coefficients when cond == nullptr).
+int compute_signals(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, rxgs_txstate st, const double* d_rx,
+                    int n_rx, float2* d_sig) {
+    cudaStream_t s = ctx->stream;
+    const size_t ag_n = static_cast<size_t>(n_rx) * sc->L * 4 * sc->channels;
+    RXGS_CUDA(ctx->ag.ensure(std::max<size_t>(ag_n, 1) * sizeof(float)));
+    cudaEvent_t ev;
+    if (c && c->use_global()) {
+        timing_begin(ctx, "cond_global", &ev);
+        RXGS_CUDA(launch_cond_global(*c, d_rx, n_rx, ctx->ag.as<float>(), s));
+        timing_end(ctx, "cond_global", ev, static_cast<double>(n_rx) * sc->L);
+    } else {
+        RXGS_CUDA(cudaMemsetAsync(ctx->ag.p, 0, ag_n * sizeof(float), s));
+    }
+    ctx->launches += 1;
+    timing_begin(ctx, "cond_signal", &ev);
+    RXGS_CUDA(launch_cond_signal(c, *sc, *st, d_rx, n_rx, ctx->ag.as<float>(), d_sig, nullptr, s));
+    timing_end(ctx, "cond_signal", ev, static_cast<double>(st->visible) * n_rx);
+    ctx->launches += 1;
+    return RXGS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rxgs_last_error(void) { return g_err.c_str(); }
+int rxgs_version(void) { return 1; }
+
+// ------------------------------------------------------------------ context
+int rxgs_ctx_create(int device, rxgs_ctx* out) {
+    API_BEGIN
+    if (!out) return fail(RXGS_ERR_INVALID, "rxgs_ctx_create: null out");
+    int n = 0;
+    RXGS_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) return fail(RXGS_ERR_INVALID, "rxgs_ctx_create: bad device ordinal");
+    RXGS_CUDA(cudaSetDevice(device));
+    auto* ctx = new rxgs_ctx_s;
+    ctx->device = device;
+    RXGS_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+    ctx->stream = ctx->own_stream;
+    cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+    *out = ctx;
+    return RXGS_OK;
+    API_END
+}
+
+int rxgs_ctx_destroy(rxgs_ctx ctx) {
+    if (!ctx) return RXGS_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& p : ctx->pending) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    for (auto e : ctx->event_pool) cudaEventDestroy(e);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+    return RXGS_OK;
+}
+
+int rxgs_ctx_set_stream(rxgs_ctx ctx, void* stream) {
+    if (!ctx) return fail(RXGS_ERR_INVALID, "null context");
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    return RXGS_OK;
+}
+
+int rxgs_ctx_synchronize(rxgs_ctx ctx) {
+    if (!ctx) return fail(RXGS_ERR_INVALID, "null context");
+    RX_TRY(set_device(ctx));
+    RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RXGS_OK;
+}
+
+int rxgs_ctx_profile(rxgs_ctx ctx, int enable) {
+    if (!ctx) return fail(RXGS_ERR_INVALID, "null context");
+    ctx->profile = enable != 0;
+    return RXGS_OK;
+}
+
+int rxgs_ctx_kernel_stats(rxgs_ctx ctx, const char* name, double* total_ms, int64_t* launches,
+                          double* work) {
+    if (!ctx || !name) return fail(RXGS_ERR_INVALID, "null argument");
+    resolve_timings(ctx);
+    const auto it = ctx->stats.find(name);
+    const KStat st = it == ctx->stats.end() ? KStat{} : it->second;
+    if (total_ms) *total_ms = st.ms;
+    if (launches) *launches = st.launches;
+    if (work) *work = st.work;
+    return RXGS_OK;
+}
+
+int rxgs_ctx_reset_stats(rxgs_ctx ctx) {
+    if (!ctx) return fail(RXGS_ERR_INVALID, "null context");
+    resolve_timings(ctx);
+    ctx->stats.clear();
+    ctx->launches = 0;
+    return RXGS_OK;
+}
+
+int64_t rxgs_ctx_launch_count(rxgs_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+// ------------------------------------------------------------------ scene
+int rxgs_scene_create(rxgs_ctx ctx, int k, int l_max, int channels, int modality, const double* pos,
+                      const double* ls, const double* q, const double* tau, const double* coeffs,
+                      rxgs_scene* out) {
+    API_BEGIN
+    if (!ctx || !out) return fail(RXGS_ERR_INVALID, "rxgs_scene_create: null argument");
+    if (k < 0 || l_max < 0 || channels < 1 || modality < 0 || modality > 2)
+        return fail(RXGS_ERR_INVALID, "scene: per-Gaussian arrays out of alignment");
+    if (l_max > kMaxLmax) return fail(RXGS_ERR_INVALID, "scene: l_max > 15 is not supported by the B200 path");
+    RX_TRY(set_device(ctx));
+    auto* sc = new rxgs_scene_s;
+    sc->ctx = ctx;
+    sc->k = k;
+    sc->l_max = l_max;
+    sc->channels = channels;
+    sc->L = (l_max + 1) * (l_max + 1);
+    sc->modality = modality;
+    const size_t nc = static_cast<size_t>(k) * sc->L * channels * 2;
+    sc->h_pos = to_host(pos, 3 * static_cast<size_t>(k));
+    sc->h_ls = to_host(ls, 3 * static_cast<size_t>(k));
+    sc->h_q = to_host(q, 4 * static_cast<size_t>(k));
+    sc->h_tau = to_host(tau, static_cast<size_t>(k));
+    sc->h_coeffs = to_host(coeffs, nc);
+    auto up = [&](DevBuf& b, const std::vector<double>& h) -> int {
+        RXGS_CUDA(b.ensure(std::max<size_t>(h.size(), 1) * sizeof(double)));
+        if (!h.empty()) RXGS_CUDA(cudaMemcpy(b.p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+        return RXGS_OK;
+    };
+    int rc = up(sc->d_pos, sc->h_pos);
+    if (!rc) rc = up(sc->d_ls, sc->h_ls);
+    if (!rc) rc = up(sc->d_q, sc->h_q);
+    if (!rc) rc = up(sc->d_tau, sc->h_tau);
+    if (!rc) rc = up(sc->d_coeffs64, sc->h_coeffs);
+    if (!rc) {
+        std::vector<float> p4(4 * static_cast<size_t>(std::max(k, 1)), 0.f);
+        for (int i = 0; i < k; ++i)
+            for (int a = 0; a < 3; ++a) p4[4 * i + a] = static_cast<float>(sc->h_pos[3 * i + a]);
+        const cudaError_t e1 = sc->d_pos32.ensure(p4.size() * sizeof(float));
+        if (e1 != cudaSuccess) rc = cuda_fail(e1, "scene pos32");
+        else {
+            const cudaError_t e2 = cudaMemcpy(sc->d_pos32.p, p4.data(), p4.size() * sizeof(float), cudaMemcpyHostToDevice);
+            if (e2 != cudaSuccess) rc = cuda_fail(e2, "scene pos32 copy");
+        }
+    }
+    if (rc) {
+        delete sc;
+        return rc;
+    }
+    *out = sc;
+    return RXGS_OK;
+    API_END
+}
+
+int rxgs_scene_destroy(rxgs_scene sc) {
+    if (!sc) return RXGS_OK;
+    cudaSetDevice(sc->ctx->device);
+    cudaStreamSynchronize(sc->ctx->stream);
+    delete sc;
+    return RXGS_OK;
+}
+
+int rxgs_scene_bounds(rxgs_scene sc, double inflate, double lo[3], double hi[3]) {
+    if (!sc) return fail(RXGS_ERR_INVALID, "null scene");
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = 1.7976931348623157e308;
+        hi[a] = -1.7976931348623157e308;
+    }
+    for (int k = 0; k < sc->k; ++k)
+        for (int a = 0; a < 3; ++a) {
+            const double v = sc->h_pos[3 * k + a];
+            lo[a] = std::min(lo[a], v);
+            hi[a] = std::max(hi[a], v);
+        }
+    for (int a = 0; a < 3; ++a) {  // Aabb::inflated, linalg.hpp:143-147
+        const double pad = (hi[a] - lo[a]) * (0.5 * inflate);
+        lo[a] = lo[a] - pad;
+        hi[a] = hi[a] + pad;
+    }
+    return RXGS_OK;
+}
+
+// ------------------------------------------------------------------ tx state
+int rxgs_tx_state_build(rxgs_ctx ctx, rxgs_scene sc, const double tx[3], const rxgs_grid* grid,
+                        rxgs_txstate* out) {
+    API_BEGIN
+    if (!ctx || !sc || !tx || !out) return fail(RXGS_ERR_INVALID, "rxgs_tx_state_build: null argument");
+    RX_TRY(validate_grid(grid));
+    RX_TRY(set_device(ctx));
+    cudaStream_t s = ctx->stream;
+    auto* st = new rxgs_txstate_s;
+    st->ctx = ctx;
+    st->k = sc->k;
+    st->l_max = sc->l_max;
+    st->L = sc->L;
+    st->channels = sc->channels;
+    st->grid = make_grid(grid);
+    const double txh[3] = {tx[0], tx[1], tx[2]};
+    std::vector<double> txv = to_host(tx, 3);
+    for (int a = 0; a < 3; ++a) st->tx[a] = txv[a];
+    (void)txh;
+    const size_t K = std::max(sc->k, 1);
+    auto fail_st = [&](int rc) {
+        delete st;
+        return rc;
+    };
+    int rc = RXGS_OK;
+#define ENS(buf, bytes)                                              \
+    do {                                                             \
+        const cudaError_t e__ = st->buf.ensure(bytes);               \
+        if (e__ != cudaSuccess) return fail_st(cuda_fail(e__, #buf)); \
+    } while (0)
+    ENS(rec, K * sizeof(GaussRec));
+    ENS(culled, K * sizeof(int));
+    ENS(geom, K * 12 * sizeof(double));
+    ENS(spans, K * sizeof(int4));
+    ENS(basis64, K * sc->L * 2 * sizeof(double));
+    ENS(basis32, K * sc->L * sizeof(float2));
+    ENS(gb32, K * sc->L * sc->channels * sizeof(float2));
+    ENS(depth_key, K * sizeof(uint64_t));
+    ENS(tile_count, K * sizeof(int));
+    cudaEvent_t ev;
+    timing_begin(ctx, "tx_prep", &ev);
+    {
+        const cudaError_t e = launch_tx_prep(*sc, *st, s);
+        if (e != cudaSuccess) return fail_st(cuda_fail(e, "tx_prep"));
+    }
+    timing_end(ctx, "tx_prep", ev, sc->k);
+    ctx->launches += 1;
+    rc = bin_tiles(ctx, *st, s);
+    if (rc) return fail_st(rc);
+    // visible = Gaussians with a finite depth key (culled sort last)
+    {
+        std::vector<int> cul = std::vector<int>(static_cast<size_t>(sc->k));
+        if (sc->k) {
+            const cudaError_t e = cudaMemcpyAsync(cul.data(), st->culled.p, sc->k * sizeof(int),
+                                                  cudaMemcpyDeviceToHost, s);
+            if (e != cudaSuccess) return fail_st(cuda_fail(e, "culled"));
+            cudaStreamSynchronize(s);
+        }
+        int64_t v = 0;
+        for (int x : cul) v += x ? 0 : 1;
+        st->visible = v;
+    }
+    const DevGrid& g = st->grid;
+    const size_t cells = static_cast<size_t>(g.nt) * g.np;
+    ENS(tw, std::max<size_t>(st->entries, 1) * g.cell_blocks * kMaxCellsPerBlock * sizeof(float));
+    ENS(walk_len, static_cast<size_t>(g.n_tiles) * g.cell_blocks * sizeof(int));
+    ENS(cell_T, cells * sizeof(double));
+    ENS(cell_len, cells * sizeof(int));
+#undef ENS
+    timing_begin(ctx, "walk", &ev);
+    {
+        const cudaError_t e = launch_walk(*st, s);
+        if (e != cudaSuccess) return fail_st(cuda_fail(e, "walk"));
+    }
+    timing_end(ctx, "walk", ev, static_cast<double>(cells));
+    ctx->launches += 1;
+    *out = st;
+    return RXGS_OK;
+    API_END
+}
+
+int rxgs_tx_state_destroy(rxgs_txstate st) {
+    if (!st) return RXGS_OK;
+    cudaSetDevice(st->ctx->device);
+    cudaStreamSynchronize(st->ctx->stream);
+    delete st;
+    return RXGS_OK;
+}
+
+int64_t rxgs_tx_state_entries(rxgs_txstate st) { return st ? st->entries : -1; }
+
+int rxgs_tx_state_get(rxgs_txstate st, int32_t* culled, double* geom, int32_t* spans, double* basis,
+                      int64_t* offsets, int32_t* indices) {
+    API_BEGIN
+    if (!st) return fail(RXGS_ERR_INVALID, "null tx state");
+    rxgs_ctx ctx = st->ctx;
+    RX_TRY(set_device(ctx));
+    RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    const size_t K = st->k;
+    if (culled && K) RXGS_CUDA(cudaMemcpy(culled, st->culled.p, K * sizeof(int), cudaMemcpyDefault));
+    if (geom && K) RXGS_CUDA(cudaMemcpy(geom, st->geom.p, K * 12 * sizeof(double), cudaMemcpyDefault));
+    if (spans && K) RXGS_CUDA(cudaMemcpy(spans, st->spans.p, K * 4 * sizeof(int), cudaMemcpyDefault));
+    if (basis && K)
+        RXGS_CUDA(cudaMemcpy(basis, st->basis64.p, K * st->L * 2 * sizeof(double), cudaMemcpyDefault));
+    if (offsets)
+        RXGS_CUDA(cudaMemcpy(offsets, st->tile_offsets.p, (st->grid.n_tiles + 1) * sizeof(int64_t),
+                             cudaMemcpyDefault));
+    if (indices && st->entries)
+        RXGS_CUDA(cudaMemcpy(indices, st->list.p, st->entries * sizeof(int), cudaMemcpyDefault));
+    return RXGS_OK;
+    API_END
+}
+
+int rxgs_tx_state_keys(rxgs_txstate st, uint64_t* keys) {
+    if (!st || !keys) return fail(RXGS_ERR_INVALID, "null argument");
+    RX_TRY(set_device(st->ctx));
+    RXGS_CUDA(cudaStreamSynchronize(st->ctx->stream));
+    if (st->entries)
+        RXGS_CUDA(cudaMemcpy(keys, st->keys.p, st->entries * sizeof(uint64_t), cudaMemcpyDefault));
+    return RXGS_OK;
+}
+
+int rxgs_tx_state_stats(rxgs_txstate st, int64_t* visible, int64_t* entries, double* walk_per_cell,
+                        double* tile_walk_per_cell) {
+    API_BEGIN
+    if (!st) return fail(RXGS_ERR_INVALID, "null tx state");
+    RX_TRY(set_device(st->ctx));
+    RXGS_CUDA(cudaStreamSynchronize(st->ctx->stream));
+    const DevGrid& g = st->grid;
+    const size_t cells = static_cast<size_t>(g.nt) * g.np;
+    std::vector<int> len(cells), wl(static_cast<size_t>(g.n_tiles) * g.cell_blocks);
+    RXGS_CUDA(cudaMemcpy(len.data(), st->cell_len.p, cells * sizeof(int), cudaMemcpyDeviceToHost));
+    RXGS_CUDA(cudaMemcpy(wl.data(), st->walk_len.p, wl.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    double s = 0.0, ts = 0.0;
+    for (int x : len) s += x;
+    for (int t = 0; t < g.n_tiles; ++t) {
+        const int tt = t / g.tiles_p, tp = t % g.tiles_p;
+        const int rows = std::min(g.ts, g.nt - tt * g.ts), cols = std::min(g.ts, g.np - tp * g.ts);
+        int mx = 0;
+        for (int b = 0; b < g.cell_blocks; ++b) mx = std::max(mx, wl[static_cast<size_t>(t) * g.cell_blocks + b]);
+        ts += static_cast<double>(mx) * rows * cols;
+    }
+    if (visible) *visible = st->visible;
+    if (entries) *entries = st->entries;
+    if (walk_per_cell) *walk_per_cell = cells ? s / cells : 0.0;
+    if (tile_walk_per_cell) *tile_walk_per_cell = cells ? ts / cells : 0.0;
+    return RXGS_OK;
+    API_END
+}
+
+int rxgs_tx_state_transmittance(rxgs_txstate st, double* out) {
+    if (!st || !out) return fail(RXGS_ERR_INVALID, "null argument");
+    RX_TRY(set_device(st->ctx));
+    RXGS_CUDA(cudaStreamSynchronize(st->ctx->stream));
+    const size_t cells = static_cast<size_t>(st->grid.nt) * st->grid.np;
+    RXGS_CUDA(cudaMemcpy(out, st->cell_T.p, cells * sizeof(double), cudaMemcpyDefault));
+    return RXGS_OK;
+}
+
+int rxgs_bin_and_sort(rxgs_ctx ctx, int k, const int32_t* culled, const double* depth,
+                      const int32_t* spans, const rxgs_grid* grid, int64_t* offsets, int32_t* indices,
+                      int64_t cap, int64_t* entries) {
+    API_BEGIN
+    if (!ctx || k < 0) return fail(RXGS_ERR_INVALID, "rxgs_bin_and_sort: bad argument");
+    if (!grid || grid->tile_size < 1 || grid->n_theta < 1 || grid->n_phi < 1)
+        return fail(RXGS_ERR_INVALID, "grid: n_theta * n_phi must be >= 1");
+    RX_TRY(set_device(ctx));
+    rxgs_txstate_s st;
+    st.ctx = ctx;
+    st.k = k;
+    st.grid = make_grid(grid);
+    const size_t K = std::max(k, 1);
+    std::vector<int> cul = to_host(culled, static_cast<size_t>(k));
+    std::vector<double> dep = to_host(depth, static_cast<size_t>(k));
+    std::vector<int> sp = to_host(spans, 4 * static_cast<size_t>(k));
+    std::vector<uint64_t> dkey(K, ~0ull);
+    std::vector<int> cnt(K, 0);
+    for (int i = 0; i < k; ++i) {
+        if (cul[i]) continue;
+        uint64_t b;
+        std::memcpy(&b, &dep[i], 8);
+        dkey[i] = b;
+        cnt[i] = (sp[4 * i + 1] - sp[4 * i] + 1) * (sp[4 * i + 3] - sp[4 * i + 2] + 1);
+    }
+    RXGS_CUDA(st.depth_key.ensure(K * 8));
+    RXGS_CUDA(st.tile_count.ensure(K * 4));
+    RXGS_CUDA(st.spans.ensure(K * 16));
+    RXGS_CUDA(cudaMemcpy(st.depth_key.p, dkey.data(), K * 8, cudaMemcpyHostToDevice));
+    RXGS_CUDA(cudaMemcpy(st.tile_count.p, cnt.data(), K * 4, cudaMemcpyHostToDevice));
+    if (k) RXGS_CUDA(cudaMemcpy(st.spans.p, sp.data(), static_cast<size_t>(k) * 16, cudaMemcpyHostToDevice));
+    RX_TRY(bin_tiles(ctx, st, ctx->stream));
+    RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (entries) *entries = st.entries;
+    if (offsets)
+        RXGS_CUDA(cudaMemcpy(offsets, st.tile_offsets.p, (st.grid.n_tiles + 1) * sizeof(int64_t),
+                             cudaMemcpyDefault));
+    if (indices && cap >= st.entries && st.entries)
+        RXGS_CUDA(cudaMemcpy(indices, st.list.p, st.entries * sizeof(int), cudaMemcpyDefault));
+    return RXGS_OK;
+    API_END
+}
+
+// ------------------------------------------------------------------ render
+int rxgs_render_field(rxgs_ctx ctx, rxgs_txstate st, rxgs_scene sc, const double* coeffs, int n_rx,
+                      double* values, double* transmittance) {
+    API_BEGIN
+    if (!ctx || !st || !sc) return fail(RXGS_ERR_INVALID, "render_field: null argument");
+    if (n_rx < 1) return fail(RXGS_ERR_INVALID, "render_field: n_rx must be >= 1");
+    if (sc->k != st->k || sc->channels != st->channels || sc->L != st->L)
+        return fail(RXGS_ERR_INVALID, "render_field: coefficient tensor has wrong size");
+    RX_TRY(set_device(ctx));
+    cudaStream_t s = ctx->stream;
+    const size_t stride = static_cast<size_t>(sc->L) * sc->channels * 2;
+    const size_t nco = static_cast<size_t>(n_rx) * sc->k * stride;
+    const double* d_co = nullptr;
+    RX_TRY(dev_in(ctx, coeffs, nco, ctx->host_in, &d_co));
+    RXGS_CUDA(ctx->signals.ensure(std::max<size_t>(static_cast<size_t>(sc->k) * n_rx * sc->channels, 1) * sizeof(float2)));
+    RX_TRY(reset_err_flag(ctx));
+    if (nco) {
+        RXGS_CUDA(launch_reduce_signals(*st, d_co, n_rx, ctx->signals.as<float2>(), ctx->err_flag.as<int>(), s));
+        ctx->launches += 2;
+    }
+    int err = INT_MAX;
+    RX_TRY(check_err_flag(ctx, ctx->err_flag.as<int>(), &err));
+    if (err != INT_MAX) {
+        const int j = err / std::max(sc->k, 1), k = err % std::max(sc->k, 1);
+        return fail(RXGS_ERR_INVALID, "render_field: non-finite coefficient at rx " + std::to_string(j) +
+                                          ", gaussian " + std::to_string(k));
+    }
+    const size_t plane = static_cast<size_t>(st->grid.nt) * st->grid.np;
+    const size_t nv = static_cast<size_t>(n_rx) * sc->channels * 2 * plane;
+    double* d_vals = nullptr;
+    double* d_T = nullptr;
+    RX_TRY(dev_out(values, nv, ctx->host_out, &d_vals));
+    RX_TRY(dev_out(transmittance, static_cast<size_t>(n_rx) * plane, ctx->scratch_c, &d_T));
+    CompositeOut co;
+    co.values = d_vals;
+    cudaEvent_t ev;
+    timing_begin(ctx, "composite", &ev);
+    RXGS_CUDA(launch_composite(*st, ctx->signals.as<float2>(), n_rx, co, s));
+    timing_end(ctx, "composite", ev, static_cast<double>(n_rx) * sc->channels);
+    ctx->launches += 1;
+    if (d_T) {
+        RXGS_CUDA(launch_fill_transmittance(*st, n_rx, d_T, s));
+        ctx->launches += 1;
+    }
+    RX_TRY(finish_out(ctx, values, d_vals, nv));
+    RX_TRY(finish_out(ctx, transmittance, d_T, static_cast<size_t>(n_rx) * plane));
+    RXGS_CUDA(cudaStreamSynchronize(s));
+    return RXGS_OK;
+    API_END
+}
+
+int rxgs_aggregate_modality(rxgs_ctx ctx, const rxgs_grid* grid, int modality, int n_rx, int channels,
+                            const double* values, double* out) {
+    API_BEGIN
+    if (!ctx || !grid) return fail(RXGS_ERR_INVALID, "aggregate_modality: null argument");
+    RX_TRY(set_device(ctx));
+    const DevGrid g = make_grid(grid);
+    const size_t plane = static_cast<size_t>(g.nt) * g.np;
+    const size_t nv = static_cast<size_t>(n_rx) * channels * 2 * plane;
+    const double* d_v = nullptr;
+    RX_TRY(dev_in(ctx, values, nv, ctx->host_in, &d_v));
+    RX_TRY(reset_err_flag(ctx));
+    const size_t no = modality == 0 ? n_rx : (modality == 1 ? static_cast<size_t>(n_rx) * channels * 2 : n_rx * plane);
+    // finiteness first (sphraster.cpp:325-326), then the channel check (:327-328)
+    RXGS_CUDA(ctx->scratch_d.ensure(std::max<size_t>(no, 1) * sizeof(double)));
+    double* d_out = nullptr;
+    RX_TRY(dev_out(out, no, ctx->host_out, &d_out));
+    if (!d_out) d_out = ctx->scratch_d.as<double>();
+    const bool ch_ok = modality == 1 || channels == 1;
+    RXGS_CUDA(launch_aggregate(g, modality, n_rx, channels, d_v, d_out, ctx->err_flag.as<int>(), ch_ok,
+                               ctx->stream));
+    ctx->launches += 2;
+    int err = INT_MAX;
+    RX_TRY(check_err_flag(ctx, ctx->err_flag.as<int>(), &err));
+    if (err != INT_MAX) return fail(RXGS_ERR_INVALID, "aggregate_modality: non-finite field");
+    if (!ch_ok) return fail(RXGS_ERR_INVALID, "aggregate_modality: scalar modalities need channels == 1");
+    RX_TRY(finish_out(ctx, out, d_out, no));
+    RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RXGS_OK;
+    API_END
+}
+
+// ------------------------------------------------------------------ conditioning
+int rxgs_cond_create(rxgs_ctx ctx, const int32_t cfg[9], const double* params, const double* occ,
+                     const double occ_lo[3], const double occ_hi[3], rxgs_cond* out) {
+    API_BEGIN
+    if (!ctx || !cfg || !params || !out) return fail(RXGS_ERR_INVALID, "rxgs_cond_create: null argument");
+    if (cfg[0] < 1 || cfg[1] < 1 || cfg[2] < 1)
+        return fail(RXGS_ERR_INVALID, "init_conditioning: bad dimensions");
+    if (cfg[1] > 64) return fail(RXGS_ERR_INVALID, "conditioning: hidden > 64 is not supported by the B200 path");
+    if (cfg[8] < 1 || cfg[8] > 8) return fail(RXGS_ERR_INVALID, "conditioning: channels must be in [1, 8]");
+    if (cfg[6] < 0 || cfg[6] > 4) return fail(RXGS_ERR_INVALID, "unknown conditioning mode");
+    if (cfg[3] < 1) return fail(RXGS_ERR_INVALID, "probe_segment: samples must be >= 1");
+    RX_TRY(set_device(ctx));
+    auto* c = new rxgs_cond_s;
+    c->ctx = ctx;
+    c->F = cfg[0]; c->hidden = cfg[1]; c->dc = cfg[2]; c->S = cfg[3]; c->R = cfg[4];
+    c->nearest = cfg[5]; c->mode = cfg[6]; c->l_max = cfg[7]; c->C = cfg[8];
+    layout_cond(*c);
+    c->h_params = to_host(params, static_cast<size_t>(c->n_params));
+    std::vector<float> p32(c->h_params.begin(), c->h_params.end());
+    auto bad = [&](cudaError_t e, const char* w) {
+        delete c;
+        return cuda_fail(e, w);
+    };
+    cudaError_t e = c->d_params64.ensure(c->h_params.size() * sizeof(double));
+    if (e != cudaSuccess) return bad(e, "params64");
+    e = cudaMemcpy(c->d_params64.p, c->h_params.data(), c->h_params.size() * sizeof(double), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return bad(e, "params64 copy");
+    e = c->d_params32.ensure(p32.size() * sizeof(float));
+    if (e != cudaSuccess) return bad(e, "params32");
+    e = cudaMemcpy(c->d_params32.p, p32.data(), p32.size() * sizeof(float), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return bad(e, "params32 copy");
+    if (occ) {
+        const size_t n = static_cast<size_t>(c->R) * c->R * c->R;
+        std::vector<double> h = to_host(occ, n);
+        std::vector<float> f(h.begin(), h.end());
+        e = c->d_occ32.ensure(n * sizeof(float));
+        if (e != cudaSuccess) return bad(e, "occ");
+        e = cudaMemcpy(c->d_occ32.p, f.data(), n * sizeof(float), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return bad(e, "occ copy");
+        std::vector<double> lo = to_host(occ_lo, 3), hi = to_host(occ_hi, 3);
+        for (int a = 0; a < 3; ++a) {
+            c->lo[a] = lo[a];
+            c->hi[a] = hi[a];
+        }
+        c->has_occ = true;
+    }
+    *out = c;
+    return RXGS_OK;
+    API_END
+}
+
+int rxgs_cond_destroy(rxgs_cond c) {
+    if (!c) return RXGS_OK;
+    cudaSetDevice(c->ctx->device);
+    cudaStreamSynchronize(c->ctx->stream);
+    delete c;
+    return RXGS_OK;
+}
+
+int64_t rxgs_cond_param_count(rxgs_cond c) { return c ? c->n_params : -1; }
+
+int rxgs_cond_calls(rxgs_cond c, int64_t* g, int64_t* l) {
+    if (!c) return fail(RXGS_ERR_INVALID, "null conditioning");
+    if (g) *g = c->global_calls;
+    if (l) *l = c->local_calls;
+    return RXGS_OK;
+}
+
+int rxgs_build_occupancy(rxgs_ctx ctx, rxgs_scene sc, int R, const double lo_[3], const double hi_[3],
+                         double* out, rxgs_cond attach) {
+    API_BEGIN
+    if (!ctx || !sc || !lo_ || !hi_) return fail(RXGS_ERR_INVALID, "build_occupancy: null argument");
+    if (R < 1) return fail(RXGS_ERR_INVALID, "build_occupancy: resolution must be >= 1");
+    std::vector<double> lo = to_host(lo_, 3), hi = to_host(hi_, 3);
+    if (!(hi[0] - lo[0] > 0 && hi[1] - lo[1] > 0 && hi[2] - lo[2] > 0))
+        return fail(RXGS_ERR_INVALID, "build_occupancy: degenerate bounds");
+    RX_TRY(set_device(ctx));
+    const size_t n = static_cast<size_t>(R) * R * R;
+    double* d64 = nullptr;
+    RX_TRY(dev_out(out, n, ctx->host_out, &d64));
+    float* d32 = nullptr;
+    if (attach) {
+        RXGS_CUDA(attach->d_occ32.ensure(n * sizeof(float)));
+        d32 = attach->d_occ32.as<float>();
+    }
+    cudaEvent_t ev;
+    timing_begin(ctx, "occupancy", &ev);
+    RXGS_CUDA(launch_occupancy(*sc, R, lo.data(), hi.data(), d64, d32, ctx->stream));
+    timing_end(ctx, "occupancy", ev, sc->k);
+    ctx->launches += 2;
+    if (attach) {
+        attach->R = R;
+        for (int a = 0; a < 3; ++a) {
+            attach->lo[a] = lo[a];
+            attach->hi[a] = hi[a];
+        }
+        attach->has_occ = true;
+    }
+    RX_TRY(finish_out(ctx, out, d64, n));
+    RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RXGS_OK;
+    API_END
+}
+
+int rxgs_probe_segments(rxgs_ctx ctx, rxgs_cond c, int n, const double* from, const double* to,
+                        double* out) {
+    API_BEGIN
+    if (!ctx || !c) return fail(RXGS_ERR_INVALID, "probe_segment: null argument");
+    if (c->S < 1) return fail(RXGS_ERR_INVALID, "probe_segment: samples must be >= 1");
+    RX_TRY(set_device(ctx));
+    const double *d_from = nullptr, *d_to = nullptr;
+    RX_TRY(dev_in(ctx, from, 3 * static_cast<size_t>(n), ctx->scratch_c, &d_from));
+    RX_TRY(dev_in(ctx, to, 3 * static_cast<size_t>(n), ctx->scratch_d, &d_to));
+    double* d_out = nullptr;
+    RX_TRY(dev_out(out, 2 * static_cast<size_t>(n), ctx->host_out, &d_out));
+    RXGS_CUDA(launch_probe(*c, n, d_from, d_to, d_out, ctx->stream));
+    ctx->launches += 1;
+    RX_TRY(finish_out(ctx, out, d_out, 2 * static_cast<size_t>(n)));
+    RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RXGS_OK;
+    API_END
+}
+
+int rxgs_condition_batch(rxgs_ctx ctx, rxgs_cond c, rxgs_scene sc, const double* rx, int n_rx,
+                         double* out) {
+    API_BEGIN
+    if (!ctx || !c || !sc || !rx) return fail(RXGS_ERR_INVALID, "condition_forward: null argument");
+    if (sc->l_max != c->l_max || sc->channels != c->C)
+        return fail(RXGS_ERR_INVALID, "condition_forward: scene/state shape mismatch");
+    RX_TRY(set_device(ctx));
+    cudaStream_t s = ctx->stream;
+    const double* d_rx = nullptr;
+    RX_TRY(dev_in(ctx, rx, 3 * static_cast<size_t>(n_rx), ctx->scratch_c, &d_rx));
+    if (c->use_local()) {
+        RX_TRY(reset_err_flag(ctx));
+        RXGS_CUDA(launch_check_coincide(*sc, d_rx, n_rx, ctx->err_flag.as<int>(), s));
+        ctx->launches += 1;
+        int err = INT_MAX;
+        RX_TRY(check_err_flag(ctx, ctx->err_flag.as<int>(), &err));
+        if (err != INT_MAX)
+            return fail(RXGS_ERR_INVALID, "condition_forward: receiver coincides with gaussian " +
+                                              std::to_string(err % std::max(sc->k, 1)));
+    }
+    const size_t stride = static_cast<size_t>(sc->L) * sc->channels * 2;
+    const size_t no = static_cast<size_t>(n_rx) * sc->k * stride;
+    const size_t ag_n = static_cast<size_t>(n_rx) * sc->L * 4 * sc->channels;
+    RXGS_CUDA(ctx->ag.ensure(std::max<size_t>(ag_n, 1) * sizeof(float)));
+    RXGS_CUDA(launch_cond_global(*c, d_rx, n_rx, ctx->ag.as<float>(), s));
+    double* d_out = nullptr;
+    RX_TRY(dev_out(out, no, ctx->host_out, &d_out));
+    RXGS_CUDA(launch_cond_materialize(*c, *sc, d_rx, n_rx, ctx->ag.as<float>(), d_out, nullptr, nullptr, s));
+    ctx->launches += 2;
+    if (c->use_global()) c->global_calls += static_cast<int64_t>(n_rx) * sc->L;
+    if (c->use_local()) c->local_calls += static_cast<int64_t>(n_rx) * sc->k;
+    RX_TRY(finish_out(ctx, out, d_out, no));
+    RXGS_CUDA(cudaStreamSynchronize(s));
+    return RXGS_OK;
+    API_END
+}
+
+int rxgs_condition_forward(rxgs_ctx ctx, rxgs_cond c, rxgs_scene sc, const double rx[3], double* out,
+                           double* local_in) {
+    API_BEGIN
+    if (!local_in) return rxgs_condition_batch(ctx, c, sc, rx, 1, out);
+    if (!ctx || !c || !sc || !rx) return fail(RXGS_ERR_INVALID, "condition_forward: null argument");
+    if (sc->l_max != c->l_max || sc->channels != c->C)
+        return fail(RXGS_ERR_INVALID, "condition_forward: scene/state shape mismatch");
+    // Workspace variant: same pipeline, plus the local features.
+    RX_TRY(rxgs_condition_batch(ctx, c, sc, rx, 1, out));
+    c->global_calls -= c->use_global() ? sc->L : 0;  // counted once below
+    c->local_calls -= c->use_local() ? sc->k : 0;
+    cudaStream_t s = ctx->stream;
+    const double* d_rx = nullptr;
+    RX_TRY(dev_in(ctx, rx, 3, ctx->scratch_c, &d_rx));
+    const size_t stride = static_cast<size_t>(sc->L) * sc->channels * 2;
+    RXGS_CUDA(ctx->scratch_d.ensure(std::max<size_t>(static_cast<size_t>(sc->k) * stride, 1) * sizeof(double)));
+    double* d_li = nullptr;
+    RX_TRY(dev_out(local_in, static_cast<size_t>(sc->k) * 6, ctx->host_out, &d_li));
+    RXGS_CUDA(launch_cond_global(*c, d_rx, 1, ctx->ag.as<float>(), s));
+    RXGS_CUDA(launch_cond_materialize(*c, *sc, d_rx, 1, ctx->ag.as<float>(), ctx->scratch_d.as<double>(), d_li,
+                                      nullptr, s));
+    ctx->launches += 2;
+    if (c->use_global()) c->global_calls += sc->L;
+    if (c->use_local()) c->local_calls += sc->k;
+    RX_TRY(finish_out(ctx, local_in, d_li, static_cast<size_t>(sc->k) * 6));
+    RXGS_CUDA(cudaStreamSynchronize(s));
+    return RXGS_OK;
+    API_END
+}
+
+// ------------------------------------------------------------------ queries
+int rxgs_render_queries(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, rxgs_txstate st, const double* rx,
+                        int n_rx, float* out_spectrum, float* out_rssi) {
+    API_BEGIN
+    if (!ctx || !sc || !st) return fail(RXGS_ERR_INVALID, "render_queries: null argument");
+    if (n_rx < 0) return fail(RXGS_ERR_INVALID, "render_field: n_rx must be >= 1");
+    if (n_rx == 0) return RXGS_OK;
+    if (!rx) return fail(RXGS_ERR_INVALID, "render_queries: null receivers");
+    if (sc->k != st->k || sc->L != st->L || sc->channels != st->channels)
+        return fail(RXGS_ERR_INVALID, "render_queries: scene / tx-state mismatch");
+    if (c && (sc->l_max != c->l_max || sc->channels != c->C))
+        return fail(RXGS_ERR_INVALID, "condition_forward: scene/state shape mismatch");
+    if (sc->channels != 1)
+        return fail(RXGS_ERR_INVALID, "aggregate_modality: scalar modalities need channels == 1");
+    RX_TRY(set_device(ctx));
+    cudaStream_t s = ctx->stream;
+    const double* d_rx = nullptr;
+    RX_TRY(dev_in(ctx, rx, 3 * static_cast<size_t>(n_rx), ctx->scratch_c, &d_rx));
+    if (c && c->use_local()) {
+        RX_TRY(reset_err_flag(ctx));
+        RXGS_CUDA(launch_check_coincide(*sc, d_rx, n_rx, ctx->err_flag.as<int>(), s));
+        ctx->launches += 1;
+        int err = INT_MAX;
+        RX_TRY(check_err_flag(ctx, ctx->err_flag.as<int>(), &err));
+        if (err != INT_MAX)
+            return fail(RXGS_ERR_INVALID, "condition_forward: receiver coincides with gaussian " +
+                                              std::to_string(err % std::max(sc->k, 1)));
+    }
+    const DevGrid& g = st->grid;
+    const size_t plane = static_cast<size_t>(g.nt) * g.np;
+    const int n_tb = g.n_tiles * g.cell_blocks;
+    float* d_spec = nullptr;
+    float* d_rssi = nullptr;
+    RX_TRY(dev_out(out_spectrum, static_cast<size_t>(n_rx) * plane, ctx->host_out, &d_spec));
+    RX_TRY(dev_out(out_rssi, static_cast<size_t>(n_rx), ctx->scratch_d, &d_rssi));
+    // receiver chunks bound the signal buffer (K x chunk complex f32) to ~4 GB
+    const size_t per_rx = std::max<size_t>(static_cast<size_t>(sc->k), 1) * sizeof(float2);
+    int chunk = static_cast<int>(std::min<size_t>(static_cast<size_t>(n_rx), (size_t{4} << 30) / per_rx));
+    chunk = std::max(chunk, 1);
+    RXGS_CUDA(ctx->signals.ensure(per_rx * chunk));
+    RXGS_CUDA(ctx->partial.ensure(std::max<size_t>(static_cast<size_t>(n_tb) * chunk, 1) * sizeof(float)));
+    for (int j0 = 0; j0 < n_rx; j0 += chunk) {
+        const int nj = std::min(chunk, n_rx - j0);
+        RX_TRY(compute_signals(ctx, sc, c, st, d_rx + 3 * static_cast<size_t>(j0), nj, ctx->signals.as<float2>()));
+        CompositeOut co;
+        co.spectrum = d_spec ? d_spec + static_cast<size_t>(j0) * plane : nullptr;
+        co.rssi_partial = d_rssi ? ctx->partial.as<float>() : nullptr;
+        cudaEvent_t ev;
+        timing_begin(ctx, "composite", &ev);
+        RXGS_CUDA(launch_composite(*st, ctx->signals.as<float2>(), nj, co, s));
+        timing_end(ctx, "composite", ev, nj);
+        ctx->launches += 1;
+        if (d_rssi) {
+            RXGS_CUDA(launch_rssi_finalize(ctx->partial.as<float>(), n_tb, nj, d_rssi + j0, nullptr, s));
+            ctx->launches += 1;
+        }
+    }
+    if (c) {
+        if (c->use_global()) c->global_calls += static_cast<int64_t>(n_rx) * sc->L;
+        if (c->use_local()) c->local_calls += static_cast<int64_t>(n_rx) * sc->k;
+    }
+    const bool host_out = (out_spectrum && d_spec != out_spectrum) || (out_rssi && d_rssi != out_rssi);
+    RX_TRY(finish_out(ctx, out_spectrum, d_spec, static_cast<size_t>(n_rx) * plane));
+    RX_TRY(finish_out(ctx, out_rssi, d_rssi, static_cast<size_t>(n_rx)));
+    if (host_out || !is_device_ptr(rx)) RXGS_CUDA(cudaStreamSynchronize(s));
+    return RXGS_OK;
+    API_END
+}
+
+int rxgs_predict(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const rxgs_grid* grid, const double tx[3],
+                 const double rx[3], double* out) {
+    API_BEGIN
+    if (!ctx || !sc || !grid || !tx || !rx || !out) return fail(RXGS_ERR_INVALID, "predict: null argument");
+    const size_t stride = static_cast<size_t>(sc->L) * sc->channels * 2;
+    std::vector<double> coeffs(static_cast<size_t>(sc->k) * stride);
+    if (c) {
+        RX_TRY(rxgs_condition_forward(ctx, c, sc, rx, coeffs.data(), nullptr));
+    } else {
+        coeffs = sc->h_coeffs;
+    }
+    rxgs_txstate st = nullptr;
+    RX_TRY(rxgs_tx_state_build(ctx, sc, tx, grid, &st));
+    const size_t plane = static_cast<size_t>(grid->n_theta) * grid->n_phi;
+    std::vector<double> vals(static_cast<size_t>(sc->channels) * 2 * plane);
+    int rc = rxgs_render_field(ctx, st, sc, coeffs.data(), 1, vals.data(), nullptr);
+    rxgs_tx_state_destroy(st);
+    if (rc) return rc;
+    return rxgs_aggregate_modality(ctx, grid, sc->modality, 1, sc->channels, vals.data(), out);
+    API_END
+}
+
+}  // extern "C"

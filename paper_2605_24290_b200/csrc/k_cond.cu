@@ -1,0 +1,545 @@
+// Receiver conditioning on sm_100a (conditioning.cpp:284-423).
+//
+//   k_cond_global      global branch: fourier_encode (:255-265) + the per-
+//                      component MLP (:317-361) for every (receiver, l);
+//                      tiny (N*L rows), run in FP64.
+//   k_cond_signal      THE hot kernel of the query path: per (Gaussian,
+//                      receiver) the local features (:376-396, probe_segment
+//                      :163-178 over an occupancy grid held in shared memory),
+//                      the local MLP 6->H->H->4C (:397), both complex affines
+//                      (:271-275) and the FLE reduction of reduce_signals
+//                      (sphraster.cpp:190-226), fused so the N*K*L*C*2
+//                      coefficient tensor is never materialised:
+//                        s = (1+aL) * sum_l[(1+aG_l) (B_l base_l) + bG_l B_l]
+//                            + bL * sum_l B_l
+//                      FP32 SIMT, persistent CTAs, one warp = 32 receivers of
+//                      one Gaussian (Gaussian data broadcast, receiver data
+//                      per lane).
+//   k_cond_materialize condition_forward's materialised output (FP64 affine
+//                      on the FP64 base, so zero branches are bitwise identity
+//                      exactly as in the reference).
+#include "rxgs_internal.cuh"
+
+namespace rxgs_b200 {
+namespace {
+
+constexpr int kHMax = 64;
+constexpr int kCMax = 8;
+
+struct CondDev {
+    const float* p32;
+    const double* p64;
+    const float* occ;
+    int F, H, dc, S, R, nearest, mode, L, C, gin;
+    int o_freq, o_gw1, o_gb1, o_gw2, o_gb2, o_gw3, o_gb3, o_emb, o_lw1, o_lb1, o_lw2, o_lb2, o_lw3, o_lb3;
+    int probe;  // 1 = sample the occupancy grid, 0 = T=1, rho=0
+    int use_global, use_local, additive;
+    float lo[3], cell[3];
+};
+
+CondDev make_dev(const rxgs_cond_s& c) {
+    CondDev d{};
+    d.p32 = c.d_params32.as<float>();
+    d.p64 = c.d_params64.as<double>();
+    d.occ = c.d_occ32.as<float>();
+    d.F = c.F; d.H = c.hidden; d.dc = c.dc; d.S = c.S; d.R = c.R; d.nearest = c.nearest;
+    d.mode = c.mode; d.L = c.L; d.C = c.C; d.gin = c.gin;
+    d.o_freq = static_cast<int>(c.o_freq); d.o_gw1 = static_cast<int>(c.o_gw1);
+    d.o_gb1 = static_cast<int>(c.o_gb1); d.o_gw2 = static_cast<int>(c.o_gw2);
+    d.o_gb2 = static_cast<int>(c.o_gb2); d.o_gw3 = static_cast<int>(c.o_gw3);
+    d.o_gb3 = static_cast<int>(c.o_gb3); d.o_emb = static_cast<int>(c.o_emb);
+    d.o_lw1 = static_cast<int>(c.o_lw1); d.o_lb1 = static_cast<int>(c.o_lb1);
+    d.o_lw2 = static_cast<int>(c.o_lw2); d.o_lb2 = static_cast<int>(c.o_lb2);
+    d.o_lw3 = static_cast<int>(c.o_lw3); d.o_lb3 = static_cast<int>(c.o_lb3);
+    d.probe = c.no_occ() ? 0 : 1;
+    d.use_global = c.use_global();
+    d.use_local = c.use_local();
+    d.additive = c.additive();
+    for (int a = 0; a < 3; ++a) {
+        d.lo[a] = static_cast<float>(c.lo[a]);
+        d.cell[a] = static_cast<float>((c.hi[a] - c.lo[a]) / c.R);
+    }
+    return d;
+}
+
+// ------------------------------------------------------------------ global branch (FP64)
+__global__ void k_cond_global(CondDev c, const double* __restrict__ rx, int n_rx,
+                              float* __restrict__ ag) {
+    extern __shared__ double sm[];
+    double* in = sm;
+    double* h1 = in + c.gin;
+    double* h2 = h1 + c.H;
+    const int row = blockIdx.x;
+    const int j = row / c.L, comp = row % c.L;
+    const double* p = c.p64;
+    int l = 0;
+    while ((l + 1) * (l + 1) <= comp) ++l;
+    const int m = comp - l * l - l;
+    int l_max = 0;
+    while ((l_max + 1) * (l_max + 1) < c.L) ++l_max;
+    const double den = l_max > 0 ? static_cast<double>(l_max) : 1.0;  // conditioning.cpp:328
+    for (int i = threadIdx.x; i < c.gin; i += blockDim.x) {
+        double v;
+        if (i < 6 * c.F) {
+            const int a = i / (2 * c.F), band = (i % (2 * c.F)) / 2;
+            const double arg = p[c.o_freq + band * 3 + a] * rx[3 * j + a];
+            v = (i % 2) ? cos(arg) : sin(arg);
+        } else if (i == 6 * c.F) {
+            v = l / den;
+        } else if (i == 6 * c.F + 1) {
+            v = m / den;
+        } else {
+            v = p[c.o_emb + comp * c.dc + (i - 6 * c.F - 2)];
+        }
+        in[i] = v;
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < c.H; o += blockDim.x) {
+        double acc = p[c.o_gb1 + o];
+        const double* w = p + c.o_gw1 + static_cast<size_t>(o) * c.gin;
+        for (int i = 0; i < c.gin; ++i) acc += w[i] * in[i];
+        h1[o] = acc > 0.0 ? acc : 0.0;
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < c.H; o += blockDim.x) {
+        double acc = p[c.o_gb2 + o];
+        const double* w = p + c.o_gw2 + static_cast<size_t>(o) * c.H;
+        for (int i = 0; i < c.H; ++i) acc += w[i] * h1[i];
+        h2[o] = acc > 0.0 ? acc : 0.0;
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < 4 * c.C; o += blockDim.x) {
+        double acc = p[c.o_gb3 + o];
+        const double* w = p + c.o_gw3 + static_cast<size_t>(o) * c.H;
+        for (int i = 0; i < c.H; ++i) acc += w[i] * h2[i];
+        if (c.additive && (o % 4) < 2) acc = 0.0;
+        ag[(static_cast<size_t>(j) * c.L + comp) * 4 * c.C + o] = static_cast<float>(acc);
+    }
+}
+
+// ------------------------------------------------------------------ local branch helpers
+struct LocalSmem {
+    const float* occ;
+    const float* w1;
+    const float* b1;
+    const float* w2;
+    const float* b2;
+    const float* w3;
+    const float* b3;
+};
+
+__device__ __forceinline__ float sample_tri(const CondDev& c, const float* occ, float qx, float qy,
+                                            float qz) {
+    const int R = c.R;
+    const float u0 = (qx - c.lo[0]) / c.cell[0] - 0.5f;
+    const float u1 = (qy - c.lo[1]) / c.cell[1] - 0.5f;
+    const float u2 = (qz - c.lo[2]) / c.cell[2] - 0.5f;
+    const float f0 = floorf(u0), f1 = floorf(u1), f2 = floorf(u2);
+    const int i0 = static_cast<int>(f0), i1 = static_cast<int>(f1), i2 = static_cast<int>(f2);
+    const float a0 = u0 - f0, a1 = u1 - f1, a2 = u2 - f2;
+    float acc = 0.f;
+#pragma unroll
+    for (int dx = 0; dx < 2; ++dx)
+#pragma unroll
+        for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+            for (int dz = 0; dz < 2; ++dz) {
+                const int ix = i0 + dx, iy = i1 + dy, iz = i2 + dz;
+                if (ix < 0 || iy < 0 || iz < 0 || ix >= R || iy >= R || iz >= R) continue;
+                const float w = (dx ? a0 : 1.f - a0) * (dy ? a1 : 1.f - a1) * (dz ? a2 : 1.f - a2);
+                acc += w * occ[(ix * R + iy) * R + iz];
+            }
+    return acc;
+}
+
+__device__ __forceinline__ float sample_near(const CondDev& c, const float* occ, float qx, float qy,
+                                             float qz) {
+    const int R = c.R;
+    const int ix = static_cast<int>(floorf((qx - c.lo[0]) / c.cell[0]));
+    const int iy = static_cast<int>(floorf((qy - c.lo[1]) / c.cell[1]));
+    const int iz = static_cast<int>(floorf((qz - c.lo[2]) / c.cell[2]));
+    if (ix < 0 || iy < 0 || iz < 0 || ix >= R || iy >= R || iz >= R) return 0.f;
+    return occ[(ix * R + iy) * R + iz];
+}
+
+// Local features [v_hat, d, T, rho] (conditioning.cpp:377-396).
+__device__ __forceinline__ void local_features(const CondDev& c, const float* occ, float px,
+                                               float py, float pz, float rx, float ry, float rz,
+                                               float* in) {
+    const float dx = rx - px, dy = ry - py, dz = rz - pz;
+    const float d = sqrtf(dx * dx + dy * dy + dz * dz);
+    in[0] = dx / d;
+    in[1] = dy / d;
+    in[2] = dz / d;
+    in[3] = d;
+    float T = 1.f, rho = 0.f;
+    if (c.probe) {
+        float sum = 0.f;
+        for (int s = 0; s < c.S; ++s) {
+            const float t = c.S == 1 ? 0.5f : 0.05f + 0.9f * static_cast<float>(s) / (c.S - 1);
+            const float qx = px + dx * t, qy = py + dy * t, qz = pz + dz * t;
+            const float v = c.nearest ? sample_near(c, occ, qx, qy, qz) : sample_tri(c, occ, qx, qy, qz);
+            T *= 1.f - v;
+            sum += v;
+        }
+        rho = sum / c.S;
+    }
+    in[4] = T;
+    in[5] = rho;
+}
+
+// Local MLP 6 -> H -> H -> 4C (mlp_forward :23-29) in FP32; y has 4C outputs.
+template <int HT, int CT>
+__device__ __forceinline__ void local_mlp(const CondDev& c, const LocalSmem& w, const float* in,
+                                          float* y) {
+    constexpr int HM = HT > 0 ? HT : kHMax;
+    constexpr int YM = CT > 0 ? 4 * CT : 4 * kCMax;
+    const int H = HT > 0 ? HT : c.H;
+    const int NY = CT > 0 ? 4 * CT : 4 * c.C;
+    float h1[HM];
+#pragma unroll
+    for (int o = 0; o < HM; ++o) {
+        if (HT == 0 && o >= H) break;
+        float acc = w.b1[o];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) acc = fmaf(w.w1[o * 6 + i], in[i], acc);
+        h1[o] = fmaxf(acc, 0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < YM; ++q)
+        if (q < NY) y[q] = w.b3[q];
+#pragma unroll 2
+    for (int o = 0; o < H; ++o) {
+        const float* row = w.w2 + o * H;
+        float acc = w.b2[o];
+        if (HT > 0) {
+#pragma unroll
+            for (int i = 0; i < HM; i += 4) {
+                const float4 wv = *reinterpret_cast<const float4*>(row + i);
+                acc = fmaf(wv.x, h1[i], acc);
+                acc = fmaf(wv.y, h1[i + 1], acc);
+                acc = fmaf(wv.z, h1[i + 2], acc);
+                acc = fmaf(wv.w, h1[i + 3], acc);
+            }
+        } else {
+            for (int i = 0; i < H; ++i) acc = fmaf(row[i], h1[i], acc);
+        }
+        const float h2 = fmaxf(acc, 0.f);
+#pragma unroll
+        for (int q = 0; q < YM; ++q)
+            if (q < NY) y[q] = fmaf(w.w3[q * H + o], h2, y[q]);
+    }
+}
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// ------------------------------------------------------------------ fused hot kernel
+template <int HT, int CT>
+__global__ void __launch_bounds__(512, 1)
+    k_cond_signal(CondDev c, int n_vis, const int* __restrict__ vis, const float4* __restrict__ pos32,
+                  const double* __restrict__ rx, int n_rx, const float2* __restrict__ B,
+                  const float2* __restrict__ GB, const float* __restrict__ ag,
+                  float2* __restrict__ sig) {
+    extern __shared__ __align__(16) float smem[];
+    const int H = HT > 0 ? HT : c.H;
+    const int C = CT > 0 ? CT : c.C;
+    const int R3 = c.probe ? c.R * c.R * c.R : 0;
+    // layout: w2 (H*H) | w1 (H*6) | b1 (H) | b2 (H) | w3 (4C*H) | b3 (4C) | occ (R^3)
+    float* s_w2 = smem;
+    float* s_w1 = s_w2 + H * H;
+    float* s_b1 = s_w1 + H * 6;
+    float* s_b2 = s_b1 + H;
+    float* s_w3 = s_b2 + H;
+    float* s_b3 = s_w3 + 4 * C * H;
+    float* s_occ = s_b3 + ((4 * C + 3) & ~3);
+    const float* p = c.p32;
+    if (c.use_local) {
+        for (int i = threadIdx.x; i < H * H; i += blockDim.x) s_w2[i] = p[c.o_lw2 + i];
+        for (int i = threadIdx.x; i < H * 6; i += blockDim.x) s_w1[i] = p[c.o_lw1 + i];
+        for (int i = threadIdx.x; i < H; i += blockDim.x) {
+            s_b1[i] = p[c.o_lb1 + i];
+            s_b2[i] = p[c.o_lb2 + i];
+        }
+        for (int i = threadIdx.x; i < 4 * C * H; i += blockDim.x) s_w3[i] = p[c.o_lw3 + i];
+        for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) s_b3[i] = p[c.o_lb3 + i];
+        for (int i = threadIdx.x; i < R3; i += blockDim.x) s_occ[i] = c.occ[i];
+    }
+    __syncthreads();
+    const LocalSmem w{s_occ, s_w1, s_b1, s_w2, s_b2, s_w3, s_b3};
+
+    const int lane = threadIdx.x & 31;
+    const int warps_per_block = blockDim.x >> 5;
+    const int n_jc = (n_rx + 31) >> 5;
+    const long long items = static_cast<long long>(n_vis) * n_jc;
+    const long long stride = static_cast<long long>(gridDim.x) * warps_per_block;
+    const int L = c.L;
+    constexpr int YM = CT > 0 ? 4 * CT : 4 * kCMax;
+    for (long long it = static_cast<long long>(blockIdx.x) * warps_per_block + (threadIdx.x >> 5);
+         it < items; it += stride) {
+        const int vi = static_cast<int>(it / n_jc);
+        const int jc = static_cast<int>(it % n_jc);
+        const int j = jc * 32 + lane;
+        if (j >= n_rx) continue;
+        const int k = vis[vi];
+        const float4 pk = pos32[k];
+        const float rxx = static_cast<float>(rx[3 * j]);
+        const float rxy = static_cast<float>(rx[3 * j + 1]);
+        const float rxz = static_cast<float>(rx[3 * j + 2]);
+        float y[YM];
+        if (c.use_local) {
+            float in[6];
+            local_features(c, s_occ, pk.x, pk.y, pk.z, rxx, rxy, rxz, in);
+            local_mlp<HT, CT>(c, w, in, y);
+        } else {
+#pragma unroll
+            for (int q = 0; q < YM; ++q) y[q] = 0.f;
+        }
+        for (int ch = 0; ch < C; ++ch) {
+            float2 M = make_float2(0.f, 0.f), Bs = make_float2(0.f, 0.f);
+            const float4* a4 = reinterpret_cast<const float4*>(ag) + static_cast<size_t>(j) * L * C + ch;
+            for (int l = 0; l < L; ++l) {
+                const float2 b = B[static_cast<size_t>(k) * L + l];
+                const float2 gb = GB[(static_cast<size_t>(k) * L + l) * C + ch];
+                const float4 a = a4[static_cast<size_t>(l) * C];
+                const float2 one_a = make_float2(1.f + a.x, a.y);
+                const float2 t0 = cmul(one_a, gb), t1 = cmul(make_float2(a.z, a.w), b);
+                M.x += t0.x + t1.x;
+                M.y += t0.y + t1.y;
+                Bs.x += b.x;
+                Bs.y += b.y;
+            }
+            const float ar = c.additive ? 0.f : y[4 * ch], ai = c.additive ? 0.f : y[4 * ch + 1];
+            const float2 s0 = cmul(make_float2(1.f + ar, ai), M);
+            const float2 s1 = cmul(make_float2(y[4 * ch + 2], y[4 * ch + 3]), Bs);
+            sig[(static_cast<size_t>(k) * n_rx + j) * C + ch] = make_float2(s0.x + s1.x, s0.y + s1.y);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ materialised output
+__global__ void k_cond_materialize(CondDev c, int K, const float4* __restrict__ pos32,
+                                   const double* __restrict__ rx, int n_rx,
+                                   const double* __restrict__ base, const float* __restrict__ ag,
+                                   double* __restrict__ out, double* __restrict__ local_in) {
+    extern __shared__ __align__(16) float smem[];
+    const int H = c.H, C = c.C, L = c.L;
+    const int R3 = (c.probe && c.use_local) ? c.R * c.R * c.R : 0;
+    float* s_w2 = smem;
+    float* s_w1 = s_w2 + H * H;
+    float* s_b1 = s_w1 + H * 6;
+    float* s_b2 = s_b1 + H;
+    float* s_w3 = s_b2 + H;
+    float* s_b3 = s_w3 + 4 * C * H;
+    float* s_occ = s_b3 + ((4 * C + 3) & ~3);
+    const float* p = c.p32;
+    if (c.use_local) {
+        for (int i = threadIdx.x; i < H * H; i += blockDim.x) s_w2[i] = p[c.o_lw2 + i];
+        for (int i = threadIdx.x; i < H * 6; i += blockDim.x) s_w1[i] = p[c.o_lw1 + i];
+        for (int i = threadIdx.x; i < H; i += blockDim.x) {
+            s_b1[i] = p[c.o_lb1 + i];
+            s_b2[i] = p[c.o_lb2 + i];
+        }
+        for (int i = threadIdx.x; i < 4 * C * H; i += blockDim.x) s_w3[i] = p[c.o_lw3 + i];
+        for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) s_b3[i] = p[c.o_lb3 + i];
+        for (int i = threadIdx.x; i < R3; i += blockDim.x) s_occ[i] = c.occ[i];
+    }
+    __syncthreads();
+    const LocalSmem w{s_occ, s_w1, s_b1, s_w2, s_b2, s_w3, s_b3};
+    const long long row = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (row >= static_cast<long long>(K) * n_rx) return;
+    const int j = static_cast<int>(row / K), k = static_cast<int>(row % K);
+    float y[4 * kCMax];
+    for (int q = 0; q < 4 * C; ++q) y[q] = 0.f;
+    if (c.use_local) {
+        const float4 pk = pos32[k];
+        float in[6];
+        local_features(c, s_occ, pk.x, pk.y, pk.z, static_cast<float>(rx[3 * j]),
+                       static_cast<float>(rx[3 * j + 1]), static_cast<float>(rx[3 * j + 2]), in);
+        local_mlp<0, 0>(c, w, in, y);
+        if (local_in && j == 0)
+            for (int i = 0; i < 6; ++i) local_in[static_cast<size_t>(k) * 6 + i] = in[i];
+    }
+    const size_t stride = static_cast<size_t>(L) * C * 2;
+    for (int l = 0; l < L; ++l)
+        for (int ch = 0; ch < C; ++ch) {
+            const size_t idx = static_cast<size_t>(k) * stride + (static_cast<size_t>(l) * C + ch) * 2;
+            const double zr = base[idx], zi = base[idx + 1];
+            double mr = zr, mi = zi;
+            if (c.use_global) {
+                const float* a = ag + (static_cast<size_t>(j) * L + l) * 4 * C + 4 * ch;
+                const double ar = a[0], ai = a[1], br = a[2], bi = a[3];
+                mr = zr + (ar * zr - ai * zi + br);
+                mi = zi + (ai * zr + ar * zi + bi);
+            }
+            double orr = mr, oi = mi;
+            if (c.use_local) {
+                const double ar = c.additive ? 0.0 : y[4 * ch], ai = c.additive ? 0.0 : y[4 * ch + 1];
+                const double br = y[4 * ch + 2], bi = y[4 * ch + 3];
+                orr = mr + (ar * mr - ai * mi + br);
+                oi = mi + (ai * mr + ar * mi + bi);
+            }
+            const size_t o = static_cast<size_t>(j) * K * stride + idx;
+            out[o] = orr;
+            out[o + 1] = oi;
+        }
+}
+
+__global__ void k_probe(CondDev c, int n, const double* __restrict__ from,
+                        const double* __restrict__ to, double* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float px = static_cast<float>(from[3 * i]), py = static_cast<float>(from[3 * i + 1]),
+                pz = static_cast<float>(from[3 * i + 2]);
+    float in[6];
+    local_features(c, c.occ, px, py, pz, static_cast<float>(to[3 * i]),
+                   static_cast<float>(to[3 * i + 1]), static_cast<float>(to[3 * i + 2]), in);
+    out[2 * i] = in[4];
+    out[2 * i + 1] = in[5];
+}
+
+// reduce_signals (sphraster.cpp:190-226) from the materialised f64 tensor.
+__global__ void k_reduce_signals(int K, int L, int C, int n_rx, const int* __restrict__ culled,
+                                 const double* __restrict__ basis64, const double* __restrict__ co,
+                                 float2* __restrict__ sig) {
+    const long long row = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (row >= static_cast<long long>(K) * n_rx) return;
+    const int k = static_cast<int>(row / n_rx), j = static_cast<int>(row % n_rx);
+    const size_t stride = static_cast<size_t>(L) * C * 2;
+    const double* cb = co + (static_cast<size_t>(j) * K + k) * stride;
+    const double* b = basis64 + static_cast<size_t>(k) * L * 2;
+    for (int ch = 0; ch < C; ++ch) {
+        double sr = 0.0, si = 0.0;
+        if (!culled[k])
+            for (int l = 0; l < L; ++l) {
+                const double a = cb[(l * C + ch) * 2], bb = cb[(l * C + ch) * 2 + 1];
+                sr += a * b[2 * l] - bb * b[2 * l + 1];
+                si += a * b[2 * l + 1] + bb * b[2 * l];
+            }
+        sig[(static_cast<size_t>(k) * n_rx + j) * C + ch] =
+            make_float2(static_cast<float>(sr), static_cast<float>(si));
+    }
+}
+
+__global__ void k_check_finite(long long n, long long per_row, const double* __restrict__ co,
+                               int* __restrict__ err) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    if (!isfinite(co[i])) atomicMin(err, static_cast<int>(i / per_row));
+}
+
+__global__ void k_check_coincide(int K, const double* __restrict__ pos, const double* __restrict__ rx,
+                                 int n_rx, int* __restrict__ err) {
+    const long long row = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (row >= static_cast<long long>(K) * n_rx) return;
+    const int j = static_cast<int>(row / K), k = static_cast<int>(row % K);
+    const double dx = rx[3 * j] - pos[3 * k], dy = rx[3 * j + 1] - pos[3 * k + 1],
+                 dz = rx[3 * j + 2] - pos[3 * k + 2];
+    if (sqrt(dx * dx + dy * dy + dz * dz) == 0.0) atomicMin(err, static_cast<int>(row));
+}
+
+size_t local_smem_bytes(const CondDev& d, bool with_occ) {
+    const size_t f = static_cast<size_t>(d.H) * d.H + d.H * 6 + 2 * d.H + 4 * d.C * d.H +
+                     ((4 * d.C + 3) & ~3) + (with_occ ? static_cast<size_t>(d.R) * d.R * d.R : 0);
+    return f * sizeof(float);
+}
+
+}  // namespace
+
+cudaError_t launch_cond_global(const rxgs_cond_s& c, const double* d_rx, int n_rx, float* d_ag,
+                               cudaStream_t s) {
+    if (n_rx == 0) return cudaSuccess;
+    if (!c.use_global()) return cudaMemsetAsync(d_ag, 0, sizeof(float) * n_rx * c.L * 4 * c.C, s);
+    const CondDev d = make_dev(c);
+    const size_t smem = sizeof(double) * (c.gin + 2 * c.hidden);
+    k_cond_global<<<n_rx * c.L, 64, smem, s>>>(d, d_rx, n_rx, d_ag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cond_signal(const rxgs_cond_s* c, const rxgs_scene_s& sc,
+                               const rxgs_txstate_s& st, const double* d_rx, int n_rx,
+                               const float* d_ag, float2* d_sig, int* d_err, cudaStream_t s) {
+    (void)d_err;
+    if (st.visible == 0 || n_rx == 0) return cudaSuccess;
+    CondDev d{};
+    if (c) {
+        d = make_dev(*c);
+    } else {  // unconditioned model: identity branches
+        d.H = 1; d.C = sc.channels; d.L = sc.L; d.use_global = 0; d.use_local = 0; d.probe = 0;
+    }
+    const size_t smem = d.use_local ? local_smem_bytes(d, d.probe) : 16;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long items = static_cast<long long>(st.visible) * ((n_rx + 31) / 32);
+    const int threads = 512;
+    const long long want = (items + (threads / 32) - 1) / (threads / 32);
+    const int blocks = static_cast<int>(want < sms ? want : sms);
+    const bool fast = d.use_local && d.H == 64 && d.C == 1;
+    if (fast) {
+        cudaFuncSetAttribute(k_cond_signal<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        k_cond_signal<64, 1><<<blocks, threads, smem, s>>>(
+            d, static_cast<int>(st.visible), st.order.as<int>(), sc.d_pos32.as<float4>(), d_rx, n_rx,
+            st.basis32.as<float2>(), st.gb32.as<float2>(), d_ag, d_sig);
+    } else {
+        if (d.H > kHMax || d.C > kCMax) return cudaErrorInvalidValue;
+        cudaFuncSetAttribute(k_cond_signal<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        k_cond_signal<0, 0><<<blocks, threads, smem, s>>>(
+            d, static_cast<int>(st.visible), st.order.as<int>(), sc.d_pos32.as<float4>(), d_rx, n_rx,
+            st.basis32.as<float2>(), st.gb32.as<float2>(), d_ag, d_sig);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cond_materialize(const rxgs_cond_s& c, const rxgs_scene_s& sc,
+                                    const double* d_rx, int n_rx, const float* d_ag, double* d_out,
+                                    double* d_local_in, int* d_err, cudaStream_t s) {
+    (void)d_err;
+    if (sc.k == 0 || n_rx == 0) return cudaSuccess;
+    const CondDev d = make_dev(c);
+    if (d.H > kHMax || d.C > kCMax) return cudaErrorInvalidValue;
+    const size_t smem = local_smem_bytes(d, d.probe && d.use_local);
+    cudaFuncSetAttribute(k_cond_materialize, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    const long long rows = static_cast<long long>(sc.k) * n_rx;
+    k_cond_materialize<<<static_cast<unsigned>((rows + 255) / 256), 256, smem, s>>>(
+        d, sc.k, sc.d_pos32.as<float4>(), d_rx, n_rx, sc.d_coeffs64.as<double>(), d_ag, d_out,
+        d_local_in);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_probe(const rxgs_cond_s& c, int n, const double* d_from, const double* d_to,
+                         double* d_out, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    CondDev d = make_dev(c);
+    d.probe = c.has_occ ? 1 : 0;
+    k_probe<<<(n + 127) / 128, 128, 0, s>>>(d, n, d_from, d_to, d_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_signals(const rxgs_txstate_s& st, const double* d_coeffs, int n_rx,
+                                  float2* d_sig, int* d_err, cudaStream_t s) {
+    const long long n = static_cast<long long>(n_rx) * st.k * st.L * st.channels * 2;
+    if (n == 0) return cudaSuccess;
+    k_check_finite<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+        n, static_cast<long long>(st.L) * st.channels * 2, d_coeffs, d_err);
+    const long long rows = static_cast<long long>(st.k) * n_rx;
+    k_reduce_signals<<<static_cast<unsigned>((rows + 255) / 256), 256, 0, s>>>(
+        st.k, st.L, st.channels, n_rx, st.culled.as<int>(), st.basis64.as<double>(), d_coeffs, d_sig);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_coincide(const rxgs_scene_s& sc, const double* d_rx, int n_rx, int* d_err,
+                                  cudaStream_t s) {
+    const long long rows = static_cast<long long>(sc.k) * n_rx;
+    if (rows == 0) return cudaSuccess;
+    k_check_coincide<<<static_cast<unsigned>((rows + 255) / 256), 256, 0, s>>>(
+        sc.k, sc.d_pos.as<double>(), d_rx, n_rx, d_err);
+    return cudaGetLastError();
+}
+
+}  // namespace rxgs_b200

@@ -1,0 +1,286 @@
+// Transmitter-side geometry in FP64 on sm_100a.
+//
+// Compiled with -fmad=false: the reference is built without FMA contraction
+// (x86-64 baseline), and the per-tile lists must match
+// it bit for bit, so every FP64 expression here keeps the reference's
+// operation order and rounding steps.
+//
+//   k_tx_prep   = covariance_from (scene.cpp:42-51) + project_gaussian
+//                 (sphraster.cpp:22-83) + eval_basis (radiance.cpp:79-92),
+//                 one thread per Gaussian.
+//   k_occupancy = build_occupancy (conditioning.cpp:114-161): scatter-max of
+//                 tau*exp(-m2/2) with atomicMax on the IEEE bits of the
+//                 non-negative doubles (order independent, hence exact).
+#include "rxgs_internal.cuh"
+
+namespace rxgs_b200 {
+namespace {
+
+__device__ __forceinline__ double wrap_two_pi(double a) {  // linalg.hpp:160-164
+    a = fmod(a, kTwoPi);
+    if (a < 0.0) a += kTwoPi;
+    return a;
+}
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+__device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }
+
+// quat_to_rotation (linalg.hpp:122-131) then M = R diag(e^s), Sigma = M M^T.
+__device__ void covariance(const double* ls, const double* q, double* sig) {
+    const double n = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    const double w = q[0] / n, x = q[1] / n, y = q[2] / n, z = q[3] / n;
+    double m[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z),     2 * (x * z + w * y),
+                   2 * (x * y + w * z),     1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                   2 * (x * z - w * y),     2 * (y * z + w * x),     1 - 2 * (x * x + y * y)};
+    const double e[3] = {exp(ls[0]), exp(ls[1]), exp(ls[2])};
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) m[r * 3 + c] *= e[c];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) s += m[i * 3 + k] * m[j * 3 + k];
+            sig[i * 3 + j] = s;
+        }
+}
+
+__device__ __forceinline__ double normalization(int l, int am) {  // radiance.cpp:9-14
+    double ratio = 1.0;
+    for (int i = l - am + 1; i <= l + am; ++i) ratio /= static_cast<double>(i);
+    return sqrt((2.0 * l + 1.0) / (4.0 * kPi) * ratio);
+}
+
+__global__ void k_tx_prep(int K, int l_max, int C, const double* __restrict__ pos,
+                          const double* __restrict__ ls, const double* __restrict__ q,
+                          const double* __restrict__ tau_logit,
+                          const double* __restrict__ coeffs64, double tx0, double tx1, double tx2,
+                          DevGrid g, GaussRec* __restrict__ rec, int* __restrict__ culled,
+                          double* __restrict__ geom, int4* __restrict__ spans,
+                          double* __restrict__ basis64, float2* __restrict__ basis32,
+                          float2* __restrict__ gb32, uint64_t* __restrict__ depth_key,
+                          int* __restrict__ tile_count) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    const int L = (l_max + 1) * (l_max + 1);
+    double* gm = geom + 12 * static_cast<size_t>(k);
+    for (int i = 0; i < 12; ++i) gm[i] = 0.0;
+    int4 sp = make_int4(0, -1, 0, -1);
+    int is_culled = 1;
+    GaussRec r{};
+
+    double sig[9];
+    covariance(ls + 3 * static_cast<size_t>(k), q + 4 * static_cast<size_t>(k), sig);
+    const double tau = 1.0 / (1.0 + exp(-tau_logit[k]));  // linalg.hpp:157
+
+    const double u0 = pos[3 * static_cast<size_t>(k)] - tx0;
+    const double u1 = pos[3 * static_cast<size_t>(k) + 1] - tx1;
+    const double u2 = pos[3 * static_cast<size_t>(k) + 2] - tx2;
+    const double d = sqrt(u0 * u0 + u1 * u1 + u2 * u2);
+    double theta = 0.0, phi = 0.0;
+    if ((d >= g.radius) && d != 0.0) {
+        const double rho = sqrt(u0 * u0 + u1 * u1);
+        theta = atan2(rho, u2);
+        phi = wrap_two_pi(atan2(u1, u0));
+        gm[0] = theta;
+        gm[1] = phi;
+        gm[2] = d;
+        gm[11] = tau;
+        const double st = sin(theta), ct = cos(theta), sp_ = sin(phi), cp = cos(phi);
+        const double et[3] = {ct * cp, ct * sp_, -st};
+        const double ep[3] = {-sp_, cp, 0.0};
+        const double inv_d2 = 1.0 / (d * d);
+        double t[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) t[i] = sig[3 * i] * et[0] + sig[3 * i + 1] * et[1] + sig[3 * i + 2] * et[2];
+        const double a = (et[0] * t[0] + et[1] * t[1] + et[2] * t[2]) * inv_d2;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) t[i] = sig[3 * i] * ep[0] + sig[3 * i + 1] * ep[1] + sig[3 * i + 2] * ep[2];
+        const double b = (et[0] * t[0] + et[1] * t[1] + et[2] * t[2]) * inv_d2;
+        const double dd = (ep[0] * t[0] + ep[1] * t[1] + ep[2] * t[2]) * inv_d2;
+        const double det = a * dd - b * b;
+        const double pa = dd / det, pb = -b / det, pc = -b / det, pd = a / det;
+        gm[3] = a; gm[4] = b; gm[5] = b; gm[6] = dd;
+        gm[7] = pa; gm[8] = pb; gm[9] = pc; gm[10] = pd;
+
+        const double r_theta = 3.0 * sqrt(dmax(a, 0.0));
+        const double r_phi_scaled = 3.0 * sqrt(dmax(dd, 0.0));
+        const double theta_lo = theta - r_theta, theta_hi = theta + r_theta;
+        if (!(theta_hi < g.tmin || theta_lo > g.tmax)) {
+            const int i0 = clampi(static_cast<int>(floor((theta_lo - g.tmin) / g.dth)), 0, g.nt - 1);
+            const int i1 = clampi(static_cast<int>(floor((theta_hi - g.tmin) / g.dth)), 0, g.nt - 1);
+            sp.x = i0 / g.ts;
+            sp.y = i1 / g.ts;
+            const double w_phi = st > 1e-12 ? r_phi_scaled / st : kPi;
+            if (w_phi >= kPi) {
+                sp.z = 0;
+                sp.w = g.tiles_p - 1;
+            } else {
+                const int j0 = clampi(static_cast<int>(floor(wrap_two_pi(phi - w_phi) / g.dph)), 0, g.np - 1);
+                const int j1 = clampi(static_cast<int>(floor(wrap_two_pi(phi + w_phi) / g.dph)), 0, g.np - 1);
+                sp.z = j0 / g.ts;
+                sp.w = j1 / g.ts;
+                if (j0 > j1) sp.w += g.tiles_p;
+                if (sp.w - sp.z + 1 > g.tiles_p) {
+                    sp.z = 0;
+                    sp.w = g.tiles_p - 1;
+                }
+            }
+            is_culled = 0;
+            r.theta = theta;
+            r.phi = phi;
+            r.sin_theta = st;
+            r.pa = pa;
+            r.pbc = pb + pc;
+            r.pd = pd;
+            r.tau = tau;
+        }
+    }
+    rec[k] = r;
+    culled[k] = is_culled;
+    spans[k] = sp;
+    tile_count[k] = is_culled ? 0 : (sp.y - sp.x + 1) * (sp.w - sp.z + 1);
+    depth_key[k] = is_culled ? ~0ull : static_cast<uint64_t>(__double_as_longlong(d));
+
+    // FLE basis at the centre direction (zero for culled Gaussians).
+    double* b64 = basis64 + static_cast<size_t>(k) * L * 2;
+    float2* b32 = basis32 + static_cast<size_t>(k) * L;
+    float2* g32 = gb32 + static_cast<size_t>(k) * L * C;
+    const double* cb = coeffs64 + static_cast<size_t>(k) * L * C * 2;
+    if (is_culled) {
+        for (int i = 0; i < L; ++i) {
+            b64[2 * i] = 0.0;
+            b64[2 * i + 1] = 0.0;
+            b32[i] = make_float2(0.f, 0.f);
+            for (int c = 0; c < C; ++c) g32[i * C + c] = make_float2(0.f, 0.f);
+        }
+        return;
+    }
+    // legendre_table (radiance.cpp:16-37) on x = cos(theta), without the
+    // Condon-Shortley phase; entries packed l*(l+1)/2 + m.
+    double P[(kMaxLmax + 1) * (kMaxLmax + 2) / 2];
+    double x = cos(theta);
+    x = x < -1.0 ? -1.0 : (x > 1.0 ? 1.0 : x);
+    const double s = sqrt(dmax(0.0, (1.0 - x) * (1.0 + x)));
+#define AT(l, m) P[(l) * ((l) + 1) / 2 + (m)]
+    AT(0, 0) = 1.0;
+    for (int m = 1; m <= l_max; ++m) AT(m, m) = AT(m - 1, m - 1) * (2.0 * m - 1.0) * s;
+    for (int m = 0; m < l_max; ++m) AT(m + 1, m) = x * (2.0 * m + 1.0) * AT(m, m);
+    for (int m = 0; m <= l_max; ++m)
+        for (int l = m + 2; l <= l_max; ++l)
+            AT(l, m) = (x * (2.0 * l - 1.0) * AT(l - 1, m) - (l + m - 1.0) * AT(l - 2, m)) /
+                       static_cast<double>(l - m);
+    for (int l = 0; l <= l_max; ++l)
+        for (int m = -l; m <= l; ++m) {
+            const int am = m < 0 ? -m : m;
+            const double np = normalization(l, am) * AT(l, am);
+            const int idx = l * l + m + l;
+            const double br = np * cos(m * phi), bi = np * sin(m * phi);
+            b64[2 * idx] = br;
+            b64[2 * idx + 1] = bi;
+            b32[idx] = make_float2(static_cast<float>(br), static_cast<float>(bi));
+            for (int c = 0; c < C; ++c) {
+                const double a_ = cb[(idx * C + c) * 2], b_ = cb[(idx * C + c) * 2 + 1];
+                g32[idx * C + c] = make_float2(static_cast<float>(a_ * br - b_ * bi),
+                                               static_cast<float>(a_ * bi + b_ * br));
+            }
+        }
+#undef AT
+}
+
+__global__ void k_occupancy(int K, int R, const double* __restrict__ pos,
+                            const double* __restrict__ ls, const double* __restrict__ q,
+                            const double* __restrict__ tau_logit, double lo0, double lo1,
+                            double lo2, double hi0, double hi1, double hi2,
+                            unsigned long long* __restrict__ out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    const double lo[3] = {lo0, lo1, lo2};
+    const double ext[3] = {hi0 - lo0, hi1 - lo1, hi2 - lo2};
+    const double cell[3] = {ext[0] / R, ext[1] / R, ext[2] / R};
+    const double* p = pos + 3 * static_cast<size_t>(k);
+    double m[9], r[9];
+    covariance(ls + 3 * static_cast<size_t>(k), q + 4 * static_cast<size_t>(k), m);
+    // Mat3::inverse (linalg.hpp:88-100)
+    const double det = m[0] * (m[4] * m[8] - m[5] * m[7]) - m[1] * (m[3] * m[8] - m[5] * m[6]) +
+                       m[2] * (m[3] * m[7] - m[4] * m[6]);
+    r[0] = (m[4] * m[8] - m[5] * m[7]) / det; r[1] = (m[2] * m[7] - m[1] * m[8]) / det;
+    r[2] = (m[1] * m[5] - m[2] * m[4]) / det; r[3] = (m[5] * m[6] - m[3] * m[8]) / det;
+    r[4] = (m[0] * m[8] - m[2] * m[6]) / det; r[5] = (m[2] * m[3] - m[0] * m[5]) / det;
+    r[6] = (m[3] * m[7] - m[4] * m[6]) / det; r[7] = (m[1] * m[6] - m[0] * m[7]) / det;
+    r[8] = (m[0] * m[4] - m[1] * m[3]) / det;
+    const double tau = 1.0 / (1.0 + exp(-tau_logit[k]));
+    int a0[3], a1[3];
+    for (int a = 0; a < 3; ++a) {
+        const double half = 2.0 * sqrt(m[a * 4]);
+        const int l = static_cast<int>(floor((p[a] - half - lo[a]) / cell[a] - 0.5));
+        const int h = static_cast<int>(ceil((p[a] + half - lo[a]) / cell[a] - 0.5));
+        a0[a] = l > 0 ? l : 0;
+        a1[a] = h < R - 1 ? h : R - 1;
+    }
+    for (int ix = a0[0]; ix <= a1[0]; ++ix)
+        for (int iy = a0[1]; iy <= a1[1]; ++iy)
+            for (int iz = a0[2]; iz <= a1[2]; ++iz) {
+                const double d0 = (lo[0] + (ix + 0.5) * cell[0]) - p[0];
+                const double d1 = (lo[1] + (iy + 0.5) * cell[1]) - p[1];
+                const double d2 = (lo[2] + (iz + 0.5) * cell[2]) - p[2];
+                const double q0 = r[0] * d0 + r[1] * d1 + r[2] * d2;
+                const double q1 = r[3] * d0 + r[4] * d1 + r[5] * d2;
+                const double q2 = r[6] * d0 + r[7] * d1 + r[8] * d2;
+                const double m2 = d0 * q0 + d1 * q1 + d2 * q2;
+                if (m2 > 4.0) continue;
+                const double v = tau * exp(-0.5 * m2);
+                atomicMax(out + (static_cast<size_t>(ix) * R + iy) * R + iz,
+                          static_cast<unsigned long long>(__double_as_longlong(v)));
+            }
+}
+
+__global__ void k_occ_finish(size_t n, const unsigned long long* __restrict__ bits,
+                             double* __restrict__ out64, float* __restrict__ out32) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    double v = __longlong_as_double(static_cast<long long>(bits[i]));
+    v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+    if (out64) out64[i] = v;
+    if (out32) out32[i] = static_cast<float>(v);
+}
+
+}  // namespace
+
+cudaError_t launch_tx_prep(const rxgs_scene_s& sc, rxgs_txstate_s& st, cudaStream_t s) {
+    if (sc.k == 0) return cudaSuccess;
+    const int threads = 128;
+    const int blocks = (sc.k + threads - 1) / threads;
+    k_tx_prep<<<blocks, threads, 0, s>>>(
+        sc.k, sc.l_max, sc.channels, sc.d_pos.as<double>(), sc.d_ls.as<double>(),
+        sc.d_q.as<double>(), sc.d_tau.as<double>(), sc.d_coeffs64.as<double>(), st.tx[0], st.tx[1],
+        st.tx[2], st.grid, st.rec.as<GaussRec>(), st.culled.as<int>(), st.geom.as<double>(),
+        st.spans.as<int4>(), st.basis64.as<double>(), st.basis32.as<float2>(),
+        st.gb32.as<float2>(), st.depth_key.as<uint64_t>(), st.tile_count.as<int>());
+    return cudaGetLastError();
+}
+
+cudaError_t launch_occupancy(const rxgs_scene_s& sc, int R, const double* lo, const double* hi,
+                             double* d_out64, float* d_out32, cudaStream_t s) {
+    const size_t n = static_cast<size_t>(R) * R * R;
+    unsigned long long* bits = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&bits), n * 8, s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(bits, 0, n * 8, s);
+    if (e != cudaSuccess) return e;
+    if (sc.k > 0) {
+        k_occupancy<<<(sc.k + 127) / 128, 128, 0, s>>>(
+            sc.k, R, sc.d_pos.as<double>(), sc.d_ls.as<double>(), sc.d_q.as<double>(),
+            sc.d_tau.as<double>(), lo[0], lo[1], lo[2], hi[0], hi[1], hi[2], bits);
+    }
+    k_occ_finish<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(n, bits, d_out64, d_out32);
+    e = cudaGetLastError();
+    cudaFreeAsync(bits, s);
+    return e;
+}
+
+}  // namespace rxgs_b200

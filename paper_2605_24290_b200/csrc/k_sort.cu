@@ -1,0 +1,167 @@
+// Tile binning: the device form of bin_and_sort (sphraster.cpp:85-102).
+//
+// The reference pushes Gaussian indices into each covered tile in index
+// order and std::stable_sort's every list by FP64 depth, i.e. each list is
+// ordered by (depth, index).  On the device:
+//   1. radix-sort all K Gaussians by the IEEE bits of their FP64 depth
+//      (positive doubles order like their bit patterns; culled -> ~0).  The
+//      sort is stable over an index-ordered input, so ties keep index order:
+//      rank[g] = position of g in (depth, index) order;
+//   2. scan the per-Gaussian tile counts in rank order and emit one
+//      (tile, g) pair per covered tile, in rank order;
+//   3. stable radix sort of the pairs by the tile id alone (ceil(log2 tiles)
+//      bits, 2 passes at 12 bits): within a tile the rank order survives;
+//   4. per-tile [begin, end) from a histogram scan, and the 64-bit sort keys
+//      (tile << 32) | rank that the north star asks to be bit-exact.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "rxgs_internal.cuh"
+
+namespace rxgs_b200 {
+namespace {
+
+__global__ void k_iota(int n, int* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = i;
+}
+
+__global__ void k_rank(int K, const int* __restrict__ order, const int* __restrict__ tile_count,
+                       int* __restrict__ rank, int64_t* __restrict__ cnt_sorted) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r > K) return;
+    if (r == K) {
+        cnt_sorted[K] = 0;
+        return;
+    }
+    const int g = order[r];
+    rank[g] = r;
+    cnt_sorted[r] = tile_count[g];
+}
+
+__global__ void k_emit(int K, int tiles_p, const int* __restrict__ order,
+                       const int4* __restrict__ spans, const int64_t* __restrict__ scan,
+                       uint32_t* __restrict__ tkey, int* __restrict__ tval,
+                       int* __restrict__ tile_hist) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= K) return;
+    const int64_t begin = scan[r];
+    const int64_t n = scan[r + 1] - begin;
+    if (n == 0) return;
+    const int g = order[r];
+    const int4 sp = spans[g];
+    int64_t o = begin;
+    for (int tt = sp.x; tt <= sp.y; ++tt)
+        for (int pp = sp.z; pp <= sp.w; ++pp) {
+            const int tile = tt * tiles_p + pp % tiles_p;
+            tkey[o] = static_cast<uint32_t>(tile);
+            tval[o] = g;
+            atomicAdd(tile_hist + tile, 1);
+            ++o;
+        }
+}
+
+__global__ void k_keys(int64_t n, const uint32_t* __restrict__ tkey, const int* __restrict__ list,
+                       const int* __restrict__ rank, uint64_t* __restrict__ keys) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    keys[i] = (static_cast<uint64_t>(tkey[i]) << 32) | static_cast<uint32_t>(rank[list[i]]);
+}
+
+__global__ void k_widen(int n, const int* __restrict__ in, int64_t* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = in[i];
+    if (i == n) out[n] = 0;
+}
+
+int bits_for(int n) {
+    int b = 1;
+    while ((1 << b) < n) ++b;
+    return b;
+}
+
+}  // namespace
+
+int bin_tiles(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
+    const int K = st.k;
+    const int n_tiles = st.grid.n_tiles;
+    RXGS_CUDA(st.order.ensure(sizeof(int) * (K + 1)));
+    RXGS_CUDA(st.rank.ensure(sizeof(int) * (K + 1)));
+    RXGS_CUDA(st.scan.ensure(sizeof(int64_t) * (K + 1)));
+    RXGS_CUDA(st.tile_offsets.ensure(sizeof(int64_t) * (n_tiles + 1)));
+
+    // scratch: sorted depth keys (K u64) | iota (K int) | cnt_sorted (K+1 i64) | hist
+    const size_t off_iota = sizeof(uint64_t) * (K + 1);
+    const size_t off_cnt = off_iota + sizeof(int) * (K + 2);
+    const size_t off_hist = off_cnt + sizeof(int64_t) * (K + 2);
+    const size_t off_hist64 = off_hist + sizeof(int) * (n_tiles + 2);
+    RXGS_CUDA(ctx->scratch_a.ensure(off_hist64 + sizeof(int64_t) * (n_tiles + 2)));
+    char* base = ctx->scratch_a.as<char>();
+    uint64_t* dk_sorted = reinterpret_cast<uint64_t*>(base);
+    int* iota = reinterpret_cast<int*>(base + off_iota);
+    int64_t* cnt_sorted = reinterpret_cast<int64_t*>(base + off_cnt);
+    int* hist = reinterpret_cast<int*>(base + off_hist);
+    int64_t* hist64 = reinterpret_cast<int64_t*>(base + off_hist64);
+
+    RXGS_CUDA(cudaMemsetAsync(hist, 0, sizeof(int) * (n_tiles + 1), s));
+    if (K > 0) {
+        k_iota<<<(K + 255) / 256, 256, 0, s>>>(K, iota);
+        size_t tmp = 0;
+        RXGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, st.depth_key.as<uint64_t>(), dk_sorted,
+                                                  iota, st.order.as<int>(), K, 0, 64, s));
+        RXGS_CUDA(ctx->sort_tmp.ensure(tmp));
+        RXGS_CUDA(cub::DeviceRadixSort::SortPairs(ctx->sort_tmp.p, tmp, st.depth_key.as<uint64_t>(),
+                                                  dk_sorted, iota, st.order.as<int>(), K, 0, 64, s));
+        k_rank<<<(K + 1 + 255) / 256, 256, 0, s>>>(K, st.order.as<int>(), st.tile_count.as<int>(),
+                                                   st.rank.as<int>(), cnt_sorted);
+        tmp = 0;
+        RXGS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt_sorted, st.scan.as<int64_t>(), K + 1, s));
+        RXGS_CUDA(ctx->sort_tmp.ensure(tmp));
+        RXGS_CUDA(cub::DeviceScan::ExclusiveSum(ctx->sort_tmp.p, tmp, cnt_sorted, st.scan.as<int64_t>(),
+                                                K + 1, s));
+    }
+    int64_t total = 0;
+    if (K > 0) {
+        RXGS_CUDA(cudaMemcpyAsync(&total, st.scan.as<int64_t>() + K, sizeof(int64_t),
+                                  cudaMemcpyDeviceToHost, s));
+        RXGS_CUDA(cudaStreamSynchronize(s));
+    }
+    st.entries = total;
+    RXGS_CUDA(st.list.ensure(sizeof(int) * (total + 1)));
+    RXGS_CUDA(st.keys.ensure(sizeof(uint64_t) * (total + 1)));
+    // pair scratch: tkey | tval | tkey_sorted
+    const size_t o_tval = sizeof(uint32_t) * (total + 1);
+    const size_t o_tks = o_tval + sizeof(int) * (total + 1);
+    RXGS_CUDA(ctx->scratch_b.ensure(o_tks + sizeof(uint32_t) * (total + 1)));
+    char* pb = ctx->scratch_b.as<char>();
+    uint32_t* tkey = reinterpret_cast<uint32_t*>(pb);
+    int* tval = reinterpret_cast<int*>(pb + o_tval);
+    uint32_t* tks = reinterpret_cast<uint32_t*>(pb + o_tks);
+    if (total > 0) {
+        k_emit<<<(K + 127) / 128, 128, 0, s>>>(K, st.grid.tiles_p, st.order.as<int>(), st.spans.as<int4>(),
+                                               st.scan.as<int64_t>(), tkey, tval, hist);
+        size_t tmp = 0;
+        const int end_bit = bits_for(n_tiles);
+        RXGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, tkey, tks, tval, st.list.as<int>(),
+                                                  static_cast<int>(total), 0, end_bit, s));
+        RXGS_CUDA(ctx->sort_tmp.ensure(tmp));
+        RXGS_CUDA(cub::DeviceRadixSort::SortPairs(ctx->sort_tmp.p, tmp, tkey, tks, tval,
+                                                  st.list.as<int>(), static_cast<int>(total), 0,
+                                                  end_bit, s));
+        k_keys<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(total, tks, st.list.as<int>(),
+                                                                          st.rank.as<int>(),
+                                                                          st.keys.as<uint64_t>());
+    }
+    k_widen<<<(n_tiles + 1 + 255) / 256, 256, 0, s>>>(n_tiles, hist, hist64);
+    size_t tmp = 0;
+    RXGS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, hist64, st.tile_offsets.as<int64_t>(),
+                                            n_tiles + 1, s));
+    RXGS_CUDA(ctx->sort_tmp.ensure(tmp));
+    RXGS_CUDA(cub::DeviceScan::ExclusiveSum(ctx->sort_tmp.p, tmp, hist64,
+                                            st.tile_offsets.as<int64_t>(), n_tiles + 1, s));
+    ctx->launches += 8;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? RXGS_OK : cuda_fail(e, "bin_tiles");
+}
+
+}  // namespace rxgs_b200

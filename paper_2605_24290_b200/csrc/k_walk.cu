@@ -1,0 +1,106 @@
+// Receiver-independent front-to-back blend weights, FP64 (-fmad=false).
+//
+// render_field (sphraster.cpp:278-298) walks each cell's tile list, computing
+// w = min(tau * exp(-m2/2), 0.999) (gaussian_weight :239-251), accumulating
+// T*w*s for every receiver, updating T *= 1-w and stopping once T < 1e-4.
+// Neither w nor T depends on the receiver, so the walk is done ONCE per
+// transmitter here, in FP64 with the reference's operation order (the exit
+// decision is a discontinuity: it must be taken exactly where the reference
+// takes it).  The result is the blend-weight matrix of every tile,
+//     tw[entry][cell] = T_prev(cell, entry) * w(cell, entry)    (f32),
+// zero past each cell's exit, truncated at the tile's longest walk.  The
+// per-receiver composite is then a plain (cells x walk) x (walk x receivers)
+// product (k_composite.cu).
+//
+// One CTA per (tile, 64-cell block); records are staged through shared
+// memory in chunks of 64 list entries; the CTA stops loading as soon as every
+// cell has exited (block-wide early exit via __syncthreads_or).
+#include "rxgs_internal.cuh"
+
+namespace rxgs_b200 {
+namespace {
+
+constexpr int kChunk = 64;
+
+__device__ __forceinline__ double wrap_pm_pi(double a) {  // linalg.hpp:152-157
+    a = fmod(a, kTwoPi);
+    if (a > kPi) a -= kTwoPi;
+    if (a <= -kPi) a += kTwoPi;
+    return a;
+}
+
+__global__ void __launch_bounds__(64) k_walk(DevGrid g, const int64_t* __restrict__ tile_offsets,
+                                             const int* __restrict__ list,
+                                             const GaussRec* __restrict__ rec,
+                                             float* __restrict__ tw, int* __restrict__ walk_len,
+                                             double* __restrict__ cell_T,
+                                             int* __restrict__ cell_len) {
+    __shared__ GaussRec srec[kChunk];
+    __shared__ int s_max;
+    const int tile = blockIdx.x;
+    const int cb = blockIdx.y;
+    const int lane = threadIdx.x;
+    const int tt = tile / g.tiles_p, tp = tile % g.tiles_p;
+    const int lc = cb * kMaxCellsPerBlock + lane;
+    const int row = tt * g.ts + lc / g.ts;
+    const int col = tp * g.ts + lc % g.ts;
+    const bool valid = lc < g.cpt && (lc / g.ts) < g.ts && row < g.nt && col < g.np;
+    const int64_t begin = tile_offsets[tile];
+    const int n = static_cast<int>(tile_offsets[tile + 1] - begin);
+    const size_t stride = static_cast<size_t>(g.cell_blocks) * kMaxCellsPerBlock;
+    float* out = tw + static_cast<size_t>(begin) * stride + static_cast<size_t>(cb) * kMaxCellsPerBlock + lane;
+
+    const double theta_r = valid ? g.tmin + (row + 0.5) * g.dth : 0.0;
+    const double phi_r = valid ? (col + 0.5) * g.dph : 0.0;
+    double T = 1.0;
+    int len = valid ? n : 0;
+    bool alive = valid && n > 0;
+    if (lane == 0) s_max = 0;
+    for (int c0 = 0; c0 < n; c0 += kChunk) {
+        if (!__syncthreads_or(alive)) break;
+        const int m = min(kChunk, n - c0);
+        if (lane < m) srec[lane] = rec[list[begin + c0 + lane]];
+        __syncthreads();
+        if (alive) {
+            for (int i = 0; i < m; ++i) {
+                const GaussRec r = srec[i];
+                const double dt = theta_r - r.theta;
+                const double dpraw = wrap_pm_pi(phi_r - r.phi);
+                const double dp = r.sin_theta * dpraw;
+                const double m2 = r.pa * dt * dt + r.pbc * dt * dp + r.pd * dp * dp;
+                double w = r.tau * exp(-0.5 * m2);
+                w = kWeightClamp < w ? kWeightClamp : w;  // std::min(w, 0.999)
+                out[static_cast<size_t>(c0 + i) * stride] = static_cast<float>(T * w);
+                T *= 1.0 - w;
+                if (T < kEarlyExitT) {
+                    len = c0 + i + 1;
+                    alive = false;
+                    break;
+                }
+            }
+        }
+    }
+    atomicMax(&s_max, len);
+    __syncthreads();
+    const int wmax = s_max;
+    for (int e = len; e < wmax; ++e) out[static_cast<size_t>(e) * stride] = 0.0f;
+    if (lane == 0) walk_len[tile * g.cell_blocks + cb] = wmax;
+    if (valid) {
+        const size_t cell = static_cast<size_t>(row) * g.np + col;
+        cell_T[cell] = T;
+        cell_len[cell] = len;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_walk(rxgs_txstate_s& st, cudaStream_t s) {
+    const DevGrid& g = st.grid;
+    dim3 grid(g.n_tiles, g.cell_blocks);
+    k_walk<<<grid, 64, 0, s>>>(g, st.tile_offsets.as<int64_t>(), st.list.as<int>(),
+                               st.rec.as<GaussRec>(), st.tw.as<float>(), st.walk_len.as<int>(),
+                               st.cell_T.as<double>(), st.cell_len.as<int>());
+    return cudaGetLastError();
+}
+
+}  // namespace rxgs_b200

@@ -1,0 +1,190 @@
+// Internal types shared by the C-ABI layer (capi.cu) and the kernels.
+// Device-side data layout is documented in DESIGN.md section 3.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "rxgs_b200.h"
+
+namespace rxgs_b200 {
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kTwoPi = 2.0 * kPi;
+constexpr double kWeightClamp = 0.999;  // sphraster.hpp:72
+constexpr double kEarlyExitT = 1e-4;    // sphraster.hpp:73
+constexpr double kRssiFloor = 1e-12;    // channelsim.hpp:115
+constexpr double kAmpEps = 1e-8;        // radiance.hpp:80
+constexpr int kMaxLmax = 15;            // basis recurrences kept in registers/local memory
+constexpr int kMaxCellsPerBlock = 64;   // composite cell block (one 8x8 tile)
+
+struct DevGrid {
+    int nt, np, ts, tiles_t, tiles_p, n_tiles, cpt, cell_blocks;
+    double radius, tmin, tmax, dth, dph;
+};
+
+// Receiver-independent per-Gaussian record read by the FP64 blend walk.
+struct alignas(64) GaussRec {
+    double theta, phi, sin_theta, pa, pbc, pd, tau, pad;
+};
+
+// Error capture: thread-local message + status.
+struct Status {
+    int code = RXGS_OK;
+    std::string msg;
+};
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define RXGS_CUDA(call)                                              \
+    do {                                                             \
+        cudaError_t e__ = (call);                                    \
+        if (e__ != cudaSuccess) return ::rxgs_b200::cuda_fail(e__, #call); \
+    } while (0)
+
+// Grow-only device buffer.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    cudaError_t ensure(size_t n) {
+        if (n <= bytes && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMalloc(&p, n ? n : 16);
+        if (e == cudaSuccess) bytes = n;
+        return e;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct KStat {
+    double ms = 0.0;
+    int64_t launches = 0;
+    double work = 0.0;
+};
+
+struct PendingTiming {
+    std::string name;
+    cudaEvent_t a, b;
+    double work;
+};
+
+}  // namespace rxgs_b200
+
+struct rxgs_ctx_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    bool profile = false;
+    int64_t launches = 0;
+    std::map<std::string, rxgs_b200::KStat> stats;
+    std::vector<rxgs_b200::PendingTiming> pending;
+    std::vector<cudaEvent_t> event_pool;
+    // scratch
+    rxgs_b200::DevBuf sort_tmp, scratch_a, scratch_b, scratch_c, scratch_d, signals, ag, partial,
+        err_flag, host_in, host_out;
+    int sm_count = 148;
+};
+
+struct rxgs_scene_s {
+    rxgs_ctx ctx = nullptr;
+    int k = 0, l_max = 0, channels = 1, L = 1, modality = 0;
+    std::vector<double> h_pos, h_ls, h_q, h_tau, h_coeffs;
+    rxgs_b200::DevBuf d_pos, d_ls, d_q, d_tau, d_coeffs64, d_coeffs32, d_pos32;
+};
+
+struct rxgs_txstate_s {
+    rxgs_ctx ctx = nullptr;
+    int k = 0, l_max = 0, L = 1, channels = 1;
+    rxgs_b200::DevGrid grid{};
+    double tx[3] = {0, 0, 0};
+    int64_t entries = 0, visible = 0;
+    double walk_sum = 0.0, tile_walk_sum = 0.0;
+    rxgs_b200::DevBuf rec, culled, geom, spans, basis64, basis32, gb32, depth_key, tile_count,
+        order, rank, scan, tile_offsets, list, keys, tw, walk_len, cell_T, cell_len;
+};
+
+struct rxgs_cond_s {
+    rxgs_ctx ctx = nullptr;
+    int F = 6, hidden = 64, dc = 16, S = 16, R = 32, nearest = 0, mode = 0, l_max = 0, C = 1;
+    int L = 1, gin = 0;
+    int64_t n_params = 0;
+    size_t o_freq, o_gw1, o_gb1, o_gw2, o_gb2, o_gw3, o_gb3, o_emb, o_lw1, o_lb1, o_lw2, o_lb2,
+        o_lw3, o_lb3;
+    std::vector<double> h_params;
+    bool has_occ = false;
+    double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    int64_t global_calls = 0, local_calls = 0;
+    rxgs_b200::DevBuf d_params32, d_params64, d_occ32;
+    bool use_global() const { return mode != 2; }
+    bool use_local() const { return mode != 1; }
+    bool additive() const { return mode == 3; }
+    bool no_occ() const { return mode == 4 || !has_occ; }
+};
+
+namespace rxgs_b200 {
+
+// ---- timing helpers (capi.cu)
+void timing_begin(rxgs_ctx ctx, const char* name, cudaEvent_t* a);
+void timing_end(rxgs_ctx ctx, const char* name, cudaEvent_t a, double work);
+
+// ---- k_geometry.cu (FP64, compiled with -fmad=false)
+cudaError_t launch_tx_prep(const rxgs_scene_s& sc, rxgs_txstate_s& st, cudaStream_t s);
+cudaError_t launch_occupancy(const rxgs_scene_s& sc, int R, const double* lo, const double* hi,
+                             double* d_out64, float* d_out32, cudaStream_t s);
+
+// ---- k_sort.cu
+// Bins culled/spans/depth_key already in st; fills tile_offsets, list, keys.
+int bin_tiles(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s);
+
+// ---- k_walk.cu (FP64, -fmad=false)
+cudaError_t launch_walk(rxgs_txstate_s& st, cudaStream_t s);
+
+// ---- k_cond.cu
+cudaError_t launch_cond_global(const rxgs_cond_s& c, const double* d_rx, int n_rx, float* d_ag,
+                               cudaStream_t s);
+// Fused local branch + FLE reduction: signals[k][j][c] complex f32.
+cudaError_t launch_cond_signal(const rxgs_cond_s* c, const rxgs_scene_s& sc,
+                               const rxgs_txstate_s& st, const double* d_rx, int n_rx,
+                               const float* d_ag, float2* d_sig, int* d_err, cudaStream_t s);
+// Materialised conditioned coefficients (condition_forward API).
+cudaError_t launch_cond_materialize(const rxgs_cond_s& c, const rxgs_scene_s& sc,
+                                    const double* d_rx, int n_rx, const float* d_ag, double* d_out,
+                                    double* d_local_in, int* d_err, cudaStream_t s);
+cudaError_t launch_probe(const rxgs_cond_s& c, int n, const double* d_from, const double* d_to,
+                         double* d_out, cudaStream_t s);
+cudaError_t launch_check_coincide(const rxgs_scene_s& sc, const double* d_rx, int n_rx, int* d_err,
+                                  cudaStream_t s);
+// reduce_signals from materialised f64 coefficients.
+cudaError_t launch_reduce_signals(const rxgs_txstate_s& st, const double* d_coeffs, int n_rx,
+                                  float2* d_sig, int* d_err, cudaStream_t s);
+
+// ---- k_composite.cu
+struct CompositeOut {
+    float* spectrum = nullptr;    // [j][cell] (C == 1)
+    float* rssi_partial = nullptr;  // [tile][j] power partials (C == 1)
+    double* values = nullptr;     // [j][c][re/im][cell] f64 (materialised field)
+    float* csi_partial = nullptr; // [tile][j][c][2]
+};
+cudaError_t launch_composite(const rxgs_txstate_s& st, const float2* d_sig, int n_rx,
+                             const CompositeOut& out, cudaStream_t s);
+cudaError_t launch_rssi_finalize(const float* d_partial, int n_tiles, int n_rx, float* d_rssi,
+                                 double* d_rssi64, cudaStream_t s);
+cudaError_t launch_aggregate(const DevGrid& g, int modality, int n_rx, int channels,
+                             const double* d_values, double* d_out, int* d_err, bool reduce,
+                             cudaStream_t s);
+cudaError_t launch_fill_transmittance(const rxgs_txstate_s& st, int n_rx, double* d_T,
+                                      cudaStream_t s);
+
+}  // namespace rxgs_b200
