@@ -282,6 +282,7 @@ int rxgs_ctx_destroy(rxgs_ctx ctx) {
         cudaEventDestroy(p.b);
     }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
+    delete ctx->spare_tx;
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
     return RXGS_OK;
@@ -417,7 +418,11 @@ int rxgs_tx_state_build(rxgs_ctx ctx, rxgs_scene sc, const double tx[3], const r
     RX_TRY(validate_grid(grid));
     RX_TRY(set_device(ctx));
     cudaStream_t s = ctx->stream;
-    auto* st = new rxgs_txstate_s;
+    // Reuse the device buffers of the last destroyed state (grow-only), so a
+    // per-transmitter rebuild does not pay cudaMalloc/cudaFree every time.
+    rxgs_txstate_s* st = ctx->spare_tx ? ctx->spare_tx : new rxgs_txstate_s;
+    ctx->spare_tx = nullptr;
+    st->entries = st->visible = 0;
     st->ctx = ctx;
     st->k = sc->k;
     st->l_max = sc->l_max;
@@ -458,19 +463,6 @@ int rxgs_tx_state_build(rxgs_ctx ctx, rxgs_scene sc, const double tx[3], const r
     ctx->launches += 1;
     rc = bin_tiles(ctx, *st, s);
     if (rc) return fail_st(rc);
-    // visible = Gaussians with a finite depth key (culled sort last)
-    {
-        std::vector<int> cul = std::vector<int>(static_cast<size_t>(sc->k));
-        if (sc->k) {
-            const cudaError_t e = cudaMemcpyAsync(cul.data(), st->culled.p, sc->k * sizeof(int),
-                                                  cudaMemcpyDeviceToHost, s);
-            if (e != cudaSuccess) return fail_st(cuda_fail(e, "culled"));
-            cudaStreamSynchronize(s);
-        }
-        int64_t v = 0;
-        for (int x : cul) v += x ? 0 : 1;
-        st->visible = v;
-    }
     const DevGrid& g = st->grid;
     const size_t cells = static_cast<size_t>(g.nt) * g.np;
     ENS(tw, std::max<size_t>(st->entries, 1) * g.cell_blocks * kMaxCellsPerBlock * sizeof(float));
@@ -492,8 +484,15 @@ int rxgs_tx_state_build(rxgs_ctx ctx, rxgs_scene sc, const double tx[3], const r
 
 int rxgs_tx_state_destroy(rxgs_txstate st) {
     if (!st) return RXGS_OK;
-    cudaSetDevice(st->ctx->device);
-    cudaStreamSynchronize(st->ctx->stream);
+    rxgs_ctx ctx = st->ctx;
+    cudaSetDevice(ctx->device);
+    if (!ctx->spare_tx) {
+        // Keep the buffers for the next build; stream order makes reuse safe
+        // (later kernels on this stream run after every reader of st).
+        ctx->spare_tx = st;
+        return RXGS_OK;
+    }
+    cudaStreamSynchronize(ctx->stream);
     delete st;
     return RXGS_OK;
 }

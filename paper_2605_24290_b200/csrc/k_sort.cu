@@ -27,7 +27,8 @@ __global__ void k_iota(int n, int* __restrict__ out) {
 }
 
 __global__ void k_rank(int K, const int* __restrict__ order, const int* __restrict__ tile_count,
-                       int* __restrict__ rank, int64_t* __restrict__ cnt_sorted) {
+                       const uint64_t* __restrict__ depth_key, int* __restrict__ rank,
+                       int64_t* __restrict__ cnt_sorted, unsigned long long* __restrict__ n_culled) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r > K) return;
     if (r == K) {
@@ -37,6 +38,7 @@ __global__ void k_rank(int K, const int* __restrict__ order, const int* __restri
     const int g = order[r];
     rank[g] = r;
     cnt_sorted[r] = tile_count[g];
+    if (depth_key[g] == ~0ull) atomicAdd(n_culled, 1ull);
 }
 
 __global__ void k_emit(int K, int tiles_p, const int* __restrict__ order,
@@ -90,20 +92,25 @@ int bin_tiles(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
     RXGS_CUDA(st.scan.ensure(sizeof(int64_t) * (K + 1)));
     RXGS_CUDA(st.tile_offsets.ensure(sizeof(int64_t) * (n_tiles + 1)));
 
-    // scratch: sorted depth keys (K u64) | iota (K int) | cnt_sorted (K+1 i64) | hist
-    const size_t off_iota = sizeof(uint64_t) * (K + 1);
-    const size_t off_cnt = off_iota + sizeof(int) * (K + 2);
-    const size_t off_hist = off_cnt + sizeof(int64_t) * (K + 2);
-    const size_t off_hist64 = off_hist + sizeof(int) * (n_tiles + 2);
-    RXGS_CUDA(ctx->scratch_a.ensure(off_hist64 + sizeof(int64_t) * (n_tiles + 2)));
+    // scratch: sorted depth keys (K u64) | iota (K int) | cnt_sorted (K+1 i64) | hist |
+    // hist64 | [total, culled] (every sub-buffer 256-byte aligned)
+    auto al = [](size_t x) { return (x + 255) & ~static_cast<size_t>(255); };
+    const size_t off_iota = al(sizeof(uint64_t) * (K + 1));
+    const size_t off_cnt = off_iota + al(sizeof(int) * (K + 2));
+    const size_t off_hist = off_cnt + al(sizeof(int64_t) * (K + 2));
+    const size_t off_hist64 = off_hist + al(sizeof(int) * (n_tiles + 2));
+    const size_t off_red = off_hist64 + al(sizeof(int64_t) * (n_tiles + 2));
+    RXGS_CUDA(ctx->scratch_a.ensure(off_red + 256));
     char* base = ctx->scratch_a.as<char>();
     uint64_t* dk_sorted = reinterpret_cast<uint64_t*>(base);
     int* iota = reinterpret_cast<int*>(base + off_iota);
     int64_t* cnt_sorted = reinterpret_cast<int64_t*>(base + off_cnt);
     int* hist = reinterpret_cast<int*>(base + off_hist);
     int64_t* hist64 = reinterpret_cast<int64_t*>(base + off_hist64);
+    int64_t* red = reinterpret_cast<int64_t*>(base + off_red);  // [0] entries, [1] culled
 
     RXGS_CUDA(cudaMemsetAsync(hist, 0, sizeof(int) * (n_tiles + 1), s));
+    RXGS_CUDA(cudaMemsetAsync(red, 0, 2 * sizeof(int64_t), s));
     if (K > 0) {
         k_iota<<<(K + 255) / 256, 256, 0, s>>>(K, iota);
         size_t tmp = 0;
@@ -113,20 +120,23 @@ int bin_tiles(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
         RXGS_CUDA(cub::DeviceRadixSort::SortPairs(ctx->sort_tmp.p, tmp, st.depth_key.as<uint64_t>(),
                                                   dk_sorted, iota, st.order.as<int>(), K, 0, 64, s));
         k_rank<<<(K + 1 + 255) / 256, 256, 0, s>>>(K, st.order.as<int>(), st.tile_count.as<int>(),
-                                                   st.rank.as<int>(), cnt_sorted);
+                                                   st.depth_key.as<uint64_t>(), st.rank.as<int>(),
+                                                   cnt_sorted, reinterpret_cast<unsigned long long*>(red + 1));
         tmp = 0;
         RXGS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt_sorted, st.scan.as<int64_t>(), K + 1, s));
         RXGS_CUDA(ctx->sort_tmp.ensure(tmp));
         RXGS_CUDA(cub::DeviceScan::ExclusiveSum(ctx->sort_tmp.p, tmp, cnt_sorted, st.scan.as<int64_t>(),
                                                 K + 1, s));
     }
-    int64_t total = 0;
+    int64_t total = 0, culled = 0;
     if (K > 0) {
         RXGS_CUDA(cudaMemcpyAsync(&total, st.scan.as<int64_t>() + K, sizeof(int64_t),
                                   cudaMemcpyDeviceToHost, s));
+        RXGS_CUDA(cudaMemcpyAsync(&culled, red + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         RXGS_CUDA(cudaStreamSynchronize(s));
     }
     st.entries = total;
+    st.visible = K - culled;
     RXGS_CUDA(st.list.ensure(sizeof(int) * (total + 1)));
     RXGS_CUDA(st.keys.ensure(sizeof(uint64_t) * (total + 1)));
     // pair scratch: tkey | tval | tkey_sorted

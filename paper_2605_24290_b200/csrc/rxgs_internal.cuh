@@ -82,7 +82,10 @@ struct PendingTiming {
 
 }  // namespace rxgs_b200
 
+struct rxgs_txstate_s;
+
 struct rxgs_ctx_s {
+    rxgs_txstate_s* spare_tx = nullptr;  // recycled transmitter-state buffers
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;
