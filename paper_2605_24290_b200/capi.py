@@ -188,9 +188,9 @@ class Context:
         _check(_lib.rxgs_ctx_create(device, C.byref(h)))
         self.h = h
 
-    def close(self):
+    def close(self, _fn=_lib.rxgs_ctx_destroy):
         if getattr(self, "h", None):
-            _lib.rxgs_ctx_destroy(self.h)
+            _fn(self.h)
             self.h = None
 
     def __del__(self):
@@ -266,9 +266,9 @@ class Scene:
                                       ptr(sc["fle_coeffs"], np.float64), C.byref(h)))
         self.h = h
 
-    def __del__(self):
+    def __del__(self, _fn=_lib.rxgs_scene_destroy):
         if getattr(self, "h", None):
-            _lib.rxgs_scene_destroy(self.h)
+            _fn(self.h)
             self.h = None
 
     def bounds(self, inflate=0.0):
@@ -317,9 +317,9 @@ class TxState:
         _check(_lib.rxgs_tx_state_build(scene.ctx.h, scene.h, ptr(tx, np.float64), C.byref(grid), C.byref(h)))
         self.h = h
 
-    def __del__(self):
+    def __del__(self, _fn=_lib.rxgs_tx_state_destroy):
         if getattr(self, "h", None):
-            _lib.rxgs_tx_state_destroy(self.h)
+            _fn(self.h)
             self.h = None
 
     @property
@@ -368,9 +368,9 @@ class Cond:
                                      ptr(hi, np.float64) if hi is not None else None, C.byref(h)))
         self.h = h
 
-    def __del__(self):
+    def __del__(self, _fn=_lib.rxgs_cond_destroy):
         if getattr(self, "h", None):
-            _lib.rxgs_cond_destroy(self.h)
+            _fn(self.h)
             self.h = None
 
     @property

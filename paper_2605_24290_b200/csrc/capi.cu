@@ -282,7 +282,7 @@ int rxgs_ctx_destroy(rxgs_ctx ctx) {
         cudaEventDestroy(p.b);
     }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
-    delete ctx->spare_tx;
+    for (auto* t : ctx->spare_tx) delete t;
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
     return RXGS_OK;
@@ -420,8 +420,13 @@ int rxgs_tx_state_build(rxgs_ctx ctx, rxgs_scene sc, const double tx[3], const r
     cudaStream_t s = ctx->stream;
     // Reuse the device buffers of the last destroyed state (grow-only), so a
     // per-transmitter rebuild does not pay cudaMalloc/cudaFree every time.
-    rxgs_txstate_s* st = ctx->spare_tx ? ctx->spare_tx : new rxgs_txstate_s;
-    ctx->spare_tx = nullptr;
+    rxgs_txstate_s* st = nullptr;
+    if (!ctx->spare_tx.empty()) {
+        st = ctx->spare_tx.back();
+        ctx->spare_tx.pop_back();
+    } else {
+        st = new rxgs_txstate_s;
+    }
     st->entries = st->visible = 0;
     st->ctx = ctx;
     st->k = sc->k;
@@ -486,10 +491,10 @@ int rxgs_tx_state_destroy(rxgs_txstate st) {
     if (!st) return RXGS_OK;
     rxgs_ctx ctx = st->ctx;
     cudaSetDevice(ctx->device);
-    if (!ctx->spare_tx) {
+    if (ctx->spare_tx.size() < 2) {
         // Keep the buffers for the next build; stream order makes reuse safe
         // (later kernels on this stream run after every reader of st).
-        ctx->spare_tx = st;
+        ctx->spare_tx.push_back(st);
         return RXGS_OK;
     }
     cudaStreamSynchronize(ctx->stream);

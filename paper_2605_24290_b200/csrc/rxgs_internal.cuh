@@ -85,7 +85,7 @@ struct PendingTiming {
 struct rxgs_txstate_s;
 
 struct rxgs_ctx_s {
-    rxgs_txstate_s* spare_tx = nullptr;  // recycled transmitter-state buffers
+    std::vector<rxgs_txstate_s*> spare_tx;  // recycled transmitter-state buffers (<= 2)
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;
