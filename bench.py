@@ -161,7 +161,10 @@ def run_b200(args):
     dev = torch.device("cuda", local)
     sc, rx_np = make_inputs(args, capi, rank)
     ctx = capi.Context(local)
-    stream = torch.cuda.current_stream(dev)
+    # One explicit stream for torch (flush, events) and the library: the
+    # legacy default stream (handle 0) cannot be shared with the C-ABI.
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     scene = ctx.scene(sc, "spectrum")
     lo, hi = scene.bounds(0.0)

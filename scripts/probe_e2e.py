@@ -5,7 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2605_24290_b200 import capi
 dev = torch.device("cuda", 0)
 ctx = capi.Context(0)
-stream = torch.cuda.current_stream(dev); ctx.set_stream(stream.cuda_stream)
+stream = torch.cuda.Stream(dev); torch.cuda.set_stream(stream); ctx.set_stream(stream.cuda_stream)
 sc = capi.synth_scene(100_000, 2, 1, 7); scene = ctx.scene(sc)
 lo, hi = scene.bounds(0.0); cfg = capi.cond_cfg(); cond = ctx.cond(cfg, capi.synth_cond(cfg, 2, 1, lo, hi, 3, True))
 olo, ohi = scene.bounds(0.1); cond.build_occupancy(scene, 32, olo, ohi)
