@@ -66,6 +66,12 @@ int rxgs_ctx_kernel_stats(rxgs_ctx ctx, const char* name, double* total_ms, int6
 int rxgs_ctx_reset_stats(rxgs_ctx ctx);
 /* Number of kernels of this library launched since the last reset. */
 int64_t rxgs_ctx_launch_count(rxgs_ctx ctx);
+/* Conditioning kernel selection: 0 = auto (tcgen05 when hidden == 64 and
+ * C == 1, else FP32 SIMT), 1 = force the FP32 SIMT kernel (A/B checks). */
+int rxgs_ctx_set_cond_kernel(rxgs_ctx ctx, int which);
+/* Diagnostic: a 128x64x64 bf16 tcgen05 GEMM with A in TMEM and with A in
+ * shared memory, max |error| vs FP32 FMA of the same values. */
+int rxgs_selftest_tcgen05(rxgs_ctx ctx, double* err_tmem_a, double* err_smem_a);
 
 /* ------------------------------------------------------------ synthetic inputs
  * DESIGN.md section 5 (bit-identical to oracle/ and to the reference-side

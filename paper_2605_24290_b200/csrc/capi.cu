@@ -329,6 +329,26 @@ int rxgs_ctx_reset_stats(rxgs_ctx ctx) {
 
 int64_t rxgs_ctx_launch_count(rxgs_ctx ctx) { return ctx ? ctx->launches : 0; }
 
+int rxgs_ctx_set_cond_kernel(rxgs_ctx ctx, int which) {
+    if (!ctx || which < 0 || which > 1) return fail(RXGS_ERR_INVALID, "rxgs_ctx_set_cond_kernel: bad argument");
+    ctx->cond_kernel = which;
+    return RXGS_OK;
+}
+
+int rxgs_selftest_tcgen05(rxgs_ctx ctx, double* err_tmem_a, double* err_smem_a) {
+    if (!ctx) return fail(RXGS_ERR_INVALID, "null context");
+    RX_TRY(set_device(ctx));
+    RXGS_CUDA(ctx->err_flag.ensure(16));
+    RXGS_CUDA(cudaMemsetAsync(ctx->err_flag.p, 0, 8, ctx->stream));
+    RXGS_CUDA(launch_tc_selftest(ctx->err_flag.as<float>(), ctx->stream));
+    float e[2] = {0.f, 0.f};
+    RXGS_CUDA(cudaMemcpyAsync(e, ctx->err_flag.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (err_tmem_a) *err_tmem_a = e[0];
+    if (err_smem_a) *err_smem_a = e[1];
+    return RXGS_OK;
+}
+
 // ------------------------------------------------------------------ scene
 int rxgs_scene_create(rxgs_ctx ctx, int k, int l_max, int channels, int modality, const double* pos,
                       const double* ls, const double* q, const double* tau, const double* coeffs,

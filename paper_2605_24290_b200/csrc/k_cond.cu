@@ -18,49 +18,14 @@
 //   k_cond_materialize condition_forward's materialised output (FP64 affine
 //                      on the FP64 base, so zero branches are bitwise identity
 //                      exactly as in the reference).
+#include "cond_common.cuh"
 #include "rxgs_internal.cuh"
 
 namespace rxgs_b200 {
 namespace {
 
-constexpr int kHMax = 64;
-constexpr int kCMax = 8;
+using namespace cond_dev;
 
-struct CondDev {
-    const float* p32;
-    const double* p64;
-    const float* occ;
-    int F, H, dc, S, R, nearest, mode, L, C, gin;
-    int o_freq, o_gw1, o_gb1, o_gw2, o_gb2, o_gw3, o_gb3, o_emb, o_lw1, o_lb1, o_lw2, o_lb2, o_lw3, o_lb3;
-    int probe;  // 1 = sample the occupancy grid, 0 = T=1, rho=0
-    int use_global, use_local, additive;
-    float lo[3], cell[3];
-};
-
-CondDev make_dev(const rxgs_cond_s& c) {
-    CondDev d{};
-    d.p32 = c.d_params32.as<float>();
-    d.p64 = c.d_params64.as<double>();
-    d.occ = c.d_occ32.as<float>();
-    d.F = c.F; d.H = c.hidden; d.dc = c.dc; d.S = c.S; d.R = c.R; d.nearest = c.nearest;
-    d.mode = c.mode; d.L = c.L; d.C = c.C; d.gin = c.gin;
-    d.o_freq = static_cast<int>(c.o_freq); d.o_gw1 = static_cast<int>(c.o_gw1);
-    d.o_gb1 = static_cast<int>(c.o_gb1); d.o_gw2 = static_cast<int>(c.o_gw2);
-    d.o_gb2 = static_cast<int>(c.o_gb2); d.o_gw3 = static_cast<int>(c.o_gw3);
-    d.o_gb3 = static_cast<int>(c.o_gb3); d.o_emb = static_cast<int>(c.o_emb);
-    d.o_lw1 = static_cast<int>(c.o_lw1); d.o_lb1 = static_cast<int>(c.o_lb1);
-    d.o_lw2 = static_cast<int>(c.o_lw2); d.o_lb2 = static_cast<int>(c.o_lb2);
-    d.o_lw3 = static_cast<int>(c.o_lw3); d.o_lb3 = static_cast<int>(c.o_lb3);
-    d.probe = c.no_occ() ? 0 : 1;
-    d.use_global = c.use_global();
-    d.use_local = c.use_local();
-    d.additive = c.additive();
-    for (int a = 0; a < 3; ++a) {
-        d.lo[a] = static_cast<float>(c.lo[a]);
-        d.cell[a] = static_cast<float>((c.hi[a] - c.lo[a]) / c.R);
-    }
-    return d;
-}
 
 // ------------------------------------------------------------------ global branch (FP64)
 __global__ void k_cond_global(CondDev c, const double* __restrict__ rx, int n_rx,
@@ -118,122 +83,6 @@ __global__ void k_cond_global(CondDev c, const double* __restrict__ rx, int n_rx
 }
 
 // ------------------------------------------------------------------ local branch helpers
-struct LocalSmem {
-    const float* occ;
-    const float* w1;
-    const float* b1;
-    const float* w2;
-    const float* b2;
-    const float* w3;
-    const float* b3;
-};
-
-__device__ __forceinline__ float sample_tri(const CondDev& c, const float* occ, float qx, float qy,
-                                            float qz) {
-    const int R = c.R;
-    const float u0 = (qx - c.lo[0]) / c.cell[0] - 0.5f;
-    const float u1 = (qy - c.lo[1]) / c.cell[1] - 0.5f;
-    const float u2 = (qz - c.lo[2]) / c.cell[2] - 0.5f;
-    const float f0 = floorf(u0), f1 = floorf(u1), f2 = floorf(u2);
-    const int i0 = static_cast<int>(f0), i1 = static_cast<int>(f1), i2 = static_cast<int>(f2);
-    const float a0 = u0 - f0, a1 = u1 - f1, a2 = u2 - f2;
-    float acc = 0.f;
-#pragma unroll
-    for (int dx = 0; dx < 2; ++dx)
-#pragma unroll
-        for (int dy = 0; dy < 2; ++dy)
-#pragma unroll
-            for (int dz = 0; dz < 2; ++dz) {
-                const int ix = i0 + dx, iy = i1 + dy, iz = i2 + dz;
-                if (ix < 0 || iy < 0 || iz < 0 || ix >= R || iy >= R || iz >= R) continue;
-                const float w = (dx ? a0 : 1.f - a0) * (dy ? a1 : 1.f - a1) * (dz ? a2 : 1.f - a2);
-                acc += w * occ[(ix * R + iy) * R + iz];
-            }
-    return acc;
-}
-
-__device__ __forceinline__ float sample_near(const CondDev& c, const float* occ, float qx, float qy,
-                                             float qz) {
-    const int R = c.R;
-    const int ix = static_cast<int>(floorf((qx - c.lo[0]) / c.cell[0]));
-    const int iy = static_cast<int>(floorf((qy - c.lo[1]) / c.cell[1]));
-    const int iz = static_cast<int>(floorf((qz - c.lo[2]) / c.cell[2]));
-    if (ix < 0 || iy < 0 || iz < 0 || ix >= R || iy >= R || iz >= R) return 0.f;
-    return occ[(ix * R + iy) * R + iz];
-}
-
-// Local features [v_hat, d, T, rho] (conditioning.cpp:377-396).
-__device__ __forceinline__ void local_features(const CondDev& c, const float* occ, float px,
-                                               float py, float pz, float rx, float ry, float rz,
-                                               float* in) {
-    const float dx = rx - px, dy = ry - py, dz = rz - pz;
-    const float d = sqrtf(dx * dx + dy * dy + dz * dz);
-    in[0] = dx / d;
-    in[1] = dy / d;
-    in[2] = dz / d;
-    in[3] = d;
-    float T = 1.f, rho = 0.f;
-    if (c.probe) {
-        float sum = 0.f;
-        for (int s = 0; s < c.S; ++s) {
-            const float t = c.S == 1 ? 0.5f : 0.05f + 0.9f * static_cast<float>(s) / (c.S - 1);
-            const float qx = px + dx * t, qy = py + dy * t, qz = pz + dz * t;
-            const float v = c.nearest ? sample_near(c, occ, qx, qy, qz) : sample_tri(c, occ, qx, qy, qz);
-            T *= 1.f - v;
-            sum += v;
-        }
-        rho = sum / c.S;
-    }
-    in[4] = T;
-    in[5] = rho;
-}
-
-// Local MLP 6 -> H -> H -> 4C (mlp_forward :23-29) in FP32; y has 4C outputs.
-template <int HT, int CT>
-__device__ __forceinline__ void local_mlp(const CondDev& c, const LocalSmem& w, const float* in,
-                                          float* y) {
-    constexpr int HM = HT > 0 ? HT : kHMax;
-    constexpr int YM = CT > 0 ? 4 * CT : 4 * kCMax;
-    const int H = HT > 0 ? HT : c.H;
-    const int NY = CT > 0 ? 4 * CT : 4 * c.C;
-    float h1[HM];
-#pragma unroll
-    for (int o = 0; o < HM; ++o) {
-        if (HT == 0 && o >= H) break;
-        float acc = w.b1[o];
-#pragma unroll
-        for (int i = 0; i < 6; ++i) acc = fmaf(w.w1[o * 6 + i], in[i], acc);
-        h1[o] = fmaxf(acc, 0.f);
-    }
-#pragma unroll
-    for (int q = 0; q < YM; ++q)
-        if (q < NY) y[q] = w.b3[q];
-#pragma unroll 2
-    for (int o = 0; o < H; ++o) {
-        const float* row = w.w2 + o * H;
-        float acc = w.b2[o];
-        if (HT > 0) {
-#pragma unroll
-            for (int i = 0; i < HM; i += 4) {
-                const float4 wv = *reinterpret_cast<const float4*>(row + i);
-                acc = fmaf(wv.x, h1[i], acc);
-                acc = fmaf(wv.y, h1[i + 1], acc);
-                acc = fmaf(wv.z, h1[i + 2], acc);
-                acc = fmaf(wv.w, h1[i + 3], acc);
-            }
-        } else {
-            for (int i = 0; i < H; ++i) acc = fmaf(row[i], h1[i], acc);
-        }
-        const float h2 = fmaxf(acc, 0.f);
-#pragma unroll
-        for (int q = 0; q < YM; ++q)
-            if (q < NY) y[q] = fmaf(w.w3[q * H + o], h2, y[q]);
-    }
-}
-
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
 
 // ------------------------------------------------------------------ fused hot kernel
 template <int HT, int CT>
@@ -462,6 +311,8 @@ cudaError_t launch_cond_signal(const rxgs_cond_s* c, const rxgs_scene_s& sc,
                                const float* d_ag, float2* d_sig, int* d_err, cudaStream_t s) {
     (void)d_err;
     if (st.visible == 0 || n_rx == 0) return cudaSuccess;
+    if (sc.ctx->cond_kernel != 1 && cond_tc_eligible(c))
+        return launch_cond_signal_tc(*c, sc, st, d_rx, n_rx, d_ag, d_sig, s);
     CondDev d{};
     if (c) {
         d = make_dev(*c);

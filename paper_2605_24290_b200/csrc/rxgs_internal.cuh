@@ -98,6 +98,7 @@ struct rxgs_ctx_s {
     rxgs_b200::DevBuf sort_tmp, scratch_a, scratch_b, scratch_c, scratch_d, signals, ag, partial,
         err_flag, host_in, host_out;
     int sm_count = 148;
+    int cond_kernel = 0;  // 0 auto (tcgen05 when eligible), 1 force SIMT
 };
 
 struct rxgs_scene_s {
@@ -169,6 +170,12 @@ cudaError_t launch_probe(const rxgs_cond_s& c, int n, const double* d_from, cons
                          double* d_out, cudaStream_t s);
 cudaError_t launch_check_coincide(const rxgs_scene_s& sc, const double* d_rx, int n_rx, int* d_err,
                                   cudaStream_t s);
+// tcgen05 variant of the hot kernel (k_cond_tc.cu): hidden 64, C == 1.
+bool cond_tc_eligible(const rxgs_cond_s* c);
+cudaError_t launch_cond_signal_tc(const rxgs_cond_s& c, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
+                                  const double* d_rx, int n_rx, const float* d_ag, float2* d_sig,
+                                  cudaStream_t s);
+cudaError_t launch_tc_selftest(float* d_err, cudaStream_t s);
 // reduce_signals from materialised f64 coefficients.
 cudaError_t launch_reduce_signals(const rxgs_txstate_s& st, const double* d_coeffs, int n_rx,
                                   float2* d_sig, int* d_err, cudaStream_t s);

@@ -199,3 +199,30 @@ def test_predict_api(ctx, capi, orc):
     got = scene.predict(cond, grid, TX, [1.1, 0.7, 0.2])
     want = orc.predict(oscene, ocond, og, TX, [1.1, 0.7, 0.2], "spectrum")
     assert rel_err(got, want).max() < TOL
+
+
+def test_tcgen05_selftest(ctx):
+    """128x64x64 bf16 GEMM with A in TMEM and in smem vs FP32 FMA of the same values."""
+    e_tmem, e_smem = ctx.selftest_tcgen05()
+    assert e_tmem < 1e-3 and e_smem < 1e-3, (e_tmem, e_smem)
+
+
+def test_tcgen05_kernel_matches_simt_and_oracle(ctx, capi, orc):
+    """The tcgen05 hot kernel and the FP32 SIMT kernel agree, and both match the oracle."""
+    import oracle as O
+    sc = capi.synth_scene(6000, 2, 1, 17)
+    scene, cond, oscene, ocond = _setup_cond(capi, ctx, orc, sc)
+    grid = capi.Grid(45, 90, 8, 1.0)
+    st = scene.tx_state(TX, grid)
+    rx = capi.synth_points(70, 19, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
+    s_tc, r_tc = scene.render_queries(cond, st, rx)
+    ctx.set_cond_kernel("simt")
+    try:
+        s_si, r_si = scene.render_queries(cond, st, rx)
+    finally:
+        ctx.set_cond_kernel("auto")
+    assert rel_err(s_tc, s_si).max() < TOL and rel_err(r_tc, r_si).max() < TOL
+    og = O.Grid(45, 90, 8, 1.0)
+    for j in (0, 33, 69):
+        want = orc.predict(oscene, ocond, og, TX, rx[j], "spectrum").reshape(45, 90)
+        assert rel_err(s_tc[j], want).max() < TOL
