@@ -82,6 +82,61 @@ __device__ __forceinline__ float sample_tri(const CondDev& c, const float* occ, 
     return acc;
 }
 
+// Occupancy held with a one-voxel zero border, (R+2)^3: the trilinear lookup
+// then needs no per-corner bounds test -- a sample is either fully inside the
+// padded range (corners read real data or the zero border, exactly the
+// reference's "out-of-bounds corners read 0", conditioning.cpp:91) or it
+// reads 0.
+__device__ __forceinline__ int padded_index(int R, int ix, int iy, int iz) {
+    const int P = R + 2;
+    return ((ix + 1) * P + (iy + 1)) * P + (iz + 1);
+}
+
+// Fill a padded copy of the R^3 grid (called by all threads of a CTA).
+__device__ __forceinline__ void load_padded_occ(const CondDev& c, float* dst) {
+    const int R = c.R, P = R + 2, n = P * P * P;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int ix = i / (P * P) - 1, iy = (i / P) % P - 1, iz = i % P - 1;
+        const bool in = ix >= 0 && iy >= 0 && iz >= 0 && ix < R && iy < R && iz < R;
+        dst[i] = in ? c.occ[(ix * R + iy) * R + iz] : 0.f;
+    }
+}
+
+// probe_segment (conditioning.cpp:163-178) with trilinear lookups on the
+// padded grid; the segment p -> p + d is walked incrementally in voxel units.
+__device__ __forceinline__ void probe_padded(const CondDev& c, const float* occ, float px, float py, float pz,
+                                             float dx, float dy, float dz, float& T, float& rho) {
+    const int R = c.R, P = R + 2;
+    const float i0 = 1.f / c.cell[0], i1 = 1.f / c.cell[1], i2 = 1.f / c.cell[2];
+    const float b0 = (px - c.lo[0]) * i0 - 0.5f, b1 = (py - c.lo[1]) * i1 - 0.5f, b2 = (pz - c.lo[2]) * i2 - 0.5f;
+    const float s0 = dx * i0, s1 = dy * i1, s2 = dz * i2;
+    float tr = 1.f, sum = 0.f;
+    const int S = c.S;
+    for (int s = 0; s < S; ++s) {
+        const float t = S == 1 ? 0.5f : 0.05f + 0.9f * static_cast<float>(s) / (S - 1);
+        const float u0 = fmaf(t, s0, b0), u1 = fmaf(t, s1, b1), u2 = fmaf(t, s2, b2);
+        const float f0 = floorf(u0), f1 = floorf(u1), f2 = floorf(u2);
+        const int a0 = static_cast<int>(f0), a1 = static_cast<int>(f1), a2 = static_cast<int>(f2);
+        const bool ok = a0 >= -1 && a0 < R && a1 >= -1 && a1 < R && a2 >= -1 && a2 < R;
+        float v = 0.f;
+        if (ok) {
+            const float w0 = u0 - f0, w1 = u1 - f1, w2 = u2 - f2;
+            const float* q = occ + ((a0 + 1) * P + (a1 + 1)) * P + (a2 + 1);
+            const float c00 = fmaf(w2, q[1] - q[0], q[0]);
+            const float c01 = fmaf(w2, q[P + 1] - q[P], q[P]);
+            const float c10 = fmaf(w2, q[P * P + 1] - q[P * P], q[P * P]);
+            const float c11 = fmaf(w2, q[P * P + P + 1] - q[P * P + P], q[P * P + P]);
+            const float c0 = fmaf(w1, c01 - c00, c00);
+            const float c1 = fmaf(w1, c11 - c10, c10);
+            v = fmaf(w0, c1 - c0, c0);
+        }
+        tr *= 1.f - v;
+        sum += v;
+    }
+    T = tr;
+    rho = sum / S;
+}
+
 __device__ __forceinline__ float sample_near(const CondDev& c, const float* occ, float qx, float qy,
                                              float qz) {
     const int R = c.R;
@@ -92,23 +147,38 @@ __device__ __forceinline__ float sample_near(const CondDev& c, const float* occ,
     return occ[(ix * R + iy) * R + iz];
 }
 
-// Local features [v_hat, d, T, rho] (conditioning.cpp:377-396).
+// Local features [v_hat, d, T, rho] (conditioning.cpp:377-396).  PADDED:
+// occ is the (R+2)^3 zero-bordered copy (trilinear fast path); otherwise the
+// plain R^3 grid.
+template <bool PADDED = false>
 __device__ __forceinline__ void local_features(const CondDev& c, const float* occ, float px,
                                                float py, float pz, float rx, float ry, float rz,
                                                float* in) {
     const float dx = rx - px, dy = ry - py, dz = rz - pz;
     const float d = sqrtf(dx * dx + dy * dy + dz * dz);
-    in[0] = dx / d;
-    in[1] = dy / d;
-    in[2] = dz / d;
+    const float inv = 1.f / d;
+    in[0] = dx * inv;
+    in[1] = dy * inv;
+    in[2] = dz * inv;
     in[3] = d;
     float T = 1.f, rho = 0.f;
-    if (c.probe) {
+    if (PADDED && c.probe && !c.nearest) {
+        probe_padded(c, occ, px, py, pz, dx, dy, dz, T, rho);
+    } else if (c.probe) {
         float sum = 0.f;
         for (int s = 0; s < c.S; ++s) {
             const float t = c.S == 1 ? 0.5f : 0.05f + 0.9f * static_cast<float>(s) / (c.S - 1);
             const float qx = px + dx * t, qy = py + dy * t, qz = pz + dz * t;
-            const float v = c.nearest ? sample_near(c, occ, qx, qy, qz) : sample_tri(c, occ, qx, qy, qz);
+            float v;
+            if (PADDED) {  // nearest lookup on the padded grid
+                const int ix = static_cast<int>(floorf((qx - c.lo[0]) / c.cell[0]));
+                const int iy = static_cast<int>(floorf((qy - c.lo[1]) / c.cell[1]));
+                const int iz = static_cast<int>(floorf((qz - c.lo[2]) / c.cell[2]));
+                const bool in_ = ix >= 0 && iy >= 0 && iz >= 0 && ix < c.R && iy < c.R && iz < c.R;
+                v = in_ ? occ[padded_index(c.R, ix, iy, iz)] : 0.f;
+            } else {
+                v = c.nearest ? sample_near(c, occ, qx, qy, qz) : sample_tri(c, occ, qx, qy, qz);
+            }
             T *= 1.f - v;
             sum += v;
         }

@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(512, 1)
         }
         for (int i = threadIdx.x; i < 4 * C * H; i += blockDim.x) s_w3[i] = p[c.o_lw3 + i];
         for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) s_b3[i] = p[c.o_lb3 + i];
-        for (int i = threadIdx.x; i < R3; i += blockDim.x) s_occ[i] = c.occ[i];
+        if (R3) load_padded_occ(c, s_occ);
     }
     __syncthreads();
     const LocalSmem w{s_occ, s_w1, s_b1, s_w2, s_b2, s_w3, s_b3};
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(512, 1)
         float y[YM];
         if (c.use_local) {
             float in[6];
-            local_features(c, s_occ, pk.x, pk.y, pk.z, rxx, rxy, rxz, in);
+            local_features<true>(c, s_occ, pk.x, pk.y, pk.z, rxx, rxy, rxz, in);
             local_mlp<HT, CT>(c, w, in, y);
         } else {
 #pragma unroll
@@ -192,7 +192,7 @@ __global__ void k_cond_materialize(CondDev c, int K, const float4* __restrict__ 
         }
         for (int i = threadIdx.x; i < 4 * C * H; i += blockDim.x) s_w3[i] = p[c.o_lw3 + i];
         for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) s_b3[i] = p[c.o_lb3 + i];
-        for (int i = threadIdx.x; i < R3; i += blockDim.x) s_occ[i] = c.occ[i];
+        if (R3) load_padded_occ(c, s_occ);
     }
     __syncthreads();
     const LocalSmem w{s_occ, s_w1, s_b1, s_w2, s_b2, s_w3, s_b3};
@@ -204,7 +204,7 @@ __global__ void k_cond_materialize(CondDev c, int K, const float4* __restrict__ 
     if (c.use_local) {
         const float4 pk = pos32[k];
         float in[6];
-        local_features(c, s_occ, pk.x, pk.y, pk.z, static_cast<float>(rx[3 * j]),
+        local_features<true>(c, s_occ, pk.x, pk.y, pk.z, static_cast<float>(rx[3 * j]),
                        static_cast<float>(rx[3 * j + 1]), static_cast<float>(rx[3 * j + 2]), in);
         local_mlp<0, 0>(c, w, in, y);
         if (local_in && j == 0)
@@ -290,7 +290,7 @@ __global__ void k_check_coincide(int K, const double* __restrict__ pos, const do
 
 size_t local_smem_bytes(const CondDev& d, bool with_occ) {
     const size_t f = static_cast<size_t>(d.H) * d.H + d.H * 6 + 2 * d.H + 4 * d.C * d.H +
-                     ((4 * d.C + 3) & ~3) + (with_occ ? static_cast<size_t>(d.R) * d.R * d.R : 0);
+                     ((4 * d.C + 3) & ~3) + (with_occ ? static_cast<size_t>(d.R + 2) * (d.R + 2) * (d.R + 2) : 0);
     return f * sizeof(float);
 }
 

@@ -77,8 +77,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         *reinterpret_cast<uint16_t*>(w2hi + canon_off(n, k)) = static_cast<uint16_t>(ph & 0xFFFFu);
         *reinterpret_cast<uint16_t*>(w2lo + canon_off(n, k)) = static_cast<uint16_t>(pl & 0xFFFFu);
     }
-    const int R3 = c.probe ? c.R * c.R * c.R : 0;
-    for (int i = tid; i < R3; i += kThreads) s_occ[i] = c.occ[i];
+    if (c.probe) load_padded_occ(c, s_occ);
     if (warp == 0) {
         tc::tmem_alloc(&tbase_s, 512);
         tc::tmem_relinquish();
@@ -118,7 +117,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float in[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         if (active) {
             const float4 pk = pos32[k];
-            local_features(c, s_occ, pk.x, pk.y, pk.z, static_cast<float>(rx[3 * j]),
+            local_features<true>(c, s_occ, pk.x, pk.y, pk.z, static_cast<float>(rx[3 * j]),
                            static_cast<float>(rx[3 * j + 1]), static_cast<float>(rx[3 * j + 2]), in);
         }
         // ---- layer 1 (FFMA, constant-bank weights) -> bf16 hi/lo -> TMEM (A operand)
@@ -267,7 +266,7 @@ __global__ void __launch_bounds__(128) k_tc_selftest(float* __restrict__ err) {
 }  // namespace
 
 bool cond_tc_eligible(const rxgs_cond_s* c) {
-    return c && c->use_local() && c->hidden == kH && c->C == 1 && c->R * c->R * c->R <= 40960;
+    return c && c->use_local() && c->hidden == kH && c->C == 1 && (c->R + 2) * (c->R + 2) * (c->R + 2) <= 48000;
 }
 
 cudaError_t launch_cond_signal_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
@@ -284,7 +283,8 @@ cudaError_t launch_cond_signal_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc,
     }
     for (int i = 0; i < 4 * kH; ++i) w.w3[i] = static_cast<float>(p[cs.o_lw3 + i]);
     for (int i = 0; i < 4; ++i) w.b3[i] = static_cast<float>(p[cs.o_lb3 + i]);
-    const size_t smem = 2 * kW2Bytes + (d.probe ? static_cast<size_t>(d.R) * d.R * d.R * sizeof(float) : 0);
+    const size_t P = static_cast<size_t>(d.R) + 2;
+    const size_t smem = 2 * kW2Bytes + (d.probe ? P * P * P * sizeof(float) : 0);
     cudaError_t e = cudaFuncSetAttribute(k_cond_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 148;
