@@ -70,8 +70,9 @@ int64_t rxgs_ctx_launch_count(rxgs_ctx ctx);
  * C == 1, else FP32 SIMT), 1 = force the FP32 SIMT kernel (A/B checks). */
 int rxgs_ctx_set_cond_kernel(rxgs_ctx ctx, int which);
 /* Diagnostic: a 128x64x64 bf16 tcgen05 GEMM with A in TMEM and with A in
- * shared memory, max |error| vs FP32 FMA of the same values. */
-int rxgs_selftest_tcgen05(rxgs_ctx ctx, double* err_tmem_a, double* err_smem_a);
+ * shared memory, max |error| vs FP32 FMA of the same values; err[4] =
+ * {smooth: A-in-TMEM, A-in-smem; small integers (exact): TMEM, smem}. */
+int rxgs_selftest_tcgen05(rxgs_ctx ctx, double* err);
 
 /* ------------------------------------------------------------ synthetic inputs
  * DESIGN.md section 5 (bit-identical to oracle/ and to the reference-side

@@ -70,7 +70,7 @@ _SIG = {
     "rxgs_ctx_reset_stats": (C.c_int, [_vp]),
     "rxgs_ctx_launch_count": (_i64, [_vp]),
     "rxgs_ctx_set_cond_kernel": (C.c_int, [_vp, C.c_int]),
-    "rxgs_selftest_tcgen05": (C.c_int, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "rxgs_selftest_tcgen05": (C.c_int, [_vp, _vp]),
     "rxgs_synth_scene": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint64, _vp, _vp, _vp, _vp, _vp]),
     "rxgs_synth_points": (C.c_int, [C.c_int, C.c_uint64, C.c_char_p, _vp, _vp, C.c_double, _vp]),
     "rxgs_synth_cond": (_i64, [_vp, C.c_int, C.c_int, _vp, _vp, C.c_uint64, C.c_int, _vp]),
@@ -223,9 +223,9 @@ class Context:
         _check(_lib.rxgs_ctx_set_cond_kernel(self.h, {"auto": 0, "simt": 1}[which]))
 
     def selftest_tcgen05(self):
-        a, b = C.c_double(), C.c_double()
-        _check(_lib.rxgs_selftest_tcgen05(self.h, C.byref(a), C.byref(b)))
-        return a.value, b.value
+        e = np.zeros(4)
+        _check(_lib.rxgs_selftest_tcgen05(self.h, e.ctypes.data))
+        return tuple(float(x) for x in e)
 
     # ---------------------------------------------------------- objects
     def scene(self, sc, modality="spectrum"):

@@ -335,17 +335,16 @@ int rxgs_ctx_set_cond_kernel(rxgs_ctx ctx, int which) {
     return RXGS_OK;
 }
 
-int rxgs_selftest_tcgen05(rxgs_ctx ctx, double* err_tmem_a, double* err_smem_a) {
+int rxgs_selftest_tcgen05(rxgs_ctx ctx, double* err) {
     if (!ctx) return fail(RXGS_ERR_INVALID, "null context");
     RX_TRY(set_device(ctx));
     RXGS_CUDA(ctx->err_flag.ensure(16));
-    RXGS_CUDA(cudaMemsetAsync(ctx->err_flag.p, 0, 8, ctx->stream));
+    RXGS_CUDA(cudaMemsetAsync(ctx->err_flag.p, 0, 16, ctx->stream));
     RXGS_CUDA(launch_tc_selftest(ctx->err_flag.as<float>(), ctx->stream));
-    float e[2] = {0.f, 0.f};
-    RXGS_CUDA(cudaMemcpyAsync(e, ctx->err_flag.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    float e[4] = {0.f, 0.f, 0.f, 0.f};
+    RXGS_CUDA(cudaMemcpyAsync(e, ctx->err_flag.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
     RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (err_tmem_a) *err_tmem_a = e[0];
-    if (err_smem_a) *err_smem_a = e[1];
+    for (int i = 0; i < 4; ++i) err[i] = e[i];
     return RXGS_OK;
 }
 

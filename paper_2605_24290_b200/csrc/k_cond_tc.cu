@@ -186,14 +186,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ------------------------------------------------------------------ self test
 // 128x64x64 bf16 GEMM through both operand paths (A in TMEM and A in shared
 // memory) against FP32 FMA of the same bf16 values.
-__global__ void __launch_bounds__(128) k_tc_selftest(float* __restrict__ err) {
+__global__ void __launch_bounds__(128) k_tc_selftest(float* __restrict__ err, int mode) {
     __shared__ __align__(1024) uint8_t sB[kW2Bytes];
     __shared__ __align__(1024) uint8_t sA[128 * kH * 2];
     __shared__ uint64_t bar;
     __shared__ uint32_t tb;
     const int tid = threadIdx.x, warp = tid >> 5;
-    auto Aval = [](int m, int k) { return tc::bf16_round(sinf(0.37f * m + 0.11f * k)); };
-    auto Bval = [](int n, int k) { return tc::bf16_round(cosf(0.23f * n - 0.07f * k)); };
+    // mode 0: smooth values; mode 1: small integers (products and sums exact in FP32)
+    auto Aval = [mode](int m, int k) {
+        return mode ? static_cast<float>((m + 3 * k) % 5 - 2) : tc::bf16_round(sinf(0.37f * m + 0.11f * k));
+    };
+    auto Bval = [mode](int n, int k) {
+        return mode ? static_cast<float>((2 * n + k) % 7 - 3) : tc::bf16_round(cosf(0.23f * n - 0.07f * k));
+    };
     for (int i = tid; i < kH * kH; i += 128) {
         const int n = i / kH, k = i % kH;
         *reinterpret_cast<uint16_t*>(sB + canon_off(n, k)) =
@@ -301,7 +306,8 @@ cudaError_t launch_cond_signal_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc,
 }
 
 cudaError_t launch_tc_selftest(float* d_err, cudaStream_t s) {
-    k_tc_selftest<<<1, 128, 0, s>>>(d_err);
+    k_tc_selftest<<<1, 128, 0, s>>>(d_err, 0);
+    k_tc_selftest<<<1, 128, 0, s>>>(d_err + 2, 1);
     return cudaGetLastError();
 }
 

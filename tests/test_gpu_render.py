@@ -203,8 +203,9 @@ def test_predict_api(ctx, capi, orc):
 
 def test_tcgen05_selftest(ctx):
     """128x64x64 bf16 GEMM with A in TMEM and in smem vs FP32 FMA of the same values."""
-    e_tmem, e_smem = ctx.selftest_tcgen05()
-    assert e_tmem < 1e-3 and e_smem < 1e-3, (e_tmem, e_smem)
+    e = ctx.selftest_tcgen05()
+    assert e[2] == 0.0 and e[3] == 0.0, e  # exact data: layouts and descriptors
+    assert e[0] < 1e-2 and e[1] < 1e-2, e  # smooth data: tensor-core accumulation
 
 
 def test_tcgen05_kernel_matches_simt_and_oracle(ctx, capi, orc):
