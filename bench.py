@@ -193,8 +193,9 @@ def run_b200(args):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    for _ in range(args.warmup):
-        step_device()
+    last = None
+    for _ in range(args.warmup):  # same pattern as the timed loop (fills the state pool)
+        last = step_device()
     barrier()
 
     # ---------------- device-resident timed region

@@ -256,7 +256,11 @@ __global__ void __launch_bounds__(128) k_tc_selftest(float* __restrict__ err, in
         for (int q = 0; q < 16; ++q) {
             const int n = c0 + q;
             float ref = 0.f;
-            for (int k = 0; k < kH; ++k) ref = fmaf(Aval(tid, k), Bval(n, k), ref);
+            for (int k = 0; k < kH; ++k) {  // from the stored bf16 operands
+                const float a = __uint_as_float(static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(sA + canon_off(tid, k))) << 16);
+                const float b = __uint_as_float(static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(sB + canon_off(n, k))) << 16);
+                ref = fmaf(a, b, ref);
+            }
             e_ts = fmaxf(e_ts, fabsf(__uint_as_float(r[q]) - ref));
             e_ss = fmaxf(e_ss, fabsf(__uint_as_float(r2[q]) - ref));
         }
