@@ -1,0 +1,397 @@
+// include/rxgs_b200.hpp -- header-only C++ shim: the reference's C++ API for
+// the render path (rxgs::raster / rxgs::cond / rxgs::train, same struct
+// fields, same exception types and messages) implemented on top of the
+// C-ABI in rxgs_b200.h, i.e. on the B200 kernels.
+//
+// Reference headers replaced (paths under /root/reference/proj/include/rxgs):
+//   scene.hpp:19-48        GaussianScene
+//   sphraster.hpp:15-133   SphericalGrid, ProjectedGaussian, TxState,
+//                          build_tx_state, bin_and_sort, RenderedField,
+//                          render_field (x2), Measurement, aggregate_modality
+//   conditioning.hpp:13-123 MlpLayer, Mlp, OccupancyGrid, ConditioningConfig,
+//                          ConditioningState, build_occupancy,
+//                          condition_forward, condition_batch
+//   trainer.hpp:42-50      Model, predict
+// Usage: include this header instead of the reference headers and link
+// librxgs_b200.so.  Define RXGS_B200_AS_RXGS to expose everything as
+// namespace rxgs (source-compatible with reference callers).
+#pragma once
+
+#include <array>
+#include <complex>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rxgs_b200.h"
+
+namespace rxgs_b200 {
+namespace api {
+
+using cplx = std::complex<double>;
+inline constexpr double kPi = 3.14159265358979323846;
+inline constexpr double kTwoPi = 2.0 * kPi;
+
+struct Vec3 {
+    double x = 0.0, y = 0.0, z = 0.0;
+};
+
+enum class Modality { Rssi, Csi, Spectrum };  // channelsim.hpp:79
+
+namespace detail {
+inline void check(int rc) {
+    if (rc == RXGS_OK) return;
+    const std::string msg = rxgs_last_error();
+    if (rc == RXGS_ERR_INVALID) throw std::invalid_argument(msg);
+    throw std::runtime_error(msg);
+}
+struct Ctx {
+    rxgs_ctx h = nullptr;
+    Ctx() { check(rxgs_ctx_create(0, &h)); }
+    ~Ctx() { rxgs_ctx_destroy(h); }
+};
+inline rxgs_ctx ctx() {
+    thread_local Ctx c;
+    return c.h;
+}
+struct SceneHandle {
+    rxgs_scene h = nullptr;
+    ~SceneHandle() { rxgs_scene_destroy(h); }
+};
+struct TxHandle {
+    rxgs_txstate h = nullptr;
+    std::shared_ptr<SceneHandle> scene;
+    ~TxHandle() { rxgs_tx_state_destroy(h); }
+};
+}  // namespace detail
+
+inline int component_count(int l_max) { return (l_max + 1) * (l_max + 1); }
+
+// GaussianScene (scene.hpp:19-48)
+struct GaussianScene {
+    int l_max = 0;
+    int channels = 1;
+    Modality modality = Modality::Rssi;
+    std::vector<double> positions, log_scales, quaternions, tau_logits, fle_coeffs;
+    int count() const { return static_cast<int>(tau_logits.size()); }
+    int n_components() const { return component_count(l_max); }
+    std::size_t coeff_stride() const { return static_cast<std::size_t>(n_components()) * channels * 2; }
+    Vec3 position(int k) const { return {positions[3 * k], positions[3 * k + 1], positions[3 * k + 2]}; }
+};
+
+namespace detail {
+inline std::shared_ptr<SceneHandle> upload(const GaussianScene& s) {
+    auto h = std::make_shared<SceneHandle>();
+    check(rxgs_scene_create(ctx(), s.count(), s.l_max, s.channels, static_cast<int>(s.modality),
+                            s.positions.data(), s.log_scales.data(), s.quaternions.data(),
+                            s.tau_logits.data(), s.fle_coeffs.data(), &h->h));
+    return h;
+}
+}  // namespace detail
+
+namespace raster {
+
+inline constexpr double kWeightClamp = 0.999;
+inline constexpr double kEarlyExitT = 1e-4;
+
+struct SphericalGrid {  // sphraster.hpp:15-32
+    int n_theta = 1, n_phi = 1, tile_size = 8;
+    double radius = 1.0, theta_min = 0.0, theta_max = kPi;
+    double dtheta() const { return (theta_max - theta_min) / n_theta; }
+    double dphi() const { return kTwoPi / n_phi; }
+    double theta_at(int i) const { return theta_min + (i + 0.5) * dtheta(); }
+    double phi_at(int j) const { return (j + 0.5) * dphi(); }
+    int tiles_theta() const { return (n_theta + tile_size - 1) / tile_size; }
+    int tiles_phi() const { return (n_phi + tile_size - 1) / tile_size; }
+    std::size_t cells() const { return static_cast<std::size_t>(n_theta) * n_phi; }
+    rxgs_grid c() const { return {n_theta, n_phi, tile_size, 0, radius, theta_min, theta_max}; }
+};
+
+struct Mat2 {
+    double a = 0.0, b = 0.0, c = 0.0, d = 0.0;
+};
+
+struct ProjectedGaussian {  // sphraster.hpp:34-44
+    bool culled = true;
+    double theta = 0.0, phi = 0.0, depth = 0.0;
+    Mat2 angular_cov, angular_prec;
+    double weight_scale = 0.0;
+    int t0 = 0, t1 = -1, p0 = 0, p1 = -1;
+};
+
+struct TxState {  // sphraster.hpp:52-61 (materialised from the device)
+    SphericalGrid grid;
+    int k = 0, l_max = 0;
+    std::vector<ProjectedGaussian> proj;
+    std::vector<std::vector<int>> tile_lists;
+    std::vector<cplx> basis;
+    std::shared_ptr<detail::TxHandle> device;  // B200 state (lists, blend weights)
+};
+
+inline TxState build_tx_state(const GaussianScene& scene, const Vec3& tx, const SphericalGrid& grid) {
+    auto th = std::make_shared<detail::TxHandle>();
+    th->scene = detail::upload(scene);
+    const double t[3] = {tx.x, tx.y, tx.z};
+    const rxgs_grid g = grid.c();
+    detail::check(rxgs_tx_state_build(detail::ctx(), th->scene->h, t, &g, &th->h));
+    TxState st;
+    st.grid = grid;
+    st.k = scene.count();
+    st.l_max = scene.l_max;
+    st.device = th;
+    const int K = st.k, L = scene.n_components();
+    const int64_t E = rxgs_tx_state_entries(th->h);
+    std::vector<int32_t> culled(K), spans(4 * static_cast<std::size_t>(K)), idx(E > 0 ? E : 1);
+    std::vector<double> geom(12 * static_cast<std::size_t>(K)), basis(2 * static_cast<std::size_t>(K) * L);
+    std::vector<int64_t> offs(static_cast<std::size_t>(grid.tiles_theta()) * grid.tiles_phi() + 1);
+    detail::check(rxgs_tx_state_get(th->h, culled.data(), geom.data(), spans.data(), basis.data(), offs.data(),
+                                    idx.data()));
+    st.proj.resize(K);
+    for (int k = 0; k < K; ++k) {
+        ProjectedGaussian& p = st.proj[k];
+        const double* g12 = geom.data() + 12 * static_cast<std::size_t>(k);
+        p.culled = culled[k] != 0;
+        p.theta = g12[0]; p.phi = g12[1]; p.depth = g12[2];
+        p.angular_cov = {g12[3], g12[4], g12[5], g12[6]};
+        p.angular_prec = {g12[7], g12[8], g12[9], g12[10]};
+        p.weight_scale = g12[11];
+        p.t0 = spans[4 * k]; p.t1 = spans[4 * k + 1]; p.p0 = spans[4 * k + 2]; p.p1 = spans[4 * k + 3];
+    }
+    st.basis.resize(static_cast<std::size_t>(K) * L);
+    for (std::size_t i = 0; i < st.basis.size(); ++i) st.basis[i] = {basis[2 * i], basis[2 * i + 1]};
+    st.tile_lists.resize(offs.size() - 1);
+    for (std::size_t t = 0; t + 1 < offs.size(); ++t)
+        st.tile_lists[t].assign(idx.begin() + offs[t], idx.begin() + offs[t + 1]);
+    return st;
+}
+
+inline std::vector<std::vector<int>> bin_and_sort(const std::vector<ProjectedGaussian>& projected,
+                                                  const SphericalGrid& grid) {
+    const int K = static_cast<int>(projected.size());
+    std::vector<int32_t> culled(K), spans(4 * static_cast<std::size_t>(K));
+    std::vector<double> depth(K);
+    for (int k = 0; k < K; ++k) {
+        const auto& p = projected[k];
+        culled[k] = p.culled ? 1 : 0;
+        depth[k] = p.depth;
+        spans[4 * k] = p.t0; spans[4 * k + 1] = p.t1; spans[4 * k + 2] = p.p0; spans[4 * k + 3] = p.p1;
+    }
+    const rxgs_grid g = grid.c();
+    std::vector<int64_t> offs(static_cast<std::size_t>(grid.tiles_theta()) * grid.tiles_phi() + 1);
+    int64_t n = 0;
+    detail::check(rxgs_bin_and_sort(detail::ctx(), K, culled.data(), depth.data(), spans.data(), &g, offs.data(),
+                                    nullptr, 0, &n));
+    std::vector<int32_t> idx(n > 0 ? n : 1);
+    detail::check(rxgs_bin_and_sort(detail::ctx(), K, culled.data(), depth.data(), spans.data(), &g, offs.data(),
+                                    idx.data(), n, &n));
+    std::vector<std::vector<int>> lists(offs.size() - 1);
+    for (std::size_t t = 0; t + 1 < offs.size(); ++t) lists[t].assign(idx.begin() + offs[t], idx.begin() + offs[t + 1]);
+    return lists;
+}
+
+struct RenderedField {  // sphraster.hpp:75-86
+    int n_rx = 0, channels = 1, h = 0, w = 0;
+    std::vector<double> values;
+    std::vector<double> transmittance;
+    std::size_t plane() const { return static_cast<std::size_t>(h) * w; }
+    double value(int j, int c, int reim, std::size_t cell) const {
+        return values[((static_cast<std::size_t>(j) * channels + c) * 2 + reim) * plane() + cell];
+    }
+};
+
+inline RenderedField render_field(const TxState& st, const GaussianScene& scene, const std::vector<double>& coeffs,
+                                  int n_rx, int /*threads*/ = 1) {
+    if (n_rx < 1) throw std::invalid_argument("render_field: n_rx must be >= 1");
+    if (coeffs.size() != static_cast<std::size_t>(n_rx) * scene.count() * scene.coeff_stride())
+        throw std::invalid_argument("render_field: coefficient tensor has wrong size");
+    RenderedField f;
+    f.n_rx = n_rx;
+    f.channels = scene.channels;
+    f.h = st.grid.n_theta;
+    f.w = st.grid.n_phi;
+    f.values.assign(static_cast<std::size_t>(n_rx) * f.channels * 2 * f.plane(), 0.0);
+    f.transmittance.assign(static_cast<std::size_t>(n_rx) * f.plane(), 1.0);
+    detail::check(rxgs_render_field(detail::ctx(), st.device->h, st.device->scene->h,
+                                    coeffs.empty() ? nullptr : coeffs.data(), n_rx, f.values.data(),
+                                    f.transmittance.data()));
+    return f;
+}
+
+inline RenderedField render_field(const GaussianScene& scene, const Vec3& tx, const SphericalGrid& grid,
+                                  const std::vector<double>& coeffs, int n_rx, int threads = 1) {
+    return render_field(build_tx_state(scene, tx, grid), scene, coeffs, n_rx, threads);
+}
+
+struct Measurement {  // sphraster.hpp:100-105
+    Modality modality = Modality::Rssi;
+    double scalar = 0.0;
+    std::vector<cplx> csi;
+    std::vector<double> image;
+};
+
+inline std::vector<Measurement> aggregate_modality(const RenderedField& field, Modality modality,
+                                                   const SphericalGrid& grid) {
+    const rxgs_grid g = grid.c();
+    const int m = static_cast<int>(modality);
+    const std::size_t n = m == 0 ? field.n_rx
+                                 : (m == 1 ? static_cast<std::size_t>(field.n_rx) * field.channels * 2
+                                           : static_cast<std::size_t>(field.n_rx) * field.plane());
+    std::vector<double> out(n > 0 ? n : 1);
+    detail::check(rxgs_aggregate_modality(detail::ctx(), &g, m, field.n_rx, field.channels, field.values.data(),
+                                          out.data()));
+    std::vector<Measurement> ms(field.n_rx);
+    for (int j = 0; j < field.n_rx; ++j) {
+        Measurement& r = ms[j];
+        r.modality = modality;
+        if (m == 0) {
+            r.scalar = out[j];
+        } else if (m == 1) {
+            for (int c = 0; c < field.channels; ++c)
+                r.csi.push_back({out[(static_cast<std::size_t>(j) * field.channels + c) * 2],
+                                 out[(static_cast<std::size_t>(j) * field.channels + c) * 2 + 1]});
+        } else {
+            r.image.assign(out.begin() + static_cast<std::ptrdiff_t>(j * field.plane()),
+                           out.begin() + static_cast<std::ptrdiff_t>((j + 1) * field.plane()));
+        }
+    }
+    return ms;
+}
+
+}  // namespace raster
+
+namespace cond {
+
+struct MlpLayer {  // conditioning.hpp:13-19
+    int in = 0, out = 0;
+    std::vector<double> w, b;
+};
+struct Mlp {
+    MlpLayer l1, l2, l3;
+};
+struct Aabb {
+    Vec3 lo, hi;
+};
+struct OccupancyGrid {  // conditioning.hpp:29-37
+    int resolution = 0;
+    Aabb bounds;
+    std::vector<double> densities;
+    bool empty() const { return densities.empty(); }
+};
+enum class ConditioningMode { Full, GlobalOnly, LocalOnly, AdditiveOnly, NoOcclusion };
+struct ConditioningConfig {  // conditioning.hpp:58-66
+    int fourier_bands = 6, hidden = 64, embed_dim = 16, probe_samples = 16, occupancy_resolution = 32;
+    bool nearest_lookup = false;
+    ConditioningMode mode = ConditioningMode::Full;
+};
+struct ConditioningState {  // conditioning.hpp:72-92
+    ConditioningConfig config;
+    int l_max = 0, channels = 1;
+    std::vector<double> fourier_freqs;
+    Mlp global_mlp;
+    std::vector<double> component_embed;
+    Mlp local_mlp;
+    OccupancyGrid occupancy;
+    mutable std::int64_t global_calls = 0;
+    mutable std::int64_t local_calls = 0;
+};
+
+namespace detail_c {
+struct CondHandle {
+    rxgs_cond h = nullptr;
+    ~CondHandle() { rxgs_cond_destroy(h); }
+};
+inline std::unique_ptr<CondHandle> upload(const ConditioningState& s) {
+    const ConditioningConfig& c = s.config;
+    const int32_t cfg[9] = {c.fourier_bands, c.hidden, c.embed_dim, c.probe_samples,
+                            s.occupancy.empty() ? c.occupancy_resolution : s.occupancy.resolution,
+                            c.nearest_lookup ? 1 : 0, static_cast<int32_t>(c.mode), s.l_max, s.channels};
+    std::vector<double> p;
+    auto put = [&p](const std::vector<double>& v) { p.insert(p.end(), v.begin(), v.end()); };
+    put(s.fourier_freqs);
+    for (const MlpLayer* l : {&s.global_mlp.l1, &s.global_mlp.l2, &s.global_mlp.l3}) {
+        put(l->w);
+        put(l->b);
+    }
+    put(s.component_embed);
+    for (const MlpLayer* l : {&s.local_mlp.l1, &s.local_mlp.l2, &s.local_mlp.l3}) {
+        put(l->w);
+        put(l->b);
+    }
+    auto h = std::make_unique<CondHandle>();
+    const double lo[3] = {s.occupancy.bounds.lo.x, s.occupancy.bounds.lo.y, s.occupancy.bounds.lo.z};
+    const double hi[3] = {s.occupancy.bounds.hi.x, s.occupancy.bounds.hi.y, s.occupancy.bounds.hi.z};
+    api::detail::check(rxgs_cond_create(api::detail::ctx(), cfg, p.data(),
+                                        s.occupancy.empty() ? nullptr : s.occupancy.densities.data(), lo, hi, &h->h));
+    return h;
+}
+}  // namespace detail_c
+
+inline OccupancyGrid build_occupancy(const GaussianScene& scene, int resolution, const Aabb& bounds) {
+    auto sh = api::detail::upload(scene);
+    OccupancyGrid g;
+    g.resolution = resolution;
+    g.bounds = bounds;
+    const double lo[3] = {bounds.lo.x, bounds.lo.y, bounds.lo.z};
+    const double hi[3] = {bounds.hi.x, bounds.hi.y, bounds.hi.z};
+    g.densities.resize(resolution > 0 ? static_cast<std::size_t>(resolution) * resolution * resolution : 0);
+    api::detail::check(rxgs_build_occupancy(api::detail::ctx(), sh->h, resolution, lo, hi,
+                                            g.densities.empty() ? nullptr : g.densities.data(), nullptr));
+    return g;
+}
+
+inline std::vector<double> condition_batch(const ConditioningState& state, const std::vector<double>& base,
+                                           const GaussianScene& scene, const std::vector<Vec3>& rx_list) {
+    if (base.size() != static_cast<std::size_t>(scene.count()) * scene.coeff_stride())
+        throw std::invalid_argument("condition_forward: base coefficient size mismatch");
+    GaussianScene s2 = scene;
+    s2.fle_coeffs = base;
+    auto sh = api::detail::upload(s2);
+    auto ch = detail_c::upload(state);
+    std::vector<double> rx;
+    for (const Vec3& r : rx_list) rx.insert(rx.end(), {r.x, r.y, r.z});
+    std::vector<double> out(base.size() * rx_list.size());
+    if (!rx_list.empty())
+        api::detail::check(rxgs_condition_batch(api::detail::ctx(), ch->h, sh->h, rx.data(),
+                                                static_cast<int>(rx_list.size()), out.data()));
+    if (state.config.mode != ConditioningMode::LocalOnly)
+        state.global_calls += static_cast<std::int64_t>(rx_list.size()) * scene.n_components();
+    if (state.config.mode != ConditioningMode::GlobalOnly)
+        state.local_calls += static_cast<std::int64_t>(rx_list.size()) * scene.count();
+    return out;
+}
+
+inline std::vector<double> condition_forward(const ConditioningState& state, const std::vector<double>& base,
+                                             const GaussianScene& scene, const Vec3& rx) {
+    return condition_batch(state, base, scene, {rx});
+}
+
+}  // namespace cond
+
+namespace train {
+
+struct Model {  // trainer.hpp:42-47
+    GaussianScene scene;
+    raster::SphericalGrid grid;
+    bool has_conditioning = false;
+    cond::ConditioningState conditioning;
+};
+
+// trainer.cpp:147-154
+inline raster::Measurement predict(const Model& model, const Vec3& tx, const Vec3& rx, int threads = 1) {
+    const std::vector<double> coeffs =
+        model.has_conditioning ? cond::condition_forward(model.conditioning, model.scene.fle_coeffs, model.scene, rx)
+                               : model.scene.fle_coeffs;
+    const auto field = raster::render_field(model.scene, tx, model.grid, coeffs, 1, threads);
+    return raster::aggregate_modality(field, model.scene.modality, model.grid)[0];
+}
+
+}  // namespace train
+
+}  // namespace api
+}  // namespace rxgs_b200
+
+#ifdef RXGS_B200_AS_RXGS
+namespace rxgs = rxgs_b200::api;
+#endif

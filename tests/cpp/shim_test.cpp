@@ -1,0 +1,163 @@
+// Reference-style tests written against the reference's C++ API, compiled
+// against include/rxgs_b200.hpp (RXGS_B200_AS_RXGS) and run on the B200.
+// Cases restate test_sphraster.cpp / test_conditioning.cpp known answers.
+#define RXGS_B200_AS_RXGS
+#include "rxgs_b200.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <random>
+
+using namespace rxgs;
+using namespace rxgs::raster;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(x)                                                            \
+    do {                                                                    \
+        ++g_checks;                                                         \
+        if (!(x)) {                                                         \
+            ++g_fail;                                                       \
+            std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #x);        \
+        }                                                                   \
+    } while (0)
+
+static double rel_err(double a, double b) {
+    return std::abs(a - b) / std::max({1.0, std::abs(a), std::abs(b)});
+}
+
+static GaussianScene random_scene(unsigned seed, int k, int l_max, int channels) {
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> u(0.0, 1.0);
+    std::normal_distribution<double> nrm(0.0, 1.0);
+    GaussianScene s;
+    s.l_max = l_max;
+    s.channels = channels;
+    for (int i = 0; i < k; ++i) {
+        double x = 1.0 + 3.0 * u(rng);
+        if (u(rng) < 0.5) x = -x;
+        s.positions.insert(s.positions.end(), {x, -3.0 + 6.0 * u(rng), -2.0 + 4.0 * u(rng)});
+        for (int a = 0; a < 3; ++a) s.log_scales.push_back(-1.8 + 1.2 * u(rng));
+        double q[4], n = 0;
+        for (double& v : q) { v = nrm(rng); n += v * v; }
+        for (double v : q) s.quaternions.push_back(v / std::sqrt(n));
+        s.tau_logits.push_back(-2.0 + 3.0 * u(rng));
+    }
+    s.fle_coeffs.resize(static_cast<std::size_t>(k) * s.coeff_stride());
+    for (double& c : s.fle_coeffs) c = nrm(rng);
+    return s;
+}
+
+static SphericalGrid small_grid() {
+    SphericalGrid g;
+    g.n_theta = 6;
+    g.n_phi = 12;
+    g.tile_size = 4;
+    g.radius = 0.25;
+    return g;
+}
+
+int main() {
+    {  // projection: axis direction (test_sphraster.cpp:59-66) + culling (:88-94)
+        GaussianScene s;
+        s.positions = {1, 0, 0, 0.1, 0, 0};
+        s.log_scales = {std::log(0.1), std::log(0.1), std::log(0.1), 0, 0, 0};
+        s.quaternions = {1, 0, 0, 0, 1, 0, 0, 0};
+        s.tau_logits = {0, 0};
+        s.fle_coeffs = {0, 0, 0, 0};
+        const auto st = build_tx_state(s, {0, 0, 0}, small_grid());
+        CHECK(!st.proj[0].culled);
+        CHECK(rel_err(st.proj[0].theta, kPi / 2) < 1e-14);
+        CHECK(std::abs(st.proj[0].phi) < 1e-14);
+        CHECK(st.proj[1].culled);
+    }
+    {  // bin_and_sort: coverage, depth order, index tiebreak (test_sphraster.cpp:96-119)
+        std::vector<ProjectedGaussian> proj(3);
+        for (auto& p : proj) p.culled = false;
+        proj[0].depth = 2.0; proj[0].t0 = 0; proj[0].t1 = 1; proj[0].p0 = 0; proj[0].p1 = 2;
+        proj[1].depth = 1.0; proj[1].t0 = 0; proj[1].t1 = 0; proj[1].p0 = 1; proj[1].p1 = 1;
+        proj[2].depth = 2.0; proj[2].t0 = 0; proj[2].t1 = 0; proj[2].p0 = 1; proj[2].p1 = 1;
+        const auto lists = bin_and_sort(proj, small_grid());
+        CHECK(lists.size() == 6);
+        CHECK((lists[1] == std::vector<int>{1, 0, 2}));
+        std::vector<ProjectedGaussian> seam(1);
+        seam[0].culled = false; seam[0].depth = 1.0; seam[0].t0 = 0; seam[0].t1 = 0; seam[0].p0 = 2; seam[0].p1 = 3;
+        const auto l2 = bin_and_sort(seam, small_grid());
+        CHECK((l2[0] == std::vector<int>{0}) && l2[1].empty() && (l2[2] == std::vector<int>{0}));
+    }
+    {  // render: batched == sequential bitwise (test_sphraster.cpp:180-199)
+        const auto scene = random_scene(41, 6, 2, 2);
+        const int n_rx = 3;
+        std::vector<double> coeffs(n_rx * scene.count() * scene.coeff_stride());
+        std::mt19937_64 rng(42);
+        std::normal_distribution<double> nrm(0.0, 1.0);
+        for (double& c : coeffs) c = nrm(rng);
+        const auto batched = render_field(scene, {0, 0, 0}, small_grid(), coeffs, n_rx);
+        const std::size_t stride = scene.coeff_stride() * scene.count();
+        for (int j = 0; j < n_rx; ++j) {
+            const std::vector<double> slice(coeffs.begin() + j * stride, coeffs.begin() + (j + 1) * stride);
+            const auto single = render_field(scene, {0, 0, 0}, small_grid(), slice, 1);
+            const std::size_t per_rx = static_cast<std::size_t>(scene.channels) * 2 * batched.plane();
+            bool same = true;
+            for (std::size_t i = 0; i < per_rx; ++i) same &= batched.values[j * per_rx + i] == single.values[i];
+            CHECK(same);
+        }
+    }
+    {  // located non-finite error (test_sphraster.cpp:211-223)
+        const auto scene = random_scene(45, 3, 1, 1);
+        std::vector<double> coeffs(2 * scene.count() * scene.coeff_stride(), 0.5);
+        coeffs[scene.coeff_stride() * scene.count() + 5] = std::nan("");
+        bool threw = false;
+        try {
+            render_field(scene, {0, 0, 0}, small_grid(), coeffs, 2);
+        } catch (const std::invalid_argument& e) {
+            threw = std::string(e.what()).find("rx 1") != std::string::npos &&
+                    std::string(e.what()).find("gaussian 0") != std::string::npos;
+        }
+        CHECK(threw);
+    }
+    {  // empty scene (test_sphraster.cpp:170-178)
+        GaussianScene s;
+        s.l_max = 1;
+        const auto f = render_field(s, {0, 0, 0}, small_grid(), {}, 2);
+        bool ok = true;
+        for (double v : f.values) ok &= v == 0.0;
+        for (double t : f.transmittance) ok &= t == 1.0;
+        CHECK(ok);
+    }
+    {  // spectrum stabiliser (test_sphraster.cpp:289-303)
+        RenderedField f;
+        f.n_rx = 1; f.channels = 1; f.h = 1; f.w = 1;
+        f.values = {3.0, 4.0};
+        f.transmittance = {1.0};
+        SphericalGrid g;
+        const auto ms = aggregate_modality(f, Modality::Spectrum, g);
+        CHECK(rel_err(ms[0].image[0], std::sqrt(25.0 + 1e-8)) < 1e-15);
+    }
+    {  // conditioning: zero final layers = identity, bitwise (test_conditioning.cpp:157-169)
+        auto scene = random_scene(101, 5, 1, 2);
+        cond::ConditioningState st;
+        st.config.fourier_bands = 2; st.config.hidden = 8; st.config.embed_dim = 3; st.config.probe_samples = 4;
+        st.l_max = 1; st.channels = 2;
+        st.fourier_freqs.assign(6, 1.0);
+        auto layer = [](int in, int out, double v) { cond::MlpLayer l; l.in = in; l.out = out; l.w.assign(in * out, v); l.b.assign(out, 0.1); return l; };
+        st.global_mlp = {layer(6 * 2 + 2 + 3, 8, 0.05), layer(8, 8, 0.05), layer(8, 8, 0.0)};
+        st.global_mlp.l3.b.assign(8, 0.0);
+        st.component_embed.assign(4 * 3, 0.01);
+        st.local_mlp = {layer(6, 8, 0.05), layer(8, 8, 0.05), layer(8, 8, 0.0)};
+        st.local_mlp.l3.b.assign(8, 0.0);
+        st.occupancy = cond::build_occupancy(scene, 8, {{-4, -4, -4}, {4, 4, 4}});
+        const auto out = cond::condition_forward(st, scene.fle_coeffs, scene, {0.3, 0.2, -1.0});
+        CHECK(out == scene.fle_coeffs);
+        CHECK(st.global_calls == 4 && st.local_calls == 5);
+        bool threw = false;
+        try {
+            cond::condition_forward(st, scene.fle_coeffs, scene, scene.position(1));
+        } catch (const std::invalid_argument& e) {
+            threw = std::string(e.what()).find("gaussian 1") != std::string::npos;
+        }
+        CHECK(threw);
+    }
+    std::printf("%d checks, %d failures\n", g_checks, g_fail);
+    return g_fail ? 1 : 0;
+}

@@ -227,3 +227,18 @@ def test_tcgen05_kernel_matches_simt_and_oracle(ctx, capi, orc):
     for j in (0, 33, 69):
         want = orc.predict(oscene, ocond, og, TX, rx[j], "spectrum").reshape(45, 90)
         assert rel_err(s_tc[j], want).max() < TOL
+
+
+def test_reference_api_shim_cpp(capi, tmp_path):
+    """include/rxgs_b200.hpp: reference-shaped C++ callers (tests/cpp/shim_test.cpp)
+    compile against the shim, link librxgs_b200.so and pass on the B200."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.dirname(capi.LIB_PATH)
+    exe = str(tmp_path / "shim_test")
+    subprocess.check_call(["g++", "-std=c++17", "-O1", "-I", os.path.join(root, "include"),
+                           os.path.join(root, "tests", "cpp", "shim_test.cpp"), "-L", libdir, "-lrxgs_b200",
+                           "-Wl,-rpath," + libdir, "-o", exe])
+    out = subprocess.run([exe], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
