@@ -118,6 +118,9 @@ int rxgs_tx_state_keys(rxgs_txstate st, uint64_t* keys);
  * mean walk per cell, mean tile-walk per cell (roofline inputs). */
 int rxgs_tx_state_stats(rxgs_txstate st, int64_t* visible, int64_t* entries, double* walk_per_cell,
                         double* tile_walk_per_cell);
+/* Gaussians reached by at least one cell's front-to-back walk (list position
+ * below the tile's longest walk): the rows the batched query conditions. */
+int rxgs_tx_state_needed(rxgs_txstate st, int64_t* needed);
 /* Per-cell final transmittance (cells f64); identical for every receiver. */
 int rxgs_tx_state_transmittance(rxgs_txstate st, double* out);
 

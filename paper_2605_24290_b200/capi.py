@@ -86,6 +86,7 @@ _SIG = {
     "rxgs_tx_state_stats": (C.c_int, [_vp, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(C.c_double),
                                       C.POINTER(C.c_double)]),
     "rxgs_tx_state_transmittance": (C.c_int, [_vp, _vp]),
+    "rxgs_tx_state_needed": (C.c_int, [_vp, C.POINTER(_i64)]),
     "rxgs_bin_and_sort": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, C.POINTER(Grid), _vp, _vp, _i64,
                                     C.POINTER(_i64)]),
     "rxgs_render_field": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int, _vp, _vp]),
@@ -358,7 +359,10 @@ class TxState:
     def stats(self):
         v, e, w, tw = _i64(), _i64(), C.c_double(), C.c_double()
         _check(_lib.rxgs_tx_state_stats(self.h, C.byref(v), C.byref(e), C.byref(w), C.byref(tw)))
-        return dict(visible=v.value, entries=e.value, walk_per_cell=w.value, tile_walk_per_cell=tw.value)
+        nd = _i64()
+        _check(_lib.rxgs_tx_state_needed(self.h, C.byref(nd)))
+        return dict(visible=v.value, entries=e.value, walk_per_cell=w.value, tile_walk_per_cell=tw.value,
+                    needed=nd.value)
 
     def transmittance(self):
         out = _out((self.grid.n_theta, self.grid.n_phi))

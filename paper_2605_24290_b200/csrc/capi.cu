@@ -243,7 +243,8 @@ int compute_signals(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, rxgs_txstate st, c
     ctx->launches += 1;
     timing_begin(ctx, "cond_signal", &ev);
     RXGS_CUDA(launch_cond_signal(c, *sc, *st, d_rx, n_rx, ctx->ag.as<float>(), d_sig, nullptr, s));
-    timing_end(ctx, "cond_signal", ev, static_cast<double>(st->visible) * n_rx);
+    timing_end(ctx, "cond_signal", ev,
+               static_cast<double>(st->needed_host >= 0 ? st->needed_host : st->visible) * n_rx);
     ctx->launches += 1;
     return RXGS_OK;
 }
@@ -500,6 +501,10 @@ int rxgs_tx_state_build(rxgs_ctx ctx, rxgs_scene sc, const double tx[3], const r
         if (e != cudaSuccess) return fail_st(cuda_fail(e, "walk"));
     }
     timing_end(ctx, "walk", ev, static_cast<double>(cells));
+    {
+        const int rc = compact_needed(ctx, *st, s);
+        if (rc) return fail_st(rc);
+    }
     ctx->launches += 1;
     *out = st;
     return RXGS_OK;
@@ -580,6 +585,16 @@ int rxgs_tx_state_stats(rxgs_txstate st, int64_t* visible, int64_t* entries, dou
     if (tile_walk_per_cell) *tile_walk_per_cell = cells ? ts / cells : 0.0;
     return RXGS_OK;
     API_END
+}
+
+int rxgs_tx_state_needed(rxgs_txstate st, int64_t* needed) {
+    if (!st || !needed) return fail(RXGS_ERR_INVALID, "null argument");
+    RX_TRY(set_device(st->ctx));
+    int h = 0;
+    RXGS_CUDA(cudaMemcpyAsync(&h, st->needed_count.p, sizeof(int), cudaMemcpyDeviceToHost, st->ctx->stream));
+    RXGS_CUDA(cudaStreamSynchronize(st->ctx->stream));
+    *needed = h;
+    return RXGS_OK;
 }
 
 int rxgs_tx_state_transmittance(rxgs_txstate st, double* out) {

@@ -87,7 +87,7 @@ __global__ void k_cond_global(CondDev c, const double* __restrict__ rx, int n_rx
 // ------------------------------------------------------------------ fused hot kernel
 template <int HT, int CT>
 __global__ void __launch_bounds__(512, 1)
-    k_cond_signal(CondDev c, int n_vis, const int* __restrict__ vis, const float4* __restrict__ pos32,
+    k_cond_signal(CondDev c, const int* __restrict__ n_rows, const int* __restrict__ vis, const float4* __restrict__ pos32,
                   const double* __restrict__ rx, int n_rx, const float2* __restrict__ B,
                   const float2* __restrict__ GB, const float* __restrict__ ag,
                   float2* __restrict__ sig) {
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(512, 1)
     const int lane = threadIdx.x & 31;
     const int warps_per_block = blockDim.x >> 5;
     const int n_jc = (n_rx + 31) >> 5;
-    const long long items = static_cast<long long>(n_vis) * n_jc;
+    const long long items = static_cast<long long>(*n_rows) * n_jc;
     const long long stride = static_cast<long long>(gridDim.x) * warps_per_block;
     const int L = c.L;
     constexpr int YM = CT > 0 ? 4 * CT : 4 * kCMax;
@@ -333,14 +333,14 @@ cudaError_t launch_cond_signal(const rxgs_cond_s* c, const rxgs_scene_s& sc,
         cudaFuncSetAttribute(k_cond_signal<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
         k_cond_signal<64, 1><<<blocks, threads, smem, s>>>(
-            d, static_cast<int>(st.visible), st.order.as<int>(), sc.d_pos32.as<float4>(), d_rx, n_rx,
+            d, st.needed_count.as<int>(), st.needed_order.as<int>(), sc.d_pos32.as<float4>(), d_rx, n_rx,
             st.basis32.as<float2>(), st.gb32.as<float2>(), d_ag, d_sig);
     } else {
         if (d.H > kHMax || d.C > kCMax) return cudaErrorInvalidValue;
         cudaFuncSetAttribute(k_cond_signal<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
         k_cond_signal<0, 0><<<blocks, threads, smem, s>>>(
-            d, static_cast<int>(st.visible), st.order.as<int>(), sc.d_pos32.as<float4>(), d_rx, n_rx,
+            d, st.needed_count.as<int>(), st.needed_order.as<int>(), sc.d_pos32.as<float4>(), d_rx, n_rx,
             st.basis32.as<float2>(), st.gb32.as<float2>(), d_ag, d_sig);
     }
     return cudaGetLastError();

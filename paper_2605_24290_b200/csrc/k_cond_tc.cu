@@ -52,7 +52,7 @@ __device__ __forceinline__ uint32_t canon_off(int r, int k) {
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    k_cond_tc(const __grid_constant__ LocalW W, CondDev c, int n_vis, const int* __restrict__ vis,
+    k_cond_tc(const __grid_constant__ LocalW W, CondDev c, const int* __restrict__ n_rows, const int* __restrict__ vis,
               const float4* __restrict__ pos32, const double* __restrict__ rx, int n_rx,
               const float2* __restrict__ Bm, const float2* __restrict__ GB, const float* __restrict__ ag,
               float2* __restrict__ sig) {
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t w2hi_a = tc::smem_u32(w2hi), w2lo_a = tc::smem_u32(w2lo);
 
     const int n_jc = (n_rx + 31) >> 5;
-    const long long items = static_cast<long long>(n_vis) * n_jc;
+    const long long items = static_cast<long long>(*n_rows) * n_jc;
     const long long tiles = (items + 3) >> 2;
     const long long step = static_cast<long long>(gridDim.x) * kGroups;
     const int L = c.L;
@@ -303,7 +303,7 @@ cudaError_t launch_cond_signal_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc,
     const long long tiles = (items + 3) / 4;
     const long long want = (tiles + kGroups - 1) / kGroups;
     const int blocks = static_cast<int>(want < sms ? want : sms);
-    k_cond_tc<<<blocks, kThreads, smem, s>>>(w, d, static_cast<int>(st.visible), st.order.as<int>(),
+    k_cond_tc<<<blocks, kThreads, smem, s>>>(w, d, st.needed_count.as<int>(), st.needed_order.as<int>(),
                                               sc.d_pos32.as<float4>(), d_rx, n_rx, st.basis32.as<float2>(),
                                               st.gb32.as<float2>(), d_ag, d_sig);
     return cudaGetLastError();

@@ -175,3 +175,62 @@ int bin_tiles(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
 }
 
 }  // namespace rxgs_b200
+
+// ---------------------------------------------------------------- needed rows
+#include <cub/device/device_select.cuh>
+
+namespace rxgs_b200 {
+namespace {
+
+__global__ void k_mark_needed(DevGrid g, const int64_t* __restrict__ tile_offsets, const int* __restrict__ list,
+                              const int* __restrict__ walk_len, unsigned char* __restrict__ needed) {
+    const int tile = blockIdx.x;
+    int w = 0;
+    for (int b = 0; b < g.cell_blocks; ++b) w = max(w, walk_len[tile * g.cell_blocks + b]);
+    const int64_t begin = tile_offsets[tile];
+    for (int p = threadIdx.x; p < w; p += blockDim.x) needed[list[begin + p]] = 1;
+}
+
+__global__ void k_flags_in_order(int n, const int* __restrict__ order, const unsigned char* __restrict__ needed,
+                                 unsigned char* __restrict__ flags) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n) flags[r] = needed[order[r]];
+}
+
+}  // namespace
+
+int compact_needed(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
+    const int K = st.k;
+    const int n = static_cast<int>(st.visible);
+    RXGS_CUDA(st.needed.ensure(static_cast<size_t>(K + 1) * 2));
+    RXGS_CUDA(st.needed_order.ensure(sizeof(int) * (K + 1)));
+    RXGS_CUDA(st.needed_count.ensure(sizeof(int) * 4));
+    unsigned char* needed = st.needed.as<unsigned char>();
+    unsigned char* flags = needed + (K + 1);
+    RXGS_CUDA(cudaMemsetAsync(needed, 0, static_cast<size_t>(K + 1), s));
+    RXGS_CUDA(cudaMemsetAsync(st.needed_count.p, 0, sizeof(int), s));
+    if (st.entries > 0)
+        k_mark_needed<<<st.grid.n_tiles, 128, 0, s>>>(st.grid, st.tile_offsets.as<int64_t>(), st.list.as<int>(),
+                                                       st.walk_len.as<int>(), needed);
+    if (n > 0) {
+        k_flags_in_order<<<(n + 255) / 256, 256, 0, s>>>(n, st.order.as<int>(), needed, flags);
+        size_t tmp = 0;
+        RXGS_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, st.order.as<int>(), flags, st.needed_order.as<int>(),
+                                             st.needed_count.as<int>(), n, s));
+        RXGS_CUDA(ctx->sort_tmp.ensure(tmp));
+        RXGS_CUDA(cub::DeviceSelect::Flagged(ctx->sort_tmp.p, tmp, st.order.as<int>(), flags,
+                                             st.needed_order.as<int>(), st.needed_count.as<int>(), n, s));
+    }
+    st.needed_host = -1;
+    if (ctx->profile) {  // roofline bookkeeping only: the row count of the next conditioning launch
+        int h = 0;
+        RXGS_CUDA(cudaMemcpyAsync(&h, st.needed_count.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        RXGS_CUDA(cudaStreamSynchronize(s));
+        st.needed_host = h;
+    }
+    ctx->launches += 3;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? RXGS_OK : cuda_fail(e, "compact_needed");
+}
+
+}  // namespace rxgs_b200

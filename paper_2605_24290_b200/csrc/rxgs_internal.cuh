@@ -116,7 +116,12 @@ struct rxgs_txstate_s {
     int64_t entries = 0, visible = 0;
     double walk_sum = 0.0, tile_walk_sum = 0.0;
     rxgs_b200::DevBuf rec, culled, geom, spans, basis64, basis32, gb32, depth_key, tile_count,
-        order, rank, scan, tile_offsets, list, keys, tw, walk_len, cell_T, cell_len;
+        order, rank, scan, tile_offsets, list, keys, tw, walk_len, cell_T, cell_len, needed,
+        needed_order, needed_count;
+    // Gaussians reached by at least one cell's walk (list position < the
+    // tile's longest walk), in depth order: the only rows whose conditioned
+    // signal is ever read by the compositor.  needed_count is device-side.
+    int64_t needed_host = -1;
 };
 
 struct rxgs_cond_s {
@@ -154,6 +159,8 @@ int bin_tiles(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s);
 
 // ---- k_walk.cu (FP64, -fmad=false)
 cudaError_t launch_walk(rxgs_txstate_s& st, cudaStream_t s);
+// Marks and compacts the Gaussians the walk reaches (st.needed_order/count).
+int compact_needed(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s);
 
 // ---- k_cond.cu
 cudaError_t launch_cond_global(const rxgs_cond_s& c, const double* d_rx, int n_rx, float* d_ag,
