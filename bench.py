@@ -68,9 +68,12 @@ def workload(args):
             "parallelism": "receiver shards, scene replicated"}
 
 
-def make_inputs(args, lib, rank):
+def make_inputs(args, lib, rank, world):
+    """Replicated scene; this rank's shard of the world * rx receiver query set."""
+    from paper_2605_24290_b200.dist import shard_range
     sc = lib.synth_scene(args.gaussians, 2, 1, 7)
-    rx = lib.synth_points(args.rx, 11 + 1000 * rank, "bench.rx", BOX_LO, BOX_HI, 0.05)
+    b, e = shard_range(world * args.rx, rank, world)
+    rx = lib.synth_points(world * args.rx, 11, "bench.rx", BOX_LO, BOX_HI, 0.05)[b:e]
     return sc, rx
 
 
@@ -159,7 +162,7 @@ def run_b200(args):
     from paper_2605_24290_b200 import capi
 
     dev = torch.device("cuda", local)
-    sc, rx_np = make_inputs(args, capi, rank)
+    sc, rx_np = make_inputs(args, capi, rank, world)
     ctx = capi.Context(local)
     # One explicit stream for torch (flush, events) and the library: the
     # legacy default stream (handle 0) cannot be shared with the C-ABI.
