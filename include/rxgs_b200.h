@@ -38,6 +38,7 @@ typedef struct rxgs_ctx_s* rxgs_ctx;
 typedef struct rxgs_scene_s* rxgs_scene;
 typedef struct rxgs_txstate_s* rxgs_txstate;
 typedef struct rxgs_cond_s* rxgs_cond;
+typedef struct rxgs_trainer_s* rxgs_trainer;
 
 /* raster::SphericalGrid (sphraster.hpp:15-32). */
 typedef struct rxgs_grid {
@@ -185,6 +186,37 @@ int rxgs_render_queries(rxgs_ctx ctx, rxgs_scene scene, rxgs_cond c, rxgs_txstat
  * scene modality's measurement (spectrum H*W, rssi 1, csi C*2) in f64. */
 int rxgs_predict(rxgs_ctx ctx, rxgs_scene scene, rxgs_cond c, const rxgs_grid* grid,
                  const double tx[3], const double rx[3], double* out);
+
+/* ------------------------------------------------------------ training (config 4)
+ * One step of the Stage-II chain of conditioned_training_loop
+ * (trainer.cpp:410-466): condition_forward -> render_field -> spectrum
+ * aggregate -> composite_loss (L1; lambda_ssim = lambda_fft = 0) ->
+ * aggregate_modality_backward -> backward_render (coefficient part) ->
+ * condition_backward, for a batch of receivers sharing one transmitter.
+ * hyper = {feature_lr, rest_lr_ratio, conditioning_lr, lambda_ssim,
+ * lambda_fft, adam beta1, beta2, epsilon} (trainer.hpp:68-97 defaults
+ * 5e-3, 0.2, 1e-3, 0, 0, 0.9, 0.999, 1e-8); NULL = defaults. */
+int rxgs_trainer_create(rxgs_ctx ctx, rxgs_scene scene, rxgs_cond c, const double hyper[8], rxgs_trainer* out);
+int rxgs_trainer_destroy(rxgs_trainer t);
+/* Sum over the n_rx samples of the per-sample gradients (the reference's
+ * d_base and ConditioningGrads, packed like the parameters) into the
+ * trainer's flat f64 gradient buffer [d_base | d_params] (added to it when
+ * accumulate != 0).  targets: n_rx x H x W spectra (f32); losses: n_rx. */
+int rxgs_train_grads(rxgs_trainer t, rxgs_txstate st, const double* rx, int n_rx, const float* targets,
+                     double* losses, int accumulate);
+/* Device pointer and sizes of the flat gradient buffer, for the caller's
+ * data-parallel all-reduce (sum) before rxgs_train_apply. */
+int rxgs_train_grad_buffer(rxgs_trainer t, double** dev_ptr, int64_t* n, int64_t* n_base);
+int rxgs_train_get_grads(rxgs_trainer t, double* d_base, double* d_params);
+/* Optimizer::step on "features" (degree >= 1 scaled by rest_lr_ratio) and
+ * every conditioning group (diffengine.cpp:50-58): throws the reference's
+ * "optimizer: non-finite gradient in group ..." error, else Adam in place on
+ * the device copies of the scene coefficients and conditioning parameters. */
+int rxgs_train_apply(rxgs_trainer t);
+int64_t rxgs_train_step_count(rxgs_trainer t);
+/* Current (possibly trained) device parameters. */
+int rxgs_scene_get_coeffs(rxgs_scene scene, double* out);
+int rxgs_cond_get_params(rxgs_cond c, double* out);
 
 #ifdef __cplusplus
 }

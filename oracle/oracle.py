@@ -348,3 +348,30 @@ def reference() -> Checker | None:
 def cond_cfg(F=6, hidden=64, dc=16, S=16, R=32, nearest=0, mode="full", l_max=2, C_=1):
     return np.array([F, hidden, dc, S, R, nearest, MODE[mode] if isinstance(mode, str) else mode,
                      l_max, C_], np.int32)
+
+
+def _train_sample(self, scene_h, cond_h, grid: Grid, tx, rx, target, lambda_ssim=0.0, lambda_fft=0.0, geometry=False):
+    """Reference one-sample Stage-II gradient (ref_train_sample, reference build only)."""
+    sc = scene_h.data
+    k = len(sc["tau_logits"])
+    L = (sc["l_max"] + 1) ** 2
+    n_par = len(cond_h.data["params"])
+    loss = np.zeros(1)
+    d_base = np.empty(k * L * sc["channels"] * 2)
+    d_par = np.empty(n_par)
+    geo = [np.empty(k * 3), np.empty(k * 3), np.empty(k * 4), np.empty(k)] if geometry else [None] * 4
+    err = C.create_string_buffer(512)
+    rc = self._train_sample(scene_h.ptr, cond_h.ptr, grid.gi, grid.gd, _d(np.asarray(tx, np.float64)),
+                            _d(np.asarray(rx, np.float64)), _d(np.asarray(target, np.float64)), lambda_ssim,
+                            lambda_fft, 1, loss.ctypes.data_as(_dp), d_base.ctypes.data_as(_dp),
+                            d_par.ctypes.data_as(_dp), *[None if g is None else g.ctypes.data_as(_dp) for g in geo],
+                            err, 512)
+    if rc:
+        raise CheckerError(err.value.decode())
+    out = dict(loss=float(loss[0]), d_base=d_base, d_params=d_par)
+    if geometry:
+        out.update(d_positions=geo[0], d_log_scales=geo[1], d_quaternions=geo[2], d_tau_logits=geo[3])
+    return out
+
+
+Checker.train_sample = _train_sample

@@ -101,6 +101,15 @@ _SIG = {
     "rxgs_condition_batch": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int, _vp]),
     "rxgs_render_queries": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp]),
     "rxgs_predict": (C.c_int, [_vp, _vp, _vp, C.POINTER(Grid), _vp, _vp, _vp]),
+    "rxgs_trainer_create": (C.c_int, [_vp, _vp, _vp, _vp, C.POINTER(_vp)]),
+    "rxgs_trainer_destroy": (C.c_int, [_vp]),
+    "rxgs_train_grads": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp, _vp, C.c_int]),
+    "rxgs_train_grad_buffer": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_i64), C.POINTER(_i64)]),
+    "rxgs_train_get_grads": (C.c_int, [_vp, _vp, _vp]),
+    "rxgs_train_apply": (C.c_int, [_vp]),
+    "rxgs_train_step_count": (_i64, [_vp]),
+    "rxgs_scene_get_coeffs": (C.c_int, [_vp, _vp]),
+    "rxgs_cond_get_params": (C.c_int, [_vp, _vp]),
 }
 for _name, (_res, _args) in _SIG.items():
     _f = getattr(_lib, _name)
@@ -429,4 +438,73 @@ def build_occupancy(ctx: Context, scene: Scene, R, lo, hi):
     out = _out((R, R, R))
     _check(_lib.rxgs_build_occupancy(ctx.h, scene.h, R, ptr(lo, np.float64), ptr(hi, np.float64), out.ctypes.data,
                                      None))
+    return out
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of a device buffer owned by the library
+    (lets torch.distributed all-reduce it in place, zero copy)."""
+
+    def __init__(self, ptr, n, typestr="<f8"):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3}
+
+
+class Trainer:
+    """Training step of the conditioned Stage-II chain (trainer.cpp:410-466)."""
+
+    DEFAULTS = (5e-3, 0.2, 1e-3, 0.0, 0.0, 0.9, 0.999, 1e-8)
+
+    def __init__(self, ctx: Context, scene: Scene, cond: Cond, hyper=None):
+        self.ctx, self.scene, self.cond = ctx, scene, cond
+        hp = np.asarray(hyper if hyper is not None else self.DEFAULTS, np.float64)
+        h = _vp()
+        _check(_lib.rxgs_trainer_create(ctx.h, scene.h, cond.h, hp.ctypes.data, C.byref(h)))
+        self.h = h
+        p, n, nb = _vp(), _i64(), _i64()
+        _check(_lib.rxgs_train_grad_buffer(self.h, C.byref(p), C.byref(n), C.byref(nb)))
+        self.grad_ptr, self.n, self.n_base = p.value, n.value, nb.value
+
+    def __del__(self, _fn=_lib.rxgs_trainer_destroy):
+        if getattr(self, "h", None):
+            _fn(self.h)
+            self.h = None
+
+    def grads(self, st: TxState, rx, targets, accumulate=False):
+        """Loss per sample; gradients summed into the device buffer."""
+        rx = rx if hasattr(rx, "data_ptr") else np.ascontiguousarray(rx, np.float64)
+        tg = targets if hasattr(targets, "data_ptr") else np.ascontiguousarray(targets, np.float32)
+        n = int(rx.shape[0])
+        loss = np.empty(n)
+        _check(_lib.rxgs_train_grads(self.h, st.h, ptr(rx), n, ptr(tg), loss.ctypes.data, int(accumulate)))
+        return loss
+
+    def grad_tensor(self):
+        """The flat f64 gradient buffer as a zero-copy CUDA torch tensor."""
+        import torch
+        return torch.as_tensor(_CudaArray(self.grad_ptr, self.n), device=f"cuda:{torch.cuda.current_device()}")
+
+    def get_grads(self):
+        db = np.empty(self.n_base)
+        dp = np.empty(self.n - self.n_base)
+        _check(_lib.rxgs_train_get_grads(self.h, db.ctypes.data, dp.ctypes.data))
+        return db, dp
+
+    def apply(self):
+        _check(_lib.rxgs_train_apply(self.h))
+
+    @property
+    def step_count(self):
+        return int(_lib.rxgs_train_step_count(self.h))
+
+
+def scene_coeffs(scene: Scene):
+    out = np.empty(scene.k * scene.L * scene.channels * 2)
+    _check(_lib.rxgs_scene_get_coeffs(scene.h, out.ctypes.data))
+    return out
+
+
+def cond_params(cond: Cond):
+    out = np.empty(cond.param_count)
+    _check(_lib.rxgs_cond_get_params(cond.h, out.ctypes.data))
     return out

@@ -230,6 +230,12 @@ void layout_cond(rxgs_cond_s& c) {
 int compute_signals(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, rxgs_txstate st, const double* d_rx,
                     int n_rx, float2* d_sig) {
     cudaStream_t s = ctx->stream;
+    if (c && c->host_stale) {  // the tcgen05 kernel takes layers 1/3 as a kernel parameter from the host copy
+        RXGS_CUDA(cudaStreamSynchronize(s));
+        RXGS_CUDA(cudaMemcpy(c->h_params.data(), c->d_params64.p, c->h_params.size() * sizeof(double),
+                             cudaMemcpyDeviceToHost));
+        c->host_stale = false;
+    }
     const size_t ag_n = static_cast<size_t>(n_rx) * sc->L * 4 * sc->channels;
     RXGS_CUDA(ctx->ag.ensure(std::max<size_t>(ag_n, 1) * sizeof(float)));
     cudaEvent_t ev;
@@ -999,6 +1005,12 @@ int rxgs_predict(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const rxgs_grid* grid
     if (c) {
         RX_TRY(rxgs_condition_forward(ctx, c, sc, rx, coeffs.data(), nullptr));
     } else {
+        if (sc->host_stale) {
+            RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
+            RXGS_CUDA(cudaMemcpy(sc->h_coeffs.data(), sc->d_coeffs64.p, sc->h_coeffs.size() * sizeof(double),
+                                 cudaMemcpyDeviceToHost));
+            sc->host_stale = false;
+        }
         coeffs = sc->h_coeffs;
     }
     rxgs_txstate st = nullptr;

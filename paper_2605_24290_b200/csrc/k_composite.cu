@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(kThreads)
                 const float* __restrict__ tw, const int* __restrict__ walk_len,
                 const float2* __restrict__ sig, int n_rx, int C, float* __restrict__ spectrum,
                 float* __restrict__ rssi_partial, double* __restrict__ values,
-                float* __restrict__ csi_partial) {
+                float* __restrict__ csi_partial, float* __restrict__ field32) {
     __shared__ __align__(16) float s_tw[2][kP][kMaxCellsPerBlock];
     __shared__ __align__(16) float2 s_sig[2][kP][kCols];
     const int tile = blockIdx.x, cb = blockIdx.y, chunk = blockIdx.z;
@@ -137,6 +137,11 @@ __global__ void __launch_bounds__(kThreads)
                 const size_t base = (static_cast<size_t>(j) * C + ch) * 2 * plane;
                 values[base + cell] = re;
                 values[base + plane + cell] = im;
+            }
+            if (field32) {
+                const size_t base = (static_cast<size_t>(j) * C + ch) * 2 * plane;
+                field32[base + cell] = re;
+                field32[base + plane + cell] = im;
             }
             pw[b] += (re * re + im * im) * dom;
             cr[b] += re * dom;
@@ -251,7 +256,7 @@ cudaError_t launch_composite(const rxgs_txstate_s& st, const float2* d_sig, int 
     k_composite<<<grid, kThreads, 0, s>>>(g, st.tile_offsets.as<int64_t>(), st.list.as<int>(),
                                           st.tw.as<float>(), st.walk_len.as<int>(), d_sig, n_rx,
                                           st.channels, out.spectrum, out.rssi_partial, out.values,
-                                          out.csi_partial);
+                                          out.csi_partial, out.field32);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,658 @@
+// Training step (Stage-II / joint chain of conditioned_training_loop,
+// trainer.cpp:410-466) for a batch of receivers sharing one transmitter:
+//
+//   forward   conditioning + FLE reduction (k_cond.cu), compositing with an
+//             f32 field epilogue (k_composite.cu);
+//   loss      spectrum L1 (composite_loss, trainer.cpp:80-145, lambda_ssim =
+//             lambda_fft = 0) fused with aggregate_modality_backward
+//             (sphraster.cpp:435-445)                       -> k_loss_spectrum
+//   render    d signal of every walked list entry = tw^T * dField per tile
+//   adjoint   (the d_signals part of backward_render, sphraster.cpp:541-579),
+//             then a fixed-order per-Gaussian reduction        -> k_composite_T,
+//                                                                 k_reduce_ds
+//   cond      condition_backward (conditioning.cpp:472-587) fused with the
+//   adjoint   signal adjoint (backward_render :619-646): local MLP backward per
+//             (Gaussian, receiver) row with deterministic per-CTA weight
+//             gradients; d_base; the global branch reduced over Gaussians
+//             and back-propagated in FP64                       -> k_cond_bwd,
+//                                                                 k_dbase,
+//                                                                 k_global_red,
+//                                                                 k_global_bwd
+//   update    Adam with bias correction (diffengine.cpp:10-34), per-element
+//             learning-rate scale for FLE degree >= 1 (trainer.cpp:213-229)
+//                                                               -> k_adam
+// Every reduction runs in a fixed order (no floating-point atomics), so a
+// step is bitwise reproducible, as the reference requires.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "cond_common.cuh"
+#include "rxgs_internal.cuh"
+
+namespace rxgs_b200 {
+namespace {
+
+using namespace cond_dev;
+
+constexpr int kBwdThreads = 128;  // rows per tile in k_cond_bwd
+
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+
+// ------------------------------------------------------------------ base -> B * base
+__global__ void k_refresh_gb(int K, int L, int C, const int* __restrict__ culled, const double* __restrict__ basis64,
+                             const double* __restrict__ base64, float2* __restrict__ gb32) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= static_cast<long long>(K) * L * C) return;
+    const int k = static_cast<int>(i / (L * C));
+    const int l = static_cast<int>((i / C) % L);
+    if (culled[k]) {
+        gb32[i] = make_float2(0.f, 0.f);
+        return;
+    }
+    const double br = basis64[(static_cast<size_t>(k) * L + l) * 2], bi = basis64[(static_cast<size_t>(k) * L + l) * 2 + 1];
+    const double a = base64[i * 2], b = base64[i * 2 + 1];
+    gb32[i] = make_float2(static_cast<float>(a * br - b * bi), static_cast<float>(a * bi + b * br));
+}
+
+// ------------------------------------------------------------------ loss + aggregate adjoint
+// Spectrum L1: loss_j = lw/P sum|amp - gt|, d_amp = lw/P sign(amp - gt);
+// d_re = d_amp re/amp, d_im = d_amp im/amp.  G layout: [j][cell] complex.
+__global__ void k_loss_spectrum(int n_rx, int P, const float* __restrict__ field, const float* __restrict__ target,
+                                double l_weight, float2* __restrict__ G, double* __restrict__ loss_part) {
+    __shared__ double red[256];
+    const int j = blockIdx.y;
+    double acc = 0.0;
+    const float* re_p = field + static_cast<size_t>(j) * 2 * P;
+    const float* im_p = re_p + P;
+    const float w = static_cast<float>(l_weight / P);
+    for (int cell = blockIdx.x * blockDim.x + threadIdx.x; cell < P; cell += gridDim.x * blockDim.x) {
+        const float re = re_p[cell], im = im_p[cell];
+        const float amp = sqrtf(re * re + im * im + static_cast<float>(kAmpEps));
+        const float d = amp - target[static_cast<size_t>(j) * P + cell];
+        acc += fabs(static_cast<double>(d));
+        const float s = d > 0.f ? w : (d < 0.f ? -w : 0.f);
+        G[static_cast<size_t>(j) * P + cell] = make_float2(s * re / amp, s * im / amp);
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+        if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) loss_part[static_cast<size_t>(j) * gridDim.x + blockIdx.x] = red[0] * l_weight / P;
+}
+
+__global__ void k_loss_finalize(int n_rx, int nb, const double* __restrict__ part, double* __restrict__ loss) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n_rx) return;
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += part[static_cast<size_t>(j) * nb + b];
+    loss[j] = s;
+}
+
+// ------------------------------------------------------------------ composite transpose
+// d_entry[e][j] = sum_cells tw[e][cell] * G_j[cell] for the first W rows of a tile.
+__global__ void __launch_bounds__(256) k_composite_T(DevGrid g, const int64_t* __restrict__ tile_offsets,
+                                                     const float* __restrict__ tw, const int* __restrict__ walk_len,
+                                                     const float2* __restrict__ G, int n_rx,
+                                                     float2* __restrict__ d_entry) {
+    extern __shared__ float2 sG[];  // [cell_blocks*64][n_rx]
+    const int tile = blockIdx.x;
+    const int tt = tile / g.tiles_p, tp = tile % g.tiles_p;
+    const int ncell = g.cell_blocks * kMaxCellsPerBlock;
+    const size_t plane = static_cast<size_t>(g.nt) * g.np;
+    for (int i = threadIdx.x; i < ncell * n_rx; i += blockDim.x) {
+        const int lc = i / n_rx, j = i % n_rx;
+        const int row = tt * g.ts + lc / g.ts, col = tp * g.ts + lc % g.ts;
+        const bool valid = lc < g.cpt && row < g.nt && col < g.np;
+        sG[i] = valid ? G[static_cast<size_t>(j) * plane + static_cast<size_t>(row) * g.np + col] : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    int W = 0;
+    for (int b = 0; b < g.cell_blocks; ++b) W = max(W, walk_len[tile * g.cell_blocks + b]);
+    const int64_t begin = tile_offsets[tile];
+    const size_t stride = static_cast<size_t>(g.cell_blocks) * kMaxCellsPerBlock;
+    for (int i = threadIdx.x; i < W * n_rx; i += blockDim.x) {
+        const int pos = i / n_rx, j = i % n_rx;
+        const float* t = tw + static_cast<size_t>(begin + pos) * stride;
+        float ar = 0.f, ai = 0.f;
+        for (int c = 0; c < ncell; ++c) {
+            const float w = t[c];
+            const float2 gv = sG[c * n_rx + j];
+            ar = fmaf(w, gv.x, ar);
+            ai = fmaf(w, gv.y, ai);
+        }
+        d_entry[static_cast<size_t>(begin + pos) * n_rx + j] = make_float2(ar, ai);
+    }
+}
+
+// keys for the per-Gaussian regrouping of walked entries (others -> K)
+__global__ void k_entry_keys(DevGrid g, int K, const int64_t* __restrict__ tile_offsets, const int* __restrict__ list,
+                             const int* __restrict__ walk_len, int* __restrict__ keys, int* __restrict__ vals) {
+    const int tile = blockIdx.x;
+    int W = 0;
+    for (int b = 0; b < g.cell_blocks; ++b) W = max(W, walk_len[tile * g.cell_blocks + b]);
+    const int64_t begin = tile_offsets[tile], n = tile_offsets[tile + 1] - begin;
+    for (int p = threadIdx.x; p < n; p += blockDim.x) {
+        keys[begin + p] = p < W ? list[begin + p] : K;
+        vals[begin + p] = static_cast<int>(begin + p);
+    }
+}
+
+__global__ void k_key_hist(int64_t n, const int* __restrict__ keys, int* __restrict__ hist) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) atomicAdd(hist + keys[i], 1);
+}
+
+// d_s[k][j] = sum of the k's walked entries, in tile order.
+__global__ void k_reduce_ds(const int* __restrict__ n_rows, const int* __restrict__ rows, const int* __restrict__ goff,
+                            const int* __restrict__ gent, const float2* __restrict__ d_entry, int n_rx,
+                            float2* __restrict__ d_s) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= static_cast<long long>(*n_rows) * n_rx) return;
+    const int k = rows[i / n_rx], j = static_cast<int>(i % n_rx);
+    float2 acc = make_float2(0.f, 0.f);
+    for (int e = goff[k]; e < goff[k + 1]; ++e) acc = cadd(acc, d_entry[static_cast<size_t>(gent[e]) * n_rx + j]);
+    d_s[static_cast<size_t>(k) * n_rx + j] = acc;
+}
+
+// ------------------------------------------------------------------ conditioning adjoint
+// Local-parameter partial layout per CTA (floats): w1 H*6 | b1 H | w2 H*H | b2 H | w3 4H | b3 4
+__host__ __device__ constexpr int local_grad_count(int H) { return H * 6 + H + H * H + H + 4 * H + 4; }
+
+// One row = (needed Gaussian k, receiver j), C == 1, hidden H == 64.
+// smem per CTA: W2 (H*H) | per-row h1 | h2 | dh2 | dh1 (4 x 128 x H) | x (128 x 6) | dy (128 x 4)
+__global__ void __launch_bounds__(kBwdThreads) k_cond_bwd(CondDev c, const int* __restrict__ n_rows,
+                                                          const int* __restrict__ rows, const float4* __restrict__ pos32,
+                                                          const double* __restrict__ rx, int n_rx,
+                                                          const float2* __restrict__ Bm, const float2* __restrict__ GB,
+                                                          const float* __restrict__ ag, const float2* __restrict__ d_s,
+                                                          float2* __restrict__ u_out, float* __restrict__ part) {
+    constexpr int H = 64;
+    extern __shared__ __align__(16) float sm[];
+    float* sW2 = sm;
+    float* sH1 = sW2 + H * H;
+    float* sH2 = sH1 + kBwdThreads * H;
+    float* sDH2 = sH2 + kBwdThreads * H;
+    float* sDH1 = sDH2 + kBwdThreads * H;
+    float* sX = sDH1 + kBwdThreads * H;
+    float* sDY = sX + kBwdThreads * 6;
+    const float* p = c.p32;
+    for (int i = threadIdx.x; i < H * H; i += blockDim.x) sW2[i] = p[c.o_lw2 + i];
+    __syncthreads();
+    const int t = threadIdx.x;
+    // per-thread ownership of the weight-gradient accumulators
+    float gw2[32];  // dW2[o = t/2][i = (t%2)*32 .. +32)
+    for (int q = 0; q < 32; ++q) gw2[q] = 0.f;
+    float gw1[3] = {0.f, 0.f, 0.f};  // dW1 entries t*3 .. t*3+2 (of 384)
+    float gw3[2] = {0.f, 0.f};        // dW3 entries t*2, t*2+1 (of 256)
+    float gb1 = 0.f, gb2 = 0.f, gb3 = 0.f;  // b1[t], b2[t] (t < 64), b3[t] (t < 4)
+    const long long rows_total = static_cast<long long>(*n_rows) * n_rx;
+    const int L = c.L;
+    for (long long base_row = static_cast<long long>(blockIdx.x) * kBwdThreads; base_row < rows_total;
+         base_row += static_cast<long long>(gridDim.x) * kBwdThreads) {
+        const long long row = base_row + t;
+        const bool active = row < rows_total;
+        float* h1 = sH1 + t * H;
+        float* h2 = sH2 + t * H;
+        float* dh2 = sDH2 + t * H;
+        float* dh1 = sDH1 + t * H;
+        float x[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        float dy[4] = {0.f, 0.f, 0.f, 0.f};
+        if (active && !c.use_local) {  // global-only mode: no local branch, u = d_s
+            const int k = rows[row / n_rx], j = static_cast<int>(row % n_rx);
+            u_out[static_cast<size_t>(k) * n_rx + j] = d_s[static_cast<size_t>(k) * n_rx + j];
+            for (int o = 0; o < H; ++o) h1[o] = h2[o] = dh2[o] = dh1[o] = 0.f;
+        } else if (active) {
+            const int k = rows[row / n_rx], j = static_cast<int>(row % n_rx);
+            const float4 pk = pos32[k];
+            local_features<false>(c, c.occ, pk.x, pk.y, pk.z, static_cast<float>(rx[3 * j]),
+                                  static_cast<float>(rx[3 * j + 1]), static_cast<float>(rx[3 * j + 2]), x);
+            // forward (same arithmetic as the SIMT forward kernel)
+            for (int o = 0; o < H; ++o) {
+                float a = p[c.o_lb1 + o];
+                for (int i = 0; i < 6; ++i) a = fmaf(p[c.o_lw1 + o * 6 + i], x[i], a);
+                h1[o] = fmaxf(a, 0.f);
+            }
+            float y[4] = {p[c.o_lb3], p[c.o_lb3 + 1], p[c.o_lb3 + 2], p[c.o_lb3 + 3]};
+            for (int o = 0; o < H; ++o) {
+                float a = p[c.o_lb2 + o];
+                const float* wr = sW2 + o * H;
+                for (int i = 0; i < H; ++i) a = fmaf(wr[i], h1[i], a);
+                const float hv = fmaxf(a, 0.f);
+                h2[o] = hv;
+                for (int q = 0; q < 4; ++q) y[q] = fmaf(p[c.o_lw3 + q * H + o], hv, y[q]);
+            }
+            // signal pieces M = sum_l mid_l B_l, Bs = sum_l B_l (k_cond signal math)
+            float2 M = make_float2(0.f, 0.f), Bs = make_float2(0.f, 0.f);
+            const float4* a4 = reinterpret_cast<const float4*>(ag) + static_cast<size_t>(j) * L;
+            for (int l = 0; l < L; ++l) {
+                const float2 b = Bm[static_cast<size_t>(k) * L + l];
+                const float2 gb = GB[static_cast<size_t>(k) * L + l];
+                const float4 a = a4[l];
+                const float2 t0 = cmul(make_float2(1.f + a.x, a.y), gb), t1 = cmul(make_float2(a.z, a.w), b);
+                M = cadd(M, cadd(t0, t1));
+                Bs = cadd(Bs, b);
+            }
+            const float ar = c.additive ? 0.f : y[0], ai = c.additive ? 0.f : y[1];
+            const float2 ds = d_s[static_cast<size_t>(k) * n_rx + j];
+            // d alpha_L = ds conj(M), d beta_L = ds conj(Bs), u = conj(1 + alpha_L) ds
+            const float2 da = cmul(ds, cconj(M)), db = cmul(ds, cconj(Bs));
+            dy[0] = c.additive ? 0.f : da.x;
+            dy[1] = c.additive ? 0.f : da.y;
+            dy[2] = db.x;
+            dy[3] = db.y;
+            u_out[static_cast<size_t>(k) * n_rx + j] = cmul(make_float2(1.f + ar, -ai), ds);
+            // backward through layer 3 and the layer-2 ReLU
+            for (int o = 0; o < H; ++o) {
+                float a = 0.f;
+                for (int q = 0; q < 4; ++q) a = fmaf(p[c.o_lw3 + q * H + o], dy[q], a);
+                dh2[o] = h2[o] > 0.f ? a : 0.f;
+            }
+            for (int i = 0; i < H; ++i) dh1[i] = 0.f;
+            for (int o = 0; o < H; ++o) {
+                const float g = dh2[o];
+                if (g == 0.f) continue;
+                const float* wr = sW2 + o * H;
+                for (int i = 0; i < H; ++i) dh1[i] = fmaf(wr[i], g, dh1[i]);
+            }
+            for (int i = 0; i < H; ++i) dh1[i] = h1[i] > 0.f ? dh1[i] : 0.f;
+        } else {
+            for (int o = 0; o < H; ++o) h1[o] = h2[o] = dh2[o] = dh1[o] = 0.f;
+        }
+        for (int i = 0; i < 6; ++i) sX[t * 6 + i] = x[i];
+        for (int q = 0; q < 4; ++q) sDY[t * 4 + q] = dy[q];
+        __syncthreads();
+        // ---- weight gradients over the 128 rows of this tile, fixed row order
+        {
+            const int o = t >> 1, i0 = (t & 1) * 32;
+            for (int r = 0; r < kBwdThreads; ++r) {
+                const float g = sDH2[r * H + o];
+                if (g == 0.f) continue;
+                const float* hr = sH1 + r * H + i0;
+                for (int q = 0; q < 32; ++q) gw2[q] = fmaf(g, hr[q], gw2[q]);
+            }
+            for (int e = 0; e < 3; ++e) {
+                const int idx = t * 3 + e, oi = idx / 6, fi = idx % 6;
+                float a = gw1[e];
+                for (int r = 0; r < kBwdThreads; ++r) a = fmaf(sDH1[r * H + oi], sX[r * 6 + fi], a);
+                gw1[e] = a;
+            }
+            for (int e = 0; e < 2; ++e) {
+                const int idx = t * 2 + e, q = idx / H, oo = idx % H;
+                float a = gw3[e];
+                for (int r = 0; r < kBwdThreads; ++r) a = fmaf(sDY[r * 4 + q], sH2[r * H + oo], a);
+                gw3[e] = a;
+            }
+            if (t < H) {
+                float a1 = gb1, a2 = gb2;
+                for (int r = 0; r < kBwdThreads; ++r) {
+                    a1 += sDH1[r * H + t];
+                    a2 += sDH2[r * H + t];
+                }
+                gb1 = a1;
+                gb2 = a2;
+            }
+            if (t < 4) {
+                float a = gb3;
+                for (int r = 0; r < kBwdThreads; ++r) a += sDY[r * 4 + t];
+                gb3 = a;
+            }
+        }
+        __syncthreads();
+    }
+    // ---- per-CTA partials
+    constexpr int NG = local_grad_count(H);
+    float* out = part + static_cast<size_t>(blockIdx.x) * NG;
+    const int o_w1 = 0, o_b1 = H * 6, o_w2 = o_b1 + H, o_b2 = o_w2 + H * H, o_w3 = o_b2 + H, o_b3 = o_w3 + 4 * H;
+    for (int q = 0; q < 32; ++q) out[o_w2 + (t >> 1) * H + (t & 1) * 32 + q] = gw2[q];
+    for (int e = 0; e < 3; ++e) out[o_w1 + t * 3 + e] = gw1[e];
+    for (int e = 0; e < 2; ++e) out[o_w3 + t * 2 + e] = gw3[e];
+    if (t < H) {
+        out[o_b1 + t] = gb1;
+        out[o_b2 + t] = gb2;
+    }
+    if (t < 4) out[o_b3 + t] = gb3;
+}
+
+// sum CTA partials in CTA order into the f64 gradient vector
+__global__ void k_reduce_parts(int n_parts, int n, const float* __restrict__ part, double* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int b = 0; b < n_parts; ++b) s += part[static_cast<size_t>(b) * n + i];
+    out[i] += s;
+}
+
+// d_base[k][l] = conj(B_kl) * sum_j conj(1 + aG_jl) u_kj   (C == 1)
+__global__ void k_dbase(const int* __restrict__ n_rows, const int* __restrict__ rows, int L, int n_rx,
+                        const float2* __restrict__ Bm, const float* __restrict__ ag, int use_global, int additive,
+                        const float2* __restrict__ u, double* __restrict__ d_base) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= static_cast<long long>(*n_rows) * L) return;
+    const int k = rows[i / L], l = static_cast<int>(i % L);
+    double sr = 0.0, si = 0.0;
+    for (int j = 0; j < n_rx; ++j) {
+        const float2 uv = u[static_cast<size_t>(k) * n_rx + j];
+        const float* a = ag + (static_cast<size_t>(j) * L + l) * 4;
+        const double ar = (use_global && !additive) ? a[0] : 0.0, ai = (use_global && !additive) ? a[1] : 0.0;
+        // conj(1 + a) * u
+        sr += (1.0 + ar) * uv.x + ai * uv.y;
+        si += (1.0 + ar) * uv.y - ai * uv.x;
+    }
+    const float2 b = Bm[static_cast<size_t>(k) * L + l];
+    // conj(B) * s
+    d_base[(static_cast<size_t>(k) * L + l) * 2] += b.x * sr + b.y * si;
+    d_base[(static_cast<size_t>(k) * L + l) * 2 + 1] += b.x * si - b.y * sr;
+}
+
+// partial sums over Gaussians for the global branch:
+// daG_jl = sum_k u_kj conj(GB_kl), dbG_jl = sum_k u_kj conj(B_kl)
+__global__ void k_global_red(const int* __restrict__ n_rows, const int* __restrict__ rows, int L, int n_rx,
+                             const float2* __restrict__ Bm, const float2* __restrict__ GB,
+                             const float2* __restrict__ u, double* __restrict__ part) {
+    const int npair = n_rx * L;
+    const int nk = *n_rows;
+    const int per = (nk + gridDim.x - 1) / gridDim.x;
+    const int k0 = blockIdx.x * per, k1 = min(nk, k0 + per);
+    for (int pr = threadIdx.x; pr < npair; pr += blockDim.x) {
+        const int j = pr / L, l = pr % L;
+        double ar = 0, ai = 0, br = 0, bi = 0;
+        for (int r = k0; r < k1; ++r) {
+            const int k = rows[r];
+            const float2 uv = u[static_cast<size_t>(k) * n_rx + j];
+            const float2 g = GB[static_cast<size_t>(k) * L + l], b = Bm[static_cast<size_t>(k) * L + l];
+            ar += static_cast<double>(uv.x) * g.x + static_cast<double>(uv.y) * g.y;
+            ai += static_cast<double>(uv.y) * g.x - static_cast<double>(uv.x) * g.y;
+            br += static_cast<double>(uv.x) * b.x + static_cast<double>(uv.y) * b.y;
+            bi += static_cast<double>(uv.y) * b.x - static_cast<double>(uv.x) * b.y;
+        }
+        double* o = part + (static_cast<size_t>(blockIdx.x) * npair + pr) * 4;
+        o[0] = ar;
+        o[1] = ai;
+        o[2] = br;
+        o[3] = bi;
+    }
+}
+
+// Global branch adjoint for one (receiver, l) row in FP64 (mlp_backward
+// conditioning.cpp:33-70 with d_input, :530-583).  Writes the row's partial
+// gradient over [freqs | global w1 b1 w2 b2 w3 b3 | embed] (packed order).
+__global__ void k_global_bwd(CondDev c, int n_rx, const double* __restrict__ rx, const double* __restrict__ red_part,
+                             int n_red, double* __restrict__ row_part, int n_gpar) {
+    extern __shared__ double gs[];
+    const int H = c.H, gin = c.gin, L = c.L, F = c.F;
+    double* in = gs;
+    double* h1 = in + gin;
+    double* h2 = h1 + H;
+    double* dh2 = h2 + H;
+    double* dh1 = dh2 + H;
+    double* din = dh1 + H;
+    double* dy = din + gin;
+    const int row = blockIdx.x;
+    const int j = row / L, comp = row % L;
+    const double* p = c.p64;
+    double* out = row_part + static_cast<size_t>(row) * n_gpar;
+    for (int i = threadIdx.x; i < n_gpar; i += blockDim.x) out[i] = 0.0;
+    int l = 0;
+    while ((l + 1) * (l + 1) <= comp) ++l;
+    const int m = comp - l * l - l;
+    int l_max = 0;
+    while ((l_max + 1) * (l_max + 1) < L) ++l_max;
+    const double den = l_max > 0 ? static_cast<double>(l_max) : 1.0;
+    for (int i = threadIdx.x; i < gin; i += blockDim.x) {
+        double v;
+        if (i < 6 * F) {
+            const int a = i / (2 * F), band = (i % (2 * F)) / 2;
+            const double arg = p[c.o_freq + band * 3 + a] * rx[3 * j + a];
+            v = (i % 2) ? cos(arg) : sin(arg);
+        } else if (i == 6 * F) {
+            v = l / den;
+        } else if (i == 6 * F + 1) {
+            v = m / den;
+        } else {
+            v = p[c.o_emb + comp * c.dc + (i - 6 * F - 2)];
+        }
+        in[i] = v;
+    }
+    if (threadIdx.x < 4) {
+        double s = 0.0;
+        for (int b = 0; b < n_red; ++b) s += red_part[(static_cast<size_t>(b) * n_rx * L + row) * 4 + threadIdx.x];
+        dy[threadIdx.x] = (c.additive && threadIdx.x < 2) ? 0.0 : s;
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < H; o += blockDim.x) {
+        double a = p[c.o_gb1 + o];
+        for (int i = 0; i < gin; ++i) a += p[c.o_gw1 + static_cast<size_t>(o) * gin + i] * in[i];
+        h1[o] = a > 0.0 ? a : 0.0;
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < H; o += blockDim.x) {
+        double a = p[c.o_gb2 + o];
+        for (int i = 0; i < H; ++i) a += p[c.o_gw2 + static_cast<size_t>(o) * H + i] * h1[i];
+        h2[o] = a > 0.0 ? a : 0.0;
+    }
+    __syncthreads();
+    // offsets inside the packed global slice [freqs | w1 b1 w2 b2 w3 b3 | embed]
+    const int g_w1 = F * 3, g_b1 = g_w1 + H * gin, g_w2 = g_b1 + H, g_b2 = g_w2 + H * H, g_w3 = g_b2 + H,
+              g_b3 = g_w3 + 4 * H, g_emb = g_b3 + 4;
+    for (int o = threadIdx.x; o < H; o += blockDim.x) {
+        double a = 0.0;
+        for (int q = 0; q < 4; ++q) a += p[c.o_gw3 + q * H + o] * dy[q];
+        dh2[o] = h2[o] > 0.0 ? a : 0.0;
+        for (int q = 0; q < 4; ++q) out[g_w3 + q * H + o] = dy[q] * h2[o];
+    }
+    if (threadIdx.x < 4) out[g_b3 + threadIdx.x] = dy[threadIdx.x];
+    __syncthreads();
+    for (int i = threadIdx.x; i < H; i += blockDim.x) {
+        double a = 0.0;
+        for (int o = 0; o < H; ++o) a += p[c.o_gw2 + static_cast<size_t>(o) * H + i] * dh2[o];
+        dh1[i] = h1[i] > 0.0 ? a : 0.0;
+    }
+    for (int e = threadIdx.x; e < H * H; e += blockDim.x) out[g_w2 + e] = dh2[e / H] * h1[e % H];
+    for (int o = threadIdx.x; o < H; o += blockDim.x) out[g_b2 + o] = dh2[o];
+    __syncthreads();
+    for (int e = threadIdx.x; e < H * gin; e += blockDim.x) out[g_w1 + e] = dh1[e / gin] * in[e % gin];
+    for (int o = threadIdx.x; o < H; o += blockDim.x) out[g_b1 + o] = dh1[o];
+    for (int i = threadIdx.x; i < gin; i += blockDim.x) {
+        double a = 0.0;
+        for (int o = 0; o < H; ++o) a += p[c.o_gw1 + static_cast<size_t>(o) * gin + i] * dh1[o];
+        din[i] = a;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < c.dc; e += blockDim.x) out[g_emb + comp * c.dc + e] = din[6 * F + 2 + e];
+    for (int i = threadIdx.x; i < 3 * F; i += blockDim.x) {  // fourier adjoint (conditioning.cpp:573-583)
+        const int a = i / F, band = i % F;
+        const double freq = p[c.o_freq + band * 3 + a];
+        const double arg = freq * rx[3 * j + a];
+        const double ds = din[(a * F + band) * 2], dc = din[(a * F + band) * 2 + 1];
+        out[band * 3 + a] = ds * rx[3 * j + a] * cos(arg) - dc * rx[3 * j + a] * sin(arg);
+    }
+}
+
+__global__ void k_reduce_rows64(int n_rows, int n, const double* __restrict__ part, double* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int r = 0; r < n_rows; ++r) s += part[static_cast<size_t>(r) * n + i];
+    out[i] += s;
+}
+
+// scatter of the packed-global slice into the full packed parameter order
+__global__ void k_scatter_global(int n_freq, int n_mlp, int n_emb, size_t o_gw1, size_t o_emb,
+                                 const double* __restrict__ g, double* __restrict__ grad) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n_freq) grad[i] += g[i];
+    else if (i < n_freq + n_mlp) grad[o_gw1 + (i - n_freq)] += g[i];
+    else if (i < n_freq + n_mlp + n_emb) grad[o_emb + (i - n_freq - n_mlp)] += g[i];
+}
+
+__global__ void k_check_finite64(int64_t n, const double* __restrict__ v, int* __restrict__ bad) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n && !isfinite(v[i])) atomicMin(bad, 0);
+}
+
+// Adam with bias correction (diffengine.cpp:10-34) on f64 masters; lr_scale
+// for FLE degree >= 1 coefficients; f32 mirror refreshed in the same pass.
+__global__ void k_adam(int64_t n, double* __restrict__ w, const double* __restrict__ g, double* __restrict__ m,
+                       double* __restrict__ v, double lr, double bc1, double bc2, double b1, double b2, double eps,
+                       int lr_scale_L, int per_comp, double rest_ratio, float* __restrict__ w32) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const double gi = g[i];
+    const double mi = b1 * m[i] + (1.0 - b1) * gi;
+    const double vi = b2 * v[i] + (1.0 - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    double rate = lr;
+    if (lr_scale_L > 0) {
+        const int comp = static_cast<int>((i / per_comp) % lr_scale_L);
+        if (comp > 0) rate = lr * rest_ratio;  // degree 0 <=> comp 0
+    }
+    const double wn = w[i] - rate * (mi / bc1) / (sqrt(vi / bc2) + eps);
+    w[i] = wn;
+    if (w32) w32[i] = static_cast<float>(wn);
+}
+
+}  // namespace
+
+int train_regroup(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
+    const int64_t E = st.entries;
+    const int K = st.k;
+    RXGS_CUDA(st.gauss_off.ensure(sizeof(int) * (K + 2)));
+    RXGS_CUDA(st.gauss_ent.ensure(sizeof(int) * (E + 1)));
+    auto al = [](size_t x) { return (x + 255) & ~static_cast<size_t>(255); };
+    const size_t o_vals = al(sizeof(int) * (E + 1)), o_ks = o_vals + al(sizeof(int) * (E + 1)),
+                 o_hist = o_ks + al(sizeof(int) * (E + 1));
+    RXGS_CUDA(ctx->scratch_b.ensure(o_hist + al(sizeof(int) * (K + 2))));
+    char* pb = ctx->scratch_b.as<char>();
+    int* keys = reinterpret_cast<int*>(pb);
+    int* vals = reinterpret_cast<int*>(pb + o_vals);
+    int* ks = reinterpret_cast<int*>(pb + o_ks);
+    int* hist = reinterpret_cast<int*>(pb + o_hist);
+    RXGS_CUDA(cudaMemsetAsync(hist, 0, sizeof(int) * (K + 2), s));
+    if (E > 0) {
+        k_entry_keys<<<st.grid.n_tiles, 128, 0, s>>>(st.grid, K, st.tile_offsets.as<int64_t>(), st.list.as<int>(),
+                                                      st.walk_len.as<int>(), keys, vals);
+        int bits = 1;
+        while ((1 << bits) <= K) ++bits;
+        size_t tmp = 0;
+        RXGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, ks, vals, st.gauss_ent.as<int>(),
+                                                  static_cast<int>(E), 0, bits, s));
+        RXGS_CUDA(ctx->sort_tmp.ensure(tmp));
+        RXGS_CUDA(cub::DeviceRadixSort::SortPairs(ctx->sort_tmp.p, tmp, keys, ks, vals, st.gauss_ent.as<int>(),
+                                                  static_cast<int>(E), 0, bits, s));
+        k_key_hist<<<static_cast<unsigned>((E + 255) / 256), 256, 0, s>>>(E, keys, hist);
+    }
+    size_t tmp = 0;
+    RXGS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, hist, st.gauss_off.as<int>(), K + 1, s));
+    RXGS_CUDA(ctx->sort_tmp.ensure(tmp));
+    RXGS_CUDA(cub::DeviceScan::ExclusiveSum(ctx->sort_tmp.p, tmp, hist, st.gauss_off.as<int>(), K + 1, s));
+    st.regrouped = true;
+    ctx->launches += 5;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? RXGS_OK : cuda_fail(e, "train_regroup");
+}
+
+cudaError_t launch_refresh_gb(const rxgs_scene_s& sc, rxgs_txstate_s& st, cudaStream_t s) {
+    const long long n = static_cast<long long>(sc.k) * sc.L * sc.channels;
+    if (n == 0) return cudaSuccess;
+    k_refresh_gb<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(sc.k, sc.L, sc.channels, st.culled.as<int>(),
+                                                                         st.basis64.as<double>(),
+                                                                         sc.d_coeffs64.as<double>(), st.gb32.as<float2>());
+    return cudaGetLastError();
+}
+
+cudaError_t launch_loss_spectrum(int n_rx, int P, const float* field, const float* target, double l_weight,
+                                 float2* G, double* loss_part, double* loss, cudaStream_t s) {
+    const int nb = 16;
+    k_loss_spectrum<<<dim3(nb, n_rx), 256, 0, s>>>(n_rx, P, field, target, l_weight, G, loss_part);
+    k_loss_finalize<<<(n_rx + 127) / 128, 128, 0, s>>>(n_rx, nb, loss_part, loss);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_render_adjoint(const rxgs_txstate_s& st, const float2* G, int n_rx, float2* d_entry, float2* d_s,
+                                  cudaStream_t s) {
+    const DevGrid& g = st.grid;
+    const size_t smem = sizeof(float2) * g.cell_blocks * kMaxCellsPerBlock * n_rx;
+    if (st.entries > 0) {
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(k_composite_T, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        k_composite_T<<<g.n_tiles, 256, smem, s>>>(g, st.tile_offsets.as<int64_t>(), st.tw.as<float>(),
+                                                   st.walk_len.as<int>(), G, n_rx, d_entry);
+    }
+    const long long rows = static_cast<long long>(st.visible) * n_rx;
+    if (rows > 0)
+        k_reduce_ds<<<static_cast<unsigned>((rows + 255) / 256), 256, 0, s>>>(
+            st.needed_count.as<int>(), st.needed_order.as<int>(), st.gauss_off.as<int>(), st.gauss_ent.as<int>(),
+            d_entry, n_rx, d_s);
+    return cudaGetLastError();
+}
+
+size_t cond_bwd_smem() { return sizeof(float) * (64 * 64 + 4 * kBwdThreads * 64 + kBwdThreads * 10); }
+int cond_bwd_parts(int sms) { return sms * 2; }
+int local_grad_n() { return local_grad_count(64); }
+
+cudaError_t launch_cond_bwd(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
+                            const double* d_rx, int n_rx, const float* d_ag, const float2* d_s, float2* u,
+                            float* part, int n_parts, cudaStream_t s) {
+    const CondDev d = make_dev(cs);
+    const size_t smem = cond_bwd_smem();
+    cudaError_t e = cudaFuncSetAttribute(k_cond_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    k_cond_bwd<<<n_parts, kBwdThreads, smem, s>>>(d, st.needed_count.as<int>(), st.needed_order.as<int>(),
+                                                  sc.d_pos32.as<float4>(), d_rx, n_rx, st.basis32.as<float2>(),
+                                                  st.gb32.as<float2>(), d_ag, d_s, u, part);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_parts(int n_parts, int n, const float* part, double* out, cudaStream_t s) {
+    k_reduce_parts<<<(n + 255) / 256, 256, 0, s>>>(n_parts, n, part, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dbase(const rxgs_cond_s* cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st, int n_rx,
+                         const float* d_ag, const float2* u, double* d_base, cudaStream_t s) {
+    const long long n = static_cast<long long>(st.visible) * sc.L;
+    if (n == 0) return cudaSuccess;
+    k_dbase<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+        st.needed_count.as<int>(), st.needed_order.as<int>(), sc.L, n_rx, st.basis32.as<float2>(), d_ag,
+        cs && cs->use_global() ? 1 : 0, cs && cs->additive() ? 1 : 0, u, d_base);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_global_bwd(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st, int n_rx,
+                              const double* d_rx, const float2* u, double* red_part, int n_red, double* row_part,
+                              double* gslice, double* grad, cudaStream_t s) {
+    const CondDev d = make_dev(cs);
+    const int npair = n_rx * cs.L;
+    k_global_red<<<n_red, 128, 0, s>>>(st.needed_count.as<int>(), st.needed_order.as<int>(), cs.L, n_rx,
+                                       st.basis32.as<float2>(), st.gb32.as<float2>(), u, red_part);
+    const int n_gpar = static_cast<int>(cs.F * 3 + (cs.o_emb - cs.o_gw1) + cs.L * cs.dc);
+    const size_t smem = sizeof(double) * (2 * cs.gin + 4 * cs.hidden + 4);
+    k_global_bwd<<<npair, 128, smem, s>>>(d, n_rx, d_rx, red_part, n_red, row_part, n_gpar);
+    cudaMemsetAsync(gslice, 0, sizeof(double) * n_gpar, s);
+    k_reduce_rows64<<<(n_gpar + 255) / 256, 256, 0, s>>>(npair, n_gpar, row_part, gslice);
+    const int n_freq = cs.F * 3, n_mlp = static_cast<int>(cs.o_emb - cs.o_gw1), n_emb = cs.L * cs.dc;
+    k_scatter_global<<<(n_gpar + 255) / 256, 256, 0, s>>>(n_freq, n_mlp, n_emb, cs.o_gw1, cs.o_emb, gslice, grad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_finite64(int64_t n, const double* v, int* bad, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    k_check_finite64<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(n, v, bad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_adam(int64_t n, double* w, const double* g, double* m, double* v, double lr, int64_t step,
+                        double b1, double b2, double eps, int lr_scale_L, int per_comp, double rest_ratio, float* w32,
+                        cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const double bc1 = 1.0 - pow(b1, static_cast<double>(step)), bc2 = 1.0 - pow(b2, static_cast<double>(step));
+    k_adam<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(n, w, g, m, v, lr, bc1, bc2, b1, b2, eps,
+                                                                  lr_scale_L, per_comp, rest_ratio, w32);
+    return cudaGetLastError();
+}
+
+}  // namespace rxgs_b200

@@ -106,6 +106,7 @@ struct rxgs_scene_s {
     int k = 0, l_max = 0, channels = 1, L = 1, modality = 0;
     std::vector<double> h_pos, h_ls, h_q, h_tau, h_coeffs;
     rxgs_b200::DevBuf d_pos, d_ls, d_q, d_tau, d_coeffs64, d_coeffs32, d_pos32;
+    bool host_stale = false;  // device coefficients updated by the optimizer
 };
 
 struct rxgs_txstate_s {
@@ -122,6 +123,9 @@ struct rxgs_txstate_s {
     // tile's longest walk), in depth order: the only rows whose conditioned
     // signal is ever read by the compositor.  needed_count is device-side.
     int64_t needed_host = -1;
+    // walked list entries regrouped by Gaussian (training adjoint), built lazily
+    rxgs_b200::DevBuf gauss_off, gauss_ent;
+    bool regrouped = false;
 };
 
 struct rxgs_cond_s {
@@ -136,6 +140,7 @@ struct rxgs_cond_s {
     double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     int64_t global_calls = 0, local_calls = 0;
     rxgs_b200::DevBuf d_params32, d_params64, d_occ32;
+    bool host_stale = false;  // device parameters updated by the optimizer
     bool use_global() const { return mode != 2; }
     bool use_local() const { return mode != 1; }
     bool additive() const { return mode == 3; }
@@ -193,6 +198,7 @@ struct CompositeOut {
     float* rssi_partial = nullptr;  // [tile][j] power partials (C == 1)
     double* values = nullptr;     // [j][c][re/im][cell] f64 (materialised field)
     float* csi_partial = nullptr; // [tile][j][c][2]
+    float* field32 = nullptr;     // [j][c][re/im][cell] f32 (training forward)
 };
 cudaError_t launch_composite(const rxgs_txstate_s& st, const float2* d_sig, int n_rx,
                              const CompositeOut& out, cudaStream_t s);
@@ -203,5 +209,29 @@ cudaError_t launch_aggregate(const DevGrid& g, int modality, int n_rx, int chann
                              cudaStream_t s);
 cudaError_t launch_fill_transmittance(const rxgs_txstate_s& st, int n_rx, double* d_T,
                                       cudaStream_t s);
+
+// ---- k_train.cu
+int train_regroup(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s);
+cudaError_t launch_refresh_gb(const rxgs_scene_s& sc, rxgs_txstate_s& st, cudaStream_t s);
+cudaError_t launch_loss_spectrum(int n_rx, int P, const float* field, const float* target, double l_weight,
+                                 float2* G, double* loss_part, double* loss, cudaStream_t s);
+cudaError_t launch_render_adjoint(const rxgs_txstate_s& st, const float2* G, int n_rx, float2* d_entry, float2* d_s,
+                                  cudaStream_t s);
+size_t cond_bwd_smem();
+int cond_bwd_parts(int sms);
+int local_grad_n();
+cudaError_t launch_cond_bwd(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
+                            const double* d_rx, int n_rx, const float* d_ag, const float2* d_s, float2* u,
+                            float* part, int n_parts, cudaStream_t s);
+cudaError_t launch_reduce_parts(int n_parts, int n, const float* part, double* out, cudaStream_t s);
+cudaError_t launch_dbase(const rxgs_cond_s* cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st, int n_rx,
+                         const float* d_ag, const float2* u, double* d_base, cudaStream_t s);
+cudaError_t launch_global_bwd(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st, int n_rx,
+                              const double* d_rx, const float2* u, double* red_part, int n_red, double* row_part,
+                              double* gslice, double* grad, cudaStream_t s);
+cudaError_t launch_check_finite64(int64_t n, const double* v, int* bad, cudaStream_t s);
+cudaError_t launch_adam(int64_t n, double* w, const double* g, double* m, double* v, double lr, int64_t step,
+                        double b1, double b2, double eps, int lr_scale_L, int per_comp, double rest_ratio, float* w32,
+                        cudaStream_t s);
 
 }  // namespace rxgs_b200
