@@ -280,8 +280,14 @@ int rxgs_ctx_create(int device, rxgs_ctx* out) {
     API_END
 }
 
-int rxgs_ctx_destroy(rxgs_ctx ctx) {
-    if (!ctx) return RXGS_OK;
+}  // extern "C"
+
+namespace rxgs_b200 {
+// Handles (scene, conditioning, tx state, trainer) hold a reference on their
+// context; rxgs_ctx_destroy only marks it closed while any is alive, so
+// destruction order (e.g. garbage-collected bindings) cannot free it early.
+void ctx_retain(rxgs_ctx ctx) { ++ctx->refs; }
+static void ctx_free(rxgs_ctx ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     for (auto& p : ctx->pending) {
@@ -292,6 +298,18 @@ int rxgs_ctx_destroy(rxgs_ctx ctx) {
     for (auto* t : ctx->spare_tx) delete t;
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
+}
+void ctx_release(rxgs_ctx ctx) {
+    if (--ctx->refs == 0 && ctx->closed) ctx_free(ctx);
+}
+}  // namespace rxgs_b200
+
+extern "C" {
+
+int rxgs_ctx_destroy(rxgs_ctx ctx) {
+    if (!ctx) return RXGS_OK;
+    ctx->closed = true;
+    if (ctx->refs == 0) ctx_free(ctx);
     return RXGS_OK;
 }
 
@@ -403,6 +421,7 @@ int rxgs_scene_create(rxgs_ctx ctx, int k, int l_max, int channels, int modality
         delete sc;
         return rc;
     }
+    ctx_retain(ctx);
     *out = sc;
     return RXGS_OK;
     API_END
@@ -410,9 +429,11 @@ int rxgs_scene_create(rxgs_ctx ctx, int k, int l_max, int channels, int modality
 
 int rxgs_scene_destroy(rxgs_scene sc) {
     if (!sc) return RXGS_OK;
-    cudaSetDevice(sc->ctx->device);
-    cudaStreamSynchronize(sc->ctx->stream);
+    rxgs_ctx ctx = sc->ctx;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
     delete sc;
+    ctx_release(ctx);
     return RXGS_OK;
 }
 
@@ -454,6 +475,8 @@ int rxgs_tx_state_build(rxgs_ctx ctx, rxgs_scene sc, const double tx[3], const r
         st = new rxgs_txstate_s;
     }
     st->entries = st->visible = 0;
+    st->needed_host = -1;
+    st->regrouped = false;  // recycled buffers: per-state derived data must be rebuilt
     st->ctx = ctx;
     st->k = sc->k;
     st->l_max = sc->l_max;
@@ -512,6 +535,7 @@ int rxgs_tx_state_build(rxgs_ctx ctx, rxgs_scene sc, const double tx[3], const r
         if (rc) return fail_st(rc);
     }
     ctx->launches += 1;
+    ctx_retain(ctx);
     *out = st;
     return RXGS_OK;
     API_END
@@ -525,10 +549,11 @@ int rxgs_tx_state_destroy(rxgs_txstate st) {
         // Keep the buffers for the next build; stream order makes reuse safe
         // (later kernels on this stream run after every reader of st).
         ctx->spare_tx.push_back(st);
-        return RXGS_OK;
+    } else {
+        cudaStreamSynchronize(ctx->stream);
+        delete st;
     }
-    cudaStreamSynchronize(ctx->stream);
-    delete st;
+    ctx_release(ctx);
     return RXGS_OK;
 }
 
@@ -783,6 +808,7 @@ int rxgs_cond_create(rxgs_ctx ctx, const int32_t cfg[9], const double* params, c
         }
         c->has_occ = true;
     }
+    ctx_retain(ctx);
     *out = c;
     return RXGS_OK;
     API_END
@@ -790,9 +816,11 @@ int rxgs_cond_create(rxgs_ctx ctx, const int32_t cfg[9], const double* params, c
 
 int rxgs_cond_destroy(rxgs_cond c) {
     if (!c) return RXGS_OK;
-    cudaSetDevice(c->ctx->device);
-    cudaStreamSynchronize(c->ctx->stream);
+    rxgs_ctx ctx = c->ctx;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
     delete c;
+    ctx_release(ctx);
     return RXGS_OK;
 }
 

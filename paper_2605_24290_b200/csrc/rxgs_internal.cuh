@@ -99,6 +99,8 @@ struct rxgs_ctx_s {
         err_flag, host_in, host_out;
     int sm_count = 148;
     int cond_kernel = 0;  // 0 auto (tcgen05 when eligible), 1 force SIMT
+    int refs = 0;         // live handles on this context
+    bool closed = false;  // rxgs_ctx_destroy called while handles were alive
 };
 
 struct rxgs_scene_s {
@@ -148,6 +150,10 @@ struct rxgs_cond_s {
 };
 
 namespace rxgs_b200 {
+
+// ---- context lifetime (capi.cu)
+void ctx_retain(rxgs_ctx ctx);
+void ctx_release(rxgs_ctx ctx);
 
 // ---- timing helpers (capi.cu)
 void timing_begin(rxgs_ctx ctx, const char* name, cudaEvent_t* a);

@@ -86,15 +86,18 @@ int rxgs_trainer_create(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const double h
     cudaMemset(t->m.p, 0, n * 8);
     cudaMemset(t->v.p, 0, n * 8);
     t->n_parts = cond_bwd_parts(ctx->sm_count);
+    ctx_retain(ctx);
     *out = t;
     return RXGS_OK;
 }
 
 int rxgs_trainer_destroy(rxgs_trainer t) {
     if (!t) return RXGS_OK;
-    cudaSetDevice(t->ctx->device);
-    cudaStreamSynchronize(t->ctx->stream);
+    rxgs_ctx ctx = t->ctx;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
     delete t;
+    ctx_release(ctx);
     return RXGS_OK;
 }
 
