@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=0, help="receivers in the CPU baseline sample (0=auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-train", action="store_true")
+    ap.add_argument("--train-batch", type=int, default=16, help="(tx, rx) samples per GPU per training step")
     return ap.parse_args()
 
 
@@ -292,6 +294,8 @@ def run_b200(args):
                     "share_of_step": (cond_ms / cond_n) / ms_local,
                     "composite_ms": comp_ms / max(comp_n, 1), "walk_ms": walk_ms / max(comp_n, 1)}
 
+    train = None if args.no_train else bench_train(args, capi, ctx, scene, cond, grid, stream, dev, rank, world)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -312,10 +316,54 @@ def run_b200(args):
                 "vs_baseline": None, "dtype": "f32 (FP64 geometry/walk)", "data": "synthetic",
                 "config": workload(args), "e2e": e2e, "gpu_launches": int(launches),
                 "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
-                "tx_state": stats}
+                "tx_state": stats, "train_config4": train}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def bench_train(args, capi, ctx, scene, cond, grid, stream, dev, rank, world):
+    """BASELINE config 4: Stage-II training step (conditioning + compositing
+    forward and backward, spectrum L1) on B samples per GPU, the flat f64
+    gradient all-reduced over NCCL when world > 1, then Adam.  Geometry is
+    frozen (Stage II), so the transmitter state is cached (trainer.cpp:417-427)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2605_24290_b200.dist import allreduce_grads, max_over_ranks, shard_range
+
+    B = args.train_batch
+    b, e = shard_range(world * B, rank, world)
+    rx = capi.synth_points(world * B, 23, "bench.train.rx", BOX_LO, BOX_HI, 0.05)[b:e]
+    rng = np.random.default_rng(29 + rank)
+    targets = torch.from_numpy(rng.uniform(0.0, 2.0, (B, grid.cells)).astype(np.float32)).to(dev)
+    rx_d = torch.from_numpy(rx).to(dev)
+    st = scene.tx_state(np.array(TX), grid)
+    tr = capi.Trainer(ctx, scene, cond)
+    gbuf = tr.grad_tensor()
+
+    def step():
+        tr.grads(st, rx_d, targets)
+        allreduce_grads(gbuf)  # NCCL over NVLink (no-op at world 1)
+        tr.apply()
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    n_steps = max(3, min(args.steps, 10))
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(n_steps):
+        step()
+    s1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = max_over_ranks(s0.elapsed_time(s1) / n_steps, dev)
+    return {"workload": f"config4: K={args.gaussians} Stage-II step, {B} (tx, rx) samples per GPU, spectrum L1, "
+                        f"conditioning + compositing forward/backward, Adam; f64 gradient all-reduce "
+                        f"({'NCCL' if world > 1 else 'none at 1 GPU'}) of {tr.n} values",
+            "ms_per_step": ms, "steps_per_s": 1e3 / ms, "samples_per_s": world * B * 1e3 / ms,
+            "grad_floats": tr.n, "n_gpus": world}
 
 
 def run_reference(args):
