@@ -359,11 +359,33 @@ def bench_train(args, capi, ctx, scene, cond, grid, stream, dev, rank, world):
     s1.record(stream)
     torch.cuda.synchronize(dev)
     ms = max_over_ranks(s0.elapsed_time(s1) / n_steps, dev)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:  # reference CPU training sample (oracle/_ref), one sample, all host threads in render/backward
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import oracle as O
+            chk = O.reference()
+            sc = chk.synth_scene(args.gaussians, 2, 1, 7)
+            h = chk.scene(sc, "spectrum")
+            lo, hi = chk.scene_bounds(h, 0.0)
+            cfg = O.cond_cfg()
+            params = chk.synth_cond(cfg, 2, 1, lo, hi, 3, True)
+            olo, ohi = chk.scene_bounds(h, 0.1)
+            rc = chk.cond(cfg, params, chk.build_occupancy(h, 32, olo, ohi), olo, ohi)
+            og = O.Grid(args.n_theta, args.n_phi, 8, 1.0)
+            t0 = time.perf_counter()
+            chk.train_sample(h, rc, og, TX, rx[0], targets[0].cpu().numpy().astype(np.float64))
+            secs = time.perf_counter() - t0
+            cpu = {"samples_per_s": 1.0 / secs, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": "1 (tx, rx) sample: build_tx_state + condition_forward + render_field + "
+                             "composite_loss + aggregate/render/conditioning adjoints (render threads = nproc)"}
+        except Exception as ex:
+            cpu = {"error": str(ex)}
     return {"workload": f"config4: K={args.gaussians} Stage-II step, {B} (tx, rx) samples per GPU, spectrum L1, "
                         f"conditioning + compositing forward/backward, Adam; f64 gradient all-reduce "
                         f"({'NCCL' if world > 1 else 'none at 1 GPU'}) of {tr.n} values",
             "ms_per_step": ms, "steps_per_s": 1e3 / ms, "samples_per_s": world * B * 1e3 / ms,
-            "grad_floats": tr.n, "n_gpus": world}
+            "grad_floats": tr.n, "n_gpus": world, "cpu_reference": cpu}
 
 
 def run_reference(args):
