@@ -225,6 +225,45 @@ void layout_cond(rxgs_cond_s& c) {
     c.n_params = static_cast<int64_t>(o);
 }
 
+
+// First (receiver j, Gaussian k) in j-major order with rx_j exactly at a
+// Gaussian centre, -1 if none.  Host-side hash lookup (no device pass):
+// |rx - p| == 0 in the reference (conditioning.cpp:379-382) is bitwise
+// equality of the coordinates for any representable positions.
+int64_t find_coincident(rxgs_scene sc, const double* rx_host, int n_rx) {
+    auto key = [](double x, double y, double z) {
+        std::string k(24, '\0');
+        x += 0.0;  // -0 == +0
+        y += 0.0;
+        z += 0.0;
+        std::memcpy(&k[0], &x, 8);
+        std::memcpy(&k[8], &y, 8);
+        std::memcpy(&k[16], &z, 8);
+        return k;
+    };
+    if (!sc->pos_index_built) {
+        sc->pos_index.reserve(static_cast<size_t>(sc->k) * 2);
+        for (int k = sc->k - 1; k >= 0; --k)
+            sc->pos_index[key(sc->h_pos[3 * k], sc->h_pos[3 * k + 1], sc->h_pos[3 * k + 2])] = k;
+        sc->pos_index_built = true;
+    }
+    for (int j = 0; j < n_rx; ++j) {
+        const auto it = sc->pos_index.find(key(rx_host[3 * j], rx_host[3 * j + 1], rx_host[3 * j + 2]));
+        if (it != sc->pos_index.end()) return static_cast<int64_t>(j) * std::max(sc->k, 1) + it->second;
+    }
+    return -1;
+}
+
+int check_receivers(rxgs_ctx ctx, rxgs_scene sc, const double* rx, int n_rx) {
+    std::vector<double> h = to_host(rx, 3 * static_cast<size_t>(n_rx));
+    const int64_t e = find_coincident(sc, h.data(), n_rx);
+    if (e >= 0)
+        return fail(RXGS_ERR_INVALID, "condition_forward: receiver coincides with gaussian " +
+                                          std::to_string(e % std::max(sc->k, 1)));
+    (void)ctx;
+    return RXGS_OK;
+}
+
 // Signals for a receiver chunk: fused conditioning (or the bare base
 // coefficients when cond == nullptr).
 int compute_signals(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, rxgs_txstate st, const double* d_rx,
@@ -296,6 +335,8 @@ static void ctx_free(rxgs_ctx ctx) {
     }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
     for (auto* t : ctx->spare_tx) delete t;
+    for (auto e : ctx->chunk_events) cudaEventDestroy(e);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
 }
@@ -898,16 +939,7 @@ int rxgs_condition_batch(rxgs_ctx ctx, rxgs_cond c, rxgs_scene sc, const double*
     cudaStream_t s = ctx->stream;
     const double* d_rx = nullptr;
     RX_TRY(dev_in(ctx, rx, 3 * static_cast<size_t>(n_rx), ctx->scratch_c, &d_rx));
-    if (c->use_local()) {
-        RX_TRY(reset_err_flag(ctx));
-        RXGS_CUDA(launch_check_coincide(*sc, d_rx, n_rx, ctx->err_flag.as<int>(), s));
-        ctx->launches += 1;
-        int err = INT_MAX;
-        RX_TRY(check_err_flag(ctx, ctx->err_flag.as<int>(), &err));
-        if (err != INT_MAX)
-            return fail(RXGS_ERR_INVALID, "condition_forward: receiver coincides with gaussian " +
-                                              std::to_string(err % std::max(sc->k, 1)));
-    }
+    if (c->use_local()) RX_TRY(check_receivers(ctx, sc, rx, n_rx));
     const size_t stride = static_cast<size_t>(sc->L) * sc->channels * 2;
     const size_t no = static_cast<size_t>(n_rx) * sc->k * stride;
     const size_t ag_n = static_cast<size_t>(n_rx) * sc->L * 4 * sc->channels;
@@ -973,16 +1005,7 @@ int rxgs_render_queries(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, rxgs_txstate s
     cudaStream_t s = ctx->stream;
     const double* d_rx = nullptr;
     RX_TRY(dev_in(ctx, rx, 3 * static_cast<size_t>(n_rx), ctx->scratch_c, &d_rx));
-    if (c && c->use_local()) {
-        RX_TRY(reset_err_flag(ctx));
-        RXGS_CUDA(launch_check_coincide(*sc, d_rx, n_rx, ctx->err_flag.as<int>(), s));
-        ctx->launches += 1;
-        int err = INT_MAX;
-        RX_TRY(check_err_flag(ctx, ctx->err_flag.as<int>(), &err));
-        if (err != INT_MAX)
-            return fail(RXGS_ERR_INVALID, "condition_forward: receiver coincides with gaussian " +
-                                              std::to_string(err % std::max(sc->k, 1)));
-    }
+    if (c && c->use_local()) RX_TRY(check_receivers(ctx, sc, rx, n_rx));
     const DevGrid& g = st->grid;
     const size_t plane = static_cast<size_t>(g.nt) * g.np;
     const int n_tb = g.n_tiles * g.cell_blocks;
@@ -990,10 +1013,16 @@ int rxgs_render_queries(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, rxgs_txstate s
     float* d_rssi = nullptr;
     RX_TRY(dev_out(out_spectrum, static_cast<size_t>(n_rx) * plane, ctx->host_out, &d_spec));
     RX_TRY(dev_out(out_rssi, static_cast<size_t>(n_rx), ctx->scratch_d, &d_rssi));
-    // receiver chunks bound the signal buffer (K x chunk complex f32) to ~4 GB
+    // receiver chunks bound the signal buffer (K x chunk complex f32) to ~4 GB;
+    // with host spectra, smaller chunks let the D2H of chunk i (copy stream)
+    // overlap the conditioning of chunk i+1
     const size_t per_rx = std::max<size_t>(static_cast<size_t>(sc->k), 1) * sizeof(float2);
     int chunk = static_cast<int>(std::min<size_t>(static_cast<size_t>(n_rx), (size_t{4} << 30) / per_rx));
+    const bool pipelined = out_spectrum && d_spec != out_spectrum && n_rx >= 256;
+    if (pipelined) chunk = std::min(chunk, ((n_rx + 4 * 32 - 1) / (4 * 32)) * 32);
     chunk = std::max(chunk, 1);
+    if (pipelined && !ctx->copy_stream) RXGS_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    int n_chunk_ev = 0;
     RXGS_CUDA(ctx->signals.ensure(per_rx * chunk));
     RXGS_CUDA(ctx->partial.ensure(std::max<size_t>(static_cast<size_t>(n_tb) * chunk, 1) * sizeof(float)));
     for (int j0 = 0; j0 < n_rx; j0 += chunk) {
@@ -1011,14 +1040,29 @@ int rxgs_render_queries(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, rxgs_txstate s
             RXGS_CUDA(launch_rssi_finalize(ctx->partial.as<float>(), n_tb, nj, d_rssi + j0, nullptr, s));
             ctx->launches += 1;
         }
+        if (pipelined) {
+            if (static_cast<int>(ctx->chunk_events.size()) <= n_chunk_ev) {
+                cudaEvent_t e;
+                RXGS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                ctx->chunk_events.push_back(e);
+            }
+            cudaEvent_t e = ctx->chunk_events[n_chunk_ev++];
+            RXGS_CUDA(cudaEventRecord(e, s));
+            RXGS_CUDA(cudaStreamWaitEvent(ctx->copy_stream, e, 0));
+            RXGS_CUDA(cudaMemcpyAsync(out_spectrum + static_cast<size_t>(j0) * plane,
+                                      d_spec + static_cast<size_t>(j0) * plane,
+                                      sizeof(float) * static_cast<size_t>(nj) * plane, cudaMemcpyDeviceToHost,
+                                      ctx->copy_stream));
+        }
     }
     if (c) {
         if (c->use_global()) c->global_calls += static_cast<int64_t>(n_rx) * sc->L;
         if (c->use_local()) c->local_calls += static_cast<int64_t>(n_rx) * sc->k;
     }
     const bool host_out = (out_spectrum && d_spec != out_spectrum) || (out_rssi && d_rssi != out_rssi);
-    RX_TRY(finish_out(ctx, out_spectrum, d_spec, static_cast<size_t>(n_rx) * plane));
+    if (!pipelined) RX_TRY(finish_out(ctx, out_spectrum, d_spec, static_cast<size_t>(n_rx) * plane));
     RX_TRY(finish_out(ctx, out_rssi, d_rssi, static_cast<size_t>(n_rx)));
+    if (pipelined) RXGS_CUDA(cudaStreamSynchronize(ctx->copy_stream));
     if (host_out || !is_device_ptr(rx)) RXGS_CUDA(cudaStreamSynchronize(s));
     return RXGS_OK;
     API_END

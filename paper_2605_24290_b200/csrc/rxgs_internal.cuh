@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <map>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "rxgs_b200.h"
@@ -100,6 +101,8 @@ struct rxgs_ctx_s {
     int sm_count = 148;
     int cond_kernel = 0;  // 0 auto (tcgen05 when eligible), 1 force SIMT
     int refs = 0;         // live handles on this context
+    cudaStream_t copy_stream = nullptr;  // D2H of finished receiver chunks (host outputs)
+    std::vector<cudaEvent_t> chunk_events;
     bool closed = false;  // rxgs_ctx_destroy called while handles were alive
 };
 
@@ -109,6 +112,10 @@ struct rxgs_scene_s {
     std::vector<double> h_pos, h_ls, h_q, h_tau, h_coeffs;
     rxgs_b200::DevBuf d_pos, d_ls, d_q, d_tau, d_coeffs64, d_coeffs32, d_pos32;
     bool host_stale = false;  // device coefficients updated by the optimizer
+    // exact position -> lowest Gaussian index (receiver-on-Gaussian check,
+    // conditioning.cpp:380-382), built lazily on the host
+    std::unordered_map<std::string, int> pos_index;
+    bool pos_index_built = false;
 };
 
 struct rxgs_txstate_s {
