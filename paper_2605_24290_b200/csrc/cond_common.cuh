@@ -82,19 +82,21 @@ __device__ __forceinline__ float sample_tri(const CondDev& c, const float* occ, 
     return acc;
 }
 
-// Occupancy held with a one-voxel zero border, (R+2)^3: the trilinear lookup
-// then needs no per-corner bounds test -- a sample is either fully inside the
-// padded range (corners read real data or the zero border, exactly the
-// reference's "out-of-bounds corners read 0", conditioning.cpp:91) or it
-// reads 0.
+// Occupancy held with a zero border -- one voxel below, two above: a
+// (R+3)^3 grid.  A trilinear sample then needs no per-corner bounds test:
+// each voxel coordinate u is clamped to [-1, R]; every corner of the clamped
+// sample is either real data or border, and a clamped axis lands on the
+// border with weight 1, which reproduces the reference's "out-of-bounds
+// corners read 0" (conditioning.cpp:91) exactly.
+__host__ __device__ constexpr int padded_dim(int R) { return R + 3; }
 __device__ __forceinline__ int padded_index(int R, int ix, int iy, int iz) {
-    const int P = R + 2;
+    const int P = padded_dim(R);
     return ((ix + 1) * P + (iy + 1)) * P + (iz + 1);
 }
 
-// Fill a padded copy of the R^3 grid (called by all threads of a CTA).
+// Fill the padded copy of the R^3 grid (called by all threads of a CTA).
 __device__ __forceinline__ void load_padded_occ(const CondDev& c, float* dst) {
-    const int R = c.R, P = R + 2, n = P * P * P;
+    const int R = c.R, P = padded_dim(R), n = P * P * P;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const int ix = i / (P * P) - 1, iy = (i / P) % P - 1, iz = i % P - 1;
         const bool in = ix >= 0 && iy >= 0 && iz >= 0 && ix < R && iy < R && iz < R;
@@ -102,39 +104,48 @@ __device__ __forceinline__ void load_padded_occ(const CondDev& c, float* dst) {
     }
 }
 
-// probe_segment (conditioning.cpp:163-178) with trilinear lookups on the
-// padded grid; the segment p -> p + d is walked incrementally in voxel units.
+// probe_segment (conditioning.cpp:163-178), trilinear, on the padded grid.
+// The segment p -> p + d is walked in voxel units; ST / RT > 0 specialise the
+// sample count / resolution at compile time (fully unrolled, immediate
+// corner offsets), 0 = runtime values.
+template <int ST = 0, int RT = 0>
 __device__ __forceinline__ void probe_padded(const CondDev& c, const float* occ, float px, float py, float pz,
                                              float dx, float dy, float dz, float& T, float& rho) {
-    const int R = c.R, P = R + 2;
+    const int R = RT > 0 ? RT : c.R;
+    const int P = padded_dim(R);
+    const int S = ST > 0 ? ST : c.S;
+    const float hi = static_cast<float>(R);
     const float i0 = 1.f / c.cell[0], i1 = 1.f / c.cell[1], i2 = 1.f / c.cell[2];
     const float b0 = (px - c.lo[0]) * i0 - 0.5f, b1 = (py - c.lo[1]) * i1 - 0.5f, b2 = (pz - c.lo[2]) * i2 - 0.5f;
     const float s0 = dx * i0, s1 = dy * i1, s2 = dz * i2;
+    const float dt = S == 1 ? 0.f : 0.9f / static_cast<float>(S - 1);
     float tr = 1.f, sum = 0.f;
-    const int S = c.S;
-    for (int s = 0; s < S; ++s) {
-        const float t = S == 1 ? 0.5f : 0.05f + 0.9f * static_cast<float>(s) / (S - 1);
-        const float u0 = fmaf(t, s0, b0), u1 = fmaf(t, s1, b1), u2 = fmaf(t, s2, b2);
-        const float f0 = floorf(u0), f1 = floorf(u1), f2 = floorf(u2);
-        const int a0 = static_cast<int>(f0), a1 = static_cast<int>(f1), a2 = static_cast<int>(f2);
-        const bool ok = a0 >= -1 && a0 < R && a1 >= -1 && a1 < R && a2 >= -1 && a2 < R;
-        float v = 0.f;
-        if (ok) {
+#pragma unroll
+    for (int s = 0; s < (ST > 0 ? ST : 1); ++s) {
+        for (int si = (ST > 0 ? s : 0); si < (ST > 0 ? s + 1 : S); ++si) {
+            const float t = S == 1 ? 0.5f : fmaf(static_cast<float>(si), dt, 0.05f);
+            const float u0 = fminf(fmaxf(fmaf(t, s0, b0), -1.f), hi);
+            const float u1 = fminf(fmaxf(fmaf(t, s1, b1), -1.f), hi);
+            const float u2 = fminf(fmaxf(fmaf(t, s2, b2), -1.f), hi);
+            const float f0 = floorf(u0), f1 = floorf(u1), f2 = floorf(u2);
             const float w0 = u0 - f0, w1 = u1 - f1, w2 = u2 - f2;
-            const float* q = occ + ((a0 + 1) * P + (a1 + 1)) * P + (a2 + 1);
+            // padded linear index, exact in FP32 (P^3 < 2^24)
+            const int idx = static_cast<int>(fmaf(f0 + 1.f, static_cast<float>(P * P),
+                                                  fmaf(f1 + 1.f, static_cast<float>(P), f2 + 1.f)));
+            const float* q = occ + idx;
             const float c00 = fmaf(w2, q[1] - q[0], q[0]);
             const float c01 = fmaf(w2, q[P + 1] - q[P], q[P]);
             const float c10 = fmaf(w2, q[P * P + 1] - q[P * P], q[P * P]);
             const float c11 = fmaf(w2, q[P * P + P + 1] - q[P * P + P], q[P * P + P]);
             const float c0 = fmaf(w1, c01 - c00, c00);
             const float c1 = fmaf(w1, c11 - c10, c10);
-            v = fmaf(w0, c1 - c0, c0);
+            const float v = fmaf(w0, c1 - c0, c0);
+            tr *= 1.f - v;
+            sum += v;
         }
-        tr *= 1.f - v;
-        sum += v;
     }
     T = tr;
-    rho = sum / S;
+    rho = sum / static_cast<float>(S);
 }
 
 __device__ __forceinline__ float sample_near(const CondDev& c, const float* occ, float qx, float qy,
@@ -150,7 +161,7 @@ __device__ __forceinline__ float sample_near(const CondDev& c, const float* occ,
 // Local features [v_hat, d, T, rho] (conditioning.cpp:377-396).  PADDED:
 // occ is the (R+2)^3 zero-bordered copy (trilinear fast path); otherwise the
 // plain R^3 grid.
-template <bool PADDED = false>
+template <bool PADDED = false, int ST = 0, int RT = 0>
 __device__ __forceinline__ void local_features(const CondDev& c, const float* occ, float px,
                                                float py, float pz, float rx, float ry, float rz,
                                                float* in) {
@@ -163,7 +174,7 @@ __device__ __forceinline__ void local_features(const CondDev& c, const float* oc
     in[3] = d;
     float T = 1.f, rho = 0.f;
     if (PADDED && c.probe && !c.nearest) {
-        probe_padded(c, occ, px, py, pz, dx, dy, dz, T, rho);
+        probe_padded<ST, RT>(c, occ, px, py, pz, dx, dy, dz, T, rho);
     } else if (c.probe) {
         float sum = 0.f;
         for (int s = 0; s < c.S; ++s) {

@@ -290,7 +290,7 @@ __global__ void k_check_coincide(int K, const double* __restrict__ pos, const do
 
 size_t local_smem_bytes(const CondDev& d, bool with_occ) {
     const size_t f = static_cast<size_t>(d.H) * d.H + d.H * 6 + 2 * d.H + 4 * d.C * d.H +
-                     ((4 * d.C + 3) & ~3) + (with_occ ? static_cast<size_t>(d.R + 2) * (d.R + 2) * (d.R + 2) : 0);
+                     ((4 * d.C + 3) & ~3) + (with_occ ? static_cast<size_t>(padded_dim(d.R)) * padded_dim(d.R) * padded_dim(d.R) : 0);
     return f * sizeof(float);
 }
 

@@ -35,6 +35,7 @@ constexpr int kGroups = 4;
 constexpr int kThreads = 128 * kGroups;
 constexpr uint32_t kIdesc = tc::idesc_bf16_f32(128, kH);
 constexpr int kW2Bytes = kH * kH * 2;  // one bf16 64x64 matrix
+constexpr int kW1Bytes = kH * 16 * 2;  // one bf16 64x16 matrix
 
 struct LocalW {
     float w1[kH * 6];
@@ -51,6 +52,19 @@ __device__ __forceinline__ uint32_t canon_off(int r, int k) {
     return static_cast<uint32_t>(((r >> 3) * 8 + (k >> 3)) * 128 + (r & 7) * 16 + (k & 7) * 2);
 }
 
+// byte offset of element (row r, k) in a no-swizzle K-major tile with 16
+// K-elements per row (2 K-chunks): LBO = 128 B, SBO = 256 B.
+__device__ __forceinline__ uint32_t canon_off16(int r, int k) {
+    return static_cast<uint32_t>(((r >> 3) * 2 + (k >> 3)) * 128 + (r & 7) * 16 + (k & 7) * 2);
+}
+
+__device__ __forceinline__ void split_store(uint8_t* hi_base, uint8_t* lo_base, uint32_t off, float w) {
+    const float hi = tc::bf16_round(w);
+    *reinterpret_cast<uint16_t*>(hi_base + off) = static_cast<uint16_t>(tc::pack_bf16(hi, 0.f) & 0xFFFFu);
+    *reinterpret_cast<uint16_t*>(lo_base + off) = static_cast<uint16_t>(tc::pack_bf16(w - hi, 0.f) & 0xFFFFu);
+}
+
+template <int ST, int RT>
 __global__ void __launch_bounds__(kThreads, 1)
     k_cond_tc(const __grid_constant__ LocalW W, CondDev c, const int* __restrict__ n_rows, const int* __restrict__ vis,
               const float4* __restrict__ pos32, const double* __restrict__ rx, int n_rx,
@@ -59,7 +73,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* w2hi = smem;
     uint8_t* w2lo = smem + kW2Bytes;
-    float* s_occ = reinterpret_cast<float*>(smem + 2 * kW2Bytes);
+    uint8_t* w1hi = smem + 2 * kW2Bytes;           // [W1 | b1 | 0] : 64 x 16 bf16
+    uint8_t* w1lo = w1hi + kW1Bytes;
+    float* s_occ = reinterpret_cast<float*>(smem + 2 * kW2Bytes + 2 * kW1Bytes);
     __shared__ uint64_t bars[kGroups];
     __shared__ uint32_t tbase_s;
 
@@ -67,15 +83,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = tid >> 5, lane = tid & 31;
     const int g = warp >> 2, wl = warp & 3;
 
-    // ---- one-time setup: W2 split into bf16 hi/lo core matrices, occupancy
-    for (int i = tid; i < kH * kH; i += kThreads) {
-        const int n = i / kH, k = i % kH;
-        const float w = c.p32[c.o_lw2 + i];
-        const float hi = tc::bf16_round(w);
-        const float lo = w - hi;
-        const uint32_t ph = tc::pack_bf16(hi, 0.f), pl = tc::pack_bf16(lo, 0.f);
-        *reinterpret_cast<uint16_t*>(w2hi + canon_off(n, k)) = static_cast<uint16_t>(ph & 0xFFFFu);
-        *reinterpret_cast<uint16_t*>(w2lo + canon_off(n, k)) = static_cast<uint16_t>(pl & 0xFFFFu);
+    // ---- one-time setup: W1 (+bias column) and W2 as bf16 hi/lo core matrices, occupancy
+    for (int i = tid; i < kH * kH; i += kThreads) split_store(w2hi, w2lo, canon_off(i / kH, i % kH), c.p32[c.o_lw2 + i]);
+    for (int i = tid; i < kH * 16; i += kThreads) {
+        const int n = i / 16, k = i % 16;
+        const float w = k < 6 ? c.p32[c.o_lw1 + n * 6 + k] : (k == 6 ? c.p32[c.o_lb1 + n] : 0.f);
+        split_store(w1hi, w1lo, canon_off16(n, k), w);
     }
     if (c.probe) load_padded_occ(c, s_occ);
     if (warp == 0) {
@@ -93,10 +106,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const uint32_t tbase = tbase_s;
     const uint32_t lane_off = static_cast<uint32_t>(32 * wl) << 16;
-    const uint32_t tm_d = tbase + 128 * g;       // 64 f32 columns
-    const uint32_t tm_ahi = tm_d + 64;           // 32 columns = 64 bf16
+    const uint32_t tm_d = tbase + 128 * g;       // 64 f32 columns (layer-1 then layer-2 accumulator)
+    const uint32_t tm_ahi = tm_d + 64;           // 32 columns = 64 bf16 (layer-1 A uses the first 8)
     const uint32_t tm_alo = tm_d + 96;
     const uint32_t w2hi_a = tc::smem_u32(w2hi), w2lo_a = tc::smem_u32(w2lo);
+    const uint32_t w1hi_a = tc::smem_u32(w1hi), w1lo_a = tc::smem_u32(w1lo);
 
     const int n_jc = (n_rx + 31) >> 5;
     const long long items = static_cast<long long>(*n_rows) * n_jc;
@@ -117,27 +131,50 @@ __global__ void __launch_bounds__(kThreads, 1)
         float in[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         if (active) {
             const float4 pk = pos32[k];
-            local_features<true>(c, s_occ, pk.x, pk.y, pk.z, static_cast<float>(rx[3 * j]),
-                           static_cast<float>(rx[3 * j + 1]), static_cast<float>(rx[3 * j + 2]), in);
+            local_features<true, ST, RT>(c, s_occ, pk.x, pk.y, pk.z, static_cast<float>(rx[3 * j]),
+                                         static_cast<float>(rx[3 * j + 1]), static_cast<float>(rx[3 * j + 2]), in);
         }
-        // ---- layer 1 (FFMA, constant-bank weights) -> bf16 hi/lo -> TMEM (A operand)
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
+        // ---- layer 1 on the tensor cores: A1 = [x, 1, 0...] (K = 16) hi/lo -> TMEM
+        {
             uint32_t hi[8], lo[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                const int o = 16 * ch + 2 * q;
-                float ha = W.b1[o], hb = W.b1[o + 1];
+                const float xa = 2 * q < 6 ? in[2 * q] : (2 * q == 6 ? 1.f : 0.f);
+                const float xb = 2 * q + 1 < 6 ? in[2 * q + 1] : 0.f;
+                hi[q] = tc::pack_bf16(xa, xb);
+                lo[q] = tc::pack_bf16(xa - __uint_as_float(hi[q] << 16), xb - __uint_as_float(hi[q] & 0xFFFF0000u));
+            }
+            tc::tmem_st8(tm_ahi + lane_off, hi);
+            tc::tmem_st8(tm_alo + lane_off, lo);
+        }
+        tc::wait_st();
+        tc::fence_before_sync();
+        tc::named_bar_sync(1 + g, 128);
+        if (wl == 0 && lane == 0) {
+            tc::fence_after_sync();
+            const uint64_t bh = tc::sdesc_kmajor_noswizzle(w1hi_a, 128, 256);
+            const uint64_t bl = tc::sdesc_kmajor_noswizzle(w1lo_a, 128, 256);
+            tc::mma_ts(tm_d, tm_ahi, bh, kIdesc, 0u);
+            tc::mma_ts(tm_d, tm_ahi, bl, kIdesc, 1u);
+            tc::mma_ts(tm_d, tm_alo, bh, kIdesc, 1u);
+            tc::mma_commit(&bars[g]);
+        }
+        tc::mbar_wait(&bars[g], phase);
+        phase ^= 1u;
+        tc::fence_after_sync();
+        // ---- ReLU(h1) -> bf16 hi/lo -> TMEM (layer-2 A operand; overwrites A1)
 #pragma unroll
-                for (int i = 0; i < 6; ++i) {
-                    ha = fmaf(W.w1[o * 6 + i], in[i], ha);
-                    hb = fmaf(W.w1[(o + 1) * 6 + i], in[i], hb);
-                }
-                ha = fmaxf(ha, 0.f);
-                hb = fmaxf(hb, 0.f);
+        for (int ch = 0; ch < 4; ++ch) {
+            uint32_t r[16];
+            tc::tmem_ld16(tm_d + lane_off + 16 * ch, r);
+            tc::wait_ld();
+            uint32_t hi[8], lo[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const float ha = fmaxf(__uint_as_float(r[2 * q]), 0.f);
+                const float hb = fmaxf(__uint_as_float(r[2 * q + 1]), 0.f);
                 hi[q] = tc::pack_bf16(ha, hb);
-                const float ra = __uint_as_float(hi[q] << 16), rb = __uint_as_float(hi[q] & 0xFFFF0000u);
-                lo[q] = tc::pack_bf16(ha - ra, hb - rb);
+                lo[q] = tc::pack_bf16(ha - __uint_as_float(hi[q] << 16), hb - __uint_as_float(hi[q] & 0xFFFF0000u));
             }
             tc::tmem_st8(tm_ahi + lane_off + 8 * ch, hi);
             tc::tmem_st8(tm_alo + lane_off + 8 * ch, lo);
@@ -176,6 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int t = 0; t < 4; ++t) y[t] = fmaf(W.w3[t * kH + o], h2, y[t]);
             }
         }
+        tc::fence_before_sync();  // the next tile's layer-1 MMA overwrites D after the barrier
         if (active) sig[static_cast<size_t>(k) * n_rx + j] = fused_signal(c, k, j, 0, L, 1, Bm, GB, ag, y);
     }
     tc::fence_before_sync();
@@ -275,7 +313,7 @@ __global__ void __launch_bounds__(128) k_tc_selftest(float* __restrict__ err, in
 }  // namespace
 
 bool cond_tc_eligible(const rxgs_cond_s* c) {
-    return c && c->use_local() && c->hidden == kH && c->C == 1 && (c->R + 2) * (c->R + 2) * (c->R + 2) <= 48000;
+    return c && c->use_local() && c->hidden == kH && c->C == 1 && padded_dim(c->R) * padded_dim(c->R) * padded_dim(c->R) <= 48000;
 }
 
 cudaError_t launch_cond_signal_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
@@ -292,10 +330,8 @@ cudaError_t launch_cond_signal_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc,
     }
     for (int i = 0; i < 4 * kH; ++i) w.w3[i] = static_cast<float>(p[cs.o_lw3 + i]);
     for (int i = 0; i < 4; ++i) w.b3[i] = static_cast<float>(p[cs.o_lb3 + i]);
-    const size_t P = static_cast<size_t>(d.R) + 2;
-    const size_t smem = 2 * kW2Bytes + (d.probe ? P * P * P * sizeof(float) : 0);
-    cudaError_t e = cudaFuncSetAttribute(k_cond_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
+    const size_t P = static_cast<size_t>(padded_dim(d.R));
+    const size_t smem = 2 * kW2Bytes + 2 * kW1Bytes + (d.probe ? P * P * P * sizeof(float) : 0);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -303,9 +339,13 @@ cudaError_t launch_cond_signal_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc,
     const long long tiles = (items + 3) / 4;
     const long long want = (tiles + kGroups - 1) / kGroups;
     const int blocks = static_cast<int>(want < sms ? want : sms);
-    k_cond_tc<<<blocks, kThreads, smem, s>>>(w, d, st.needed_count.as<int>(), st.needed_order.as<int>(),
-                                              sc.d_pos32.as<float4>(), d_rx, n_rx, st.basis32.as<float2>(),
-                                              st.gb32.as<float2>(), d_ag, d_sig);
+    const bool fast = d.S == 16 && d.R == 32 && !d.nearest;
+    auto kern = fast ? k_cond_tc<16, 32> : k_cond_tc<0, 0>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<blocks, kThreads, smem, s>>>(w, d, st.needed_count.as<int>(), st.needed_order.as<int>(),
+                                        sc.d_pos32.as<float4>(), d_rx, n_rx, st.basis32.as<float2>(),
+                                        st.gb32.as<float2>(), d_ag, d_sig);
     return cudaGetLastError();
 }
 
