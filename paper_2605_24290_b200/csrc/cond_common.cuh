@@ -108,30 +108,28 @@ __device__ __forceinline__ void load_padded_occ(const CondDev& c, float* dst) {
 // The segment p -> p + d is walked in voxel units; ST / RT > 0 specialise the
 // sample count / resolution at compile time (fully unrolled, immediate
 // corner offsets), 0 = runtime values.
-template <int ST = 0, int RT = 0>
-__device__ __forceinline__ void probe_padded(const CondDev& c, const float* occ, float px, float py, float pz,
-                                             float dx, float dy, float dz, float& T, float& rho) {
-    const int R = RT > 0 ? RT : c.R;
+template <int ST, int RT, bool CLAMP>
+__device__ __forceinline__ void probe_walk(const float* occ, int R, int S, float b0, float b1, float b2, float s0,
+                                           float s1, float s2, float& tr, float& sum) {
     const int P = padded_dim(R);
-    const int S = ST > 0 ? ST : c.S;
     const float hi = static_cast<float>(R);
-    const float i0 = 1.f / c.cell[0], i1 = 1.f / c.cell[1], i2 = 1.f / c.cell[2];
-    const float b0 = (px - c.lo[0]) * i0 - 0.5f, b1 = (py - c.lo[1]) * i1 - 0.5f, b2 = (pz - c.lo[2]) * i2 - 0.5f;
-    const float s0 = dx * i0, s1 = dy * i1, s2 = dz * i2;
+    const float cidx = static_cast<float>(P * P + P + 1);  // the +1 border offset of each axis
     const float dt = S == 1 ? 0.f : 0.9f / static_cast<float>(S - 1);
-    float tr = 1.f, sum = 0.f;
 #pragma unroll
     for (int s = 0; s < (ST > 0 ? ST : 1); ++s) {
         for (int si = (ST > 0 ? s : 0); si < (ST > 0 ? s + 1 : S); ++si) {
             const float t = S == 1 ? 0.5f : fmaf(static_cast<float>(si), dt, 0.05f);
-            const float u0 = fminf(fmaxf(fmaf(t, s0, b0), -1.f), hi);
-            const float u1 = fminf(fmaxf(fmaf(t, s1, b1), -1.f), hi);
-            const float u2 = fminf(fmaxf(fmaf(t, s2, b2), -1.f), hi);
+            float u0 = fmaf(t, s0, b0), u1 = fmaf(t, s1, b1), u2 = fmaf(t, s2, b2);
+            if (CLAMP) {
+                u0 = fminf(fmaxf(u0, -1.f), hi);
+                u1 = fminf(fmaxf(u1, -1.f), hi);
+                u2 = fminf(fmaxf(u2, -1.f), hi);
+            }
             const float f0 = floorf(u0), f1 = floorf(u1), f2 = floorf(u2);
             const float w0 = u0 - f0, w1 = u1 - f1, w2 = u2 - f2;
             // padded linear index, exact in FP32 (P^3 < 2^24)
-            const int idx = static_cast<int>(fmaf(f0 + 1.f, static_cast<float>(P * P),
-                                                  fmaf(f1 + 1.f, static_cast<float>(P), f2 + 1.f)));
+            const int idx = static_cast<int>(
+                fmaf(f0, static_cast<float>(P * P), fmaf(f1, static_cast<float>(P), f2 + cidx)));
             const float* q = occ + idx;
             const float c00 = fmaf(w2, q[1] - q[0], q[0]);
             const float c01 = fmaf(w2, q[P + 1] - q[P], q[P]);
@@ -144,6 +142,29 @@ __device__ __forceinline__ void probe_padded(const CondDev& c, const float* occ,
             sum += v;
         }
     }
+}
+
+template <int ST = 0, int RT = 0>
+__device__ __forceinline__ void probe_padded(const CondDev& c, const float* occ, float px, float py, float pz,
+                                             float dx, float dy, float dz, float& T, float& rho) {
+    const int R = RT > 0 ? RT : c.R;
+    const int S = ST > 0 ? ST : c.S;
+    const float i0 = 1.f / c.cell[0], i1 = 1.f / c.cell[1], i2 = 1.f / c.cell[2];
+    const float b0 = (px - c.lo[0]) * i0 - 0.5f, b1 = (py - c.lo[1]) * i1 - 0.5f, b2 = (pz - c.lo[2]) * i2 - 0.5f;
+    const float s0 = dx * i0, s1 = dy * i1, s2 = dz * i2;
+    float tr = 1.f, sum = 0.f;
+    // The sampled points lie on the segment between t = 0.05 and t = 0.95; if
+    // both ends are inside [-1, R] on every axis so is every sample, and the
+    // clamps can be skipped (the usual case: receivers inside the room).
+    const float hi = static_cast<float>(R);
+    auto inside = [&](float t) {
+        const float a = fmaf(t, s0, b0), b = fmaf(t, s1, b1), d = fmaf(t, s2, b2);
+        return a >= -1.f && a <= hi && b >= -1.f && b <= hi && d >= -1.f && d <= hi;
+    };
+    if (inside(0.05f) && inside(0.95f) && inside(0.5f))
+        probe_walk<ST, RT, false>(occ, R, S, b0, b1, b2, s0, s1, s2, tr, sum);
+    else
+        probe_walk<ST, RT, true>(occ, R, S, b0, b1, b2, s0, s1, s2, tr, sum);
     T = tr;
     rho = sum / static_cast<float>(S);
 }
@@ -246,12 +267,13 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
     return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
-// s = (1+aL) * sum_l[(1+aG_l) GB_l + bG_l B_l] + bL * sum_l B_l for one
-// (Gaussian k, receiver j, channel ch); y = local MLP output (4C).
-__device__ __forceinline__ float2 fused_signal(const CondDev& c, int k, int j, int ch, int L, int C,
-                                               const float2* __restrict__ B, const float2* __restrict__ GB,
-                                               const float* __restrict__ ag, const float* y) {
-    float2 M = make_float2(0.f, 0.f), Bs = make_float2(0.f, 0.f);
+// The receiver-dependent but MLP-independent half of the fused signal:
+// M = sum_l [(1+aG_l) GB_l + bG_l B_l] = sum_l mid_l B_l and Bs = sum_l B_l.
+__device__ __forceinline__ void fle_reduce(int k, int j, int ch, int L, int C, const float2* __restrict__ B,
+                                           const float2* __restrict__ GB, const float* __restrict__ ag, float2& M,
+                                           float2& Bs) {
+    M = make_float2(0.f, 0.f);
+    Bs = make_float2(0.f, 0.f);
     const float4* a4 = reinterpret_cast<const float4*>(ag) + static_cast<size_t>(j) * L * C + ch;
     for (int l = 0; l < L; ++l) {
         const float2 b = B[static_cast<size_t>(k) * L + l];
@@ -263,10 +285,24 @@ __device__ __forceinline__ float2 fused_signal(const CondDev& c, int k, int j, i
         Bs.x += b.x;
         Bs.y += b.y;
     }
+}
+
+// s = (1+aL) M + bL Bs, y = local MLP output (4C) for channel ch.
+__device__ __forceinline__ float2 local_affine(const CondDev& c, int ch, float2 M, float2 Bs, const float* y) {
     const float ar = c.additive ? 0.f : y[4 * ch], ai = c.additive ? 0.f : y[4 * ch + 1];
     const float2 s0 = cmul(make_float2(1.f + ar, ai), M);
     const float2 s1 = cmul(make_float2(y[4 * ch + 2], y[4 * ch + 3]), Bs);
     return make_float2(s0.x + s1.x, s0.y + s1.y);
+}
+
+// s = (1+aL) * sum_l[(1+aG_l) GB_l + bG_l B_l] + bL * sum_l B_l for one
+// (Gaussian k, receiver j, channel ch); y = local MLP output (4C).
+__device__ __forceinline__ float2 fused_signal(const CondDev& c, int k, int j, int ch, int L, int C,
+                                               const float2* __restrict__ B, const float2* __restrict__ GB,
+                                               const float* __restrict__ ag, const float* y) {
+    float2 M, Bs;
+    fle_reduce(k, j, ch, L, C, B, GB, ag, M, Bs);
+    return local_affine(c, ch, M, Bs, y);
 }
 
 }  // namespace cond_dev
