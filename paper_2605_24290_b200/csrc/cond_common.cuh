@@ -153,18 +153,7 @@ __device__ __forceinline__ void probe_padded(const CondDev& c, const float* occ,
     const float b0 = (px - c.lo[0]) * i0 - 0.5f, b1 = (py - c.lo[1]) * i1 - 0.5f, b2 = (pz - c.lo[2]) * i2 - 0.5f;
     const float s0 = dx * i0, s1 = dy * i1, s2 = dz * i2;
     float tr = 1.f, sum = 0.f;
-    // The sampled points lie on the segment between t = 0.05 and t = 0.95; if
-    // both ends are inside [-1, R] on every axis so is every sample, and the
-    // clamps can be skipped (the usual case: receivers inside the room).
-    const float hi = static_cast<float>(R);
-    auto inside = [&](float t) {
-        const float a = fmaf(t, s0, b0), b = fmaf(t, s1, b1), d = fmaf(t, s2, b2);
-        return a >= -1.f && a <= hi && b >= -1.f && b <= hi && d >= -1.f && d <= hi;
-    };
-    if (inside(0.05f) && inside(0.95f) && inside(0.5f))
-        probe_walk<ST, RT, false>(occ, R, S, b0, b1, b2, s0, s1, s2, tr, sum);
-    else
-        probe_walk<ST, RT, true>(occ, R, S, b0, b1, b2, s0, s1, s2, tr, sum);
+    probe_walk<ST, RT, true>(occ, R, S, b0, b1, b2, s0, s1, s2, tr, sum);
     T = tr;
     rho = sum / static_cast<float>(S);
 }
