@@ -70,9 +70,12 @@ int64_t rxgs_ctx_launch_count(rxgs_ctx ctx);
 /* Conditioning kernel selection: 0 = auto (tcgen05 when hidden == 64 and
  * C == 1, else FP32 SIMT), 1 = force the FP32 SIMT kernel (A/B checks). */
 int rxgs_ctx_set_cond_kernel(rxgs_ctx ctx, int which);
+/* Query-path compositing: 0 = auto (tcgen05 for 8x8 tiles, C == 1), 1 = FP32 SIMT. */
+int rxgs_ctx_set_composite_kernel(rxgs_ctx ctx, int which);
 /* Diagnostic: a 128x64x64 bf16 tcgen05 GEMM with A in TMEM and with A in
- * shared memory, max |error| vs FP32 FMA of the same values; err[4] =
- * {smooth: A-in-TMEM, A-in-smem; small integers (exact): TMEM, smem}. */
+ * shared memory, max |error| vs FP32 FMA of the same values; err[5] =
+ * {smooth: A-in-TMEM, A-in-smem; small integers (exact): TMEM, smem;
+ * small integers, both operands MN-major (the compositor's layout)}. */
 int rxgs_selftest_tcgen05(rxgs_ctx ctx, double* err);
 
 /* ------------------------------------------------------------ synthetic inputs

@@ -70,6 +70,7 @@ _SIG = {
     "rxgs_ctx_reset_stats": (C.c_int, [_vp]),
     "rxgs_ctx_launch_count": (_i64, [_vp]),
     "rxgs_ctx_set_cond_kernel": (C.c_int, [_vp, C.c_int]),
+    "rxgs_ctx_set_composite_kernel": (C.c_int, [_vp, C.c_int]),
     "rxgs_selftest_tcgen05": (C.c_int, [_vp, _vp]),
     "rxgs_synth_scene": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint64, _vp, _vp, _vp, _vp, _vp]),
     "rxgs_synth_points": (C.c_int, [C.c_int, C.c_uint64, C.c_char_p, _vp, _vp, C.c_double, _vp]),
@@ -232,8 +233,12 @@ class Context:
         """'auto' (tcgen05 when eligible) or 'simt'."""
         _check(_lib.rxgs_ctx_set_cond_kernel(self.h, {"auto": 0, "simt": 1}[which]))
 
+    def set_composite_kernel(self, which):
+        """'auto' (tcgen05 when eligible) or 'simt'."""
+        _check(_lib.rxgs_ctx_set_composite_kernel(self.h, {"auto": 0, "simt": 1}[which]))
+
     def selftest_tcgen05(self):
-        e = np.zeros(4)
+        e = np.zeros(5)
         _check(_lib.rxgs_selftest_tcgen05(self.h, e.ctypes.data))
         return tuple(float(x) for x in e)
 

@@ -401,16 +401,23 @@ int rxgs_ctx_set_cond_kernel(rxgs_ctx ctx, int which) {
     return RXGS_OK;
 }
 
+int rxgs_ctx_set_composite_kernel(rxgs_ctx ctx, int which) {
+    if (!ctx || which < 0 || which > 1) return fail(RXGS_ERR_INVALID, "rxgs_ctx_set_composite_kernel: bad argument");
+    ctx->composite_kernel = which;
+    return RXGS_OK;
+}
+
 int rxgs_selftest_tcgen05(rxgs_ctx ctx, double* err) {
     if (!ctx) return fail(RXGS_ERR_INVALID, "null context");
     RX_TRY(set_device(ctx));
-    RXGS_CUDA(ctx->err_flag.ensure(16));
-    RXGS_CUDA(cudaMemsetAsync(ctx->err_flag.p, 0, 16, ctx->stream));
+    RXGS_CUDA(ctx->err_flag.ensure(32));
+    RXGS_CUDA(cudaMemsetAsync(ctx->err_flag.p, 0, 20, ctx->stream));
     RXGS_CUDA(launch_tc_selftest(ctx->err_flag.as<float>(), ctx->stream));
-    float e[4] = {0.f, 0.f, 0.f, 0.f};
-    RXGS_CUDA(cudaMemcpyAsync(e, ctx->err_flag.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    RXGS_CUDA(launch_tc_selftest_mn(ctx->err_flag.as<float>() + 4, ctx->stream));
+    float e[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+    RXGS_CUDA(cudaMemcpyAsync(e, ctx->err_flag.p, 20, cudaMemcpyDeviceToHost, ctx->stream));
     RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
-    for (int i = 0; i < 4; ++i) err[i] = e[i];
+    for (int i = 0; i < 5; ++i) err[i] = e[i];
     return RXGS_OK;
 }
 
@@ -1033,7 +1040,10 @@ int rxgs_render_queries(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, rxgs_txstate s
         co.rssi_partial = d_rssi ? ctx->partial.as<float>() : nullptr;
         cudaEvent_t ev;
         timing_begin(ctx, "composite", &ev);
-        RXGS_CUDA(launch_composite(*st, ctx->signals.as<float2>(), nj, co, s));
+        if (ctx->composite_kernel != 1 && composite_tc_eligible(*st))
+            RXGS_CUDA(launch_composite_tc(*st, ctx->signals.as<float2>(), nj, co, s));
+        else
+            RXGS_CUDA(launch_composite(*st, ctx->signals.as<float2>(), nj, co, s));
         timing_end(ctx, "composite", ev, nj);
         ctx->launches += 1;
         if (d_rssi) {

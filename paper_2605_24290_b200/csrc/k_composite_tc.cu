@@ -1,0 +1,302 @@
+// Per-tile compositing on the tensor cores (tcgen05), the query-path
+// counterpart of k_composite (k_composite.cu; render_field,
+// sphraster.cpp:255-315, with the aggregate_modality epilogues :323-381).
+//
+// For one 8x8-cell tile and a chunk of 64 receivers:
+//     D[m][cell] = sum_{pos < W} A[m][pos] * B[cell][pos]
+//     A[m][pos]  = s[list[pos]][j0 + m/2].{re, im}   (m = 2 j + re/im)   M = 128
+//     B[cell][pos] = tw[pos][cell]                                        N = 64
+// i.e. the transposed tile product with receivers on the 128 TMEM lanes.
+// Both operands are staged through shared memory in the no-swizzle
+// MN-major canonical layout (8 MN-elements x 8 K-rows core matrices), split
+// into bf16 hi/lo on the fly (D = Ahi Bhi + Ahi Blo + Alo Bhi, ~2^-17
+// relative); 32 list positions per stage, two stages in flight: the MMAs of
+// stage i (6 x tcgen05.mma M128 N64 K16, committed to the stage's mbarrier)
+// overlap the gather/convert of stage i+1.  Epilogue: tcgen05.ld, re/im lane
+// pairs exchanged with shuffles, spectrum amplitude, RSSI partial per tile,
+// optional f32 field (training forward).
+#include "rxgs_internal.cuh"
+#include "tc_util.cuh"
+
+namespace rxgs_b200 {
+namespace {
+
+constexpr int kM = 128;       // 64 receivers x {re, im}
+constexpr int kN = 64;        // cells of an 8x8 tile
+constexpr int kKS = 32;       // list positions per stage
+constexpr int kThr = 128;
+constexpr int kABytes = kKS * kM * 2;  // one bf16 operand stage (8 KB)
+constexpr int kBBytes = kKS * kN * 2;  // 4 KB
+constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;  // hi + lo of A and B (24 KB)
+// MN-major no-swizzle: core matrix = 8 K-rows x 16 B; MN groups 128 B apart
+// (SBO), K groups LBO apart.
+constexpr uint32_t kSBO = 128;
+constexpr uint32_t kALBO = (kM / 8) * 128;  // 2048
+constexpr uint32_t kBLBO = (kN / 8) * 128;  // 1024
+constexpr uint32_t kIdesc = tc::idesc_bf16_f32(kM, kN) | (1u << 15) | (1u << 16);  // A, B MN-major
+
+__device__ __forceinline__ uint32_t mn_off(int mn, int k, uint32_t lbo) {
+    return static_cast<uint32_t>((k >> 3) * lbo + (mn >> 3) * kSBO + (k & 7) * 16 + (mn & 7) * 2);
+}
+
+__device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
+    uint32_t h[4], l[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        h[q] = tc::pack_bf16(v[2 * q], v[2 * q + 1]);
+        l[q] = tc::pack_bf16(v[2 * q] - __uint_as_float(h[q] << 16), v[2 * q + 1] - __uint_as_float(h[q] & 0xFFFF0000u));
+    }
+    hi = make_uint4(h[0], h[1], h[2], h[3]);
+    lo = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+__global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t* __restrict__ tile_offsets,
+                                                       const int* __restrict__ list, const float* __restrict__ tw,
+                                                       const int* __restrict__ walk_len,
+                                                       const float2* __restrict__ sig, int n_rx,
+                                                       float* __restrict__ spectrum, float* __restrict__ rssi_partial,
+                                                       float* __restrict__ field32) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bars[2];
+    __shared__ uint32_t tbase_s;
+    __shared__ float s_dom[8];  // solid angle of the tile's 8 rows
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tile = blockIdx.x;
+    if (tid < 8) {
+        const int row = (tile / g.tiles_p) * 8 + tid;
+        s_dom[tid] = static_cast<float>(sin(g.tmin + (row + 0.5) * g.dth) * g.dth * g.dph);
+    }
+    const int j0 = blockIdx.y * (kM / 2);
+    const int W = walk_len[tile];
+    const int64_t begin = tile_offsets[tile];
+
+    if (warp == 0) {
+        tc::tmem_alloc(&tbase_s, 64);
+        tc::tmem_relinquish();
+    }
+    if (tid == 0) {
+        tc::mbar_init(&bars[0], 1);
+        tc::mbar_init(&bars[1], 1);
+        tc::fence_mbar_init();
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tm_d = tbase_s;
+    const int n_stages = (W + kKS - 1) / kKS;
+    uint32_t ph[2] = {0u, 0u};
+
+    // loader mapping: position p = tid / 4 of the stage, quarter q = tid % 4
+    const int lp = tid >> 2, lq = tid & 3;
+    for (int st = 0; st < n_stages; ++st) {
+        const int buf = st & 1;
+        uint8_t* base = smem + buf * kStageBytes;
+        uint8_t* a_hi = base;
+        uint8_t* a_lo = base + kABytes;
+        uint8_t* b_hi = base + 2 * kABytes;
+        uint8_t* b_lo = base + 2 * kABytes + kBBytes;
+        if (st >= 2) {  // the MMAs that read this buffer two stages ago must be done
+            tc::mbar_wait(&bars[buf], ph[buf]);
+            ph[buf] ^= 1u;
+        }
+        const int pos = st * kKS + lp;
+        const bool live = pos < W;
+        // ---- A: 32 m-values (16 receivers, re/im interleaved) of position pos
+        {
+            const int k = live ? list[begin + pos] : 0;
+            const float2* row = sig + static_cast<size_t>(k) * n_rx + j0 + 16 * lq;
+#pragma unroll
+            for (int gq = 0; gq < 4; ++gq) {  // 4 groups of 8 m-values = 4 receivers each
+                float v[8];
+                const int jb = j0 + 16 * lq + 4 * gq;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    float2 sv = make_float2(0.f, 0.f);
+                    if (live && jb + r < n_rx) sv = row[4 * gq + r];
+                    v[2 * r] = sv.x;
+                    v[2 * r + 1] = sv.y;
+                }
+                uint4 hi, lo;
+                split8(v, hi, lo);
+                const uint32_t off = mn_off(32 * lq + 8 * gq, lp, kALBO);
+                *reinterpret_cast<uint4*>(a_hi + off) = hi;
+                *reinterpret_cast<uint4*>(a_lo + off) = lo;
+            }
+        }
+        // ---- B: 16 cells of position pos (blend weights, zero past W)
+        {
+            const float* trow = tw + static_cast<size_t>(begin + pos) * kN + 16 * lq;
+#pragma unroll
+            for (int gq = 0; gq < 2; ++gq) {
+                float v[8];
+                if (live) {
+                    const float4 x0 = *reinterpret_cast<const float4*>(trow + 8 * gq);
+                    const float4 x1 = *reinterpret_cast<const float4*>(trow + 8 * gq + 4);
+                    v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
+                    v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) v[q] = 0.f;
+                }
+                uint4 hi, lo;
+                split8(v, hi, lo);
+                const uint32_t off = mn_off(16 * lq + 8 * gq, lp, kBLBO);
+                *reinterpret_cast<uint4*>(b_hi + off) = hi;
+                *reinterpret_cast<uint4*>(b_lo + off) = lo;
+            }
+        }
+        tc::fence_proxy_async_smem();
+        tc::fence_before_sync();
+        __syncthreads();
+        if (tid == 0) {
+            tc::fence_after_sync();
+            const uint32_t ah = tc::smem_u32(a_hi), al = tc::smem_u32(a_lo);
+            const uint32_t bh = tc::smem_u32(b_hi), bl = tc::smem_u32(b_lo);
+#pragma unroll
+            for (int ks = 0; ks < kKS / 16; ++ks) {
+                const uint64_t dah = tc::sdesc_kmajor_noswizzle(ah + 2 * kALBO * ks, kALBO, kSBO);
+                const uint64_t dal = tc::sdesc_kmajor_noswizzle(al + 2 * kALBO * ks, kALBO, kSBO);
+                const uint64_t dbh = tc::sdesc_kmajor_noswizzle(bh + 2 * kBLBO * ks, kBLBO, kSBO);
+                const uint64_t dbl = tc::sdesc_kmajor_noswizzle(bl + 2 * kBLBO * ks, kBLBO, kSBO);
+                const uint32_t acc0 = (st > 0 || ks > 0) ? 1u : 0u;
+                tc::mma_ss(tm_d, dah, dbh, kIdesc, acc0);
+                tc::mma_ss(tm_d, dah, dbl, kIdesc, 1u);
+                tc::mma_ss(tm_d, dal, dbh, kIdesc, 1u);
+            }
+            tc::mma_commit(&bars[buf]);
+        }
+    }
+    // ---- wait for the last stage(s)
+    if (n_stages >= 2) {
+        const int b2 = (n_stages - 2) & 1;
+        tc::mbar_wait(&bars[b2], ph[b2]);
+    }
+    if (n_stages >= 1) {
+        const int b1 = (n_stages - 1) & 1;
+        tc::mbar_wait(&bars[b1], ph[b1]);
+    }
+    tc::fence_after_sync();
+
+    // ---- epilogue: lane m = 32 warp + lane holds row m = 2 jl + (re|im)
+    const int m = 32 * warp + lane;
+    const int j = j0 + (m >> 1);
+    const bool is_im = m & 1;
+    const int tt = tile / g.tiles_p, tp = tile % g.tiles_p;
+    const size_t plane = static_cast<size_t>(g.nt) * g.np;
+    float pw = 0.f;
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch) {
+        uint32_t r[16];
+        if (n_stages > 0) {
+            tc::tmem_ld16(tm_d + (static_cast<uint32_t>(32 * warp) << 16) + 16 * ch, r);
+            tc::wait_ld();
+        } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) r[q] = 0u;
+        }
+        const bool mine = (ch < 2) != is_im;  // even lane: cells 0-31, odd lane: 32-63
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const float v = __uint_as_float(r[q]);
+            const float o = __shfl_xor_sync(0xffffffffu, v, 1);
+            const int cell = 16 * ch + q;
+            const int row = tt * 8 + (cell >> 3), col = tp * 8 + (cell & 7);
+            const bool valid = row < g.nt && col < g.np && j < n_rx;
+            if (field32 && valid)
+                field32[(static_cast<size_t>(j) * 2 + (is_im ? 1 : 0)) * plane + static_cast<size_t>(row) * g.np + col] = v;
+            if (mine && valid) {
+                const float re = is_im ? o : v, im = is_im ? v : o;
+                const float p2 = re * re + im * im;
+                if (spectrum)
+                    spectrum[static_cast<size_t>(j) * plane + static_cast<size_t>(row) * g.np + col] =
+                        sqrtf(p2 + static_cast<float>(kAmpEps));
+                pw += p2 * s_dom[cell >> 3];
+            }
+        }
+    }
+    pw += __shfl_xor_sync(0xffffffffu, pw, 1);
+    if (rssi_partial && !is_im && j < n_rx) rssi_partial[static_cast<size_t>(j) * g.n_tiles + tile] = pw;
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(tm_d, 64);
+}
+
+// 128x64x64 GEMM with A and B both MN-major in shared memory (the
+// composite's operand layout), small-integer data: must be exact.
+__global__ void __launch_bounds__(128) k_tc_selftest_mn(float* __restrict__ err) {
+    __shared__ __align__(1024) uint8_t sA[128 * 64 * 2];
+    __shared__ __align__(1024) uint8_t sB[64 * 64 * 2];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tb;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    auto Av = [](int m, int k) { return static_cast<float>((m + 3 * k) % 5 - 2); };
+    auto Bv = [](int n, int k) { return static_cast<float>((2 * n + k) % 7 - 3); };
+    for (int i = tid; i < 128 * 64; i += 128) {
+        const int m = i % 128, k = i / 128;
+        *reinterpret_cast<uint16_t*>(sA + mn_off(m, k, kALBO)) = static_cast<uint16_t>(tc::pack_bf16(Av(m, k), 0.f));
+    }
+    for (int i = tid; i < 64 * 64; i += 128) {
+        const int n = i % 64, k = i / 64;
+        *reinterpret_cast<uint16_t*>(sB + mn_off(n, k, kBLBO)) = static_cast<uint16_t>(tc::pack_bf16(Bv(n, k), 0.f));
+    }
+    if (warp == 0) {
+        tc::tmem_alloc(&tb, 64);
+        tc::tmem_relinquish();
+    }
+    if (tid == 0) {
+        tc::mbar_init(&bar, 1);
+        tc::fence_mbar_init();
+    }
+    tc::fence_proxy_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    if (tid == 0) {
+        for (int ks = 0; ks < 4; ++ks)
+            tc::mma_ss(tb, tc::sdesc_kmajor_noswizzle(tc::smem_u32(sA) + 2 * kALBO * ks, kALBO, kSBO),
+                       tc::sdesc_kmajor_noswizzle(tc::smem_u32(sB) + 2 * kBLBO * ks, kBLBO, kSBO), kIdesc, ks > 0);
+        tc::mma_commit(&bar);
+    }
+    tc::mbar_wait(&bar, 0);
+    tc::fence_after_sync();
+    float e = 0.f;
+    for (int c0 = 0; c0 < 64; c0 += 16) {
+        uint32_t r[16];
+        tc::tmem_ld16(tb + (static_cast<uint32_t>(32 * warp) << 16) + c0, r);
+        tc::wait_ld();
+        for (int q = 0; q < 16; ++q) {
+            float ref = 0.f;
+            for (int k = 0; k < 64; ++k) ref += Av(tid, k) * Bv(c0 + q, k);
+            e = fmaxf(e, fabsf(__uint_as_float(r[q]) - ref));
+        }
+    }
+    atomicMax(reinterpret_cast<int*>(err), __float_as_int(e));
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(tb, 64);
+}
+
+}  // namespace
+
+cudaError_t launch_tc_selftest_mn(float* d_err, cudaStream_t s) {
+    k_tc_selftest_mn<<<1, 128, 0, s>>>(d_err);
+    return cudaGetLastError();
+}
+
+bool composite_tc_eligible(const rxgs_txstate_s& st) { return st.grid.cell_blocks == 1 && st.grid.ts == 8 && st.channels == 1; }
+
+cudaError_t launch_composite_tc(const rxgs_txstate_s& st, const float2* d_sig, int n_rx, const CompositeOut& out,
+                                cudaStream_t s) {
+    const DevGrid& g = st.grid;
+    const size_t smem = 2 * kStageBytes;
+    cudaError_t e = cudaFuncSetAttribute(k_composite_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    dim3 grid(g.n_tiles, (n_rx + kM / 2 - 1) / (kM / 2));
+    k_composite_tc<<<grid, kThr, smem, s>>>(g, st.tile_offsets.as<int64_t>(), st.list.as<int>(), st.tw.as<float>(),
+                                            st.walk_len.as<int>(), d_sig, n_rx, out.spectrum, out.rssi_partial,
+                                            out.field32);
+    return cudaGetLastError();
+}
+
+}  // namespace rxgs_b200

@@ -100,6 +100,7 @@ struct rxgs_ctx_s {
         err_flag, host_in, host_out;
     int sm_count = 148;
     int cond_kernel = 0;  // 0 auto (tcgen05 when eligible), 1 force SIMT
+    int composite_kernel = 0;  // 0 auto (tcgen05 when eligible), 1 force SIMT
     int refs = 0;         // live handles on this context
     cudaStream_t copy_stream = nullptr;  // D2H of finished receiver chunks (host outputs)
     std::vector<cudaEvent_t> chunk_events;
@@ -201,6 +202,7 @@ cudaError_t launch_cond_signal_tc(const rxgs_cond_s& c, const rxgs_scene_s& sc, 
                                   const double* d_rx, int n_rx, const float* d_ag, float2* d_sig,
                                   cudaStream_t s);
 cudaError_t launch_tc_selftest(float* d_err, cudaStream_t s);
+cudaError_t launch_tc_selftest_mn(float* d_err, cudaStream_t s);
 // reduce_signals from materialised f64 coefficients.
 cudaError_t launch_reduce_signals(const rxgs_txstate_s& st, const double* d_coeffs, int n_rx,
                                   float2* d_sig, int* d_err, cudaStream_t s);
@@ -215,6 +217,10 @@ struct CompositeOut {
 };
 cudaError_t launch_composite(const rxgs_txstate_s& st, const float2* d_sig, int n_rx,
                              const CompositeOut& out, cudaStream_t s);
+// tcgen05 compositing (k_composite_tc.cu): 8x8 tiles, C == 1.
+bool composite_tc_eligible(const rxgs_txstate_s& st);
+cudaError_t launch_composite_tc(const rxgs_txstate_s& st, const float2* d_sig, int n_rx, const CompositeOut& out,
+                                cudaStream_t s);
 cudaError_t launch_rssi_finalize(const float* d_partial, int n_tiles, int n_rx, float* d_rssi,
                                  double* d_rssi64, cudaStream_t s);
 cudaError_t launch_aggregate(const DevGrid& g, int modality, int n_rx, int channels,

@@ -204,7 +204,7 @@ def test_predict_api(ctx, capi, orc):
 def test_tcgen05_selftest(ctx):
     """128x64x64 bf16 GEMM with A in TMEM and in smem vs FP32 FMA of the same values."""
     e = ctx.selftest_tcgen05()
-    assert e[2] == 0.0 and e[3] == 0.0, e  # exact data: layouts and descriptors
+    assert e[2] == 0.0 and e[3] == 0.0 and e[4] == 0.0, e  # exact data: layouts and descriptors
     assert e[0] < 1e-2 and e[1] < 1e-2, e  # smooth data: tensor-core accumulation
 
 
@@ -242,3 +242,24 @@ def test_reference_api_shim_cpp(capi, tmp_path):
                            "-Wl,-rpath," + libdir, "-o", exe])
     out = subprocess.run([exe], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
+
+
+def test_tcgen05_composite_matches_simt_and_oracle(ctx, capi, orc):
+    """The tensor-core compositor and the SIMT compositor agree; both match the oracle."""
+    import oracle as O
+    sc = capi.synth_scene(8000, 2, 1, 21)
+    scene, cond, oscene, ocond = _setup_cond(capi, ctx, orc, sc)
+    grid = capi.Grid(45, 90, 8, 1.0)
+    st = scene.tx_state(TX, grid)
+    rx = capi.synth_points(100, 29, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])  # two 64-receiver chunks, ragged
+    s_tc, r_tc = scene.render_queries(cond, st, rx)
+    ctx.set_composite_kernel("simt")
+    try:
+        s_si, r_si = scene.render_queries(cond, st, rx)
+    finally:
+        ctx.set_composite_kernel("auto")
+    assert rel_err(s_tc, s_si).max() < TOL and rel_err(r_tc, r_si).max() < TOL
+    og = O.Grid(45, 90, 8, 1.0)
+    for j in (0, 63, 64, 99):
+        want = orc.predict(oscene, ocond, og, TX, rx[j], "spectrum").reshape(45, 90)
+        assert rel_err(s_tc[j], want).max() < TOL
