@@ -39,17 +39,6 @@ __device__ __forceinline__ uint32_t mn_off(int mn, int k, uint32_t lbo) {
     return static_cast<uint32_t>((k >> 3) * lbo + (mn >> 3) * kSBO + (k & 7) * 16 + (mn & 7) * 2);
 }
 
-__device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
-    uint32_t h[4], l[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        h[q] = tc::pack_bf16(v[2 * q], v[2 * q + 1]);
-        l[q] = tc::pack_bf16(v[2 * q] - __uint_as_float(h[q] << 16), v[2 * q + 1] - __uint_as_float(h[q] & 0xFFFF0000u));
-    }
-    hi = make_uint4(h[0], h[1], h[2], h[3]);
-    lo = make_uint4(l[0], l[1], l[2], l[3]);
-}
-
 __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t* __restrict__ tile_offsets,
                                                        const int* __restrict__ list, const float* __restrict__ tw,
                                                        const int* __restrict__ walk_len,
@@ -86,8 +75,45 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
     const int n_stages = (W + kKS - 1) / kKS;
     uint32_t ph[2] = {0u, 0u};
 
-    // loader mapping: position p = tid / 4 of the stage, quarter q = tid % 4
-    const int lp = tid >> 2, lq = tid & 3;
+    // Loader: warp w stages list positions 8w .. 8w+7 of a stage.  A: one
+    // coalesced 512 B row (64 receivers, complex) per position, lane l holding
+    // receivers j0+2l, j0+2l+1 (= m-values 4l..4l+3); B: one 256 B blend-weight
+    // row per half-warp (lane holds cells 4(l%16)..+3).  Loads for stage s+1
+    // are issued before stage s's barrier/MMA so their latency is hidden.
+    float4 ra[8], rb[4];
+    const bool even_n = (n_rx & 1) == 0;
+    auto load = [&](int st) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int pos = st * kKS + 8 * warp + i;
+            ra[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (pos < W) {
+                const int k = list[begin + pos];
+                const int jj = j0 + 2 * lane;
+                const float2* rowp = sig + static_cast<size_t>(k) * n_rx + jj;
+                if (even_n && jj + 1 < n_rx) {
+                    ra[i] = *reinterpret_cast<const float4*>(rowp);
+                } else {
+                    const float2 a = jj < n_rx ? rowp[0] : make_float2(0.f, 0.f);
+                    const float2 b = jj + 1 < n_rx ? rowp[1] : make_float2(0.f, 0.f);
+                    ra[i] = make_float4(a.x, a.y, b.x, b.y);
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int pos = st * kKS + 8 * warp + 2 * i + (lane >> 4);
+            rb[i] = pos < W ? *reinterpret_cast<const float4*>(tw + static_cast<size_t>(begin + pos) * kN + 4 * (lane & 15))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+    auto split4 = [](float4 v, uint2& hi, uint2& lo) {
+        hi.x = tc::pack_bf16(v.x, v.y);
+        hi.y = tc::pack_bf16(v.z, v.w);
+        lo.x = tc::pack_bf16(v.x - __uint_as_float(hi.x << 16), v.y - __uint_as_float(hi.x & 0xFFFF0000u));
+        lo.y = tc::pack_bf16(v.z - __uint_as_float(hi.y << 16), v.w - __uint_as_float(hi.y & 0xFFFF0000u));
+    };
+    if (n_stages > 0) load(0);
     for (int st = 0; st < n_stages; ++st) {
         const int buf = st & 1;
         uint8_t* base = smem + buf * kStageBytes;
@@ -99,52 +125,23 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
             tc::mbar_wait(&bars[buf], ph[buf]);
             ph[buf] ^= 1u;
         }
-        const int pos = st * kKS + lp;
-        const bool live = pos < W;
-        // ---- A: 32 m-values (16 receivers, re/im interleaved) of position pos
-        {
-            const int k = live ? list[begin + pos] : 0;
-            const float2* row = sig + static_cast<size_t>(k) * n_rx + j0 + 16 * lq;
 #pragma unroll
-            for (int gq = 0; gq < 4; ++gq) {  // 4 groups of 8 m-values = 4 receivers each
-                float v[8];
-                const int jb = j0 + 16 * lq + 4 * gq;
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    float2 sv = make_float2(0.f, 0.f);
-                    if (live && jb + r < n_rx) sv = row[4 * gq + r];
-                    v[2 * r] = sv.x;
-                    v[2 * r + 1] = sv.y;
-                }
-                uint4 hi, lo;
-                split8(v, hi, lo);
-                const uint32_t off = mn_off(32 * lq + 8 * gq, lp, kALBO);
-                *reinterpret_cast<uint4*>(a_hi + off) = hi;
-                *reinterpret_cast<uint4*>(a_lo + off) = lo;
-            }
+        for (int i = 0; i < 8; ++i) {
+            uint2 hi, lo;
+            split4(ra[i], hi, lo);
+            const uint32_t off = mn_off(4 * lane, 8 * warp + i, kALBO);
+            *reinterpret_cast<uint2*>(a_hi + off) = hi;
+            *reinterpret_cast<uint2*>(a_lo + off) = lo;
         }
-        // ---- B: 16 cells of position pos (blend weights, zero past W)
-        {
-            const float* trow = tw + static_cast<size_t>(begin + pos) * kN + 16 * lq;
 #pragma unroll
-            for (int gq = 0; gq < 2; ++gq) {
-                float v[8];
-                if (live) {
-                    const float4 x0 = *reinterpret_cast<const float4*>(trow + 8 * gq);
-                    const float4 x1 = *reinterpret_cast<const float4*>(trow + 8 * gq + 4);
-                    v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
-                    v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) v[q] = 0.f;
-                }
-                uint4 hi, lo;
-                split8(v, hi, lo);
-                const uint32_t off = mn_off(16 * lq + 8 * gq, lp, kBLBO);
-                *reinterpret_cast<uint4*>(b_hi + off) = hi;
-                *reinterpret_cast<uint4*>(b_lo + off) = lo;
-            }
+        for (int i = 0; i < 4; ++i) {
+            uint2 hi, lo;
+            split4(rb[i], hi, lo);
+            const uint32_t off = mn_off(4 * (lane & 15), 8 * warp + 2 * i + (lane >> 4), kBLBO);
+            *reinterpret_cast<uint2*>(b_hi + off) = hi;
+            *reinterpret_cast<uint2*>(b_lo + off) = lo;
         }
+        if (st + 1 < n_stages) load(st + 1);
         tc::fence_proxy_async_smem();
         tc::fence_before_sync();
         __syncthreads();
