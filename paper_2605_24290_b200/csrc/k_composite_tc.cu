@@ -82,13 +82,19 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
     // are issued before stage s's barrier/MMA so their latency is hidden.
     float4 ra[8], rb[4];
     const bool even_n = (n_rx & 1) == 0;
+    // list indices of a whole stage in one coalesced load (lane i <-> position i)
+    auto load_idx = [&](int st) {
+        const int pos = st * kKS + lane;
+        return pos < W ? list[begin + pos] : 0;
+    };
+    int kidx = n_stages > 0 ? load_idx(0) : 0;
     auto load = [&](int st) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const int pos = st * kKS + 8 * warp + i;
+            const int k = __shfl_sync(0xffffffffu, kidx, 8 * warp + i);
             ra[i] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (pos < W) {
-                const int k = list[begin + pos];
                 const int jj = j0 + 2 * lane;
                 const float2* rowp = sig + static_cast<size_t>(k) * n_rx + jj;
                 if (even_n && jj + 1 < n_rx) {
@@ -106,6 +112,7 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
             rb[i] = pos < W ? *reinterpret_cast<const float4*>(tw + static_cast<size_t>(begin + pos) * kN + 4 * (lane & 15))
                             : make_float4(0.f, 0.f, 0.f, 0.f);
         }
+        kidx = st + 1 < n_stages ? load_idx(st + 1) : 0;  // next stage's indices, one stage early
     };
     auto split4 = [](float4 v, uint2& hi, uint2& lo) {
         hi.x = tc::pack_bf16(v.x, v.y);
@@ -176,10 +183,12 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
 
     // ---- epilogue: lane m = 32 warp + lane holds row m = 2 jl + (re|im)
     const int m = 32 * warp + lane;
-    const int j = j0 + (m >> 1);
+    const int jl = m >> 1;
+    const int j = j0 + jl;
     const bool is_im = m & 1;
     const int tt = tile / g.tiles_p, tp = tile % g.tiles_p;
     const size_t plane = static_cast<size_t>(g.nt) * g.np;
+    float* s_amp = reinterpret_cast<float*>(smem);  // [64 receivers][64 cells] (stage buffers are free now)
     float pw = 0.f;
 #pragma unroll
     for (int ch = 0; ch < 4; ++ch) {
@@ -198,21 +207,35 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
             const float o = __shfl_xor_sync(0xffffffffu, v, 1);
             const int cell = 16 * ch + q;
             const int row = tt * 8 + (cell >> 3), col = tp * 8 + (cell & 7);
-            const bool valid = row < g.nt && col < g.np && j < n_rx;
-            if (field32 && valid)
+            if (field32 && row < g.nt && col < g.np && j < n_rx)
                 field32[(static_cast<size_t>(j) * 2 + (is_im ? 1 : 0)) * plane + static_cast<size_t>(row) * g.np + col] = v;
-            if (mine && valid) {
+            if (mine) {
                 const float re = is_im ? o : v, im = is_im ? v : o;
                 const float p2 = re * re + im * im;
-                if (spectrum)
-                    spectrum[static_cast<size_t>(j) * plane + static_cast<size_t>(row) * g.np + col] =
-                        sqrtf(p2 + static_cast<float>(kAmpEps));
-                pw += p2 * s_dom[cell >> 3];
+                s_amp[jl * 64 + cell] = sqrtf(p2 + static_cast<float>(kAmpEps));
+                if (row < g.nt) pw += p2 * s_dom[cell >> 3];
             }
         }
     }
     pw += __shfl_xor_sync(0xffffffffu, pw, 1);
     if (rssi_partial && !is_im && j < n_rx) rssi_partial[static_cast<size_t>(j) * g.n_tiles + tile] = pw;
+    if (spectrum) {
+        __syncthreads();
+        // 64 receivers x 8 tile rows = 512 row segments of 8 cells (32 B)
+        for (int sgm = tid; sgm < 64 * 8; sgm += kThr) {
+            const int r8 = sgm & 7, jr = sgm >> 3;
+            const int jg = j0 + jr, row = tt * 8 + r8, col0 = tp * 8;
+            if (jg >= n_rx || row >= g.nt) continue;
+            const float* src = s_amp + jr * 64 + r8 * 8;
+            float* dst = spectrum + static_cast<size_t>(jg) * plane + static_cast<size_t>(row) * g.np + col0;
+            if (col0 + 8 <= g.np && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(src);
+                *reinterpret_cast<float4*>(dst + 4) = *reinterpret_cast<const float4*>(src + 4);
+            } else {
+                for (int c = 0; c < 8 && col0 + c < g.np; ++c) dst[c] = src[c];
+            }
+        }
+    }
     tc::fence_before_sync();
     __syncthreads();
     if (warp == 0) tc::tmem_dealloc(tm_d, 64);
