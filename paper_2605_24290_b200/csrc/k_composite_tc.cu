@@ -25,14 +25,16 @@ constexpr int kM = 128;       // 64 receivers x {re, im}
 constexpr int kN = 64;        // cells of an 8x8 tile
 constexpr int kKS = 32;       // list positions per stage
 constexpr int kThr = 128;
-constexpr int kABytes = kKS * kM * 2;  // one bf16 operand stage (8 KB)
-constexpr int kBBytes = kKS * kN * 2;  // 4 KB
+constexpr int kABytes = (kKS / 8) * (kM / 8) * 144;  // one bf16 operand stage (9 KB with SBO padding)
+constexpr int kBBytes = (kKS / 8) * (kN / 8) * 144;  // 4.5 KB
 constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;  // hi + lo of A and B (24 KB)
-// MN-major no-swizzle: core matrix = 8 K-rows x 16 B; MN groups 128 B apart
-// (SBO), K groups LBO apart.
-constexpr uint32_t kSBO = 128;
-constexpr uint32_t kALBO = (kM / 8) * 128;  // 2048
-constexpr uint32_t kBLBO = (kN / 8) * 128;  // 1024
+// MN-major no-swizzle: core matrix = 8 K-rows x 16 B (128 B contiguous);
+// MN groups SBO apart, K groups LBO apart.  SBO = 144 B (not 128): the 16 B
+// stores of one K-row across MN groups then spread over all 32 banks
+// (2 wavefronts per warp instead of a 16-way conflict).
+constexpr uint32_t kSBO = 144;
+constexpr uint32_t kALBO = (kM / 8) * kSBO;  // 2304
+constexpr uint32_t kBLBO = (kN / 8) * kSBO;  // 1152
 constexpr uint32_t kIdesc = tc::idesc_bf16_f32(kM, kN) | (1u << 15) | (1u << 16);  // A, B MN-major
 
 __device__ __forceinline__ uint32_t mn_off(int mn, int k, uint32_t lbo) {
@@ -188,7 +190,8 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
     const bool is_im = m & 1;
     const int tt = tile / g.tiles_p, tp = tile % g.tiles_p;
     const size_t plane = static_cast<size_t>(g.nt) * g.np;
-    float* s_amp = reinterpret_cast<float*>(smem);  // [64 receivers][64 cells] (stage buffers are free now)
+    float* s_amp = reinterpret_cast<float*>(smem);  // [64 receivers][68] (stage buffers are free now)
+    constexpr int kAmpStride = 68;                  // 16 B aligned rows, bank-spread
     float pw = 0.f;
 #pragma unroll
     for (int ch = 0; ch < 4; ++ch) {
@@ -212,7 +215,7 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
             if (mine) {
                 const float re = is_im ? o : v, im = is_im ? v : o;
                 const float p2 = re * re + im * im;
-                s_amp[jl * 64 + cell] = sqrtf(p2 + static_cast<float>(kAmpEps));
+                s_amp[jl * kAmpStride + cell] = sqrtf(p2 + static_cast<float>(kAmpEps));
                 if (row < g.nt) pw += p2 * s_dom[cell >> 3];
             }
         }
@@ -226,7 +229,7 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
             const int r8 = sgm & 7, jr = sgm >> 3;
             const int jg = j0 + jr, row = tt * 8 + r8, col0 = tp * 8;
             if (jg >= n_rx || row >= g.nt) continue;
-            const float* src = s_amp + jr * 64 + r8 * 8;
+            const float* src = s_amp + jr * kAmpStride + r8 * 8;
             float* dst = spectrum + static_cast<size_t>(jg) * plane + static_cast<size_t>(row) * g.np + col0;
             if (col0 + 8 <= g.np && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
                 *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(src);
@@ -244,8 +247,8 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
 // 128x64x64 GEMM with A and B both MN-major in shared memory (the
 // composite's operand layout), small-integer data: must be exact.
 __global__ void __launch_bounds__(128) k_tc_selftest_mn(float* __restrict__ err) {
-    __shared__ __align__(1024) uint8_t sA[128 * 64 * 2];
-    __shared__ __align__(1024) uint8_t sB[64 * 64 * 2];
+    __shared__ __align__(1024) uint8_t sA[8 * (128 / 8) * 144];
+    __shared__ __align__(1024) uint8_t sB[8 * (64 / 8) * 144];
     __shared__ uint64_t bar;
     __shared__ uint32_t tb;
     const int tid = threadIdx.x, warp = tid >> 5;
