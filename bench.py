@@ -281,12 +281,16 @@ def run_b200(args):
         pk = json.load(open(peaks_path))
         peak, peak_src = float(pk.get("bf16_tflops", 1590.0)), "measured bf16_tflops (MEASURED_PEAKS.json)"
     roofline = None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r1_traffic.json")
+    if os.path.exists(tpath):  # dram bytes of the same kernel from the committed ncu --set full capture
+        traffic = json.load(open(tpath)).get("k_cond_tc", {}).get("dram_bytes_per_launch")
     if cond_n:
         per_launch_rows = cond_rows / cond_n
         avg_ms = cond_ms / cond_n
         achieved = flop_row * per_launch_rows / (avg_ms / 1e3) / 1e12
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak, "traffic": None,
+                    "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per launch (profiles/r1_traffic.json)",
                     "kernel": "k_cond_tc (probe + local MLP on tcgen05 + FLE reduction)",
                     "pipe": "tcgen05 bf16x3 (hidden layer) + FP32 SIMT (probe, layers 1/3, FLE)", "peak_source": peak_src,
                     "flop_per_row": flop_row, "rows_per_launch": per_launch_rows,
