@@ -147,6 +147,22 @@ int rxgs_render_field(rxgs_ctx ctx, rxgs_txstate st, rxgs_scene scene, const dou
 int rxgs_aggregate_modality(rxgs_ctx ctx, const rxgs_grid* grid, int modality, int n_rx,
                             int channels, const double* values, double* out);
 
+/* raster::aggregate_modality_backward (sphraster.cpp:383-449).  upstream has
+ * rxgs_aggregate_modality's out layout; d_values the field layout
+ * (n_rx*C*2*H*W f64).  Scalar modalities need channels == 1. */
+int rxgs_aggregate_modality_backward(rxgs_ctx ctx, const rxgs_grid* grid, int modality, int n_rx,
+                                     int channels, const double* values, const double* upstream,
+                                     double* d_values);
+
+/* raster::backward_render (sphraster.cpp:509-733): exact FP64 adjoint of
+ * rxgs_render_field.  d_values: n_rx*C*2*H*W; outputs (GradientBundle,
+ * sphraster.hpp): d_positions K*3, d_log_scales K*3, d_quaternions K*4,
+ * d_tau_logits K, d_coeffs n_rx*K*L*C*2.  Any output may be NULL. */
+int rxgs_backward_render(rxgs_ctx ctx, rxgs_txstate st, rxgs_scene scene, const double* coeffs,
+                         int n_rx, const double* d_values, double* d_positions,
+                         double* d_log_scales, double* d_quaternions, double* d_tau_logits,
+                         double* d_coeffs);
+
 /* ------------------------------------------------------------ conditioning
  * cond::ConditioningState (conditioning.hpp:72-92).  cfg = {F, hidden, d_c,
  * S, R, nearest_lookup, mode, l_max, C}; params packed as

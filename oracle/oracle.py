@@ -296,6 +296,33 @@ class Checker:
             raise CheckerError(err.value.decode())
         return out
 
+    def aggregate_backward(self, values, grid: Grid, modality, upstream):
+        """raster::aggregate_modality_backward (sphraster.cpp:383-449); reference only."""
+        values = np.ascontiguousarray(values, np.float64)
+        n_rx, C_ = values.shape[0], values.shape[1]
+        out = np.empty_like(values)
+        self._aggregate_backward(n_rx, C_, grid.gi, grid.gd, _d(values), MODALITY[modality],
+                                 _d(np.ascontiguousarray(upstream, np.float64)), out.ctypes.data_as(_dp))
+        return out
+
+    def backward_render(self, tx_h, scene_h, coeffs, n_rx, d_values, threads=1):
+        """raster::backward_render (sphraster.cpp:509-733); reference only.
+        Returns the GradientBundle as a dict."""
+        sc = scene_h.data
+        k = len(sc["tau_logits"])
+        co = np.ascontiguousarray(coeffs, np.float64)
+        dv = np.ascontiguousarray(d_values, np.float64)
+        out = dict(d_positions=np.empty((k, 3)), d_log_scales=np.empty((k, 3)), d_quaternions=np.empty((k, 4)),
+                   d_tau_logits=np.empty(k), d_coeffs=np.empty(co.shape))
+        err = C.create_string_buffer(512)
+        rc = self._backward_render(tx_h.ptr, scene_h.ptr, _d(co), co.size, n_rx, _d(dv), dv.size, threads,
+                                   *(out[n].ctypes.data_as(_dp) for n in ("d_positions", "d_log_scales",
+                                                                          "d_quaternions", "d_tau_logits",
+                                                                          "d_coeffs")), err, 512)
+        if rc:
+            raise CheckerError(err.value.decode())
+        return out
+
     # ------------------------------------------------------------ reference-only extras
     def bench_queries(self, scene_h, cond_h, grid: Grid, tx, rx, threads, want_outputs=False):
         rx = np.ascontiguousarray(rx, np.float64)

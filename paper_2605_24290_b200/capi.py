@@ -92,6 +92,9 @@ _SIG = {
                                     C.POINTER(_i64)]),
     "rxgs_render_field": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int, _vp, _vp]),
     "rxgs_aggregate_modality": (C.c_int, [_vp, C.POINTER(Grid), C.c_int, C.c_int, C.c_int, _vp, _vp]),
+    "rxgs_aggregate_modality_backward": (C.c_int, [_vp, C.POINTER(Grid), C.c_int, C.c_int, C.c_int, _vp, _vp,
+                                                   _vp]),
+    "rxgs_backward_render": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]),
     "rxgs_cond_create": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(_vp)]),
     "rxgs_cond_destroy": (C.c_int, [_vp]),
     "rxgs_cond_param_count": (_i64, [_vp]),
@@ -274,6 +277,16 @@ class Context:
         return out
 
 
+    def aggregate_backward(self, values, grid: Grid, modality, upstream):
+        """raster::aggregate_modality_backward (sphraster.cpp:383-449)."""
+        values = np.ascontiguousarray(values, np.float64)
+        n_rx, ch = values.shape[0], values.shape[1]
+        out = _out(values.shape)
+        _check(_lib.rxgs_aggregate_modality_backward(self.h, C.byref(grid), MODALITY[modality], n_rx, ch,
+                                                     values.ctypes.data, ptr(upstream, np.float64),
+                                                     out.ctypes.data))
+        return out
+
 class Scene:
     """GaussianScene upload (scene.hpp:19-48)."""
 
@@ -313,6 +326,17 @@ class Scene:
         _check(_lib.rxgs_render_field(self.ctx.h, st.h, self.h, ptr(coeffs, np.float64), n_rx, ptr(values),
                                       ptr(transmittance)))
         return values, transmittance
+
+    def backward_render(self, st, coeffs, n_rx, d_values):
+        """raster::backward_render (sphraster.cpp:509-733) -> GradientBundle dict."""
+        co = np.ascontiguousarray(coeffs, np.float64)
+        out = dict(d_positions=_out((self.k, 3)), d_log_scales=_out((self.k, 3)), d_quaternions=_out((self.k, 4)),
+                   d_tau_logits=_out(self.k), d_coeffs=_out(co.shape))
+        _check(_lib.rxgs_backward_render(self.ctx.h, st.h, self.h, co.ctypes.data, n_rx, ptr(d_values, np.float64),
+                                         *(out[n].ctypes.data for n in ("d_positions", "d_log_scales",
+                                                                        "d_quaternions", "d_tau_logits",
+                                                                        "d_coeffs"))))
+        return out
 
     def render_queries(self, cond, st, rx, spectrum=None, rssi=None, want=("spectrum", "rssi")):
         """Fused batched query path; numpy in -> numpy out unless torch tensors are passed."""

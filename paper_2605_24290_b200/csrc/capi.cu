@@ -810,6 +810,108 @@ int rxgs_aggregate_modality(rxgs_ctx ctx, const rxgs_grid* grid, int modality, i
     API_END
 }
 
+// ------------------------------------------------------------------ adjoints (sphraster.cpp:383-733)
+int rxgs_aggregate_modality_backward(rxgs_ctx ctx, const rxgs_grid* grid, int modality, int n_rx, int channels,
+                                     const double* values, const double* upstream, double* d_values) {
+    API_BEGIN
+    if (!ctx || !grid || !values || !upstream || !d_values)
+        return fail(RXGS_ERR_INVALID, "aggregate_modality_backward: null argument");
+    if (n_rx < 0 || channels < 1 || modality < 0 || modality > 2)
+        return fail(RXGS_ERR_INVALID, "aggregate_modality_backward: bad arguments");
+    if (modality != 1 && channels != 1)
+        return fail(RXGS_ERR_INVALID, "aggregate_modality_backward: scalar modalities need channels == 1");
+    RX_TRY(set_device(ctx));
+    const DevGrid g = make_grid(grid);
+    const size_t plane = static_cast<size_t>(g.nt) * g.np;
+    const size_t nv = static_cast<size_t>(n_rx) * channels * 2 * plane;
+    const size_t nu = modality == 0 ? n_rx : (modality == 1 ? static_cast<size_t>(n_rx) * channels * 2 : n_rx * plane);
+    DevBuf tv, tu, to;
+    const double* d_v = nullptr;
+    const double* d_u = nullptr;
+    double* d_o = nullptr;
+    RX_TRY(dev_in(ctx, values, nv, tv, &d_v));
+    RX_TRY(dev_in(ctx, upstream, nu, tu, &d_u));
+    RX_TRY(dev_out(d_values, nv, to, &d_o));
+    RXGS_CUDA(launch_aggregate_bwd(g, modality, n_rx, channels, d_v, d_u, d_o, ctx->stream));
+    ctx->launches += 1;
+    RX_TRY(finish_out(ctx, d_values, d_o, nv));
+    RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RXGS_OK;
+    API_END
+}
+
+int rxgs_backward_render(rxgs_ctx ctx, rxgs_txstate st, rxgs_scene sc, const double* coeffs, int n_rx,
+                         const double* d_values, double* d_positions, double* d_log_scales, double* d_quaternions,
+                         double* d_tau_logits, double* d_coeffs) {
+    API_BEGIN
+    if (!ctx || !st || !sc || !coeffs || !d_values)
+        return fail(RXGS_ERR_INVALID, "backward_render: null argument");
+    if (n_rx < 1) return fail(RXGS_ERR_INVALID, "backward_render: n_rx must be >= 1");
+    if (sc->k != st->k || sc->channels != st->channels || sc->L != st->L)
+        return fail(RXGS_ERR_INVALID, "render_field: coefficient tensor has wrong size");
+    RX_TRY(set_device(ctx));
+    cudaStream_t s = ctx->stream;
+    const int K = sc->k, C = sc->channels;
+    const size_t stride = static_cast<size_t>(sc->L) * C * 2;
+    const size_t nco = static_cast<size_t>(n_rx) * K * stride;
+    const size_t plane = static_cast<size_t>(st->grid.nt) * st->grid.np;
+    const size_t nv = static_cast<size_t>(n_rx) * C * 2 * plane;
+    const size_t n_jc = static_cast<size_t>(n_rx) * C;
+    DevBuf t_co, t_dv, b_sig, b_eg, b_eds, b_rg, b_rds, o_pos, o_ls, o_q, o_tau, o_co;
+    const double* d_co = nullptr;
+    const double* d_dv = nullptr;
+    RX_TRY(dev_in(ctx, coeffs, nco, t_co, &d_co));
+    RX_TRY(dev_in(ctx, d_values, nv, t_dv, &d_dv));
+    // non-finite coefficients are rejected exactly as the forward does (sphraster.cpp:197-206)
+    RXGS_CUDA(ctx->signals.ensure(std::max<size_t>(static_cast<size_t>(K) * n_jc, 1) * sizeof(float2)));
+    RX_TRY(reset_err_flag(ctx));
+    if (nco) {
+        RXGS_CUDA(launch_reduce_signals(*st, d_co, n_rx, ctx->signals.as<float2>(), ctx->err_flag.as<int>(), s));
+        ctx->launches += 2;
+    }
+    int err = INT_MAX;
+    RX_TRY(check_err_flag(ctx, ctx->err_flag.as<int>(), &err));
+    if (err != INT_MAX) {
+        const int j = err / std::max(K, 1), k = err % std::max(K, 1);
+        return fail(RXGS_ERR_INVALID, "render_field: non-finite coefficient at rx " + std::to_string(j) +
+                                          ", gaussian " + std::to_string(k));
+    }
+    if (!st->regrouped) RX_TRY(train_regroup(ctx, *st, s));
+    const size_t E = std::max<int64_t>(st->entries, 1);
+    RXGS_CUDA(b_sig.ensure(std::max<size_t>(K * n_jc, 1) * sizeof(double2)));
+    RXGS_CUDA(b_eg.ensure(E * 7 * sizeof(double)));
+    RXGS_CUDA(b_eds.ensure(E * n_jc * sizeof(double2)));
+    RXGS_CUDA(b_rg.ensure(std::max<size_t>(K, 1) * 7 * sizeof(double)));
+    RXGS_CUDA(b_rds.ensure(std::max<size_t>(K * n_jc, 1) * sizeof(double2)));
+    double *dp = nullptr, *dl = nullptr, *dq = nullptr, *dt = nullptr, *dc = nullptr;
+    RX_TRY(dev_out(d_positions, 3 * static_cast<size_t>(K), o_pos, &dp));
+    RX_TRY(dev_out(d_log_scales, 3 * static_cast<size_t>(K), o_ls, &dl));
+    RX_TRY(dev_out(d_quaternions, 4 * static_cast<size_t>(K), o_q, &dq));
+    RX_TRY(dev_out(d_tau_logits, static_cast<size_t>(K), o_tau, &dt));
+    RX_TRY(dev_out(d_coeffs, nco, o_co, &dc));
+    // every output is produced; absent ones land in scratch
+    if (!dp) { RXGS_CUDA(o_pos.ensure(std::max<size_t>(3 * K, 1) * sizeof(double))); dp = o_pos.as<double>(); }
+    if (!dl) { RXGS_CUDA(o_ls.ensure(std::max<size_t>(3 * K, 1) * sizeof(double))); dl = o_ls.as<double>(); }
+    if (!dq) { RXGS_CUDA(o_q.ensure(std::max<size_t>(4 * K, 1) * sizeof(double))); dq = o_q.as<double>(); }
+    if (!dt) { RXGS_CUDA(o_tau.ensure(std::max<size_t>(K, 1) * sizeof(double))); dt = o_tau.as<double>(); }
+    if (!dc) { RXGS_CUDA(o_co.ensure(std::max<size_t>(nco, 1) * sizeof(double))); dc = o_co.as<double>(); }
+    cudaEvent_t ev;
+    timing_begin(ctx, "backward_render", &ev);
+    RXGS_CUDA(launch_backward_render(*st, *sc, d_co, n_rx, d_dv, b_sig.as<double2>(), b_eg.as<double>(),
+                                     b_eds.as<double2>(), b_rg.as<double>(), b_rds.as<double2>(), dp, dl, dq, dt, dc,
+                                     s));
+    timing_end(ctx, "backward_render", ev, static_cast<double>(n_rx));
+    ctx->launches += 3 + st->grid.cell_blocks * static_cast<int64_t>((n_jc + 7) / 8);
+    RX_TRY(finish_out(ctx, d_positions, dp, 3 * static_cast<size_t>(K)));
+    RX_TRY(finish_out(ctx, d_log_scales, dl, 3 * static_cast<size_t>(K)));
+    RX_TRY(finish_out(ctx, d_quaternions, dq, 4 * static_cast<size_t>(K)));
+    RX_TRY(finish_out(ctx, d_tau_logits, dt, static_cast<size_t>(K)));
+    RX_TRY(finish_out(ctx, d_coeffs, dc, nco));
+    RXGS_CUDA(cudaStreamSynchronize(s));
+    return RXGS_OK;
+    API_END
+}
+
 // ------------------------------------------------------------------ conditioning
 int rxgs_cond_create(rxgs_ctx ctx, const int32_t cfg[9], const double* params, const double* occ,
                      const double occ_lo[3], const double occ_hi[3], rxgs_cond* out) {

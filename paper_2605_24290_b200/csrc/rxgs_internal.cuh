@@ -231,6 +231,14 @@ cudaError_t launch_fill_transmittance(const rxgs_txstate_s& st, int n_rx, double
 
 // ---- k_train.cu
 int train_regroup(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s);
+// ---- k_backward.cu (FP64 adjoints of the materialised API)
+cudaError_t launch_aggregate_bwd(const DevGrid& g, int modality, int n_rx, int channels, const double* values,
+                                 const double* up, double* dv, cudaStream_t s);
+cudaError_t launch_backward_render(const rxgs_txstate_s& st, const rxgs_scene_s& sc, const double* d_coeffs_in,
+                                   int n_rx, const double* d_values, double2* sig64, double* ent_geo,
+                                   double2* ent_ds, double* raw_geo, double2* raw_ds, double* d_pos, double* d_ls,
+                                   double* d_q, double* d_tau, double* d_coeffs, cudaStream_t s);
+
 cudaError_t launch_refresh_gb(const rxgs_scene_s& sc, rxgs_txstate_s& st, cudaStream_t s);
 cudaError_t launch_loss_spectrum(int n_rx, int P, const float* field, const float* target, double l_weight,
                                  float2* G, double* loss_part, double* loss, cudaStream_t s);

@@ -150,3 +150,49 @@ def test_single_gaussian_render_closed_form(orc):
             assert abs(vals[0, 0, 0, row, col] - w * s.real) < 1e-14
             assert abs(T[0, row, col] - (1 - w)) < 1e-14
             del covered
+
+
+def test_reference_adjoints_match_finite_differences(orc, ref):
+    """Pins the adjoint wrappers (oracle/_ref) that the GPU backward tests
+    compare against: d_coeffs is exact (render is linear in the
+    coefficients); d_tau_logits / d_positions by central differences of the
+    restated forward; the spectrum aggregate adjoint likewise."""
+    import oracle as O
+    rng = np.random.default_rng(2)
+    k, n_rx = 60, 1
+    sc = orc.synth_scene(k, 1, 1, 5)
+    g = O.Grid(8, 16, 4, 1.0)
+    tx = np.array([0.3, -0.2, 0.1])
+    co = rng.standard_normal((n_rx, k, 4, 1, 2))
+    dv = rng.standard_normal((n_rx, 1, 2, 8, 16))
+    rs = ref.scene(sc)
+    b = ref.backward_render(ref.tx_state(rs, tx, g), rs, co, n_rx, dv)
+
+    def loss(s, c=co):
+        h = orc.scene(s)
+        v, _ = orc.render(orc.tx_state(h, tx, g), h, c, n_rx)
+        return float((v * dv).sum())
+
+    idx = np.argsort(-np.abs(b["d_tau_logits"]))[:3]
+    for kk in idx:
+        for name, arr, comp in (("d_tau_logits", "tau_logits", None), ("d_positions", "positions", 0)):
+            hi = {n: (v.copy() if isinstance(v, np.ndarray) else v) for n, v in sc.items()}
+            lo = {n: (v.copy() if isinstance(v, np.ndarray) else v) for n, v in sc.items()}
+            eps = 1e-6
+            if comp is None:
+                hi[arr][kk] += eps; lo[arr][kk] -= eps
+                want = b[name][kk]
+            else:
+                hi[arr][kk, comp] += eps; lo[arr][kk, comp] -= eps
+                want = b[name][kk, comp]
+            fd = (loss(hi) - loss(lo)) / (2 * eps)
+            assert abs(fd - want) <= 1e-4 * max(1.0, abs(want)), (name, kk, fd, want)
+    e = np.zeros_like(co); e[0, idx[0], 1, 0, 1] = 1.0
+    assert abs(loss(sc, e) - b["d_coeffs"][0, idx[0], 1, 0, 1]) < 1e-10
+    vals = rng.standard_normal((2, 1, 2, 8, 16))
+    up = rng.standard_normal((2, 8, 16))
+    d = ref.aggregate_backward(vals, g, "spectrum", up)
+    p = vals.copy(); p[1, 0, 0, 3, 5] += 1e-6
+    m = vals.copy(); m[1, 0, 0, 3, 5] -= 1e-6
+    fd = ((orc.aggregate(p, g, "spectrum") - orc.aggregate(m, g, "spectrum")) * up).sum() / 2e-6
+    assert abs(fd - d[1, 0, 0, 3, 5]) < 1e-6
