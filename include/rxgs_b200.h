@@ -187,6 +187,15 @@ int rxgs_probe_segments(rxgs_ctx ctx, rxgs_cond c, int n, const double* from, co
  * out K*L*C*2.  local_in (K*6) may be NULL (ConditionWorkspace::local_in). */
 int rxgs_condition_forward(rxgs_ctx ctx, rxgs_cond c, rxgs_scene scene, const double rx[3],
                            double* out, double* local_in);
+
+/* cond::condition_backward (conditioning.cpp:472-587) for one receiver, with
+ * the workspace recomputed on device.  d_out: K*L*C*2 gradient w.r.t. the
+ * conditioned coefficients; d_base: K*L*C*2 gradient w.r.t. the scene's
+ * base coefficients; d_params: ConditioningGrads packed in the
+ * rxgs_cond_create parameter order (freqs | global MLP | embed | local MLP),
+ * rxgs_cond_param_count values.  d_base / d_params may be NULL. */
+int rxgs_condition_backward(rxgs_ctx ctx, rxgs_cond cond, rxgs_scene scene, const double rx[3],
+                            const double* d_out, double* d_base, double* d_params);
 /* cond::condition_batch (conditioning.cpp:425-435): out n_rx*K*L*C*2. */
 int rxgs_condition_batch(rxgs_ctx ctx, rxgs_cond c, rxgs_scene scene, const double* rx, int n_rx,
                          double* out);

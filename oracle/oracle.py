@@ -305,6 +305,16 @@ class Checker:
                                  _d(np.ascontiguousarray(upstream, np.float64)), out.ctypes.data_as(_dp))
         return out
 
+    def cond_backward(self, cond_h, scene_h, rx, d_out):
+        """cond::condition_backward (conditioning.cpp:472-587) after a forward
+        at rx; reference only.  Returns (d_base, packed d_params)."""
+        d_out = np.ascontiguousarray(d_out, np.float64)
+        d_base = np.empty_like(d_out)
+        d_params = np.empty(len(cond_h.data["params"]))
+        self._cond_backward(cond_h.ptr, scene_h.ptr, _d(np.asarray(rx, np.float64)), _d(d_out),
+                            d_base.ctypes.data_as(_dp), d_params.ctypes.data_as(_dp))
+        return d_base, d_params
+
     def backward_render(self, tx_h, scene_h, coeffs, n_rx, d_values, threads=1):
         """raster::backward_render (sphraster.cpp:509-733); reference only.
         Returns the GradientBundle as a dict."""

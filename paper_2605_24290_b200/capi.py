@@ -102,6 +102,7 @@ _SIG = {
     "rxgs_build_occupancy": (C.c_int, [_vp, _vp, C.c_int, _vp, _vp, _vp, _vp]),
     "rxgs_probe_segments": (C.c_int, [_vp, _vp, C.c_int, _vp, _vp, _vp]),
     "rxgs_condition_forward": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "rxgs_condition_backward": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "rxgs_condition_batch": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int, _vp]),
     "rxgs_render_queries": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp]),
     "rxgs_predict": (C.c_int, [_vp, _vp, _vp, C.POINTER(Grid), _vp, _vp, _vp]),
@@ -455,6 +456,14 @@ class Cond:
         _check(_lib.rxgs_condition_forward(self.ctx.h, self.h, scene.h, ptr(rx, np.float64), out.ctypes.data,
                                            None if lin is None else lin.ctypes.data))
         return (out, lin) if workspace else out
+
+    def backward(self, scene: Scene, rx, d_out):
+        """cond::condition_backward (conditioning.cpp:472-587) -> (d_base, packed d_params)."""
+        d_base = _out((scene.k, scene.L, scene.channels, 2))
+        d_params = _out(int(_lib.rxgs_cond_param_count(self.h)))
+        _check(_lib.rxgs_condition_backward(self.ctx.h, self.h, scene.h, ptr(rx, np.float64),
+                                            ptr(d_out, np.float64), d_base.ctypes.data, d_params.ctypes.data))
+        return d_base, d_params
 
     def batch(self, scene: Scene, rx):
         rx = np.ascontiguousarray(rx, np.float64).reshape(-1, 3)

@@ -1096,6 +1096,41 @@ int rxgs_condition_forward(rxgs_ctx ctx, rxgs_cond c, rxgs_scene sc, const doubl
     API_END
 }
 
+int rxgs_condition_backward(rxgs_ctx ctx, rxgs_cond c, rxgs_scene sc, const double rx[3], const double* d_out,
+                            double* d_base, double* d_params) {
+    API_BEGIN
+    if (!ctx || !c || !sc || !rx || !d_out) return fail(RXGS_ERR_INVALID, "condition_backward: null argument");
+    if (sc->l_max != c->l_max || sc->channels != c->C)
+        return fail(RXGS_ERR_INVALID, "condition_forward: scene/state shape mismatch");
+    RX_TRY(set_device(ctx));
+    cudaStream_t s = ctx->stream;
+    if (c->use_local()) RX_TRY(check_receivers(ctx, sc, rx, 1));
+    const size_t nco = static_cast<size_t>(sc->k) * sc->L * sc->channels * 2;
+    const size_t npar = c->h_params.size();
+    DevBuf t_rx, t_do, o_base, o_par, ws;
+    const double* d_rx = nullptr;
+    const double* d_do = nullptr;
+    RX_TRY(dev_in(ctx, rx, 3, t_rx, &d_rx));
+    RX_TRY(dev_in(ctx, d_out, nco, t_do, &d_do));
+    double* db = nullptr;
+    double* dp = nullptr;
+    RX_TRY(dev_out(d_base, nco, o_base, &db));
+    RX_TRY(dev_out(d_params, npar, o_par, &dp));
+    if (!db) { RXGS_CUDA(o_base.ensure(std::max<size_t>(nco, 1) * sizeof(double))); db = o_base.as<double>(); }
+    if (!dp) { RXGS_CUDA(o_par.ensure(std::max<size_t>(npar, 1) * sizeof(double))); dp = o_par.as<double>(); }
+    RXGS_CUDA(ws.ensure(cond_backward_ws_bytes(*c, sc->k, ctx->sm_count)));
+    cudaEvent_t ev;
+    timing_begin(ctx, "condition_backward", &ev);
+    RXGS_CUDA(launch_cond_backward(*c, *sc, d_rx, d_do, db, dp, ws.p, ctx->sm_count, s));
+    timing_end(ctx, "condition_backward", ev, static_cast<double>(sc->k));
+    ctx->launches += 6;
+    RX_TRY(finish_out(ctx, d_base, db, nco));
+    RX_TRY(finish_out(ctx, d_params, dp, npar));
+    RXGS_CUDA(cudaStreamSynchronize(s));
+    return RXGS_OK;
+    API_END
+}
+
 // ------------------------------------------------------------------ queries
 int rxgs_render_queries(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, rxgs_txstate st, const double* rx,
                         int n_rx, float* out_spectrum, float* out_rssi) {

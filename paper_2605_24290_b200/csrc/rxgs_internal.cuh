@@ -231,6 +231,11 @@ cudaError_t launch_fill_transmittance(const rxgs_txstate_s& st, int n_rx, double
 
 // ---- k_train.cu
 int train_regroup(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s);
+// ---- k_cond_bwd.cu (FP64 materialised conditioning adjoint)
+size_t cond_backward_ws_bytes(const rxgs_cond_s& cs, int K, int sms);
+cudaError_t launch_cond_backward(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const double* d_rx,
+                                 const double* d_out, double* d_base, double* d_params, void* ws, int sms,
+                                 cudaStream_t s);
 // ---- k_backward.cu (FP64 adjoints of the materialised API)
 cudaError_t launch_aggregate_bwd(const DevGrid& g, int modality, int n_rx, int channels, const double* values,
                                  const double* up, double* dv, cudaStream_t s);

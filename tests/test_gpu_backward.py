@@ -101,3 +101,30 @@ def test_backward_render_deterministic(ctx, capi):
     b = scene.backward_render(st, co, 2, dv)
     for n in a:
         assert np.array_equal(a[n], b[n]), n
+
+
+@pytest.mark.parametrize("mode,hidden,C,occ", [
+    ("full", 64, 1, True), ("global_only", 64, 1, True), ("local_only", 64, 1, True), ("additive_only", 64, 1, True),
+    ("no_occlusion", 64, 1, True), ("full", 32, 2, True), ("full", 64, 1, False)])
+def test_condition_backward_matches_reference(ctx, capi, ref, mode, hidden, C, occ):
+    from test_gpu_render import _setup_cond
+    rng = np.random.default_rng(8)
+    k = 700
+    sc = capi.synth_scene(k, 2, C, 7)
+    scene, cond, rscene, rcond = _setup_cond(capi, ctx, ref, sc, mode=mode, hidden=hidden, occ=occ)
+    rx = np.array([0.45, -0.35, 0.2])
+    d_out = rng.standard_normal((k, 9, C, 2))
+    db, dp = cond.backward(scene, rx, d_out)
+    wdb, wdp = ref.cond_backward(rcond, rscene, rx, d_out)
+    assert rel_err(db, wdb).max() < TOL
+    assert rel_err(dp, wdp).max() < TOL
+    assert np.abs(wdp).max() > 0.0
+
+
+def test_condition_backward_rejects_coincident_receiver(ctx, capi):
+    from test_gpu_render import _setup_cond
+    import oracle as O
+    sc = capi.synth_scene(50, 2, 1, 7)
+    scene, cond, _, _ = _setup_cond(capi, ctx, O.restatement(), sc)
+    with pytest.raises(capi.InvalidArgument, match="receiver coincides with gaussian 3"):
+        cond.backward(scene, sc["positions"][3], np.zeros((50, 9, 1, 2)))
