@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--train-batch", type=int, default=16, help="(tx, rx) samples per GPU per training step")
+    ap.add_argument("--no-config3", action="store_true", help="skip the coverage-table (config 3) leg")
+    ap.add_argument("--no-config5", action="store_true", help="skip the 2M / 180x720 (config 5) leg")
     return ap.parse_args()
 
 
@@ -299,6 +301,9 @@ def run_b200(args):
                     "composite_ms": comp_ms / max(comp_n, 1), "walk_ms": walk_ms / max(comp_n, 1)}
 
     train = None if args.no_train else bench_train(args, capi, ctx, scene, cond, grid, stream, dev, rank, world)
+    del scene, cond
+    cov = None if args.no_config3 else bench_coverage(args, capi, ctx, stream, dev, rank, world)
+    large = None if args.no_config5 else bench_large(args, capi, ctx, stream, dev, rank, world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -320,7 +325,7 @@ def run_b200(args):
                 "vs_baseline": None, "dtype": "f32 (FP64 geometry/walk)", "data": "synthetic",
                 "config": workload(args), "e2e": e2e, "gpu_launches": int(launches),
                 "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
-                "tx_state": stats, "train_config4": train}
+                "tx_state": stats, "train_config4": train, "config3": cov, "config5": large}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -390,6 +395,174 @@ def bench_train(args, capi, ctx, scene, cond, grid, stream, dev, rank, world):
                         f"({'NCCL' if world > 1 else 'none at 1 GPU'}) of {tr.n} values",
             "ms_per_step": ms, "steps_per_s": 1e3 / ms, "samples_per_s": world * B * 1e3 / ms,
             "grad_floats": tr.n, "n_gpus": world, "cpu_reference": cpu}
+
+
+def _cond_for(capi, ctx, scene, lib=None):
+    lo, hi = scene.bounds(0.0)
+    cfg = capi.cond_cfg()
+    params = capi.synth_cond(cfg, 2, 1, lo, hi, 3, True)
+    cond = ctx.cond(cfg, params)
+    olo, ohi = scene.bounds(0.1)
+    cond.build_occupancy(scene, 32, olo, ohi)
+    return cond
+
+
+def _ref_model(O, chk, k):
+    sc = chk.synth_scene(k, 2, 1, 7)
+    h = chk.scene(sc, "spectrum")
+    lo, hi = chk.scene_bounds(h, 0.0)
+    cfg = O.cond_cfg()
+    params = chk.synth_cond(cfg, 2, 1, lo, hi, 3, True)
+    olo, ohi = chk.scene_bounds(h, 0.1)
+    return h, chk.cond(cfg, params, chk.build_occupancy(h, 32, olo, ohi), olo, ohi)
+
+
+def bench_coverage(args, capi, ctx, stream, dev, rank, world):
+    """BASELINE config 3: RSSI coverage table, K=500k, 64 Tx x 1024 Rx, 90x360.
+    Receivers sharded over ranks (1024 total), every rank does all 64 Tx
+    (strong scaling of the fixed table).  One step = the whole table through
+    rxgs_coverage_table: global + local conditioning once per receiver
+    (Tx-independent, cached in HBM), then per Tx build_tx_state + factorised
+    signal + RSSI compositing."""
+    import torch
+    from paper_2605_24290_b200.dist import max_over_ranks, shard_range
+    K, n_tx, n_rx_total = 500_000, 64, 1024
+    b, e = shard_range(n_rx_total, rank, world)
+    rx = capi.synth_points(n_rx_total, 11, "bench.rx", BOX_LO, BOX_HI, 0.05)[b:e]
+    tx = capi.synth_points(n_tx, 13, "bench.tx", BOX_LO, BOX_HI, 0.05)
+    scene = ctx.scene(capi.synth_scene(K, 2, 1, 7), "rssi")
+    cond = _cond_for(capi, ctx, scene)
+    grid = capi.Grid(90, 360, 8, 1.0)
+    rx_d, tx_d = torch.from_numpy(rx).to(dev), torch.from_numpy(tx).to(dev)
+    out_d = torch.empty((n_tx, rx.shape[0]), dtype=torch.float32, device=dev)
+    n_steps = max(2, min(args.steps, 3))
+    scene.coverage_table(cond, grid, tx_d, rx_d, out_d)  # warm-up (pool, caches)
+    torch.cuda.synchronize(dev)
+    ctx.reset_stats()
+    ctx.profile(True)
+    l0 = ctx.launch_count()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(n_steps):
+        scene.coverage_table(cond, grid, tx_d, rx_d, out_d)
+    s1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = max_over_ranks(s0.elapsed_time(s1) / n_steps, dev)
+    launches = (ctx.launch_count() - l0) // n_steps
+    phases = {n: ctx.kernel_stats(n)[0] / n_steps for n in ("cond_global", "local_cache", "tx_prep", "walk",
+                                                             "cov_signal", "composite")}
+    ctx.profile(False)
+    # end to end with host buffers (tx/rx in, table out)
+    out_h = np.empty((n_tx, rx.shape[0]), np.float32)
+    t0 = time.perf_counter()
+    scene.coverage_table(cond, grid, tx, rx, out_h)
+    e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3, dev)
+    queries = n_tx * n_rx_total
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import oracle as O  # cpu_baseline leg
+            chk = O.reference()
+            h, rc = _ref_model(O, chk, K)
+            s_tx, s_rx, threads = 2, 16, os.cpu_count() or 1
+            secs, _, ph = chk.bench_coverage(h, rc, O.Grid(90, 360, 8, 1.0), tx[:s_tx], rx[:s_rx], threads)
+            full = ph[0] / s_rx * n_rx_total + ph[1] / s_tx * n_tx + ph[2] / (s_tx * s_rx) * queries
+            cpu = {"value": queries / full, "unit": "queries/s", "cores": threads, "kind": "reference",
+                   "sample": f"{s_tx} Tx x {s_rx} Rx timed ({secs:.1f} s wall: conditioning {ph[0]:.1f} s, "
+                             f"build_tx_state {ph[1]:.1f} s, render+RSSI {ph[2]:.1f} s), extrapolated linearly to "
+                             f"64 Tx x 1024 Rx with conditioning once per Rx (BASELINE.md config-3 rule)",
+                   "est_table_s": full}
+        except Exception as ex:
+            cpu = {"error": str(ex)}
+    del scene, cond
+    ctx.release_cache()
+    return {"workload": "config3: K=500k, 64 Tx x 1024 Rx RSSI coverage table, 90x360, conditioned (full)",
+            "value": queries / (ms / 1e3), "unit": "queries/s", "ms_per_table": ms, "steps": n_steps,
+            "scaling": "strong (Rx sharded, all Tx per rank)", "n_gpus": world,
+            "e2e": {"value": queries / (e2e_ms / 1e3), "unit": "queries/s", "ms_per_table": e2e_ms,
+                    "h2d_bytes_per_step": int(tx.nbytes + rx.nbytes), "d2h_bytes_per_step": int(out_h.nbytes)},
+            "phase_ms": phases, "gpu_launches": int(launches), "cpu_baseline": cpu}
+
+
+def bench_large(args, capi, ctx, stream, dev, rank, world):
+    """BASELINE config 5: K=2M, 180x720 (2,070 tiles), 256 Rx per rank, 1 Tx,
+    spectrum + RSSI: stress of the sort and the compositor."""
+    import torch
+    from paper_2605_24290_b200.dist import max_over_ranks, shard_range
+    K, n = 2_000_000, 256
+    b, e = shard_range(world * n, rank, world)
+    rx = capi.synth_points(world * n, 11, "bench.rx", BOX_LO, BOX_HI, 0.05)[b:e]
+    scene = ctx.scene(capi.synth_scene(K, 2, 1, 7), "spectrum")
+    cond = _cond_for(capi, ctx, scene)
+    grid = capi.Grid(180, 720, 8, 1.0)
+    tx = np.array(TX)
+    rx_d = torch.from_numpy(rx).to(dev)
+    spec = torch.empty((n, 180, 720), dtype=torch.float32, device=dev)
+    rssi = torch.empty(n, dtype=torch.float32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        st = scene.tx_state(tx, grid)
+        scene.render_queries(cond, st, rx_d, spec, rssi)
+        return st
+
+    last = None
+    for _ in range(2):
+        last = step()
+    torch.cuda.synchronize(dev)
+    n_steps = max(3, min(args.steps, 5))
+    ctx.reset_stats()
+    ctx.profile(True)
+    l0 = ctx.launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_steps)]
+    for i in range(n_steps):
+        flush.fill_(float(i))
+        evs[i][0].record(stream)
+        last = step()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in evs) / n_steps, dev)
+    launches = (ctx.launch_count() - l0) // n_steps
+    phases = {nm: ctx.kernel_stats(nm)[0] / n_steps for nm in ("tx_prep", "sort", "walk", "cond_global",
+                                                              "cond_signal", "composite")}
+    ctx.profile(False)
+    stats = last.stats()
+    del last
+    spec_h = torch.empty((n, 180, 720), dtype=torch.float32).pin_memory().numpy()
+    rssi_h = torch.empty(n, dtype=torch.float32).pin_memory().numpy()
+    rx_h = torch.from_numpy(rx.copy()).pin_memory().numpy()
+    st = scene.tx_state(tx, grid)  # warm the host-buffer path
+    scene.render_queries(cond, st, rx_h, spec_h, rssi_h)
+    del st
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    st = scene.tx_state(tx, grid)
+    scene.render_queries(cond, st, rx_h, spec_h, rssi_h)
+    del st
+    e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3, dev)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import oracle as O  # cpu_baseline leg
+            chk = O.reference()
+            h, rc = _ref_model(O, chk, K)
+            threads, sample = os.cpu_count() or 1, 2
+            secs, _, _ = chk.bench_queries(h, rc, O.Grid(180, 720, 8, 1.0), TX, rx[:sample], threads)
+            cpu = {"value": sample / secs, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"{sample} receivers, build_tx_state + conditioning + render + aggregation, "
+                             f"{secs:.1f} s wall"}
+        except Exception as ex:
+            cpu = {"error": str(ex)}
+    del scene, cond
+    ctx.release_cache()
+    return {"workload": "config5: K=2M, 1 Tx x 256 Rx per rank, 180x720 spectrum + RSSI, conditioned (full)",
+            "value": world * n / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "steps": n_steps, "scaling": "weak",
+            "n_gpus": world, "l2": "flushed between timed steps",
+            "e2e": {"value": world * n / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": int(rx.nbytes + 24), "d2h_bytes_per_step": int(spec_h.nbytes + rssi_h.nbytes)},
+            "phase_ms": phases, "gpu_launches": int(launches), "tx_state": stats, "cpu_baseline": cpu}
 
 
 def run_reference(args):

@@ -65,6 +65,9 @@ int rxgs_ctx_profile(rxgs_ctx ctx, int enable);
 int rxgs_ctx_kernel_stats(rxgs_ctx ctx, const char* name, double* total_ms, int64_t* launches,
                           double* work_units);
 int rxgs_ctx_reset_stats(rxgs_ctx ctx);
+/* Free the context's grow-only work buffers and recycled Tx-state buffers
+ * (e.g. between workloads of very different sizes). */
+int rxgs_ctx_release_cache(rxgs_ctx ctx);
 /* Number of kernels of this library launched since the last reset. */
 int64_t rxgs_ctx_launch_count(rxgs_ctx ctx);
 /* Conditioning kernel selection: 0 = auto (tcgen05 when hidden == 64 and
@@ -209,6 +212,16 @@ int rxgs_condition_batch(rxgs_ctx ctx, rxgs_cond c, rxgs_scene scene, const doub
  * f32 dB (may be NULL).  cond may be NULL (unconditioned model). */
 int rxgs_render_queries(rxgs_ctx ctx, rxgs_scene scene, rxgs_cond c, rxgs_txstate st,
                         const double* rx, int n_rx, float* out_spectrum, float* out_rssi);
+
+/* Coverage table (BASELINE config 3): out_rssi[t*n_rx + j] = RSSI (dB) of
+ * train::predict(model, tx_t, rx_j) (trainer.cpp:147-154), the table
+ * apps::coverage_fraction / greedy_plan consume (apps.cpp:70-116, layout
+ * rssi_table[t*candidates + c]).  The Tx-independent conditioning (local
+ * branch per (Gaussian, rx), global branch per rx) is computed once and
+ * reused for every transmitter.  cond may be NULL (unconditioned scene).
+ * Requires channels == 1. */
+int rxgs_coverage_table(rxgs_ctx ctx, rxgs_scene scene, rxgs_cond cond, const rxgs_grid* grid,
+                        const double* tx, int n_tx, const double* rx, int n_rx, float* out_rssi);
 
 /* train::predict for one (tx, rx): builds the TxState internally; out is the
  * scene modality's measurement (spectrum H*W, rssi 1, csi C*2) in f64. */

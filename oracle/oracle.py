@@ -129,6 +129,8 @@ class Checker:
             sig.update({
                 "bench_queries": (C.c_double, [C.c_void_p, C.c_void_p, _ip, _dp, _dp, _dp, C.c_int, C.c_int,
                                                _fp, _dp]),
+                "bench_coverage": (C.c_double, [C.c_void_p, C.c_void_p, _ip, _dp, _dp, C.c_int, _dp, C.c_int,
+                                                C.c_int, _dp, _dp]),
                 "aggregate_backward": (C.c_int, [C.c_int, C.c_int, _ip, _dp, _dp, C.c_int, _dp, _dp]),
                 "backward_render": (C.c_int, [C.c_void_p, C.c_void_p, _dp, C.c_long, C.c_int, _dp, C.c_long,
                                               C.c_int, _dp, _dp, _dp, _dp, _dp, C.c_char_p, C.c_int]),
@@ -345,6 +347,17 @@ class Checker:
                                    None if rssi is None else rssi.ctypes.data_as(_dp))
         return secs, spec, rssi
 
+
+    def bench_coverage(self, scene_h, cond_h, grid: Grid, tx, rx, threads):
+        """Reference CPU coverage table (config 3 rules): returns (secs, table, phases)."""
+        tx = np.ascontiguousarray(tx, np.float64).reshape(-1, 3)
+        rx = np.ascontiguousarray(rx, np.float64).reshape(-1, 3)
+        out = np.empty((tx.shape[0], rx.shape[0]))
+        ph = np.zeros(3)
+        secs = self._bench_coverage(scene_h.ptr, None if cond_h is None else cond_h.ptr, grid.gi, grid.gd, _d(tx),
+                                    tx.shape[0], _d(rx), rx.shape[0], threads, out.ctypes.data_as(_dp),
+                                    ph.ctypes.data_as(_dp))
+        return secs, out, ph
 
 def _i_out(a):
     return a.ctypes.data_as(_ip)

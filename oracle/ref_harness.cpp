@@ -569,6 +569,68 @@ double ref_bench_queries(void* scene, void* cond, const int* gi, const double* g
     return std::chrono::duration<double>(clk::now() - t0).count();
 }
 
+// Coverage-table CPU baseline (BASELINE config 3 timing rules, BASELINE.md
+// "Coverage per config"): condition every receiver once (fanned over
+// threads, one ConditioningState copy each), then per Tx build_tx_state +
+// render_field (chunks of 16, `threads`) + RSSI aggregation, reusing the
+// conditioned coefficients.  out_rssi[t*n_rx + j]; phase[0..2] = seconds in
+// conditioning, build_tx_state, render+aggregate.
+double ref_bench_coverage(void* scene, void* cond, const int* gi, const double* gd, const double* tx,
+                          int n_tx, const double* rx, int n_rx, int threads, double* out_rssi,
+                          double* phase) {
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
+    const GaussianScene& sc = static_cast<Handle*>(scene)->scene;
+    const auto grid = make_grid(gi, gd);
+    const std::size_t per = sc.fle_coeffs.size();
+    std::vector<double> coeffs(per * static_cast<std::size_t>(n_rx));
+    if (cond) {
+        const int nt = std::max(1, std::min(threads, n_rx));
+        std::vector<std::thread> pool;
+        for (int t = 0; t < nt; ++t)
+            pool.emplace_back([&, t] {
+                cond::ConditioningState local = *static_cast<cond::ConditioningState*>(cond);
+                for (int j = t; j < n_rx; j += nt) {
+                    const auto o = cond::condition_forward(local, sc.fle_coeffs, sc,
+                                                           {rx[3 * j], rx[3 * j + 1], rx[3 * j + 2]});
+                    std::memcpy(coeffs.data() + per * static_cast<std::size_t>(j), o.data(),
+                                per * sizeof(double));
+                }
+            });
+        for (auto& th : pool) th.join();
+    } else {
+        for (int j = 0; j < n_rx; ++j)
+            std::memcpy(coeffs.data() + per * static_cast<std::size_t>(j), sc.fle_coeffs.data(),
+                        per * sizeof(double));
+    }
+    const auto t1 = clk::now();
+    double t_build = 0.0, t_render = 0.0;
+    const int chunk = 16;
+    for (int t = 0; t < n_tx; ++t) {
+        const auto a = clk::now();
+        const raster::TxState st =
+            raster::build_tx_state(sc, {tx[3 * t], tx[3 * t + 1], tx[3 * t + 2]}, grid);
+        const auto b = clk::now();
+        for (int j0 = 0; j0 < n_rx; j0 += chunk) {
+            const int nj = std::min(chunk, n_rx - j0);
+            const std::vector<double> part(coeffs.begin() + per * static_cast<std::size_t>(j0),
+                                           coeffs.begin() + per * static_cast<std::size_t>(j0 + nj));
+            const auto f = raster::render_field(st, sc, part, nj, threads);
+            const auto rssi = raster::aggregate_modality(f, Modality::Rssi, grid);
+            for (int j = 0; j < nj; ++j)
+                if (out_rssi) out_rssi[static_cast<std::size_t>(t) * n_rx + j0 + j] = rssi[j].scalar;
+        }
+        t_build += std::chrono::duration<double>(b - a).count();
+        t_render += std::chrono::duration<double>(clk::now() - b).count();
+    }
+    if (phase) {
+        phase[0] = std::chrono::duration<double>(t1 - t0).count();
+        phase[1] = t_build;
+        phase[2] = t_render;
+    }
+    return std::chrono::duration<double>(clk::now() - t0).count();
+}
+
 // One conditioned training sample (trainer.cpp:429-449): condition -> render
 // (N=1) -> aggregate(spectrum) -> composite_loss vs target -> adjoints.
 // Outputs loss, d_base (K*L*C*2), d_params (packed cond order), and the

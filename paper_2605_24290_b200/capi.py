@@ -68,6 +68,7 @@ _SIG = {
     "rxgs_ctx_kernel_stats": (C.c_int, [_vp, C.c_char_p, C.POINTER(C.c_double), C.POINTER(_i64),
                                         C.POINTER(C.c_double)]),
     "rxgs_ctx_reset_stats": (C.c_int, [_vp]),
+    "rxgs_ctx_release_cache": (C.c_int, [_vp]),
     "rxgs_ctx_launch_count": (_i64, [_vp]),
     "rxgs_ctx_set_cond_kernel": (C.c_int, [_vp, C.c_int]),
     "rxgs_ctx_set_composite_kernel": (C.c_int, [_vp, C.c_int]),
@@ -105,6 +106,7 @@ _SIG = {
     "rxgs_condition_backward": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "rxgs_condition_batch": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int, _vp]),
     "rxgs_render_queries": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp]),
+    "rxgs_coverage_table": (C.c_int, [_vp, _vp, _vp, C.POINTER(Grid), _vp, C.c_int, _vp, C.c_int, _vp]),
     "rxgs_predict": (C.c_int, [_vp, _vp, _vp, C.POINTER(Grid), _vp, _vp, _vp]),
     "rxgs_trainer_create": (C.c_int, [_vp, _vp, _vp, _vp, C.POINTER(_vp)]),
     "rxgs_trainer_destroy": (C.c_int, [_vp]),
@@ -233,6 +235,9 @@ class Context:
     def launch_count(self):
         return int(_lib.rxgs_ctx_launch_count(self.h))
 
+    def release_cache(self):
+        _check(_lib.rxgs_ctx_release_cache(self.h))
+
     def set_cond_kernel(self, which):
         """'auto' (tcgen05 when eligible) or 'simt'."""
         _check(_lib.rxgs_ctx_set_cond_kernel(self.h, {"auto": 0, "simt": 1}[which]))
@@ -349,6 +354,17 @@ class Scene:
         _check(_lib.rxgs_render_queries(self.ctx.h, self.h, None if cond is None else cond.h, st.h,
                                         ptr(rx, np.float64), n, ptr(spectrum), ptr(rssi)))
         return spectrum, rssi
+
+    def coverage_table(self, cond, grid: Grid, tx, rx, out=None):
+        """RSSI table [n_tx][n_rx] (BASELINE config 3; apps.cpp:70-116 layout)."""
+        tx = tx if hasattr(tx, "data_ptr") else np.ascontiguousarray(tx, np.float64).reshape(-1, 3)
+        rx = rx if hasattr(rx, "data_ptr") else np.ascontiguousarray(rx, np.float64).reshape(-1, 3)
+        n_tx, n_rx = int(tx.shape[0]), int(rx.shape[0])
+        if out is None:
+            out = np.empty((n_tx, n_rx), np.float32)
+        _check(_lib.rxgs_coverage_table(self.ctx.h, self.h, None if cond is None else cond.h, C.byref(grid),
+                                        ptr(tx, np.float64), n_tx, ptr(rx, np.float64), n_rx, ptr(out)))
+        return out
 
     def predict(self, cond, grid: Grid, tx, rx):
         m = MODALITY[self.modality]

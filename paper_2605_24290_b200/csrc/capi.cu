@@ -393,6 +393,23 @@ int rxgs_ctx_reset_stats(rxgs_ctx ctx) {
     return RXGS_OK;
 }
 
+int rxgs_ctx_release_cache(rxgs_ctx ctx) {
+    API_BEGIN
+    if (!ctx) return fail(RXGS_ERR_INVALID, "null context");
+    RX_TRY(set_device(ctx));
+    RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (DevBuf* b : {&ctx->sort_tmp, &ctx->scratch_a, &ctx->scratch_b, &ctx->scratch_c, &ctx->scratch_d,
+                      &ctx->signals, &ctx->ag, &ctx->partial, &ctx->host_in, &ctx->host_out, &ctx->ycache}) {
+        if (b->p) cudaFree(b->p);
+        b->p = nullptr;
+        b->bytes = 0;
+    }
+    for (rxgs_txstate_s* st : ctx->spare_tx) delete st;
+    ctx->spare_tx.clear();
+    return RXGS_OK;
+    API_END
+}
+
 int64_t rxgs_ctx_launch_count(rxgs_ctx ctx) { return ctx ? ctx->launches : 0; }
 
 int rxgs_ctx_set_cond_kernel(rxgs_ctx ctx, int which) {
@@ -563,8 +580,10 @@ int rxgs_tx_state_build(rxgs_ctx ctx, rxgs_scene sc, const double tx[3], const r
     }
     timing_end(ctx, "tx_prep", ev, sc->k);
     ctx->launches += 1;
+    timing_begin(ctx, "sort", &ev);
     rc = bin_tiles(ctx, *st, s);
     if (rc) return fail_st(rc);
+    timing_end(ctx, "sort", ev, sc->k);
     const DevGrid& g = st->grid;
     const size_t cells = static_cast<size_t>(g.nt) * g.np;
     ENS(tw, std::max<size_t>(st->entries, 1) * g.cell_blocks * kMaxCellsPerBlock * sizeof(float));
@@ -1211,6 +1230,99 @@ int rxgs_render_queries(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, rxgs_txstate s
     RX_TRY(finish_out(ctx, out_rssi, d_rssi, static_cast<size_t>(n_rx)));
     if (pipelined) RXGS_CUDA(cudaStreamSynchronize(ctx->copy_stream));
     if (host_out || !is_device_ptr(rx)) RXGS_CUDA(cudaStreamSynchronize(s));
+    return RXGS_OK;
+    API_END
+}
+
+int rxgs_coverage_table(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const rxgs_grid* grid, const double* tx,
+                        int n_tx, const double* rx, int n_rx, float* out_rssi) {
+    API_BEGIN
+    if (!ctx || !sc || !grid) return fail(RXGS_ERR_INVALID, "coverage_table: null argument");
+    if (n_tx < 0 || n_rx < 0) return fail(RXGS_ERR_INVALID, "coverage_table: negative count");
+    if (n_tx == 0 || n_rx == 0) return RXGS_OK;
+    if (!tx || !rx || !out_rssi) return fail(RXGS_ERR_INVALID, "coverage_table: null argument");
+    if (c && (sc->l_max != c->l_max || sc->channels != c->C))
+        return fail(RXGS_ERR_INVALID, "condition_forward: scene/state shape mismatch");
+    if (sc->channels != 1)
+        return fail(RXGS_ERR_INVALID, "aggregate_modality: scalar modalities need channels == 1");
+    RX_TRY(validate_grid(grid));
+    RX_TRY(set_device(ctx));
+    cudaStream_t s = ctx->stream;
+    if (c && c->host_stale) {
+        RXGS_CUDA(cudaStreamSynchronize(s));
+        RXGS_CUDA(cudaMemcpy(c->h_params.data(), c->d_params64.p, c->h_params.size() * sizeof(double),
+                             cudaMemcpyDeviceToHost));
+        c->host_stale = false;
+    }
+    DevBuf t_rx;
+    const double* d_rx = nullptr;
+    RX_TRY(dev_in(ctx, rx, 3 * static_cast<size_t>(n_rx), t_rx, &d_rx));
+    const std::vector<double> txh = to_host(tx, 3 * static_cast<size_t>(n_tx));
+    if (c && c->use_local()) RX_TRY(check_receivers(ctx, sc, rx, n_rx));
+    float* d_out = nullptr;
+    DevBuf t_out;
+    RX_TRY(dev_out(out_rssi, static_cast<size_t>(n_tx) * n_rx, t_out, &d_out));
+    // Tx-independent halves of the conditioning, once for all transmitters
+    const size_t ag_n = static_cast<size_t>(n_rx) * sc->L * 4;
+    RXGS_CUDA(ctx->ag.ensure(std::max<size_t>(ag_n, 1) * sizeof(float)));
+    cudaEvent_t ev;
+    if (c && c->use_global()) {
+        timing_begin(ctx, "cond_global", &ev);
+        RXGS_CUDA(launch_cond_global(*c, d_rx, n_rx, ctx->ag.as<float>(), s));
+        timing_end(ctx, "cond_global", ev, static_cast<double>(n_rx) * sc->L);
+    } else {
+        RXGS_CUDA(cudaMemsetAsync(ctx->ag.p, 0, ag_n * sizeof(float), s));
+    }
+    DevBuf t_agT;
+    RXGS_CUDA(t_agT.ensure(std::max<size_t>(ag_n, 1) * sizeof(float)));
+    RXGS_CUDA(launch_ag_transpose(n_rx, sc->L, ctx->ag.as<float>(), t_agT.as<float>(), s));
+    ctx->launches += 2;
+    const float4* yc = nullptr;
+    if (c && c->use_local()) {
+        RXGS_CUDA(ctx->ycache.ensure(std::max<size_t>(static_cast<size_t>(sc->k) * n_rx, 1) * sizeof(float4)));
+        timing_begin(ctx, "local_cache", &ev);
+        RXGS_CUDA(launch_local_cache(*c, *sc, d_rx, n_rx, ctx->ycache.as<float4>(), s));
+        timing_end(ctx, "local_cache", ev, static_cast<double>(sc->k) * n_rx);
+        ctx->launches += 1;
+        yc = ctx->ycache.as<float4>();
+    }
+    RXGS_CUDA(ctx->signals.ensure(std::max<size_t>(static_cast<size_t>(sc->k) * n_rx, 1) * sizeof(float2)));
+    for (int t = 0; t < n_tx; ++t) {
+        rxgs_txstate st = nullptr;
+        RX_TRY(rxgs_tx_state_build(ctx, sc, txh.data() + 3 * static_cast<size_t>(t), grid, &st));
+        const DevGrid& g = st->grid;
+        const int n_tb = g.n_tiles * g.cell_blocks;
+        int rc = RXGS_OK;
+        cudaError_t e = ctx->partial.ensure(std::max<size_t>(static_cast<size_t>(n_tb) * n_rx, 1) * sizeof(float));
+        if (e == cudaSuccess) {
+            timing_begin(ctx, "cov_signal", &ev);
+            e = launch_cov_signal(c, *st, n_rx, t_agT.as<float>(), yc, ctx->signals.as<float2>(), s);
+            timing_end(ctx, "cov_signal", ev,
+                       static_cast<double>(st->needed_host >= 0 ? st->needed_host : st->visible) * n_rx);
+        }
+        if (e == cudaSuccess) {
+            CompositeOut co;
+            co.rssi_partial = ctx->partial.as<float>();
+            timing_begin(ctx, "composite", &ev);
+            e = (ctx->composite_kernel != 1 && composite_tc_eligible(*st))
+                    ? launch_composite_tc(*st, ctx->signals.as<float2>(), n_rx, co, s)
+                    : launch_composite(*st, ctx->signals.as<float2>(), n_rx, co, s);
+            timing_end(ctx, "composite", ev, n_rx);
+        }
+        if (e == cudaSuccess)
+            e = launch_rssi_finalize(ctx->partial.as<float>(), n_tb, n_rx, d_out + static_cast<size_t>(t) * n_rx,
+                                     nullptr, s);
+        ctx->launches += 3;
+        if (e != cudaSuccess) rc = cuda_fail(e, "coverage_table");
+        rxgs_tx_state_destroy(st);
+        if (rc) return rc;
+    }
+    if (c) {
+        if (c->use_global()) c->global_calls += static_cast<int64_t>(n_rx) * sc->L;
+        if (c->use_local()) c->local_calls += static_cast<int64_t>(n_rx) * sc->k;
+    }
+    RX_TRY(finish_out(ctx, out_rssi, d_out, static_cast<size_t>(n_tx) * n_rx));
+    RXGS_CUDA(cudaStreamSynchronize(s));
     return RXGS_OK;
     API_END
 }

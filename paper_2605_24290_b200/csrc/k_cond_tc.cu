@@ -64,12 +64,15 @@ __device__ __forceinline__ void split_store(uint8_t* hi_base, uint8_t* lo_base, 
     *reinterpret_cast<uint16_t*>(lo_base + off) = static_cast<uint16_t>(tc::pack_bf16(w - hi, 0.f) & 0xFFFFu);
 }
 
-template <int ST, int RT>
+// YOUT: rows are all K Gaussians (vis unused) and the local-branch output
+// y = (alpha_L, beta_L) is written to ycache[k][j] instead of the signal (the
+// Tx-independent cache of the coverage workload).
+template <int ST, int RT, bool YOUT>
 __global__ void __launch_bounds__(kThreads, 1)
     k_cond_tc(const __grid_constant__ LocalW W, CondDev c, const int* __restrict__ n_rows, const int* __restrict__ vis,
               const float4* __restrict__ pos32, const double* __restrict__ rx, int n_rx,
               const float2* __restrict__ Bm, const float2* __restrict__ GB, const float* __restrict__ ag,
-              float2* __restrict__ sig) {
+              float2* __restrict__ sig, float4* __restrict__ ycache, int n_all) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* w2hi = smem;
     uint8_t* w2lo = smem + kW2Bytes;
@@ -113,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t w1hi_a = tc::smem_u32(w1hi), w1lo_a = tc::smem_u32(w1lo);
 
     const int n_jc = (n_rx + 31) >> 5;
-    const long long items = static_cast<long long>(*n_rows) * n_jc;
+    const long long items = static_cast<long long>(YOUT ? n_all : *n_rows) * n_jc;
     const long long tiles = (items + 3) >> 2;
     const long long step = static_cast<long long>(gridDim.x) * kGroups;
     const int L = c.L;
@@ -126,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int jc = valid_item ? static_cast<int>(item % n_jc) : 0;
         const int j = jc * 32 + lane;
         const bool active = valid_item && j < n_rx;
-        const int k = valid_item ? vis[vi] : 0;
+        const int k = valid_item ? (YOUT ? vi : vis[vi]) : 0;
 
         float in[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         if (active) {
@@ -215,7 +218,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         tc::fence_before_sync();  // the next tile's layer-1 MMA overwrites D after the barrier
-        if (active) {  // FLE reduction after the MMAs (measured faster than overlapping them)
+        if (YOUT) {
+            if (active) ycache[static_cast<size_t>(k) * n_rx + j] = make_float4(y[0], y[1], y[2], y[3]);
+        } else if (active) {  // FLE reduction after the MMAs (measured faster than overlapping them)
             float2 M, Bs;
             fle_reduce(k, j, 0, L, 1, Bm, GB, ag, M, Bs);
             sig[static_cast<size_t>(k) * n_rx + j] = local_affine(c, 0, M, Bs, y);
@@ -321,10 +326,13 @@ bool cond_tc_eligible(const rxgs_cond_s* c) {
     return c && c->use_local() && c->hidden == kH && c->C == 1 && padded_dim(c->R) * padded_dim(c->R) * padded_dim(c->R) <= 48000;
 }
 
-cudaError_t launch_cond_signal_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
-                                  const double* d_rx, int n_rx, const float* d_ag, float2* d_sig,
-                                  cudaStream_t s) {
-    if (st.visible == 0 || n_rx == 0) return cudaSuccess;
+namespace {
+
+template <bool YOUT>
+cudaError_t launch_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const int* n_rows, const int* vis,
+                      long long rows_host, const double* d_rx, int n_rx, const float2* basis32, const float2* gb32,
+                      const float* d_ag, float2* d_sig, float4* ycache, cudaStream_t s) {
+    if (rows_host == 0 || n_rx == 0) return cudaSuccess;
     const CondDev d = make_dev(cs);
     LocalW w{};
     const std::vector<double>& p = cs.h_params;
@@ -340,18 +348,31 @@ cudaError_t launch_cond_signal_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc,
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const long long items = static_cast<long long>(st.visible) * ((n_rx + 31) / 32);
+    const long long items = rows_host * ((n_rx + 31) / 32);
     const long long tiles = (items + 3) / 4;
     const long long want = (tiles + kGroups - 1) / kGroups;
     const int blocks = static_cast<int>(want < sms ? want : sms);
     const bool fast = d.S == 16 && d.R == 32 && !d.nearest;
-    auto kern = fast ? k_cond_tc<16, 32> : k_cond_tc<0, 0>;
+    auto kern = fast ? k_cond_tc<16, 32, YOUT> : k_cond_tc<0, 0, YOUT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    kern<<<blocks, kThreads, smem, s>>>(w, d, st.needed_count.as<int>(), st.needed_order.as<int>(),
-                                        sc.d_pos32.as<float4>(), d_rx, n_rx, st.basis32.as<float2>(),
-                                        st.gb32.as<float2>(), d_ag, d_sig);
+    kern<<<blocks, kThreads, smem, s>>>(w, d, n_rows, vis, sc.d_pos32.as<float4>(), d_rx, n_rx, basis32, gb32, d_ag,
+                                        d_sig, ycache, static_cast<int>(rows_host));
     return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_cond_signal_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
+                                  const double* d_rx, int n_rx, const float* d_ag, float2* d_sig,
+                                  cudaStream_t s) {
+    return launch_tc<false>(cs, sc, st.needed_count.as<int>(), st.needed_order.as<int>(), st.visible, d_rx, n_rx,
+                            st.basis32.as<float2>(), st.gb32.as<float2>(), d_ag, d_sig, nullptr, s);
+}
+
+cudaError_t launch_local_cache_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const double* d_rx, int n_rx,
+                                  float4* ycache, cudaStream_t s) {
+    return launch_tc<true>(cs, sc, nullptr, nullptr, sc.k, d_rx, n_rx, nullptr, nullptr, nullptr, nullptr, ycache, s);
 }
 
 cudaError_t launch_tc_selftest(float* d_err, cudaStream_t s) {

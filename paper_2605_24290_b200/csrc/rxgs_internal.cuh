@@ -97,7 +97,7 @@ struct rxgs_ctx_s {
     std::vector<cudaEvent_t> event_pool;
     // scratch
     rxgs_b200::DevBuf sort_tmp, scratch_a, scratch_b, scratch_c, scratch_d, signals, ag, partial,
-        err_flag, host_in, host_out;
+        err_flag, host_in, host_out, ycache;
     int sm_count = 148;
     int cond_kernel = 0;  // 0 auto (tcgen05 when eligible), 1 force SIMT
     int composite_kernel = 0;  // 0 auto (tcgen05 when eligible), 1 force SIMT
@@ -231,6 +231,14 @@ cudaError_t launch_fill_transmittance(const rxgs_txstate_s& st, int n_rx, double
 
 // ---- k_train.cu
 int train_regroup(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s);
+// ---- k_coverage.cu (config-3 coverage table)
+cudaError_t launch_local_cache_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const double* d_rx, int n_rx,
+                                  float4* ycache, cudaStream_t s);
+cudaError_t launch_local_cache(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const double* d_rx, int n_rx,
+                               float4* ycache, cudaStream_t s);
+cudaError_t launch_ag_transpose(int n_rx, int L, const float* d_ag, float* d_agT, cudaStream_t s);
+cudaError_t launch_cov_signal(const rxgs_cond_s* cs, const rxgs_txstate_s& st, int n_rx, const float* d_agT,
+                              const float4* ycache, float2* d_sig, cudaStream_t s);
 // ---- k_cond_bwd.cu (FP64 materialised conditioning adjoint)
 size_t cond_backward_ws_bytes(const rxgs_cond_s& cs, int K, int sms);
 cudaError_t launch_cond_backward(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const double* d_rx,

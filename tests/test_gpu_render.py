@@ -263,3 +263,29 @@ def test_tcgen05_composite_matches_simt_and_oracle(ctx, capi, orc):
     for j in (0, 63, 64, 99):
         want = orc.predict(oscene, ocond, og, TX, rx[j], "spectrum").reshape(45, 90)
         assert rel_err(s_tc[j], want).max() < TOL
+
+
+@pytest.mark.parametrize("mode,hidden", [("full", 64), ("full", 32), ("additive_only", 64), ("global_only", 64),
+                                         (None, 64)])
+def test_coverage_table_matches_oracle_predict(ctx, capi, orc, mode, hidden):
+    """Config-3 path: Tx-independent conditioning cached once, reused per Tx."""
+    import oracle as O
+    sc = capi.synth_scene(2500, 2, 1, 7)
+    grid, og = capi.Grid(18, 36, 6, 1.0), O.Grid(18, 36, 6, 1.0)
+    if mode is None:
+        scene, cond = ctx.scene(sc, "rssi"), None
+        oscene, ocond = orc.scene(sc, "rssi"), None
+    else:
+        scene, cond, _, ocond = _setup_cond(capi, ctx, orc, sc, mode=mode, hidden=hidden)
+        oscene = orc.scene(sc, "rssi")
+    tx = capi.synth_points(3, 13, "bench.tx", [-4, -3, -1.5], [4, 3, 1.5])
+    rx = capi.synth_points(37, 11, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
+    table = scene.coverage_table(cond, grid, tx, rx)
+    for t in range(3):
+        for j in range(0, 37, 4):
+            want = orc.predict(oscene, ocond, og, tx[t], rx[j], "rssi")[0]
+            assert rel_err(table[t, j], want) < TOL, (t, j)
+    # the per-Tx fused query path gives the same table
+    st = scene.tx_state(tx[1], grid)
+    _, r = scene.render_queries(cond, st, rx, want=("rssi",))
+    assert rel_err(table[1], r).max() < 1e-5
