@@ -482,6 +482,7 @@ int rxgs_scene_create(rxgs_ctx ctx, int k, int l_max, int channels, int modality
             if (e2 != cudaSuccess) rc = cuda_fail(e2, "scene pos32 copy");
         }
     }
+    if (!rc) rc = build_scene_order(ctx, *sc, ctx->stream);
     if (rc) {
         delete sc;
         return rc;
@@ -598,7 +599,7 @@ int rxgs_tx_state_build(rxgs_ctx ctx, rxgs_scene sc, const double tx[3], const r
     }
     timing_end(ctx, "walk", ev, static_cast<double>(cells));
     {
-        const int rc = compact_needed(ctx, *st, s);
+        const int rc = compact_needed(ctx, *sc, *st, s);
         if (rc) return fail_st(rc);
     }
     ctx->launches += 1;

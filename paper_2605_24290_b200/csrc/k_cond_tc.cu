@@ -3,27 +3,41 @@
 // Same math as k_cond_signal (k_cond.cu): per (Gaussian k, receiver j) row
 // the local features + occupancy probe, the local MLP 6 -> 64 -> 64 -> 4 and
 // the fused affine + FLE reduction (conditioning.cpp:369-421 with
-// reduce_signals, sphraster.cpp:190-226).  The 64x64 hidden layer (86% of
-// the MLP FLOPs) runs on tcgen05:
-//   * a CTA owns the whole SM (512 threads = 4 independent 128-row groups);
-//     each group's 128 rows map 1:1 to the 128 TMEM lanes;
-//   * every thread writes its row of h1 = relu(W1 x + b1), split into bf16
-//     hi + lo parts, straight into TMEM with tcgen05.st (A operand in TMEM:
-//     no shared-memory staging);
-//   * W2 (hi/lo, bf16, no-swizzle K-major core matrices) sits in shared
-//     memory for the whole kernel;
-//   * one elected thread per group issues 12 tcgen05.mma (4 K-steps x
-//     {hi*hi, hi*lo, lo*hi}: ~2^-17 relative error, FP32-class accuracy for
-//     the 1e-4 parity bar) into a 64-column FP32 accumulator, commits to the
-//     group's mbarrier; the group reads the accumulator back with tcgen05.ld;
-//   * layers 1 and 3 and the biases are FFMAs with constant-bank operands
-//     (the weights travel as a __grid_constant__ kernel parameter);
-//   * while one group waits on its MMAs the other three run their SIMT parts.
+// reduce_signals, sphraster.cpp:190-226).
+//
+// Row mapping.  A CTA owns the whole SM: 512 threads = 4 independent groups
+// of 128 rows, one row per TMEM lane.  Within a group's 128-row tile, warp w
+// takes receiver 4*jq + w and lane i takes conditioning row 32*gb + i, where
+// rows are the Gaussians the walk reaches in the scene's Morton order
+// (compact_needed).  The 32 probes of a warp therefore run from 32
+// neighbouring Gaussians to one receiver: every trilinear corner load of the
+// warp falls in a ~3^3-voxel neighbourhood, i.e. distinct shared-memory
+// banks (the padded grid's strides are 9 and 3 banks), instead of 32
+// segments fanning out from one Gaussian to 32 receivers across the room.
+// Per-row Tx data (basis, basis*base, basis sum, position) is gathered once
+// per launch into row order, transposed to [l][row], so the FLE loads are
+// coalesced 256-byte warp loads.
+//
+// Per tile:
+//   * layer 1 on tcgen05: A = [x, 1, 0..] (K = 16, bias as a constant-1
+//     feature) as bf16 hi/lo in TMEM, W1|b1 hi/lo in shared memory;
+//   * ReLU(h1) -> bf16 hi/lo -> TMEM (layer-2 A operand);
+//   * layer 2 on tcgen05: D = 1*b2 (constant-A K-step from shared memory,
+//     bias folded into the MMA) + Ahi Bhi + Ahi Blo + Alo Bhi over 4 K-steps
+//     (~2^-17 relative error: FP32-class accuracy for the 1e-4 parity bar);
+//   * ReLU(h2) and layer 3 (4 outputs) as FFMAs with constant-bank weights;
+//   * the FLE reduction and the affine, one scattered 8-byte signal store.
+// While one group waits on its MMAs the other three run their SIMT parts.
+// The occupancy probe takes a clamp-free, fully unrolled path when all 32
+// segments of the warp lie inside the padded grid (the usual case: receivers
+// and Gaussians inside the occupancy box), else a rolled clamped loop.
 // TMEM: 512 columns per CTA = 4 groups x (64 accumulator + 32 A-hi + 32 A-lo).
-// Shared memory: W2 hi/lo (16 KB) + the occupancy grid (R^3 FP32, 128 KB).
+// Shared memory: W2 hi/lo (16 KB), W1 hi/lo (4 KB), b2 hi/lo + the constant
+// A tile (8 KB), the zero-bordered occupancy grid ((R+3)^3 FP32, 168 KB).
 #include "cond_common.cuh"
 #include "rxgs_internal.cuh"
 #include "tc_util.cuh"
+#include "f32x2.cuh"
 
 namespace rxgs_b200 {
 namespace {
@@ -34,15 +48,16 @@ constexpr int kH = 64;
 constexpr int kGroups = 4;
 constexpr int kThreads = 128 * kGroups;
 constexpr uint32_t kIdesc = tc::idesc_bf16_f32(128, kH);
-constexpr int kW2Bytes = kH * kH * 2;  // one bf16 64x64 matrix
-constexpr int kW1Bytes = kH * 16 * 2;  // one bf16 64x16 matrix
+constexpr int kW2Bytes = kH * kH * 2;   // one bf16 64x64 matrix
+constexpr int kW1Bytes = kH * 16 * 2;   // one bf16 64x16 matrix
+constexpr int kA1Bytes = 128 * 16 * 2;  // one bf16 128x16 matrix
+constexpr int kFixedSmem = 2 * kW2Bytes + 4 * kW1Bytes + kA1Bytes;
 
 struct LocalW {
-    float w1[kH * 6];
-    float b1[kH];
-    float b2[kH];
-    float w3[4 * kH];
+    float4 w3[kH];  // layer-3 column o: (W3[0][o], W3[1][o], W3[2][o], W3[3][o])
     float b3[4];
+    float icell[3];  // 1 / voxel size
+    float blo[3];    // (lo / cell) + 0.5: voxel coordinate u = p * icell - blo
 };
 
 // byte offset of element (row r, k) in a no-swizzle K-major canonical tile
@@ -64,21 +79,135 @@ __device__ __forceinline__ void split_store(uint8_t* hi_base, uint8_t* lo_base, 
     *reinterpret_cast<uint16_t*>(lo_base + off) = static_cast<uint16_t>(tc::pack_bf16(w - hi, 0.f) & 0xFFFFu);
 }
 
-// YOUT: rows are all K Gaussians (vis unused) and the local-branch output
+// Trilinear occupancy probe of one segment on the zero-bordered grid
+// (probe_segment, conditioning.cpp:163-178; sample_trilinear :74-98).  u =
+// b + t s in voxel units.  CLAMP keeps every corner inside the padded grid
+// (a clamped axis lands on the zero border with weight 1: the reference's
+// "out-of-bounds corners read 0"); without it the caller guarantees both
+// end samples -- hence, by monotonicity of fmaf in t, all samples -- are in
+// [-1, R] on every axis.
+template <int ST, int RT, bool CLAMP>
+__device__ __forceinline__ void probe_seg(const float* occ, int R, int S, float b0, float b1, float b2, float s0,
+                                          float s1, float s2, float& tr, float& sum) {
+    const int P = padded_dim(RT > 0 ? RT : R);
+    const float hi = static_cast<float>(RT > 0 ? RT : R);
+    const float cidx = static_cast<float>(P * P + P + 1);  // the +1 border offset of each axis
+    const int NS = ST > 0 ? ST : S;
+    const float dt = NS == 1 ? 0.f : 0.9f / static_cast<float>(NS - 1);
+#pragma unroll(CLAMP ? 1 : (ST > 0 ? ST : 1))
+    for (int si = 0; si < NS; ++si) {
+        const float t = NS == 1 ? 0.5f : fmaf(static_cast<float>(si), dt, 0.05f);
+        float u0 = fmaf(t, s0, b0), u1 = fmaf(t, s1, b1), u2 = fmaf(t, s2, b2);
+        if (CLAMP) {
+            u0 = fminf(fmaxf(u0, -1.f), hi);
+            u1 = fminf(fmaxf(u1, -1.f), hi);
+            u2 = fminf(fmaxf(u2, -1.f), hi);
+        }
+        const float f0 = floorf(u0), f1 = floorf(u1), f2 = floorf(u2);
+        const float w0 = u0 - f0, w1 = u1 - f1, w2 = u2 - f2;
+        // padded linear index, exact in FP32 (P^3 < 2^24)
+        const int idx =
+            static_cast<int>(fmaf(f0, static_cast<float>(P * P), fmaf(f1, static_cast<float>(P), f2 + cidx)));
+        const float* q = occ + idx;
+        const float c00 = fmaf(w2, q[1] - q[0], q[0]);
+        const float c01 = fmaf(w2, q[P + 1] - q[P], q[P]);
+        const float c10 = fmaf(w2, q[P * P + 1] - q[P * P], q[P * P]);
+        const float c11 = fmaf(w2, q[P * P + P + 1] - q[P * P + P], q[P * P + P]);
+        const float c0 = fmaf(w1, c01 - c00, c00);
+        const float c1 = fmaf(w1, c11 - c10, c10);
+        const float v = fmaf(w0, c1 - c0, c0);
+        tr *= 1.f - v;
+        sum += v;
+    }
+}
+
+// The clamp-free probe, two samples per instruction (FFMA2/FADD2/FMUL2):
+// lanes .x / .y of every float2 are samples 2i and 2i+1.  The transmittance
+// is accumulated as two interleaved products, multiplied at the end.
+template <int ST, int RT>
+__device__ __forceinline__ void probe_seg_x2(const float* occ, float b0, float b1, float b2, float s0, float s1,
+                                             float s2, float& tr, float& sum) {
+    static_assert(ST >= 2 && ST % 2 == 0 && RT > 0, "paired probe needs an even, static sample count");
+    constexpr int P = padded_dim(RT);
+    constexpr float cidx = static_cast<float>(P * P + P + 1);
+    constexpr float dt = 0.9f / static_cast<float>(ST - 1);
+    float2 tr2 = make_float2(1.f, 1.f), sum2 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int sp = 0; sp < ST / 2; ++sp) {
+        const float2 t = make_float2(fmaf(static_cast<float>(2 * sp), dt, 0.05f),
+                                     fmaf(static_cast<float>(2 * sp + 1), dt, 0.05f));
+        const float2 u0 = x2::fma(t, x2::bc(s0), x2::bc(b0));
+        const float2 u1 = x2::fma(t, x2::bc(s1), x2::bc(b1));
+        const float2 u2 = x2::fma(t, x2::bc(s2), x2::bc(b2));
+        const float2 f0 = make_float2(floorf(u0.x), floorf(u0.y));
+        const float2 f1 = make_float2(floorf(u1.x), floorf(u1.y));
+        const float2 f2 = make_float2(floorf(u2.x), floorf(u2.y));
+        const float2 w0 = x2::sub(u0, f0), w1 = x2::sub(u1, f1), w2 = x2::sub(u2, f2);
+        const float2 fi = x2::fma(f0, x2::bc(static_cast<float>(P * P)),
+                                  x2::fma(f1, x2::bc(static_cast<float>(P)), x2::add(f2, x2::bc(cidx))));
+        const float* qa = occ + static_cast<int>(fi.x);
+        const float* qb = occ + static_cast<int>(fi.y);
+        const float2 q000 = make_float2(qa[0], qb[0]), q001 = make_float2(qa[1], qb[1]);
+        const float2 q010 = make_float2(qa[P], qb[P]), q011 = make_float2(qa[P + 1], qb[P + 1]);
+        const float2 q100 = make_float2(qa[P * P], qb[P * P]), q101 = make_float2(qa[P * P + 1], qb[P * P + 1]);
+        const float2 q110 = make_float2(qa[P * P + P], qb[P * P + P]);
+        const float2 q111 = make_float2(qa[P * P + P + 1], qb[P * P + P + 1]);
+        const float2 c00 = x2::fma(w2, x2::sub(q001, q000), q000);
+        const float2 c01 = x2::fma(w2, x2::sub(q011, q010), q010);
+        const float2 c10 = x2::fma(w2, x2::sub(q101, q100), q100);
+        const float2 c11 = x2::fma(w2, x2::sub(q111, q110), q110);
+        const float2 c0 = x2::fma(w1, x2::sub(c01, c00), c00);
+        const float2 c1 = x2::fma(w1, x2::sub(c11, c10), c10);
+        const float2 v = x2::fma(w0, x2::sub(c1, c0), c0);
+        tr2 = x2::mul(tr2, x2::sub(x2::bc(1.f), v));
+        sum2 = x2::add(sum2, v);
+    }
+    tr = tr2.x * tr2.y;
+    sum = sum2.x + sum2.y;
+}
+
+// Gathers the per-row Tx data of the needed rows: position, (basis*base,
+// basis) transposed to [l][row] as float4, and the sums over l of both.
+__global__ void k_gather_rows(const int* __restrict__ n_rows, const int* __restrict__ rows, int cap, int L,
+                              const float4* __restrict__ pos32, const float2* __restrict__ B,
+                              const float2* __restrict__ GB, float4* __restrict__ rpos, float4* __restrict__ rGB,
+                              float4* __restrict__ rS) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= *n_rows) return;
+    const int k = rows[r];
+    rpos[r] = pos32[k];
+    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int l = 0; l < L; ++l) {
+        const float2 b = B[static_cast<size_t>(k) * L + l];
+        const float2 gb = GB[static_cast<size_t>(k) * L + l];
+        rGB[static_cast<size_t>(l) * cap + r] = make_float4(gb.x, gb.y, b.x, b.y);
+        sum.x += gb.x;
+        sum.y += gb.y;
+        sum.z += b.x;
+        sum.w += b.y;
+    }
+    rS[r] = sum;
+}
+
+// YOUT: rows are all K Gaussians (Morton order) and the local-branch output
 // y = (alpha_L, beta_L) is written to ycache[k][j] instead of the signal (the
 // Tx-independent cache of the coverage workload).
 template <int ST, int RT, bool YOUT>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_cond_tc(const __grid_constant__ LocalW W, CondDev c, const int* __restrict__ n_rows, const int* __restrict__ vis,
-              const float4* __restrict__ pos32, const double* __restrict__ rx, int n_rx,
-              const float2* __restrict__ Bm, const float2* __restrict__ GB, const float* __restrict__ ag,
-              float2* __restrict__ sig, float4* __restrict__ ycache, int n_all) {
+    k_cond_tc(const __grid_constant__ LocalW W, CondDev c, const int* __restrict__ n_rows_dev, int n_rows_host,
+              int cap, const int* __restrict__ rows, const float4* __restrict__ rpos, const double* __restrict__ rx,
+              int n_rx, const float4* __restrict__ rGB, const float4* __restrict__ rS,
+              const float* __restrict__ ag, float2* __restrict__ sig,
+              float4* __restrict__ ycache) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* w2hi = smem;
     uint8_t* w2lo = smem + kW2Bytes;
-    uint8_t* w1hi = smem + 2 * kW2Bytes;           // [W1 | b1 | 0] : 64 x 16 bf16
+    uint8_t* w1hi = smem + 2 * kW2Bytes;  // [W1 | b1 | 0] : 64 x 16 bf16
     uint8_t* w1lo = w1hi + kW1Bytes;
-    float* s_occ = reinterpret_cast<float*>(smem + 2 * kW2Bytes + 2 * kW1Bytes);
+    uint8_t* b2hi = w1lo + kW1Bytes;      // [b2 | 0] : 64 x 16 bf16
+    uint8_t* b2lo = b2hi + kW1Bytes;
+    uint8_t* aone = b2lo + kW1Bytes;      // [1 | 0] : 128 x 16 bf16
+    float* s_occ = reinterpret_cast<float*>(smem + kFixedSmem);
     __shared__ uint64_t bars[kGroups];
     __shared__ uint32_t tbase_s;
 
@@ -86,12 +215,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = tid >> 5, lane = tid & 31;
     const int g = warp >> 2, wl = warp & 3;
 
-    // ---- one-time setup: W1 (+bias column) and W2 as bf16 hi/lo core matrices, occupancy
+    // ---- one-time setup: weights as bf16 hi/lo core matrices, occupancy
     for (int i = tid; i < kH * kH; i += kThreads) split_store(w2hi, w2lo, canon_off(i / kH, i % kH), c.p32[c.o_lw2 + i]);
     for (int i = tid; i < kH * 16; i += kThreads) {
         const int n = i / 16, k = i % 16;
         const float w = k < 6 ? c.p32[c.o_lw1 + n * 6 + k] : (k == 6 ? c.p32[c.o_lb1 + n] : 0.f);
         split_store(w1hi, w1lo, canon_off16(n, k), w);
+        split_store(b2hi, b2lo, canon_off16(n, k), k == 0 ? c.p32[c.o_lb2 + n] : 0.f);
+    }
+    for (int i = tid; i < 128 * 16; i += kThreads) {
+        const int r = i / 16, k = i % 16;
+        *reinterpret_cast<uint16_t*>(aone + canon_off16(r, k)) = k == 0 ? 0x3F80u : 0u;  // bf16 1.0
     }
     if (c.probe) load_padded_occ(c, s_occ);
     if (warp == 0) {
@@ -114,39 +248,109 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tm_alo = tm_d + 96;
     const uint32_t w2hi_a = tc::smem_u32(w2hi), w2lo_a = tc::smem_u32(w2lo);
     const uint32_t w1hi_a = tc::smem_u32(w1hi), w1lo_a = tc::smem_u32(w1lo);
+    const uint32_t b2hi_a = tc::smem_u32(b2hi), b2lo_a = tc::smem_u32(b2lo), aone_a = tc::smem_u32(aone);
 
-    const int n_jc = (n_rx + 31) >> 5;
-    const long long items = static_cast<long long>(YOUT ? n_all : *n_rows) * n_jc;
-    const long long tiles = (items + 3) >> 2;
+    const int n_rows = YOUT ? n_rows_host : *n_rows_dev;
+    const int nq = (n_rx + 3) >> 2;
+    const long long tiles = static_cast<long long>((n_rows + 31) >> 5) * nq;
     const long long step = static_cast<long long>(gridDim.x) * kGroups;
     const int L = c.L;
+    const int R = RT > 0 ? RT : c.R;
+    const float hiR = static_cast<float>(R);
+    const int S = ST > 0 ? ST : c.S;
+    const float tlast = S == 1 ? 0.5f : fmaf(static_cast<float>(S - 1), 0.9f / static_cast<float>(S - 1), 0.05f);
+    const float tfirst = S == 1 ? 0.5f : 0.05f;
     uint32_t phase = 0;
 
-    for (long long tile = static_cast<long long>(blockIdx.x) * kGroups + g; tile < tiles; tile += step) {
-        const long long item = tile * 4 + wl;
-        const bool valid_item = item < items;
-        const int vi = valid_item ? static_cast<int>(item / n_jc) : 0;
-        const int jc = valid_item ? static_cast<int>(item % n_jc) : 0;
-        const int j = jc * 32 + lane;
-        const bool active = valid_item && j < n_rx;
-        const int k = valid_item ? (YOUT ? vi : vis[vi]) : 0;
-
-        float in[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        if (active) {
-            const float4 pk = pos32[k];
-            local_features<true, ST, RT>(c, s_occ, pk.x, pk.y, pk.z, static_cast<float>(rx[3 * j]),
-                                         static_cast<float>(rx[3 * j + 1]), static_cast<float>(rx[3 * j + 2]), in);
+    // tile -> (row r, receiver j) of this thread
+    auto coords = [&](long long tile, int& r, int& j) {
+        const int gb = static_cast<int>(tile / nq);
+        const int jq = static_cast<int>(tile - static_cast<long long>(gb) * nq);
+        r = gb * 32 + lane;
+        j = jq * 4 + wl;
+    };
+    // local features [v_hat, d, T, rho] of one row (conditioning.cpp:377-396)
+    auto features = [&](bool active, float4 pk, float qx, float qy, float qz, float* in) {
+        const float px = active ? pk.x : 0.f, py = active ? pk.y : 0.f, pz = active ? pk.z : 0.f;
+        if (!active) {
+            qx = 1.f;
+            qy = qz = 0.f;
         }
+        const float dx = qx - px, dy = qy - py, dz = qz - pz;
+        const float d = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+        const float inv = 1.f / d;
+        in[0] = dx * inv;
+        in[1] = dy * inv;
+        in[2] = dz * inv;
+        in[3] = d;
+        float T = 1.f, rho = 0.f;
+        if (c.probe) {
+            const float b0 = fmaf(px, W.icell[0], -W.blo[0]), b1 = fmaf(py, W.icell[1], -W.blo[1]),
+                        b2 = fmaf(pz, W.icell[2], -W.blo[2]);
+            const float s0 = dx * W.icell[0], s1 = dy * W.icell[1], s2 = dz * W.icell[2];
+            auto inside = [&](float t) {
+                const float u0 = fmaf(t, s0, b0), u1 = fmaf(t, s1, b1), u2 = fmaf(t, s2, b2);
+                return u0 >= -1.f && u0 <= hiR && u1 >= -1.f && u1 <= hiR && u2 >= -1.f && u2 <= hiR;
+            };
+            const bool ok = !active || (inside(tfirst) && inside(tlast));
+            float tr = 1.f, sum = 0.f;
+            if (__all_sync(0xffffffffu, ok)) {
+                if constexpr (ST >= 2 && ST % 2 == 0 && RT > 0) {
+                    if (active) probe_seg_x2<ST, RT>(s_occ, b0, b1, b2, s0, s1, s2, tr, sum);
+                } else {
+                    if (active) probe_seg<ST, RT, false>(s_occ, R, S, b0, b1, b2, s0, s1, s2, tr, sum);
+                }
+            } else if (active) {
+                probe_seg<ST, RT, true>(s_occ, R, S, b0, b1, b2, s0, s1, s2, tr, sum);
+            }
+            T = tr;
+            rho = sum * (1.f / static_cast<float>(S));
+        }
+        in[4] = T;
+        in[5] = rho;
+    };
+
+    long long tile = static_cast<long long>(blockIdx.x) * kGroups + g;
+    int r = 0, j = 0;
+    float in[6];
+    if (tile < tiles) {  // prologue: features of the first tile
+        coords(tile, r, j);
+        const bool act = r < n_rows && j < n_rx;
+        float4 pk = make_float4(0.f, 0.f, 0.f, 0.f);
+        float qx = 0.f, qy = 0.f, qz = 0.f;
+        if (act) {
+            pk = rpos[r];
+            qx = static_cast<float>(rx[3 * j]);
+            qy = static_cast<float>(rx[3 * j + 1]);
+            qz = static_cast<float>(rx[3 * j + 2]);
+        }
+        features(act, pk, qx, qy, qz, in);
+    }
+    for (; tile < tiles; tile += step) {
+        const bool active = r < n_rows && j < n_rx;
+        const long long ntile = tile + step;
+        int rn = 0, jn = 0;
+        coords(ntile, rn, jn);
+        const bool nact = ntile < tiles && rn < n_rows && jn < n_rx;
+        // prefetch the next tile's row position / receiver and this row's output index
+        float4 pkn = make_float4(0.f, 0.f, 0.f, 0.f);
+        double qxn = 0.0, qyn = 0.0, qzn = 0.0;
+        if (nact) {
+            pkn = rpos[rn];
+            qxn = rx[3 * jn];
+            qyn = rx[3 * jn + 1];
+            qzn = rx[3 * jn + 2];
+        }
+        const int k = active ? rows[r] : 0;
         // ---- layer 1 on the tensor cores: A1 = [x, 1, 0...] (K = 16) hi/lo -> TMEM
         {
             uint32_t hi[8], lo[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const float xa = 2 * q < 6 ? in[2 * q] : (2 * q == 6 ? 1.f : 0.f);
-                const float xb = 2 * q + 1 < 6 ? in[2 * q + 1] : 0.f;
-                hi[q] = tc::pack_bf16(xa, xb);
-                lo[q] = tc::pack_bf16(xa - __uint_as_float(hi[q] << 16), xb - __uint_as_float(hi[q] & 0xFFFF0000u));
-            }
+            for (int q = 0; q < 3; ++q) x2::split_bf16(in[2 * q], in[2 * q + 1], hi[q], lo[q]);
+            hi[3] = 0x3F80u;  // (1, 0): the bias feature
+            lo[3] = 0u;
+#pragma unroll
+            for (int q = 4; q < 8; ++q) hi[q] = lo[q] = 0u;
             tc::tmem_st8(tm_ahi + lane_off, hi);
             tc::tmem_st8(tm_alo + lane_off, lo);
         }
@@ -162,69 +366,116 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mma_ts(tm_d, tm_alo, bh, kIdesc, 1u);
             tc::mma_commit(&bars[g]);
         }
+        // ---- overlaps the layer-1 MMA: the next tile's features and probe
+        float inn[6];
+        if (ntile < tiles)
+            features(nact, pkn, static_cast<float>(qxn), static_cast<float>(qyn), static_cast<float>(qzn), inn);
         tc::mbar_wait(&bars[g], phase);
         phase ^= 1u;
         tc::fence_after_sync();
         // ---- ReLU(h1) -> bf16 hi/lo -> TMEM (layer-2 A operand; overwrites A1)
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) {
-            uint32_t r[16];
-            tc::tmem_ld16(tm_d + lane_off + 16 * ch, r);
+            uint32_t v[16];
+            tc::tmem_ld16(tm_d + lane_off + 16 * ch, v);
             tc::wait_ld();
             uint32_t hi[8], lo[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const float ha = fmaxf(__uint_as_float(r[2 * q]), 0.f);
-                const float hb = fmaxf(__uint_as_float(r[2 * q + 1]), 0.f);
-                hi[q] = tc::pack_bf16(ha, hb);
-                lo[q] = tc::pack_bf16(ha - __uint_as_float(hi[q] << 16), hb - __uint_as_float(hi[q] & 0xFFFF0000u));
-            }
+            for (int q = 0; q < 8; ++q)
+                x2::relu_split_bf16(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]), hi[q], lo[q]);
             tc::tmem_st8(tm_ahi + lane_off + 8 * ch, hi);
             tc::tmem_st8(tm_alo + lane_off + 8 * ch, lo);
         }
         tc::wait_st();
         tc::fence_before_sync();
         tc::named_bar_sync(1 + g, 128);
-        // ---- layer 2 on the tensor cores: D = Ahi Bhi + Ahi Blo + Alo Bhi
+        // ---- layer 2 on the tensor cores: D = 1 b2 + Ahi Bhi + Ahi Blo + Alo Bhi
         if (wl == 0 && lane == 0) {
             tc::fence_after_sync();
+            const uint64_t ad = tc::sdesc_kmajor_noswizzle(aone_a, 128, 256);
+            tc::mma_ss(tm_d, ad, tc::sdesc_kmajor_noswizzle(b2hi_a, 128, 256), kIdesc, 0u);
+            tc::mma_ss(tm_d, ad, tc::sdesc_kmajor_noswizzle(b2lo_a, 128, 256), kIdesc, 1u);
 #pragma unroll
             for (int s = 0; s < 4; ++s) {
                 const uint64_t bh = tc::sdesc_kmajor_noswizzle(w2hi_a + 256 * s, 128, 1024);
                 const uint64_t bl = tc::sdesc_kmajor_noswizzle(w2lo_a + 256 * s, 128, 1024);
-                tc::mma_ts(tm_d, tm_ahi + 8 * s, bh, kIdesc, s > 0 ? 1u : 0u);
+                tc::mma_ts(tm_d, tm_ahi + 8 * s, bh, kIdesc, 1u);
                 tc::mma_ts(tm_d, tm_ahi + 8 * s, bl, kIdesc, 1u);
                 tc::mma_ts(tm_d, tm_alo + 8 * s, bh, kIdesc, 1u);
             }
             tc::mma_commit(&bars[g]);
         }
-        // FLE reduction (global loads) overlaps the layer-2 MMAs
+        // ---- overlaps the layer-2 MMA: M = sum_l [(1+aG_l) GB_l + bG_l B_l]
+        // (fle_reduce, cond_common.cuh) as sum_l GB_l + sum_l [aG_l GB_l + bG_l B_l],
+        // complex products on FFMA2 (i z = (-z.y, z.x) via swapped / negated operands)
+        float2 M = make_float2(0.f, 0.f), Bs = make_float2(0.f, 0.f);
+        if (!YOUT && active) {
+            const float4 sums = rS[r];
+            M = make_float2(sums.x, sums.y);
+            Bs = make_float2(sums.z, sums.w);
+            const float4* a4 = reinterpret_cast<const float4*>(ag) + static_cast<size_t>(j) * L;
+            const float4* e4 = rGB + r;
+            int l = 0;
+            for (; l + 3 <= L; l += 3) {
+                float4 e[3], a[3];
+#pragma unroll
+                for (int u = 0; u < 3; ++u) {
+                    e[u] = e4[static_cast<size_t>(l + u) * cap];
+                    a[u] = a4[l + u];
+                }
+#pragma unroll
+                for (int u = 0; u < 3; ++u) {
+                    M = x2::fma(x2::bc(a[u].x), make_float2(e[u].x, e[u].y), M);
+                    M = x2::fma(make_float2(e[u].y, e[u].x), make_float2(-a[u].y, a[u].y), M);
+                    M = x2::fma(x2::bc(a[u].z), make_float2(e[u].z, e[u].w), M);
+                    M = x2::fma(make_float2(e[u].w, e[u].z), make_float2(-a[u].w, a[u].w), M);
+                }
+            }
+            for (; l < L; ++l) {
+                const float4 e = e4[static_cast<size_t>(l) * cap];
+                const float4 a = a4[l];
+                M = x2::fma(x2::bc(a.x), make_float2(e.x, e.y), M);
+                M = x2::fma(make_float2(e.y, e.x), make_float2(-a.y, a.y), M);
+                M = x2::fma(x2::bc(a.z), make_float2(e.z, e.w), M);
+                M = x2::fma(make_float2(e.w, e.z), make_float2(-a.w, a.w), M);
+            }
+        }
         tc::mbar_wait(&bars[g], phase);
         phase ^= 1u;
         tc::fence_after_sync();
-        // ---- layer-2 bias + ReLU, layer 3 (FFMA) from the TMEM accumulator
-        float y[4] = {W.b3[0], W.b3[1], W.b3[2], W.b3[3]};
+        // ---- ReLU(h2), layer 3 on FFMA2 from the TMEM accumulator
+        float2 ya = make_float2(W.b3[0], W.b3[1]), yb = make_float2(W.b3[2], W.b3[3]);
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) {
-            uint32_t r[16];
-            tc::tmem_ld16(tm_d + lane_off + 16 * ch, r);
+            uint32_t v[16];
+            tc::tmem_ld16(tm_d + lane_off + 16 * ch, v);
             tc::wait_ld();
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
-                const int o = 16 * ch + q;
-                const float h2 = fmaxf(__uint_as_float(r[q]) + W.b2[o], 0.f);
-#pragma unroll
-                for (int t = 0; t < 4; ++t) y[t] = fmaf(W.w3[t * kH + o], h2, y[t]);
+                const float4 w3 = W.w3[16 * ch + q];
+                const float2 h2 = x2::bc(fmaxf(__uint_as_float(v[q]), 0.f));
+                ya = x2::fma(h2, make_float2(w3.x, w3.y), ya);
+                yb = x2::fma(h2, make_float2(w3.z, w3.w), yb);
             }
         }
         tc::fence_before_sync();  // the next tile's layer-1 MMA overwrites D after the barrier
-        if (YOUT) {
-            if (active) ycache[static_cast<size_t>(k) * n_rx + j] = make_float4(y[0], y[1], y[2], y[3]);
-        } else if (active) {  // FLE reduction after the MMAs (measured faster than overlapping them)
-            float2 M, Bs;
-            fle_reduce(k, j, 0, L, 1, Bm, GB, ag, M, Bs);
-            sig[static_cast<size_t>(k) * n_rx + j] = local_affine(c, 0, M, Bs, y);
+        if (active) {
+            if (YOUT) {
+                ycache[static_cast<size_t>(k) * n_rx + j] = make_float4(ya.x, ya.y, yb.x, yb.y);
+            } else {
+                // s = (1 + aL) M + bL Bs (local_affine; additive mode: aL = 0)
+                const float2 al = c.additive ? make_float2(0.f, 0.f) : ya;
+                float2 sg = x2::fma(x2::bc(al.x), M, M);
+                sg = x2::fma(make_float2(M.y, M.x), make_float2(-al.y, al.y), sg);
+                sg = x2::fma(x2::bc(yb.x), Bs, sg);
+                sg = x2::fma(make_float2(Bs.y, Bs.x), make_float2(-yb.y, yb.y), sg);
+                sig[static_cast<size_t>(k) * n_rx + j] = sg;
+            }
         }
+        r = rn;
+        j = jn;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) in[q] = inn[q];
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -323,41 +574,42 @@ __global__ void __launch_bounds__(128) k_tc_selftest(float* __restrict__ err, in
 }  // namespace
 
 bool cond_tc_eligible(const rxgs_cond_s* c) {
-    return c && c->use_local() && c->hidden == kH && c->C == 1 && padded_dim(c->R) * padded_dim(c->R) * padded_dim(c->R) <= 48000;
+    return c && c->use_local() && c->hidden == kH && c->C == 1 && !c->nearest &&
+           kFixedSmem + padded_dim(c->R) * padded_dim(c->R) * padded_dim(c->R) * 4 <= 227 * 1024;
 }
 
 namespace {
 
 template <bool YOUT>
-cudaError_t launch_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const int* n_rows, const int* vis,
-                      long long rows_host, const double* d_rx, int n_rx, const float2* basis32, const float2* gb32,
+cudaError_t launch_tc(const rxgs_cond_s& cs, const int* n_rows_dev, long long rows_host, int cap, const int* rows,
+                      const float4* rpos, const double* d_rx, int n_rx, const float4* rGB, const float4* rS,
                       const float* d_ag, float2* d_sig, float4* ycache, cudaStream_t s) {
     if (rows_host == 0 || n_rx == 0) return cudaSuccess;
     const CondDev d = make_dev(cs);
     LocalW w{};
     const std::vector<double>& p = cs.h_params;
-    for (int i = 0; i < kH * 6; ++i) w.w1[i] = static_cast<float>(p[cs.o_lw1 + i]);
-    for (int i = 0; i < kH; ++i) {
-        w.b1[i] = static_cast<float>(p[cs.o_lb1 + i]);
-        w.b2[i] = static_cast<float>(p[cs.o_lb2 + i]);
-    }
-    for (int i = 0; i < 4 * kH; ++i) w.w3[i] = static_cast<float>(p[cs.o_lw3 + i]);
+    for (int o = 0; o < kH; ++o)
+        w.w3[o] = make_float4(static_cast<float>(p[cs.o_lw3 + o]), static_cast<float>(p[cs.o_lw3 + kH + o]),
+                              static_cast<float>(p[cs.o_lw3 + 2 * kH + o]), static_cast<float>(p[cs.o_lw3 + 3 * kH + o]));
     for (int i = 0; i < 4; ++i) w.b3[i] = static_cast<float>(p[cs.o_lb3 + i]);
+    for (int a = 0; a < 3; ++a) {
+        w.icell[a] = 1.f / d.cell[a];
+        w.blo[a] = d.lo[a] * w.icell[a] + 0.5f;
+    }
     const size_t P = static_cast<size_t>(padded_dim(d.R));
-    const size_t smem = 2 * kW2Bytes + 2 * kW1Bytes + (d.probe ? P * P * P * sizeof(float) : 0);
+    const size_t smem = kFixedSmem + (d.probe ? P * P * P * sizeof(float) : 0);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const long long items = rows_host * ((n_rx + 31) / 32);
-    const long long tiles = (items + 3) / 4;
+    const long long tiles = ((rows_host + 31) / 32) * ((n_rx + 3) / 4);
     const long long want = (tiles + kGroups - 1) / kGroups;
     const int blocks = static_cast<int>(want < sms ? want : sms);
-    const bool fast = d.S == 16 && d.R == 32 && !d.nearest;
+    const bool fast = d.S == 16 && d.R == 32;
     auto kern = fast ? k_cond_tc<16, 32, YOUT> : k_cond_tc<0, 0, YOUT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    kern<<<blocks, kThreads, smem, s>>>(w, d, n_rows, vis, sc.d_pos32.as<float4>(), d_rx, n_rx, basis32, gb32, d_ag,
-                                        d_sig, ycache, static_cast<int>(rows_host));
+    kern<<<blocks, kThreads, smem, s>>>(w, d, n_rows_dev, static_cast<int>(rows_host), cap, rows, rpos, d_rx, n_rx,
+                                        rGB, rS, d_ag, d_sig, ycache);
     return cudaGetLastError();
 }
 
@@ -366,13 +618,30 @@ cudaError_t launch_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const int* 
 cudaError_t launch_cond_signal_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
                                   const double* d_rx, int n_rx, const float* d_ag, float2* d_sig,
                                   cudaStream_t s) {
-    return launch_tc<false>(cs, sc, st.needed_count.as<int>(), st.needed_order.as<int>(), st.visible, d_rx, n_rx,
-                            st.basis32.as<float2>(), st.gb32.as<float2>(), d_ag, d_sig, nullptr, s);
+    if (st.visible == 0 || n_rx == 0) return cudaSuccess;
+    rxgs_ctx ctx = sc.ctx;
+    const int cap = st.k;
+    const int L = st.L;
+    cudaError_t e;
+    if ((e = ctx->row_pos.ensure(sizeof(float4) * cap)) != cudaSuccess) return e;
+    if ((e = ctx->row_GB.ensure(sizeof(float4) * cap * L)) != cudaSuccess) return e;
+    if ((e = ctx->row_S.ensure(sizeof(float4) * cap)) != cudaSuccess) return e;
+    const int* n_rows = st.needed_count.as<int>();
+    const int* rows = st.needed_order.as<int>();
+    const long long bound = st.needed_host >= 0 ? st.needed_host : st.visible;
+    k_gather_rows<<<static_cast<unsigned>((bound + 255) / 256), 256, 0, s>>>(
+        n_rows, rows, cap, L, sc.d_pos32.as<float4>(), st.basis32.as<float2>(), st.gb32.as<float2>(),
+        ctx->row_pos.as<float4>(), ctx->row_GB.as<float4>(), ctx->row_S.as<float4>());
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ctx->launches += 1;
+    return launch_tc<false>(cs, n_rows, bound, cap, rows, ctx->row_pos.as<float4>(), d_rx, n_rx,
+                            ctx->row_GB.as<float4>(), ctx->row_S.as<float4>(), d_ag, d_sig, nullptr, s);
 }
 
 cudaError_t launch_local_cache_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const double* d_rx, int n_rx,
                                   float4* ycache, cudaStream_t s) {
-    return launch_tc<true>(cs, sc, nullptr, nullptr, sc.k, d_rx, n_rx, nullptr, nullptr, nullptr, nullptr, ycache, s);
+    return launch_tc<true>(cs, nullptr, sc.k, sc.k, sc.d_morton.as<int>(), sc.d_mpos32.as<float4>(), d_rx, n_rx,
+                           nullptr, nullptr, nullptr, nullptr, ycache, s);
 }
 
 cudaError_t launch_tc_selftest(float* d_err, cudaStream_t s) {

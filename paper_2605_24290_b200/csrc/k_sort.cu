@@ -199,9 +199,8 @@ __global__ void k_flags_in_order(int n, const int* __restrict__ order, const uns
 
 }  // namespace
 
-int compact_needed(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
+int compact_needed(rxgs_ctx ctx, const rxgs_scene_s& sc, rxgs_txstate_s& st, cudaStream_t s) {
     const int K = st.k;
-    const int n = static_cast<int>(st.visible);
     RXGS_CUDA(st.needed.ensure(static_cast<size_t>(K + 1) * 2));
     RXGS_CUDA(st.needed_order.ensure(sizeof(int) * (K + 1)));
     RXGS_CUDA(st.needed_count.ensure(sizeof(int) * 4));
@@ -212,14 +211,16 @@ int compact_needed(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
     if (st.entries > 0)
         k_mark_needed<<<st.grid.n_tiles, 128, 0, s>>>(st.grid, st.tile_offsets.as<int64_t>(), st.list.as<int>(),
                                                        st.walk_len.as<int>(), needed);
-    if (n > 0) {
-        k_flags_in_order<<<(n + 255) / 256, 256, 0, s>>>(n, st.order.as<int>(), needed, flags);
+    if (st.visible > 0 && K > 0) {
+        // compact in the scene's spatial (Morton) order: consecutive
+        // conditioning rows are nearby Gaussians (k_cond_tc.cu)
+        k_flags_in_order<<<(K + 255) / 256, 256, 0, s>>>(K, sc.d_morton.as<int>(), needed, flags);
         size_t tmp = 0;
-        RXGS_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, st.order.as<int>(), flags, st.needed_order.as<int>(),
-                                             st.needed_count.as<int>(), n, s));
+        RXGS_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, sc.d_morton.as<int>(), flags, st.needed_order.as<int>(),
+                                             st.needed_count.as<int>(), K, s));
         RXGS_CUDA(ctx->sort_tmp.ensure(tmp));
-        RXGS_CUDA(cub::DeviceSelect::Flagged(ctx->sort_tmp.p, tmp, st.order.as<int>(), flags,
-                                             st.needed_order.as<int>(), st.needed_count.as<int>(), n, s));
+        RXGS_CUDA(cub::DeviceSelect::Flagged(ctx->sort_tmp.p, tmp, sc.d_morton.as<int>(), flags,
+                                             st.needed_order.as<int>(), st.needed_count.as<int>(), K, s));
     }
     st.needed_host = -1;
     if (ctx->profile) {  // roofline bookkeeping only: the row count of the next conditioning launch
@@ -231,6 +232,74 @@ int compact_needed(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
     ctx->launches += 3;
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? RXGS_OK : cuda_fail(e, "compact_needed");
+}
+
+// ------------------------------------------------------------- scene order
+// Morton (Z-order) permutation of the scene's Gaussians over their bounding
+// box, 10 bits per axis: the spatial order the conditioning kernel walks
+// rows in, so a warp's 32 occupancy probes stay within a few voxels.
+namespace {
+__device__ __forceinline__ uint32_t spread3(uint32_t v) {
+    v &= 0x3FFu;
+    v = (v | (v << 16)) & 0x030000FFu;
+    v = (v | (v << 8)) & 0x0300F00Fu;
+    v = (v | (v << 4)) & 0x030C30C3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+__global__ void k_morton(int K, const float4* __restrict__ pos, float lx, float ly, float lz, float sx, float sy,
+                         float sz, uint32_t* __restrict__ key, int* __restrict__ idx) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    const float4 p = pos[k];
+    auto q = [](float v, float lo, float sc) {
+        const float u = (v - lo) * sc;
+        return static_cast<uint32_t>(fminf(fmaxf(u, 0.f), 1023.f));
+    };
+    key[k] = (spread3(q(p.x, lx, sx)) << 2) | (spread3(q(p.y, ly, sy)) << 1) | spread3(q(p.z, lz, sz));
+    idx[k] = k;
+}
+__global__ void k_gather_pos(int K, const int* __restrict__ order, const float4* __restrict__ pos,
+                             float4* __restrict__ out) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < K) out[r] = pos[order[r]];
+}
+}  // namespace
+
+int build_scene_order(rxgs_ctx ctx, rxgs_scene_s& sc, cudaStream_t s) {
+    const int K = sc.k;
+    RXGS_CUDA(sc.d_morton.ensure(sizeof(int) * std::max(K, 1)));
+    RXGS_CUDA(sc.d_mpos32.ensure(sizeof(float4) * std::max(K, 1)));
+    if (K == 0) return RXGS_OK;
+    double lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = 1.7976931348623157e308;
+        hi[a] = -1.7976931348623157e308;
+    }
+    for (int k = 0; k < K; ++k)
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = std::min(lo[a], sc.h_pos[3 * k + a]);
+            hi[a] = std::max(hi[a], sc.h_pos[3 * k + a]);
+        }
+    float scale[3];
+    for (int a = 0; a < 3; ++a) scale[a] = hi[a] > lo[a] ? static_cast<float>(1024.0 / (hi[a] - lo[a])) : 0.f;
+    DevBuf keys;
+    RXGS_CUDA(keys.ensure(static_cast<size_t>(K) * 2 * (sizeof(uint32_t) + sizeof(int))));
+    uint32_t* k_in = keys.as<uint32_t>();
+    uint32_t* k_out = k_in + K;
+    int* i_in = reinterpret_cast<int*>(k_out + K);
+    k_morton<<<(K + 255) / 256, 256, 0, s>>>(K, sc.d_pos32.as<float4>(), static_cast<float>(lo[0]),
+                                              static_cast<float>(lo[1]), static_cast<float>(lo[2]), scale[0],
+                                              scale[1], scale[2], k_in, i_in);
+    size_t tmp = 0;
+    RXGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k_in, k_out, i_in, sc.d_morton.as<int>(), K, 0, 30, s));
+    RXGS_CUDA(ctx->sort_tmp.ensure(tmp));
+    RXGS_CUDA(cub::DeviceRadixSort::SortPairs(ctx->sort_tmp.p, tmp, k_in, k_out, i_in, sc.d_morton.as<int>(), K, 0,
+                                              30, s));
+    k_gather_pos<<<(K + 255) / 256, 256, 0, s>>>(K, sc.d_morton.as<int>(), sc.d_pos32.as<float4>(),
+                                                  sc.d_mpos32.as<float4>());
+    RXGS_CUDA(cudaStreamSynchronize(s));  // keys is freed on return
+    return RXGS_OK;
 }
 
 }  // namespace rxgs_b200

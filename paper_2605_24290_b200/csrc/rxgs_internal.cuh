@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <map>
 #include <string>
@@ -98,6 +99,9 @@ struct rxgs_ctx_s {
     // scratch
     rxgs_b200::DevBuf sort_tmp, scratch_a, scratch_b, scratch_c, scratch_d, signals, ag, partial,
         err_flag, host_in, host_out, ycache;
+    // conditioning rows gathered into row order (k_cond_tc.cu): positions,
+    // (basis*base, basis) transposed to [l][row], their sums over l
+    rxgs_b200::DevBuf row_pos, row_GB, row_S;
     int sm_count = 148;
     int cond_kernel = 0;  // 0 auto (tcgen05 when eligible), 1 force SIMT
     int composite_kernel = 0;  // 0 auto (tcgen05 when eligible), 1 force SIMT
@@ -112,6 +116,9 @@ struct rxgs_scene_s {
     int k = 0, l_max = 0, channels = 1, L = 1, modality = 0;
     std::vector<double> h_pos, h_ls, h_q, h_tau, h_coeffs;
     rxgs_b200::DevBuf d_pos, d_ls, d_q, d_tau, d_coeffs64, d_coeffs32, d_pos32;
+    // Morton (Z-order) permutation of the Gaussians and their f32 positions
+    // in that order (build_scene_order, k_sort.cu)
+    rxgs_b200::DevBuf d_morton, d_mpos32;
     bool host_stale = false;  // device coefficients updated by the optimizer
     // exact position -> lowest Gaussian index (receiver-on-Gaussian check,
     // conditioning.cpp:380-382), built lazily on the host
@@ -130,8 +137,9 @@ struct rxgs_txstate_s {
         order, rank, scan, tile_offsets, list, keys, tw, walk_len, cell_T, cell_len, needed,
         needed_order, needed_count;
     // Gaussians reached by at least one cell's walk (list position < the
-    // tile's longest walk), in depth order: the only rows whose conditioned
-    // signal is ever read by the compositor.  needed_count is device-side.
+    // tile's longest walk), in the scene's Morton order: the only rows whose
+    // conditioned signal is ever read by the compositor.  needed_count is
+    // device-side.
     int64_t needed_host = -1;
     // walked list entries regrouped by Gaussian (training adjoint), built lazily
     rxgs_b200::DevBuf gauss_off, gauss_ent;
@@ -179,7 +187,9 @@ int bin_tiles(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s);
 // ---- k_walk.cu (FP64, -fmad=false)
 cudaError_t launch_walk(rxgs_txstate_s& st, cudaStream_t s);
 // Marks and compacts the Gaussians the walk reaches (st.needed_order/count).
-int compact_needed(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s);
+int compact_needed(rxgs_ctx ctx, const rxgs_scene_s& sc, rxgs_txstate_s& st, cudaStream_t s);
+// Morton order of the scene (sc.d_morton, sc.d_mpos32), once at scene creation.
+int build_scene_order(rxgs_ctx ctx, rxgs_scene_s& sc, cudaStream_t s);
 
 // ---- k_cond.cu
 cudaError_t launch_cond_global(const rxgs_cond_s& c, const double* d_rx, int n_rx, float* d_ag,
