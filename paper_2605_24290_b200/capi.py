@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librxgs_b200.so")
+LIB_PATH = os.environ.get("RXGS_B200_LIB") or os.path.join(HERE, "librxgs_b200.so")  # override: A/B builds
 
 RXGS_OK, RXGS_ERR_INVALID, RXGS_ERR_RUNTIME, RXGS_ERR_CUDA = 0, 1, 2, 3
 MODALITY = {"rssi": 0, "csi": 1, "spectrum": 2}

@@ -28,57 +28,76 @@ using namespace cond_dev;
 
 
 // ------------------------------------------------------------------ global branch (FP64)
-__global__ void k_cond_global(CondDev c, const double* __restrict__ rx, int n_rx,
-                              float* __restrict__ ag) {
+// Persistent CTAs loop over receivers.  Per receiver the Fourier part of
+// layer 1 (the first 6F inputs, shared by all L components) is summed once
+// and each (component, unit) thread continues the same sequential sum over
+// [l/l_max, m/l_max, e_l] -- the reference's summation order
+// (mlp_forward, conditioning.cpp:23-29), so the result is unchanged; W2 is
+// staged transposed in shared memory once per CTA.
+constexpr int kGlobThreads = 256;
+
+__global__ void __launch_bounds__(kGlobThreads) k_cond_global(CondDev c, const double* __restrict__ rx, int n_rx,
+                                                              float* __restrict__ ag) {
     extern __shared__ double sm[];
-    double* in = sm;
-    double* h1 = in + c.gin;
-    double* h2 = h1 + c.H;
-    const int row = blockIdx.x;
-    const int j = row / c.L, comp = row % c.L;
+    const int H = c.H, F6 = 6 * c.F, CH = kGlobThreads / H > 0 ? kGlobThreads / H : 1;
+    double* w2t = sm;                  // [i][o]
+    double* gam = w2t + H * H;         // 6F
+    double* pre = gam + F6;            // H
+    double* h1 = pre + H;              // CH x H
+    double* h2 = h1 + CH * H;          // CH x H
     const double* p = c.p64;
-    int l = 0;
-    while ((l + 1) * (l + 1) <= comp) ++l;
-    const int m = comp - l * l - l;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < H * H; i += blockDim.x) w2t[(i % H) * H + i / H] = p[c.o_gw2 + i];
     int l_max = 0;
     while ((l_max + 1) * (l_max + 1) < c.L) ++l_max;
     const double den = l_max > 0 ? static_cast<double>(l_max) : 1.0;  // conditioning.cpp:328
-    for (int i = threadIdx.x; i < c.gin; i += blockDim.x) {
-        double v;
-        if (i < 6 * c.F) {
+    const int NY = 4 * c.C;
+    for (int j = blockIdx.x; j < n_rx; j += gridDim.x) {
+        __syncthreads();
+        for (int i = tid; i < F6; i += blockDim.x) {  // fourier_encode, conditioning.cpp:255-265
             const int a = i / (2 * c.F), band = (i % (2 * c.F)) / 2;
             const double arg = p[c.o_freq + band * 3 + a] * rx[3 * j + a];
-            v = (i % 2) ? cos(arg) : sin(arg);
-        } else if (i == 6 * c.F) {
-            v = l / den;
-        } else if (i == 6 * c.F + 1) {
-            v = m / den;
-        } else {
-            v = p[c.o_emb + comp * c.dc + (i - 6 * c.F - 2)];
+            gam[i] = (i % 2) ? cos(arg) : sin(arg);
         }
-        in[i] = v;
-    }
-    __syncthreads();
-    for (int o = threadIdx.x; o < c.H; o += blockDim.x) {
-        double acc = p[c.o_gb1 + o];
-        const double* w = p + c.o_gw1 + static_cast<size_t>(o) * c.gin;
-        for (int i = 0; i < c.gin; ++i) acc += w[i] * in[i];
-        h1[o] = acc > 0.0 ? acc : 0.0;
-    }
-    __syncthreads();
-    for (int o = threadIdx.x; o < c.H; o += blockDim.x) {
-        double acc = p[c.o_gb2 + o];
-        const double* w = p + c.o_gw2 + static_cast<size_t>(o) * c.H;
-        for (int i = 0; i < c.H; ++i) acc += w[i] * h1[i];
-        h2[o] = acc > 0.0 ? acc : 0.0;
-    }
-    __syncthreads();
-    for (int o = threadIdx.x; o < 4 * c.C; o += blockDim.x) {
-        double acc = p[c.o_gb3 + o];
-        const double* w = p + c.o_gw3 + static_cast<size_t>(o) * c.H;
-        for (int i = 0; i < c.H; ++i) acc += w[i] * h2[i];
-        if (c.additive && (o % 4) < 2) acc = 0.0;
-        ag[(static_cast<size_t>(j) * c.L + comp) * 4 * c.C + o] = static_cast<float>(acc);
+        __syncthreads();
+        for (int o = tid; o < H; o += blockDim.x) {
+            double acc = p[c.o_gb1 + o];
+            const double* w = p + c.o_gw1 + static_cast<size_t>(o) * c.gin;
+            for (int i = 0; i < F6; ++i) acc += w[i] * gam[i];
+            pre[o] = acc;
+        }
+        for (int c0 = 0; c0 < c.L; c0 += CH) {
+            __syncthreads();
+            const int cl = tid / H, o = tid % H, comp = c0 + cl;
+            const bool valid = cl < CH && comp < c.L;
+            if (valid) {
+                int l = 0;
+                while ((l + 1) * (l + 1) <= comp) ++l;
+                const int m = comp - l * l - l;
+                const double* w = p + c.o_gw1 + static_cast<size_t>(o) * c.gin + F6;
+                double acc = pre[o];
+                acc += w[0] * (l / den);
+                acc += w[1] * (m / den);
+                for (int e = 0; e < c.dc; ++e) acc += w[2 + e] * p[c.o_emb + comp * c.dc + e];
+                h1[cl * H + o] = acc > 0.0 ? acc : 0.0;
+            }
+            __syncthreads();
+            if (valid) {
+                double acc = p[c.o_gb2 + o];
+                for (int i = 0; i < H; ++i) acc += w2t[i * H + o] * h1[cl * H + i];
+                h2[cl * H + o] = acc > 0.0 ? acc : 0.0;
+            }
+            __syncthreads();
+            for (int t = tid; t < CH * NY; t += blockDim.x) {
+                const int cl3 = t / NY, oo = t % NY, comp3 = c0 + cl3;
+                if (comp3 >= c.L) continue;
+                double acc = p[c.o_gb3 + oo];
+                const double* w = p + c.o_gw3 + static_cast<size_t>(oo) * H;
+                for (int i = 0; i < H; ++i) acc += w[i] * h2[cl3 * H + i];
+                if (c.additive && (oo % 4) < 2) acc = 0.0;
+                ag[(static_cast<size_t>(j) * c.L + comp3) * NY + oo] = static_cast<float>(acc);
+            }
+        }
     }
 }
 
@@ -301,8 +320,15 @@ cudaError_t launch_cond_global(const rxgs_cond_s& c, const double* d_rx, int n_r
     if (n_rx == 0) return cudaSuccess;
     if (!c.use_global()) return cudaMemsetAsync(d_ag, 0, sizeof(float) * n_rx * c.L * 4 * c.C, s);
     const CondDev d = make_dev(c);
-    const size_t smem = sizeof(double) * (c.gin + 2 * c.hidden);
-    k_cond_global<<<n_rx * c.L, 64, smem, s>>>(d, d_rx, n_rx, d_ag);
+    const int H = c.hidden, CH = kGlobThreads / H > 0 ? kGlobThreads / H : 1;
+    if (H > kGlobThreads) return cudaErrorInvalidValue;
+    const size_t smem = sizeof(double) * (static_cast<size_t>(H) * H + 6 * c.F + H + 2 * CH * H);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaFuncSetAttribute(k_cond_global, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    k_cond_global<<<std::min(n_rx, 2 * sms), kGlobThreads, smem, s>>>(d, d_rx, n_rx, d_ag);
     return cudaGetLastError();
 }
 

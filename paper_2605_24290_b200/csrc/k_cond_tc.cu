@@ -39,6 +39,10 @@
 #include "tc_util.cuh"
 #include "f32x2.cuh"
 
+#ifndef RXGS_MBAR_WAIT
+#define RXGS_MBAR_WAIT tc::mbar_wait_sleep
+#endif
+
 namespace rxgs_b200 {
 namespace {
 
@@ -121,19 +125,36 @@ __device__ __forceinline__ void probe_seg(const float* occ, int R, int S, float 
     }
 }
 
+// Group rendezvous without a blocking barrier: each warp, after its TMEM
+// stores (tcgen05.wait::st + fence::before_thread_sync), bumps the group's
+// counter with release/acquire semantics; the warp that arrives last (old
+// value = 3 mod 4) issues the MMAs.  The other three warps go straight on to
+// their next independent work instead of idling at a bar.sync.
+__device__ __forceinline__ bool arrive_last(uint32_t* cnt, int lane) {
+    __syncwarp();
+    uint32_t old = 0;
+    if (lane == 0)
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                     : "=r"(old)
+                     : "r"(tc::smem_u32(cnt))
+                     : "memory");
+    old = __shfl_sync(0xffffffffu, old, 0);
+    return (old & 3u) == 3u;
+}
+
 // The clamp-free probe, two samples per instruction (FFMA2/FADD2/FMUL2):
-// lanes .x / .y of every float2 are samples 2i and 2i+1.  The transmittance
-// is accumulated as two interleaved products, multiplied at the end.
-template <int ST, int RT>
-__device__ __forceinline__ void probe_seg_x2(const float* occ, float b0, float b1, float b2, float s0, float s1,
-                                             float s2, float& tr, float& sum) {
+// lanes .x / .y of every float2 are samples 2i and 2i+1 for the sample pairs
+// [P0, P1).  The transmittance is accumulated as two interleaved products
+// (tr2.x * tr2.y at the end), the density as two partial sums.
+template <int ST, int RT, int P0, int P1>
+__device__ __forceinline__ void probe_pairs(const float* occ, float b0, float b1, float b2, float s0, float s1,
+                                            float s2, float2& tr2, float2& sum2) {
     static_assert(ST >= 2 && ST % 2 == 0 && RT > 0, "paired probe needs an even, static sample count");
     constexpr int P = padded_dim(RT);
     constexpr float cidx = static_cast<float>(P * P + P + 1);
     constexpr float dt = 0.9f / static_cast<float>(ST - 1);
-    float2 tr2 = make_float2(1.f, 1.f), sum2 = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int sp = 0; sp < ST / 2; ++sp) {
+    for (int sp = P0; sp < P1; ++sp) {
         const float2 t = make_float2(fmaf(static_cast<float>(2 * sp), dt, 0.05f),
                                      fmaf(static_cast<float>(2 * sp + 1), dt, 0.05f));
         const float2 u0 = x2::fma(t, x2::bc(s0), x2::bc(b0));
@@ -162,9 +183,14 @@ __device__ __forceinline__ void probe_seg_x2(const float* occ, float b0, float b
         tr2 = x2::mul(tr2, x2::sub(x2::bc(1.f), v));
         sum2 = x2::add(sum2, v);
     }
-    tr = tr2.x * tr2.y;
-    sum = sum2.x + sum2.y;
 }
+
+// Per-row probe state carried between the two halves of the split probe.
+struct ProbeState {
+    float b0, b1, b2, s0, s1, s2;
+    float2 tr2, sum2;
+    bool split;  // paired fast path: second half still to run
+};
 
 // Gathers the per-row Tx data of the needed rows: position, (basis*base,
 // basis) transposed to [l][row] as float4, and the sums over l of both.
@@ -209,11 +235,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* aone = b2lo + kW1Bytes;      // [1 | 0] : 128 x 16 bf16
     float* s_occ = reinterpret_cast<float*>(smem + kFixedSmem);
     __shared__ uint64_t bars[kGroups];
+    __shared__ uint32_t arrivals[kGroups];
     __shared__ uint32_t tbase_s;
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int g = warp >> 2, wl = warp & 3;
+    if (tid < kGroups) arrivals[tid] = 0u;
 
     // ---- one-time setup: weights as bf16 hi/lo core matrices, occupancy
     for (int i = tid; i < kH * kH; i += kThreads) split_store(w2hi, w2lo, canon_off(i / kH, i % kH), c.p32[c.o_lw2 + i]);
@@ -269,8 +297,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         r = gb * 32 + lane;
         j = jq * 4 + wl;
     };
-    // local features [v_hat, d, T, rho] of one row (conditioning.cpp:377-396)
-    auto features = [&](bool active, float4 pk, float qx, float qy, float qz, float* in) {
+    constexpr bool kSplit = ST >= 2 && ST % 2 == 0 && RT > 0;
+// A/B-measured (scripts/ab_variants.sh): the whole probe in the layer-2
+// window and the FLE in the layer-1 window is fastest.
+#ifndef RXGS_PROBE_FIRST_PAIRS
+#define RXGS_PROBE_FIRST_PAIRS 0
+#endif
+#ifndef RXGS_FLE_FIRST
+#define RXGS_FLE_FIRST 1
+#endif
+    // sample pairs of the next tile's probe run in the layer-1 MMA window;
+    // the rest (and the FLE unless RXGS_FLE_FIRST) in the layer-2 window
+    constexpr int kHalf = kSplit ? (RXGS_PROBE_FIRST_PAIRS < ST / 2 ? RXGS_PROBE_FIRST_PAIRS : ST / 2) : 0;
+    // local features [v_hat, d, T, rho] of one row (conditioning.cpp:377-396).
+    // feat_begin computes [v_hat, d] and, on the paired fast path, the first
+    // half of the probe; feat_end the second half (it runs in the layer-2
+    // MMA window) and writes [T, rho].  Clamped / generic probes run whole in
+    // feat_begin.
+    auto feat_begin = [&](bool active, float4 pk, float qx, float qy, float qz, float* in, ProbeState& ps) {
         const float px = active ? pk.x : 0.f, py = active ? pk.y : 0.f, pz = active ? pk.z : 0.f;
         if (!active) {
             qx = 1.f;
@@ -283,31 +327,49 @@ __global__ void __launch_bounds__(kThreads, 1)
         in[1] = dy * inv;
         in[2] = dz * inv;
         in[3] = d;
-        float T = 1.f, rho = 0.f;
+        in[4] = 1.f;
+        in[5] = 0.f;
+        ps.split = false;
+        ps.tr2 = make_float2(1.f, 1.f);
+        ps.sum2 = make_float2(0.f, 0.f);
         if (c.probe) {
-            const float b0 = fmaf(px, W.icell[0], -W.blo[0]), b1 = fmaf(py, W.icell[1], -W.blo[1]),
-                        b2 = fmaf(pz, W.icell[2], -W.blo[2]);
-            const float s0 = dx * W.icell[0], s1 = dy * W.icell[1], s2 = dz * W.icell[2];
+            ps.b0 = fmaf(px, W.icell[0], -W.blo[0]);
+            ps.b1 = fmaf(py, W.icell[1], -W.blo[1]);
+            ps.b2 = fmaf(pz, W.icell[2], -W.blo[2]);
+            ps.s0 = dx * W.icell[0];
+            ps.s1 = dy * W.icell[1];
+            ps.s2 = dz * W.icell[2];
             auto inside = [&](float t) {
-                const float u0 = fmaf(t, s0, b0), u1 = fmaf(t, s1, b1), u2 = fmaf(t, s2, b2);
+                const float u0 = fmaf(t, ps.s0, ps.b0), u1 = fmaf(t, ps.s1, ps.b1), u2 = fmaf(t, ps.s2, ps.b2);
                 return u0 >= -1.f && u0 <= hiR && u1 >= -1.f && u1 <= hiR && u2 >= -1.f && u2 <= hiR;
             };
             const bool ok = !active || (inside(tfirst) && inside(tlast));
             float tr = 1.f, sum = 0.f;
             if (__all_sync(0xffffffffu, ok)) {
-                if constexpr (ST >= 2 && ST % 2 == 0 && RT > 0) {
-                    if (active) probe_seg_x2<ST, RT>(s_occ, b0, b1, b2, s0, s1, s2, tr, sum);
+                if constexpr (kSplit) {
+                    ps.split = true;
+                    if (active) probe_pairs<ST, RT, 0, kHalf>(s_occ, ps.b0, ps.b1, ps.b2, ps.s0, ps.s1, ps.s2, ps.tr2,
+                                                             ps.sum2);
+                    return;
                 } else {
-                    if (active) probe_seg<ST, RT, false>(s_occ, R, S, b0, b1, b2, s0, s1, s2, tr, sum);
+                    if (active) probe_seg<ST, RT, false>(s_occ, R, S, ps.b0, ps.b1, ps.b2, ps.s0, ps.s1, ps.s2, tr, sum);
                 }
             } else if (active) {
-                probe_seg<ST, RT, true>(s_occ, R, S, b0, b1, b2, s0, s1, s2, tr, sum);
+                probe_seg<ST, RT, true>(s_occ, R, S, ps.b0, ps.b1, ps.b2, ps.s0, ps.s1, ps.s2, tr, sum);
             }
-            T = tr;
-            rho = sum * (1.f / static_cast<float>(S));
+            in[4] = tr;
+            in[5] = sum * (1.f / static_cast<float>(S));
         }
-        in[4] = T;
-        in[5] = rho;
+    };
+    auto feat_end = [&](bool active, float* in, ProbeState& ps) {
+        if constexpr (kSplit) {
+            if (ps.split) {  // warp-uniform
+                if (active) probe_pairs<ST, RT, kHalf, (kSplit ? ST / 2 : 0)>(s_occ, ps.b0, ps.b1, ps.b2, ps.s0, ps.s1, ps.s2, ps.tr2,
+                                                             ps.sum2);
+                in[4] = ps.tr2.x * ps.tr2.y;
+                in[5] = (ps.sum2.x + ps.sum2.y) * (1.f / static_cast<float>(S));
+            }
+        }
     };
 
     long long tile = static_cast<long long>(blockIdx.x) * kGroups + g;
@@ -324,7 +386,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             qy = static_cast<float>(rx[3 * j + 1]);
             qz = static_cast<float>(rx[3 * j + 2]);
         }
-        features(act, pk, qx, qy, qz, in);
+        ProbeState ps0;
+        feat_begin(act, pk, qx, qy, qz, in, ps0);
+        feat_end(act, in, ps0);
     }
     for (; tile < tiles; tile += step) {
         const bool active = r < n_rows && j < n_rx;
@@ -342,6 +406,40 @@ __global__ void __launch_bounds__(kThreads, 1)
             qzn = rx[3 * jn + 2];
         }
         const int k = active ? rows[r] : 0;
+        float2 M = make_float2(0.f, 0.f), Bs = make_float2(0.f, 0.f);
+        auto fle = [&]() {
+        if (!YOUT && active) {
+            const float4 sums = rS[r];
+            M = make_float2(sums.x, sums.y);
+            Bs = make_float2(sums.z, sums.w);
+            const float4* a4 = reinterpret_cast<const float4*>(ag) + static_cast<size_t>(j) * L;
+            const float4* e4 = rGB + r;
+            // two independent accumulators (even / odd l) for FFMA2 latency
+            float2 M1 = make_float2(0.f, 0.f);
+            auto acc = [](float2 m, float4 e, float4 a) {
+                m = x2::fma(x2::bc(a.x), make_float2(e.x, e.y), m);
+                m = x2::fma(make_float2(-e.y, e.x), x2::bc(a.y), m);
+                m = x2::fma(x2::bc(a.z), make_float2(e.z, e.w), m);
+                return x2::fma(make_float2(-e.w, e.z), x2::bc(a.w), m);
+            };
+            int l = 0;
+            for (; l + 4 <= L; l += 4) {
+                float4 e[4], a[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    e[u] = e4[static_cast<size_t>(l + u) * cap];
+                    a[u] = a4[l + u];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u += 2) {
+                    M = acc(M, e[u], a[u]);
+                    M1 = acc(M1, e[u + 1], a[u + 1]);
+                }
+            }
+            for (; l < L; ++l) M = acc(M, e4[static_cast<size_t>(l) * cap], a4[l]);
+            M = x2::add(M, M1);
+        }
+        };
         // ---- layer 1 on the tensor cores: A1 = [x, 1, 0...] (K = 16) hi/lo -> TMEM
         {
             uint32_t hi[8], lo[8];
@@ -356,8 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc::wait_st();
         tc::fence_before_sync();
-        tc::named_bar_sync(1 + g, 128);
-        if (wl == 0 && lane == 0) {
+        if (arrive_last(&arrivals[g], lane) && lane == 0) {
             tc::fence_after_sync();
             const uint64_t bh = tc::sdesc_kmajor_noswizzle(w1hi_a, 128, 256);
             const uint64_t bl = tc::sdesc_kmajor_noswizzle(w1lo_a, 128, 256);
@@ -368,9 +465,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // ---- overlaps the layer-1 MMA: the next tile's features and probe
         float inn[6];
+        ProbeState ps;
+        ps.split = false;
         if (ntile < tiles)
-            features(nact, pkn, static_cast<float>(qxn), static_cast<float>(qyn), static_cast<float>(qzn), inn);
-        tc::mbar_wait(&bars[g], phase);
+            feat_begin(nact, pkn, static_cast<float>(qxn), static_cast<float>(qyn), static_cast<float>(qzn), inn, ps);
+        if (RXGS_FLE_FIRST) fle();
+        RXGS_MBAR_WAIT(&bars[g], phase);
         phase ^= 1u;
         tc::fence_after_sync();
         // ---- ReLU(h1) -> bf16 hi/lo -> TMEM (layer-2 A operand; overwrites A1)
@@ -388,9 +488,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc::wait_st();
         tc::fence_before_sync();
-        tc::named_bar_sync(1 + g, 128);
         // ---- layer 2 on the tensor cores: D = 1 b2 + Ahi Bhi + Ahi Blo + Alo Bhi
-        if (wl == 0 && lane == 0) {
+        if (arrive_last(&arrivals[g], lane) && lane == 0) {
             tc::fence_after_sync();
             const uint64_t ad = tc::sdesc_kmajor_noswizzle(aone_a, 128, 256);
             tc::mma_ss(tm_d, ad, tc::sdesc_kmajor_noswizzle(b2hi_a, 128, 256), kIdesc, 0u);
@@ -408,56 +507,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---- overlaps the layer-2 MMA: M = sum_l [(1+aG_l) GB_l + bG_l B_l]
         // (fle_reduce, cond_common.cuh) as sum_l GB_l + sum_l [aG_l GB_l + bG_l B_l],
         // complex products on FFMA2 (i z = (-z.y, z.x) via swapped / negated operands)
-        float2 M = make_float2(0.f, 0.f), Bs = make_float2(0.f, 0.f);
-        if (!YOUT && active) {
-            const float4 sums = rS[r];
-            M = make_float2(sums.x, sums.y);
-            Bs = make_float2(sums.z, sums.w);
-            const float4* a4 = reinterpret_cast<const float4*>(ag) + static_cast<size_t>(j) * L;
-            const float4* e4 = rGB + r;
-            int l = 0;
-            for (; l + 3 <= L; l += 3) {
-                float4 e[3], a[3];
-#pragma unroll
-                for (int u = 0; u < 3; ++u) {
-                    e[u] = e4[static_cast<size_t>(l + u) * cap];
-                    a[u] = a4[l + u];
-                }
-#pragma unroll
-                for (int u = 0; u < 3; ++u) {
-                    M = x2::fma(x2::bc(a[u].x), make_float2(e[u].x, e[u].y), M);
-                    M = x2::fma(make_float2(e[u].y, e[u].x), make_float2(-a[u].y, a[u].y), M);
-                    M = x2::fma(x2::bc(a[u].z), make_float2(e[u].z, e[u].w), M);
-                    M = x2::fma(make_float2(e[u].w, e[u].z), make_float2(-a[u].w, a[u].w), M);
-                }
-            }
-            for (; l < L; ++l) {
-                const float4 e = e4[static_cast<size_t>(l) * cap];
-                const float4 a = a4[l];
-                M = x2::fma(x2::bc(a.x), make_float2(e.x, e.y), M);
-                M = x2::fma(make_float2(e.y, e.x), make_float2(-a.y, a.y), M);
-                M = x2::fma(x2::bc(a.z), make_float2(e.z, e.w), M);
-                M = x2::fma(make_float2(e.w, e.z), make_float2(-a.w, a.w), M);
-            }
-        }
-        tc::mbar_wait(&bars[g], phase);
+        feat_end(nact, inn, ps);  // second half of the next tile's probe
+        if (!RXGS_FLE_FIRST) fle();
+        RXGS_MBAR_WAIT(&bars[g], phase);
         phase ^= 1u;
         tc::fence_after_sync();
         // ---- ReLU(h2), layer 3 on FFMA2 from the TMEM accumulator
         float2 ya = make_float2(W.b3[0], W.b3[1]), yb = make_float2(W.b3[2], W.b3[3]);
+        float2 ya1 = make_float2(0.f, 0.f), yb1 = make_float2(0.f, 0.f);  // odd columns (FFMA2 latency)
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) {
             uint32_t v[16];
             tc::tmem_ld16(tm_d + lane_off + 16 * ch, v);
             tc::wait_ld();
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                const float4 w3 = W.w3[16 * ch + q];
+            for (int q = 0; q < 16; q += 2) {
+                const float4 w3 = W.w3[16 * ch + q], w3b = W.w3[16 * ch + q + 1];
                 const float2 h2 = x2::bc(fmaxf(__uint_as_float(v[q]), 0.f));
+                const float2 h2b = x2::bc(fmaxf(__uint_as_float(v[q + 1]), 0.f));
                 ya = x2::fma(h2, make_float2(w3.x, w3.y), ya);
                 yb = x2::fma(h2, make_float2(w3.z, w3.w), yb);
+                ya1 = x2::fma(h2b, make_float2(w3b.x, w3b.y), ya1);
+                yb1 = x2::fma(h2b, make_float2(w3b.z, w3b.w), yb1);
             }
         }
+        ya = x2::add(ya, ya1);
+        yb = x2::add(yb, yb1);
         tc::fence_before_sync();  // the next tile's layer-1 MMA overwrites D after the barrier
         if (active) {
             if (YOUT) {
@@ -466,9 +541,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // s = (1 + aL) M + bL Bs (local_affine; additive mode: aL = 0)
                 const float2 al = c.additive ? make_float2(0.f, 0.f) : ya;
                 float2 sg = x2::fma(x2::bc(al.x), M, M);
-                sg = x2::fma(make_float2(M.y, M.x), make_float2(-al.y, al.y), sg);
+                sg = x2::fma(make_float2(-M.y, M.x), x2::bc(al.y), sg);
                 sg = x2::fma(x2::bc(yb.x), Bs, sg);
-                sg = x2::fma(make_float2(Bs.y, Bs.x), make_float2(-yb.y, yb.y), sg);
+                sg = x2::fma(make_float2(-Bs.y, Bs.x), x2::bc(yb.y), sg);
                 sig[static_cast<size_t>(k) * n_rx + j] = sg;
             }
         }
