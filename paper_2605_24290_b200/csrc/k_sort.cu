@@ -11,7 +11,7 @@
 //      (tile, g) pair per covered tile, in rank order;
 //   3. stable radix sort of the pairs by the tile id alone (ceil(log2 tiles)
 //      bits, 2 passes at 12 bits): within a tile the rank order survives;
-//   4. per-tile [begin, end) from a histogram scan, and the 64-bit sort keys
+//   4. per-tile [begin, end) from the tile-id steps of the sorted pairs, and the 64-bit sort keys
 //      (tile << 32) | rank that the north star asks to be bit-exact.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -43,8 +43,7 @@ __global__ void k_rank(int K, const int* __restrict__ order, const int* __restri
 
 __global__ void k_emit(int K, int tiles_p, const int* __restrict__ order,
                        const int4* __restrict__ spans, const int64_t* __restrict__ scan,
-                       uint32_t* __restrict__ tkey, int* __restrict__ tval,
-                       int* __restrict__ tile_hist) {
+                       uint32_t* __restrict__ tkey, int* __restrict__ tval) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= K) return;
     const int64_t begin = scan[r];
@@ -58,7 +57,6 @@ __global__ void k_emit(int K, int tiles_p, const int* __restrict__ order,
             const int tile = tt * tiles_p + pp % tiles_p;
             tkey[o] = static_cast<uint32_t>(tile);
             tval[o] = g;
-            atomicAdd(tile_hist + tile, 1);
             ++o;
         }
 }
@@ -70,10 +68,15 @@ __global__ void k_keys(int64_t n, const uint32_t* __restrict__ tkey, const int* 
     keys[i] = (static_cast<uint64_t>(tkey[i]) << 32) | static_cast<uint32_t>(rank[list[i]]);
 }
 
-__global__ void k_widen(int n, const int* __restrict__ in, int64_t* __restrict__ out) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = in[i];
-    if (i == n) out[n] = 0;
+// tile_offsets[t] = first position of tile t in the tile-sorted pairs
+// (= lower_bound), written by the entry where the tile id steps up; no
+// histogram atomics.
+__global__ void k_offsets(int64_t n, int n_tiles, const uint32_t* __restrict__ tks, int64_t* __restrict__ off) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i > n) return;
+    const int prev = i == 0 ? -1 : static_cast<int>(tks[i - 1]);
+    const int cur = i == n ? n_tiles : static_cast<int>(tks[i]);
+    for (int t = prev + 1; t <= cur; ++t) off[t] = i;
 }
 
 int bits_for(int n) {
@@ -92,24 +95,19 @@ int bin_tiles(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
     RXGS_CUDA(st.scan.ensure(sizeof(int64_t) * (K + 1)));
     RXGS_CUDA(st.tile_offsets.ensure(sizeof(int64_t) * (n_tiles + 1)));
 
-    // scratch: sorted depth keys (K u64) | iota (K int) | cnt_sorted (K+1 i64) | hist |
-    // hist64 | [total, culled] (every sub-buffer 256-byte aligned)
+    // scratch: sorted depth keys (K u64) | iota (K int) | cnt_sorted (K+1 i64) |
+    // [total, culled] (every sub-buffer 256-byte aligned)
     auto al = [](size_t x) { return (x + 255) & ~static_cast<size_t>(255); };
     const size_t off_iota = al(sizeof(uint64_t) * (K + 1));
     const size_t off_cnt = off_iota + al(sizeof(int) * (K + 2));
-    const size_t off_hist = off_cnt + al(sizeof(int64_t) * (K + 2));
-    const size_t off_hist64 = off_hist + al(sizeof(int) * (n_tiles + 2));
-    const size_t off_red = off_hist64 + al(sizeof(int64_t) * (n_tiles + 2));
+    const size_t off_red = off_cnt + al(sizeof(int64_t) * (K + 2));
     RXGS_CUDA(ctx->scratch_a.ensure(off_red + 256));
     char* base = ctx->scratch_a.as<char>();
     uint64_t* dk_sorted = reinterpret_cast<uint64_t*>(base);
     int* iota = reinterpret_cast<int*>(base + off_iota);
     int64_t* cnt_sorted = reinterpret_cast<int64_t*>(base + off_cnt);
-    int* hist = reinterpret_cast<int*>(base + off_hist);
-    int64_t* hist64 = reinterpret_cast<int64_t*>(base + off_hist64);
     int64_t* red = reinterpret_cast<int64_t*>(base + off_red);  // [0] entries, [1] culled
 
-    RXGS_CUDA(cudaMemsetAsync(hist, 0, sizeof(int) * (n_tiles + 1), s));
     RXGS_CUDA(cudaMemsetAsync(red, 0, 2 * sizeof(int64_t), s));
     if (K > 0) {
         k_iota<<<(K + 255) / 256, 256, 0, s>>>(K, iota);
@@ -149,7 +147,7 @@ int bin_tiles(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
     uint32_t* tks = reinterpret_cast<uint32_t*>(pb + o_tks);
     if (total > 0) {
         k_emit<<<(K + 127) / 128, 128, 0, s>>>(K, st.grid.tiles_p, st.order.as<int>(), st.spans.as<int4>(),
-                                               st.scan.as<int64_t>(), tkey, tval, hist);
+                                               st.scan.as<int64_t>(), tkey, tval);
         size_t tmp = 0;
         const int end_bit = bits_for(n_tiles);
         RXGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, tkey, tks, tval, st.list.as<int>(),
@@ -162,13 +160,8 @@ int bin_tiles(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
                                                                           st.rank.as<int>(),
                                                                           st.keys.as<uint64_t>());
     }
-    k_widen<<<(n_tiles + 1 + 255) / 256, 256, 0, s>>>(n_tiles, hist, hist64);
-    size_t tmp = 0;
-    RXGS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, hist64, st.tile_offsets.as<int64_t>(),
-                                            n_tiles + 1, s));
-    RXGS_CUDA(ctx->sort_tmp.ensure(tmp));
-    RXGS_CUDA(cub::DeviceScan::ExclusiveSum(ctx->sort_tmp.p, tmp, hist64,
-                                            st.tile_offsets.as<int64_t>(), n_tiles + 1, s));
+    k_offsets<<<static_cast<unsigned>((total + 1 + 255) / 256), 256, 0, s>>>(total, n_tiles, tks,
+                                                                              st.tile_offsets.as<int64_t>());
     ctx->launches += 8;
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? RXGS_OK : cuda_fail(e, "bin_tiles");

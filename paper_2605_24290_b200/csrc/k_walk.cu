@@ -12,80 +12,113 @@
 // per-receiver composite is then a plain (cells x walk) x (walk x receivers)
 // product (k_composite.cu).
 //
-// One CTA per (tile, 64-cell block); records are staged through shared
-// memory in chunks of 64 list entries; the CTA stops loading as soon as every
-// cell has exited (block-wide early exit via __syncthreads_or).
+// One CTA per (tile, 64-cell block), 256 threads.  Records are staged
+// through shared memory in chunks of 64 list entries.  Only the
+// transmittance recurrence is sequential, so each chunk runs in two phases:
+//   A. all 256 threads evaluate the weights of the chunk's (entry, cell)
+//      pairs of still-alive cells (4 threads per cell, 16 independent exp
+//      chains each) into shared memory;
+//   B. the 64 cell owners run T through the chunk in list order, exactly as
+//      the reference does, writing tw and stopping at T < 1e-4.
+// The kernel's duration is set by the longest tile walk, so phase A's 4-way
+// parallelism is what shortens it.  The CTA stops loading as soon as every
+// cell has exited.
 #include "rxgs_internal.cuh"
 
 namespace rxgs_b200 {
 namespace {
 
 constexpr int kChunk = 64;
+constexpr int kWalkThreads = 256;
+constexpr int kLanesPerCell = kWalkThreads / kMaxCellsPerBlock;  // 4
 
 __device__ __forceinline__ double wrap_pm_pi(double a) {  // linalg.hpp:152-157
-    a = fmod(a, kTwoPi);
+    // fmod(a, 2 pi) is exact and returns a itself when |a| < 2 pi -- always
+    // the case for two azimuths in [0, 2 pi) -- so the call is skipped there
+    if (!(fabs(a) < kTwoPi)) a = fmod(a, kTwoPi);
     if (a > kPi) a -= kTwoPi;
     if (a <= -kPi) a += kTwoPi;
     return a;
 }
 
-__global__ void __launch_bounds__(64) k_walk(DevGrid g, const int64_t* __restrict__ tile_offsets,
-                                             const int* __restrict__ list,
-                                             const GaussRec* __restrict__ rec,
-                                             float* __restrict__ tw, int* __restrict__ walk_len,
-                                             double* __restrict__ cell_T,
-                                             int* __restrict__ cell_len) {
+__global__ void __launch_bounds__(kWalkThreads) k_walk(DevGrid g, const int64_t* __restrict__ tile_offsets,
+                                                       const int* __restrict__ list,
+                                                       const GaussRec* __restrict__ rec, float* __restrict__ tw,
+                                                       int* __restrict__ walk_len, double* __restrict__ cell_T,
+                                                       int* __restrict__ cell_len) {
     __shared__ GaussRec srec[kChunk];
-    __shared__ int s_max;
+    __shared__ double sw[kChunk][kMaxCellsPerBlock];
+    __shared__ int s_alive[kMaxCellsPerBlock];
+    __shared__ int s_len[kMaxCellsPerBlock];
+    __shared__ int s_max, s_min;
     const int tile = blockIdx.x;
     const int cb = blockIdx.y;
-    const int lane = threadIdx.x;
+    const int tid = threadIdx.x;
+    const int cl = tid % kMaxCellsPerBlock;  // this thread's cell in phase A
     const int tt = tile / g.tiles_p, tp = tile % g.tiles_p;
-    const int lc = cb * kMaxCellsPerBlock + lane;
+    const int lc = cb * kMaxCellsPerBlock + cl;
     const int row = tt * g.ts + lc / g.ts;
     const int col = tp * g.ts + lc % g.ts;
     const bool valid = lc < g.cpt && (lc / g.ts) < g.ts && row < g.nt && col < g.np;
     const int64_t begin = tile_offsets[tile];
     const int n = static_cast<int>(tile_offsets[tile + 1] - begin);
     const size_t stride = static_cast<size_t>(g.cell_blocks) * kMaxCellsPerBlock;
-    float* out = tw + static_cast<size_t>(begin) * stride + static_cast<size_t>(cb) * kMaxCellsPerBlock + lane;
+    float* out = tw + static_cast<size_t>(begin) * stride + static_cast<size_t>(cb) * kMaxCellsPerBlock + cl;
+    const bool owner = tid < kMaxCellsPerBlock;
 
     const double theta_r = valid ? g.tmin + (row + 0.5) * g.dth : 0.0;
     const double phi_r = valid ? (col + 0.5) * g.dph : 0.0;
     double T = 1.0;
     int len = valid ? n : 0;
-    bool alive = valid && n > 0;
-    if (lane == 0) s_max = 0;
+    bool alive = owner && valid && n > 0;
+    if (owner) s_alive[cl] = alive ? 1 : 0;
+    if (tid == 0) {
+        s_max = 0;
+        s_min = 0x7fffffff;
+    }
     for (int c0 = 0; c0 < n; c0 += kChunk) {
         if (!__syncthreads_or(alive)) break;
         const int m = min(kChunk, n - c0);
-        if (lane < m) srec[lane] = rec[list[begin + c0 + lane]];
+        if (tid < m) srec[tid] = rec[list[begin + c0 + tid]];
         __syncthreads();
-        if (alive) {
-            for (int i = 0; i < m; ++i) {
-                const GaussRec r = srec[i];
+        if (s_alive[cl]) {  // phase A: weights (gaussian_weight, sphraster.cpp:239-251)
+            for (int e = tid / kMaxCellsPerBlock; e < m; e += kLanesPerCell) {
+                const GaussRec& r = srec[e];
                 const double dt = theta_r - r.theta;
                 const double dpraw = wrap_pm_pi(phi_r - r.phi);
                 const double dp = r.sin_theta * dpraw;
                 const double m2 = r.pa * dt * dt + r.pbc * dt * dp + r.pd * dp * dp;
-                double w = r.tau * exp(-0.5 * m2);
-                w = kWeightClamp < w ? kWeightClamp : w;  // std::min(w, 0.999)
-                out[static_cast<size_t>(c0 + i) * stride] = static_cast<float>(T * w);
+                const double w = r.tau * exp(-0.5 * m2);
+                sw[e][cl] = kWeightClamp < w ? kWeightClamp : w;  // std::min(w, 0.999)
+            }
+        }
+        __syncthreads();
+        if (alive) {  // phase B: the front-to-back recurrence (render_field :285-298)
+            for (int e = 0; e < m; ++e) {
+                const double w = sw[e][cl];
+                out[static_cast<size_t>(c0 + e) * stride] = static_cast<float>(T * w);
                 T *= 1.0 - w;
                 if (T < kEarlyExitT) {
-                    len = c0 + i + 1;
+                    len = c0 + e + 1;
                     alive = false;
                     break;
                 }
             }
+            s_alive[cl] = alive ? 1 : 0;
         }
     }
-    atomicMax(&s_max, len);
+    if (owner) {
+        s_len[cl] = len;
+        atomicMax(&s_max, len);
+        atomicMin(&s_min, len);
+    }
     __syncthreads();
     const int wmax = s_max;
-    for (int e = len; e < wmax; ++e) out[static_cast<size_t>(e) * stride] = 0.0f;
-    if (lane == 0) walk_len[tile * g.cell_blocks + cb] = wmax;
-    if (valid) {
+    // zero the rows past each cell's exit up to the tile's longest walk
+    for (int e = s_min + tid / kMaxCellsPerBlock; e < wmax; e += kLanesPerCell)
+        if (e >= s_len[cl]) out[static_cast<size_t>(e) * stride] = 0.0f;
+    if (tid == 0) walk_len[tile * g.cell_blocks + cb] = wmax;
+    if (owner && valid) {
         const size_t cell = static_cast<size_t>(row) * g.np + col;
         cell_T[cell] = T;
         cell_len[cell] = len;
@@ -97,7 +130,7 @@ __global__ void __launch_bounds__(64) k_walk(DevGrid g, const int64_t* __restric
 cudaError_t launch_walk(rxgs_txstate_s& st, cudaStream_t s) {
     const DevGrid& g = st.grid;
     dim3 grid(g.n_tiles, g.cell_blocks);
-    k_walk<<<grid, 64, 0, s>>>(g, st.tile_offsets.as<int64_t>(), st.list.as<int>(),
+    k_walk<<<grid, kWalkThreads, 0, s>>>(g, st.tile_offsets.as<int64_t>(), st.list.as<int>(),
                                st.rec.as<GaussRec>(), st.tw.as<float>(), st.walk_len.as<int>(),
                                st.cell_T.as<double>(), st.cell_len.as<int>());
     return cudaGetLastError();
