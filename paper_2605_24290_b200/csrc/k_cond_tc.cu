@@ -544,7 +544,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 sg = x2::fma(make_float2(-M.y, M.x), x2::bc(al.y), sg);
                 sg = x2::fma(x2::bc(yb.x), Bs, sg);
                 sg = x2::fma(make_float2(-Bs.y, Bs.x), x2::bc(yb.y), sg);
+#ifdef RXGS_AB_NOSTORE
+                if (sg.x == 12345.f) sig[static_cast<size_t>(k) * n_rx + j] = sg;
+#else
                 sig[static_cast<size_t>(k) * n_rx + j] = sg;
+#endif
             }
         }
         r = rn;

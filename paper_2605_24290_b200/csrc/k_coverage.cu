@@ -12,6 +12,7 @@
 //   k_cov_signal   per (needed Gaussian, receiver) signal from the caches
 #include "cond_common.cuh"
 #include "rxgs_internal.cuh"
+#include "f32x2.cuh"
 
 namespace rxgs_b200 {
 namespace {
@@ -42,34 +43,105 @@ __global__ void k_ag_transpose(int n_rx, int L, const float4* __restrict__ ag, f
     agT[i] = ag[static_cast<size_t>(j) * L + l];
 }
 
-__global__ void __launch_bounds__(256) k_cov_signal(CondDev c, const int* __restrict__ n_rows,
-                                                    const int* __restrict__ rows, int n_rx, int L,
-                                                    const float2* __restrict__ B, const float2* __restrict__ GB,
-                                                    const float4* __restrict__ agT, const float4* __restrict__ ycache,
-                                                    float2* __restrict__ sig) {
-    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-    if (i >= static_cast<long long>(*n_rows) * n_rx) return;
-    const int k = rows[i / n_rx], j = static_cast<int>(i % n_rx);
-    float2 M = make_float2(0.f, 0.f), Bs = make_float2(0.f, 0.f);
-    for (int l = 0; l < L; ++l) {  // fle_reduce (cond_common.cuh) with the transposed global branch
-        const float2 b = B[static_cast<size_t>(k) * L + l];
-        const float2 gb = GB[static_cast<size_t>(k) * L + l];
-        const float4 a = agT[static_cast<size_t>(l) * n_rx + j];
-        const float2 t0 = cmul(make_float2(1.f + a.x, a.y), gb), t1 = cmul(make_float2(a.z, a.w), b);
-        M.x += t0.x + t1.x;
-        M.y += t0.y + t1.y;
-        Bs.x += b.x;
-        Bs.y += b.y;
+// One CTA = 32 conditioning rows (Morton order) x 256 receivers; thread =
+// one receiver.  The receiver's global-branch terms (alpha_G, beta_G) for all
+// l stay in registers for the 32 rows; the rows' (basis*base, basis) pairs
+// are staged in shared memory and read as broadcasts.  Per (row, receiver):
+// one coalesced 16-byte y read, L x 4 FFMA2, one coalesced signal store --
+// HBM-bound on the y cache.
+constexpr int kCovRows = 32;
+constexpr int kCovThreads = 256;
+
+// LT > 0: L == LT, the receiver's (alpha_G, beta_G) held in registers;
+// LT == 0 (other l_max): re-read per row from the transposed cache.
+template <int LT>
+__global__ void __launch_bounds__(kCovThreads, 3) k_cov_signal(CondDev c, const int* __restrict__ n_rows,
+                                                            const int* __restrict__ rows, int n_rx, int L,
+                                                            const float2* __restrict__ B, const float2* __restrict__ GB,
+                                                            const float4* __restrict__ agT,
+                                                            const float4* __restrict__ ycache, float2* __restrict__ sig) {
+    extern __shared__ float4 s_e_dyn[];  // (GB, B) per (row, l): [kCovRows][L], then s_a
+    __shared__ float4 s_sum[kCovRows];          // (sum_l GB, sum_l B)
+    __shared__ int s_k[kCovRows];
+    const int nr = *n_rows;
+    const int r0 = blockIdx.x * kCovRows;
+    if (r0 >= nr) return;
+    const int tid = threadIdx.x;
+#pragma unroll 1
+    for (int i = tid; i < kCovRows * L; i += kCovThreads) {
+        const int rr = i / L, l = i % L;
+        const int r = r0 + rr;
+        const int k = r < nr ? rows[r] : 0;
+        const float2 b = B[static_cast<size_t>(k) * L + l], gb = GB[static_cast<size_t>(k) * L + l];
+        s_e_dyn[rr * L + l] = make_float4(gb.x, gb.y, b.x, b.y);
     }
-    float y[4] = {0.f, 0.f, 0.f, 0.f};
-    if (ycache) {
-        const float4 v = ycache[static_cast<size_t>(k) * n_rx + j];
-        y[0] = v.x;
-        y[1] = v.y;
-        y[2] = v.z;
-        y[3] = v.w;
+    __syncthreads();
+    if (tid < kCovRows) {
+        const int r = r0 + tid;
+        s_k[tid] = r < nr ? rows[r] : -1;
+        float4 sm = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+        for (int l = 0; l < L; ++l) {  // same l order as fle_reduce
+            const float4 e = s_e_dyn[tid * L + l];
+            sm.x += e.x;
+            sm.y += e.y;
+            sm.z += e.z;
+            sm.w += e.w;
+        }
+        s_sum[tid] = sm;
     }
-    sig[static_cast<size_t>(k) * n_rx + j] = local_affine(c, 0, M, Bs, y);
+    const int j = blockIdx.y * kCovThreads + tid;
+    const bool jok = j < n_rx;
+    // this receiver's (alpha_G, beta_G) per l, [l][thread] in shared memory
+    float4* s_a = s_e_dyn + kCovRows * L;
+#pragma unroll 1
+    for (int l = 0; l < LT; ++l)
+        s_a[l * kCovThreads + tid] = jok ? agT[static_cast<size_t>(l) * n_rx + j] : make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    if (!jok) return;
+    auto load_y = [&](int rr) {
+        const int k = rr < kCovRows ? s_k[rr] : -1;
+        return (ycache && k >= 0) ? ycache[static_cast<size_t>(k) * n_rx + j] : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    float4 ynext = load_y(0);
+#pragma unroll 1
+    for (int rr = 0; rr < kCovRows; ++rr) {
+        const int k = s_k[rr];
+        if (k < 0) break;
+        const float4 y = ynext;
+        ynext = load_y(rr + 1);  // one row ahead
+        const float4 sm = s_sum[rr];
+        // M = sum_l [(1 + aG_l) GB_l + bG_l B_l] = sum_l GB_l + sum_l [aG_l GB_l + bG_l B_l]
+        float2 M = make_float2(sm.x, sm.y), M1 = make_float2(0.f, 0.f);
+        auto term = [](float2 acc, float4 e, float4 al) {
+            acc = x2::fma(x2::bc(al.x), make_float2(e.x, e.y), acc);
+            acc = x2::fma(make_float2(-e.y, e.x), x2::bc(al.y), acc);
+            acc = x2::fma(x2::bc(al.z), make_float2(e.z, e.w), acc);
+            return x2::fma(make_float2(-e.w, e.z), x2::bc(al.w), acc);
+        };
+        if constexpr (LT > 0) {
+#pragma unroll
+            for (int l = 0; l < LT; ++l) {
+                const float4 al = s_a[l * kCovThreads + tid];
+                if (l & 1) M1 = term(M1, s_e_dyn[rr * LT + l], al);
+                else M = term(M, s_e_dyn[rr * LT + l], al);
+            }
+        } else {
+            for (int l = 0; l < L; ++l) {
+                const float4 al = agT[static_cast<size_t>(l) * n_rx + j];
+                if (l & 1) M1 = term(M1, s_e_dyn[rr * L + l], al);
+                else M = term(M, s_e_dyn[rr * L + l], al);
+            }
+        }
+        M = x2::add(M, M1);
+        // s = (1 + aL) M + bL Bs (local_affine; additive mode: aL = 0)
+        const float ar = c.additive ? 0.f : y.x, ai = c.additive ? 0.f : y.y;
+        float2 sg = x2::fma(x2::bc(ar), M, M);
+        sg = x2::fma(make_float2(-M.y, M.x), x2::bc(ai), sg);
+        sg = x2::fma(x2::bc(y.z), make_float2(sm.z, sm.w), sg);
+        sg = x2::fma(make_float2(-sm.w, sm.z), x2::bc(y.w), sg);
+        sig[static_cast<size_t>(k) * n_rx + j] = sg;
+    }
 }
 
 }  // namespace
@@ -94,13 +166,20 @@ cudaError_t launch_ag_transpose(int n_rx, int L, const float* d_ag, float* d_agT
 
 cudaError_t launch_cov_signal(const rxgs_cond_s* cs, const rxgs_txstate_s& st, int n_rx, const float* d_agT,
                               const float4* ycache, float2* d_sig, cudaStream_t s) {
-    const long long rows = static_cast<long long>(st.visible) * n_rx;  // upper bound; exact count on device
-    if (rows == 0) return cudaSuccess;
+    // upper bound on the rows; the exact count is on the device
+    const long long bound = st.needed_host >= 0 ? st.needed_host : st.visible;
+    if (bound == 0 || n_rx == 0) return cudaSuccess;
     CondDev d{};
     if (cs) d = make_dev(*cs);
-    k_cov_signal<<<static_cast<unsigned>((rows + 255) / 256), 256, 0, s>>>(
-        d, st.needed_count.as<int>(), st.needed_order.as<int>(), n_rx, st.L, st.basis32.as<float2>(),
-        st.gb32.as<float2>(), reinterpret_cast<const float4*>(d_agT), ycache, d_sig);
+    dim3 grid(static_cast<unsigned>((bound + kCovRows - 1) / kCovRows), (n_rx + kCovThreads - 1) / kCovThreads);
+    const bool reg = st.L == 9 || st.L == 4 || st.L == 1;  // specialised: alpha_G / beta_G staged per thread
+    const size_t smem = sizeof(float4) * (kCovRows + (reg ? kCovThreads : 0)) * st.L;
+    auto kern = st.L == 9 ? k_cov_signal<9> : (st.L == 4 ? k_cov_signal<4> : (st.L == 1 ? k_cov_signal<1> : k_cov_signal<0>));
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<grid, kCovThreads, smem, s>>>(d, st.needed_count.as<int>(), st.needed_order.as<int>(), n_rx, st.L,
+                                              st.basis32.as<float2>(), st.gb32.as<float2>(),
+                                              reinterpret_cast<const float4*>(d_agT), ycache, d_sig);
     return cudaGetLastError();
 }
 
