@@ -267,7 +267,7 @@ int check_receivers(rxgs_ctx ctx, rxgs_scene sc, const double* rx, int n_rx) {
 // Signals for a receiver chunk: fused conditioning (or the bare base
 // coefficients when cond == nullptr).
 int compute_signals(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, rxgs_txstate st, const double* d_rx,
-                    int n_rx, float2* d_sig) {
+                    int n_rx, SigOut d_sig) {
     cudaStream_t s = ctx->stream;
     if (c && c->host_stale) {  // the tcgen05 kernel takes layers 1/3 as a kernel parameter from the host copy
         RXGS_CUDA(cudaStreamSynchronize(s));
@@ -1189,16 +1189,19 @@ int rxgs_render_queries(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, rxgs_txstate s
     int n_chunk_ev = 0;
     RXGS_CUDA(ctx->signals.ensure(per_rx * chunk));
     RXGS_CUDA(ctx->partial.ensure(std::max<size_t>(static_cast<size_t>(n_tb) * chunk, 1) * sizeof(float)));
+    // the tcgen05 compositor reads the signals pre-split into bf16 hi/lo
+    const bool tc_comp = ctx->composite_kernel != 1 && composite_tc_eligible(*st);
+    const SigOut so = tc_comp ? SigOut::presplit(ctx->signals.p) : SigOut(ctx->signals.as<float2>());
     for (int j0 = 0; j0 < n_rx; j0 += chunk) {
         const int nj = std::min(chunk, n_rx - j0);
-        RX_TRY(compute_signals(ctx, sc, c, st, d_rx + 3 * static_cast<size_t>(j0), nj, ctx->signals.as<float2>()));
+        RX_TRY(compute_signals(ctx, sc, c, st, d_rx + 3 * static_cast<size_t>(j0), nj, so));
         CompositeOut co;
         co.spectrum = d_spec ? d_spec + static_cast<size_t>(j0) * plane : nullptr;
         co.rssi_partial = d_rssi ? ctx->partial.as<float>() : nullptr;
         cudaEvent_t ev;
         timing_begin(ctx, "composite", &ev);
-        if (ctx->composite_kernel != 1 && composite_tc_eligible(*st))
-            RXGS_CUDA(launch_composite_tc(*st, ctx->signals.as<float2>(), nj, co, s));
+        if (tc_comp)
+            RXGS_CUDA(launch_composite_tc(*st, so.split, nj, co, s));
         else
             RXGS_CUDA(launch_composite(*st, ctx->signals.as<float2>(), nj, co, s));
         timing_end(ctx, "composite", ev, nj);
@@ -1294,10 +1297,13 @@ int rxgs_coverage_table(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const rxgs_gri
         const DevGrid& g = st->grid;
         const int n_tb = g.n_tiles * g.cell_blocks;
         int rc = RXGS_OK;
+        bool tc_comp = false;
         cudaError_t e = ctx->partial.ensure(std::max<size_t>(static_cast<size_t>(n_tb) * n_rx, 1) * sizeof(float));
         if (e == cudaSuccess) {
             timing_begin(ctx, "cov_signal", &ev);
-            e = launch_cov_signal(c, *st, n_rx, t_agT.as<float>(), yc, ctx->signals.as<float2>(), s);
+            tc_comp = ctx->composite_kernel != 1 && composite_tc_eligible(*st);
+            e = launch_cov_signal(c, *st, n_rx, t_agT.as<float>(), yc,
+                                  tc_comp ? SigOut::presplit(ctx->signals.p) : SigOut(ctx->signals.as<float2>()), s);
             timing_end(ctx, "cov_signal", ev,
                        static_cast<double>(st->needed_host >= 0 ? st->needed_host : st->visible) * n_rx);
         }
@@ -1305,9 +1311,8 @@ int rxgs_coverage_table(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const rxgs_gri
             CompositeOut co;
             co.rssi_partial = ctx->partial.as<float>();
             timing_begin(ctx, "composite", &ev);
-            e = (ctx->composite_kernel != 1 && composite_tc_eligible(*st))
-                    ? launch_composite_tc(*st, ctx->signals.as<float2>(), n_rx, co, s)
-                    : launch_composite(*st, ctx->signals.as<float2>(), n_rx, co, s);
+            e = tc_comp ? launch_composite_tc(*st, ctx->signals.as<uint2>(), n_rx, co, s)
+                        : launch_composite(*st, ctx->signals.as<float2>(), n_rx, co, s);
             timing_end(ctx, "composite", ev, n_rx);
         }
         if (e == cudaSuccess)

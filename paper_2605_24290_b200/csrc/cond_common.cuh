@@ -252,6 +252,20 @@ __device__ __forceinline__ void local_mlp(const CondDev& c, const LocalSmem& w, 
     }
 }
 
+// Store one signal value (k, j, channel ch) in the requested format.
+__device__ __forceinline__ void store_sig(const SigOut& o, int k, int n_rx, int j, int C, int ch, float2 v) {
+    const size_t i = (static_cast<size_t>(k) * n_rx + j) * C + ch;
+    if (o.split) {  // C == 1
+        uint32_t h, l;
+        asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(v.y), "f"(v.x));
+        const float hx = __uint_as_float(h << 16), hy = __uint_as_float(h & 0xFFFF0000u);
+        asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(v.y - hy), "f"(v.x - hx));
+        o.split[i] = make_uint2(h, l);
+    } else {
+        o.f2[i] = v;
+    }
+}
+
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
     return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }

@@ -8,9 +8,12 @@
 //     B[cell][pos] = tw[pos][cell]                                        N = 64
 // i.e. the transposed tile product with receivers on the 128 TMEM lanes.
 // Both operands are staged through shared memory in the no-swizzle
-// MN-major canonical layout (8 MN-elements x 8 K-rows core matrices), split
-// into bf16 hi/lo on the fly (D = Ahi Bhi + Ahi Blo + Alo Bhi, ~2^-17
-// relative); 32 list positions per stage, two stages in flight: the MMAs of
+// MN-major canonical layout (8 MN-elements x 8 K-rows core matrices) as
+// bf16 hi/lo (D = Ahi Bhi + Ahi Blo + Alo Bhi, ~2^-17 relative).  The
+// signals arrive pre-split by the conditioning kernel (SigOut::presplit:
+// {bf16x2 hi, bf16x2 lo} per receiver, the same 8 bytes as complex f32), so
+// staging A is register moves only; the blend weights are split on the fly.
+// 32 list positions per stage, two stages in flight: the MMAs of
 // stage i (6 x tcgen05.mma M128 N64 K16, committed to the stage's mbarrier)
 // overlap the gather/convert of stage i+1.  Epilogue: tcgen05.ld, re/im lane
 // pairs exchanged with shuffles, spectrum amplitude, RSSI partial per tile,
@@ -41,10 +44,11 @@ __device__ __forceinline__ uint32_t mn_off(int mn, int k, uint32_t lbo) {
     return static_cast<uint32_t>((k >> 3) * lbo + (mn >> 3) * kSBO + (k & 7) * 16 + (mn & 7) * 2);
 }
 
+template <bool FIELD>
 __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t* __restrict__ tile_offsets,
                                                        const int* __restrict__ list, const float* __restrict__ tw,
                                                        const int* __restrict__ walk_len,
-                                                       const float2* __restrict__ sig, int n_rx,
+                                                       const uint2* __restrict__ sig, int n_rx,
                                                        float* __restrict__ spectrum, float* __restrict__ rssi_partial,
                                                        float* __restrict__ field32) {
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -82,7 +86,8 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
     // receivers j0+2l, j0+2l+1 (= m-values 4l..4l+3); B: one 256 B blend-weight
     // row per half-warp (lane holds cells 4(l%16)..+3).  Loads for stage s+1
     // are issued before stage s's barrier/MMA so their latency is hidden.
-    float4 ra[8], rb[4];
+    uint4 ra[8];
+    float4 rb[4];
     const bool even_n = (n_rx & 1) == 0;
     // list indices of a whole stage in one coalesced load (lane i <-> position i)
     auto load_idx = [&](int st) {
@@ -95,16 +100,16 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
         for (int i = 0; i < 8; ++i) {
             const int pos = st * kKS + 8 * warp + i;
             const int k = __shfl_sync(0xffffffffu, kidx, 8 * warp + i);
-            ra[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            ra[i] = make_uint4(0u, 0u, 0u, 0u);
             if (pos < W) {
                 const int jj = j0 + 2 * lane;
-                const float2* rowp = sig + static_cast<size_t>(k) * n_rx + jj;
+                const uint2* rowp = sig + static_cast<size_t>(k) * n_rx + jj;
                 if (even_n && jj + 1 < n_rx) {
-                    ra[i] = *reinterpret_cast<const float4*>(rowp);
+                    ra[i] = *reinterpret_cast<const uint4*>(rowp);
                 } else {
-                    const float2 a = jj < n_rx ? rowp[0] : make_float2(0.f, 0.f);
-                    const float2 b = jj + 1 < n_rx ? rowp[1] : make_float2(0.f, 0.f);
-                    ra[i] = make_float4(a.x, a.y, b.x, b.y);
+                    const uint2 a = jj < n_rx ? rowp[0] : make_uint2(0u, 0u);
+                    const uint2 b = jj + 1 < n_rx ? rowp[1] : make_uint2(0u, 0u);
+                    ra[i] = make_uint4(a.x, a.y, b.x, b.y);
                 }
             }
         }
@@ -135,12 +140,10 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
             ph[buf] ^= 1u;
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            uint2 hi, lo;
-            split4(ra[i], hi, lo);
+        for (int i = 0; i < 8; ++i) {  // {hi0, lo0, hi1, lo1} -> (hi0, hi1), (lo0, lo1)
             const uint32_t off = mn_off(4 * lane, 8 * warp + i, kALBO);
-            *reinterpret_cast<uint2*>(a_hi + off) = hi;
-            *reinterpret_cast<uint2*>(a_lo + off) = lo;
+            *reinterpret_cast<uint2*>(a_hi + off) = make_uint2(ra[i].x, ra[i].z);
+            *reinterpret_cast<uint2*>(a_lo + off) = make_uint2(ra[i].y, ra[i].w);
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -210,7 +213,7 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
             const float o = __shfl_xor_sync(0xffffffffu, v, 1);
             const int cell = 16 * ch + q;
             const int row = tt * 8 + (cell >> 3), col = tp * 8 + (cell & 7);
-            if (field32 && row < g.nt && col < g.np && j < n_rx)
+            if (FIELD && row < g.nt && col < g.np && j < n_rx)
                 field32[(static_cast<size_t>(j) * 2 + (is_im ? 1 : 0)) * plane + static_cast<size_t>(row) * g.np + col] = v;
             if (mine) {
                 const float re = is_im ? o : v, im = is_im ? v : o;
@@ -308,15 +311,15 @@ cudaError_t launch_tc_selftest_mn(float* d_err, cudaStream_t s) {
 
 bool composite_tc_eligible(const rxgs_txstate_s& st) { return st.grid.cell_blocks == 1 && st.grid.ts == 8 && st.channels == 1; }
 
-cudaError_t launch_composite_tc(const rxgs_txstate_s& st, const float2* d_sig, int n_rx, const CompositeOut& out,
+cudaError_t launch_composite_tc(const rxgs_txstate_s& st, const uint2* d_sig, int n_rx, const CompositeOut& out,
                                 cudaStream_t s) {
     const DevGrid& g = st.grid;
     const size_t smem = 2 * kStageBytes;
-    cudaError_t e = cudaFuncSetAttribute(k_composite_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    auto kern = out.field32 ? k_composite_tc<true> : k_composite_tc<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     dim3 grid(g.n_tiles, (n_rx + kM / 2 - 1) / (kM / 2));
-    k_composite_tc<<<grid, kThr, smem, s>>>(g, st.tile_offsets.as<int64_t>(), st.list.as<int>(), st.tw.as<float>(),
+    kern<<<grid, kThr, smem, s>>>(g, st.tile_offsets.as<int64_t>(), st.list.as<int>(), st.tw.as<float>(),
                                             st.walk_len.as<int>(), d_sig, n_rx, out.spectrum, out.rssi_partial,
                                             out.field32);
     return cudaGetLastError();

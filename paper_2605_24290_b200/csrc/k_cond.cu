@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(512, 1)
     k_cond_signal(CondDev c, const int* __restrict__ n_rows, const int* __restrict__ vis, const float4* __restrict__ pos32,
                   const double* __restrict__ rx, int n_rx, const float2* __restrict__ B,
                   const float2* __restrict__ GB, const float* __restrict__ ag,
-                  float2* __restrict__ sig) {
+                  SigOut sig) {
     extern __shared__ __align__(16) float smem[];
     const int H = HT > 0 ? HT : c.H;
     const int C = CT > 0 ? CT : c.C;
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(512, 1)
             const float ar = c.additive ? 0.f : y[4 * ch], ai = c.additive ? 0.f : y[4 * ch + 1];
             const float2 s0 = cmul(make_float2(1.f + ar, ai), M);
             const float2 s1 = cmul(make_float2(y[4 * ch + 2], y[4 * ch + 3]), Bs);
-            sig[(static_cast<size_t>(k) * n_rx + j) * C + ch] = make_float2(s0.x + s1.x, s0.y + s1.y);
+            store_sig(sig, k, n_rx, j, C, ch, make_float2(s0.x + s1.x, s0.y + s1.y));
         }
     }
 }
@@ -334,7 +334,7 @@ cudaError_t launch_cond_global(const rxgs_cond_s& c, const double* d_rx, int n_r
 
 cudaError_t launch_cond_signal(const rxgs_cond_s* c, const rxgs_scene_s& sc,
                                const rxgs_txstate_s& st, const double* d_rx, int n_rx,
-                               const float* d_ag, float2* d_sig, int* d_err, cudaStream_t s) {
+                               const float* d_ag, SigOut d_sig, int* d_err, cudaStream_t s) {
     (void)d_err;
     if (st.visible == 0 || n_rx == 0) return cudaSuccess;
     if (sc.ctx->cond_kernel != 1 && cond_tc_eligible(c))

@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_cond_tc(const __grid_constant__ LocalW W, CondDev c, const int* __restrict__ n_rows_dev, int n_rows_host,
               int cap, const int* __restrict__ rows, const float4* __restrict__ rpos, const double* __restrict__ rx,
               int n_rx, const float4* __restrict__ rGB, const float4* __restrict__ rS,
-              const float* __restrict__ ag, float2* __restrict__ sig,
+              const float* __restrict__ ag, SigOut sig,
               float4* __restrict__ ycache) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* w2hi = smem;
@@ -544,11 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 sg = x2::fma(make_float2(-M.y, M.x), x2::bc(al.y), sg);
                 sg = x2::fma(x2::bc(yb.x), Bs, sg);
                 sg = x2::fma(make_float2(-Bs.y, Bs.x), x2::bc(yb.y), sg);
-#ifdef RXGS_AB_NOSTORE
-                if (sg.x == 12345.f) sig[static_cast<size_t>(k) * n_rx + j] = sg;
-#else
-                sig[static_cast<size_t>(k) * n_rx + j] = sg;
-#endif
+                store_sig(sig, k, n_rx, j, 1, 0, sg);
             }
         }
         r = rn;
@@ -662,7 +658,7 @@ namespace {
 template <bool YOUT>
 cudaError_t launch_tc(const rxgs_cond_s& cs, const int* n_rows_dev, long long rows_host, int cap, const int* rows,
                       const float4* rpos, const double* d_rx, int n_rx, const float4* rGB, const float4* rS,
-                      const float* d_ag, float2* d_sig, float4* ycache, cudaStream_t s) {
+                      const float* d_ag, SigOut d_sig, float4* ycache, cudaStream_t s) {
     if (rows_host == 0 || n_rx == 0) return cudaSuccess;
     const CondDev d = make_dev(cs);
     LocalW w{};
@@ -695,7 +691,7 @@ cudaError_t launch_tc(const rxgs_cond_s& cs, const int* n_rows_dev, long long ro
 }  // namespace
 
 cudaError_t launch_cond_signal_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
-                                  const double* d_rx, int n_rx, const float* d_ag, float2* d_sig,
+                                  const double* d_rx, int n_rx, const float* d_ag, SigOut d_sig,
                                   cudaStream_t s) {
     if (st.visible == 0 || n_rx == 0) return cudaSuccess;
     rxgs_ctx ctx = sc.ctx;
@@ -720,7 +716,7 @@ cudaError_t launch_cond_signal_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc,
 cudaError_t launch_local_cache_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const double* d_rx, int n_rx,
                                   float4* ycache, cudaStream_t s) {
     return launch_tc<true>(cs, nullptr, sc.k, sc.k, sc.d_morton.as<int>(), sc.d_mpos32.as<float4>(), d_rx, n_rx,
-                           nullptr, nullptr, nullptr, nullptr, ycache, s);
+                           nullptr, nullptr, nullptr, SigOut(), ycache, s);
 }
 
 cudaError_t launch_tc_selftest(float* d_err, cudaStream_t s) {

@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(kCovThreads, 3) k_cov_signal(CondDev c, const 
                                                             const int* __restrict__ rows, int n_rx, int L,
                                                             const float2* __restrict__ B, const float2* __restrict__ GB,
                                                             const float4* __restrict__ agT,
-                                                            const float4* __restrict__ ycache, float2* __restrict__ sig) {
+                                                            const float4* __restrict__ ycache, SigOut sig) {
     extern __shared__ float4 s_e_dyn[];  // (GB, B) per (row, l): [kCovRows][L], then s_a
     __shared__ float4 s_sum[kCovRows];          // (sum_l GB, sum_l B)
     __shared__ int s_k[kCovRows];
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kCovThreads, 3) k_cov_signal(CondDev c, const 
         sg = x2::fma(make_float2(-M.y, M.x), x2::bc(ai), sg);
         sg = x2::fma(x2::bc(y.z), make_float2(sm.z, sm.w), sg);
         sg = x2::fma(make_float2(-sm.w, sm.z), x2::bc(y.w), sg);
-        sig[static_cast<size_t>(k) * n_rx + j] = sg;
+        store_sig(sig, k, n_rx, j, 1, 0, sg);
     }
 }
 
@@ -165,7 +165,7 @@ cudaError_t launch_ag_transpose(int n_rx, int L, const float* d_ag, float* d_agT
 }
 
 cudaError_t launch_cov_signal(const rxgs_cond_s* cs, const rxgs_txstate_s& st, int n_rx, const float* d_agT,
-                              const float4* ycache, float2* d_sig, cudaStream_t s) {
+                              const float4* ycache, SigOut d_sig, cudaStream_t s) {
     // upper bound on the rows; the exact count is on the device
     const long long bound = st.needed_host >= 0 ? st.needed_host : st.visible;
     if (bound == 0 || n_rx == 0) return cudaSuccess;

@@ -70,6 +70,22 @@ struct DevBuf {
     }
 };
 
+// Destination of the per-(Gaussian, receiver) signals s[k][j][c]: either
+// complex f32 (f2), or -- for the tcgen05 compositor, C == 1 -- the same 8
+// bytes pre-split for its bf16x3 product: split[k][j] = {hi, lo} with hi =
+// bf16x2(re, im) rounded to nearest and lo = bf16x2 of the remainders.
+struct SigOut {
+    float2* f2 = nullptr;
+    uint2* split = nullptr;
+    SigOut() = default;
+    SigOut(float2* p) : f2(p) {}  // NOLINT: implicit on purpose
+    static SigOut presplit(void* p) {
+        SigOut o;
+        o.split = static_cast<uint2*>(p);
+        return o;
+    }
+};
+
 struct KStat {
     double ms = 0.0;
     int64_t launches = 0;
@@ -197,7 +213,7 @@ cudaError_t launch_cond_global(const rxgs_cond_s& c, const double* d_rx, int n_r
 // Fused local branch + FLE reduction: signals[k][j][c] complex f32.
 cudaError_t launch_cond_signal(const rxgs_cond_s* c, const rxgs_scene_s& sc,
                                const rxgs_txstate_s& st, const double* d_rx, int n_rx,
-                               const float* d_ag, float2* d_sig, int* d_err, cudaStream_t s);
+                               const float* d_ag, SigOut d_sig, int* d_err, cudaStream_t s);
 // Materialised conditioned coefficients (condition_forward API).
 cudaError_t launch_cond_materialize(const rxgs_cond_s& c, const rxgs_scene_s& sc,
                                     const double* d_rx, int n_rx, const float* d_ag, double* d_out,
@@ -209,7 +225,7 @@ cudaError_t launch_check_coincide(const rxgs_scene_s& sc, const double* d_rx, in
 // tcgen05 variant of the hot kernel (k_cond_tc.cu): hidden 64, C == 1.
 bool cond_tc_eligible(const rxgs_cond_s* c);
 cudaError_t launch_cond_signal_tc(const rxgs_cond_s& c, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
-                                  const double* d_rx, int n_rx, const float* d_ag, float2* d_sig,
+                                  const double* d_rx, int n_rx, const float* d_ag, SigOut d_sig,
                                   cudaStream_t s);
 cudaError_t launch_tc_selftest(float* d_err, cudaStream_t s);
 cudaError_t launch_tc_selftest_mn(float* d_err, cudaStream_t s);
@@ -229,7 +245,8 @@ cudaError_t launch_composite(const rxgs_txstate_s& st, const float2* d_sig, int 
                              const CompositeOut& out, cudaStream_t s);
 // tcgen05 compositing (k_composite_tc.cu): 8x8 tiles, C == 1.
 bool composite_tc_eligible(const rxgs_txstate_s& st);
-cudaError_t launch_composite_tc(const rxgs_txstate_s& st, const float2* d_sig, int n_rx, const CompositeOut& out,
+// reads the pre-split signals (SigOut::presplit)
+cudaError_t launch_composite_tc(const rxgs_txstate_s& st, const uint2* d_sig, int n_rx, const CompositeOut& out,
                                 cudaStream_t s);
 cudaError_t launch_rssi_finalize(const float* d_partial, int n_tiles, int n_rx, float* d_rssi,
                                  double* d_rssi64, cudaStream_t s);
@@ -248,7 +265,7 @@ cudaError_t launch_local_cache(const rxgs_cond_s& cs, const rxgs_scene_s& sc, co
                                float4* ycache, cudaStream_t s);
 cudaError_t launch_ag_transpose(int n_rx, int L, const float* d_ag, float* d_agT, cudaStream_t s);
 cudaError_t launch_cov_signal(const rxgs_cond_s* cs, const rxgs_txstate_s& st, int n_rx, const float* d_agT,
-                              const float4* ycache, float2* d_sig, cudaStream_t s);
+                              const float4* ycache, SigOut d_sig, cudaStream_t s);
 // ---- k_cond_bwd.cu (FP64 materialised conditioning adjoint)
 size_t cond_backward_ws_bytes(const rxgs_cond_s& cs, int K, int sms);
 cudaError_t launch_cond_backward(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const double* d_rx,
