@@ -57,9 +57,9 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
     __shared__ float s_dom[8];  // solid angle of the tile's 8 rows
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int tile = blockIdx.x;
-    if (tid < 8) {
+    if (tid < 8) {  // zero for rows past the grid (partial last tile row)
         const int row = (tile / g.tiles_p) * 8 + tid;
-        s_dom[tid] = static_cast<float>(sin(g.tmin + (row + 0.5) * g.dth) * g.dth * g.dph);
+        s_dom[tid] = row < g.nt ? static_cast<float>(sin(g.tmin + (row + 0.5) * g.dth) * g.dth * g.dph) : 0.f;
     }
     const int j0 = blockIdx.y * (kM / 2);
     const int W = walk_len[tile];
@@ -95,21 +95,28 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
         return pos < W ? list[begin + pos] : 0;
     };
     int kidx = n_stages > 0 ? load_idx(0) : 0;
+    // A: lane holds receivers j0 + 4 (lane % 16) .. +3 of list position
+    // 8w + 2i + lane / 16 (i = 0..3): two 16-byte loads of {hi, lo} pairs,
+    // regrouped into one 16-byte row (4 receivers re/im) per bf16 plane.
     auto load = [&](int st) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int pos = st * kKS + 8 * warp + i;
-            const int k = __shfl_sync(0xffffffffu, kidx, 8 * warp + i);
-            ra[i] = make_uint4(0u, 0u, 0u, 0u);
+        for (int i = 0; i < 4; ++i) {
+            const int pp = 8 * warp + 2 * i + (lane >> 4);
+            const int pos = st * kKS + pp;
+            const int k = __shfl_sync(0xffffffffu, kidx, pp);
+            ra[2 * i] = ra[2 * i + 1] = make_uint4(0u, 0u, 0u, 0u);
             if (pos < W) {
-                const int jj = j0 + 2 * lane;
+                const int jj = j0 + 4 * (lane & 15);
                 const uint2* rowp = sig + static_cast<size_t>(k) * n_rx + jj;
-                if (even_n && jj + 1 < n_rx) {
-                    ra[i] = *reinterpret_cast<const uint4*>(rowp);
+                if (even_n && jj + 3 < n_rx) {
+                    ra[2 * i] = *reinterpret_cast<const uint4*>(rowp);
+                    ra[2 * i + 1] = *reinterpret_cast<const uint4*>(rowp + 2);
                 } else {
-                    const uint2 a = jj < n_rx ? rowp[0] : make_uint2(0u, 0u);
-                    const uint2 b = jj + 1 < n_rx ? rowp[1] : make_uint2(0u, 0u);
-                    ra[i] = make_uint4(a.x, a.y, b.x, b.y);
+                    uint2 t[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) t[q] = jj + q < n_rx ? rowp[q] : make_uint2(0u, 0u);
+                    ra[2 * i] = make_uint4(t[0].x, t[0].y, t[1].x, t[1].y);
+                    ra[2 * i + 1] = make_uint4(t[2].x, t[2].y, t[3].x, t[3].y);
                 }
             }
         }
@@ -140,10 +147,10 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
             ph[buf] ^= 1u;
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {  // {hi0, lo0, hi1, lo1} -> (hi0, hi1), (lo0, lo1)
-            const uint32_t off = mn_off(4 * lane, 8 * warp + i, kALBO);
-            *reinterpret_cast<uint2*>(a_hi + off) = make_uint2(ra[i].x, ra[i].z);
-            *reinterpret_cast<uint2*>(a_lo + off) = make_uint2(ra[i].y, ra[i].w);
+        for (int i = 0; i < 4; ++i) {  // {hi0, lo0, hi1, lo1}, {hi2, lo2, hi3, lo3} -> (hi0..hi3), (lo0..lo3)
+            const uint32_t off = mn_off(8 * (lane & 15), 8 * warp + 2 * i + (lane >> 4), kALBO);
+            *reinterpret_cast<uint4*>(a_hi + off) = make_uint4(ra[2 * i].x, ra[2 * i].z, ra[2 * i + 1].x, ra[2 * i + 1].z);
+            *reinterpret_cast<uint4*>(a_lo + off) = make_uint4(ra[2 * i].y, ra[2 * i].w, ra[2 * i + 1].y, ra[2 * i + 1].w);
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -195,6 +202,10 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
     const size_t plane = static_cast<size_t>(g.nt) * g.np;
     float* s_amp = reinterpret_cast<float*>(smem);  // [64 receivers][68] (stage buffers are free now)
     constexpr int kAmpStride = 68;                  // 16 B aligned rows, bank-spread
+    // Lanes 2j / 2j+1 hold re / im of receiver j for every cell.  For each
+    // column pair (q, q+1) one exchange gives the even lane (re, im) of cell
+    // q and the odd lane (re, im) of cell q+1: every lane finishes one cell
+    // per pair, no divergence.
     float pw = 0.f;
 #pragma unroll
     for (int ch = 0; ch < 4; ++ch) {
@@ -206,21 +217,27 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
 #pragma unroll
             for (int q = 0; q < 16; ++q) r[q] = 0u;
         }
-        const bool mine = (ch < 2) != is_im;  // even lane: cells 0-31, odd lane: 32-63
+        if (FIELD) {
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            const float v = __uint_as_float(r[q]);
-            const float o = __shfl_xor_sync(0xffffffffu, v, 1);
-            const int cell = 16 * ch + q;
-            const int row = tt * 8 + (cell >> 3), col = tp * 8 + (cell & 7);
-            if (FIELD && row < g.nt && col < g.np && j < n_rx)
-                field32[(static_cast<size_t>(j) * 2 + (is_im ? 1 : 0)) * plane + static_cast<size_t>(row) * g.np + col] = v;
-            if (mine) {
-                const float re = is_im ? o : v, im = is_im ? v : o;
-                const float p2 = re * re + im * im;
-                s_amp[jl * kAmpStride + cell] = sqrtf(p2 + static_cast<float>(kAmpEps));
-                if (row < g.nt) pw += p2 * s_dom[cell >> 3];
+            for (int q = 0; q < 16; ++q) {
+                const int cell = 16 * ch + q;
+                const int row = tt * 8 + (cell >> 3), col = tp * 8 + (cell & 7);
+                if (row < g.nt && col < g.np && j < n_rx)
+                    field32[(static_cast<size_t>(j) * 2 + (is_im ? 1 : 0)) * plane + static_cast<size_t>(row) * g.np + col] =
+                        __uint_as_float(r[q]);
             }
+        }
+#pragma unroll
+        for (int q = 0; q < 16; q += 2) {
+            const float v0 = __uint_as_float(r[q]), v1 = __uint_as_float(r[q + 1]);
+            const float got = __shfl_xor_sync(0xffffffffu, is_im ? v0 : v1, 1);
+            const float re = is_im ? got : v0, im = is_im ? v1 : got;
+            const int cell = 16 * ch + q + (is_im ? 1 : 0);
+            const float p2 = fmaf(re, re, im * im);
+            float amp;
+            asm("sqrt.approx.f32 %0, %1;" : "=f"(amp) : "f"(p2 + static_cast<float>(kAmpEps)));
+            s_amp[jl * kAmpStride + cell] = amp;
+            pw = fmaf(p2, s_dom[cell >> 3], pw);  // rows past the grid have s_dom = 0
         }
     }
     pw += __shfl_xor_sync(0xffffffffu, pw, 1);
