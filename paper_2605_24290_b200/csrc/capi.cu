@@ -977,6 +977,9 @@ int rxgs_cond_create(rxgs_ctx ctx, const int32_t cfg[9], const double* params, c
             c->hi[a] = hi[a];
         }
         c->has_occ = true;
+        e = launch_occ_cubes(*c, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) return bad(e, "occ cubes");
     }
     ctx_retain(ctx);
     *out = c;
@@ -1032,6 +1035,7 @@ int rxgs_build_occupancy(rxgs_ctx ctx, rxgs_scene sc, int R, const double lo_[3]
             attach->hi[a] = hi[a];
         }
         attach->has_occ = true;
+        RXGS_CUDA(launch_occ_cubes(*attach, ctx->stream));
     }
     RX_TRY(finish_out(ctx, out, d64, n));
     RXGS_CUDA(cudaStreamSynchronize(ctx->stream));

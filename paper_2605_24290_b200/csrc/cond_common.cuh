@@ -16,6 +16,7 @@ struct CondDev {
     const float* p32;
     const double* p64;
     const float* occ;
+    const float* cube;  // trilinear cell table (rxgs_cond_s::d_occ_cube)
     int F, H, dc, S, R, nearest, mode, L, C, gin;
     int o_freq, o_gw1, o_gb1, o_gw2, o_gb2, o_gw3, o_gb3, o_emb, o_lw1, o_lb1, o_lw2, o_lb2, o_lw3, o_lb3;
     int probe;  // 1 = sample the occupancy grid, 0 = T=1, rho=0
@@ -28,6 +29,7 @@ inline CondDev make_dev(const rxgs_cond_s& c) {
     d.p32 = c.d_params32.as<float>();
     d.p64 = c.d_params64.as<double>();
     d.occ = c.d_occ32.as<float>();
+    d.cube = c.d_occ_cube.as<float>();
     d.F = c.F; d.H = c.hidden; d.dc = c.dc; d.S = c.S; d.R = c.R; d.nearest = c.nearest;
     d.mode = c.mode; d.L = c.L; d.C = c.C; d.gin = c.gin;
     d.o_freq = static_cast<int>(c.o_freq); d.o_gw1 = static_cast<int>(c.o_gw1);

@@ -101,6 +101,35 @@ __global__ void __launch_bounds__(kGlobThreads) k_cond_global(CondDev c, const d
     }
 }
 
+// ------------------------------------------------------------------ trilinear cell table
+// Cell (cx, cy, cz) in [-1, R]^3 (the cells a clamped or in-grid sample can
+// fall in) -> the coefficients of v = a + b w0 + c w1 + d w2 + e w0 w1 +
+// f w0 w2 + g w1 w2 + h w0 w1 w2 (out-of-grid corners read 0, as in
+// sample_trilinear, conditioning.cpp:74-98), stored [a, d, b, f, c, g, e, h]
+// so the probe evaluates it with three FFMA2 and one FFMA (k_cond_tc.cu).
+// Computed in FP64 from the FP32 grid values, rounded once.
+__global__ void k_occ_cubes(int R, const float* __restrict__ occ, float* __restrict__ cube) {
+    const int P = R + 2;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P * P * P) return;
+    const int cx = i / (P * P) - 1, cy = (i / P) % P - 1, cz = i % P - 1;
+    auto q = [&](int x, int y, int z) -> double {
+        return (x < 0 || y < 0 || z < 0 || x >= R || y >= R || z >= R) ? 0.0 : occ[(x * R + y) * R + z];
+    };
+    const double q000 = q(cx, cy, cz), q001 = q(cx, cy, cz + 1), q010 = q(cx, cy + 1, cz), q011 = q(cx, cy + 1, cz + 1);
+    const double q100 = q(cx + 1, cy, cz), q101 = q(cx + 1, cy, cz + 1), q110 = q(cx + 1, cy + 1, cz),
+                 q111 = q(cx + 1, cy + 1, cz + 1);
+    float* o = cube + 8 * static_cast<size_t>(i);
+    o[0] = static_cast<float>(q000);                                      // a
+    o[1] = static_cast<float>(q001 - q000);                               // d (z)
+    o[2] = static_cast<float>(q100 - q000);                               // b (x)
+    o[3] = static_cast<float>(q101 - q100 - q001 + q000);                 // f (xz)
+    o[4] = static_cast<float>(q010 - q000);                               // c (y)
+    o[5] = static_cast<float>(q011 - q010 - q001 + q000);                 // g (yz)
+    o[6] = static_cast<float>(q110 - q100 - q010 + q000);                 // e (xy)
+    o[7] = static_cast<float>(q111 - q110 - q101 - q011 + q100 + q010 + q001 - q000);  // h (xyz)
+}
+
 // ------------------------------------------------------------------ local branch helpers
 
 // ------------------------------------------------------------------ fused hot kernel
@@ -386,6 +415,15 @@ cudaError_t launch_cond_materialize(const rxgs_cond_s& c, const rxgs_scene_s& sc
     k_cond_materialize<<<static_cast<unsigned>((rows + 255) / 256), 256, smem, s>>>(
         d, sc.k, sc.d_pos32.as<float4>(), d_rx, n_rx, sc.d_coeffs64.as<double>(), d_ag, d_out,
         d_local_in);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_occ_cubes(rxgs_cond_s& c, cudaStream_t s) {
+    const int P = c.R + 2;
+    const size_t n = static_cast<size_t>(P) * P * P;
+    cudaError_t e = c.d_occ_cube.ensure(n * 8 * sizeof(float));
+    if (e != cudaSuccess) return e;
+    k_occ_cubes<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(c.R, c.d_occ32.as<float>(), c.d_occ_cube.as<float>());
     return cudaGetLastError();
 }
 

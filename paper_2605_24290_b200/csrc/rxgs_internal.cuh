@@ -174,6 +174,9 @@ struct rxgs_cond_s {
     double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     int64_t global_calls = 0, local_calls = 0;
     rxgs_b200::DevBuf d_params32, d_params64, d_occ32;
+    // trilinear cell table: per cell c in [-1, R]^3 the 8 polynomial
+    // coefficients of its trilinear patch (k_occ_cubes, k_cond.cu)
+    rxgs_b200::DevBuf d_occ_cube;
     bool host_stale = false;  // device parameters updated by the optimizer
     bool use_global() const { return mode != 2; }
     bool use_local() const { return mode != 1; }
@@ -218,6 +221,8 @@ cudaError_t launch_cond_signal(const rxgs_cond_s* c, const rxgs_scene_s& sc,
 cudaError_t launch_cond_materialize(const rxgs_cond_s& c, const rxgs_scene_s& sc,
                                     const double* d_rx, int n_rx, const float* d_ag, double* d_out,
                                     double* d_local_in, int* d_err, cudaStream_t s);
+// (re)build rxgs_cond_s::d_occ_cube from d_occ32
+cudaError_t launch_occ_cubes(rxgs_cond_s& c, cudaStream_t s);
 cudaError_t launch_probe(const rxgs_cond_s& c, int n, const double* d_from, const double* d_to,
                          double* d_out, cudaStream_t s);
 cudaError_t launch_check_coincide(const rxgs_scene_s& sc, const double* d_rx, int n_rx, int* d_err,
