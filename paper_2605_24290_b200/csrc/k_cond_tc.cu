@@ -49,8 +49,19 @@ namespace {
 using namespace cond_dev;
 
 constexpr int kH = 64;
-constexpr int kGroups = 4;
+// RXGS_A2_SMEM: the layer-2 A operand (bf16 hi/lo of ReLU(h1), 32 KB per
+// group) lives in shared memory instead of TMEM, so a group needs only 80
+// TMEM columns (D + the layer-1 A) and up to 6 groups fit one SM.
+#ifndef RXGS_A2_SMEM
+#define RXGS_A2_SMEM 0
+#endif
+#ifndef RXGS_GROUPS
+#define RXGS_GROUPS 4
+#endif
+constexpr int kGroups = RXGS_GROUPS;
+static_assert(RXGS_A2_SMEM || kGroups == 4, "more than 4 groups need the A2 operand in shared memory");
 constexpr int kThreads = 128 * kGroups;
+constexpr int kA2Bytes = 128 * 64 * 2;  // one bf16 128x64 K-major operand
 constexpr uint32_t kIdesc = tc::idesc_bf16_f32(128, kH);
 constexpr int kW2Bytes = kH * kH * 2;   // one bf16 64x64 matrix
 constexpr int kW1Bytes = kH * 16 * 2;   // one bf16 64x16 matrix
@@ -310,11 +321,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* w2hi = smem;
     uint8_t* w2lo = smem + kW2Bytes;
-    uint8_t* w1hi = smem + 2 * kW2Bytes;  // [W1 | b1 | 0] : 64 x 16 bf16
+    // layer 1 in two K=16 MMAs against A1 = [x_hi (6), 1, 0, x_lo (6), 0, 0]:
+    //   w1hi = [W1hi | b1hi | 0 | W1hi | 0 0]   (x_hi W1hi + b1hi + x_lo W1hi)
+    //   w1lo = [W1lo | b1lo | 0 ...]            (x_hi W1lo + b1lo)
+    uint8_t* w1hi = smem + 2 * kW2Bytes;
     uint8_t* w1lo = w1hi + kW1Bytes;
-    uint8_t* b2hi = w1lo + kW1Bytes;      // [b2 | 0] : 64 x 16 bf16
-    uint8_t* b2lo = b2hi + kW1Bytes;
-    uint8_t* aone = b2lo + kW1Bytes;      // [1 | 0] : 128 x 16 bf16
+    uint8_t* b2hi = w1lo + kW1Bytes;      // [b2hi | b2lo | 0] : 64 x 16 bf16 (one MMA against aone)
+    uint8_t* b2lo = b2hi + kW1Bytes;      // (unused)
+    uint8_t* aone = b2lo + kW1Bytes;      // [1 | 1 | 0] : 128 x 16 bf16
     float* s_occ = reinterpret_cast<float*>(smem + kFixedSmem);
     __shared__ uint64_t bars[kGroups];
     __shared__ uint32_t arrivals[kGroups];
@@ -330,12 +344,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = tid; i < kH * 16; i += kThreads) {
         const int n = i / 16, k = i % 16;
         const float w = k < 6 ? c.p32[c.o_lw1 + n * 6 + k] : (k == 6 ? c.p32[c.o_lb1 + n] : 0.f);
-        split_store(w1hi, w1lo, canon_off16(n, k), w);
-        split_store(b2hi, b2lo, canon_off16(n, k), k == 0 ? c.p32[c.o_lb2 + n] : 0.f);
+        const float whi = tc::bf16_round(w);
+        const uint32_t off = canon_off16(n, k);
+        // k < 7: W1|b1 hi and lo;  8 <= k < 14: W1 hi again (multiplies x_lo)
+        const float wa = k < 7 ? whi : ((k >= 8 && k < 14) ? tc::bf16_round(c.p32[c.o_lw1 + n * 6 + (k - 8)]) : 0.f);
+        const float wb = k < 7 ? w - whi : 0.f;
+        *reinterpret_cast<uint16_t*>(w1hi + off) = static_cast<uint16_t>(tc::pack_bf16(wa, 0.f) & 0xFFFFu);
+        *reinterpret_cast<uint16_t*>(w1lo + off) = static_cast<uint16_t>(tc::pack_bf16(wb, 0.f) & 0xFFFFu);
+        const float b2 = c.p32[c.o_lb2 + n], b2h = tc::bf16_round(b2);
+        const float bv = k == 0 ? b2h : (k == 1 ? b2 - b2h : 0.f);
+        *reinterpret_cast<uint16_t*>(b2hi + off) = static_cast<uint16_t>(tc::pack_bf16(bv, 0.f) & 0xFFFFu);
     }
     for (int i = tid; i < 128 * 16; i += kThreads) {
         const int r = i / 16, k = i % 16;
-        *reinterpret_cast<uint16_t*>(aone + canon_off16(r, k)) = k == 0 ? 0x3F80u : 0u;  // bf16 1.0
+        *reinterpret_cast<uint16_t*>(aone + canon_off16(r, k)) = k < 2 ? 0x3F80u : 0u;  // bf16 1.0
     }
     if (c.probe && !RXGS_PROBE_CUBE) load_padded_occ(c, s_occ);
     if (warp == 0) {
@@ -353,12 +375,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const uint32_t tbase = tbase_s;
     const uint32_t lane_off = static_cast<uint32_t>(32 * wl) << 16;
+#if RXGS_A2_SMEM
+    const uint32_t tm_d = tbase + 64 * g;                    // 64 f32 columns (layer-1 then layer-2 accumulator)
+    const uint32_t tm_ahi = tbase + 64 * kGroups + 16 * g;  // layer-1 A: 8 columns hi + 8 lo
+    const uint32_t tm_alo = tm_ahi + 8;
+    uint8_t* a2hi = smem + kFixedSmem + static_cast<size_t>(g) * 2 * kA2Bytes;
+    uint8_t* a2lo = a2hi + kA2Bytes;
+    const uint32_t a2hi_a = tc::smem_u32(a2hi), a2lo_a = tc::smem_u32(a2lo);
+    const int arow = 32 * wl + lane;  // this thread's A row (= TMEM lane)
+#else
     const uint32_t tm_d = tbase + 128 * g;       // 64 f32 columns (layer-1 then layer-2 accumulator)
     const uint32_t tm_ahi = tm_d + 64;           // 32 columns = 64 bf16 (layer-1 A uses the first 8)
     const uint32_t tm_alo = tm_d + 96;
+#endif
     const uint32_t w2hi_a = tc::smem_u32(w2hi), w2lo_a = tc::smem_u32(w2lo);
     const uint32_t w1hi_a = tc::smem_u32(w1hi), w1lo_a = tc::smem_u32(w1lo);
-    const uint32_t b2hi_a = tc::smem_u32(b2hi), b2lo_a = tc::smem_u32(b2lo), aone_a = tc::smem_u32(aone);
+    const uint32_t b2hi_a = tc::smem_u32(b2hi), aone_a = tc::smem_u32(aone);
 
     const int n_rows = YOUT ? n_rows_host : *n_rows_dev;
     const int nq = (n_rx + 3) >> 2;
@@ -522,27 +554,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             M = x2::add(M, M1);
         }
         };
-        // ---- layer 1 on the tensor cores: A1 = [x, 1, 0...] (K = 16) hi/lo -> TMEM
+        // ---- layer 1 on the tensor cores: A1 = [x_hi, 1, 0, x_lo, 0, 0] (K = 16) -> TMEM,
+        // two MMAs (hi.hi + lo.hi + bias in one, hi.lo in the other)
         {
-            uint32_t hi[8], lo[8];
+            uint32_t a[8];
 #pragma unroll
-            for (int q = 0; q < 3; ++q) x2::split_bf16(in[2 * q], in[2 * q + 1], hi[q], lo[q]);
-            hi[3] = 0x3F80u;  // (1, 0): the bias feature
-            lo[3] = 0u;
-#pragma unroll
-            for (int q = 4; q < 8; ++q) hi[q] = lo[q] = 0u;
-            tc::tmem_st8(tm_ahi + lane_off, hi);
-            tc::tmem_st8(tm_alo + lane_off, lo);
+            for (int q = 0; q < 3; ++q) x2::split_bf16(in[2 * q], in[2 * q + 1], a[q], a[4 + q]);
+            a[3] = 0x3F80u;  // (1, 0): the bias feature
+            a[7] = 0u;
+            tc::tmem_st8(tm_ahi + lane_off, a);
         }
         tc::wait_st();
         tc::fence_before_sync();
         if (arrive_last(&arrivals[g], lane) && lane == 0) {
             tc::fence_after_sync();
-            const uint64_t bh = tc::sdesc_kmajor_noswizzle(w1hi_a, 128, 256);
-            const uint64_t bl = tc::sdesc_kmajor_noswizzle(w1lo_a, 128, 256);
-            tc::mma_ts(tm_d, tm_ahi, bh, kIdesc, 0u);
-            tc::mma_ts(tm_d, tm_ahi, bl, kIdesc, 1u);
-            tc::mma_ts(tm_d, tm_alo, bh, kIdesc, 1u);
+            tc::mma_ts(tm_d, tm_ahi, tc::sdesc_kmajor_noswizzle(w1hi_a, 128, 256), kIdesc, 0u);
+            tc::mma_ts(tm_d, tm_ahi, tc::sdesc_kmajor_noswizzle(w1lo_a, 128, 256), kIdesc, 1u);
             tc::mma_commit(&bars[g]);
         }
         // ---- overlaps the layer-1 MMA: the next tile's features and probe
@@ -565,24 +592,43 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int q = 0; q < 8; ++q)
                 x2::relu_split_bf16(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]), hi[q], lo[q]);
+#if RXGS_A2_SMEM
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {  // K 16ch + 8hh .. +7: one 16-byte core-matrix row per plane
+                const uint32_t off = canon_off(arow, 16 * ch + 8 * hh);
+                *reinterpret_cast<uint4*>(a2hi + off) = make_uint4(hi[4 * hh], hi[4 * hh + 1], hi[4 * hh + 2], hi[4 * hh + 3]);
+                *reinterpret_cast<uint4*>(a2lo + off) = make_uint4(lo[4 * hh], lo[4 * hh + 1], lo[4 * hh + 2], lo[4 * hh + 3]);
+            }
+#else
             tc::tmem_st8(tm_ahi + lane_off + 8 * ch, hi);
             tc::tmem_st8(tm_alo + lane_off + 8 * ch, lo);
+#endif
         }
+#if RXGS_A2_SMEM
+        tc::fence_proxy_async_smem();  // generic-proxy stores -> the MMA's async-proxy reads
+#else
         tc::wait_st();
+#endif
         tc::fence_before_sync();
         // ---- layer 2 on the tensor cores: D = 1 b2 + Ahi Bhi + Ahi Blo + Alo Bhi
         if (arrive_last(&arrivals[g], lane) && lane == 0) {
             tc::fence_after_sync();
-            const uint64_t ad = tc::sdesc_kmajor_noswizzle(aone_a, 128, 256);
-            tc::mma_ss(tm_d, ad, tc::sdesc_kmajor_noswizzle(b2hi_a, 128, 256), kIdesc, 0u);
-            tc::mma_ss(tm_d, ad, tc::sdesc_kmajor_noswizzle(b2lo_a, 128, 256), kIdesc, 1u);
+            // 1 b2hi + 1 b2lo in one K=16 MMA
+            tc::mma_ss(tm_d, tc::sdesc_kmajor_noswizzle(aone_a, 128, 256), tc::sdesc_kmajor_noswizzle(b2hi_a, 128, 256),
+                       kIdesc, 0u);
 #pragma unroll
             for (int s = 0; s < 4; ++s) {
                 const uint64_t bh = tc::sdesc_kmajor_noswizzle(w2hi_a + 256 * s, 128, 1024);
                 const uint64_t bl = tc::sdesc_kmajor_noswizzle(w2lo_a + 256 * s, 128, 1024);
+#if RXGS_A2_SMEM
+                const uint64_t ah = tc::sdesc_kmajor_noswizzle(a2hi_a + 256 * s, 128, 1024);
+                const uint64_t al = tc::sdesc_kmajor_noswizzle(a2lo_a + 256 * s, 128, 1024);
+                tc::mma_ss(tm_d, ah, bh, kIdesc, 1u);
+                tc::mma_ss(tm_d, ah, bl, kIdesc, 1u);
+                tc::mma_ss(tm_d, al, bh, kIdesc, 1u);
+#else
                 tc::mma_ts(tm_d, tm_ahi + 8 * s, bh, kIdesc, 1u);
                 tc::mma_ts(tm_d, tm_ahi + 8 * s, bl, kIdesc, 1u);
-#ifndef RXGS_AB_L2_NOLO
                 tc::mma_ts(tm_d, tm_alo + 8 * s, bh, kIdesc, 1u);
 #endif
             }
@@ -734,7 +780,7 @@ __global__ void __launch_bounds__(128) k_tc_selftest(float* __restrict__ err, in
 
 bool cond_tc_eligible(const rxgs_cond_s* c) {
     return c && c->use_local() && c->hidden == kH && c->C == 1 && !c->nearest &&
-           kFixedSmem + padded_dim(c->R) * padded_dim(c->R) * padded_dim(c->R) * 4 <= 227 * 1024;
+           (RXGS_PROBE_CUBE || kFixedSmem + padded_dim(c->R) * padded_dim(c->R) * padded_dim(c->R) * 4 <= 227 * 1024);
 }
 
 namespace {
@@ -756,7 +802,8 @@ cudaError_t launch_tc(const rxgs_cond_s& cs, const int* n_rows_dev, long long ro
         w.blo[a] = d.lo[a] * w.icell[a] + 0.5f;
     }
     const size_t P = static_cast<size_t>(padded_dim(d.R));
-    const size_t smem = kFixedSmem + (d.probe && !RXGS_PROBE_CUBE ? P * P * P * sizeof(float) : 0);
+    const size_t smem = kFixedSmem + (RXGS_A2_SMEM ? static_cast<size_t>(kGroups) * 2 * kA2Bytes : 0) +
+                        (d.probe && !RXGS_PROBE_CUBE ? P * P * P * sizeof(float) : 0);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
