@@ -1186,9 +1186,29 @@ int rxgs_render_queries(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, rxgs_txstate s
     // overlap the conditioning of chunk i+1
     const size_t per_rx = std::max<size_t>(static_cast<size_t>(sc->k), 1) * sizeof(float2);
     int chunk = static_cast<int>(std::min<size_t>(static_cast<size_t>(n_rx), (size_t{4} << 30) / per_rx));
+    // host spectra: four shrinking receiver chunks (3/8, 5/16, 3/16, 1/8 of
+    // the batch, multiples of 32): the D2H of each overlaps the next chunk's
+    // compute and only the smallest, last one is exposed
     const bool pipelined = out_spectrum && d_spec != out_spectrum && n_rx >= 256;
-    if (pipelined) chunk = std::min(chunk, ((n_rx + 4 * 32 - 1) / (4 * 32)) * 32);
+    std::vector<int> bounds{0};
+    if (pipelined) {
+        const double frac[4] = {3.0 / 8, 3.0 / 8 + 5.0 / 16, 7.0 / 8, 1.0};
+        for (double f : frac) {
+            int b = static_cast<int>(std::lround(f * n_rx / 32.0)) * 32;
+            b = std::min(std::max(b, bounds.back() + 1), n_rx);
+            if (f == 1.0) b = n_rx;
+            if (b > bounds.back()) bounds.push_back(b);
+        }
+        int widest = 0;
+        for (size_t i = 1; i < bounds.size(); ++i) widest = std::max(widest, bounds[i] - bounds[i - 1]);
+        chunk = std::min(chunk, widest);
+    }
     chunk = std::max(chunk, 1);
+    if (!pipelined || bounds.back() != n_rx || chunk < (bounds.size() > 1 ? bounds[1] : 0)) {
+        bounds.assign(1, 0);  // uniform chunks
+        for (int b = chunk; b < n_rx; b += chunk) bounds.push_back(b);
+        bounds.push_back(n_rx);
+    }
     if (pipelined && !ctx->copy_stream) RXGS_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
     int n_chunk_ev = 0;
     RXGS_CUDA(ctx->signals.ensure(per_rx * chunk));
@@ -1196,8 +1216,8 @@ int rxgs_render_queries(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, rxgs_txstate s
     // the tcgen05 compositor reads the signals pre-split into bf16 hi/lo
     const bool tc_comp = ctx->composite_kernel != 1 && composite_tc_eligible(*st);
     const SigOut so = tc_comp ? SigOut::presplit(ctx->signals.p) : SigOut(ctx->signals.as<float2>());
-    for (int j0 = 0; j0 < n_rx; j0 += chunk) {
-        const int nj = std::min(chunk, n_rx - j0);
+    for (size_t ci = 0; ci + 1 < bounds.size(); ++ci) {
+        const int j0 = bounds[ci], nj = bounds[ci + 1] - bounds[ci];
         RX_TRY(compute_signals(ctx, sc, c, st, d_rx + 3 * static_cast<size_t>(j0), nj, so));
         CompositeOut co;
         co.spectrum = d_spec ? d_spec + static_cast<size_t>(j0) * plane : nullptr;
