@@ -1,0 +1,37 @@
+"""Turn the gpurun_out/ captures of scripts/gpu_profiles.sh into profiles/
+summaries (committed) and profiles/<tag>_traffic.json (read by bench.py)."""
+import csv, json, os, subprocess, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, "scripts"))
+import ncu_summary as S
+
+tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
+out = os.path.join(ROOT, "gpurun_out")
+prof = os.path.join(ROOT, "profiles")
+lc = os.path.join(out, f"{tag}_launches.csv")
+if os.path.exists(lc):
+    open(os.path.join(prof, f"{tag}_launches.txt"), "w").write(S.launches(lc) + "\n")
+traffic = {"source": "ncu --set full --clock-control none, one launch each; bench.py config 2 (K=100k, 1024 rx, 90x360); "
+                     "k_cov_signal from the config-3 leg (K=500k)"}
+for k in ["k_cond_tc", "k_composite_tc", "k_walk", "k_tx_prep", "k_cov_signal"]:
+    rep = os.path.join(out, f"{tag}_{k}.ncu-rep")
+    if not os.path.exists(rep):
+        continue
+    open(os.path.join(prof, f"{tag}_{k}.txt"), "w").write(S.report(rep) + "\n")
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    h, u, v = rows[0], rows[1], rows[2]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1.0, "usecond": 1.0,
+             "ms": 1e3, "msecond": 1e3, "nsecond": 1e-3}
+
+    def get(m):  # value in base units (bytes, microseconds)
+        if m not in h:
+            return None
+        i = h.index(m)
+        return float(v[i].replace(",", "")) * scale.get(u[i], 1.0)
+
+    rd, wr = get("dram__bytes_read.sum"), get("dram__bytes_write.sum")
+    traffic[k] = {"dram_bytes_per_launch": (rd + wr) if rd is not None else None,
+                  "duration_us": get("gpu__time_duration.sum")}
+json.dump(traffic, open(os.path.join(prof, f"{tag}_traffic.json"), "w"), indent=1)
+print(json.dumps(traffic, indent=1))
