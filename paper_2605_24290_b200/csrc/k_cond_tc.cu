@@ -42,6 +42,10 @@
 #ifndef RXGS_MBAR_WAIT
 #define RXGS_MBAR_WAIT tc::mbar_wait_sleep
 #endif
+// double-buffered TMEM readback of the 64 accumulator columns
+#ifndef RXGS_LD_DB
+#define RXGS_LD_DB 0
+#endif
 
 namespace rxgs_b200 {
 namespace {
@@ -582,27 +586,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         RXGS_MBAR_WAIT(&bars[g], phase);
         phase ^= 1u;
         tc::fence_after_sync();
-        // ---- ReLU(h1) -> bf16 hi/lo -> TMEM (layer-2 A operand; overwrites A1)
+        // ---- ReLU(h1) -> bf16 hi/lo -> TMEM (layer-2 A operand; overwrites A1).
+        // TMEM reads double-buffered: chunk ch+1 is in flight while ch is split.
+        {
+            uint32_t vb[2][16];
+            tc::tmem_ld16(tm_d + lane_off, vb[0]);
+            tc::wait_ld_regs(vb[0]);
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-            uint32_t v[16];
-            tc::tmem_ld16(tm_d + lane_off + 16 * ch, v);
-            tc::wait_ld();
-            uint32_t hi[8], lo[8];
+            for (int ch = 0; ch < 4; ++ch) {
+                uint32_t(&v)[16] = vb[ch & 1];
+                if (RXGS_LD_DB && ch + 1 < 4) tc::tmem_ld16(tm_d + lane_off + 16 * (ch + 1), vb[(ch + 1) & 1]);
+                uint32_t hi[8], lo[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-                x2::relu_split_bf16(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]), hi[q], lo[q]);
+                for (int q = 0; q < 8; ++q)
+                    x2::relu_split_bf16(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]), hi[q], lo[q]);
 #if RXGS_A2_SMEM
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {  // K 16ch + 8hh .. +7: one 16-byte core-matrix row per plane
-                const uint32_t off = canon_off(arow, 16 * ch + 8 * hh);
-                *reinterpret_cast<uint4*>(a2hi + off) = make_uint4(hi[4 * hh], hi[4 * hh + 1], hi[4 * hh + 2], hi[4 * hh + 3]);
-                *reinterpret_cast<uint4*>(a2lo + off) = make_uint4(lo[4 * hh], lo[4 * hh + 1], lo[4 * hh + 2], lo[4 * hh + 3]);
-            }
+                for (int hh = 0; hh < 2; ++hh) {  // K 16ch + 8hh .. +7: one 16-byte core-matrix row per plane
+                    const uint32_t off = canon_off(arow, 16 * ch + 8 * hh);
+                    *reinterpret_cast<uint4*>(a2hi + off) = make_uint4(hi[4 * hh], hi[4 * hh + 1], hi[4 * hh + 2], hi[4 * hh + 3]);
+                    *reinterpret_cast<uint4*>(a2lo + off) = make_uint4(lo[4 * hh], lo[4 * hh + 1], lo[4 * hh + 2], lo[4 * hh + 3]);
+                }
 #else
-            tc::tmem_st8(tm_ahi + lane_off + 8 * ch, hi);
-            tc::tmem_st8(tm_alo + lane_off + 8 * ch, lo);
+                tc::tmem_st8(tm_ahi + lane_off + 8 * ch, hi);
+                tc::tmem_st8(tm_alo + lane_off + 8 * ch, lo);
 #endif
+                if (ch + 1 < 4) {
+                    if (!RXGS_LD_DB) tc::tmem_ld16(tm_d + lane_off + 16 * (ch + 1), vb[(ch + 1) & 1]);
+                    tc::wait_ld_regs(vb[(ch + 1) & 1]);
+                }
+            }
         }
 #if RXGS_A2_SMEM
         tc::fence_proxy_async_smem();  // generic-proxy stores -> the MMA's async-proxy reads
@@ -645,11 +658,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---- ReLU(h2), layer 3 on FFMA2 from the TMEM accumulator
         float2 ya = make_float2(W.b3[0], W.b3[1]), yb = make_float2(W.b3[2], W.b3[3]);
         float2 ya1 = make_float2(0.f, 0.f), yb1 = make_float2(0.f, 0.f);  // odd columns (FFMA2 latency)
+        {
+            uint32_t vb[2][16];
+            tc::tmem_ld16(tm_d + lane_off, vb[0]);
+            tc::wait_ld_regs(vb[0]);
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-            uint32_t v[16];
-            tc::tmem_ld16(tm_d + lane_off + 16 * ch, v);
-            tc::wait_ld();
+            for (int ch = 0; ch < 4; ++ch) {
+                uint32_t(&v)[16] = vb[ch & 1];
+                if (RXGS_LD_DB && ch + 1 < 4) tc::tmem_ld16(tm_d + lane_off + 16 * (ch + 1), vb[(ch + 1) & 1]);
 #pragma unroll
             for (int q = 0; q < 16; q += 2) {
                 const float4 w3 = W.w3[16 * ch + q], w3b = W.w3[16 * ch + q + 1];
@@ -659,6 +675,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 yb = x2::fma(h2, make_float2(w3.z, w3.w), yb);
                 ya1 = x2::fma(h2b, make_float2(w3b.x, w3b.y), ya1);
                 yb1 = x2::fma(h2b, make_float2(w3b.z, w3b.w), yb1);
+            }
+                if (ch + 1 < 4) {
+                    if (!RXGS_LD_DB) tc::tmem_ld16(tm_d + lane_off + 16 * (ch + 1), vb[(ch + 1) & 1]);
+                    tc::wait_ld_regs(vb[(ch + 1) & 1]);
+                }
             }
         }
         ya = x2::add(ya, ya1);
