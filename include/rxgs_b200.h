@@ -33,6 +33,7 @@ extern "C" {
 #define RXGS_ERR_INVALID 1 /* reference: std::invalid_argument */
 #define RXGS_ERR_RUNTIME 2 /* reference: std::runtime_error    */
 #define RXGS_ERR_CUDA 3    /* device / driver failure          */
+#define RXGS_ERR_IO 4      /* reference: io::IoError (dataset.hpp:16) */
 
 typedef struct rxgs_ctx_s* rxgs_ctx;
 typedef struct rxgs_scene_s* rxgs_scene;
@@ -165,6 +166,29 @@ int rxgs_backward_render(rxgs_ctx ctx, rxgs_txstate st, rxgs_scene scene, const 
                          int n_rx, const double* d_values, double* d_positions,
                          double* d_log_scales, double* d_quaternions, double* d_tau_logits,
                          double* d_coeffs);
+
+/* ------------------------------------------------------------ scene / model load
+ * io::save_checkpoint / io::load_checkpoint (checkpoint.hpp:17-18,
+ * checkpoint.cpp:93-231): the RXGS container ("RXGS", u32 version 1, u64
+ * header length, JSON header with a named f64 array manifest, the arrays).
+ * save: the scene (device coefficients synced first), the grid and, when
+ * cond is non-NULL, the conditioning state incl. its occupancy grid.
+ * load: creates the scene on ctx, fills *grid, and creates *cond when the
+ * file has a conditioning state (cond may be NULL to skip it).  Errors
+ * carry the reference's IoError text (RXGS_ERR_IO). */
+int rxgs_checkpoint_save(const char* path, rxgs_scene scene, const rxgs_grid* grid, rxgs_cond cond);
+int rxgs_checkpoint_load(rxgs_ctx ctx, const char* path, rxgs_scene* scene, rxgs_grid* grid, rxgs_cond* cond);
+/* Shape of a scene (GaussianScene::count / l_max / channels / modality) and
+ * the configuration of a conditioning state (rxgs_cond_create's cfg). */
+int rxgs_scene_info(rxgs_scene scene, int32_t* k, int32_t* l_max, int32_t* channels, int32_t* modality);
+int rxgs_cond_config(rxgs_cond cond, int32_t cfg[9]);
+/* Host copies of a scene's per-Gaussian arrays (any pointer may be NULL;
+ * coefficients are the device's current values). */
+int rxgs_scene_get_arrays(rxgs_scene scene, double* positions, double* log_scales, double* quaternions,
+                          double* tau_logits, double* fle_coeffs);
+/* A conditioning state's occupancy grid: *has = 0 for an empty grid;
+ * densities (R^3, may be NULL) and bounds (may be NULL) otherwise. */
+int rxgs_cond_get_occupancy(rxgs_cond cond, int32_t* has, double* densities, double lo[3], double hi[3]);
 
 /* ------------------------------------------------------------ conditioning
  * cond::ConditioningState (conditioning.hpp:72-92).  cfg = {F, hidden, d_c,

@@ -389,6 +389,102 @@ inline raster::Measurement predict(const Model& model, const Vec3& tx, const Vec
 
 }  // namespace train
 
+namespace io {  // checkpoint.hpp / dataset.hpp
+
+struct IoError : std::runtime_error {  // dataset.hpp:16
+    using std::runtime_error::runtime_error;
+};
+
+namespace detail_io {
+inline void check(int rc) {
+    if (rc == RXGS_ERR_IO) throw IoError(rxgs_last_error());
+    api::detail::check(rc);
+}
+}  // namespace detail_io
+
+// checkpoint.cpp:93-155: the RXGS container, written by the B200 library
+inline void save_checkpoint(const std::string& path, const train::Model& model) {
+    auto sh = api::detail::upload(model.scene);
+    std::unique_ptr<cond::detail_c::CondHandle> ch;
+    if (model.has_conditioning) ch = cond::detail_c::upload(model.conditioning);
+    const rxgs_grid g = model.grid.c();
+    detail_io::check(rxgs_checkpoint_save(path.c_str(), sh->h, &g, ch ? ch->h : nullptr));
+}
+
+// checkpoint.cpp:157-231: read by the library, materialised as host structs
+inline train::Model load_checkpoint(const std::string& path) {
+    auto sh = std::make_shared<api::detail::SceneHandle>();
+    rxgs_grid g{};
+    rxgs_cond c = nullptr;
+    detail_io::check(rxgs_checkpoint_load(api::detail::ctx(), path.c_str(), &sh->h, &g, &c));
+    cond::detail_c::CondHandle ch;
+    ch.h = c;
+    train::Model m;
+    int32_t k = 0, l_max = 0, channels = 1, modality = 0;
+    api::detail::check(rxgs_scene_info(sh->h, &k, &l_max, &channels, &modality));
+    GaussianScene& s = m.scene;
+    s.l_max = l_max;
+    s.channels = channels;
+    s.modality = static_cast<Modality>(modality);
+    s.positions.resize(3 * static_cast<std::size_t>(k));
+    s.log_scales.resize(3 * static_cast<std::size_t>(k));
+    s.quaternions.resize(4 * static_cast<std::size_t>(k));
+    s.tau_logits.resize(k);
+    s.fle_coeffs.resize(static_cast<std::size_t>(k) * s.coeff_stride());
+    api::detail::check(rxgs_scene_get_arrays(sh->h, s.positions.data(), s.log_scales.data(), s.quaternions.data(),
+                                             s.tau_logits.data(), s.fle_coeffs.data()));
+    m.grid.n_theta = g.n_theta;
+    m.grid.n_phi = g.n_phi;
+    m.grid.tile_size = g.tile_size;
+    m.grid.radius = g.radius;
+    m.grid.theta_min = g.theta_min;
+    m.grid.theta_max = g.theta_max;
+    m.has_conditioning = c != nullptr;
+    if (c) {
+        int32_t cfg[9];
+        api::detail::check(rxgs_cond_config(c, cfg));
+        cond::ConditioningState& st = m.conditioning;
+        st.config = {cfg[0], cfg[1], cfg[2], cfg[3], cfg[4], cfg[5] != 0, static_cast<cond::ConditioningMode>(cfg[6])};
+        st.l_max = cfg[7];
+        st.channels = cfg[8];
+        std::vector<double> p(static_cast<std::size_t>(rxgs_cond_param_count(c)));
+        api::detail::check(rxgs_cond_get_params(c, p.data()));
+        std::size_t o = 0;
+        auto take = [&](std::vector<double>& v, std::size_t n) {
+            v.assign(p.begin() + static_cast<std::ptrdiff_t>(o), p.begin() + static_cast<std::ptrdiff_t>(o + n));
+            o += n;
+        };
+        const std::size_t F = cfg[0], d = cfg[1], dc = cfg[2], C4 = 4 * static_cast<std::size_t>(cfg[8]);
+        const std::size_t L = static_cast<std::size_t>(component_count(cfg[7]));
+        auto mlp = [&](cond::Mlp& net, int in) {
+            net.l1 = {in, static_cast<int>(d), {}, {}};
+            net.l2 = {static_cast<int>(d), static_cast<int>(d), {}, {}};
+            net.l3 = {static_cast<int>(d), static_cast<int>(C4), {}, {}};
+            take(net.l1.w, d * in);
+            take(net.l1.b, d);
+            take(net.l2.w, d * d);
+            take(net.l2.b, d);
+            take(net.l3.w, C4 * d);
+            take(net.l3.b, C4);
+        };
+        take(st.fourier_freqs, 3 * F);
+        mlp(st.global_mlp, static_cast<int>(6 * F + 2 + dc));
+        take(st.component_embed, L * dc);
+        mlp(st.local_mlp, 6);
+        int32_t has = 0;
+        double lo[3], hi[3];
+        const std::size_t R = cfg[4];
+        std::vector<double> dens(R * R * R);
+        api::detail::check(rxgs_cond_get_occupancy(c, &has, dens.data(), lo, hi));
+        st.occupancy.resolution = cfg[4];
+        st.occupancy.bounds = {{lo[0], lo[1], lo[2]}, {hi[0], hi[1], hi[2]}};
+        if (has) st.occupancy.densities = std::move(dens);
+    }
+    return m;
+}
+
+}  // namespace io
+
 }  // namespace api
 }  // namespace rxgs_b200
 

@@ -17,7 +17,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("RXGS_B200_LIB") or os.path.join(HERE, "librxgs_b200.so")  # override: A/B builds
 
-RXGS_OK, RXGS_ERR_INVALID, RXGS_ERR_RUNTIME, RXGS_ERR_CUDA = 0, 1, 2, 3
+RXGS_OK, RXGS_ERR_INVALID, RXGS_ERR_RUNTIME, RXGS_ERR_CUDA, RXGS_ERR_IO = 0, 1, 2, 3, 4
 MODALITY = {"rssi": 0, "csi": 1, "spectrum": 2}
 MODE = {"full": 0, "global_only": 1, "local_only": 2, "additive_only": 3, "no_occlusion": 4}
 
@@ -116,6 +116,10 @@ _SIG = {
     "rxgs_train_apply": (C.c_int, [_vp]),
     "rxgs_train_step_count": (_i64, [_vp]),
     "rxgs_scene_get_coeffs": (C.c_int, [_vp, _vp]),
+    "rxgs_checkpoint_save": (C.c_int, [C.c_char_p, _vp, C.POINTER(Grid), _vp]),
+    "rxgs_checkpoint_load": (C.c_int, [_vp, C.c_char_p, C.POINTER(_vp), C.POINTER(Grid), C.POINTER(_vp)]),
+    "rxgs_scene_info": (C.c_int, [_vp, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32)]),
+    "rxgs_cond_config": (C.c_int, [_vp, _vp]),
     "rxgs_cond_get_params": (C.c_int, [_vp, _vp]),
 }
 for _name, (_res, _args) in _SIG.items():
@@ -136,11 +140,17 @@ class InvalidArgument(RxgsError, ValueError):
     """The reference's std::invalid_argument."""
 
 
+class IoError(RxgsError, OSError):
+    """The reference's io::IoError (dataset.hpp:16)."""
+
+
 def _check(rc):
     if rc != RXGS_OK:
         msg = _lib.rxgs_last_error().decode()
         if rc == RXGS_ERR_INVALID:
             raise InvalidArgument(rc, msg)
+        if rc == RXGS_ERR_IO:
+            raise IoError(rc, msg)
         raise RxgsError(rc, msg)
 
 
@@ -258,6 +268,14 @@ class Context:
     def cond(self, cfg, params, occ=None, lo=None, hi=None):
         return Cond(self, cfg, params, occ, lo, hi)
 
+    def load_checkpoint(self, path):
+        """io::load_checkpoint (checkpoint.cpp:157-231) -> (Scene, Grid, Cond or None)."""
+        hs, hc, grid = _vp(), _vp(), Grid()
+        _check(_lib.rxgs_checkpoint_load(self.h, os.fsencode(str(path)), C.byref(hs), C.byref(grid), C.byref(hc)))
+        scene = Scene._wrap(self, hs)
+        cond = Cond._wrap(self, hc) if hc.value else None
+        return scene, grid, cond
+
     def bin_and_sort(self, culled, depth, spans, grid: Grid):
         k = len(culled)
         offs = np.empty(grid.n_tiles + 1, np.int64)
@@ -310,6 +328,22 @@ class Scene:
                                       ptr(sc["quaternions"], np.float64), ptr(sc["tau_logits"], np.float64),
                                       ptr(sc["fle_coeffs"], np.float64), C.byref(h)))
         self.h = h
+
+    @classmethod
+    def _wrap(cls, ctx: Context, h):
+        """A Scene around a handle created by the library (checkpoint load)."""
+        self = cls.__new__(cls)
+        self.ctx, self.h, self.data = ctx, h, None
+        k, l, c, m = _i32(), _i32(), _i32(), _i32()
+        _check(_lib.rxgs_scene_info(h, C.byref(k), C.byref(l), C.byref(c), C.byref(m)))
+        self.k, self.l_max, self.channels = k.value, l.value, c.value
+        self.L = (self.l_max + 1) ** 2
+        self.modality = {v: n for n, v in MODALITY.items()}[m.value]
+        return self
+
+    def save_checkpoint(self, path, grid: Grid, cond=None):
+        """io::save_checkpoint (checkpoint.cpp:93-155)."""
+        _check(_lib.rxgs_checkpoint_save(os.fsencode(str(path)), self.h, C.byref(grid), cond.h if cond else None))
 
     def __del__(self, _fn=_lib.rxgs_scene_destroy):
         if getattr(self, "h", None):
@@ -437,6 +471,14 @@ class Cond:
                                      ptr(lo, np.float64) if lo is not None else None,
                                      ptr(hi, np.float64) if hi is not None else None, C.byref(h)))
         self.h = h
+
+    @classmethod
+    def _wrap(cls, ctx: Context, h):
+        self = cls.__new__(cls)
+        self.ctx, self.h = ctx, h
+        self.cfg = np.zeros(9, np.int32)
+        _check(_lib.rxgs_cond_config(h, self.cfg.ctypes.data))
+        return self
 
     def __del__(self, _fn=_lib.rxgs_cond_destroy):
         if getattr(self, "h", None):

@@ -966,6 +966,7 @@ int rxgs_cond_create(rxgs_ctx ctx, const int32_t cfg[9], const double* params, c
     if (occ) {
         const size_t n = static_cast<size_t>(c->R) * c->R * c->R;
         std::vector<double> h = to_host(occ, n);
+        c->h_occ = h;
         std::vector<float> f(h.begin(), h.end());
         e = c->d_occ32.ensure(n * sizeof(float));
         if (e != cudaSuccess) return bad(e, "occ");
@@ -1018,6 +1019,10 @@ int rxgs_build_occupancy(rxgs_ctx ctx, rxgs_scene sc, int R, const double lo_[3]
     const size_t n = static_cast<size_t>(R) * R * R;
     double* d64 = nullptr;
     RX_TRY(dev_out(out, n, ctx->host_out, &d64));
+    if (!d64 && attach) {  // the attached state keeps a host f64 copy (checkpoint save)
+        RXGS_CUDA(ctx->host_out.ensure(n * sizeof(double)));
+        d64 = ctx->host_out.as<double>();
+    }
     float* d32 = nullptr;
     if (attach) {
         RXGS_CUDA(attach->d_occ32.ensure(n * sizeof(float)));
@@ -1036,6 +1041,8 @@ int rxgs_build_occupancy(rxgs_ctx ctx, rxgs_scene sc, int R, const double lo_[3]
         }
         attach->has_occ = true;
         RXGS_CUDA(launch_occ_cubes(*attach, ctx->stream));
+        attach->h_occ.resize(n);
+        RXGS_CUDA(cudaMemcpyAsync(attach->h_occ.data(), d64, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     }
     RX_TRY(finish_out(ctx, out, d64, n));
     RXGS_CUDA(cudaStreamSynchronize(ctx->stream));

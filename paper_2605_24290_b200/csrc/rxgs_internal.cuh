@@ -171,6 +171,7 @@ struct rxgs_cond_s {
         o_lw3, o_lb3;
     std::vector<double> h_params;
     bool has_occ = false;
+    std::vector<double> h_occ;  // host f64 copy of the occupancy densities (checkpoint save)
     double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     int64_t global_calls = 0, local_calls = 0;
     rxgs_b200::DevBuf d_params32, d_params64, d_occ32;

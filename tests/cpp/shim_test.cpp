@@ -157,6 +157,28 @@ int main() {
             threw = std::string(e.what()).find("gaussian 1") != std::string::npos;
         }
         CHECK(threw);
+        // io::save_checkpoint / load_checkpoint round trip (checkpoint.cpp:93-231)
+        train::Model m;
+        m.scene = scene;
+        m.grid = small_grid();
+        m.has_conditioning = true;
+        m.conditioning = st;
+        const std::string path = "/tmp/rxgs_shim_ckpt.rxgs";
+        io::save_checkpoint(path, m);
+        const train::Model back = io::load_checkpoint(path);
+        CHECK(back.scene.positions == m.scene.positions && back.scene.fle_coeffs == m.scene.fle_coeffs);
+        CHECK(back.scene.tau_logits == m.scene.tau_logits && back.scene.l_max == 1 && back.scene.channels == 2);
+        CHECK(back.grid.n_theta == m.grid.n_theta && back.grid.theta_max == m.grid.theta_max);
+        CHECK(back.has_conditioning && back.conditioning.local_mlp.l2.w == st.local_mlp.l2.w);
+        CHECK(back.conditioning.occupancy.densities == st.occupancy.densities);
+        CHECK(back.conditioning.occupancy.bounds.hi.z == 4.0 && back.conditioning.config.hidden == 8);
+        bool io_threw = false;
+        try {
+            io::load_checkpoint("/tmp/rxgs_shim_no_such_file.rxgs");
+        } catch (const io::IoError& e) {
+            io_threw = std::string(e.what()).find("load_checkpoint: cannot open") != std::string::npos;
+        }
+        CHECK(io_threw);
     }
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail ? 1 : 0;
