@@ -353,27 +353,34 @@ def bench_train(args, capi, ctx, scene, cond, grid, stream, dev, rank, world):
     targets = torch.from_numpy(rng.uniform(0.0, 2.0, (B, grid.cells)).astype(np.float32)).to(dev)
     rx_d = torch.from_numpy(rx).to(dev)
     st = scene.tx_state(np.array(TX), grid)
-    tr = capi.Trainer(ctx, scene, cond)
-    gbuf = tr.grad_tensor()
 
-    def step():
-        tr.grads(st, rx_d, targets)
-        allreduce_grads(gbuf)  # NCCL over NVLink (no-op at world 1)
-        tr.apply()
+    def time_trainer(hyper):
+        tr = capi.Trainer(ctx, scene, cond, hyper)
+        gbuf = tr.grad_tensor()
 
-    for _ in range(2):
-        step()
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    n_steps = max(3, min(args.steps, 10))
-    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s0.record(stream)
-    for _ in range(n_steps):
-        step()
-    s1.record(stream)
-    torch.cuda.synchronize(dev)
-    ms = max_over_ranks(s0.elapsed_time(s1) / n_steps, dev)
+        def step():
+            tr.grads(st, rx_d, targets)
+            allreduce_grads(gbuf)  # NCCL over NVLink (no-op at world 1)
+            tr.apply()
+
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        n_steps = max(3, min(args.steps, 10))
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(n_steps):
+            step()
+        s1.record(stream)
+        torch.cuda.synchronize(dev)
+        return max_over_ranks(s0.elapsed_time(s1) / n_steps, dev), tr.n
+
+    ms, n_grad = time_trainer(None)  # spectrum L1 (lambda_ssim = lambda_fft = 0)
+    hp = list(capi.Trainer.DEFAULTS)
+    hp[3], hp[4] = 0.2, 0.1  # the reference's default LossWeights (trainer.hpp:25-29)
+    ms_full, _ = time_trainer(hp)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:  # reference CPU training sample (oracle/_ref), one sample, all host threads in render/backward
@@ -398,9 +405,11 @@ def bench_train(args, capi, ctx, scene, cond, grid, stream, dev, rank, world):
             cpu = {"error": str(ex)}
     return {"workload": f"config4: K={args.gaussians} Stage-II step, {B} (tx, rx) samples per GPU, spectrum L1, "
                         f"conditioning + compositing forward/backward, Adam; f64 gradient all-reduce "
-                        f"({'NCCL' if world > 1 else 'none at 1 GPU'}) of {tr.n} values",
+                        f"({'NCCL' if world > 1 else 'none at 1 GPU'}) of {n_grad} values",
             "ms_per_step": ms, "steps_per_s": 1e3 / ms, "samples_per_s": world * B * 1e3 / ms,
-            "grad_floats": tr.n, "n_gpus": world, "cpu_reference": cpu}
+            "default_loss": {"lambda_ssim": 0.2, "lambda_fft": 0.1, "ms_per_step": ms_full,
+                             "samples_per_s": world * B * 1e3 / ms_full},
+            "grad_floats": n_grad, "n_gpus": world, "cpu_reference": cpu}
 
 
 def _cond_for(capi, ctx, scene, lib=None):

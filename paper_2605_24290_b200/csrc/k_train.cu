@@ -91,6 +91,196 @@ __global__ void k_loss_finalize(int n_rx, int nb, const double* __restrict__ par
     loss[j] = s;
 }
 
+// ------------------------------------------------------------------ full spectrum loss
+// composite_loss (trainer.cpp:80-145) with SSIM and DFT terms, FP64 from the
+// f32 field:
+//   L = l_w * mean|x - y| + lambda_ssim (1 - SSIM(x, y)) + lambda_fft sum|F x - F y|^2
+// x = amplitude sqrt(re^2 + im^2 + 1e-8), y = target.  The orthonormal,
+// zero-padded 2-D DFT is unitary, so sum|F x - F y|^2 = sum (x - y)^2
+// (Parseval) and its adjoint is 2 (x - y) -- the collapse the reference uses
+// for the gradient (trainer.cpp:131-138); the value is taken the same way.
+// SSIM (metrics.cpp:55-112): 11x11 Gaussian window (sigma 1.5), mean over
+// every fully contained window; the 2-D window is the outer product of the
+// normalised 1-D window, so both the window statistics and the adjoint
+//   d SSIM / d x_p = 1/n sum_{windows w containing p} k(p - w) (A_w + B_w y_p + G_w x_p),
+//   A = 2 my (a2 - a1)/(b1 b2) - 2 s mx (1/b1 - 1/b2), B = 2 a1/(b1 b2), G = -2 s/b2
+// (the reference's ds expanded per window) are separable passes.
+constexpr int kSsimWin = 11;
+__constant__ double c_ssim_g[kSsimWin];  // normalised 1-D Gaussian window
+
+__global__ void k_loss_amp(int n_rx, int P, const float* __restrict__ field, const float* __restrict__ target,
+                           double* __restrict__ amp, double* __restrict__ part) {
+    __shared__ double red[2][256];
+    const int j = blockIdx.y;
+    const float* re_p = field + static_cast<size_t>(j) * 2 * P;
+    const float* im_p = re_p + P;
+    double l1 = 0.0, sq = 0.0;
+    for (int cell = blockIdx.x * blockDim.x + threadIdx.x; cell < P; cell += gridDim.x * blockDim.x) {
+        const double re = re_p[cell], im = im_p[cell];
+        const double x = sqrt(re * re + im * im + kAmpEps);
+        const double d = x - static_cast<double>(target[static_cast<size_t>(j) * P + cell]);
+        amp[static_cast<size_t>(j) * P + cell] = x;
+        l1 += fabs(d);
+        sq += d * d;
+    }
+    red[0][threadIdx.x] = l1;
+    red[1][threadIdx.x] = sq;
+    __syncthreads();
+    for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+        if (threadIdx.x < st) {
+            red[0][threadIdx.x] += red[0][threadIdx.x + st];
+            red[1][threadIdx.x] += red[1][threadIdx.x + st];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[(static_cast<size_t>(j) * gridDim.x + blockIdx.x) * 2] = red[0][0];
+        part[(static_cast<size_t>(j) * gridDim.x + blockIdx.x) * 2 + 1] = red[1][0];
+    }
+}
+
+// horizontal window sums of x, y, x^2, y^2, xy: H[j][q][r][c], c < cols
+__global__ void k_ssim_h(int n_rx, int h, int w, const double* __restrict__ amp, const float* __restrict__ target,
+                         double* __restrict__ H) {
+    const int cols = w - kSsimWin + 1;
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = blockIdx.y, j = blockIdx.z;
+    if (c >= cols) return;
+    const double* x = amp + (static_cast<size_t>(j) * h + r) * w + c;
+    const float* y = target + (static_cast<size_t>(j) * h + r) * w + c;
+    double s[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+    for (int t = 0; t < kSsimWin; ++t) {
+        const double g = c_ssim_g[t], xv = x[t], yv = y[t];
+        s[0] += g * xv;
+        s[1] += g * yv;
+        s[2] += g * xv * xv;
+        s[3] += g * yv * yv;
+        s[4] += g * xv * yv;
+    }
+    const size_t plane = static_cast<size_t>(h) * cols;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) H[(static_cast<size_t>(j) * 5 + q) * plane + static_cast<size_t>(r) * cols + c] = s[q];
+}
+
+// per window: statistics -> SSIM s and the adjoint coefficients A, B, G
+__global__ void k_ssim_v(int n_rx, int h, int w, double c1, double c2, const double* __restrict__ H,
+                         double* __restrict__ S, double* __restrict__ coef) {
+    const int cols = w - kSsimWin + 1, rows = h - kSsimWin + 1;
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = blockIdx.y, j = blockIdx.z;
+    if (c >= cols) return;
+    const size_t hplane = static_cast<size_t>(h) * cols;
+    double m[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        const double* hq = H + (static_cast<size_t>(j) * 5 + q) * hplane + static_cast<size_t>(r) * cols + c;
+        double a = 0.0;
+#pragma unroll
+        for (int t = 0; t < kSsimWin; ++t) a += c_ssim_g[t] * hq[static_cast<size_t>(t) * cols];
+        m[q] = a;
+    }
+    const double mx = m[0], my = m[1];
+    const double vx = m[2] - mx * mx, vy = m[3] - my * my, cov = m[4] - mx * my;
+    const double a1 = 2.0 * mx * my + c1, b1 = mx * mx + my * my + c1;
+    const double a2 = 2.0 * cov + c2, b2 = vx + vy + c2;
+    const double sv = (a1 * a2) / (b1 * b2);
+    const size_t wplane = static_cast<size_t>(rows) * cols, wi = static_cast<size_t>(r) * cols + c;
+    S[static_cast<size_t>(j) * wplane + wi] = sv;
+    coef[(static_cast<size_t>(j) * 3 + 0) * wplane + wi] =
+        2.0 * my * (a2 - a1) / (b1 * b2) - 2.0 * sv * mx * (1.0 / b1 - 1.0 / b2);
+    coef[(static_cast<size_t>(j) * 3 + 1) * wplane + wi] = 2.0 * a1 / (b1 * b2);
+    coef[(static_cast<size_t>(j) * 3 + 2) * wplane + wi] = -2.0 * sv / b2;
+}
+
+// fixed-order per-receiver mean of the window SSIMs
+__global__ void k_ssim_mean(int rows, int cols, const double* __restrict__ S, double* __restrict__ ssim) {
+    __shared__ double red[256];
+    const int j = blockIdx.x;
+    const size_t n = static_cast<size_t>(rows) * cols;
+    double a = 0.0;
+    for (size_t i = threadIdx.x; i < n; i += blockDim.x) a += S[static_cast<size_t>(j) * n + i];
+    red[threadIdx.x] = a;
+    __syncthreads();
+    for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+        if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) ssim[j] = red[0] / static_cast<double>(n);
+}
+
+// adjoint, vertical pass: V[j][q][pr][c] = sum_t g_t coef_q[pr - t][c]
+__global__ void k_ssim_bv(int n_rx, int h, int w, const double* __restrict__ coef, double* __restrict__ V) {
+    const int cols = w - kSsimWin + 1, rows = h - kSsimWin + 1;
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int pr = blockIdx.y, j = blockIdx.z;
+    if (c >= cols) return;
+    const size_t wplane = static_cast<size_t>(rows) * cols, vplane = static_cast<size_t>(h) * cols;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const double* cq = coef + (static_cast<size_t>(j) * 3 + q) * wplane;
+        double a = 0.0;
+#pragma unroll
+        for (int t = 0; t < kSsimWin; ++t) {
+            const int r = pr - t;
+            if (r >= 0 && r < rows) a += c_ssim_g[t] * cq[static_cast<size_t>(r) * cols + c];
+        }
+        V[(static_cast<size_t>(j) * 3 + q) * vplane + static_cast<size_t>(pr) * cols + c] = a;
+    }
+}
+
+// adjoint, horizontal pass + the whole d loss / d amplitude + chain to the field:
+// G = dL/dx * (re, im) / x
+__global__ void k_loss_grad(int n_rx, int h, int w, double l_w, double lambda_ssim, double lambda_fft,
+                            const float* __restrict__ field, const float* __restrict__ target,
+                            const double* __restrict__ amp, const double* __restrict__ V, float2* __restrict__ G) {
+    const int P = h * w;
+    const int cell = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y;
+    if (cell >= P) return;
+    const double x = amp[static_cast<size_t>(j) * P + cell];
+    const double y = target[static_cast<size_t>(j) * P + cell];
+    const double d = x - y;
+    double g = l_w * (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) / P + lambda_fft * 2.0 * d;
+    if (lambda_ssim > 0.0) {
+        const int cols = w - kSsimWin + 1, rows = h - kSsimWin + 1;
+        const int pr = cell / w, pc = cell % w;
+        const size_t vplane = static_cast<size_t>(h) * cols;
+        double k3[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const double* vq = V + (static_cast<size_t>(j) * 3 + q) * vplane + static_cast<size_t>(pr) * cols;
+            double a = 0.0;
+#pragma unroll
+            for (int t = 0; t < kSsimWin; ++t) {
+                const int c = pc - t;
+                if (c >= 0 && c < cols) a += c_ssim_g[t] * vq[c];
+            }
+            k3[q] = a;
+        }
+        const double dssim = (k3[0] + y * k3[1] + x * k3[2]) / (static_cast<double>(rows) * cols);
+        g -= lambda_ssim * dssim;
+    }
+    const float* re_p = field + static_cast<size_t>(j) * 2 * P;
+    const double re = re_p[cell], im = re_p[P + cell];
+    G[static_cast<size_t>(j) * P + cell] = make_float2(static_cast<float>(g * re / x), static_cast<float>(g * im / x));
+}
+
+__global__ void k_loss_total(int n_rx, int nb, int P, double l_w, double lambda_ssim, double lambda_fft,
+                             const double* __restrict__ part, const double* __restrict__ ssim, double* __restrict__ loss) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n_rx) return;
+    double l1 = 0.0, sq = 0.0;
+    for (int b = 0; b < nb; ++b) {
+        l1 += part[(static_cast<size_t>(j) * nb + b) * 2];
+        sq += part[(static_cast<size_t>(j) * nb + b) * 2 + 1];
+    }
+    double v = l_w * l1 / P;
+    if (lambda_ssim > 0.0) v += lambda_ssim * (1.0 - ssim[j]);
+    if (lambda_fft > 0.0) v += lambda_fft * sq;
+    loss[j] = v;
+}
+
 // ------------------------------------------------------------------ composite transpose
 // d_entry[e][j] = sum_cells tw[e][cell] * G_j[cell] for the first W rows of a tile.
 __global__ void __launch_bounds__(256) k_composite_T(DevGrid g, const int64_t* __restrict__ tile_offsets,
@@ -569,6 +759,48 @@ cudaError_t launch_loss_spectrum(int n_rx, int P, const float* field, const floa
     const int nb = 16;
     k_loss_spectrum<<<dim3(nb, n_rx), 256, 0, s>>>(n_rx, P, field, target, l_weight, G, loss_part);
     k_loss_finalize<<<(n_rx + 127) / 128, 128, 0, s>>>(n_rx, nb, loss_part, loss);
+    return cudaGetLastError();
+}
+
+size_t loss_full_ws_bytes(int n_rx, int h, int w) {
+    const size_t P = static_cast<size_t>(h) * w, cols = w >= kSsimWin ? w - kSsimWin + 1 : 0,
+                 rows = h >= kSsimWin ? h - kSsimWin + 1 : 0;
+    return sizeof(double) * n_rx * (P + 5 * h * cols + 4 * rows * cols + 3 * h * cols + 2 * 16 + 1);
+}
+
+cudaError_t launch_loss_full(int n_rx, int h, int w, const float* field, const float* target, double l_w,
+                             double lambda_ssim, double lambda_fft, double dyn_range, float2* G, void* ws, double* loss,
+                             cudaStream_t s) {
+    const int P = h * w, nb = 16;
+    const int cols = w - kSsimWin + 1, rows = h - kSsimWin + 1;
+    double* amp = static_cast<double*>(ws);
+    double* H = amp + static_cast<size_t>(n_rx) * P;
+    double* S = H + static_cast<size_t>(n_rx) * 5 * h * (cols > 0 ? cols : 0);
+    double* coef = S + static_cast<size_t>(n_rx) * (rows > 0 ? rows : 0) * (cols > 0 ? cols : 0);
+    double* V = coef + static_cast<size_t>(n_rx) * 3 * (rows > 0 ? rows : 0) * (cols > 0 ? cols : 0);
+    double* part = V + static_cast<size_t>(n_rx) * 3 * h * (cols > 0 ? cols : 0);
+    double* ssim = part + static_cast<size_t>(n_rx) * 2 * nb;
+    k_loss_amp<<<dim3(nb, n_rx), 256, 0, s>>>(n_rx, P, field, target, amp, part);
+    if (lambda_ssim > 0.0) {
+        double g[kSsimWin], sum = 0.0;  // gaussian_window (metrics.cpp:38-51), 1-D factor
+        for (int t = 0; t < kSsimWin; ++t) {
+            const double d = t - kSsimWin / 2;
+            g[t] = std::exp(-(d * d) / (2.0 * 1.5 * 1.5));
+            sum += g[t];
+        }
+        for (double& v : g) v /= sum;
+        cudaError_t e = cudaMemcpyToSymbolAsync(c_ssim_g, g, sizeof(g), 0, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return e;
+        const double c1 = 0.01 * dyn_range * 0.01 * dyn_range, c2 = 0.03 * dyn_range * 0.03 * dyn_range;
+        const int tb = 128;
+        k_ssim_h<<<dim3((cols + tb - 1) / tb, h, n_rx), tb, 0, s>>>(n_rx, h, w, amp, target, H);
+        k_ssim_v<<<dim3((cols + tb - 1) / tb, rows, n_rx), tb, 0, s>>>(n_rx, h, w, c1, c2, H, S, coef);
+        k_ssim_mean<<<n_rx, 256, 0, s>>>(rows, cols, S, ssim);
+        k_ssim_bv<<<dim3((cols + tb - 1) / tb, h, n_rx), tb, 0, s>>>(n_rx, h, w, coef, V);
+    }
+    k_loss_grad<<<dim3((P + 255) / 256, n_rx), 256, 0, s>>>(n_rx, h, w, l_w, lambda_ssim, lambda_fft, field, target,
+                                                          amp, V, G);
+    k_loss_total<<<(n_rx + 127) / 128, 128, 0, s>>>(n_rx, nb, P, l_w, lambda_ssim, lambda_fft, part, ssim, loss);
     return cudaGetLastError();
 }
 

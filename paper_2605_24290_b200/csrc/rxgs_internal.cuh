@@ -288,6 +288,11 @@ cudaError_t launch_backward_render(const rxgs_txstate_s& st, const rxgs_scene_s&
 cudaError_t launch_refresh_gb(const rxgs_scene_s& sc, rxgs_txstate_s& st, cudaStream_t s);
 cudaError_t launch_loss_spectrum(int n_rx, int P, const float* field, const float* target, double l_weight,
                                  float2* G, double* loss_part, double* loss, cudaStream_t s);
+// composite_loss (spectrum) with the SSIM and DFT terms; ws of loss_full_ws_bytes
+size_t loss_full_ws_bytes(int n_rx, int h, int w);
+cudaError_t launch_loss_full(int n_rx, int h, int w, const float* field, const float* target, double l_w,
+                             double lambda_ssim, double lambda_fft, double dyn_range, float2* G, void* ws, double* loss,
+                             cudaStream_t s);
 cudaError_t launch_render_adjoint(const rxgs_txstate_s& st, const float2* G, int n_rx, float2* d_entry, float2* d_s,
                                   cudaStream_t s);
 size_t cond_bwd_smem();

@@ -24,7 +24,7 @@ struct rxgs_trainer_s {
     int64_t step = 0;
     int64_t n_base = 0, n_par = 0;
     DevBuf grad, m, v, field32, target, G, loss_part, loss, d_entry, d_s, u, part, red_part, row_part, gslice, rx,
-        flag;
+        flag, loss_ws;
     int n_parts = 0, n_red = 64;
 };
 
@@ -71,9 +71,9 @@ int rxgs_trainer_create(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const double h
         t->b2 = hyper[6];
         t->eps = hyper[7];
     }
-    if (t->lambda_ssim != 0.0 || t->lambda_fft != 0.0) {
+    if (t->lambda_ssim < 0.0 || t->lambda_fft < 0.0) {
         delete t;
-        return fail(RXGS_ERR_INVALID, "train: only the L1 spectrum loss (lambda_ssim = lambda_fft = 0) is implemented");
+        return fail(RXGS_ERR_INVALID, "train: loss weights must be non-negative");
     }
     t->n_base = static_cast<int64_t>(sc->k) * sc->L * sc->channels * 2;
     t->n_par = c->n_params;
@@ -161,8 +161,17 @@ int rxgs_train_grads(rxgs_trainer t, rxgs_txstate st, const double* rx, int n_rx
     RXGS_CUDA(t->loss_part.ensure(sizeof(double) * 16 * n_rx));
     RXGS_CUDA(t->loss.ensure(sizeof(double) * n_rx));
     const double l_weight = 1.0 - t->lambda_ssim - t->lambda_fft;
-    RXGS_CUDA(launch_loss_spectrum(n_rx, P, t->field32.as<float>(), d_tg, l_weight, t->G.as<float2>(),
-                                   t->loss_part.as<double>(), t->loss.as<double>(), s));
+    if (t->lambda_ssim == 0.0 && t->lambda_fft == 0.0) {
+        RXGS_CUDA(launch_loss_spectrum(n_rx, P, t->field32.as<float>(), d_tg, l_weight, t->G.as<float2>(),
+                                       t->loss_part.as<double>(), t->loss.as<double>(), s));
+    } else {  // composite_loss with SSIM and DFT terms (trainer.cpp:113-139)
+        const DevGrid& gg = st->grid;
+        if (t->lambda_ssim > 0.0 && (gg.nt < 11 || gg.np < 11))
+            return fail(RXGS_ERR_INVALID, "ssim: image smaller than the window");
+        RXGS_CUDA(t->loss_ws.ensure(loss_full_ws_bytes(n_rx, gg.nt, gg.np)));
+        RXGS_CUDA(launch_loss_full(n_rx, gg.nt, gg.np, t->field32.as<float>(), d_tg, l_weight, t->lambda_ssim,
+                                   t->lambda_fft, 1.0, t->G.as<float2>(), t->loss_ws.p, t->loss.as<double>(), s));
+    }
     // ---- render adjoint -> d_s
     RXGS_CUDA(t->d_entry.ensure(sizeof(float2) * std::max<size_t>(static_cast<size_t>(st->entries) * n_rx, 1)));
     RXGS_CUDA(t->d_s.ensure(sizeof(float2) * std::max<size_t>(static_cast<size_t>(sc->k) * n_rx, 1)));

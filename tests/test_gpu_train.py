@@ -56,6 +56,42 @@ def test_train_grads_match_reference_sum(ctx, capi, ref, mode):
     assert rel_err(dp, want_p).max() < TOL
 
 
+@pytest.mark.parametrize("lambdas", [(0.2, 0.1), (0.5, 0.0), (0.0, 0.3)])
+def test_train_full_loss_matches_reference(ctx, capi, ref, lambdas):
+    """composite_loss with the SSIM and DFT terms (trainer.cpp:113-139,
+    metrics.cpp:55-112): loss and summed gradients vs the reference."""
+    ls, lf = lambdas
+    sc, scene, cond, grid, og, rscene, rcond, params = _setup(capi, ctx, ref)
+    rx = capi.synth_points(3, 11, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
+    tg = _targets(3, grid.cells, 8)
+    st = scene.tx_state(TX, grid)
+    hp = list(capi.Trainer.DEFAULTS)
+    hp[3], hp[4] = ls, lf
+    tr = capi.Trainer(ctx, scene, cond, hp)
+    loss = tr.grads(st, rx, tg)
+    db, dp = tr.get_grads()
+    want_b = np.zeros_like(db)
+    want_p = np.zeros_like(dp)
+    for j in range(3):
+        r = ref.train_sample(rscene, rcond, og, TX, rx[j], tg[j].astype(np.float64), lambda_ssim=ls, lambda_fft=lf)
+        assert rel_err(loss[j], r["loss"]) < TOL
+        want_b += r["d_base"]
+        want_p += r["d_params"]
+    assert rel_err(db, want_b).max() < TOL
+    assert rel_err(dp, want_p).max() < TOL
+
+
+def test_train_ssim_needs_window(ctx, capi, ref):
+    sc, scene, cond, grid, og, rscene, rcond, params = _setup(capi, ctx, ref, nt=8, np_=36)
+    st = scene.tx_state(TX, grid)
+    hp = list(capi.Trainer.DEFAULTS)
+    hp[3] = 0.2
+    tr = capi.Trainer(ctx, scene, cond, hp)
+    rx = capi.synth_points(1, 11, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
+    with pytest.raises(capi.InvalidArgument, match="ssim: image smaller than the window"):
+        tr.grads(st, rx, _targets(1, grid.cells))
+
+
 def test_train_deterministic_and_accumulate(ctx, capi, ref):
     sc, scene, cond, grid, og, rscene, rcond, params = _setup(capi, ctx, ref, k=500)
     rx = capi.synth_points(4, 13, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
