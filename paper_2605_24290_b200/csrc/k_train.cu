@@ -352,7 +352,14 @@ __global__ void k_reduce_ds(const int* __restrict__ n_rows, const int* __restric
 __host__ __device__ constexpr int local_grad_count(int H) { return H * 6 + H + H * H + H + 4 * H + 4; }
 
 // One row = (needed Gaussian k, receiver j), C == 1, hidden H == 64.
-// smem per CTA: W2 (H*H) | per-row h1 | h2 | dh2 | dh1 (4 x 128 x H) | x (128 x 6) | dy (128 x 4)
+// Per row, the MLP forward recompute and backward run out of registers (h1,
+// dh1: 64 each; the weights are shared-memory broadcasts); h1, h2, dh1, dh2
+// then go to shared memory with a padded row stride (65 floats: conflict-free
+// both for one-row-per-thread writes and for the per-weight reads of the
+// gradient phase), where each thread owns fixed weight-gradient entries and
+// sums the tile's 128 rows in row order (deterministic).
+// smem per CTA: W2 (H*H) | h1 | h2 | dh2 | dh1 (4 x 128 x 65) | x (128 x 6) | dy (128 x 4)
+constexpr int kBwdPad = 65;
 __global__ void __launch_bounds__(kBwdThreads) k_cond_bwd(CondDev c, const int* __restrict__ n_rows,
                                                           const int* __restrict__ rows, const float4* __restrict__ pos32,
                                                           const double* __restrict__ rx, int n_rx,
@@ -363,10 +370,10 @@ __global__ void __launch_bounds__(kBwdThreads) k_cond_bwd(CondDev c, const int* 
     extern __shared__ __align__(16) float sm[];
     float* sW2 = sm;
     float* sH1 = sW2 + H * H;
-    float* sH2 = sH1 + kBwdThreads * H;
-    float* sDH2 = sH2 + kBwdThreads * H;
-    float* sDH1 = sDH2 + kBwdThreads * H;
-    float* sX = sDH1 + kBwdThreads * H;
+    float* sH2 = sH1 + kBwdThreads * kBwdPad;
+    float* sDH2 = sH2 + kBwdThreads * kBwdPad;
+    float* sDH1 = sDH2 + kBwdThreads * kBwdPad;
+    float* sX = sDH1 + kBwdThreads * kBwdPad;
     float* sDY = sX + kBwdThreads * 6;
     const float* p = c.p32;
     for (int i = threadIdx.x; i < H * H; i += blockDim.x) sW2[i] = p[c.o_lw2 + i];
@@ -384,34 +391,40 @@ __global__ void __launch_bounds__(kBwdThreads) k_cond_bwd(CondDev c, const int* 
          base_row += static_cast<long long>(gridDim.x) * kBwdThreads) {
         const long long row = base_row + t;
         const bool active = row < rows_total;
-        float* h1 = sH1 + t * H;
-        float* h2 = sH2 + t * H;
-        float* dh2 = sDH2 + t * H;
-        float* dh1 = sDH1 + t * H;
+        float* h2s = sH2 + t * kBwdPad;
+        float* dh2s = sDH2 + t * kBwdPad;
         float x[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         float dy[4] = {0.f, 0.f, 0.f, 0.f};
+        float h1[H], dh1[H];
+#pragma unroll
+        for (int o = 0; o < H; ++o) h1[o] = dh1[o] = 0.f;
         if (active && !c.use_local) {  // global-only mode: no local branch, u = d_s
             const int k = rows[row / n_rx], j = static_cast<int>(row % n_rx);
             u_out[static_cast<size_t>(k) * n_rx + j] = d_s[static_cast<size_t>(k) * n_rx + j];
-            for (int o = 0; o < H; ++o) h1[o] = h2[o] = dh2[o] = dh1[o] = 0.f;
+            for (int o = 0; o < H; ++o) h2s[o] = dh2s[o] = 0.f;
         } else if (active) {
             const int k = rows[row / n_rx], j = static_cast<int>(row % n_rx);
             const float4 pk = pos32[k];
             local_features<false>(c, c.occ, pk.x, pk.y, pk.z, static_cast<float>(rx[3 * j]),
                                   static_cast<float>(rx[3 * j + 1]), static_cast<float>(rx[3 * j + 2]), x);
             // forward (same arithmetic as the SIMT forward kernel)
+#pragma unroll
             for (int o = 0; o < H; ++o) {
                 float a = p[c.o_lb1 + o];
+#pragma unroll
                 for (int i = 0; i < 6; ++i) a = fmaf(p[c.o_lw1 + o * 6 + i], x[i], a);
                 h1[o] = fmaxf(a, 0.f);
             }
             float y[4] = {p[c.o_lb3], p[c.o_lb3 + 1], p[c.o_lb3 + 2], p[c.o_lb3 + 3]};
+#pragma unroll 1
             for (int o = 0; o < H; ++o) {
                 float a = p[c.o_lb2 + o];
                 const float* wr = sW2 + o * H;
+#pragma unroll
                 for (int i = 0; i < H; ++i) a = fmaf(wr[i], h1[i], a);
                 const float hv = fmaxf(a, 0.f);
-                h2[o] = hv;
+                h2s[o] = hv;
+#pragma unroll
                 for (int q = 0; q < 4; ++q) y[q] = fmaf(p[c.o_lw3 + q * H + o], hv, y[q]);
             }
             // signal pieces M = sum_l mid_l B_l, Bs = sum_l B_l (k_cond signal math)
@@ -434,22 +447,28 @@ __global__ void __launch_bounds__(kBwdThreads) k_cond_bwd(CondDev c, const int* 
             dy[2] = db.x;
             dy[3] = db.y;
             u_out[static_cast<size_t>(k) * n_rx + j] = cmul(make_float2(1.f + ar, -ai), ds);
-            // backward through layer 3 and the layer-2 ReLU
+            // backward through layer 3 and the layer-2 ReLU, then through W2
+#pragma unroll 1
             for (int o = 0; o < H; ++o) {
                 float a = 0.f;
+#pragma unroll
                 for (int q = 0; q < 4; ++q) a = fmaf(p[c.o_lw3 + q * H + o], dy[q], a);
-                dh2[o] = h2[o] > 0.f ? a : 0.f;
-            }
-            for (int i = 0; i < H; ++i) dh1[i] = 0.f;
-            for (int o = 0; o < H; ++o) {
-                const float g = dh2[o];
+                const float g = h2s[o] > 0.f ? a : 0.f;
+                dh2s[o] = g;
                 if (g == 0.f) continue;
                 const float* wr = sW2 + o * H;
+#pragma unroll
                 for (int i = 0; i < H; ++i) dh1[i] = fmaf(wr[i], g, dh1[i]);
             }
+#pragma unroll
             for (int i = 0; i < H; ++i) dh1[i] = h1[i] > 0.f ? dh1[i] : 0.f;
         } else {
-            for (int o = 0; o < H; ++o) h1[o] = h2[o] = dh2[o] = dh1[o] = 0.f;
+            for (int o = 0; o < H; ++o) h2s[o] = dh2s[o] = 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+            sH1[t * kBwdPad + i] = h1[i];
+            sDH1[t * kBwdPad + i] = dh1[i];
         }
         for (int i = 0; i < 6; ++i) sX[t * 6 + i] = x[i];
         for (int q = 0; q < 4; ++q) sDY[t * 4 + q] = dy[q];
@@ -458,28 +477,29 @@ __global__ void __launch_bounds__(kBwdThreads) k_cond_bwd(CondDev c, const int* 
         {
             const int o = t >> 1, i0 = (t & 1) * 32;
             for (int r = 0; r < kBwdThreads; ++r) {
-                const float g = sDH2[r * H + o];
+                const float g = sDH2[r * kBwdPad + o];
                 if (g == 0.f) continue;
-                const float* hr = sH1 + r * H + i0;
+                const float* hr = sH1 + r * kBwdPad + i0;
+#pragma unroll
                 for (int q = 0; q < 32; ++q) gw2[q] = fmaf(g, hr[q], gw2[q]);
             }
             for (int e = 0; e < 3; ++e) {
                 const int idx = t * 3 + e, oi = idx / 6, fi = idx % 6;
                 float a = gw1[e];
-                for (int r = 0; r < kBwdThreads; ++r) a = fmaf(sDH1[r * H + oi], sX[r * 6 + fi], a);
+                for (int r = 0; r < kBwdThreads; ++r) a = fmaf(sDH1[r * kBwdPad + oi], sX[r * 6 + fi], a);
                 gw1[e] = a;
             }
             for (int e = 0; e < 2; ++e) {
                 const int idx = t * 2 + e, q = idx / H, oo = idx % H;
                 float a = gw3[e];
-                for (int r = 0; r < kBwdThreads; ++r) a = fmaf(sDY[r * 4 + q], sH2[r * H + oo], a);
+                for (int r = 0; r < kBwdThreads; ++r) a = fmaf(sDY[r * 4 + q], sH2[r * kBwdPad + oo], a);
                 gw3[e] = a;
             }
             if (t < H) {
                 float a1 = gb1, a2 = gb2;
                 for (int r = 0; r < kBwdThreads; ++r) {
-                    a1 += sDH1[r * H + t];
-                    a2 += sDH2[r * H + t];
+                    a1 += sDH1[r * kBwdPad + t];
+                    a2 += sDH2[r * kBwdPad + t];
                 }
                 gb1 = a1;
                 gb2 = a2;
@@ -822,7 +842,7 @@ cudaError_t launch_render_adjoint(const rxgs_txstate_s& st, const float2* G, int
     return cudaGetLastError();
 }
 
-size_t cond_bwd_smem() { return sizeof(float) * (64 * 64 + 4 * kBwdThreads * 64 + kBwdThreads * 10); }
+size_t cond_bwd_smem() { return sizeof(float) * (64 * 64 + 4 * kBwdThreads * kBwdPad + kBwdThreads * 10); }
 int cond_bwd_parts(int sms) { return sms * 2; }
 int local_grad_n() { return local_grad_count(64); }
 
