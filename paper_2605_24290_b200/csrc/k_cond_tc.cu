@@ -42,6 +42,11 @@
 #ifndef RXGS_MBAR_WAIT
 #define RXGS_MBAR_WAIT tc::mbar_wait_sleep
 #endif
+// layer-3 weights staged in shared memory from the device parameters (1) or
+// passed as a kernel parameter from the host copy (0)
+#ifndef RXGS_W3_SMEM
+#define RXGS_W3_SMEM 0
+#endif
 // double-buffered TMEM readback of the 64 accumulator columns
 #ifndef RXGS_LD_DB
 #define RXGS_LD_DB 0
@@ -336,12 +341,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* s_occ = reinterpret_cast<float*>(smem + kFixedSmem);
     __shared__ uint64_t bars[kGroups];
     __shared__ uint32_t arrivals[kGroups];
+#if RXGS_W3_SMEM
+    // layer 3 from the device parameters (current even while training updates them)
+    __shared__ float4 s_w3[kH];
+    __shared__ float s_b3[4];
+#endif
     __shared__ uint32_t tbase_s;
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int g = warp >> 2, wl = warp & 3;
     if (tid < kGroups) arrivals[tid] = 0u;
+#if RXGS_W3_SMEM
+    if (tid < kH)
+        s_w3[tid] = make_float4(c.p32[c.o_lw3 + tid], c.p32[c.o_lw3 + kH + tid], c.p32[c.o_lw3 + 2 * kH + tid],
+                                c.p32[c.o_lw3 + 3 * kH + tid]);
+    if (tid < 4) s_b3[tid] = c.p32[c.o_lb3 + tid];
+#define RXGS_W3(o) s_w3[o]
+#define RXGS_B3(q) s_b3[q]
+#else
+#define RXGS_W3(o) W.w3[o]
+#define RXGS_B3(q) W.b3[q]
+#endif
 
     // ---- one-time setup: weights as bf16 hi/lo core matrices, occupancy
     for (int i = tid; i < kH * kH; i += kThreads) split_store(w2hi, w2lo, canon_off(i / kH, i % kH), c.p32[c.o_lw2 + i]);
@@ -656,7 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         phase ^= 1u;
         tc::fence_after_sync();
         // ---- ReLU(h2), layer 3 on FFMA2 from the TMEM accumulator
-        float2 ya = make_float2(W.b3[0], W.b3[1]), yb = make_float2(W.b3[2], W.b3[3]);
+        float2 ya = make_float2(RXGS_B3(0), RXGS_B3(1)), yb = make_float2(RXGS_B3(2), RXGS_B3(3));
         float2 ya1 = make_float2(0.f, 0.f), yb1 = make_float2(0.f, 0.f);  // odd columns (FFMA2 latency)
         {
             uint32_t vb[2][16];
@@ -668,7 +689,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (RXGS_LD_DB && ch + 1 < 4) tc::tmem_ld16(tm_d + lane_off + 16 * (ch + 1), vb[(ch + 1) & 1]);
 #pragma unroll
             for (int q = 0; q < 16; q += 2) {
-                const float4 w3 = W.w3[16 * ch + q], w3b = W.w3[16 * ch + q + 1];
+                const float4 w3 = RXGS_W3(16 * ch + q), w3b = RXGS_W3(16 * ch + q + 1);
                 const float2 h2 = x2::bc(fmaxf(__uint_as_float(v[q]), 0.f));
                 const float2 h2b = x2::bc(fmaxf(__uint_as_float(v[q + 1]), 0.f));
                 ya = x2::fma(h2, make_float2(w3.x, w3.y), ya);
