@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--train-batch", type=int, default=16, help="(tx, rx) samples per GPU per training step")
     ap.add_argument("--no-config3", action="store_true", help="skip the coverage-table (config 3) leg")
     ap.add_argument("--no-config5", action="store_true", help="skip the 2M / 180x720 (config 5) leg")
+    ap.add_argument("--no-lmax9", action="store_true", help="skip the config-2 l_max = 9 (L = 100) leg")
     return ap.parse_args()
 
 
@@ -310,6 +311,7 @@ def run_b200(args):
     del scene, cond
     cov = None if args.no_config3 else bench_coverage(args, capi, ctx, stream, dev, rank, world)
     large = None if args.no_config5 else bench_large(args, capi, ctx, stream, dev, rank, world)
+    lmax9 = None if args.no_lmax9 else bench_lmax9(args, capi, ctx, stream, dev, rank, world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -331,7 +333,8 @@ def run_b200(args):
                 "vs_baseline": None, "dtype": "f32 (FP64 geometry/walk)", "data": "synthetic",
                 "config": workload(args), "e2e": e2e, "gpu_launches": int(launches),
                 "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
-                "tx_state": stats, "train_config4": train, "config3": cov, "config5": large}
+                "tx_state": stats, "train_config4": train, "config3": cov, "config5": large,
+                "config2_lmax9": lmax9}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -527,8 +530,6 @@ def bench_large(args, capi, ctx, stream, dev, rank, world):
         last = step()
     torch.cuda.synchronize(dev)
     n_steps = max(3, min(args.steps, 5))
-    ctx.reset_stats()
-    ctx.profile(True)
     l0 = ctx.launch_count()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_steps)]
     for i in range(n_steps):
@@ -539,8 +540,14 @@ def bench_large(args, capi, ctx, stream, dev, rank, world):
     torch.cuda.synchronize(dev)
     ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in evs) / n_steps, dev)
     launches = (ctx.launch_count() - l0) // n_steps
-    phases = {nm: ctx.kernel_stats(nm)[0] / n_steps for nm in ("tx_prep", "sort", "walk", "cond_global",
-                                                              "cond_signal", "composite")}
+    ctx.reset_stats()  # per-phase times from a separate profiled pass
+    ctx.profile(True)
+    for i in range(2):
+        flush.fill_(float(i))
+        last = step()
+    torch.cuda.synchronize(dev)
+    phases = {nm: ctx.kernel_stats(nm)[0] / 2 for nm in ("tx_prep", "sort", "walk", "cond_global",
+                                                        "cond_signal", "composite")}
     ctx.profile(False)
     stats = last.stats()
     del last
@@ -578,6 +585,81 @@ def bench_large(args, capi, ctx, stream, dev, rank, world):
             "e2e": {"value": world * n / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": int(rx.nbytes + 24), "d2h_bytes_per_step": int(spec_h.nbytes + rssi_h.nbytes)},
             "phase_ms": phases, "gpu_launches": int(launches), "tx_state": stats, "cpu_baseline": cpu}
+
+
+def bench_lmax9(args, capi, ctx, stream, dev, rank, world):
+    """Config 2 at the paper's spectrum setting l_max = 9 (L = 100 FLE
+    components; SURVEY.md 8d secondary point)."""
+    import torch
+    from paper_2605_24290_b200.dist import max_over_ranks, shard_range
+    K, n, l_max = args.gaussians, args.rx, 9
+    b, e = shard_range(world * n, rank, world)
+    rx = capi.synth_points(world * n, 11, "bench.rx", BOX_LO, BOX_HI, 0.05)[b:e]
+    scene = ctx.scene(capi.synth_scene(K, l_max, 1, 7), "spectrum")
+    lo, hi = scene.bounds(0.0)
+    cfg = capi.cond_cfg(l_max=l_max)
+    cond = ctx.cond(cfg, capi.synth_cond(cfg, l_max, 1, lo, hi, 3, True))
+    olo, ohi = scene.bounds(0.1)
+    cond.build_occupancy(scene, 32, olo, ohi)
+    grid = capi.Grid(args.n_theta, args.n_phi, 8, 1.0)
+    tx = np.array(TX)
+    rx_d = torch.from_numpy(rx).to(dev)
+    spec = torch.empty((n, args.n_theta, args.n_phi), dtype=torch.float32, device=dev)
+    rssi = torch.empty(n, dtype=torch.float32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        st = scene.tx_state(tx, grid)
+        scene.render_queries(cond, st, rx_d, spec, rssi)
+        return st
+
+    last = None
+    for _ in range(2):
+        last = step()
+    torch.cuda.synchronize(dev)
+    n_steps = max(3, min(args.steps, 5))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_steps)]
+    for i in range(n_steps):
+        flush.fill_(float(i))
+        evs[i][0].record(stream)
+        last = step()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in evs) / n_steps, dev)
+    ctx.reset_stats()
+    ctx.profile(True)
+    last = step()
+    torch.cuda.synchronize(dev)
+    phases = {nm: ctx.kernel_stats(nm)[0] for nm in ("tx_prep", "sort", "walk", "cond_global", "cond_signal",
+                                                    "composite")}
+    ctx.profile(False)
+    del last
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import oracle as O  # cpu_baseline leg
+            chk = O.reference()
+            sc = chk.synth_scene(K, l_max, 1, 7)
+            h = chk.scene(sc, "spectrum")
+            rlo, rhi = chk.scene_bounds(h, 0.0)
+            rcfg = O.cond_cfg(l_max=l_max)
+            params = chk.synth_cond(rcfg, l_max, 1, rlo, rhi, 3, True)
+            rolo, rohi = chk.scene_bounds(h, 0.1)
+            rc = chk.cond(rcfg, params, chk.build_occupancy(h, 32, rolo, rohi), rolo, rohi)
+            threads, sample = os.cpu_count() or 1, 8
+            secs, _, _ = chk.bench_queries(h, rc, O.Grid(args.n_theta, args.n_phi, 8, 1.0), TX, rx[:sample], threads)
+            cpu = {"value": sample / secs, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"{sample} receivers, build_tx_state + conditioning + render + aggregation, "
+                             f"{secs:.1f} s wall"}
+        except Exception as ex:
+            cpu = {"error": str(ex)}
+    del scene, cond
+    ctx.release_cache()
+    return {"workload": f"config2 at l_max=9: K={K}, 1 Tx x {n} Rx per rank, {args.n_theta}x{args.n_phi}, "
+                        f"L=100 FLE components, spectrum + RSSI, conditioned (full)",
+            "value": world * n / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "steps": n_steps, "scaling": "weak",
+            "n_gpus": world, "l2": "flushed between timed steps", "phase_ms": phases, "cpu_baseline": cpu}
 
 
 def run_reference(args):

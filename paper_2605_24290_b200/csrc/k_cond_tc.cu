@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_cond_tc(const __grid_constant__ LocalW W, CondDev c, const int* __restrict__ n_rows_dev, int n_rows_host,
               int cap, const int* __restrict__ rows, const float4* __restrict__ rpos, const double* __restrict__ rx,
               int n_rx, const float4* __restrict__ rGB, const float4* __restrict__ rS,
-              const float* __restrict__ ag, SigOut sig,
+              const float* __restrict__ ag, const float2* __restrict__ Mpre, SigOut sig,
               float4* __restrict__ ycache) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* w2hi = smem;
@@ -547,7 +547,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int k = active ? rows[r] : 0;
         float2 M = make_float2(0.f, 0.f), Bs = make_float2(0.f, 0.f);
         auto fle = [&]() {
-        if (!YOUT && active) {
+        if (!YOUT && active && Mpre) {  // from the FLE GEMM (high l_max)
+            const float4 sums = rS[r];
+            M = Mpre[static_cast<size_t>(j) * cap + r];
+            Bs = make_float2(sums.z, sums.w);
+        } else if (!YOUT && active) {
             const float4 sums = rS[r];
             M = make_float2(sums.x, sums.y);
             Bs = make_float2(sums.z, sums.w);
@@ -830,7 +834,7 @@ namespace {
 template <bool YOUT>
 cudaError_t launch_tc(const rxgs_cond_s& cs, const int* n_rows_dev, long long rows_host, int cap, const int* rows,
                       const float4* rpos, const double* d_rx, int n_rx, const float4* rGB, const float4* rS,
-                      const float* d_ag, SigOut d_sig, float4* ycache, cudaStream_t s) {
+                      const float* d_ag, const float2* Mpre, SigOut d_sig, float4* ycache, cudaStream_t s) {
     if (rows_host == 0 || n_rx == 0) return cudaSuccess;
     const CondDev d = make_dev(cs);
     LocalW w{};
@@ -857,7 +861,7 @@ cudaError_t launch_tc(const rxgs_cond_s& cs, const int* n_rows_dev, long long ro
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     kern<<<blocks, kThreads, smem, s>>>(w, d, n_rows_dev, static_cast<int>(rows_host), cap, rows, rpos, d_rx, n_rx,
-                                        rGB, rS, d_ag, d_sig, ycache);
+                                        rGB, rS, d_ag, Mpre, d_sig, ycache);
     return cudaGetLastError();
 }
 
@@ -882,14 +886,26 @@ cudaError_t launch_cond_signal_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc,
         ctx->row_pos.as<float4>(), ctx->row_GB.as<float4>(), ctx->row_S.as<float4>());
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ctx->launches += 1;
+    // high l_max: the FLE reduction as one tensor-core GEMM instead of the per-row loop
+#ifndef RXGS_FLE_GEMM_MIN_L
+#define RXGS_FLE_GEMM_MIN_L 16
+#endif
+    const float2* Mpre = nullptr;
+    if (L >= RXGS_FLE_GEMM_MIN_L) {
+        if ((e = ctx->fle_m.ensure(sizeof(float2) * static_cast<size_t>(cap) * n_rx)) != cudaSuccess) return e;
+        if ((e = launch_fle_gemm(ctx, n_rows, bound, cap, L, n_rx, ctx->row_GB.as<float4>(), ctx->row_S.as<float4>(),
+                                 d_ag, ctx->fle_m.as<float2>(), s)) != cudaSuccess)
+            return e;
+        Mpre = ctx->fle_m.as<float2>();
+    }
     return launch_tc<false>(cs, n_rows, bound, cap, rows, ctx->row_pos.as<float4>(), d_rx, n_rx,
-                            ctx->row_GB.as<float4>(), ctx->row_S.as<float4>(), d_ag, d_sig, nullptr, s);
+                            ctx->row_GB.as<float4>(), ctx->row_S.as<float4>(), d_ag, Mpre, d_sig, nullptr, s);
 }
 
 cudaError_t launch_local_cache_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const double* d_rx, int n_rx,
                                   float4* ycache, cudaStream_t s) {
     return launch_tc<true>(cs, nullptr, sc.k, sc.k, sc.d_morton.as<int>(), sc.d_mpos32.as<float4>(), d_rx, n_rx,
-                           nullptr, nullptr, nullptr, SigOut(), ycache, s);
+                           nullptr, nullptr, nullptr, nullptr, SigOut(), ycache, s);
 }
 
 cudaError_t launch_tc_selftest(float* d_err, cudaStream_t s) {

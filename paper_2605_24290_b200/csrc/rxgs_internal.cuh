@@ -118,6 +118,8 @@ struct rxgs_ctx_s {
     // conditioning rows gathered into row order (k_cond_tc.cu): positions,
     // (basis*base, basis) transposed to [l][row], their sums over l
     rxgs_b200::DevBuf row_pos, row_GB, row_S;
+    // FLE GEMM operands / result for high l_max (k_fle_gemm.cu)
+    rxgs_b200::DevBuf fle_a, fle_b, fle_m;
     int sm_count = 148;
     int cond_kernel = 0;  // 0 auto (tcgen05 when eligible), 1 force SIMT
     int composite_kernel = 0;  // 0 auto (tcgen05 when eligible), 1 force SIMT
@@ -234,6 +236,10 @@ cudaError_t launch_cond_signal_tc(const rxgs_cond_s& c, const rxgs_scene_s& sc, 
                                   const double* d_rx, int n_rx, const float* d_ag, SigOut d_sig,
                                   cudaStream_t s);
 cudaError_t launch_tc_selftest(float* d_err, cudaStream_t s);
+// FLE reduction of the query path as a tensor-core GEMM: Mout[j][row] (k_fle_gemm.cu)
+int fle_gemm_kpad(int L);
+cudaError_t launch_fle_gemm(rxgs_ctx ctx, const int* n_rows_dev, long long rows_bound, int cap, int L, int n_rx,
+                            const float4* rGB, const float4* rS, const float* d_ag, float2* Mout, cudaStream_t s);
 cudaError_t launch_tc_selftest_mn(float* d_err, cudaStream_t s);
 // reduce_signals from materialised f64 coefficients.
 cudaError_t launch_reduce_signals(const rxgs_txstate_s& st, const double* d_coeffs, int n_rx,

@@ -173,6 +173,27 @@ def test_render_queries_matches_oracle_predict(ctx, capi, orc, k, nt, np_, mode)
         assert rel_err(rssi[j], wr) < TOL
 
 
+@pytest.mark.parametrize("l_max,n_rx", [(4, 5), (9, 3), (9, 130)])
+def test_render_queries_high_lmax_fle_gemm(ctx, capi, orc, l_max, n_rx):
+    """l_max >= 3 (L >= 16) takes the FLE reduction as a tensor-core GEMM
+    (k_fle_gemm.cu); l_max = 9 is the paper's spectrum setting.  130
+    receivers span two 128-receiver GEMM column tiles (ragged)."""
+    import oracle as O
+    sc = capi.synth_scene(2500, l_max, 1, 7)
+    scene, cond, oscene, ocond = _setup_cond(capi, ctx, orc, sc)
+    grid = capi.Grid(30, 60, 8, 1.0)
+    st = scene.tx_state(TX, grid)
+    rx = capi.synth_points(n_rx, 11, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
+    spec, rssi = scene.render_queries(cond, st, rx)
+    og = O.Grid(30, 60, 8, 1.0)
+    oscene_r = orc.scene(sc, "rssi")
+    for j in sorted({0, n_rx // 2, n_rx - 1}):
+        want = orc.predict(oscene, ocond, og, TX, rx[j], "spectrum").reshape(30, 60)
+        assert rel_err(spec[j], want).max() < TOL
+        wr = orc.predict(oscene_r, ocond, og, TX, rx[j], "rssi")[0]
+        assert rel_err(rssi[j], wr) < TOL
+
+
 def test_render_queries_unconditioned_and_batch_invariance(ctx, capi, orc):
     import oracle as O
     sc = capi.synth_scene(3000, 2, 1, 8)
