@@ -300,8 +300,8 @@ def run_b200(args):
         achieved = flop_row * per_launch_rows / (avg_ms / 1e3) / 1e12
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per launch (profiles/r1_traffic.json)",
-                    "kernel": "k_cond_tc (probe + local MLP on tcgen05 + FLE reduction)",
-                    "pipe": "tcgen05 bf16x3 (hidden layer) + FP32 SIMT (probe, layers 1/3, FLE)", "peak_source": peak_src,
+                    "kernel": "cond_signal = k_fle_gemm (FLE reduction, tcgen05 GEMM) + k_cond_tc (probe + local MLP on tcgen05 + affine)",
+                    "pipe": "tcgen05 bf16x3 (layers 1-2, FLE GEMM) + FP32 SIMT on FFMA2 (probe, layer 3, affine)", "peak_source": peak_src,
                     "flop_per_row": flop_row, "rows_per_launch": per_launch_rows,
                     "kernel_ms": avg_ms,
                     "share_of_step": (cond_ms / cond_n) / ms_local,
