@@ -167,6 +167,17 @@ int rxgs_backward_render(rxgs_ctx ctx, rxgs_txstate st, rxgs_scene scene, const 
                          double* d_log_scales, double* d_quaternions, double* d_tau_logits,
                          double* d_coeffs);
 
+/* ------------------------------------------------------------ coverage consumers
+ * apps::coverage_fraction / apps::greedy_plan (apps.hpp:34-43, apps.cpp:69-116)
+ * over a tx-major RSSI table (tx_count x cand_count f64 dBm, host or
+ * device; e.g. rxgs_coverage_table's output widened to f64).  Exact:
+ * threshold tests and counts; greedy ties break on the lower candidate.
+ * greedy_plan writes k candidate indices in selection order. */
+int rxgs_coverage_fraction(rxgs_ctx ctx, const double* table, int64_t tx_count, int64_t cand_count,
+                           const int32_t* selected, int n_selected, double threshold_dbm, double* out);
+int rxgs_greedy_plan(rxgs_ctx ctx, const double* table, int64_t tx_count, int64_t cand_count, int k,
+                     double threshold_dbm, int32_t* order);
+
 /* ------------------------------------------------------------ scene / model load
  * io::save_checkpoint / io::load_checkpoint (checkpoint.hpp:17-18,
  * checkpoint.cpp:93-231): the RXGS container ("RXGS", u32 version 1, u64

@@ -136,6 +136,9 @@ class Checker:
                                               C.c_int, _dp, _dp, _dp, _dp, _dp, C.c_char_p, C.c_int]),
                 "cond_backward": (C.c_int, [C.c_void_p, C.c_void_p, _dp, _dp, _dp, _dp]),
                 "cond_calls": (None, [C.c_void_p, _lp, _lp]),
+                "coverage_fraction": (C.c_int, [_dp, C.c_long, C.c_long, _ip, C.c_int, C.c_double, _dp,
+                                                C.c_char_p, C.c_int]),
+                "greedy_plan": (C.c_int, [_dp, C.c_long, C.c_long, C.c_int, C.c_double, _ip, C.c_char_p, C.c_int]),
                 "train_sample": (C.c_int, [C.c_void_p, C.c_void_p, _ip, _dp, _dp, _dp, _dp, C.c_double,
                                            C.c_double, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
                                            C.c_char_p, C.c_int]),
@@ -425,3 +428,30 @@ def _train_sample(self, scene_h, cond_h, grid: Grid, tx, rx, target, lambda_ssim
 
 
 Checker.train_sample = _train_sample
+
+
+def _coverage_fraction(self, table, selected, thr):
+    """apps::coverage_fraction (reference build only)."""
+    t = np.ascontiguousarray(table, np.float64)
+    sel = np.ascontiguousarray(selected, np.int32)
+    out = np.zeros(1)
+    err = C.create_string_buffer(512)
+    if self._coverage_fraction(t.ctypes.data_as(_dp), t.shape[0], t.shape[1], sel.ctypes.data_as(_ip), sel.size,
+                               float(thr), out.ctypes.data_as(_dp), err, 512):
+        raise ValueError(err.value.decode())
+    return float(out[0])
+
+
+def _greedy_plan(self, table, k, thr):
+    """apps::greedy_plan (reference build only)."""
+    t = np.ascontiguousarray(table, np.float64)
+    order = np.zeros(max(int(k), 1), np.int32)
+    err = C.create_string_buffer(512)
+    if self._greedy_plan(t.ctypes.data_as(_dp), t.shape[0], t.shape[1], int(k), float(thr),
+                         order.ctypes.data_as(_ip), err, 512):
+        raise ValueError(err.value.decode())
+    return order[:k]
+
+
+Checker.coverage_fraction = _coverage_fraction
+Checker.greedy_plan = _greedy_plan

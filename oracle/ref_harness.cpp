@@ -27,6 +27,7 @@
 #include <thread>
 #include <vector>
 
+#include "rxgs/apps.hpp"
 #include "rxgs/conditioning.hpp"
 #include "rxgs/radiance.hpp"
 #include "rxgs/rng.hpp"
@@ -676,6 +677,31 @@ int ref_train_sample(void* scene, void* cond, const int* gi, const double* gd, c
         if (d_ls) std::memcpy(d_ls, b.d_log_scales.data(), b.d_log_scales.size() * sizeof(double));
         if (d_q) std::memcpy(d_q, b.d_quaternions.data(), b.d_quaternions.size() * sizeof(double));
         if (d_tau) std::memcpy(d_tau, b.d_tau_logits.data(), b.d_tau_logits.size() * sizeof(double));
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return 1;
+    }
+}
+
+// apps::coverage_fraction / greedy_plan (apps.cpp:69-116) on a tx-major table.
+int ref_coverage_fraction(const double* table, long tx, long cand, const int* sel, int n_sel, double thr, double* out,
+                          char* err, int errlen) {
+    try {
+        *out = apps::coverage_fraction(std::vector<double>(table, table + tx * cand), static_cast<std::size_t>(tx),
+                                       static_cast<std::size_t>(cand), std::vector<int>(sel, sel + n_sel), thr);
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return 1;
+    }
+}
+
+int ref_greedy_plan(const double* table, long tx, long cand, int k, double thr, int* order, char* err, int errlen) {
+    try {
+        const auto o = apps::greedy_plan(std::vector<double>(table, table + tx * cand), static_cast<std::size_t>(tx),
+                                         static_cast<std::size_t>(cand), k, thr);
+        std::copy(o.begin(), o.end(), order);
         return 0;
     } catch (const std::exception& e) {
         set_err(err, errlen, e.what());

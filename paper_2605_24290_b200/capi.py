@@ -118,6 +118,8 @@ _SIG = {
     "rxgs_scene_get_coeffs": (C.c_int, [_vp, _vp]),
     "rxgs_checkpoint_save": (C.c_int, [C.c_char_p, _vp, C.POINTER(Grid), _vp]),
     "rxgs_checkpoint_load": (C.c_int, [_vp, C.c_char_p, C.POINTER(_vp), C.POINTER(Grid), C.POINTER(_vp)]),
+    "rxgs_coverage_fraction": (C.c_int, [_vp, _vp, _i64, _i64, _vp, C.c_int, C.c_double, C.POINTER(C.c_double)]),
+    "rxgs_greedy_plan": (C.c_int, [_vp, _vp, _i64, _i64, C.c_int, C.c_double, _vp]),
     "rxgs_scene_info": (C.c_int, [_vp, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32)]),
     "rxgs_cond_config": (C.c_int, [_vp, _vp]),
     "rxgs_cond_get_params": (C.c_int, [_vp, _vp]),
@@ -275,6 +277,24 @@ class Context:
         scene = Scene._wrap(self, hs)
         cond = Cond._wrap(self, hc) if hc.value else None
         return scene, grid, cond
+
+    def coverage_fraction(self, table, selected, threshold_dbm):
+        """apps::coverage_fraction (apps.cpp:69-84) over a tx-major table."""
+        table = np.ascontiguousarray(table, np.float64)
+        sel = np.ascontiguousarray(selected, np.int32)
+        out = C.c_double()
+        _check(_lib.rxgs_coverage_fraction(self.h, table.ctypes.data, table.shape[0], table.shape[1],
+                                           sel.ctypes.data if sel.size else None, int(sel.size),
+                                           float(threshold_dbm), C.byref(out)))
+        return out.value
+
+    def greedy_plan(self, table, k, threshold_dbm):
+        """apps::greedy_plan (apps.cpp:86-114): k candidates in selection order."""
+        table = np.ascontiguousarray(table, np.float64)
+        order = np.empty(max(int(k), 0), np.int32)
+        _check(_lib.rxgs_greedy_plan(self.h, table.ctypes.data, table.shape[0], table.shape[1], int(k),
+                                     float(threshold_dbm), order.ctypes.data if order.size else None))
+        return order
 
     def bin_and_sort(self, culled, depth, spans, grid: Grid):
         k = len(culled)
