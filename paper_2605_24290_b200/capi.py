@@ -122,6 +122,8 @@ _SIG = {
     "rxgs_greedy_plan": (C.c_int, [_vp, _vp, _i64, _i64, C.c_int, C.c_double, _vp]),
     "rxgs_scene_info": (C.c_int, [_vp, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32)]),
     "rxgs_cond_config": (C.c_int, [_vp, _vp]),
+    "rxgs_scene_get_arrays": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "rxgs_cond_get_occupancy": (C.c_int, [_vp, C.POINTER(_i32), _vp, _vp, _vp]),
     "rxgs_cond_get_params": (C.c_int, [_vp, _vp]),
 }
 for _name, (_res, _args) in _SIG.items():
