@@ -13,7 +13,7 @@ if os.path.exists(lc):
     open(os.path.join(prof, f"{tag}_launches.txt"), "w").write(S.launches(lc) + "\n")
 traffic = {"source": "ncu --set full --clock-control none, one launch each; bench.py config 2 (K=100k, 1024 rx, 90x360); "
                      "k_cov_signal from the config-3 leg (K=500k)"}
-for k in ["k_cond_tc", "k_composite_tc", "k_walk", "k_tx_prep", "k_cov_signal"]:
+for k in ["k_cond_tc", "k_fle_gemm", "k_composite_tc", "k_walk", "k_tx_prep", "k_cov_signal"]:
     rep = os.path.join(out, f"{tag}_{k}.ncu-rep")
     if not os.path.exists(rep):
         continue
