@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cmath>
 #include <cstring>
@@ -25,6 +26,11 @@ thread_local std::string g_err;
 int fail(int code, const std::string& msg) {
     g_err = msg;
     return code;
+}
+
+uint64_t next_version() {
+    static std::atomic<uint64_t> v{0};
+    return ++v;
 }
 
 int cuda_fail(cudaError_t e, const char* what) {
@@ -544,6 +550,7 @@ int rxgs_tx_state_build(rxgs_ctx ctx, rxgs_scene sc, const double tx[3], const r
     st->entries = st->visible = 0;
     st->needed_host = -1;
     st->regrouped = false;  // recycled buffers: per-state derived data must be rebuilt
+    st->version = next_version();
     st->ctx = ctx;
     st->k = sc->k;
     st->l_max = sc->l_max;

@@ -881,11 +881,15 @@ cudaError_t launch_cond_signal_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc,
     const int* n_rows = st.needed_count.as<int>();
     const int* rows = st.needed_order.as<int>();
     const long long bound = st.needed_host >= 0 ? st.needed_host : st.visible;
-    k_gather_rows<<<static_cast<unsigned>((bound + 255) / 256), 256, 0, s>>>(
-        n_rows, rows, cap, L, sc.d_pos32.as<float4>(), st.basis32.as<float2>(), st.gb32.as<float2>(),
-        ctx->row_pos.as<float4>(), ctx->row_GB.as<float4>(), ctx->row_S.as<float4>());
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    ctx->launches += 1;
+    if (ctx->rows_version != st.version) {  // receiver-independent: once per state, not per receiver chunk
+        k_gather_rows<<<static_cast<unsigned>((bound + 255) / 256), 256, 0, s>>>(
+            n_rows, rows, cap, L, sc.d_pos32.as<float4>(), st.basis32.as<float2>(), st.gb32.as<float2>(),
+            ctx->row_pos.as<float4>(), ctx->row_GB.as<float4>(), ctx->row_S.as<float4>());
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        ctx->launches += 1;
+        ctx->rows_version = st.version;
+        ctx->fle_a_version = 0;
+    }
     // high l_max: the FLE reduction as one tensor-core GEMM instead of the per-row loop
 #ifndef RXGS_FLE_GEMM_MIN_L
 #define RXGS_FLE_GEMM_MIN_L 4  // A/B at L=9: GEMM 2.70 ms vs per-row loop 2.95 ms
@@ -894,7 +898,7 @@ cudaError_t launch_cond_signal_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc,
     if (L >= RXGS_FLE_GEMM_MIN_L) {
         if ((e = ctx->fle_m.ensure(sizeof(float2) * static_cast<size_t>(cap) * n_rx)) != cudaSuccess) return e;
         if ((e = launch_fle_gemm(ctx, n_rows, bound, cap, L, n_rx, ctx->row_GB.as<float4>(), ctx->row_S.as<float4>(),
-                                 d_ag, ctx->fle_m.as<float2>(), s)) != cudaSuccess)
+                                 d_ag, ctx->fle_m.as<float2>(), s, st.version)) != cudaSuccess)
             return e;
         Mpre = ctx->fle_m.as<float2>();
     }

@@ -199,7 +199,8 @@ __global__ void __launch_bounds__(kThr) k_fle_gemm(const int* __restrict__ n_row
 int fle_gemm_kpad(int L) { return (4 * L + kTK - 1) / kTK * kTK; }
 
 cudaError_t launch_fle_gemm(rxgs_ctx ctx, const int* n_rows_dev, long long rows_bound, int cap, int L, int n_rx,
-                            const float4* rGB, const float4* rS, const float* d_ag, float2* Mout, cudaStream_t s) {
+                            const float4* rGB, const float4* rS, const float* d_ag, float2* Mout, cudaStream_t s,
+                            uint64_t a_version) {
     if (rows_bound == 0 || n_rx == 0) return cudaSuccess;
     const int Kp = fle_gemm_kpad(L);
     cudaError_t e;
@@ -210,7 +211,10 @@ cudaError_t launch_fle_gemm(rxgs_ctx ctx, const int* n_rows_dev, long long rows_
     uint16_t* b_hi = ctx->fle_b.as<uint16_t>();
     uint16_t* b_lo = b_hi + 2 * static_cast<size_t>(n_rx) * Kp;
     const long long na = rows_bound * (Kp / 4), nb = 2LL * n_rx * (Kp / 4);
-    k_fle_pack_a<<<static_cast<unsigned>((na + 255) / 256), 256, 0, s>>>(n_rows_dev, cap, L, Kp, rGB, a_hi, a_lo);
+    if (a_version == 0 || ctx->fle_a_version != a_version) {  // A depends on the state only
+        k_fle_pack_a<<<static_cast<unsigned>((na + 255) / 256), 256, 0, s>>>(n_rows_dev, cap, L, Kp, rGB, a_hi, a_lo);
+        ctx->fle_a_version = a_version;
+    }
     k_fle_pack_b<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, s>>>(n_rx, L, Kp,
                                                                           reinterpret_cast<const float4*>(d_ag), b_hi, b_lo);
     const size_t smem = kStages * kStage;

@@ -766,6 +766,7 @@ int train_regroup(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
 }
 
 cudaError_t launch_refresh_gb(const rxgs_scene_s& sc, rxgs_txstate_s& st, cudaStream_t s) {
+    st.version = next_version();  // basis*base changes: cached row data is stale
     const long long n = static_cast<long long>(sc.k) * sc.L * sc.channels;
     if (n == 0) return cudaSuccess;
     k_refresh_gb<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(sc.k, sc.L, sc.channels, st.culled.as<int>(),

@@ -40,6 +40,7 @@ struct Status {
     std::string msg;
 };
 int fail(int code, const std::string& msg);
+uint64_t next_version();  // process-wide, never 0
 int cuda_fail(cudaError_t e, const char* what);
 
 #define RXGS_CUDA(call)                                              \
@@ -120,6 +121,10 @@ struct rxgs_ctx_s {
     rxgs_b200::DevBuf row_pos, row_GB, row_S;
     // FLE GEMM operands / result for high l_max (k_fle_gemm.cu)
     rxgs_b200::DevBuf fle_a, fle_b, fle_m;
+    // version of the transmitter state whose receiver-independent row data
+    // (row_pos / row_GB / row_S and the GEMM's A operand) the buffers hold,
+    // so receiver chunks of one query batch gather and pack it once
+    uint64_t rows_version = 0, fle_a_version = 0;
     int sm_count = 148;
     int cond_kernel = 0;  // 0 auto (tcgen05 when eligible), 1 force SIMT
     int composite_kernel = 0;  // 0 auto (tcgen05 when eligible), 1 force SIMT
@@ -159,6 +164,8 @@ struct rxgs_txstate_s {
     // conditioned signal is ever read by the compositor.  needed_count is
     // device-side.
     int64_t needed_host = -1;
+    // changes whenever the state's per-Gaussian data does (build, refresh_gb)
+    uint64_t version = 0;
     // walked list entries regrouped by Gaussian (training adjoint), built lazily
     rxgs_b200::DevBuf gauss_off, gauss_ent;
     bool regrouped = false;
@@ -239,7 +246,8 @@ cudaError_t launch_tc_selftest(float* d_err, cudaStream_t s);
 // FLE reduction of the query path as a tensor-core GEMM: Mout[j][row] (k_fle_gemm.cu)
 int fle_gemm_kpad(int L);
 cudaError_t launch_fle_gemm(rxgs_ctx ctx, const int* n_rows_dev, long long rows_bound, int cap, int L, int n_rx,
-                            const float4* rGB, const float4* rS, const float* d_ag, float2* Mout, cudaStream_t s);
+                            const float4* rGB, const float4* rS, const float* d_ag, float2* Mout, cudaStream_t s,
+                            uint64_t a_version);
 cudaError_t launch_tc_selftest_mn(float* d_err, cudaStream_t s);
 // reduce_signals from materialised f64 coefficients.
 cudaError_t launch_reduce_signals(const rxgs_txstate_s& st, const double* d_coeffs, int n_rx,
