@@ -881,15 +881,7 @@ cudaError_t launch_cond_signal_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc,
     const int* n_rows = st.needed_count.as<int>();
     const int* rows = st.needed_order.as<int>();
     const long long bound = st.needed_host >= 0 ? st.needed_host : st.visible;
-    if (ctx->rows_version != st.version) {  // receiver-independent: once per state, not per receiver chunk
-        k_gather_rows<<<static_cast<unsigned>((bound + 255) / 256), 256, 0, s>>>(
-            n_rows, rows, cap, L, sc.d_pos32.as<float4>(), st.basis32.as<float2>(), st.gb32.as<float2>(),
-            ctx->row_pos.as<float4>(), ctx->row_GB.as<float4>(), ctx->row_S.as<float4>());
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        ctx->launches += 1;
-        ctx->rows_version = st.version;
-        ctx->fle_a_version = 0;
-    }
+    if ((e = gather_rows(sc, st, s)) != cudaSuccess) return e;
     // high l_max: the FLE reduction as one tensor-core GEMM instead of the per-row loop
 #ifndef RXGS_FLE_GEMM_MIN_L
 #define RXGS_FLE_GEMM_MIN_L 4  // A/B at L=9: GEMM 2.70 ms vs per-row loop 2.95 ms
@@ -904,6 +896,28 @@ cudaError_t launch_cond_signal_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc,
     }
     return launch_tc<false>(cs, n_rows, bound, cap, rows, ctx->row_pos.as<float4>(), d_rx, n_rx,
                             ctx->row_GB.as<float4>(), ctx->row_S.as<float4>(), d_ag, Mpre, d_sig, nullptr, s);
+}
+
+cudaError_t gather_rows(const rxgs_scene_s& sc, const rxgs_txstate_s& st, cudaStream_t s) {
+    rxgs_ctx ctx = sc.ctx;
+    const int cap = st.k, L = st.L;
+    cudaError_t e;
+    if ((e = ctx->row_pos.ensure(sizeof(float4) * cap)) != cudaSuccess) return e;
+    if ((e = ctx->row_GB.ensure(sizeof(float4) * cap * L)) != cudaSuccess) return e;
+    if ((e = ctx->row_S.ensure(sizeof(float4) * cap)) != cudaSuccess) return e;
+    if (ctx->rows_version == st.version) return cudaSuccess;  // receiver-independent: once per state version
+    const long long bound = st.needed_host >= 0 ? st.needed_host : st.visible;
+    if (bound > 0) {
+        k_gather_rows<<<static_cast<unsigned>((bound + 255) / 256), 256, 0, s>>>(
+            st.needed_count.as<int>(), st.needed_order.as<int>(), cap, L, sc.d_pos32.as<float4>(),
+            st.basis32.as<float2>(), st.gb32.as<float2>(), ctx->row_pos.as<float4>(), ctx->row_GB.as<float4>(),
+            ctx->row_S.as<float4>());
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        ctx->launches += 1;
+    }
+    ctx->rows_version = st.version;
+    ctx->fle_a_version = 0;
+    return cudaSuccess;
 }
 
 cudaError_t launch_local_cache_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const double* d_rx, int n_rx,

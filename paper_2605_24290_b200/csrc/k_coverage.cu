@@ -144,7 +144,50 @@ __global__ void __launch_bounds__(kCovThreads, 3) k_cov_signal(CondDev c, const 
     }
 }
 
+// s = (1 + aL) M + bL Bs from the FLE GEMM's M[row][j]: one thread per (row,
+// receiver), receivers fastest -- coalesced y, M and signal streams.
+__global__ void __launch_bounds__(256) k_cov_affine(CondDev c, const int* __restrict__ n_rows,
+                                                    const int* __restrict__ rows, int n_rx,
+                                                    const float2* __restrict__ M, const float4* __restrict__ rS,
+                                                    const float4* __restrict__ ycache, SigOut sig) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= static_cast<long long>(*n_rows) * n_rx) return;
+    const int r = static_cast<int>(i / n_rx), j = static_cast<int>(i % n_rx);
+    const int k = rows[r];
+    const float2 m = M[i];
+    const float4 sm = rS[r];
+    const float4 y = ycache ? ycache[static_cast<size_t>(k) * n_rx + j] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float ar = c.additive ? 0.f : y.x, ai = c.additive ? 0.f : y.y;
+    float2 sg = x2::fma(x2::bc(ar), m, m);
+    sg = x2::fma(make_float2(-m.y, m.x), x2::bc(ai), sg);
+    sg = x2::fma(x2::bc(y.z), make_float2(sm.z, sm.w), sg);
+    sg = x2::fma(make_float2(-sm.w, sm.z), x2::bc(y.w), sg);
+    store_sig(sig, k, n_rx, j, 1, 0, sg);
+}
+
 }  // namespace
+
+cudaError_t launch_cov_signal_gemm(const rxgs_cond_s* cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st, int n_rx,
+                                   const float* d_ag, const float4* ycache, SigOut d_sig, cudaStream_t s) {
+    const long long bound = st.needed_host >= 0 ? st.needed_host : st.visible;
+    if (bound == 0 || n_rx == 0) return cudaSuccess;
+    rxgs_ctx ctx = sc.ctx;
+    cudaError_t e;
+    if ((e = gather_rows(sc, st, s)) != cudaSuccess) return e;
+    if ((e = ctx->fle_m.ensure(sizeof(float2) * static_cast<size_t>(st.k) * n_rx)) != cudaSuccess) return e;
+    if ((e = launch_fle_gemm(ctx, st.needed_count.as<int>(), bound, st.k, st.L, n_rx, ctx->row_GB.as<float4>(),
+                             ctx->row_S.as<float4>(), d_ag, ctx->fle_m.as<float2>(), s, st.version, true)) != cudaSuccess)
+        return e;
+    CondDev d{};
+    if (cs) d = make_dev(*cs);
+    const long long n = bound * n_rx;
+    k_cov_affine<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(d, st.needed_count.as<int>(),
+                                                                      st.needed_order.as<int>(), n_rx,
+                                                                      ctx->fle_m.as<float2>(), ctx->row_S.as<float4>(),
+                                                                      ycache, d_sig);
+    ctx->launches += 1;
+    return cudaGetLastError();
+}
 
 cudaError_t launch_local_cache(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const double* d_rx, int n_rx,
                                float4* ycache, cudaStream_t s) {

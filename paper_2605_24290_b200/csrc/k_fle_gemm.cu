@@ -9,7 +9,8 @@
 //   A[r][4l + (0..3)]    = (Re GB_rl, Im GB_rl, Re B_rl, Im B_rl)
 //   Bm[2j][4l + (0..3)]   = (Re aG, -Im aG, Re bG, -Im bG)_jl   -> Re M
 //   Bm[2j+1][4l + (0..3)] = (Im aG,  Re aG, Im bG,  Re bG)_jl   -> Im M
-// then M = D + sum_l GB_rl, written [j][row] for k_cond_tc's coalesced read.
+// then M = D + sum_l GB_rl, written [j][row] for k_cond_tc's coalesced read
+// (or [row][j] for the coverage signal kernel).
 // tcgen05: 128 rows x 256 columns (128 receivers, re/im) per CTA, K in
 // steps of 16 staged by cp.async into the no-swizzle K-major canonical
 // layout, three shared-memory stages, bf16x3 (Ahi Bhi + Ahi Blo + Alo Bhi,
@@ -79,7 +80,8 @@ __global__ void k_fle_pack_b(int n_rx, int L, int Kp, const float4* __restrict__
 __global__ void __launch_bounds__(kThr) k_fle_gemm(const int* __restrict__ n_rows_dev, int cap, int n_rx, int Kp,
                                                    const uint16_t* __restrict__ a_hi, const uint16_t* __restrict__ a_lo,
                                                    const uint16_t* __restrict__ b_hi, const uint16_t* __restrict__ b_lo,
-                                                   const float4* __restrict__ rS, float2* __restrict__ Mout) {
+                                                   const float4* __restrict__ rS, float2* __restrict__ Mout,
+                                                   int row_major) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t bars[kStages];
     __shared__ uint32_t tbase_s;
@@ -185,7 +187,7 @@ __global__ void __launch_bounds__(kThr) k_fle_gemm(const int* __restrict__ n_row
         for (int q = 0; q < 8; ++q) {
             const int j = j0 + 8 * ch + q;
             if (rok && j < n_rx)
-                Mout[static_cast<size_t>(j) * cap + r] =
+                Mout[row_major ? static_cast<size_t>(r) * n_rx + j : static_cast<size_t>(j) * cap + r] =
                     make_float2(__uint_as_float(v[2 * q]) + gs.x, __uint_as_float(v[2 * q + 1]) + gs.y);
         }
     }
@@ -200,7 +202,7 @@ int fle_gemm_kpad(int L) { return (4 * L + kTK - 1) / kTK * kTK; }
 
 cudaError_t launch_fle_gemm(rxgs_ctx ctx, const int* n_rows_dev, long long rows_bound, int cap, int L, int n_rx,
                             const float4* rGB, const float4* rS, const float* d_ag, float2* Mout, cudaStream_t s,
-                            uint64_t a_version) {
+                            uint64_t a_version, bool row_major) {
     if (rows_bound == 0 || n_rx == 0) return cudaSuccess;
     const int Kp = fle_gemm_kpad(L);
     cudaError_t e;
@@ -222,7 +224,7 @@ cudaError_t launch_fle_gemm(rxgs_ctx ctx, const int* n_rows_dev, long long rows_
         cudaSuccess)
         return e;
     dim3 grid(static_cast<unsigned>((rows_bound + kTM - 1) / kTM), (2 * n_rx + kTN - 1) / kTN);
-    k_fle_gemm<<<grid, kThr, smem, s>>>(n_rows_dev, cap, n_rx, Kp, a_hi, a_lo, b_hi, b_lo, rS, Mout);
+    k_fle_gemm<<<grid, kThr, smem, s>>>(n_rows_dev, cap, n_rx, Kp, a_hi, a_lo, b_hi, b_lo, rS, Mout, row_major ? 1 : 0);
     ctx->launches += 3;
     return cudaGetLastError();
 }

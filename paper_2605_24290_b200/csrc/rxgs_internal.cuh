@@ -247,7 +247,9 @@ cudaError_t launch_tc_selftest(float* d_err, cudaStream_t s);
 int fle_gemm_kpad(int L);
 cudaError_t launch_fle_gemm(rxgs_ctx ctx, const int* n_rows_dev, long long rows_bound, int cap, int L, int n_rx,
                             const float4* rGB, const float4* rS, const float* d_ag, float2* Mout, cudaStream_t s,
-                            uint64_t a_version);
+                            uint64_t a_version, bool row_major = false);
+// Per-row Tx data of the needed rows into ctx->row_* (k_cond_tc.cu), once per state version.
+cudaError_t gather_rows(const rxgs_scene_s& sc, const rxgs_txstate_s& st, cudaStream_t s);
 cudaError_t launch_tc_selftest_mn(float* d_err, cudaStream_t s);
 // reduce_signals from materialised f64 coefficients.
 cudaError_t launch_reduce_signals(const rxgs_txstate_s& st, const double* d_coeffs, int n_rx,
@@ -286,6 +288,9 @@ cudaError_t launch_local_cache(const rxgs_cond_s& cs, const rxgs_scene_s& sc, co
 cudaError_t launch_ag_transpose(int n_rx, int L, const float* d_ag, float* d_agT, cudaStream_t s);
 cudaError_t launch_cov_signal(const rxgs_cond_s* cs, const rxgs_txstate_s& st, int n_rx, const float* d_agT,
                               const float4* ycache, SigOut d_sig, cudaStream_t s);
+// the same signals from the FLE GEMM's M[row][j] (k_coverage.cu)
+cudaError_t launch_cov_signal_gemm(const rxgs_cond_s* cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st, int n_rx,
+                                   const float* d_ag, const float4* ycache, SigOut d_sig, cudaStream_t s);
 // ---- k_cond_bwd.cu (FP64 materialised conditioning adjoint)
 size_t cond_backward_ws_bytes(const rxgs_cond_s& cs, int K, int sms);
 cudaError_t launch_cond_backward(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const double* d_rx,

@@ -286,12 +286,13 @@ def test_tcgen05_composite_matches_simt_and_oracle(ctx, capi, orc):
         assert rel_err(s_tc[j], want).max() < TOL
 
 
-@pytest.mark.parametrize("mode,hidden", [("full", 64), ("full", 32), ("additive_only", 64), ("global_only", 64),
-                                         (None, 64)])
-def test_coverage_table_matches_oracle_predict(ctx, capi, orc, mode, hidden):
-    """Config-3 path: Tx-independent conditioning cached once, reused per Tx."""
+@pytest.mark.parametrize("mode,hidden,l_max", [("full", 64, 2), ("full", 32, 2), ("additive_only", 64, 2),
+                                               ("global_only", 64, 2), (None, 64, 2), ("full", 64, 4)])
+def test_coverage_table_matches_oracle_predict(ctx, capi, orc, mode, hidden, l_max):
+    """Config-3 path: Tx-independent conditioning cached once, reused per Tx
+    (l_max 4: the FLE-GEMM signal path)."""
     import oracle as O
-    sc = capi.synth_scene(2500, 2, 1, 7)
+    sc = capi.synth_scene(2500, l_max, 1, 7)
     grid, og = capi.Grid(18, 36, 6, 1.0), O.Grid(18, 36, 6, 1.0)
     if mode is None:
         scene, cond = ctx.scene(sc, "rssi"), None
