@@ -28,8 +28,11 @@
 namespace rxgs_b200 {
 namespace {
 
-constexpr int kChunk = 64;
-constexpr int kWalkThreads = 256;
+#ifndef RXGS_WALK_CHUNK
+#define RXGS_WALK_CHUNK 128  // A/B: 128 > 64 > 32 (config-3 walk 17.5 / 18.6 / 21.1 ms)
+#endif
+constexpr int kChunk = RXGS_WALK_CHUNK;
+constexpr int kWalkThreads = 512;
 constexpr int kLanesPerCell = kWalkThreads / kMaxCellsPerBlock;  // 4
 
 __device__ __forceinline__ double wrap_pm_pi(double a) {  // linalg.hpp:152-157
@@ -46,8 +49,9 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(DevGrid g, const int64_t*
                                                        const GaussRec* __restrict__ rec, float* __restrict__ tw,
                                                        int* __restrict__ walk_len, double* __restrict__ cell_T,
                                                        int* __restrict__ cell_len) {
-    __shared__ GaussRec srec[kChunk];
-    __shared__ double sw[kChunk][kMaxCellsPerBlock];
+    extern __shared__ __align__(16) uint8_t walk_smem[];
+    GaussRec* srec = reinterpret_cast<GaussRec*>(walk_smem);
+    double(*sw)[kMaxCellsPerBlock] = reinterpret_cast<double(*)[kMaxCellsPerBlock]>(walk_smem + sizeof(GaussRec) * kChunk);
     __shared__ int s_alive[kMaxCellsPerBlock];
     __shared__ int s_len[kMaxCellsPerBlock];
     __shared__ int s_max, s_min;
@@ -79,7 +83,7 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(DevGrid g, const int64_t*
     for (int c0 = 0; c0 < n; c0 += kChunk) {
         if (!__syncthreads_or(alive)) break;
         const int m = min(kChunk, n - c0);
-        if (tid < m) srec[tid] = rec[list[begin + c0 + tid]];
+        for (int q = tid; q < m; q += kWalkThreads) srec[q] = rec[list[begin + c0 + q]];
         __syncthreads();
         if (s_alive[cl]) {  // phase A: weights (gaussian_weight, sphraster.cpp:239-251)
             for (int e = tid / kMaxCellsPerBlock; e < m; e += kLanesPerCell) {
@@ -130,7 +134,9 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(DevGrid g, const int64_t*
 cudaError_t launch_walk(rxgs_txstate_s& st, cudaStream_t s) {
     const DevGrid& g = st.grid;
     dim3 grid(g.n_tiles, g.cell_blocks);
-    k_walk<<<grid, kWalkThreads, 0, s>>>(g, st.tile_offsets.as<int64_t>(), st.list.as<int>(),
+    const size_t smem = sizeof(GaussRec) * kChunk + sizeof(double) * kChunk * kMaxCellsPerBlock;
+    cudaFuncSetAttribute(k_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_walk<<<grid, kWalkThreads, smem, s>>>(g, st.tile_offsets.as<int64_t>(), st.list.as<int>(),
                                st.rec.as<GaussRec>(), st.tw.as<float>(), st.walk_len.as<int>(),
                                st.cell_T.as<double>(), st.cell_len.as<int>());
     return cudaGetLastError();
