@@ -55,7 +55,8 @@ __device__ __forceinline__ double normalization(int l, int am) {  // radiance.cp
     return sqrt((2.0 * l + 1.0) / (4.0 * kPi) * ratio);
 }
 
-__global__ void k_tx_prep(int K, int l_max, int C, const double* __restrict__ pos,
+template <int LMT>  // LMT > 0: l_max known at compile time (tables in registers)
+__global__ void k_tx_prep(int K, int l_max_rt, int C, const double* __restrict__ pos,
                           const double* __restrict__ ls, const double* __restrict__ q,
                           const double* __restrict__ tau_logit,
                           const double* __restrict__ coeffs64, double tx0, double tx1, double tx2,
@@ -66,6 +67,7 @@ __global__ void k_tx_prep(int K, int l_max, int C, const double* __restrict__ po
                           int* __restrict__ tile_count) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= K) return;
+    const int l_max = LMT > 0 ? LMT : l_max_rt;
     const int L = (l_max + 1) * (l_max + 1);
     double* gm = geom + 12 * static_cast<size_t>(k);
     for (int i = 0; i < 12; ++i) gm[i] = 0.0;
@@ -162,26 +164,38 @@ __global__ void k_tx_prep(int K, int l_max, int C, const double* __restrict__ po
     }
     // legendre_table (radiance.cpp:16-37) on x = cos(theta), without the
     // Condon-Shortley phase; entries packed l*(l+1)/2 + m.
-    double P[(kMaxLmax + 1) * (kMaxLmax + 2) / 2];
+    constexpr int LM = LMT > 0 ? LMT : kMaxLmax;  // array bound
+    const int LB = LMT > 0 ? LMT : l_max;         // loop bound (constant when specialised)
+    double P[(LM + 1) * (LM + 2) / 2];
     double x = cos(theta);
     x = x < -1.0 ? -1.0 : (x > 1.0 ? 1.0 : x);
     const double s = sqrt(dmax(0.0, (1.0 - x) * (1.0 + x)));
 #define AT(l, m) P[(l) * ((l) + 1) / 2 + (m)]
     AT(0, 0) = 1.0;
-    for (int m = 1; m <= l_max; ++m) AT(m, m) = AT(m - 1, m - 1) * (2.0 * m - 1.0) * s;
-    for (int m = 0; m < l_max; ++m) AT(m + 1, m) = x * (2.0 * m + 1.0) * AT(m, m);
-    for (int m = 0; m <= l_max; ++m)
-        for (int l = m + 2; l <= l_max; ++l)
+#pragma unroll
+    for (int m = 1; m <= LB; ++m) AT(m, m) = AT(m - 1, m - 1) * (2.0 * m - 1.0) * s;
+#pragma unroll
+    for (int m = 0; m < LB; ++m) AT(m + 1, m) = x * (2.0 * m + 1.0) * AT(m, m);
+#pragma unroll
+    for (int m = 0; m <= LB; ++m)
+#pragma unroll
+        for (int l = m + 2; l <= LB; ++l)
             AT(l, m) = (x * (2.0 * l - 1.0) * AT(l - 1, m) - (l + m - 1.0) * AT(l - 2, m)) /
                        static_cast<double>(l - m);
-    for (int l = 0; l <= l_max; ++l)
+    // cos(m phi), sin(m phi) once per distinct m (eval_basis evaluates them
+    // per (l, m); the same argument m * phi gives the same values)
+    double cm[2 * LM + 1], sn[2 * LM + 1];
+#pragma unroll
+    for (int m = -LB; m <= LB; ++m) sincos(m * phi, &sn[m + LM], &cm[m + LM]);
+#pragma unroll
+    for (int l = 0; l <= LB; ++l) {
+#pragma unroll
         for (int m = -l; m <= l; ++m) {
             const int am = m < 0 ? -m : m;
             const double np = normalization(l, am) * AT(l, am);
             const int idx = l * l + m + l;
-            const double br = np * cos(m * phi), bi = np * sin(m * phi);
-            b64[2 * idx] = br;
-            b64[2 * idx + 1] = bi;
+            const double br = np * cm[m + LM], bi = np * sn[m + LM];
+            reinterpret_cast<double2*>(b64)[idx] = make_double2(br, bi);
             b32[idx] = make_float2(static_cast<float>(br), static_cast<float>(bi));
             for (int c = 0; c < C; ++c) {
                 const double a_ = cb[(idx * C + c) * 2], b_ = cb[(idx * C + c) * 2 + 1];
@@ -189,6 +203,7 @@ __global__ void k_tx_prep(int K, int l_max, int C, const double* __restrict__ po
                                                static_cast<float>(a_ * bi + b_ * br));
             }
         }
+    }
 #undef AT
 }
 
@@ -255,7 +270,8 @@ cudaError_t launch_tx_prep(const rxgs_scene_s& sc, rxgs_txstate_s& st, cudaStrea
     if (sc.k == 0) return cudaSuccess;
     const int threads = 128;
     const int blocks = (sc.k + threads - 1) / threads;
-    k_tx_prep<<<blocks, threads, 0, s>>>(
+    auto kern = sc.l_max == 2 ? k_tx_prep<2> : (sc.l_max == 9 ? k_tx_prep<9> : k_tx_prep<0>);
+    kern<<<blocks, threads, 0, s>>>(
         sc.k, sc.l_max, sc.channels, sc.d_pos.as<double>(), sc.d_ls.as<double>(),
         sc.d_q.as<double>(), sc.d_tau.as<double>(), sc.d_coeffs64.as<double>(), st.tx[0], st.tx[1],
         st.tx[2], st.grid, st.rec.as<GaussRec>(), st.culled.as<int>(), st.geom.as<double>(),
