@@ -259,6 +259,70 @@ inline std::vector<Measurement> aggregate_modality(const RenderedField& field, M
     return ms;
 }
 
+// sphraster.hpp:110-113: upstream Measurements (forward shapes) -> d field values
+inline std::vector<double> aggregate_modality_backward(const RenderedField& field, Modality modality,
+                                                       const SphericalGrid& grid,
+                                                       const std::vector<Measurement>& upstream) {
+    if (upstream.size() != static_cast<std::size_t>(field.n_rx))
+        throw std::invalid_argument("aggregate_modality_backward: upstream count mismatch");
+    const rxgs_grid g = grid.c();
+    const int m = static_cast<int>(modality);
+    std::vector<double> up;
+    for (const Measurement& u : upstream) {
+        if (m == 0) {
+            up.push_back(u.scalar);
+        } else if (m == 1) {
+            for (int c = 0; c < field.channels; ++c) {
+                const cplx v = c < static_cast<int>(u.csi.size()) ? u.csi[c] : cplx{0, 0};
+                up.push_back(v.real());
+                up.push_back(v.imag());
+            }
+        } else {
+            if (u.image.size() != field.plane())
+                throw std::invalid_argument("aggregate_modality_backward: image size mismatch");
+            up.insert(up.end(), u.image.begin(), u.image.end());
+        }
+    }
+    std::vector<double> dv(field.values.size());
+    detail::check(rxgs_aggregate_modality_backward(detail::ctx(), &g, m, field.n_rx, field.channels,
+                                                   field.values.data(), up.empty() ? nullptr : up.data(),
+                                                   dv.data()));
+    return dv;
+}
+
+struct GradientBundle {  // sphraster.hpp:118-128
+    std::vector<double> d_positions, d_log_scales, d_quaternions, d_tau_logits, d_coeffs;
+    void resize(int k, int n_rx, std::size_t coeff_stride) {
+        d_positions.assign(3 * static_cast<std::size_t>(k), 0.0);
+        d_log_scales.assign(3 * static_cast<std::size_t>(k), 0.0);
+        d_quaternions.assign(4 * static_cast<std::size_t>(k), 0.0);
+        d_tau_logits.assign(k, 0.0);
+        d_coeffs.assign(static_cast<std::size_t>(n_rx) * k * coeff_stride, 0.0);
+    }
+    void add(const GradientBundle& o) {
+        auto acc = [](std::vector<double>& a, const std::vector<double>& b) {
+            for (std::size_t i = 0; i < a.size() && i < b.size(); ++i) a[i] += b[i];
+        };
+        acc(d_positions, o.d_positions);
+        acc(d_log_scales, o.d_log_scales);
+        acc(d_quaternions, o.d_quaternions);
+        acc(d_tau_logits, o.d_tau_logits);
+        acc(d_coeffs, o.d_coeffs);
+    }
+};
+
+// sphraster.hpp:130-133: exact adjoint of render_field (FP64, on the B200)
+inline GradientBundle backward_render(const TxState& st, const GaussianScene& scene, const std::vector<double>& coeffs,
+                                      int n_rx, const std::vector<double>& d_values, int /*threads*/ = 1) {
+    GradientBundle b;
+    b.resize(scene.count(), n_rx, scene.coeff_stride());
+    auto sh = detail::upload(scene);
+    detail::check(rxgs_backward_render(detail::ctx(), st.device->h, sh->h, coeffs.empty() ? nullptr : coeffs.data(),
+                                       n_rx, d_values.data(), b.d_positions.data(), b.d_log_scales.data(),
+                                       b.d_quaternions.data(), b.d_tau_logits.data(), b.d_coeffs.data()));
+    return b;
+}
+
 }  // namespace raster
 
 namespace cond {
@@ -362,9 +426,85 @@ inline std::vector<double> condition_batch(const ConditioningState& state, const
     return out;
 }
 
+// conditioning.hpp:97-110.  The B200 adjoint recomputes the MLP activations on
+// the device, so only rx and local_in are materialised; scene keeps the
+// uploaded scene for condition_backward.
+struct ConditionWorkspace {
+    Vec3 rx;
+    std::vector<double> gamma, global_in, global_h1, global_h2, global_out, mid;
+    std::vector<double> local_in, local_h1, local_h2, local_out;
+    std::shared_ptr<api::detail::SceneHandle> scene;
+};
+
 inline std::vector<double> condition_forward(const ConditioningState& state, const std::vector<double>& base,
-                                             const GaussianScene& scene, const Vec3& rx) {
-    return condition_batch(state, base, scene, {rx});
+                                             const GaussianScene& scene, const Vec3& rx,
+                                             ConditionWorkspace* workspace = nullptr) {
+    if (!workspace) return condition_batch(state, base, scene, {rx});
+    if (base.size() != static_cast<std::size_t>(scene.count()) * scene.coeff_stride())
+        throw std::invalid_argument("condition_forward: base coefficient size mismatch");
+    GaussianScene s2 = scene;
+    s2.fle_coeffs = base;
+    workspace->scene = api::detail::upload(s2);
+    workspace->rx = rx;
+    workspace->local_in.assign(6 * static_cast<std::size_t>(scene.count()), 0.0);
+    auto ch = detail_c::upload(state);
+    std::vector<double> out(base.size());
+    const double r[3] = {rx.x, rx.y, rx.z};
+    api::detail::check(rxgs_condition_forward(api::detail::ctx(), ch->h, workspace->scene->h, r, out.data(),
+                                              workspace->local_in.data()));
+    if (state.config.mode != ConditioningMode::LocalOnly) state.global_calls += scene.n_components();
+    if (state.config.mode != ConditioningMode::GlobalOnly) state.local_calls += scene.count();
+    return out;
+}
+
+struct MlpGrads {  // conditioning.hpp:113-118
+    std::vector<double> w1, b1, w2, b2, w3, b3;
+    void resize(const Mlp& m) {
+        w1.assign(m.l1.w.size(), 0.0); b1.assign(m.l1.b.size(), 0.0);
+        w2.assign(m.l2.w.size(), 0.0); b2.assign(m.l2.b.size(), 0.0);
+        w3.assign(m.l3.w.size(), 0.0); b3.assign(m.l3.b.size(), 0.0);
+    }
+};
+struct ConditioningGrads {  // conditioning.hpp:120-128
+    std::vector<double> d_freqs;
+    MlpGrads d_global;
+    std::vector<double> d_embed;
+    MlpGrads d_local;
+    void resize(const ConditioningState& s) {
+        d_freqs.assign(s.fourier_freqs.size(), 0.0);
+        d_global.resize(s.global_mlp);
+        d_embed.assign(s.component_embed.size(), 0.0);
+        d_local.resize(s.local_mlp);
+    }
+};
+
+// conditioning.hpp:131-133: accumulates into d_base and grads (the packed
+// parameter order of rxgs_cond_create)
+inline void condition_backward(const ConditioningState& state, const ConditionWorkspace& ws,
+                               const std::vector<double>& base, const std::vector<double>& d_out,
+                               std::vector<double>& d_base, ConditioningGrads& grads) {
+    if (!ws.scene) throw std::invalid_argument("condition_backward: workspace not filled by condition_forward");
+    if (d_out.size() != base.size() || d_base.size() != base.size())
+        throw std::invalid_argument("condition_backward: gradient size mismatch");
+    auto ch = detail_c::upload(state);
+    std::vector<double> db(base.size()), dp(static_cast<std::size_t>(rxgs_cond_param_count(ch->h)));
+    const double r[3] = {ws.rx.x, ws.rx.y, ws.rx.z};
+    api::detail::check(rxgs_condition_backward(api::detail::ctx(), ch->h, ws.scene->h, r, d_out.data(), db.data(),
+                                               dp.data()));
+    for (std::size_t i = 0; i < db.size(); ++i) d_base[i] += db[i];
+    if (grads.d_freqs.empty()) grads.resize(state);
+    std::size_t o = 0;
+    auto take = [&](std::vector<double>& v) {
+        for (double& x : v) x += dp[o++];
+    };
+    take(grads.d_freqs);
+    for (auto* v : {&grads.d_global.w1, &grads.d_global.b1, &grads.d_global.w2, &grads.d_global.b2,
+                    &grads.d_global.w3, &grads.d_global.b3})
+        take(*v);
+    take(grads.d_embed);
+    for (auto* v : {&grads.d_local.w1, &grads.d_local.b1, &grads.d_local.w2, &grads.d_local.b2,
+                    &grads.d_local.w3, &grads.d_local.b3})
+        take(*v);
 }
 
 }  // namespace cond

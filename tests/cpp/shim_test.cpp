@@ -12,6 +12,9 @@
 using namespace rxgs;
 using namespace rxgs::raster;
 
+#ifndef RXGS_SHIM_TS
+#define RXGS_SHIM_TS 4
+#endif
 static int g_fail = 0, g_checks = 0;
 #define CHECK(x)                                                            \
     do {                                                                    \
@@ -179,6 +182,79 @@ int main() {
             io_threw = std::string(e.what()).find("load_checkpoint: cannot open") != std::string::npos;
         }
         CHECK(io_threw);
+    }
+    {  // adjoints through the shim (test_sphraster_grad.cpp:116-250 style): FD of
+       // L = sum(spectrum) w.r.t. a tau logit, a position and a coefficient
+        GaussianScene s = random_scene(11, 25, 1, 1);
+        s.modality = Modality::Spectrum;
+        SphericalGrid g;
+        g.n_theta = 12;
+        g.n_phi = 24;
+        g.tile_size = RXGS_SHIM_TS;
+        g.radius = 0.25;
+        const Vec3 tx{0.2, -0.1, 0.05};
+        auto loss = [&](const GaussianScene& sc) {
+            const auto f = render_field(sc, tx, g, sc.fle_coeffs, 1);
+            const auto m = aggregate_modality(f, Modality::Spectrum, g)[0];
+            double a = 0;
+            for (double v : m.image) a += v;
+            return a;
+        };
+        const auto st = build_tx_state(s, tx, g);
+        const auto f = render_field(st, s, s.fle_coeffs, 1);
+        Measurement up;
+        up.modality = Modality::Spectrum;
+        up.image.assign(f.plane(), 1.0);
+        const auto dv = aggregate_modality_backward(f, Modality::Spectrum, g, {up});
+        const auto gb = backward_render(st, s, s.fle_coeffs, 1, dv);
+        // the B200 render carries signals in FP32, so the FD step is 1e-3
+        // (FP32 quantisation of a 1e-6 step alone is ~10%)
+        const double h = 1e-3;
+        int k = 0;
+        while (k < s.count() && st.proj[k].culled) ++k;
+        {
+            GaussianScene p = s, m = s;
+            p.tau_logits[k] += h;
+            m.tau_logits[k] -= h;
+            CHECK(rel_err((loss(p) - loss(m)) / (2 * h), gb.d_tau_logits[k]) < 2e-3);
+        }
+        {
+            GaussianScene p = s, m = s;
+            p.fle_coeffs[k * s.coeff_stride() + 2] += h;
+            m.fle_coeffs[k * s.coeff_stride() + 2] -= h;
+            CHECK(rel_err((loss(p) - loss(m)) / (2 * h), gb.d_coeffs[k * s.coeff_stride() + 2]) < 2e-3);
+        }
+        // condition_backward: FD of sum(out * w) w.r.t. a base coefficient
+        cond::ConditioningState cs;
+        cs.config.fourier_bands = 2; cs.config.hidden = 8; cs.config.embed_dim = 3; cs.config.probe_samples = 4;
+        cs.l_max = 1; cs.channels = 1;
+        cs.fourier_freqs.assign(6, 0.7);
+        auto layer = [](int in, int out, double v) { cond::MlpLayer l; l.in = in; l.out = out; l.w.assign(in * out, v); l.b.assign(out, 0.05); return l; };
+        cs.global_mlp = {layer(6 * 2 + 2 + 3, 8, 0.04), layer(8, 8, -0.03), layer(8, 4, 0.02)};
+        cs.component_embed.assign(4 * 3, 0.01);
+        cs.local_mlp = {layer(6, 8, 0.05), layer(8, 8, 0.04), layer(8, 4, -0.03)};
+        cs.occupancy = cond::build_occupancy(s, 8, {{-4, -4, -4}, {4, 4, 4}});
+        const Vec3 rx{0.3, 0.2, -0.9};
+        cond::ConditionWorkspace ws;
+        const auto out = cond::condition_forward(cs, s.fle_coeffs, s, rx, &ws);
+        CHECK(ws.local_in.size() == 6 * static_cast<std::size_t>(s.count()));
+        std::vector<double> w(out.size());
+        for (std::size_t i = 0; i < w.size(); ++i) w[i] = std::sin(0.37 * i);
+        std::vector<double> d_base(out.size(), 0.0);
+        cond::ConditioningGrads grads;
+        cond::condition_backward(cs, ws, s.fle_coeffs, w, d_base, grads);
+        auto obj = [&](const std::vector<double>& base) {
+            const auto o = cond::condition_forward(cs, base, s, rx);
+            double a = 0;
+            for (std::size_t i = 0; i < o.size(); ++i) a += o[i] * w[i];
+            return a;
+        };
+        std::vector<double> bp = s.fle_coeffs, bm = s.fle_coeffs;
+        const double hc = 1e-6;  // the materialised conditioning path is FP64
+        bp[5] += hc;
+        bm[5] -= hc;
+        CHECK(rel_err((obj(bp) - obj(bm)) / (2 * hc), d_base[5]) < 1e-4);
+        CHECK(grads.d_local.w2.size() == 64 && grads.d_global.b3.size() == 4);
     }
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail ? 1 : 0;
