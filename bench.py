@@ -357,12 +357,18 @@ def bench_train(args, capi, ctx, scene, cond, grid, stream, dev, rank, world):
     rx_d = torch.from_numpy(rx).to(dev)
     st = scene.tx_state(np.array(TX), grid)
 
-    def time_trainer(hyper):
-        tr = capi.Trainer(ctx, scene, cond, hyper)
+    def time_trainer(hyper, geometry=None):
+        sc_t, cond_t = scene, cond
+        if geometry:  # joint step: own copy of the model, its geometry moves every step
+            sc_t = ctx.scene(scene.data, "spectrum")
+            cond_t = _cond_for(capi, ctx, sc_t)
+        tr = capi.Trainer(ctx, sc_t, cond_t, hyper, geometry=geometry)
         gbuf = tr.grad_tensor()
 
         def step():
-            tr.grads(st, rx_d, targets)
+            # joint: build_tx_state every step from the current geometry (trainer.cpp:417-421)
+            st_s = sc_t.tx_state(np.array(TX), grid) if geometry else st
+            tr.grads(st_s, rx_d, targets)
             allreduce_grads(gbuf)  # NCCL over NVLink (no-op at world 1)
             tr.apply()
 
@@ -384,6 +390,7 @@ def bench_train(args, capi, ctx, scene, cond, grid, stream, dev, rank, world):
     hp = list(capi.Trainer.DEFAULTS)
     hp[3], hp[4] = 0.2, 0.1  # the reference's default LossWeights (trainer.hpp:25-29)
     ms_full, _ = time_trainer(hp)
+    ms_joint, n_joint = time_trainer(None, geometry=True)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:  # reference CPU training sample (oracle/_ref), one sample, all host threads in render/backward
@@ -412,6 +419,9 @@ def bench_train(args, capi, ctx, scene, cond, grid, stream, dev, rank, world):
             "ms_per_step": ms, "steps_per_s": 1e3 / ms, "samples_per_s": world * B * 1e3 / ms,
             "default_loss": {"lambda_ssim": 0.2, "lambda_fft": 0.1, "ms_per_step": ms_full,
                              "samples_per_s": world * B * 1e3 / ms_full},
+            "joint": {"what": "train_joint step: + build_tx_state per step, FP64 backward_render geometry "
+                              "gradients, degree mask, Adam on position/transmittance/scaling/rotation",
+                      "ms_per_step": ms_joint, "samples_per_s": world * B * 1e3 / ms_joint, "grad_floats": n_joint},
             "grad_floats": n_grad, "n_gpus": world, "cpu_reference": cpu}
 
 

@@ -284,11 +284,32 @@ int rxgs_train_grads(rxgs_trainer t, rxgs_txstate st, const double* rx, int n_rx
  * data-parallel all-reduce (sum) before rxgs_train_apply. */
 int rxgs_train_grad_buffer(rxgs_trainer t, double** dev_ptr, int64_t* n, int64_t* n_base);
 int rxgs_train_get_grads(rxgs_trainer t, double* d_base, double* d_params);
+/* In-place NCCL all-reduce (sum, ncclFloat64) of the flat gradient buffer
+ * on the trainer's stream, over the caller's communicator (an ncclComm_t
+ * passed as void*, one rank per GPU): the data-parallel exchange between
+ * rxgs_train_grads and rxgs_train_apply. NCCL is resolved
+ * at run time from the library the process already loaded. */
+int rxgs_train_allreduce(rxgs_trainer t, void* nccl_comm);
 /* Optimizer::step on "features" (degree >= 1 scaled by rest_lr_ratio) and
  * every conditioning group (diffengine.cpp:50-58): throws the reference's
  * "optimizer: non-finite gradient in group ..." error, else Adam in place on
  * the device copies of the scene coefficients and conditioning parameters. */
 int rxgs_train_apply(rxgs_trainer t);
+/* Joint training (train_joint / the train_geometry branch of
+ * conditioned_training_loop, trainer.cpp:417-463): call once before the
+ * first step.  The flat gradient buffer grows by the geometry gradients of
+ * backward_render, [d_positions 3K | d_tau_logits K | d_log_scales 3K |
+ * d_quaternions 4K], summed over the batch; rxgs_train_apply then applies
+ * the FLE degree mask (apply_degree_mask, trainer.cpp:233-248) and Adam on
+ * position (opt::lr_at schedule, diffengine.cpp:36-48), transmittance,
+ * scaling and rotation, and renormalises the quaternions
+ * (scene.cpp:281-288).  The caller rebuilds the TxState every step, as the
+ * reference does.  geo (NULL = TrainConfig defaults, trainer.hpp:78-92):
+ * {position lr_init, lr_final, total_steps, delay_mult, delay_steps,
+ *  transmittance_lr, scaling_lr, rotation_lr, fle_ramp_interval}. */
+int rxgs_trainer_enable_geometry(rxgs_trainer t, const double geo[9]);
+int rxgs_train_get_geometry_grads(rxgs_trainer t, double* d_positions, double* d_log_scales,
+                                  double* d_quaternions, double* d_tau_logits);
 int64_t rxgs_train_step_count(rxgs_trainer t);
 /* Current (possibly trained) device parameters. */
 int rxgs_scene_get_coeffs(rxgs_scene scene, double* out);

@@ -113,6 +113,9 @@ _SIG = {
     "rxgs_train_grads": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp, _vp, C.c_int]),
     "rxgs_train_grad_buffer": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_i64), C.POINTER(_i64)]),
     "rxgs_train_get_grads": (C.c_int, [_vp, _vp, _vp]),
+    "rxgs_train_allreduce": (C.c_int, [_vp, _vp]),
+    "rxgs_trainer_enable_geometry": (C.c_int, [_vp, _vp]),
+    "rxgs_train_get_geometry_grads": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "rxgs_train_apply": (C.c_int, [_vp]),
     "rxgs_train_step_count": (_i64, [_vp]),
     "rxgs_scene_get_coeffs": (C.c_int, [_vp, _vp]),
@@ -573,12 +576,23 @@ class Trainer:
 
     DEFAULTS = (5e-3, 0.2, 1e-3, 0.0, 0.0, 0.9, 0.999, 1e-8)
 
-    def __init__(self, ctx: Context, scene: Scene, cond: Cond, hyper=None):
+    # TrainConfig geometry defaults (trainer.hpp:78-92): position lr schedule
+    # (lr_init, lr_final, total_steps, delay_mult, delay_steps), transmittance,
+    # scaling, rotation lr, fle_ramp_interval
+    GEOMETRY_DEFAULTS = (1.6e-4, 1.6e-6, 2000, 0.01, 200, 1e-2, 5e-3, 1e-3, 500)
+
+    def __init__(self, ctx: Context, scene: Scene, cond: Cond, hyper=None, geometry=None):
+        """geometry: None (Stage II, geometry frozen), True (joint with the
+        TrainConfig defaults) or a 9-tuple like GEOMETRY_DEFAULTS."""
         self.ctx, self.scene, self.cond = ctx, scene, cond
         hp = np.asarray(hyper if hyper is not None else self.DEFAULTS, np.float64)
         h = _vp()
         _check(_lib.rxgs_trainer_create(ctx.h, scene.h, cond.h, hp.ctypes.data, C.byref(h)))
         self.h = h
+        self.geometry = geometry is not None and geometry is not False
+        if self.geometry:
+            geo = np.asarray(self.GEOMETRY_DEFAULTS if geometry is True else geometry, np.float64)
+            _check(_lib.rxgs_trainer_enable_geometry(self.h, geo.ctypes.data))
         p, n, nb = _vp(), _i64(), _i64()
         _check(_lib.rxgs_train_grad_buffer(self.h, C.byref(p), C.byref(n), C.byref(nb)))
         self.grad_ptr, self.n, self.n_base = p.value, n.value, nb.value
@@ -604,9 +618,21 @@ class Trainer:
 
     def get_grads(self):
         db = np.empty(self.n_base)
-        dp = np.empty(self.n - self.n_base)
+        dp = np.empty(self.cond.param_count)
         _check(_lib.rxgs_train_get_grads(self.h, db.ctypes.data, dp.ctypes.data))
         return db, dp
+
+    def get_geometry_grads(self):
+        """(d_positions K*3, d_log_scales K*3, d_quaternions K*4, d_tau_logits K)."""
+        k = self.scene.k
+        out = [np.empty(3 * k), np.empty(3 * k), np.empty(4 * k), np.empty(k)]
+        _check(_lib.rxgs_train_get_geometry_grads(self.h, *[o.ctypes.data for o in out]))
+        return tuple(out)
+
+    def allreduce(self, nccl_comm: int):
+        """Sum the gradient buffer over the ranks of an ncclComm_t (an integer
+        handle: dist.nccl_comm_ptr(), or one made with ncclCommInitRank)."""
+        _check(_lib.rxgs_train_allreduce(self.h, C.c_void_p(int(nccl_comm))))
 
     def apply(self):
         _check(_lib.rxgs_train_apply(self.h))
@@ -619,6 +645,16 @@ class Trainer:
 def scene_coeffs(scene: Scene):
     out = np.empty(scene.k * scene.L * scene.channels * 2)
     _check(_lib.rxgs_scene_get_coeffs(scene.h, out.ctypes.data))
+    return out
+
+
+def scene_arrays(scene: Scene):
+    """Current (possibly trained) scene arrays: positions, log_scales,
+    quaternions, tau_logits, fle_coeffs (flat f64)."""
+    k, L, c = scene.k, scene.L, scene.channels
+    out = dict(positions=np.empty(3 * k), log_scales=np.empty(3 * k), quaternions=np.empty(4 * k),
+               tau_logits=np.empty(k), fle_coeffs=np.empty(k * L * c * 2))
+    _check(_lib.rxgs_scene_get_arrays(scene.h, *[v.ctypes.data for v in out.values()]))
     return out
 
 

@@ -38,6 +38,29 @@ int cuda_fail(cudaError_t e, const char* what) {
     return RXGS_ERR_CUDA;
 }
 
+int scene_sync_host(rxgs_scene_s* sc) {
+    if (!sc->host_stale && !sc->geo_stale) return RXGS_OK;
+    RXGS_CUDA(cudaSetDevice(sc->ctx->device));
+    RXGS_CUDA(cudaStreamSynchronize(sc->ctx->stream));
+    auto down = [](std::vector<double>& h, const DevBuf& d) {
+        return h.empty() ? cudaSuccess : cudaMemcpy(h.data(), d.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost);
+    };
+    if (sc->host_stale) {
+        RXGS_CUDA(down(sc->h_coeffs, sc->d_coeffs64));
+        sc->host_stale = false;
+    }
+    if (sc->geo_stale) {
+        RXGS_CUDA(down(sc->h_pos, sc->d_pos));
+        RXGS_CUDA(down(sc->h_ls, sc->d_ls));
+        RXGS_CUDA(down(sc->h_q, sc->d_q));
+        RXGS_CUDA(down(sc->h_tau, sc->d_tau));
+        sc->pos_index.clear();
+        sc->pos_index_built = false;
+        sc->geo_stale = false;
+    }
+    return RXGS_OK;
+}
+
 void timing_begin(rxgs_ctx ctx, const char* name, cudaEvent_t* a) {
     (void)name;
     *a = nullptr;
@@ -247,6 +270,7 @@ int64_t find_coincident(rxgs_scene sc, const double* rx_host, int n_rx) {
         std::memcpy(&k[16], &z, 8);
         return k;
     };
+    if (scene_sync_host(sc) != RXGS_OK) return -2;
     if (!sc->pos_index_built) {
         sc->pos_index.reserve(static_cast<size_t>(sc->k) * 2);
         for (int k = sc->k - 1; k >= 0; --k)
@@ -263,6 +287,7 @@ int64_t find_coincident(rxgs_scene sc, const double* rx_host, int n_rx) {
 int check_receivers(rxgs_ctx ctx, rxgs_scene sc, const double* rx, int n_rx) {
     std::vector<double> h = to_host(rx, 3 * static_cast<size_t>(n_rx));
     const int64_t e = find_coincident(sc, h.data(), n_rx);
+    if (e == -2) return RXGS_ERR_CUDA;
     if (e >= 0)
         return fail(RXGS_ERR_INVALID, "condition_forward: receiver coincides with gaussian " +
                                           std::to_string(e % std::max(sc->k, 1)));
@@ -512,6 +537,7 @@ int rxgs_scene_destroy(rxgs_scene sc) {
 
 int rxgs_scene_bounds(rxgs_scene sc, double inflate, double lo[3], double hi[3]) {
     if (!sc) return fail(RXGS_ERR_INVALID, "null scene");
+    if (int rc = scene_sync_host(sc)) return rc;
     for (int a = 0; a < 3; ++a) {
         lo[a] = 1.7976931348623157e308;
         hi[a] = -1.7976931348623157e308;
@@ -1397,12 +1423,7 @@ int rxgs_predict(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const rxgs_grid* grid
     if (c) {
         RX_TRY(rxgs_condition_forward(ctx, c, sc, rx, coeffs.data(), nullptr));
     } else {
-        if (sc->host_stale) {
-            RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
-            RXGS_CUDA(cudaMemcpy(sc->h_coeffs.data(), sc->d_coeffs64.p, sc->h_coeffs.size() * sizeof(double),
-                                 cudaMemcpyDeviceToHost));
-            sc->host_stale = false;
-        }
+        RX_TRY(scene_sync_host(sc));
         coeffs = sc->h_coeffs;
     }
     rxgs_txstate st = nullptr;

@@ -280,13 +280,7 @@ extern "C" {
 int rxgs_checkpoint_save(const char* path, rxgs_scene sc, const rxgs_grid* grid, rxgs_cond c) {
     try {
         if (!path || !sc || !grid) return fail(RXGS_ERR_INVALID, "save_checkpoint: null argument");
-        if (sc->host_stale) {  // device coefficients updated by the optimizer
-            cudaSetDevice(sc->ctx->device);
-            RXGS_CUDA(cudaStreamSynchronize(sc->ctx->stream));
-            RXGS_CUDA(cudaMemcpy(sc->h_coeffs.data(), sc->d_coeffs64.p, sc->h_coeffs.size() * sizeof(double),
-                                 cudaMemcpyDeviceToHost));
-            sc->host_stale = false;
-        }
+        if (int rc = scene_sync_host(sc)) return rc;  // device arrays updated by the optimizer
         if (c && c->host_stale) {
             cudaSetDevice(c->ctx->device);
             RXGS_CUDA(cudaStreamSynchronize(c->ctx->stream));
@@ -595,6 +589,7 @@ int rxgs_scene_get_arrays(rxgs_scene sc, double* pos, double* ls, double* q, dou
     auto cp = [](double* dst, const std::vector<double>& v) {
         if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(double));
     };
+    if (int rc = scene_sync_host(sc)) return rc;
     cp(pos, sc->h_pos);
     cp(ls, sc->h_ls);
     cp(q, sc->h_q);

@@ -273,8 +273,9 @@ __global__ void k_bwd_finalize(int K, int l_max, int C, int n_rx, const int* __r
     for (int a = 0; a < 4; ++a) d_q[4 * k + a] = 0.0;
     d_tau[k] = 0.0;
     const size_t stride = static_cast<size_t>(L) * C * 2;
-    for (int j = 0; j < n_rx; ++j)
-        for (size_t i = 0; i < stride; ++i) d_coeffs[(static_cast<size_t>(j) * K + k) * stride + i] = 0.0;
+    if (d_coeffs)
+        for (int j = 0; j < n_rx; ++j)
+            for (size_t i = 0; i < stride; ++i) d_coeffs[(static_cast<size_t>(j) * K + k) * stride + i] = 0.0;
     if (culled[k]) return;
     const double* gm = geom + 12 * static_cast<size_t>(k);
     const double theta = gm[0], phi = gm[1], depth = gm[2];
@@ -317,8 +318,10 @@ __global__ void k_bwd_finalize(int K, int l_max, int C, int n_rx, const int* __r
                     const int comp = l * l + m + l, am = m < 0 ? -m : m;
                     const size_t ci = cbase + (static_cast<size_t>(comp) * C + c) * 2;
                     const double br = B[2 * comp], bi = B[2 * comp + 1];
-                    d_coeffs[ci] += ds.x * br + ds.y * bi;
-                    d_coeffs[ci + 1] += -ds.x * bi + ds.y * br;
+                    if (d_coeffs) {
+                        d_coeffs[ci] += ds.x * br + ds.y * bi;
+                        d_coeffs[ci + 1] += -ds.x * bi + ds.y * br;
+                    }
                     const double a_co = coeffs[ci], b_co = coeffs[ci + 1];
                     const double db_re = ds.x * a_co + ds.y * b_co;
                     const double db_im = -ds.x * b_co + ds.y * a_co;

@@ -908,4 +908,101 @@ cudaError_t launch_adam(int64_t n, double* w, const double* g, double* m, double
     return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------- joint step
+// (trainer.cpp:440-463 with train_geometry: backward_render's geometry
+// gradients, FLE degree mask, Adam on the geometry groups, quaternion
+// renormalisation)
+namespace {
+
+// field adjoint G[j][cell] (complex f32) -> d_values[j][c=0][re/im][cell] f64
+__global__ void k_dv_from_G(int64_t n, int P, const float2* __restrict__ G, double* __restrict__ dv) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const int64_t j = i / P, cell = i % P;
+    const float2 g = G[i];
+    dv[(2 * j) * P + cell] = g.x;
+    dv[(2 * j + 1) * P + cell] = g.y;
+}
+
+// apply_degree_mask (trainer.cpp:233-248): zero the gradient of every
+// component of degree > active; component_degree(comp) = floor(sqrt(comp))
+__global__ void k_degree_mask(int64_t n, int L, int per_comp, int active, double* __restrict__ g) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const int comp = static_cast<int>((i / per_comp) % L);
+    int deg = 0;
+    while ((deg + 1) * (deg + 1) <= comp) ++deg;
+    if (deg > active) g[i] = 0.0;
+}
+
+__global__ void k_add64(int64_t n, const double* __restrict__ a, double* __restrict__ out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) out[i] += a[i];
+}
+
+// per-segment non-finite flags over one flat buffer (segments in buffer order)
+__global__ void k_check_groups(int64_t n, GroupBounds b, const double* __restrict__ g, int* __restrict__ bad) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n || isfinite(g[i])) return;
+    int seg = 0;
+    while (seg + 1 < b.n && i >= b.start[seg + 1]) ++seg;
+    bad[seg] = 1;
+}
+
+// renormalize_quaternions (scene.cpp:281-288) + the f32 position mirrors
+// (index order and the scene's Morton order) read by the conditioning kernels
+__global__ void k_geo_post(int K, double* __restrict__ q, const double* __restrict__ pos,
+                           const int* __restrict__ morton, float4* __restrict__ pos32, float4* __restrict__ mpos32) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    double* qk = q + 4 * static_cast<size_t>(k);
+    double n2 = 0.0;
+    for (int a = 0; a < 4; ++a) n2 += qk[a] * qk[a];
+    const double inv = 1.0 / sqrt(n2);
+    for (int a = 0; a < 4; ++a) qk[a] *= inv;
+    pos32[k] = make_float4(static_cast<float>(pos[3 * k]), static_cast<float>(pos[3 * k + 1]),
+                           static_cast<float>(pos[3 * k + 2]), 0.f);
+    const int src = morton[k];
+    mpos32[k] = make_float4(static_cast<float>(pos[3 * src]), static_cast<float>(pos[3 * src + 1]),
+                            static_cast<float>(pos[3 * src + 2]), 0.f);
+}
+
+unsigned blocks_for(int64_t n) { return static_cast<unsigned>((n + 255) / 256); }
+
+}  // namespace
+
+cudaError_t launch_dv_from_G(int n_rx, int P, const float2* G, double* dv, cudaStream_t s) {
+    const int64_t n = static_cast<int64_t>(n_rx) * P;
+    if (n == 0) return cudaSuccess;
+    k_dv_from_G<<<blocks_for(n), 256, 0, s>>>(n, P, G, dv);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_degree_mask(int64_t n, int L, int per_comp, int active, double* g, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    k_degree_mask<<<blocks_for(n), 256, 0, s>>>(n, L, per_comp, active, g);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_add64(int64_t n, const double* a, double* out, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    k_add64<<<blocks_for(n), 256, 0, s>>>(n, a, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_groups(int64_t n, const GroupBounds& b, const double* g, int* bad, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    k_check_groups<<<blocks_for(n), 256, 0, s>>>(n, b, g, bad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_geo_post(rxgs_scene_s& sc, cudaStream_t s) {
+    if (sc.k == 0) return cudaSuccess;
+    k_geo_post<<<(sc.k + 255) / 256, 256, 0, s>>>(sc.k, sc.d_q.as<double>(), sc.d_pos.as<double>(),
+                                                  sc.d_morton.as<int>(), sc.d_pos32.as<float4>(),
+                                                  sc.d_mpos32.as<float4>());
+    return cudaGetLastError();
+}
+
 }  // namespace rxgs_b200

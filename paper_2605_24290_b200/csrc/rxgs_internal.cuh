@@ -53,6 +53,23 @@ int cuda_fail(cudaError_t e, const char* what);
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) {
+        o.p = nullptr;
+        o.bytes = 0;
+    }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            if (p) cudaFree(p);
+            p = o.p;
+            bytes = o.bytes;
+            o.p = nullptr;
+            o.bytes = 0;
+        }
+        return *this;
+    }
     ~DevBuf() {
         if (p) cudaFree(p);
     }
@@ -143,6 +160,7 @@ struct rxgs_scene_s {
     // in that order (build_scene_order, k_sort.cu)
     rxgs_b200::DevBuf d_morton, d_mpos32;
     bool host_stale = false;  // device coefficients updated by the optimizer
+    bool geo_stale = false;   // device geometry updated by the joint optimizer
     // exact position -> lowest Gaussian index (receiver-on-Gaussian check,
     // conditioning.cpp:380-382), built lazily on the host
     std::unordered_map<std::string, int> pos_index;
@@ -327,6 +345,18 @@ cudaError_t launch_global_bwd(const rxgs_cond_s& cs, const rxgs_scene_s& sc, con
                               const double* d_rx, const float2* u, double* red_part, int n_red, double* row_part,
                               double* gslice, double* grad, cudaStream_t s);
 cudaError_t launch_check_finite64(int64_t n, const double* v, int* bad, cudaStream_t s);
+// joint (geometry) training step helpers (k_train.cu)
+struct GroupBounds {
+    int n;
+    int64_t start[24];
+};
+cudaError_t launch_dv_from_G(int n_rx, int P, const float2* G, double* dv, cudaStream_t s);
+cudaError_t launch_degree_mask(int64_t n, int L, int per_comp, int active, double* g, cudaStream_t s);
+cudaError_t launch_add64(int64_t n, const double* a, double* out, cudaStream_t s);
+cudaError_t launch_check_groups(int64_t n, const GroupBounds& b, const double* g, int* bad, cudaStream_t s);
+cudaError_t launch_geo_post(rxgs_scene_s& sc, cudaStream_t s);
+// host copies of a scene whose device arrays the optimizer updated
+int scene_sync_host(rxgs_scene_s* sc);
 cudaError_t launch_adam(int64_t n, double* w, const double* g, double* m, double* v, double lr, int64_t step,
                         double b1, double b2, double eps, int lr_scale_L, int per_comp, double rest_ratio, float* w32,
                         cudaStream_t s);

@@ -1,9 +1,11 @@
 // C-ABI of the training step (config 4): gradient of the Stage-II chain
 // (trainer.cpp:429-449) summed over a batch of receivers of one
 // transmitter, an exposed flat f64 gradient buffer for the data-parallel
-// all-reduce (NCCL, done by the caller), and the fused Adam update
+// all-reduce (NCCL: rxgs_train_allreduce on the caller's communicator, or
+// the caller's own collective on the buffer), and the fused Adam update
 // (trainer.cpp:451-462 / diffengine.cpp:10-58).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <climits>
@@ -26,6 +28,17 @@ struct rxgs_trainer_s {
     DevBuf grad, m, v, field32, target, G, loss_part, loss, d_entry, d_s, u, part, red_part, row_part, gslice, rx,
         flag, loss_ws;
     int n_parts = 0, n_red = 592;  // k_global_red blocks (fixed-order partials)
+    // joint mode (train_geometry, trainer.cpp:440-463): geometry gradients
+    // [position 3K | transmittance K | scaling 3K | rotation 4K] after the
+    // conditioning parameters in the flat buffer; defaults of TrainConfig
+    // (trainer.hpp:78-92)
+    bool geo = false;
+    double pos_lr_init = 1.6e-4, pos_lr_final = 1.6e-6, pos_delay_mult = 0.01;
+    int64_t pos_total = 2000, pos_delay = 200, ramp = 500;
+    double tau_lr = 1e-2, scale_lr = 5e-3, rot_lr = 1e-3;
+    int64_t n_geo = 0;
+    DevBuf co64, dv64, b_sig, b_eg, b_eds, b_rg, b_rds, geo_tmp;
+    int64_t n_total() const { return n_base + n_par + n_geo; }
 };
 
 namespace {
@@ -45,6 +58,56 @@ bool is_dev(const void* p) {
         const int rc__ = (expr);           \
         if (rc__ != RXGS_OK) return rc__;  \
     } while (0)
+
+}  // namespace
+
+namespace {
+
+int geometry_grads(rxgs_trainer t, rxgs_txstate_s& st, const double* d_rx, int n_rx, int P, bool accumulate,
+                   cudaStream_t s) {
+    rxgs_ctx ctx = t->ctx;
+    rxgs_scene sc = t->sc;
+    const int K = sc->k;
+    const size_t nco = static_cast<size_t>(n_rx) * K * sc->L * sc->channels * 2;
+    RXGS_CUDA(t->co64.ensure(std::max<size_t>(nco, 1) * sizeof(double)));
+    RXGS_CUDA(launch_cond_materialize(*t->c, *sc, d_rx, n_rx, ctx->ag.as<float>(), t->co64.as<double>(), nullptr,
+                                      nullptr, s));
+    RXGS_CUDA(t->dv64.ensure(std::max<size_t>(static_cast<size_t>(n_rx) * 2 * P, 1) * sizeof(double)));
+    RXGS_CUDA(launch_dv_from_G(n_rx, P, t->G.as<float2>(), t->dv64.as<double>(), s));
+    const size_t n_jc = static_cast<size_t>(n_rx) * sc->channels;
+    const size_t E = std::max<int64_t>(st.entries, 1);
+    RXGS_CUDA(t->b_sig.ensure(std::max<size_t>(K * n_jc, 1) * sizeof(double2)));
+    RXGS_CUDA(t->b_eg.ensure(E * 7 * sizeof(double)));
+    RXGS_CUDA(t->b_eds.ensure(E * n_jc * sizeof(double2)));
+    RXGS_CUDA(t->b_rg.ensure(std::max<size_t>(K, 1) * 7 * sizeof(double)));
+    RXGS_CUDA(t->b_rds.ensure(std::max<size_t>(K * n_jc, 1) * sizeof(double2)));
+    RXGS_CUDA(t->geo_tmp.ensure(std::max<size_t>(t->n_geo, 1) * sizeof(double)));
+    double* gt = t->geo_tmp.as<double>();  // [pos | tau | ls | q]
+    RXGS_CUDA(launch_backward_render(st, *sc, t->co64.as<double>(), n_rx, t->dv64.as<double>(), t->b_sig.as<double2>(),
+                                     t->b_eg.as<double>(), t->b_eds.as<double2>(), t->b_rg.as<double>(),
+                                     t->b_rds.as<double2>(), gt, gt + 4 * static_cast<size_t>(K),
+                                     gt + 7 * static_cast<size_t>(K), gt + 3 * static_cast<size_t>(K), nullptr, s));
+    double* dst = t->grad.as<double>() + t->n_base + t->n_par;
+    if (accumulate) {
+        RXGS_CUDA(launch_add64(t->n_geo, gt, dst, s));
+    } else {
+        RXGS_CUDA(cudaMemcpyAsync(dst, gt, sizeof(double) * t->n_geo, cudaMemcpyDeviceToDevice, s));
+    }
+    ctx->launches += 8;
+    return RXGS_OK;
+}
+
+// opt::lr_at (diffengine.cpp:36-48)
+double lr_at(const rxgs_trainer_s& t, int64_t step) {
+    const double frac = t.pos_total > 0 ? static_cast<double>(step) / static_cast<double>(t.pos_total) : 1.0;
+    const double base = t.pos_lr_init * std::pow(t.pos_lr_final / t.pos_lr_init, frac);
+    double ramp = 1.0;
+    if (t.pos_delay > 0) {
+        const double u = std::clamp(static_cast<double>(step) / static_cast<double>(t.pos_delay), 0.0, 1.0);
+        ramp = t.pos_delay_mult + (1.0 - t.pos_delay_mult) * std::sin(0.5 * 3.14159265358979323846 * u);
+    }
+    return base * ramp;
+}
 
 }  // namespace
 
@@ -112,7 +175,7 @@ int rxgs_train_grads(rxgs_trainer t, rxgs_txstate st, const double* rx, int n_rx
     cudaStream_t s = ctx->stream;
     const DevGrid& g = st->grid;
     const int P = g.nt * g.np;
-    const size_t n = static_cast<size_t>(t->n_base + t->n_par);
+    const size_t n = static_cast<size_t>(t->n_total());
     // inputs
     const double* d_rx = rx;
     if (!is_dev(rx)) {
@@ -200,6 +263,9 @@ int rxgs_train_grads(rxgs_trainer t, rxgs_txstate st, const double* rx, int n_rx
                                     t->row_part.as<double>(), t->gslice.as<double>(), gpar, s));
     }
     ctx->launches += 12;
+    // ---- joint mode: geometry adjoint of backward_render (sphraster.cpp:509-733)
+    // on the FP64 conditioned coefficients of the batch, summed over it
+    if (t->geo) TRY(geometry_grads(t, *st, d_rx, n_rx, P, accumulate != 0, s));
     // ---- losses out + non-finite check (trainer.cpp:436-438)
     std::vector<double> lh(n_rx);
     RXGS_CUDA(cudaMemcpyAsync(lh.data(), t->loss.p, sizeof(double) * n_rx, cudaMemcpyDeviceToHost, s));
@@ -219,7 +285,7 @@ int rxgs_train_grads(rxgs_trainer t, rxgs_txstate st, const double* rx, int n_rx
 int rxgs_train_grad_buffer(rxgs_trainer t, double** dev_ptr, int64_t* n, int64_t* n_base) {
     if (!t) return fail(RXGS_ERR_INVALID, "null trainer");
     if (dev_ptr) *dev_ptr = t->grad.as<double>();
-    if (n) *n = t->n_base + t->n_par;
+    if (n) *n = t->n_total();
     if (n_base) *n_base = t->n_base;
     return RXGS_OK;
 }
@@ -237,32 +303,185 @@ int rxgs_train_get_grads(rxgs_trainer t, double* d_base, double* d_params) {
 // Optimizer::step for "features" (lr_scale) and every conditioning group
 // (diffengine.cpp:50-58, trainer.cpp:451-462): non-finite check per group,
 // then Adam; the scene / conditioning device copies are updated in place.
+// NCCL is resolved at the first call, from the library the process already
+// has loaded (the caller's communicator must come from it): dlopen of the
+// soname returns the loaded copy (torch's bundled NCCL under
+// torch.distributed), else the system libnccl.so.2.
+namespace {
+using nccl_allreduce_fn = int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+using nccl_errstr_fn = const char* (*)(int);
+constexpr int kNcclFloat64 = 8, kNcclSum = 0;
+struct NcclSyms {
+    nccl_allreduce_fn allreduce = nullptr;
+    nccl_errstr_fn errstr = nullptr;
+};
+const NcclSyms& nccl_syms() {
+    static NcclSyms s = [] {
+        NcclSyms r;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        void* a = dlsym(h ? h : RTLD_DEFAULT, "ncclAllReduce");
+        if (!a) a = dlsym(RTLD_DEFAULT, "ncclAllReduce");
+        r.allreduce = reinterpret_cast<nccl_allreduce_fn>(a);
+        r.errstr = reinterpret_cast<nccl_errstr_fn>(dlsym(h ? h : RTLD_DEFAULT, "ncclGetErrorString"));
+        return r;
+    }();
+    return s;
+}
+}  // namespace
+
+int rxgs_train_allreduce(rxgs_trainer t, void* nccl_comm) {
+    if (!t || !nccl_comm) return fail(RXGS_ERR_INVALID, "train_allreduce: null argument");
+    const NcclSyms& n = nccl_syms();
+    if (!n.allreduce) return fail(RXGS_ERR_RUNTIME, "train_allreduce: NCCL (libnccl.so.2) not found");
+    RXGS_CUDA(cudaSetDevice(t->ctx->device));
+    const size_t count = static_cast<size_t>(t->n_base + t->n_par);
+    const int r = n.allreduce(t->grad.p, t->grad.p, count, kNcclFloat64, kNcclSum, nccl_comm, t->ctx->stream);
+    if (r != 0)
+        return fail(RXGS_ERR_CUDA, std::string("train_allreduce: ncclAllReduce failed: ") +
+                                       (n.errstr ? n.errstr(r) : std::to_string(r)));
+    t->ctx->launches += 1;
+    return RXGS_OK;
+}
+
+int rxgs_trainer_enable_geometry(rxgs_trainer t, const double geo[9]) {
+    if (!t) return fail(RXGS_ERR_INVALID, "null trainer");
+    if (t->step != 0) return fail(RXGS_ERR_INVALID, "train: enable geometry before the first step");
+    if (geo) {
+        t->pos_lr_init = geo[0];
+        t->pos_lr_final = geo[1];
+        t->pos_total = static_cast<int64_t>(geo[2]);
+        t->pos_delay_mult = geo[3];
+        t->pos_delay = static_cast<int64_t>(geo[4]);
+        t->tau_lr = geo[5];
+        t->scale_lr = geo[6];
+        t->rot_lr = geo[7];
+        t->ramp = static_cast<int64_t>(geo[8]);
+    }
+    RXGS_CUDA(cudaSetDevice(t->ctx->device));
+    RXGS_CUDA(cudaStreamSynchronize(t->ctx->stream));
+    t->geo = true;
+    t->n_geo = 11 * static_cast<int64_t>(t->sc->k);
+    const size_t n = static_cast<size_t>(t->n_total()) * sizeof(double);
+    DevBuf g, m, v;
+    RXGS_CUDA(g.ensure(n));
+    RXGS_CUDA(m.ensure(n));
+    RXGS_CUDA(v.ensure(n));
+    RXGS_CUDA(cudaMemset(g.p, 0, n));
+    RXGS_CUDA(cudaMemset(m.p, 0, n));
+    RXGS_CUDA(cudaMemset(v.p, 0, n));
+    std::swap(t->grad, g);
+    std::swap(t->m, m);
+    std::swap(t->v, v);
+    return RXGS_OK;
+}
+
+int rxgs_train_get_geometry_grads(rxgs_trainer t, double* d_positions, double* d_log_scales, double* d_quaternions,
+                                  double* d_tau_logits) {
+    if (!t) return fail(RXGS_ERR_INVALID, "null trainer");
+    if (!t->geo) return fail(RXGS_ERR_INVALID, "train: geometry gradients need rxgs_trainer_enable_geometry");
+    RXGS_CUDA(cudaSetDevice(t->ctx->device));
+    RXGS_CUDA(cudaStreamSynchronize(t->ctx->stream));
+    const size_t K = static_cast<size_t>(t->sc->k);
+    const double* g = t->grad.as<double>() + t->n_base + t->n_par;
+    if (d_positions) RXGS_CUDA(cudaMemcpy(d_positions, g, sizeof(double) * 3 * K, cudaMemcpyDefault));
+    if (d_tau_logits) RXGS_CUDA(cudaMemcpy(d_tau_logits, g + 3 * K, sizeof(double) * K, cudaMemcpyDefault));
+    if (d_log_scales) RXGS_CUDA(cudaMemcpy(d_log_scales, g + 4 * K, sizeof(double) * 3 * K, cudaMemcpyDefault));
+    if (d_quaternions) RXGS_CUDA(cudaMemcpy(d_quaternions, g + 7 * K, sizeof(double) * 4 * K, cudaMemcpyDefault));
+    return RXGS_OK;
+}
+
+// One optimizer step of conditioned_training_loop (trainer.cpp:450-463):
+// [joint: FLE degree mask, position (lr_at), transmittance, scaling,
+// rotation], features (degree >= 1 at rest_lr_ratio), then the conditioning
+// groups in step_conditioning order (trainer.cpp:258-273).  Every group is
+// checked for non-finite gradients first; the first bad group in that order
+// names the error and nothing is updated (the reference has already stepped
+// the groups before it when it throws).
 int rxgs_train_apply(rxgs_trainer t) {
     if (!t) return fail(RXGS_ERR_INVALID, "null trainer");
     rxgs_ctx ctx = t->ctx;
     RXGS_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
-    RXGS_CUDA(t->flag.ensure(16));
-    const int big = INT_MAX;
-    int bad[2] = {INT_MAX, INT_MAX};
-    RXGS_CUDA(cudaMemcpyAsync(t->flag.p, &big, sizeof(int), cudaMemcpyHostToDevice, s));
-    RXGS_CUDA(cudaMemcpyAsync(t->flag.as<int>() + 1, &big, sizeof(int), cudaMemcpyHostToDevice, s));
-    RXGS_CUDA(launch_check_finite64(t->n_base, t->grad.as<double>(), t->flag.as<int>(), s));
-    RXGS_CUDA(launch_check_finite64(t->n_par, t->grad.as<double>() + t->n_base, t->flag.as<int>() + 1, s));
-    RXGS_CUDA(cudaMemcpyAsync(bad, t->flag.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
-    RXGS_CUDA(cudaStreamSynchronize(s));
-    if (bad[0] != INT_MAX) return fail(RXGS_ERR_RUNTIME, "optimizer: non-finite gradient in group 'features'");
-    if (bad[1] != INT_MAX) return fail(RXGS_ERR_RUNTIME, "optimizer: non-finite gradient in group 'cond'");
-    t->step += 1;
     rxgs_scene sc = t->sc;
     rxgs_cond c = t->c;
-    RXGS_CUDA(launch_adam(t->n_base, sc->d_coeffs64.as<double>(), t->grad.as<double>(), t->m.as<double>(),
-                          t->v.as<double>(), t->feature_lr, t->step, t->b1, t->b2, t->eps, sc->L, sc->channels * 2,
-                          t->rest_ratio, nullptr, s));
-    RXGS_CUDA(launch_adam(t->n_par, c->d_params64.as<double>(), t->grad.as<double>() + t->n_base,
-                          t->m.as<double>() + t->n_base, t->v.as<double>() + t->n_base, t->cond_lr, t->step, t->b1,
+    const int64_t iter = t->step;  // the reference's t (0-based) for this step
+    if (t->geo && t->ramp > 0) {   // apply_degree_mask (trainer.cpp:233-248)
+        const int active = static_cast<int>(std::min<int64_t>(sc->l_max, iter / t->ramp));
+        if (active < sc->l_max)
+            RXGS_CUDA(launch_degree_mask(t->n_base, sc->L, sc->channels * 2, active, t->grad.as<double>(), s));
+    }
+    // segments in buffer order, named as the reference's optimizer groups
+    struct Seg {
+        const char* name;
+        int64_t start;
+    };
+    const int64_t P0 = t->n_base;
+    std::vector<Seg> segs = {{"features", 0},
+                             {"cond.freqs", P0 + static_cast<int64_t>(c->o_freq)},
+                             {"cond.global.w1", P0 + static_cast<int64_t>(c->o_gw1)},
+                             {"cond.global.b1", P0 + static_cast<int64_t>(c->o_gb1)},
+                             {"cond.global.w2", P0 + static_cast<int64_t>(c->o_gw2)},
+                             {"cond.global.b2", P0 + static_cast<int64_t>(c->o_gb2)},
+                             {"cond.global.w3", P0 + static_cast<int64_t>(c->o_gw3)},
+                             {"cond.global.b3", P0 + static_cast<int64_t>(c->o_gb3)},
+                             {"cond.embed", P0 + static_cast<int64_t>(c->o_emb)},
+                             {"cond.local.w1", P0 + static_cast<int64_t>(c->o_lw1)},
+                             {"cond.local.b1", P0 + static_cast<int64_t>(c->o_lb1)},
+                             {"cond.local.w2", P0 + static_cast<int64_t>(c->o_lw2)},
+                             {"cond.local.b2", P0 + static_cast<int64_t>(c->o_lb2)},
+                             {"cond.local.w3", P0 + static_cast<int64_t>(c->o_lw3)},
+                             {"cond.local.b3", P0 + static_cast<int64_t>(c->o_lb3)}};
+    if (t->geo) {
+        const int64_t G0 = P0 + t->n_par, K = sc->k;
+        segs.push_back({"position", G0});
+        segs.push_back({"transmittance", G0 + 3 * K});
+        segs.push_back({"scaling", G0 + 4 * K});
+        segs.push_back({"rotation", G0 + 7 * K});
+    }
+    GroupBounds gb{};
+    gb.n = static_cast<int>(segs.size());
+    for (int i = 0; i < gb.n; ++i) gb.start[i] = segs[i].start;
+    RXGS_CUDA(t->flag.ensure(sizeof(int) * 24));
+    RXGS_CUDA(cudaMemsetAsync(t->flag.p, 0, sizeof(int) * 24, s));
+    RXGS_CUDA(launch_check_groups(t->n_total(), gb, t->grad.as<double>(), t->flag.as<int>(), s));
+    int bad[24] = {};
+    RXGS_CUDA(cudaMemcpyAsync(bad, t->flag.p, sizeof(int) * 24, cudaMemcpyDeviceToHost, s));
+    RXGS_CUDA(cudaStreamSynchronize(s));
+    static const char* kOrder[] = {"position",       "transmittance",  "scaling",        "rotation",
+                                   "features",       "cond.freqs",     "cond.embed",     "cond.global.w1",
+                                   "cond.global.b1", "cond.global.w2", "cond.global.b2", "cond.global.w3",
+                                   "cond.global.b3", "cond.local.w1",  "cond.local.b1",  "cond.local.w2",
+                                   "cond.local.b2",  "cond.local.w3",  "cond.local.b3"};
+    for (const char* name : kOrder)
+        for (int i = 0; i < gb.n; ++i)
+            if (bad[i] && std::string(segs[i].name) == name)
+                return fail(RXGS_ERR_RUNTIME, std::string("optimizer: non-finite gradient in group '") + name + "'");
+    t->step += 1;
+    double* g = t->grad.as<double>();
+    double* m = t->m.as<double>();
+    double* v = t->v.as<double>();
+    if (t->geo) {
+        const int64_t G0 = P0 + t->n_par, K = sc->k;
+        struct {
+            double* w;
+            int64_t off, n;
+            double lr;
+        } geo[4] = {{sc->d_pos.as<double>(), G0, 3 * K, lr_at(*t, iter)},
+                    {sc->d_tau.as<double>(), G0 + 3 * K, K, t->tau_lr},
+                    {sc->d_ls.as<double>(), G0 + 4 * K, 3 * K, t->scale_lr},
+                    {sc->d_q.as<double>(), G0 + 7 * K, 4 * K, t->rot_lr}};
+        for (const auto& e : geo)
+            RXGS_CUDA(launch_adam(e.n, e.w, g + e.off, m + e.off, v + e.off, e.lr, t->step, t->b1, t->b2, t->eps, 0,
+                                  1, 1.0, nullptr, s));
+        RXGS_CUDA(launch_geo_post(*sc, s));  // renormalize_quaternions + f32 position mirrors
+        sc->geo_stale = true;
+        ctx->launches += 5;
+    }
+    RXGS_CUDA(launch_adam(t->n_base, sc->d_coeffs64.as<double>(), g, m, v, t->feature_lr, t->step, t->b1, t->b2,
+                          t->eps, sc->L, sc->channels * 2, t->rest_ratio, nullptr, s));
+    RXGS_CUDA(launch_adam(t->n_par, c->d_params64.as<double>(), g + P0, m + P0, v + P0, t->cond_lr, t->step, t->b1,
                           t->b2, t->eps, 0, 1, 1.0, c->d_params32.as<float>(), s));
-    ctx->launches += 4;
+    ctx->launches += 3;
     sc->host_stale = true;
     c->host_stale = true;
     return RXGS_OK;

@@ -50,3 +50,11 @@ def allreduce_grads(flat: torch.Tensor) -> torch.Tensor:
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(flat, op=dist.ReduceOp.SUM)
     return flat
+
+
+def nccl_comm_ptr(group=None) -> int:
+    """The ncclComm_t behind torch's NCCL process group (for
+    Trainer.allreduce, which issues ncclAllReduce on the library's stream).
+    The communicator must exist: run one collective on the group first."""
+    pg = group if group is not None else dist.distributed_c10d._get_default_group()
+    return int(pg._get_backend(torch.device("cuda"))._comm_ptr())

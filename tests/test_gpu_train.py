@@ -135,3 +135,171 @@ def test_train_apply_is_adam(ctx, capi, ref):
     spec1, _ = scene.render_queries(cond, scene.tx_state(TX, grid), rx)
     spec0 = None
     assert np.isfinite(spec1).all()
+
+
+def _nccl_one_rank_comm():
+    """A 1-rank ncclComm_t from the process's libnccl (torch's, once torch is loaded)."""
+    import ctypes
+    import torch  # noqa: F401  (loads torch's NCCL so the library resolves the same copy)
+    torch.cuda.set_device(0)
+    lib = ctypes.CDLL("libnccl.so.2")
+
+    class UniqueId(ctypes.Structure):  # ncclUniqueId, passed by value
+        _fields_ = [("internal", ctypes.c_char * 128)]
+
+    uid = UniqueId()
+    assert lib.ncclGetUniqueId(ctypes.byref(uid)) == 0
+    comm = ctypes.c_void_p()
+    lib.ncclCommInitRank.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, UniqueId, ctypes.c_int]
+    assert lib.ncclCommInitRank(ctypes.byref(comm), 1, uid, 0) == 0
+    return lib, comm
+
+
+def test_train_allreduce_nccl(ctx, capi, ref):
+    """rxgs_train_allreduce: ncclAllReduce(sum, f64) of the flat gradient buffer
+    on the library stream; over one rank the buffer is unchanged, and the
+    following apply() sees it."""
+    sc, scene, cond, grid, og, rscene, rcond, params = _setup(capi, ctx, ref)
+    rx = capi.synth_points(2, 13, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
+    tg = _targets(2, grid.cells)
+    st = scene.tx_state(TX, grid)
+    tr = capi.Trainer(ctx, scene, cond)
+    tr.grads(st, rx, tg)
+    db0, dp0 = tr.get_grads()
+    lib, comm = _nccl_one_rank_comm()
+    try:
+        tr.allreduce(comm.value)
+        db1, dp1 = tr.get_grads()
+        assert np.array_equal(db0, db1) and np.array_equal(dp0, dp1)
+        with pytest.raises(capi.RxgsError, match="null argument"):
+            tr.allreduce(0)
+    finally:
+        lib.ncclCommDestroy(comm)
+    tr.apply()
+    assert tr.step_count == 1
+
+
+def _lr_at(lr_init, lr_final, total, delay_mult, delay, t):
+    """opt::lr_at (diffengine.cpp:36-48)."""
+    frac = t / total if total > 0 else 1.0
+    base = lr_init * (lr_final / lr_init) ** frac
+    ramp = 1.0
+    if delay > 0:
+        u = min(max(t / delay, 0.0), 1.0)
+        ramp = delay_mult + (1.0 - delay_mult) * np.sin(0.5 * np.pi * u)
+    return base * ramp
+
+
+def _adam1(w, g, lr, scale=1.0):
+    """One Adam step from zero moments (diffengine.cpp:10-34)."""
+    m = 0.1 * g
+    v = 0.001 * g * g
+    return w - lr * scale * (m / 0.1) / (np.sqrt(v / 0.001) + 1e-8)
+
+
+@pytest.mark.parametrize("mode", ["full", "no_occlusion"])
+def test_train_joint_grads_match_reference_sum(ctx, capi, ref, mode):
+    """Joint step (train_geometry, trainer.cpp:440-449): the geometry gradients of
+    backward_render summed over the batch, next to d_base and the conditioning
+    gradients, vs the reference's per-sample gradients (SURVEY.md 8c4 'joint')."""
+    sc, scene, cond, grid, og, rscene, rcond, params = _setup(capi, ctx, ref, k=500, mode=mode)
+    rx = capi.synth_points(3, 19, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
+    tg = _targets(3, grid.cells, 4)
+    st = scene.tx_state(TX, grid)
+    tr = capi.Trainer(ctx, scene, cond, geometry=True)
+    assert tr.n == tr.n_base + cond.param_count + 11 * scene.k
+    loss = tr.grads(st, rx, tg)
+    db, dp = tr.get_grads()
+    gpos, gls, gq, gtau = tr.get_geometry_grads()
+    want = dict(d_base=0.0, d_params=0.0, d_positions=0.0, d_log_scales=0.0, d_quaternions=0.0, d_tau_logits=0.0)
+    for j in range(3):
+        r = ref.train_sample(rscene, rcond, og, TX, rx[j], tg[j].astype(np.float64), geometry=True)
+        assert rel_err(loss[j], r["loss"]) < TOL
+        for key in want:
+            want[key] = want[key] + r[key]
+    assert rel_err(db, want["d_base"]).max() < TOL
+    assert rel_err(dp, want["d_params"]).max() < TOL
+    for got, key in ((gpos, "d_positions"), (gls, "d_log_scales"), (gq, "d_quaternions"), (gtau, "d_tau_logits")):
+        assert np.abs(want[key]).max() > 0, key
+        assert rel_err(got, want[key]).max() < TOL, key
+    # accumulate over two calls == one batch
+    tr.grads(st, rx[:1], tg[:1])
+    tr.grads(st, rx[1:], tg[1:], accumulate=True)
+    assert rel_err(np.concatenate(tr.get_geometry_grads()), np.concatenate((gpos, gls, gq, gtau))).max() < 1e-9
+
+
+def test_train_joint_apply(ctx, capi, ref):
+    """Joint optimizer step (trainer.cpp:450-463): degree mask at t = 0 (only
+    degree-0 coefficients move), position at lr_at(position_lr, 0), the
+    constant geometry rates, quaternions renormalised; the next TxState is
+    built from the updated geometry."""
+    sc, scene, cond, grid, og, rscene, rcond, params = _setup(capi, ctx, ref, k=400)
+    rx = capi.synth_points(2, 23, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
+    tg = _targets(2, grid.cells, 6)
+    geo = (1.6e-4, 1.6e-6, 2000, 0.01, 200, 1e-2, 5e-3, 1e-3, 500)
+    olo, ohi = scene.bounds(0.1)
+    occ = cond.build_occupancy(scene, 32, olo, ohi)  # as in _setup; fixed for the run (trainer.cpp:395-397)
+    tr = capi.Trainer(ctx, scene, cond, geometry=geo)
+    a0 = capi.scene_arrays(scene)
+    par0 = capi.cond_params(cond)
+    st = scene.tx_state(TX, grid)
+    tr.grads(st, rx, tg)
+    db, dp = tr.get_grads()
+    gpos, gls, gq, gtau = tr.get_geometry_grads()
+    tr.apply()
+    a1 = capi.scene_arrays(scene)
+    lr_pos = _lr_at(*geo[:5], 0)
+    assert rel_err(a1["positions"], _adam1(a0["positions"], gpos, lr_pos)).max() < 1e-12
+    assert rel_err(a1["tau_logits"], _adam1(a0["tau_logits"], gtau, 1e-2)).max() < 1e-12
+    assert rel_err(a1["log_scales"], _adam1(a0["log_scales"], gls, 5e-3)).max() < 1e-12
+    q = _adam1(a0["quaternions"], gq, 1e-3).reshape(-1, 4)
+    q = q * (1.0 / np.sqrt((q * q).sum(axis=1)))[:, None]
+    assert rel_err(a1["quaternions"], q.ravel()).max() < 1e-12
+    L = 9
+    deg0 = (np.arange(db.size) // 2) % L == 0
+    want_f = np.where(deg0, _adam1(a0["fle_coeffs"], db, 5e-3), a0["fle_coeffs"])
+    assert rel_err(a1["fle_coeffs"], want_f).max() < 1e-12
+    assert rel_err(capi.cond_params(cond), _adam1(par0, dp, 1e-3)).max() < 1e-12
+    # step 2 on the updated geometry: TxState rebuilt, gradients still match the reference
+    r2 = ref.scene(dict(sc, positions=a1["positions"].reshape(-1, 3), log_scales=a1["log_scales"].reshape(-1, 3),
+                        quaternions=a1["quaternions"].reshape(-1, 4), tau_logits=a1["tau_logits"],
+                        fle_coeffs=a1["fle_coeffs"].reshape(sc["fle_coeffs"].shape)), "spectrum")
+    st2 = scene.tx_state(TX, grid)
+    loss2 = tr.grads(st2, rx[:1], tg[:1])
+    cfg = capi.cond_cfg(mode="full")
+    rc2 = ref.cond(cfg, capi.cond_params(cond), occ, olo, ohi)
+    r = ref.train_sample(r2, rc2, og, TX, rx[0], tg[0].astype(np.float64), geometry=True)
+    assert rel_err(loss2[0], r["loss"]) < TOL
+    assert rel_err(tr.get_geometry_grads()[0], r["d_positions"]).max() < TOL
+
+
+def test_train_nonfinite_group_names(ctx, capi, ref):
+    """The non-finite check names the reference's optimizer group, first in
+    its step order (diffengine.cpp:50-58, trainer.cpp:258-273, 450-462);
+    components hidden by the degree mask are not checked."""
+    import torch
+    sc, scene, cond, grid, og, rscene, rcond, params = _setup(capi, ctx, ref, k=300)
+    rx = capi.synth_points(1, 29, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
+    tg = _targets(1, grid.cells, 8)
+    st = scene.tx_state(TX, grid)
+    tr = capi.Trainer(ctx, scene, cond, geometry=True)
+    tr.grads(st, rx, tg)
+    g = tr.grad_tensor()
+    nb, npar, k = tr.n_base, cond.param_count, scene.k
+    g[2 * 1] = float("nan")  # component 1 (degree 1) of Gaussian 0: masked at t = 0
+    g[nb + npar - 1] = float("nan")  # cond.local.b3
+    torch.cuda.synchronize()
+    with pytest.raises(capi.RxgsError, match="non-finite gradient in group 'cond.local.b3'"):
+        tr.apply()
+    g[nb + npar + 3 * k] = float("nan")  # transmittance
+    g[nb + npar + 7 * k + 2] = float("nan")  # rotation
+    torch.cuda.synchronize()
+    with pytest.raises(capi.RxgsError, match="non-finite gradient in group 'transmittance'"):
+        tr.apply()
+    g[0] = float("nan")  # features, degree 0
+    g[nb + npar + 3 * k] = 0.0
+    g[nb + npar + 7 * k + 2] = 0.0
+    torch.cuda.synchronize()
+    with pytest.raises(capi.RxgsError, match="non-finite gradient in group 'features'"):
+        tr.apply()
+    assert tr.step_count == 0
