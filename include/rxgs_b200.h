@@ -173,6 +173,15 @@ int rxgs_backward_render(rxgs_ctx ctx, rxgs_txstate st, rxgs_scene scene, const 
  * device; e.g. rxgs_coverage_table's output widened to f64).  Exact:
  * threshold tests and counts; greedy ties break on the lower candidate.
  * greedy_plan writes k candidate indices in selection order. */
+/* met::mae / mse / psnr / ssim (metrics.hpp:14-28, metrics.cpp:11-112) of a
+ * batch of n_img images (h x w row-major; pred f32 if pred_f32 else f64, gt
+ * f64; host or device): out[4*i..] = {mae, mse, psnr(max_val), ssim}.
+ * ssim_opts = {window, sigma, dynamic_range} (NULL: SsimOptions defaults
+ * 11, 1.5, 1.0; window 0 skips SSIM and writes NaN).  Identical images give
+ * the 300 dB sentinel (kDbSentinel); errors carry the reference texts. */
+int rxgs_image_metrics(rxgs_ctx ctx, const void* pred, int pred_f32, const double* gt, int n_img, int h, int w,
+                       double max_val, const double ssim_opts[3], double* out);
+
 int rxgs_coverage_fraction(rxgs_ctx ctx, const double* table, int64_t tx_count, int64_t cand_count,
                            const int32_t* selected, int n_selected, double threshold_dbm, double* out);
 int rxgs_greedy_plan(rxgs_ctx ctx, const double* table, int64_t tx_count, int64_t cand_count, int k,

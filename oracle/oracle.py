@@ -139,6 +139,8 @@ class Checker:
                 "coverage_fraction": (C.c_int, [_dp, C.c_long, C.c_long, _ip, C.c_int, C.c_double, _dp,
                                                 C.c_char_p, C.c_int]),
                 "greedy_plan": (C.c_int, [_dp, C.c_long, C.c_long, C.c_int, C.c_double, _ip, C.c_char_p, C.c_int]),
+                "image_metrics": (C.c_int, [_dp, _dp, C.c_int, C.c_int, C.c_double, C.c_int, C.c_double,
+                                            C.c_double, _dp, C.c_char_p, C.c_int]),
                 "train_sample": (C.c_int, [C.c_void_p, C.c_void_p, _ip, _dp, _dp, _dp, _dp, C.c_double,
                                            C.c_double, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
                                            C.c_char_p, C.c_int]),
@@ -453,5 +455,18 @@ def _greedy_plan(self, table, k, thr):
     return order[:k]
 
 
+def _image_metrics(self, pred, gt, h, w, max_val=1.0, window=11, sigma=1.5, dyn=1.0):
+    """met::{mae, mse, psnr, ssim} of one image (reference build only)."""
+    p = np.ascontiguousarray(pred, np.float64)
+    g = np.ascontiguousarray(gt, np.float64)
+    out = np.zeros(4)
+    err = C.create_string_buffer(512)
+    if self._image_metrics(p.ctypes.data_as(_dp), g.ctypes.data_as(_dp), int(h), int(w), float(max_val), int(window),
+                           float(sigma), float(dyn), out.ctypes.data_as(_dp), err, 512):
+        raise ValueError(err.value.decode())
+    return out
+
+
+Checker.image_metrics = _image_metrics
 Checker.coverage_fraction = _coverage_fraction
 Checker.greedy_plan = _greedy_plan

@@ -29,6 +29,7 @@
 
 #include "rxgs/apps.hpp"
 #include "rxgs/conditioning.hpp"
+#include "rxgs/metrics.hpp"
 #include "rxgs/radiance.hpp"
 #include "rxgs/rng.hpp"
 #include "rxgs/scene.hpp"
@@ -702,6 +703,31 @@ int ref_greedy_plan(const double* table, long tx, long cand, int k, double thr, 
         const auto o = apps::greedy_plan(std::vector<double>(table, table + tx * cand), static_cast<std::size_t>(tx),
                                          static_cast<std::size_t>(cand), k, thr);
         std::copy(o.begin(), o.end(), order);
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return 1;
+    }
+}
+
+// met::mae / mse / psnr / ssim (metrics.cpp:11-112) of one image;
+// out = {mae, mse, psnr, ssim}; ssim skipped (NaN) when window == 0.
+int ref_image_metrics(const double* pred, const double* gt, int h, int w, double max_val, int window, double sigma,
+                      double dyn, double* out, char* err, int errlen) {
+    try {
+        const std::size_t n = static_cast<std::size_t>(h) * w;
+        const std::span<const double> p(pred, n), g(gt, n);
+        out[0] = met::mae(p, g);
+        out[1] = met::mse(p, g);
+        out[2] = met::psnr(p, g, max_val);
+        out[3] = std::nan("");
+        if (window > 0) {
+            met::SsimOptions o;
+            o.window = window;
+            o.sigma = sigma;
+            o.dynamic_range = dyn;
+            out[3] = met::ssim(p, g, h, w, o);
+        }
         return 0;
     } catch (const std::exception& e) {
         set_err(err, errlen, e.what());

@@ -122,6 +122,7 @@ _SIG = {
     "rxgs_checkpoint_save": (C.c_int, [C.c_char_p, _vp, C.POINTER(Grid), _vp]),
     "rxgs_checkpoint_load": (C.c_int, [_vp, C.c_char_p, C.POINTER(_vp), C.POINTER(Grid), C.POINTER(_vp)]),
     "rxgs_coverage_fraction": (C.c_int, [_vp, _vp, _i64, _i64, _vp, C.c_int, C.c_double, C.POINTER(C.c_double)]),
+    "rxgs_image_metrics": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int, C.c_int, C.c_int, C.c_double, _vp, _vp]),
     "rxgs_greedy_plan": (C.c_int, [_vp, _vp, _i64, _i64, C.c_int, C.c_double, _vp]),
     "rxgs_scene_info": (C.c_int, [_vp, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32)]),
     "rxgs_cond_config": (C.c_int, [_vp, _vp]),
@@ -300,6 +301,25 @@ class Context:
         _check(_lib.rxgs_greedy_plan(self.h, table.ctypes.data, table.shape[0], table.shape[1], int(k),
                                      float(threshold_dbm), order.ctypes.data if order.size else None))
         return order
+
+    def image_metrics(self, pred, gt, h, w, max_val=1.0, ssim=(11, 1.5, 1.0)):
+        """met::{mae, mse, psnr, ssim} per image (metrics.cpp:11-112) -> (n, 4).
+        pred: f32 or f64 (host array or CUDA tensor), gt: f64; ssim=None skips SSIM."""
+        if hasattr(pred, "data_ptr"):
+            import torch
+            f32 = pred.dtype == torch.float32
+        else:
+            pred = np.ascontiguousarray(pred)
+            if pred.dtype != np.float32:
+                pred = pred.astype(np.float64)
+            f32 = pred.dtype == np.float32
+        gt = gt if hasattr(gt, "data_ptr") else np.ascontiguousarray(gt, np.float64)
+        n = max(1, (pred.numel() if hasattr(pred, "numel") else pred.size) // max(h * w, 1))
+        out = np.empty((n, 4))
+        opts = np.asarray(ssim if ssim is not None else (0, 1.5, 1.0), np.float64)
+        _check(_lib.rxgs_image_metrics(self.h, ptr(pred), int(f32), ptr(gt), n, int(h), int(w), float(max_val),
+                                       opts.ctypes.data, out.ctypes.data))
+        return out
 
     def bin_and_sort(self, culled, depth, spans, grid: Grid):
         k = len(culled)

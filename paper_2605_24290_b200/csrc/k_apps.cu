@@ -1,4 +1,5 @@
-// Coverage consumers of the config-3 RSSI table:
+// Coverage consumers of the config-3 RSSI table and the
+// evaluation metrics (met::mae / mse / psnr / ssim, k_train.cu kernels):
 // apps::coverage_fraction and apps::greedy_plan (src/apps.cpp:53-116).
 // Integer work on a tx-major table of FP64 dBm values, exact like the
 // reference: a threshold test per (tx, candidate), counts, and a greedy
@@ -166,6 +167,42 @@ int rxgs_greedy_plan(rxgs_ctx ctx, const double* table, int64_t tx_count, int64_
     RXGS_CUDA(cudaMemcpyAsync(order_out, t_ord.p, sizeof(int) * k, cudaMemcpyDefault, s));
     RXGS_CUDA(cudaStreamSynchronize(s));
     ctx->launches += 2;
+    return RXGS_OK;
+}
+
+int rxgs_image_metrics(rxgs_ctx ctx, const void* pred, int pred_f32, const double* gt, int n_img, int h, int w,
+                       double max_val, const double ssim_opts[3], double* out) {
+    if (!ctx || !out || !pred || !gt) return fail(RXGS_ERR_INVALID, "image_metrics: null argument");
+    if (n_img < 1 || h < 0 || w < 0 || static_cast<int64_t>(h) * w == 0)
+        return fail(RXGS_ERR_INVALID, "mae: need equal non-empty inputs");
+    const int win = ssim_opts ? static_cast<int>(ssim_opts[0]) : 11;
+    const double sigma = ssim_opts ? ssim_opts[1] : 1.5, dyn = ssim_opts ? ssim_opts[2] : 1.0;
+    if (win > 0 && (h < win || w < win)) return fail(RXGS_ERR_INVALID, "ssim: image smaller than the window");
+    if (win > 64) return fail(RXGS_ERR_INVALID, "image_metrics: ssim window above 64");
+    RXGS_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const size_t n = static_cast<size_t>(n_img) * h * w;
+    DevBuf t_p, t_g, t_ws, t_out;
+    const void* d_p = pred;
+    const double* d_g = gt;
+    if (!dev_ptr(pred)) {
+        const size_t b = n * (pred_f32 ? sizeof(float) : sizeof(double));
+        RXGS_CUDA(t_p.ensure(b));
+        RXGS_CUDA(cudaMemcpyAsync(t_p.p, pred, b, cudaMemcpyHostToDevice, s));
+        d_p = t_p.p;
+    }
+    if (!dev_ptr(gt)) {
+        RXGS_CUDA(t_g.ensure(n * sizeof(double)));
+        RXGS_CUDA(cudaMemcpyAsync(t_g.p, gt, n * sizeof(double), cudaMemcpyHostToDevice, s));
+        d_g = t_g.as<double>();
+    }
+    RXGS_CUDA(t_ws.ensure(image_metrics_ws_bytes(n_img, h, w, win > 0 ? win : 0)));
+    RXGS_CUDA(t_out.ensure(sizeof(double) * 4 * n_img));
+    RXGS_CUDA(launch_image_metrics(n_img, h, w, d_p, pred_f32 != 0, d_g, max_val, win > 0 ? win : 0, sigma, dyn,
+                                   t_ws.p, t_out.as<double>(), s));
+    RXGS_CUDA(cudaMemcpyAsync(out, t_out.p, sizeof(double) * 4 * n_img, cudaMemcpyDefault, s));
+    RXGS_CUDA(cudaStreamSynchronize(s));
+    ctx->launches += win > 0 ? 5 : 2;
     return RXGS_OK;
 }
 

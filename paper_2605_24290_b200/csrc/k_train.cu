@@ -1005,4 +1005,154 @@ cudaError_t launch_geo_post(rxgs_scene_s& sc, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------- metrics
+// met::mae / mse / psnr / ssim (metrics.cpp:11-112) for a batch of images:
+// fixed-order per-image sums, SSIM through the same separable window passes
+// as the loss (any window size up to kMetMaxWin, the 1-D factor of
+// gaussian_window normalised so its outer product sums to 1).
+constexpr int kMetMaxWin = 64, kMetParts = 16;
+__constant__ double c_met_g[kMetMaxWin];
+
+namespace {
+
+template <typename TP>
+__global__ void k_met_sums(int P, const TP* __restrict__ pred, const double* __restrict__ gt, double* __restrict__ part) {
+    __shared__ double red[2][256];
+    const int j = blockIdx.y;
+    double l1 = 0.0, sq = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
+        const double d = static_cast<double>(pred[static_cast<size_t>(j) * P + i]) - gt[static_cast<size_t>(j) * P + i];
+        l1 += fabs(d);
+        sq += d * d;
+    }
+    red[0][threadIdx.x] = l1;
+    red[1][threadIdx.x] = sq;
+    __syncthreads();
+    for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+        if (threadIdx.x < st) {
+            red[0][threadIdx.x] += red[0][threadIdx.x + st];
+            red[1][threadIdx.x] += red[1][threadIdx.x + st];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[(static_cast<size_t>(j) * gridDim.x + blockIdx.x) * 2] = red[0][0];
+        part[(static_cast<size_t>(j) * gridDim.x + blockIdx.x) * 2 + 1] = red[1][0];
+    }
+}
+
+template <typename TP>
+__global__ void k_met_ssim_h(int h, int w, int win, const TP* __restrict__ pred, const double* __restrict__ gt,
+                             double* __restrict__ H) {
+    const int cols = w - win + 1;
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = blockIdx.y, j = blockIdx.z;
+    if (c >= cols) return;
+    const TP* x = pred + (static_cast<size_t>(j) * h + r) * w + c;
+    const double* y = gt + (static_cast<size_t>(j) * h + r) * w + c;
+    double s[5] = {0, 0, 0, 0, 0};
+    for (int t = 0; t < win; ++t) {
+        const double g = c_met_g[t], xv = static_cast<double>(x[t]), yv = y[t];
+        s[0] += g * xv;
+        s[1] += g * yv;
+        s[2] += g * xv * xv;
+        s[3] += g * yv * yv;
+        s[4] += g * xv * yv;
+    }
+    const size_t plane = static_cast<size_t>(h) * cols;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) H[(static_cast<size_t>(j) * 5 + q) * plane + static_cast<size_t>(r) * cols + c] = s[q];
+}
+
+__global__ void k_met_ssim_v(int h, int w, int win, double c1, double c2, const double* __restrict__ H,
+                             double* __restrict__ S) {
+    const int cols = w - win + 1, rows = h - win + 1;
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = blockIdx.y, j = blockIdx.z;
+    if (c >= cols) return;
+    const size_t hplane = static_cast<size_t>(h) * cols;
+    double m[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        const double* hq = H + (static_cast<size_t>(j) * 5 + q) * hplane + static_cast<size_t>(r) * cols + c;
+        double a = 0.0;
+        for (int t = 0; t < win; ++t) a += c_met_g[t] * hq[static_cast<size_t>(t) * cols];
+        m[q] = a;
+    }
+    const double mx = m[0], my = m[1];
+    const double vx = m[2] - mx * mx, vy = m[3] - my * my, cov = m[4] - mx * my;
+    const double a1 = 2.0 * mx * my + c1, b1 = mx * mx + my * my + c1;
+    const double a2 = 2.0 * cov + c2, b2 = vx + vy + c2;
+    S[static_cast<size_t>(j) * rows * cols + static_cast<size_t>(r) * cols + c] = (a1 * a2) / (b1 * b2);
+}
+
+__global__ void k_met_final(int n_img, int P, double max_val, const double* __restrict__ part,
+                            const double* __restrict__ ssim, double* __restrict__ out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n_img) return;
+    double l1 = 0.0, sq = 0.0;
+    for (int b = 0; b < kMetParts; ++b) {
+        l1 += part[(static_cast<size_t>(j) * kMetParts + b) * 2];
+        sq += part[(static_cast<size_t>(j) * kMetParts + b) * 2 + 1];
+    }
+    const double mse = sq / static_cast<double>(P);
+    out[4 * j] = l1 / static_cast<double>(P);
+    out[4 * j + 1] = mse;
+    out[4 * j + 2] = mse == 0.0 ? 300.0 : 10.0 * log10(max_val * max_val / mse);  // kDbSentinel (metrics.hpp:12)
+    out[4 * j + 3] = ssim ? ssim[j] : nan("");
+}
+
+}  // namespace
+
+size_t image_metrics_ws_bytes(int n_img, int h, int w, int win) {
+    size_t b = sizeof(double) * static_cast<size_t>(n_img) * kMetParts * 2;
+    if (win > 0) {
+        const size_t cols = w - win + 1, rows = h - win + 1;
+        b += sizeof(double) * static_cast<size_t>(n_img) * (5 * h * cols + rows * cols + 1);
+    }
+    return b;
+}
+
+cudaError_t launch_image_metrics(int n_img, int h, int w, const void* pred, bool pred_f32, const double* gt,
+                                 double max_val, int win, double sigma, double dyn, void* ws, double* out,
+                                 cudaStream_t s) {
+    const int P = h * w;
+    double* part = static_cast<double*>(ws);
+    double* ssim = nullptr;
+    if (pred_f32)
+        k_met_sums<float><<<dim3(kMetParts, n_img), 256, 0, s>>>(P, static_cast<const float*>(pred), gt, part);
+    else
+        k_met_sums<double><<<dim3(kMetParts, n_img), 256, 0, s>>>(P, static_cast<const double*>(pred), gt, part);
+    if (win > 0) {
+        if (win > kMetMaxWin) return cudaErrorInvalidValue;
+        double g[kMetMaxWin], sum = 0.0;  // gaussian_window (metrics.cpp:38-51), 1-D factor
+        const int half = win / 2;
+        for (int t = 0; t < win; ++t) {
+            const double d = t - half;
+            g[t] = std::exp(-(d * d) / (2.0 * sigma * sigma));
+            sum += g[t];
+        }
+        for (int t = 0; t < win; ++t) g[t] /= sum;
+        cudaError_t e = cudaMemcpyToSymbolAsync(c_met_g, g, sizeof(double) * win, 0, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return e;
+        const int cols = w - win + 1, rows = h - win + 1;
+        double* H = part + static_cast<size_t>(n_img) * kMetParts * 2;
+        double* S = H + static_cast<size_t>(n_img) * 5 * h * cols;
+        ssim = S + static_cast<size_t>(n_img) * rows * cols;
+        const double c1 = 0.01 * dyn * 0.01 * dyn, c2 = 0.03 * dyn * 0.03 * dyn;
+        const int tb = 128;
+        if (pred_f32)
+            k_met_ssim_h<float><<<dim3((cols + tb - 1) / tb, h, n_img), tb, 0, s>>>(h, w, win,
+                                                                                 static_cast<const float*>(pred), gt, H);
+        else
+            k_met_ssim_h<double><<<dim3((cols + tb - 1) / tb, h, n_img), tb, 0, s>>>(
+                h, w, win, static_cast<const double*>(pred), gt, H);
+        k_met_ssim_v<<<dim3((cols + tb - 1) / tb, rows, n_img), tb, 0, s>>>(h, w, win, c1, c2, H, S);
+        k_ssim_mean<<<n_img, 256, 0, s>>>(rows, cols, S, ssim);
+    }
+    k_met_final<<<(n_img + 127) / 128, 128, 0, s>>>(n_img, P, max_val, part, ssim, out);
+    return cudaGetLastError();
+}
+
 }  // namespace rxgs_b200

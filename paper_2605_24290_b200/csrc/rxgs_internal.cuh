@@ -355,6 +355,11 @@ cudaError_t launch_degree_mask(int64_t n, int L, int per_comp, int active, doubl
 cudaError_t launch_add64(int64_t n, const double* a, double* out, cudaStream_t s);
 cudaError_t launch_check_groups(int64_t n, const GroupBounds& b, const double* g, int* bad, cudaStream_t s);
 cudaError_t launch_geo_post(rxgs_scene_s& sc, cudaStream_t s);
+// met::{mae, mse, psnr, ssim} of a batch of images (k_train.cu)
+size_t image_metrics_ws_bytes(int n_img, int h, int w, int win);
+cudaError_t launch_image_metrics(int n_img, int h, int w, const void* pred, bool pred_f32, const double* gt,
+                                 double max_val, int win, double sigma, double dyn, void* ws, double* out,
+                                 cudaStream_t s);
 // host copies of a scene whose device arrays the optimizer updated
 int scene_sync_host(rxgs_scene_s* sc);
 cudaError_t launch_adam(int64_t n, double* w, const double* g, double* m, double* v, double lr, int64_t step,

@@ -58,3 +58,60 @@ def test_on_a_rendered_coverage_table(ctx, capi, ref):
     thr = float(np.median(table))
     assert np.array_equal(ctx.greedy_plan(table, 6, thr), ref.greedy_plan(table, 6, thr))
     assert ctx.coverage_fraction(table, [0, 5, 9], thr) == ref.coverage_fraction(table, [0, 5, 9], thr)
+
+
+# ---------------------------------------------------------------- metrics
+@pytest.mark.parametrize("n,h,w,opts,max_val,f32", [
+    (3, 20, 30, (11, 1.5, 1.0), 1.0, False),
+    (2, 90, 360, (11, 1.5, 1.0), 2.0, True),
+    (4, 16, 12, (7, 2.0, 2.0), 3.0, False),
+    (2, 9, 14, (8, 1.0, 1.0), 1.0, True),  # even window: half = n / 2 as in gaussian_window
+])
+def test_image_metrics_match_reference(ctx, ref, n, h, w, opts, max_val, f32):
+    """met::mae / mse / psnr / ssim (metrics.cpp:11-112) per image on the device vs
+    the reference build (rel_err <= 1e-12 in FP64; f32 predictions are widened)."""
+    rng = np.random.default_rng(n * h + w)
+    gt = rng.uniform(0, 2, size=(n, h, w))
+    pred = gt + rng.normal(0, 0.2, size=gt.shape)
+    if f32:
+        pred = pred.astype(np.float32)
+    got = ctx.image_metrics(pred, gt, h, w, max_val, opts)
+    for i in range(n):
+        want = ref.image_metrics(pred[i].astype(np.float64), gt[i], h, w, max_val, *opts)
+        np.testing.assert_allclose(got[i], want, rtol=1e-12, atol=1e-14)
+
+
+def test_image_metrics_edges(ctx, ref, capi):
+    gt = np.random.default_rng(1).uniform(0, 1, size=(2, 12, 12))
+    out = ctx.image_metrics(gt.copy(), gt, 12, 12)
+    assert (out[:, 2] == 300.0).all() and (out[:, 0] == 0).all()  # kDbSentinel on identical inputs
+    np.testing.assert_allclose(out[:, 3], 1.0, rtol=1e-14)
+    no_ssim = ctx.image_metrics(gt + 0.1, gt, 12, 12, ssim=None)
+    assert np.isnan(no_ssim[:, 3]).all()
+    np.testing.assert_allclose(no_ssim[:, 0], 0.1, rtol=1e-12)
+    with pytest.raises(capi.InvalidArgument, match="ssim: image smaller than the window"):
+        ctx.image_metrics(gt[:, :10, :10].copy(), gt[:, :10, :10].copy(), 10, 10)
+    with pytest.raises(ValueError, match="ssim: image smaller than the window"):
+        ref.image_metrics(gt[0, :10, :10].ravel(), gt[0, :10, :10].ravel(), 10, 10)
+
+
+def test_image_metrics_on_rendered_spectra(ctx, ref, capi):
+    """Evaluation of rendered spectra (f32 on the device, as rxgs_render_queries
+    writes them) against FP64 reference renders of the same queries."""
+    import torch
+    sc = capi.synth_scene(2000, 2, 1, 7)
+    scene = ctx.scene(sc, "spectrum")
+    grid = capi.Grid(18, 72, 8, 1.0)
+    rx = capi.synth_points(3, 11, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
+    st = scene.tx_state(np.array([0.3, -0.2, 0.1]), grid)
+    spec, _ = scene.render_queries(None, st, rx)
+    spec = np.asarray(spec, np.float32).reshape(3, grid.cells)
+    import oracle as O
+    rsc = ref.scene(sc, "spectrum")
+    og = O.Grid(18, 72, 8, 1.0)
+    gt = np.stack([ref.predict(rsc, None, og, [0.3, -0.2, 0.1], rx[j]) for j in range(3)]).reshape(3, -1)
+    got = ctx.image_metrics(torch.from_numpy(spec).cuda(), torch.from_numpy(gt).cuda(), 18, 72, 1.0)
+    for j in range(3):
+        want = ref.image_metrics(spec[j].astype(np.float64), gt[j], 18, 72, 1.0)
+        np.testing.assert_allclose(got[j], want, rtol=1e-12, atol=1e-14)
+    assert (got[:, 3] > 0.999).all()  # the B200 render agrees with the reference render
