@@ -173,6 +173,23 @@ int rxgs_backward_render(rxgs_ctx ctx, rxgs_txstate st, rxgs_scene scene, const 
  * device; e.g. rxgs_coverage_table's output widened to f64).  Exact:
  * threshold tests and counts; greedy ties break on the lower candidate.
  * greedy_plan writes k candidate indices in selection order. */
+/* ------------------------------------------------------------ Stage-I densification
+ * densify_and_prune (scene.cpp:178-274, scene.hpp:69-97) on the device, in
+ * place: the scene's row set becomes the reference's (in-place rows, then
+ * clones / second split children in source order, then the prune), with
+ * the split signs drawn from derive_stream(seed, "scene.densify",
+ * pass_index).  grad_accum / accum_count: the DensifyState (K each, host or
+ * device); thresholds = {grad_threshold, size_frac, prune_extent_frac,
+ * split_scale_factor} (NULL: DensifyThresholds defaults).  report =
+ * {cloned, split, pruned}; source_row (new K entries, caller-sized for 2K)
+ * maps each row to its source row or -1.  TxStates built before the call
+ * are stale. */
+int rxgs_densify_and_prune(rxgs_ctx ctx, rxgs_scene scene, const double* grad_accum, const int32_t* accum_count,
+                           double scene_extent, const double thresholds[4], uint64_t seed, uint64_t pass_index,
+                           int32_t report[3], int32_t* source_row, int32_t* new_count);
+/* reset_transmittance (scene.cpp:276-279): every tau logit = logit(0.01). */
+int rxgs_reset_transmittance(rxgs_scene scene);
+
 /* met::mae / mse / psnr / ssim (metrics.hpp:14-28, metrics.cpp:11-112) of a
  * batch of n_img images (h x w row-major; pred f32 if pred_f32 else f64, gt
  * f64; host or device): out[4*i..] = {mae, mse, psnr(max_val), ssim}.

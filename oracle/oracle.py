@@ -139,6 +139,11 @@ class Checker:
                 "coverage_fraction": (C.c_int, [_dp, C.c_long, C.c_long, _ip, C.c_int, C.c_double, _dp,
                                                 C.c_char_p, C.c_int]),
                 "greedy_plan": (C.c_int, [_dp, C.c_long, C.c_long, C.c_int, C.c_double, _ip, C.c_char_p, C.c_int]),
+                "scene_count": (C.c_int, [C.c_void_p]),
+                "scene_get": (None, [C.c_void_p, _dp, _dp, _dp, _dp, _dp]),
+                "densify": (C.c_int, [C.c_void_p, _dp, C.c_int, C.c_double, _dp, C.c_ulong, C.c_ulong, _ip, _ip,
+                                      C.c_char_p, C.c_int]),
+                "reset_transmittance": (None, [C.c_void_p]),
                 "image_metrics": (C.c_int, [_dp, _dp, C.c_int, C.c_int, C.c_double, C.c_int, C.c_double,
                                             C.c_double, _dp, C.c_char_p, C.c_int]),
                 "train_sample": (C.c_int, [C.c_void_p, C.c_void_p, _ip, _dp, _dp, _dp, _dp, C.c_double,
@@ -467,6 +472,34 @@ def _image_metrics(self, pred, gt, h, w, max_val=1.0, window=11, sigma=1.5, dyn=
     return out
 
 
+def _scene_arrays(self, h):
+    """Current arrays of a reference scene handle (after densify_and_prune)."""
+    k = self._scene_count(h.ptr)
+    sc = h.data
+    L = (sc["l_max"] + 1) ** 2
+    out = dict(positions=np.empty(3 * k), log_scales=np.empty(3 * k), quaternions=np.empty(4 * k),
+               tau_logits=np.empty(k), fle_coeffs=np.empty(k * L * sc["channels"] * 2))
+    self._scene_get(h.ptr, *[_d(v) for v in out.values()])
+    return out
+
+
+def _densify(self, h, d_pos_list, extent, thresholds=(2e-4, 0.01, 0.1, 0.8), seed=1, pass_index=0):
+    """densify_and_prune (scene.cpp:178-274) on the handle's scene, in place;
+    d_pos_list: accumulate() inputs (n_acc x K*3) -> (report, source_row)."""
+    k = self._scene_count(h.ptr)
+    acc = np.ascontiguousarray(d_pos_list, np.float64).reshape(-1, 3 * k)
+    thr = np.ascontiguousarray(thresholds, np.float64)
+    report = np.zeros(3, np.int32)
+    src = np.zeros(2 * k + 1, np.int32)
+    err = C.create_string_buffer(512)
+    if self._densify(h.ptr, acc.ctypes.data_as(_dp), acc.shape[0], float(extent), thr.ctypes.data_as(_dp), int(seed),
+                     int(pass_index), report.ctypes.data_as(_ip), src.ctypes.data_as(_ip), err, 512):
+        raise ValueError(err.value.decode())
+    return report, src[: self._scene_count(h.ptr)]
+
+
+Checker.scene_arrays = _scene_arrays
+Checker.densify = _densify
 Checker.image_metrics = _image_metrics
 Checker.coverage_fraction = _coverage_fraction
 Checker.greedy_plan = _greedy_plan

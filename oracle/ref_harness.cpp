@@ -203,6 +203,47 @@ void ref_scene_bounds(void* h, double inflate, double* lo, double* hi) {
         hi[a] = b.hi[a];
     }
 }
+int ref_scene_count(void* h) { return static_cast<Handle*>(h)->scene.count(); }
+void ref_scene_get(void* h, double* pos, double* ls, double* q, double* tau, double* coeffs) {
+    const GaussianScene& s = static_cast<Handle*>(h)->scene;
+    std::memcpy(pos, s.positions.data(), s.positions.size() * sizeof(double));
+    std::memcpy(ls, s.log_scales.data(), s.log_scales.size() * sizeof(double));
+    std::memcpy(q, s.quaternions.data(), s.quaternions.size() * sizeof(double));
+    std::memcpy(tau, s.tau_logits.data(), s.tau_logits.size() * sizeof(double));
+    std::memcpy(coeffs, s.fle_coeffs.data(), s.fle_coeffs.size() * sizeof(double));
+}
+// densify_and_prune (scene.cpp:178-274) in place on the handle's scene, from
+// a DensifyState built with accumulate() calls of the given d_positions
+// (n_acc of them, K*3 each); report = {cloned, split, pruned}; source_row has
+// room for 2K entries.  reset_transmittance (scene.cpp:276-279) if reset_tau.
+int ref_densify(void* h, const double* d_pos_list, int n_acc, double extent, const double* thr, unsigned long seed,
+                unsigned long pass, int* report, int* source_row, char* err, int errlen) {
+    try {
+        GaussianScene& s = static_cast<Handle*>(h)->scene;
+        DensifyState st;
+        st.resize(s.count());
+        st.scene_extent = extent;
+        const std::size_t n3 = 3 * static_cast<std::size_t>(s.count());
+        for (int a = 0; a < n_acc; ++a)
+            st.accumulate(std::vector<double>(d_pos_list + a * n3, d_pos_list + (a + 1) * n3));
+        DensifyThresholds t;
+        t.grad_threshold = thr[0];
+        t.size_frac = thr[1];
+        t.prune_extent_frac = thr[2];
+        t.split_scale_factor = thr[3];
+        const DensifyReport r = densify_and_prune(s, st, t, seed, pass);
+        report[0] = r.cloned;
+        report[1] = r.split;
+        report[2] = r.pruned;
+        std::copy(r.source_row.begin(), r.source_row.end(), source_row);
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return 1;
+    }
+}
+void ref_reset_transmittance(void* h) { reset_transmittance(static_cast<Handle*>(h)->scene); }
+
 void ref_covariance(void* h, double* out) {
     const GaussianScene& s = static_cast<Handle*>(h)->scene;
     for (int k = 0; k < s.count(); ++k) {

@@ -122,6 +122,9 @@ _SIG = {
     "rxgs_checkpoint_save": (C.c_int, [C.c_char_p, _vp, C.POINTER(Grid), _vp]),
     "rxgs_checkpoint_load": (C.c_int, [_vp, C.c_char_p, C.POINTER(_vp), C.POINTER(Grid), C.POINTER(_vp)]),
     "rxgs_coverage_fraction": (C.c_int, [_vp, _vp, _i64, _i64, _vp, C.c_int, C.c_double, C.POINTER(C.c_double)]),
+    "rxgs_densify_and_prune": (C.c_int, [_vp, _vp, _vp, _vp, C.c_double, _vp, C.c_uint64, C.c_uint64, _vp, _vp,
+                                         C.POINTER(_i32)]),
+    "rxgs_reset_transmittance": (C.c_int, [_vp]),
     "rxgs_image_metrics": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int, C.c_int, C.c_int, C.c_double, _vp, _vp]),
     "rxgs_greedy_plan": (C.c_int, [_vp, _vp, _i64, _i64, C.c_int, C.c_double, _vp]),
     "rxgs_scene_info": (C.c_int, [_vp, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32)]),
@@ -394,6 +397,23 @@ class Scene:
         if getattr(self, "h", None):
             _fn(self.h)
             self.h = None
+
+    def densify_and_prune(self, grad_accum, accum_count, extent, thresholds=None, seed=1, pass_index=0):
+        """densify_and_prune (scene.cpp:178-274) in place -> (report, source_row)."""
+        acc = grad_accum if hasattr(grad_accum, "data_ptr") else np.ascontiguousarray(grad_accum, np.float64)
+        cnt = accum_count if hasattr(accum_count, "data_ptr") else np.ascontiguousarray(accum_count, np.int32)
+        thr = None if thresholds is None else np.ascontiguousarray(thresholds, np.float64)
+        report = np.zeros(3, np.int32)
+        src = np.zeros(2 * self.k + 1, np.int32)
+        nk = _i32()
+        _check(_lib.rxgs_densify_and_prune(self.ctx.h, self.h, ptr(acc), ptr(cnt), float(extent),
+                                           None if thr is None else thr.ctypes.data, int(seed), int(pass_index),
+                                           report.ctypes.data, src.ctypes.data, C.byref(nk)))
+        self.k = nk.value
+        return report, src[: self.k]
+
+    def reset_transmittance(self):
+        _check(_lib.rxgs_reset_transmittance(self.h))
 
     def bounds(self, inflate=0.0):
         lo, hi = _out(3), _out(3)

@@ -376,6 +376,36 @@ void ctx_release(rxgs_ctx ctx) {
 }
 }  // namespace rxgs_b200
 
+namespace rxgs_b200 {
+int scene_resized(rxgs_scene_s* sc) {
+    rxgs_ctx ctx = sc->ctx;
+    RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    const size_t K = static_cast<size_t>(sc->k);
+    auto down = [](std::vector<double>& h, const DevBuf& d, size_t n) {
+        h.resize(n);
+        return n ? cudaMemcpy(h.data(), d.p, n * sizeof(double), cudaMemcpyDeviceToHost) : cudaSuccess;
+    };
+    RXGS_CUDA(down(sc->h_pos, sc->d_pos, 3 * K));
+    RXGS_CUDA(down(sc->h_ls, sc->d_ls, 3 * K));
+    RXGS_CUDA(down(sc->h_q, sc->d_q, 4 * K));
+    RXGS_CUDA(down(sc->h_tau, sc->d_tau, K));
+    RXGS_CUDA(down(sc->h_coeffs, sc->d_coeffs64, K * sc->L * sc->channels * 2));
+    sc->host_stale = sc->geo_stale = false;
+    sc->pos_index.clear();
+    sc->pos_index_built = false;
+    std::vector<float> p4(4 * std::max<size_t>(K, 1), 0.f);
+    for (size_t i = 0; i < K; ++i)
+        for (int a = 0; a < 3; ++a) p4[4 * i + a] = static_cast<float>(sc->h_pos[3 * i + a]);
+    DevBuf p32;
+    RXGS_CUDA(p32.ensure(p4.size() * sizeof(float)));
+    RXGS_CUDA(cudaMemcpy(p32.p, p4.data(), p4.size() * sizeof(float), cudaMemcpyHostToDevice));
+    sc->d_pos32 = std::move(p32);
+    sc->d_morton = DevBuf();
+    sc->d_mpos32 = DevBuf();
+    return build_scene_order(ctx, *sc, ctx->stream);
+}
+}  // namespace rxgs_b200
+
 extern "C" {
 
 int rxgs_ctx_destroy(rxgs_ctx ctx) {

@@ -49,6 +49,15 @@ int cuda_fail(cudaError_t e, const char* what);
         if (e__ != cudaSuccess) return ::rxgs_b200::cuda_fail(e__, #call); \
     } while (0)
 
+#define TRY_RC(expr)                      \
+    do {                                  \
+        const int rc__ = (expr);          \
+        if (rc__ != RXGS_OK) return rc__; \
+    } while (0)
+
+// initial SplitMix64 state of the reference's derive_stream (synth.cpp)
+uint64_t derive_stream_state(uint64_t seed, const char* tag, uint64_t counter);
+
 // Grow-only device buffer.
 struct DevBuf {
     void* p = nullptr;
@@ -360,6 +369,17 @@ size_t image_metrics_ws_bytes(int n_img, int h, int w, int win);
 cudaError_t launch_image_metrics(int n_img, int h, int w, const void* pred, bool pred_f32, const double* gt,
                                  double max_val, int win, double sigma, double dyn, void* ws, double* out,
                                  cudaStream_t s);
+// Stage-I densification (k_densify.cu)
+cudaError_t launch_dens_accumulate(int K, const double* dpos, double* accum, int* count, cudaStream_t s);
+cudaError_t launch_remap_rows(int n_rows, int width, const int* source, const double* in, double* out,
+                              cudaStream_t s);
+cudaError_t launch_fill64(int64_t n, double v, double* x, cudaStream_t s);
+// densify_and_prune on the scene's device arrays (replaced in place, then
+// scene_resized); source_out[new K] = source row or -1
+int densify_scene(rxgs_ctx ctx, rxgs_scene_s* sc, const double* d_accum, const int* d_count, double extent,
+                  const double thr[4], uint64_t stream_state, int report[3], DevBuf& source_out);
+// host copies + f32 mirrors + Morton order after the scene's row set changed
+int scene_resized(rxgs_scene_s* sc);
 // host copies of a scene whose device arrays the optimizer updated
 int scene_sync_host(rxgs_scene_s* sc);
 cudaError_t launch_adam(int64_t n, double* w, const double* g, double* m, double* v, double lr, int64_t step,

@@ -54,6 +54,13 @@ Stream stream(uint64_t seed, const std::string& tag, uint64_t counter = 0) {
 
 }  // namespace
 
+namespace rxgs_b200 {
+// initial state of derive_stream(seed, tag, counter) (rng.hpp:67-72)
+uint64_t derive_stream_state(uint64_t seed, const char* tag, uint64_t counter) {
+    return stream(seed, tag, counter).s;
+}
+}  // namespace rxgs_b200
+
 extern "C" {
 
 int rxgs_synth_scene(int k, int l_max, int channels, uint64_t seed, double* pos, double* ls,
