@@ -334,6 +334,19 @@ int rxgs_train_apply(rxgs_trainer t);
  * {position lr_init, lr_final, total_steps, delay_mult, delay_steps,
  *  transmittance_lr, scaling_lr, rotation_lr, fle_ramp_interval}. */
 int rxgs_trainer_enable_geometry(rxgs_trainer t, const double geo[9]);
+/* Stage I (train_stage1, trainer.cpp:294-380) is the joint step with
+ * cond == NULL at rxgs_trainer_create: the scene's own coefficients render,
+ * d_base is backward_render's d_coeffs, and rxgs_train_apply accumulates the
+ * DensifyState (||d_position|| per Gaussian, scene.cpp:141-151).
+ * rxgs_train_densify runs one densification tick on it (densify_and_prune +
+ * Optimizer::remap_rows of every per-Gaussian group, trainer.cpp:359-372;
+ * thresholds as rxgs_densify_and_prune); rxgs_train_reset_transmittance is
+ * reset_transmittance + optimizer.reset("transmittance") (trainer.cpp:354-358).
+ * Both need rxgs_trainer_enable_geometry; the flat gradient buffer is
+ * reallocated by rxgs_train_densify (query rxgs_train_grad_buffer again). */
+int rxgs_train_densify(rxgs_trainer t, double scene_extent, const double thresholds[4], uint64_t seed,
+                       uint64_t pass_index, int32_t report[3]);
+int rxgs_train_reset_transmittance(rxgs_trainer t);
 int rxgs_train_get_geometry_grads(rxgs_trainer t, double* d_positions, double* d_log_scales,
                                   double* d_quaternions, double* d_tau_logits);
 int64_t rxgs_train_step_count(rxgs_trainer t);

@@ -415,13 +415,13 @@ def _train_sample(self, scene_h, cond_h, grid: Grid, tx, rx, target, lambda_ssim
     sc = scene_h.data
     k = len(sc["tau_logits"])
     L = (sc["l_max"] + 1) ** 2
-    n_par = len(cond_h.data["params"])
+    n_par = len(cond_h.data["params"]) if cond_h is not None else 0
     loss = np.zeros(1)
     d_base = np.empty(k * L * sc["channels"] * 2)
     d_par = np.empty(n_par)
     geo = [np.empty(k * 3), np.empty(k * 3), np.empty(k * 4), np.empty(k)] if geometry else [None] * 4
     err = C.create_string_buffer(512)
-    rc = self._train_sample(scene_h.ptr, cond_h.ptr, grid.gi, grid.gd, _d(np.asarray(tx, np.float64)),
+    rc = self._train_sample(scene_h.ptr, None if cond_h is None else cond_h.ptr, grid.gi, grid.gd, _d(np.asarray(tx, np.float64)),
                             _d(np.asarray(rx, np.float64)), _d(np.asarray(target, np.float64)), lambda_ssim,
                             lambda_fft, 1, loss.ctypes.data_as(_dp), d_base.ctypes.data_as(_dp),
                             d_par.ctypes.data_as(_dp), *[None if g is None else g.ctypes.data_as(_dp) for g in geo],

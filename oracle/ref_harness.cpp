@@ -685,12 +685,13 @@ int ref_train_sample(void* scene, void* cond, const int* gi, const double* gd, c
                      char* err, int errlen) {
     try {
         const GaussianScene& sc = static_cast<Handle*>(scene)->scene;
-        auto& st = *static_cast<cond::ConditioningState*>(cond);
+        // cond == NULL: the unconditioned Stage-I chain (trainer.cpp:317-340)
+        auto* stp = static_cast<cond::ConditioningState*>(cond);
         const auto grid = make_grid(gi, gd);
         const raster::TxState ts = raster::build_tx_state(sc, {tx[0], tx[1], tx[2]}, grid);
         cond::ConditionWorkspace ws;
-        const auto coeffs =
-            cond::condition_forward(st, sc.fle_coeffs, sc, {rx[0], rx[1], rx[2]}, &ws);
+        const auto coeffs = stp ? cond::condition_forward(*stp, sc.fle_coeffs, sc, {rx[0], rx[1], rx[2]}, &ws)
+                                : sc.fle_coeffs;
         const auto field = raster::render_field(ts, sc, coeffs, 1, threads);
         const auto pred = raster::aggregate_modality(field, Modality::Spectrum, grid)[0];
         raster::Measurement gt;
@@ -705,16 +706,20 @@ int ref_train_sample(void* scene, void* cond, const int* gi, const double* gd, c
         const auto dv = raster::aggregate_modality_backward(field, Modality::Spectrum, grid,
                                                             {lr.d_pred});
         const auto b = raster::backward_render(ts, sc, coeffs, 1, dv, threads);
-        std::vector<double> db(sc.fle_coeffs.size(), 0.0);
-        cond::ConditioningGrads g;
-        g.resize(st);
-        cond::condition_backward(st, ws, sc.fle_coeffs, b.d_coeffs, db, g);
-        std::memcpy(d_base, db.data(), db.size() * sizeof(double));
-        std::size_t off = 0;
-        for_each_grad(g, [&](std::vector<double>& v) {
-            std::memcpy(d_params + off, v.data(), v.size() * sizeof(double));
-            off += v.size();
-        });
+        if (stp) {
+            std::vector<double> db(sc.fle_coeffs.size(), 0.0);
+            cond::ConditioningGrads g;
+            g.resize(*stp);
+            cond::condition_backward(*stp, ws, sc.fle_coeffs, b.d_coeffs, db, g);
+            std::memcpy(d_base, db.data(), db.size() * sizeof(double));
+            std::size_t off = 0;
+            for_each_grad(g, [&](std::vector<double>& v) {
+                std::memcpy(d_params + off, v.data(), v.size() * sizeof(double));
+                off += v.size();
+            });
+        } else {
+            std::memcpy(d_base, b.d_coeffs.data(), b.d_coeffs.size() * sizeof(double));
+        }
         if (d_pos) std::memcpy(d_pos, b.d_positions.data(), b.d_positions.size() * sizeof(double));
         if (d_ls) std::memcpy(d_ls, b.d_log_scales.data(), b.d_log_scales.size() * sizeof(double));
         if (d_q) std::memcpy(d_q, b.d_quaternions.data(), b.d_quaternions.size() * sizeof(double));

@@ -115,6 +115,8 @@ _SIG = {
     "rxgs_train_get_grads": (C.c_int, [_vp, _vp, _vp]),
     "rxgs_train_allreduce": (C.c_int, [_vp, _vp]),
     "rxgs_trainer_enable_geometry": (C.c_int, [_vp, _vp]),
+    "rxgs_train_densify": (C.c_int, [_vp, C.c_double, _vp, C.c_uint64, C.c_uint64, _vp]),
+    "rxgs_train_reset_transmittance": (C.c_int, [_vp]),
     "rxgs_train_get_geometry_grads": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "rxgs_train_apply": (C.c_int, [_vp]),
     "rxgs_train_step_count": (_i64, [_vp]),
@@ -627,15 +629,34 @@ class Trainer:
         self.ctx, self.scene, self.cond = ctx, scene, cond
         hp = np.asarray(hyper if hyper is not None else self.DEFAULTS, np.float64)
         h = _vp()
-        _check(_lib.rxgs_trainer_create(ctx.h, scene.h, cond.h, hp.ctypes.data, C.byref(h)))
+        _check(_lib.rxgs_trainer_create(ctx.h, scene.h, None if cond is None else cond.h, hp.ctypes.data,
+                                        C.byref(h)))
         self.h = h
         self.geometry = geometry is not None and geometry is not False
         if self.geometry:
             geo = np.asarray(self.GEOMETRY_DEFAULTS if geometry is True else geometry, np.float64)
             _check(_lib.rxgs_trainer_enable_geometry(self.h, geo.ctypes.data))
+        self._refresh()
+
+    def _refresh(self):
         p, n, nb = _vp(), _i64(), _i64()
         _check(_lib.rxgs_train_grad_buffer(self.h, C.byref(p), C.byref(n), C.byref(nb)))
         self.grad_ptr, self.n, self.n_base = p.value, n.value, nb.value
+
+    def densify(self, extent, thresholds=None, seed=1, pass_index=0):
+        """One Stage-I densification tick (trainer.cpp:359-372) -> report (cloned, split, pruned)."""
+        rep = np.zeros(3, np.int32)
+        thr = None if thresholds is None else np.ascontiguousarray(thresholds, np.float64)
+        _check(_lib.rxgs_train_densify(self.h, float(extent), None if thr is None else thr.ctypes.data, int(seed),
+                                       int(pass_index), rep.ctypes.data))
+        k = _i32()
+        _check(_lib.rxgs_scene_info(self.scene.h, C.byref(k), None, None, None))
+        self.scene.k = k.value
+        self._refresh()
+        return rep
+
+    def reset_transmittance(self):
+        _check(_lib.rxgs_train_reset_transmittance(self.h))
 
     def __del__(self, _fn=_lib.rxgs_trainer_destroy):
         if getattr(self, "h", None):
@@ -658,7 +679,7 @@ class Trainer:
 
     def get_grads(self):
         db = np.empty(self.n_base)
-        dp = np.empty(self.cond.param_count)
+        dp = np.empty(self.cond.param_count if self.cond is not None else 0)
         _check(_lib.rxgs_train_get_grads(self.h, db.ctypes.data, dp.ctypes.data))
         return db, dp
 

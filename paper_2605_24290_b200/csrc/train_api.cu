@@ -38,6 +38,10 @@ struct rxgs_trainer_s {
     double tau_lr = 1e-2, scale_lr = 5e-3, rot_lr = 1e-3;
     int64_t n_geo = 0;
     DevBuf co64, dv64, b_sig, b_eg, b_eds, b_rg, b_rds, geo_tmp;
+    // DensifyState (scene.hpp:69-79) of the Stage-I loop, accumulated in apply
+    DevBuf dens_acc, dens_cnt;
+    // optimizer.reset("transmittance") restarts that group's Adam count
+    int64_t tau_step0 = 0;
     int64_t n_total() const { return n_base + n_par + n_geo; }
 };
 
@@ -70,8 +74,15 @@ int geometry_grads(rxgs_trainer t, rxgs_txstate_s& st, const double* d_rx, int n
     const int K = sc->k;
     const size_t nco = static_cast<size_t>(n_rx) * K * sc->L * sc->channels * 2;
     RXGS_CUDA(t->co64.ensure(std::max<size_t>(nco, 1) * sizeof(double)));
-    RXGS_CUDA(launch_cond_materialize(*t->c, *sc, d_rx, n_rx, ctx->ag.as<float>(), t->co64.as<double>(), nullptr,
-                                      nullptr, s));
+    if (t->c) {
+        RXGS_CUDA(launch_cond_materialize(*t->c, *sc, d_rx, n_rx, ctx->ag.as<float>(), t->co64.as<double>(), nullptr,
+                                          nullptr, s));
+    } else {  // Stage I: every receiver sees the scene's own coefficients
+        const size_t one = nco / std::max(n_rx, 1);
+        for (int j = 0; j < n_rx; ++j)
+            RXGS_CUDA(cudaMemcpyAsync(t->co64.as<double>() + j * one, sc->d_coeffs64.p, one * sizeof(double),
+                                      cudaMemcpyDeviceToDevice, s));
+    }
     RXGS_CUDA(t->dv64.ensure(std::max<size_t>(static_cast<size_t>(n_rx) * 2 * P, 1) * sizeof(double)));
     RXGS_CUDA(launch_dv_from_G(n_rx, P, t->G.as<float2>(), t->dv64.as<double>(), s));
     const size_t n_jc = static_cast<size_t>(n_rx) * sc->channels;
@@ -114,10 +125,10 @@ double lr_at(const rxgs_trainer_s& t, int64_t step) {
 extern "C" {
 
 int rxgs_trainer_create(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const double hyper[8], rxgs_trainer* out) {
-    if (!ctx || !sc || !c || !out) return fail(RXGS_ERR_INVALID, "rxgs_trainer_create: null argument");
+    if (!ctx || !sc || !out) return fail(RXGS_ERR_INVALID, "rxgs_trainer_create: null argument");
     if (sc->modality != 2 || sc->channels != 1)
         return fail(RXGS_ERR_INVALID, "train: the B200 training step supports the spectrum modality with C == 1");
-    if (c->hidden != 64 || c->C != 1 || c->l_max != sc->l_max)
+    if (c && (c->hidden != 64 || c->C != 1 || c->l_max != sc->l_max))
         return fail(RXGS_ERR_INVALID, "train: conditioning must have hidden == 64, C == 1 and the scene's l_max");
     RXGS_CUDA(cudaSetDevice(ctx->device));
     auto* t = new rxgs_trainer_s;
@@ -139,7 +150,7 @@ int rxgs_trainer_create(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const double h
         return fail(RXGS_ERR_INVALID, "train: loss weights must be non-negative");
     }
     t->n_base = static_cast<int64_t>(sc->k) * sc->L * sc->channels * 2;
-    t->n_par = c->n_params;
+    t->n_par = c ? c->n_params : 0;
     const size_t n = static_cast<size_t>(t->n_base + t->n_par);
     if (t->grad.ensure(n * 8) != cudaSuccess || t->m.ensure(n * 8) != cudaSuccess || t->v.ensure(n * 8) != cudaSuccess) {
         delete t;
@@ -171,6 +182,8 @@ int rxgs_train_grads(rxgs_trainer t, rxgs_txstate st, const double* rx, int n_rx
     rxgs_scene sc = t->sc;
     rxgs_cond c = t->c;
     if (st->k != sc->k) return fail(RXGS_ERR_INVALID, "train: tx state / scene mismatch");
+    if (t->n_base != static_cast<int64_t>(sc->k) * sc->L * sc->channels * 2)
+        return fail(RXGS_ERR_INVALID, "train: the scene changed size outside rxgs_train_densify");
     RXGS_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
     const DevGrid& g = st->grid;
@@ -190,7 +203,7 @@ int rxgs_train_grads(rxgs_trainer t, rxgs_txstate st, const double* rx, int n_rx
                                   cudaMemcpyHostToDevice, s));
         d_tg = t->target.as<float>();
     }
-    if (c->use_local()) {
+    if (c && c->use_local()) {
         RXGS_CUDA(ctx->err_flag.ensure(16));
         const int big = INT_MAX;
         RXGS_CUDA(cudaMemcpyAsync(ctx->err_flag.p, &big, sizeof(int), cudaMemcpyHostToDevice, s));
@@ -207,7 +220,10 @@ int rxgs_train_grads(rxgs_trainer t, rxgs_txstate st, const double* rx, int n_rx
     RXGS_CUDA(launch_refresh_gb(*sc, *st, s));
     const size_t ag_n = static_cast<size_t>(n_rx) * sc->L * 4;
     RXGS_CUDA(ctx->ag.ensure(ag_n * sizeof(float)));
-    RXGS_CUDA(launch_cond_global(*c, d_rx, n_rx, ctx->ag.as<float>(), s));
+    if (c)
+        RXGS_CUDA(launch_cond_global(*c, d_rx, n_rx, ctx->ag.as<float>(), s));
+    else
+        RXGS_CUDA(cudaMemsetAsync(ctx->ag.p, 0, ag_n * sizeof(float), s));
     RXGS_CUDA(ctx->signals.ensure(std::max<size_t>(static_cast<size_t>(sc->k) * n_rx, 1) * sizeof(float2)));
     // FP32 SIMT forward (conditioning + compositing): its field is ~10x closer
     // to the FP64 reference than the bf16x3 tensor-core path, which the
@@ -249,11 +265,15 @@ int rxgs_train_grads(rxgs_trainer t, rxgs_txstate st, const double* rx, int n_rx
     double* gpar = gbase + t->n_base;
     const int nl = local_grad_n();
     RXGS_CUDA(t->part.ensure(sizeof(float) * static_cast<size_t>(t->n_parts) * nl));
-    RXGS_CUDA(launch_cond_bwd(*c, *sc, *st, d_rx, n_rx, ctx->ag.as<float>(), t->d_s.as<float2>(), t->u.as<float2>(),
+    if (!c)  // no conditioning: the adjoint of the mid coefficients is the signal adjoint
+        RXGS_CUDA(cudaMemcpyAsync(t->u.p, t->d_s.p, sizeof(float2) * static_cast<size_t>(sc->k) * n_rx,
+                                  cudaMemcpyDeviceToDevice, s));
+    else
+        RXGS_CUDA(launch_cond_bwd(*c, *sc, *st, d_rx, n_rx, ctx->ag.as<float>(), t->d_s.as<float2>(), t->u.as<float2>(),
                               t->part.as<float>(), t->n_parts, s));
-    if (c->use_local()) RXGS_CUDA(launch_reduce_parts(t->n_parts, nl, t->part.as<float>(), gpar + c->o_lw1, s));
+    if (c && c->use_local()) RXGS_CUDA(launch_reduce_parts(t->n_parts, nl, t->part.as<float>(), gpar + c->o_lw1, s));
     RXGS_CUDA(launch_dbase(c, *sc, *st, n_rx, ctx->ag.as<float>(), t->u.as<float2>(), gbase, s));
-    if (c->use_global()) {
+    if (c && c->use_global()) {
         const int npair = n_rx * c->L;
         const size_t n_gpar = static_cast<size_t>(c->F * 3) + (c->o_emb - c->o_gw1) + static_cast<size_t>(c->L) * c->dc;
         RXGS_CUDA(t->red_part.ensure(sizeof(double) * 4 * static_cast<size_t>(t->n_red) * npair));
@@ -372,6 +392,11 @@ int rxgs_trainer_enable_geometry(rxgs_trainer t, const double geo[9]) {
     std::swap(t->grad, g);
     std::swap(t->m, m);
     std::swap(t->v, v);
+    const size_t K = std::max(t->sc->k, 1);
+    RXGS_CUDA(t->dens_acc.ensure(sizeof(double) * K));
+    RXGS_CUDA(t->dens_cnt.ensure(sizeof(int) * K));
+    RXGS_CUDA(cudaMemset(t->dens_acc.p, 0, sizeof(double) * K));
+    RXGS_CUDA(cudaMemset(t->dens_cnt.p, 0, sizeof(int) * K));
     return RXGS_OK;
 }
 
@@ -416,8 +441,9 @@ int rxgs_train_apply(rxgs_trainer t) {
         int64_t start;
     };
     const int64_t P0 = t->n_base;
-    std::vector<Seg> segs = {{"features", 0},
-                             {"cond.freqs", P0 + static_cast<int64_t>(c->o_freq)},
+    std::vector<Seg> segs = {{"features", 0}};
+    if (c)
+        segs.insert(segs.end(), {{"cond.freqs", P0 + static_cast<int64_t>(c->o_freq)},
                              {"cond.global.w1", P0 + static_cast<int64_t>(c->o_gw1)},
                              {"cond.global.b1", P0 + static_cast<int64_t>(c->o_gb1)},
                              {"cond.global.w2", P0 + static_cast<int64_t>(c->o_gw2)},
@@ -430,7 +456,7 @@ int rxgs_train_apply(rxgs_trainer t) {
                              {"cond.local.w2", P0 + static_cast<int64_t>(c->o_lw2)},
                              {"cond.local.b2", P0 + static_cast<int64_t>(c->o_lb2)},
                              {"cond.local.w3", P0 + static_cast<int64_t>(c->o_lw3)},
-                             {"cond.local.b3", P0 + static_cast<int64_t>(c->o_lb3)}};
+                             {"cond.local.b3", P0 + static_cast<int64_t>(c->o_lb3)}});
     if (t->geo) {
         const int64_t G0 = P0 + t->n_par, K = sc->k;
         segs.push_back({"position", G0});
@@ -470,20 +496,100 @@ int rxgs_train_apply(rxgs_trainer t) {
                     {sc->d_tau.as<double>(), G0 + 3 * K, K, t->tau_lr},
                     {sc->d_ls.as<double>(), G0 + 4 * K, 3 * K, t->scale_lr},
                     {sc->d_q.as<double>(), G0 + 7 * K, 4 * K, t->rot_lr}};
-        for (const auto& e : geo)
-            RXGS_CUDA(launch_adam(e.n, e.w, g + e.off, m + e.off, v + e.off, e.lr, t->step, t->b1, t->b2, t->eps, 0,
-                                  1, 1.0, nullptr, s));
+        // DensifyState::accumulate(bundle.d_positions) (trainer.cpp:341)
+        RXGS_CUDA(launch_dens_accumulate(sc->k, g + G0, t->dens_acc.as<double>(), t->dens_cnt.as<int>(), s));
+        for (int e = 0; e < 4; ++e)
+            RXGS_CUDA(launch_adam(geo[e].n, geo[e].w, g + geo[e].off, m + geo[e].off, v + geo[e].off, geo[e].lr,
+                                  e == 1 ? t->step - t->tau_step0 : t->step, t->b1, t->b2, t->eps, 0, 1, 1.0, nullptr,
+                                  s));
         RXGS_CUDA(launch_geo_post(*sc, s));  // renormalize_quaternions + f32 position mirrors
         sc->geo_stale = true;
         ctx->launches += 5;
     }
     RXGS_CUDA(launch_adam(t->n_base, sc->d_coeffs64.as<double>(), g, m, v, t->feature_lr, t->step, t->b1, t->b2,
                           t->eps, sc->L, sc->channels * 2, t->rest_ratio, nullptr, s));
-    RXGS_CUDA(launch_adam(t->n_par, c->d_params64.as<double>(), g + P0, m + P0, v + P0, t->cond_lr, t->step, t->b1,
-                          t->b2, t->eps, 0, 1, 1.0, c->d_params32.as<float>(), s));
+    if (c)
+        RXGS_CUDA(launch_adam(t->n_par, c->d_params64.as<double>(), g + P0, m + P0, v + P0, t->cond_lr, t->step, t->b1,
+                              t->b2, t->eps, 0, 1, 1.0, c->d_params32.as<float>(), s));
     ctx->launches += 3;
     sc->host_stale = true;
-    c->host_stale = true;
+    if (c) c->host_stale = true;
+    return RXGS_OK;
+}
+
+// One Stage-I densification tick (trainer.cpp:359-372): densify_and_prune
+// from the trainer's DensifyState, Optimizer::remap_rows of every
+// per-Gaussian group (position, scaling, rotation, transmittance, features),
+// conditioning moments kept, DensifyState reset to the new size.
+int rxgs_train_densify(rxgs_trainer t, double scene_extent, const double thresholds[4], uint64_t seed,
+                       uint64_t pass_index, int32_t report[3]) {
+    if (!t) return fail(RXGS_ERR_INVALID, "null trainer");
+    if (!t->geo) return fail(RXGS_ERR_INVALID, "train: densification needs rxgs_trainer_enable_geometry");
+    rxgs_ctx ctx = t->ctx;
+    rxgs_scene sc = t->sc;
+    RXGS_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const double def[4] = {2e-4, 0.01, 0.1, 0.8};
+    const int K0 = sc->k;
+    const int stride = sc->L * sc->channels * 2;
+    TRY(scene_sync_host(sc));
+    DevBuf src;
+    int rep[3];
+    TRY(densify_scene(ctx, sc, t->dens_acc.as<double>(), t->dens_cnt.as<int>(), scene_extent,
+                      thresholds ? thresholds : def, derive_stream_state(seed, "scene.densify", pass_index), rep,
+                      src));
+    const int K = sc->k;
+    const int64_t nb0 = t->n_base, G0old = t->n_base + t->n_par;
+    t->n_base = static_cast<int64_t>(K) * stride;
+    t->n_geo = 11 * static_cast<int64_t>(K);
+    const int64_t G0 = t->n_base + t->n_par;
+    const size_t n = static_cast<size_t>(t->n_total());
+    DevBuf g, m, v;
+    RXGS_CUDA(g.ensure(n * 8));
+    RXGS_CUDA(m.ensure(n * 8));
+    RXGS_CUDA(v.ensure(n * 8));
+    RXGS_CUDA(cudaMemsetAsync(g.p, 0, n * 8, s));
+    const int* sr = src.as<int>();
+    const DevBuf* olds[2] = {&t->m, &t->v};
+    DevBuf* news[2] = {&m, &v};
+    for (int b = 0; b < 2; ++b) {
+        const double* in = olds[b]->as<double>();
+        double* out = news[b]->as<double>();
+        RXGS_CUDA(launch_remap_rows(K, stride, sr, in, out, s));  // features
+        if (t->n_par)
+            RXGS_CUDA(cudaMemcpyAsync(out + t->n_base, in + nb0, sizeof(double) * t->n_par, cudaMemcpyDeviceToDevice, s));
+        RXGS_CUDA(launch_remap_rows(K, 3, sr, in + G0old, out + G0, s));                   // position
+        RXGS_CUDA(launch_remap_rows(K, 1, sr, in + G0old + 3 * K0, out + G0 + 3 * K, s));  // transmittance
+        RXGS_CUDA(launch_remap_rows(K, 3, sr, in + G0old + 4 * K0, out + G0 + 4 * K, s));  // scaling
+        RXGS_CUDA(launch_remap_rows(K, 4, sr, in + G0old + 7 * K0, out + G0 + 7 * K, s));  // rotation
+    }
+    RXGS_CUDA(cudaStreamSynchronize(s));
+    t->grad = std::move(g);
+    t->m = std::move(m);
+    t->v = std::move(v);
+    DevBuf acc, cnt;
+    RXGS_CUDA(acc.ensure(sizeof(double) * std::max(K, 1)));
+    RXGS_CUDA(cnt.ensure(sizeof(int) * std::max(K, 1)));
+    RXGS_CUDA(cudaMemset(acc.p, 0, sizeof(double) * std::max(K, 1)));
+    RXGS_CUDA(cudaMemset(cnt.p, 0, sizeof(int) * std::max(K, 1)));
+    t->dens_acc = std::move(acc);
+    t->dens_cnt = std::move(cnt);
+    if (report)
+        for (int a = 0; a < 3; ++a) report[a] = rep[a];
+    ctx->launches += 10;
+    return RXGS_OK;
+}
+
+// reset_transmittance + optimizer.reset("transmittance") (trainer.cpp:354-358)
+int rxgs_train_reset_transmittance(rxgs_trainer t) {
+    if (!t) return fail(RXGS_ERR_INVALID, "null trainer");
+    if (!t->geo) return fail(RXGS_ERR_INVALID, "train: transmittance reset needs rxgs_trainer_enable_geometry");
+    TRY(rxgs_reset_transmittance(t->sc));
+    const int64_t off = t->n_base + t->n_par + 3 * static_cast<int64_t>(t->sc->k);
+    cudaStream_t s = t->ctx->stream;
+    RXGS_CUDA(cudaMemsetAsync(t->m.as<double>() + off, 0, sizeof(double) * t->sc->k, s));
+    RXGS_CUDA(cudaMemsetAsync(t->v.as<double>() + off, 0, sizeof(double) * t->sc->k, s));
+    t->tau_step0 = t->step;
     return RXGS_OK;
 }
 

@@ -303,3 +303,81 @@ def test_train_nonfinite_group_names(ctx, capi, ref):
     with pytest.raises(capi.RxgsError, match="non-finite gradient in group 'features'"):
         tr.apply()
     assert tr.step_count == 0
+
+
+def _stage1_setup(capi, ctx, ref, k=400, seed=7, big=()):
+    import oracle as O
+    sc = capi.synth_scene(k, 2, 1, seed)
+    if big:
+        ls = sc["log_scales"].copy()
+        ls[list(big)] = np.log(5.0)
+        sc = dict(sc, log_scales=ls)
+    scene = ctx.scene(sc, "spectrum")
+    grid = capi.Grid(18, 36, 8, 1.0)
+    return sc, scene, grid, O.Grid(18, 36, 8, 1.0)
+
+
+def test_stage1_grads_match_reference(ctx, capi, ref):
+    """Stage-I step (train_stage1, trainer.cpp:317-340): no conditioning, the
+    scene's coefficients render; d_base = backward_render's d_coeffs and the
+    geometry gradients, summed over the batch, vs the reference."""
+    sc, scene, grid, og = _stage1_setup(capi, ctx, ref)
+    rx = capi.synth_points(2, 31, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
+    tg = _targets(2, grid.cells, 12)
+    tr = capi.Trainer(ctx, scene, None, geometry=True)
+    assert tr.n == tr.n_base + 11 * scene.k
+    loss = tr.grads(scene.tx_state(TX, grid), rx, tg)
+    db, dp = tr.get_grads()
+    assert dp.size == 0
+    geo = tr.get_geometry_grads()
+    rs = ref.scene(sc, "spectrum")
+    want = [0.0] * 5
+    for j in range(2):
+        r = ref.train_sample(rs, None, og, TX, rx[j], tg[j].astype(np.float64), geometry=True)
+        assert rel_err(loss[j], r["loss"]) < TOL
+        for i, key in enumerate(("d_base", "d_positions", "d_log_scales", "d_quaternions", "d_tau_logits")):
+            want[i] = want[i] + r[key]
+    assert rel_err(db, want[0]).max() < TOL
+    for got, w in zip(geo, want[1:]):
+        assert rel_err(got, w).max() < TOL
+
+
+def test_stage1_densify_and_tau_reset(ctx, capi, ref):
+    """Stage-I policy ticks through the trainer (trainer.cpp:351-372):
+    DensifyState accumulated per step, densify_and_prune == the reference's on
+    the same state, the optimizer state remapped (training continues on the
+    new row set), reset_transmittance + a fresh Adam count for that group."""
+    sc, scene, grid, og = _stage1_setup(capi, ctx, ref, big=(3, 77))
+    rx = capi.synth_points(1, 37, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
+    tg = _targets(1, grid.cells, 13)
+    tr = capi.Trainer(ctx, scene, None, geometry=True)
+    d_pos = []
+    for _ in range(2):
+        tr.grads(scene.tx_state(TX, grid), rx, tg)
+        d_pos.append(tr.get_geometry_grads()[0])
+        tr.apply()
+    before = capi.scene_arrays(scene)
+    thr, extent, seed = (1e-6, 0.01, 0.1, 0.8), 40.0, 5
+    rep = tr.densify(extent, thr, seed, 2)
+    h = ref.scene(dict(sc, positions=before["positions"].reshape(-1, 3),
+                       log_scales=before["log_scales"].reshape(-1, 3),
+                       quaternions=before["quaternions"].reshape(-1, 4), tau_logits=before["tau_logits"],
+                       fle_coeffs=before["fle_coeffs"].reshape(-1, 9, 1, 2)), "spectrum")
+    rrep, rsrc = ref.densify(h, np.stack(d_pos), extent, thr, seed, 2)
+    assert list(rep) == list(rrep) and min(rep) > 0, rep
+    got, want = capi.scene_arrays(scene), ref.scene_arrays(h)
+    for key in want:
+        np.testing.assert_allclose(got[key], want[key], rtol=1e-15, atol=1e-15, err_msg=key)
+    assert scene.k == len(rsrc) and tr.n == tr.n_base + 11 * scene.k
+    # training continues on the new rows
+    loss = tr.grads(scene.tx_state(TX, grid), rx, tg)
+    assert np.isfinite(loss).all()
+    tr.apply()
+    # transmittance reset: logit(0.01) everywhere, then that group's Adam restarts at step 1
+    tr.reset_transmittance()
+    tau0 = capi.scene_arrays(scene)["tau_logits"]
+    assert np.array_equal(tau0, np.full(scene.k, np.log(0.01 / (1.0 - 0.01))))
+    tr.grads(scene.tx_state(TX, grid), rx, tg)
+    gtau = tr.get_geometry_grads()[3]
+    tr.apply()
+    assert rel_err(capi.scene_arrays(scene)["tau_logits"], _adam1(tau0, gtau, 1e-2)).max() < 1e-12
