@@ -9,6 +9,10 @@
 
 #include <cstdint>
 
+#ifndef RXGS_RELU_CVT
+#define RXGS_RELU_CVT 1
+#endif
+
 namespace rxgs_b200 {
 namespace x2 {
 
@@ -46,17 +50,22 @@ __device__ __forceinline__ float2 bc(float x) { return make_float2(x, x); }
 // a).  hi = a truncated to bf16 (same sign as a, |hi| <= |a|), lo = the exact
 // FP32 remainder a - hi rounded to bf16 (same sign again), so max(., 0) on
 // the packed halves is ReLU(a) split: hi + lo = relu(a) within 2^-16 |a|.
-// 7 instructions per pair (PRMT, 2 LOP3, FADD2, F2FP, 2 HMNMX2).
+// The ReLU of lo rides on the conversion (F2FP.RELU): 6 instructions per
+// pair (PRMT, 2 LOP3, FADD2, F2FP.RELU, HMNMX2).
 __device__ __forceinline__ void relu_split_bf16(float a, float b, uint32_t& hi, uint32_t& lo) {
     uint32_t h;
     asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(h) : "r"(__float_as_uint(a)), "r"(__float_as_uint(b)));
     const float2 t = make_float2(__uint_as_float(__float_as_uint(a) & 0xFFFF0000u),
                                  __uint_as_float(__float_as_uint(b) & 0xFFFF0000u));
     const float2 r = sub(make_float2(a, b), t);
+#if RXGS_RELU_CVT
+    asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(r.y), "f"(r.x));
+#else
     uint32_t l;
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(r.y), "f"(r.x));
-    asm("max.bf16x2 %0, %1, %2;" : "=r"(hi) : "r"(h), "r"(0u));
     asm("max.bf16x2 %0, %1, %2;" : "=r"(lo) : "r"(l), "r"(0u));
+#endif
+    asm("max.bf16x2 %0, %1, %2;" : "=r"(hi) : "r"(h), "r"(0u));
 }
 
 // Same split without the ReLU (layer-1 features).

@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // A/B-measured (scripts/ab_variants.sh): 2 of the 8 sample pairs plus the
 // FLE in the layer-1 window, the rest of the probe in the layer-2 window.
 #ifndef RXGS_PROBE_FIRST_PAIRS
-#define RXGS_PROBE_FIRST_PAIRS 2
+#define RXGS_PROBE_FIRST_PAIRS 3
 #endif
 #ifndef RXGS_FLE_FIRST
 #define RXGS_FLE_FIRST 1
