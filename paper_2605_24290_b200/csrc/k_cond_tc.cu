@@ -444,12 +444,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float tfirst = S == 1 ? 0.5f : 0.05f;
     uint32_t phase = 0;
 
-    // tile -> (row r, receiver j) of this thread
-    auto coords = [&](long long tile, int& r, int& j) {
-        const int gb = static_cast<int>(tile / nq);
-        const int jq = static_cast<int>(tile - static_cast<long long>(gb) * nq);
-        r = gb * 32 + lane;
-        j = jq * 4 + wl;
+    // tile -> (row r, receiver j) of this thread; tile = gb * nq + jq, advanced
+    // by `step` incrementally (no 64-bit division in the loop)
+    const int step_gb = static_cast<int>(step / nq), step_jq = static_cast<int>(step % nq);
+    int cur_gb = 0, cur_jq = 0;
+    auto coords_init = [&](long long tile, int& r, int& j) {
+        cur_gb = static_cast<int>(tile / nq);
+        cur_jq = static_cast<int>(tile - static_cast<long long>(cur_gb) * nq);
+        r = cur_gb * 32 + lane;
+        j = cur_jq * 4 + wl;
+    };
+    auto coords_next = [&](int& r, int& j) {
+        cur_gb += step_gb;
+        cur_jq += step_jq;
+        if (cur_jq >= nq) {
+            cur_jq -= nq;
+            ++cur_gb;
+        }
+        r = cur_gb * 32 + lane;
+        j = cur_jq * 4 + wl;
     };
     constexpr bool kSplit = ST >= 2 && ST % 2 == 0 && RT > 0;
 // A/B-measured (scripts/ab_variants.sh): 2 of the 8 sample pairs plus the
@@ -530,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int r = 0, j = 0;
     float in[6];
     if (tile < tiles) {  // prologue: features of the first tile
-        coords(tile, r, j);
+        coords_init(tile, r, j);
         const bool act = r < n_rows && j < n_rx;
         float4 pk = make_float4(0.f, 0.f, 0.f, 0.f);
         float qx = 0.f, qy = 0.f, qz = 0.f;
@@ -576,7 +589,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool active = r < n_rows && j < n_rx;
         const long long ntile = tile + step;
         int rn = 0, jn = 0;
-        coords(ntile, rn, jn);
+        coords_next(rn, jn);
         const bool nact = ntile < tiles && rn < n_rows && jn < n_rx;
         // prefetch the next tile's row position / receiver and this row's output index
         float4 pkn = make_float4(0.f, 0.f, 0.f, 0.f);
