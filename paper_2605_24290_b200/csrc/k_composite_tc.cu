@@ -44,6 +44,10 @@ __device__ __forceinline__ uint32_t mn_off(int mn, int k, uint32_t lbo) {
     return static_cast<uint32_t>((k >> 3) * lbo + (mn >> 3) * kSBO + (k & 7) * 16 + (mn & 7) * 2);
 }
 
+#ifndef RXGS_COMP_RX_FAST
+#define RXGS_COMP_RX_FAST 1
+#endif
+
 template <bool FIELD>
 __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t* __restrict__ tile_offsets,
                                                        const int* __restrict__ list, const float* __restrict__ tw,
@@ -56,12 +60,20 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
     __shared__ uint32_t tbase_s;
     __shared__ float s_dom[8];  // solid angle of the tile's 8 rows
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#if RXGS_COMP_RX_FAST  // receiver blocks of one tile back to back: its weight rows stay in L2
+    const int tile = blockIdx.y;
+#else
     const int tile = blockIdx.x;
+#endif
     if (tid < 8) {  // zero for rows past the grid (partial last tile row)
         const int row = (tile / g.tiles_p) * 8 + tid;
         s_dom[tid] = row < g.nt ? static_cast<float>(sin(g.tmin + (row + 0.5) * g.dth) * g.dth * g.dph) : 0.f;
     }
+#if RXGS_COMP_RX_FAST
+    const int j0 = blockIdx.x * (kM / 2);
+#else
     const int j0 = blockIdx.y * (kM / 2);
+#endif
     const int W = walk_len[tile];
     const int64_t begin = tile_offsets[tile];
 
@@ -335,7 +347,11 @@ cudaError_t launch_composite_tc(const rxgs_txstate_s& st, const uint2* d_sig, in
     auto kern = out.field32 ? k_composite_tc<true> : k_composite_tc<false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
+#if RXGS_COMP_RX_FAST
+    dim3 grid((n_rx + kM / 2 - 1) / (kM / 2), g.n_tiles);
+#else
     dim3 grid(g.n_tiles, (n_rx + kM / 2 - 1) / (kM / 2));
+#endif
     kern<<<grid, kThr, smem, s>>>(g, st.tile_offsets.as<int64_t>(), st.list.as<int>(), st.tw.as<float>(),
                                             st.walk_len.as<int>(), d_sig, n_rx, out.spectrum, out.rssi_partial,
                                             out.field32);
