@@ -357,7 +357,10 @@ cudaError_t launch_cond_global(const rxgs_cond_s& c, const double* d_rx, int n_r
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaError_t e = cudaFuncSetAttribute(k_cond_global, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    k_cond_global<<<std::min(n_rx, 2 * sms), kGlobThreads, smem, s>>>(d, d_rx, n_rx, d_ag);
+#ifndef RXGS_GLOB_CTAS_PER_SM
+#define RXGS_GLOB_CTAS_PER_SM 4  // A/B (2, 4, 8): 4 resident CTAs per SM hide the FP64 chains best
+#endif
+    k_cond_global<<<std::min(n_rx, RXGS_GLOB_CTAS_PER_SM * sms), kGlobThreads, smem, s>>>(d, d_rx, n_rx, d_ag);
     return cudaGetLastError();
 }
 
