@@ -963,7 +963,7 @@ int rxgs_backward_render(rxgs_ctx ctx, rxgs_txstate st, rxgs_scene sc, const dou
     if (!st->regrouped) RX_TRY(train_regroup(ctx, *st, s));
     const size_t E = std::max<int64_t>(st->entries, 1);
     RXGS_CUDA(b_sig.ensure(std::max<size_t>(K * n_jc, 1) * sizeof(double2)));
-    RXGS_CUDA(b_eg.ensure(E * 7 * sizeof(double)));
+    RXGS_CUDA(b_eg.ensure(bwd_geo_bytes(st->entries, static_cast<int>(n_jc))));
     RXGS_CUDA(b_eds.ensure(E * n_jc * sizeof(double2)));
     RXGS_CUDA(b_rg.ensure(std::max<size_t>(K, 1) * 7 * sizeof(double)));
     RXGS_CUDA(b_rds.ensure(std::max<size_t>(K * n_jc, 1) * sizeof(double2)));

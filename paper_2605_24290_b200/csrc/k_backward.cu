@@ -106,10 +106,13 @@ __global__ void k_signals64(int K, int L, int C, int n_rx, const int* __restrict
 __global__ void __launch_bounds__(64) k_bwd_walk(DevGrid g, int cb, const int64_t* __restrict__ tile_offsets,
                                                  const int* __restrict__ list, const GaussRec* __restrict__ rec,
                                                  const int* __restrict__ walk_len, const double2* __restrict__ sig,
-                                                 int n_jc, const double* __restrict__ dvals, int jc0, int nc,
+                                                 int n_jc, const double* __restrict__ dvals, int64_t n_ent,
                                                  double* __restrict__ ent_geo, double2* __restrict__ ent_ds) {
     __shared__ double red[2][7 + 2 * kNC];
     const int tile = blockIdx.x, lane = threadIdx.x;
+    // receiver chunk blockIdx.y: its own slice of the per-entry geometry sums
+    const int jc0 = blockIdx.y * kNC, nc = n_jc - jc0 < kNC ? n_jc - jc0 : kNC;
+    ent_geo += static_cast<size_t>(blockIdx.y) * n_ent * 7;
     const int tt = tile / g.tiles_p, tp = tile % g.tiles_p;
     const int lc = cb * kMaxCellsPerBlock + lane;
     const int row = tt * g.ts + lc / g.ts, col = tp * g.ts + lc % g.ts;
@@ -233,14 +236,19 @@ __global__ void __launch_bounds__(64) k_bwd_walk(DevGrid g, int cb, const int64_
 }
 
 // per-Gaussian sums of the walked entries, in tile order
-__global__ void k_bwd_gauss_reduce(int K, int n_jc, const int* __restrict__ goff, const int* __restrict__ gent,
-                                   const double* __restrict__ ent_geo, const double2* __restrict__ ent_ds,
-                                   double* __restrict__ raw_geo, double2* __restrict__ raw_ds) {
+__global__ void k_bwd_gauss_reduce(int K, int n_jc, int n_chunks, int64_t n_ent, const int* __restrict__ goff,
+                                   const int* __restrict__ gent, const double* __restrict__ ent_geo,
+                                   const double2* __restrict__ ent_ds, double* __restrict__ raw_geo,
+                                   double2* __restrict__ raw_ds) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= K) return;
     double acc[7] = {0, 0, 0, 0, 0, 0, 0};
     for (int e = goff[k]; e < goff[k + 1]; ++e)
-        for (int i = 0; i < 7; ++i) acc[i] += ent_geo[static_cast<size_t>(gent[e]) * 7 + i];
+        for (int i = 0; i < 7; ++i) {
+            double v = ent_geo[static_cast<size_t>(gent[e]) * 7 + i];  // receiver chunks in order
+            for (int ch = 1; ch < n_chunks; ++ch) v += ent_geo[(static_cast<size_t>(ch) * n_ent + gent[e]) * 7 + i];
+            acc[i] += v;
+        }
     for (int i = 0; i < 7; ++i) raw_geo[static_cast<size_t>(k) * 7 + i] = acc[i];
     for (int q = 0; q < n_jc; ++q) {
         double2 a = make_double2(0.0, 0.0);
@@ -444,6 +452,10 @@ __global__ void k_bwd_finalize(int K, int l_max, int C, int n_rx, const int* __r
 
 }  // namespace
 
+size_t bwd_geo_bytes(int64_t entries, int n_jc) {
+    return sizeof(double) * 7 * static_cast<size_t>(std::max<int64_t>(entries, 1)) * ((n_jc + kNC - 1) / kNC);
+}
+
 cudaError_t launch_aggregate_bwd(const DevGrid& g, int modality, int n_rx, int channels, const double* values,
                                  const double* up, double* dv, cudaStream_t s) {
     if (n_rx * channels == 0) return cudaSuccess;
@@ -462,20 +474,20 @@ cudaError_t launch_backward_render(const rxgs_txstate_s& st, const rxgs_scene_s&
     if (rows > 0)
         k_signals64<<<static_cast<unsigned>((rows + 255) / 256), 256, 0, s>>>(K, L, C, n_rx, st.culled.as<int>(),
                                                                              st.basis64.as<double>(), d_coeffs_in, sig64);
+    const int n_chunks = (n_jc + kNC - 1) / kNC;
     if (st.entries > 0) {
-        cudaMemsetAsync(ent_geo, 0, sizeof(double) * 7 * st.entries, s);
+        cudaMemsetAsync(ent_geo, 0, sizeof(double) * 7 * st.entries * n_chunks, s);
         cudaMemsetAsync(ent_ds, 0, sizeof(double2) * n_jc * st.entries, s);
+        // receiver chunks run concurrently (disjoint ent_ds columns, own ent_geo slices)
         for (int cb = 0; cb < g.cell_blocks; ++cb)
-            for (int jc0 = 0; jc0 < n_jc; jc0 += kNC) {
-                const int nc = n_jc - jc0 < kNC ? n_jc - jc0 : kNC;
-                k_bwd_walk<<<g.n_tiles, 64, 0, s>>>(g, cb, st.tile_offsets.as<int64_t>(), st.list.as<int>(),
-                                                    st.rec.as<GaussRec>(), st.walk_len.as<int>(), sig64, n_jc,
-                                                    d_values, jc0, nc, ent_geo, ent_ds);
-            }
+            k_bwd_walk<<<dim3(g.n_tiles, n_chunks), 64, 0, s>>>(g, cb, st.tile_offsets.as<int64_t>(),
+                                                                 st.list.as<int>(), st.rec.as<GaussRec>(),
+                                                                 st.walk_len.as<int>(), sig64, n_jc, d_values,
+                                                                 st.entries, ent_geo, ent_ds);
     }
     if (K > 0) {
-        k_bwd_gauss_reduce<<<(K + 127) / 128, 128, 0, s>>>(K, n_jc, st.gauss_off.as<int>(), st.gauss_ent.as<int>(),
-                                                          ent_geo, ent_ds, raw_geo, raw_ds);
+        k_bwd_gauss_reduce<<<(K + 127) / 128, 128, 0, s>>>(K, n_jc, n_chunks, st.entries, st.gauss_off.as<int>(),
+                                                          st.gauss_ent.as<int>(), ent_geo, ent_ds, raw_geo, raw_ds);
         k_bwd_finalize<<<(K + 63) / 64, 64, 0, s>>>(K, st.l_max, C, n_rx, st.culled.as<int>(), st.geom.as<double>(),
                                                     st.basis64.as<double>(), d_coeffs_in, raw_geo, raw_ds,
                                                     sc.d_ls.as<double>(), sc.d_q.as<double>(), d_pos, d_ls, d_q,

@@ -219,7 +219,8 @@ __global__ void __launch_bounds__(512, 1)
 __global__ void k_cond_materialize(CondDev c, int K, const float4* __restrict__ pos32,
                                    const double* __restrict__ rx, int n_rx,
                                    const double* __restrict__ base, const float* __restrict__ ag,
-                                   double* __restrict__ out, double* __restrict__ local_in) {
+                                   double* __restrict__ out, double* __restrict__ local_in,
+                                   const int* __restrict__ rows = nullptr, const int* __restrict__ n_rows = nullptr) {
     extern __shared__ __align__(16) float smem[];
     const int H = c.H, C = c.C, L = c.L;
     const int R3 = (c.probe && c.use_local) ? c.R * c.R * c.R : 0;
@@ -245,8 +246,17 @@ __global__ void k_cond_materialize(CondDev c, int K, const float4* __restrict__ 
     __syncthreads();
     const LocalSmem w{s_occ, s_w1, s_b1, s_w2, s_b2, s_w3, s_b3};
     const long long row = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-    if (row >= static_cast<long long>(K) * n_rx) return;
-    const int j = static_cast<int>(row / K), k = static_cast<int>(row % K);
+    int j, k;
+    if (rows) {  // only the listed rows (the TxState's needed Gaussians, Morton order)
+        const int n = *n_rows;
+        if (row >= static_cast<long long>(n) * n_rx) return;
+        j = static_cast<int>(row / n);
+        k = rows[row % n];
+    } else {
+        if (row >= static_cast<long long>(K) * n_rx) return;
+        j = static_cast<int>(row / K);
+        k = static_cast<int>(row % K);
+    }
     float y[4 * kCMax];
     for (int q = 0; q < 4 * C; ++q) y[q] = 0.f;
     if (c.use_local) {
@@ -418,6 +428,21 @@ cudaError_t launch_cond_materialize(const rxgs_cond_s& c, const rxgs_scene_s& sc
     k_cond_materialize<<<static_cast<unsigned>((rows + 255) / 256), 256, smem, s>>>(
         d, sc.k, sc.d_pos32.as<float4>(), d_rx, n_rx, sc.d_coeffs64.as<double>(), d_ag, d_out,
         d_local_in);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cond_materialize_needed(const rxgs_cond_s& c, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
+                                           const double* d_rx, int n_rx, const float* d_ag, double* d_out,
+                                           cudaStream_t s) {
+    if (st.visible == 0 || n_rx == 0) return cudaSuccess;
+    const CondDev d = make_dev(c);
+    if (d.H > kHMax || d.C > kCMax) return cudaErrorInvalidValue;
+    const size_t smem = local_smem_bytes(d, d.probe && d.use_local);
+    cudaFuncSetAttribute(k_cond_materialize, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    const long long bound = static_cast<long long>(st.visible) * n_rx;
+    k_cond_materialize<<<static_cast<unsigned>((bound + 255) / 256), 256, smem, s>>>(
+        d, sc.k, sc.d_pos32.as<float4>(), d_rx, n_rx, sc.d_coeffs64.as<double>(), d_ag, d_out, nullptr,
+        st.needed_order.as<int>(), st.needed_count.as<int>());
     return cudaGetLastError();
 }
 

@@ -258,6 +258,10 @@ cudaError_t launch_cond_signal(const rxgs_cond_s* c, const rxgs_scene_s& sc,
 cudaError_t launch_cond_materialize(const rxgs_cond_s& c, const rxgs_scene_s& sc,
                                     const double* d_rx, int n_rx, const float* d_ag, double* d_out,
                                     double* d_local_in, int* d_err, cudaStream_t s);
+// the same, only for the TxState's needed Gaussians (other rows untouched)
+cudaError_t launch_cond_materialize_needed(const rxgs_cond_s& c, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
+                                           const double* d_rx, int n_rx, const float* d_ag, double* d_out,
+                                           cudaStream_t s);
 // (re)build rxgs_cond_s::d_occ_cube from d_occ32
 cudaError_t launch_occ_cubes(rxgs_cond_s& c, cudaStream_t s);
 cudaError_t launch_probe(const rxgs_cond_s& c, int n, const double* d_from, const double* d_to,
@@ -326,6 +330,8 @@ cudaError_t launch_cond_backward(const rxgs_cond_s& cs, const rxgs_scene_s& sc, 
 // ---- k_backward.cu (FP64 adjoints of the materialised API)
 cudaError_t launch_aggregate_bwd(const DevGrid& g, int modality, int n_rx, int channels, const double* values,
                                  const double* up, double* dv, cudaStream_t s);
+// bytes of the ent_geo scratch of launch_backward_render (per receiver chunk)
+size_t bwd_geo_bytes(int64_t entries, int n_jc);
 cudaError_t launch_backward_render(const rxgs_txstate_s& st, const rxgs_scene_s& sc, const double* d_coeffs_in,
                                    int n_rx, const double* d_values, double2* sig64, double* ent_geo,
                                    double2* ent_ds, double* raw_geo, double2* raw_ds, double* d_pos, double* d_ls,

@@ -75,8 +75,11 @@ int geometry_grads(rxgs_trainer t, rxgs_txstate_s& st, const double* d_rx, int n
     const size_t nco = static_cast<size_t>(n_rx) * K * sc->L * sc->channels * 2;
     RXGS_CUDA(t->co64.ensure(std::max<size_t>(nco, 1) * sizeof(double)));
     if (t->c) {
-        RXGS_CUDA(launch_cond_materialize(*t->c, *sc, d_rx, n_rx, ctx->ag.as<float>(), t->co64.as<double>(), nullptr,
-                                          nullptr, s));
+        // only the needed rows: the re-walk reads signals of walked entries, and
+        // the basis-jet term only rows with a non-zero signal adjoint
+        RXGS_CUDA(cudaMemsetAsync(t->co64.p, 0, nco * sizeof(double), s));
+        RXGS_CUDA(launch_cond_materialize_needed(*t->c, *sc, st, d_rx, n_rx, ctx->ag.as<float>(), t->co64.as<double>(),
+                                                 s));
     } else {  // Stage I: every receiver sees the scene's own coefficients
         const size_t one = nco / std::max(n_rx, 1);
         for (int j = 0; j < n_rx; ++j)
@@ -88,7 +91,7 @@ int geometry_grads(rxgs_trainer t, rxgs_txstate_s& st, const double* d_rx, int n
     const size_t n_jc = static_cast<size_t>(n_rx) * sc->channels;
     const size_t E = std::max<int64_t>(st.entries, 1);
     RXGS_CUDA(t->b_sig.ensure(std::max<size_t>(K * n_jc, 1) * sizeof(double2)));
-    RXGS_CUDA(t->b_eg.ensure(E * 7 * sizeof(double)));
+    RXGS_CUDA(t->b_eg.ensure(bwd_geo_bytes(st.entries, static_cast<int>(n_jc))));
     RXGS_CUDA(t->b_eds.ensure(E * n_jc * sizeof(double2)));
     RXGS_CUDA(t->b_rg.ensure(std::max<size_t>(K, 1) * 7 * sizeof(double)));
     RXGS_CUDA(t->b_rds.ensure(std::max<size_t>(K * n_jc, 1) * sizeof(double2)));
