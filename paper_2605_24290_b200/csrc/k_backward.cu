@@ -17,7 +17,10 @@
 namespace rxgs_b200 {
 namespace {
 
-constexpr int kNC = 8;  // (receiver, channel) pairs per walk pass
+#ifndef RXGS_BWD_NC
+#define RXGS_BWD_NC 4  // A/B (2, 4, 8) on the joint step: 4
+#endif
+constexpr int kNC = RXGS_BWD_NC;  // (receiver, channel) pairs per walk pass (one receiver chunk)
 
 __device__ __forceinline__ double wrap_pm_pi(double a) {
     a = fmod(a, kTwoPi);
