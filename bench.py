@@ -299,7 +299,10 @@ def run_b200(args):
         avg_ms = cond_ms / cond_n
         achieved = flop_row * per_launch_rows / (avg_ms / 1e3) / 1e12
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per launch (profiles/r1_traffic.json)",
+                    "frac": achieved / peak,
+                    # with tcgen05 at 3 MMAs per product (bf16x3) the pipe's
+                    # usable peak for the same algorithmic FLOP is peak / 3
+                    "frac_of_bf16x3_peak": achieved / (peak / 3.0), "traffic": traffic, "traffic_unit": "bytes per launch (profiles/r1_traffic.json)",
                     "kernel": "cond_signal = k_fle_gemm (FLE reduction, tcgen05 GEMM) + k_cond_tc (probe + local MLP on tcgen05 + affine)",
                     "pipe": "tcgen05 bf16x3 (layers 1-2, FLE GEMM) + FP32 SIMT on FFMA2 (probe, layer 3, affine)", "peak_source": peak_src,
                     "flop_per_row": flop_row, "rows_per_launch": per_launch_rows,
