@@ -18,6 +18,7 @@
 #pragma once
 
 #include <array>
+#include <cmath>
 #include <complex>
 #include <cstdint>
 #include <memory>
@@ -90,6 +91,112 @@ inline std::shared_ptr<SceneHandle> upload(const GaussianScene& s) {
     return h;
 }
 }  // namespace detail
+
+// ---- Stage-I densification (scene.hpp:69-99) on the device
+struct DensifyState {
+    std::vector<double> grad_accum;  // sum of ||dL/dp_k||_2 per Gaussian
+    std::vector<int> accum_count;
+    double scene_extent = 0.0;
+    void resize(int k) {
+        grad_accum.assign(static_cast<std::size_t>(k), 0.0);
+        accum_count.assign(static_cast<std::size_t>(k), 0);
+    }
+    void accumulate(const std::vector<double>& d_positions) {  // scene.cpp:141-151
+        const std::size_t k = grad_accum.size();
+        if (d_positions.size() != 3 * k)
+            throw std::invalid_argument("DensifyState::accumulate: gradient size mismatch");
+        for (std::size_t i = 0; i < k; ++i) {
+            const double gx = d_positions[3 * i], gy = d_positions[3 * i + 1], gz = d_positions[3 * i + 2];
+            grad_accum[i] += std::sqrt(gx * gx + gy * gy + gz * gz);
+            accum_count[i] += 1;
+        }
+    }
+};
+struct DensifyThresholds {
+    double grad_threshold = 2e-4;
+    double size_frac = 0.01;
+    double prune_extent_frac = 0.1;
+    double split_scale_factor = 0.8;
+};
+struct DensifyReport {
+    int cloned = 0, split = 0, pruned = 0;
+    std::vector<int> source_row;
+};
+
+inline DensifyReport densify_and_prune(GaussianScene& scene, DensifyState& state, const DensifyThresholds& t,
+                                       uint64_t seed, uint64_t pass_index) {
+    const int k = scene.count();
+    if (static_cast<int>(state.grad_accum.size()) != k || static_cast<int>(state.accum_count.size()) != k)
+        throw std::invalid_argument("densify_and_prune: state size mismatch");
+    auto h = detail::upload(scene);
+    const double thr[4] = {t.grad_threshold, t.size_frac, t.prune_extent_frac, t.split_scale_factor};
+    int32_t rep[3] = {0, 0, 0}, nk = 0;
+    std::vector<int32_t> src(2 * static_cast<std::size_t>(k) + 1);
+    detail::check(rxgs_densify_and_prune(detail::ctx(), h->h, state.grad_accum.data(), state.accum_count.data(),
+                                         state.scene_extent, thr, seed, pass_index, rep, src.data(), &nk));
+    scene.positions.resize(3 * static_cast<std::size_t>(nk));
+    scene.log_scales.resize(3 * static_cast<std::size_t>(nk));
+    scene.quaternions.resize(4 * static_cast<std::size_t>(nk));
+    scene.tau_logits.resize(static_cast<std::size_t>(nk));
+    scene.fle_coeffs.resize(static_cast<std::size_t>(nk) * scene.coeff_stride());
+    detail::check(rxgs_scene_get_arrays(h->h, scene.positions.data(), scene.log_scales.data(), scene.quaternions.data(),
+                                        scene.tau_logits.data(), scene.fle_coeffs.data()));
+    DensifyReport r;
+    r.cloned = rep[0];
+    r.split = rep[1];
+    r.pruned = rep[2];
+    r.source_row.assign(src.begin(), src.begin() + nk);
+    state.resize(nk);
+    return r;
+}
+
+inline void reset_transmittance(GaussianScene& scene) {  // scene.cpp:276-279
+    auto h = detail::upload(scene);
+    detail::check(rxgs_reset_transmittance(h->h));
+    detail::check(rxgs_scene_get_arrays(h->h, nullptr, nullptr, nullptr, scene.tau_logits.data(), nullptr));
+}
+
+// ---- evaluation metrics (metrics.hpp:10-34) on the device
+namespace met {
+inline constexpr double kDbSentinel = 300.0;
+struct SsimOptions {
+    int window = 11;
+    double sigma = 1.5;
+    double dynamic_range = 1.0;
+};
+namespace detail_m {
+inline std::array<double, 4> all(const std::vector<double>& pred, const std::vector<double>& gt, int h, int w,
+                                 double max_val, const double* opts, const char* who) {
+    if (pred.size() != gt.size() || pred.empty())
+        throw std::invalid_argument(std::string(who) + ": need equal non-empty inputs");
+    std::array<double, 4> out{};
+    detail::check(rxgs_image_metrics(detail::ctx(), pred.data(), 0, gt.data(), 1, h, w, max_val, opts, out.data()));
+    return out;
+}
+}  // namespace detail_m
+inline double mae(const std::vector<double>& pred, const std::vector<double>& gt) {
+    const double o[3] = {0, 1.5, 1.0};
+    return detail_m::all(pred, gt, 1, static_cast<int>(pred.size()), 1.0, o, "mae")[0];
+}
+inline double mse(const std::vector<double>& pred, const std::vector<double>& gt) {
+    const double o[3] = {0, 1.5, 1.0};
+    return detail_m::all(pred, gt, 1, static_cast<int>(pred.size()), 1.0, o, "mse")[1];
+}
+inline double psnr(const std::vector<double>& pred, const std::vector<double>& gt, double max_val) {
+    const double o[3] = {0, 1.5, 1.0};
+    return detail_m::all(pred, gt, 1, static_cast<int>(pred.size()), max_val, o, "mse")[2];
+}
+// the value only (the reference's optional d_pred output is the training
+// loss's business here: rxgs_train_grads with lambda_ssim > 0)
+inline double ssim(const std::vector<double>& pred, const std::vector<double>& gt, int h, int w,
+                   const SsimOptions& options = {}) {
+    if (h < options.window || w < options.window) throw std::invalid_argument("ssim: image smaller than the window");
+    if (pred.size() != static_cast<std::size_t>(h) * w || gt.size() != pred.size())
+        throw std::invalid_argument("ssim: shape mismatch");
+    const double o[3] = {static_cast<double>(options.window), options.sigma, options.dynamic_range};
+    return detail_m::all(pred, gt, h, w, 1.0, o, "ssim")[3];
+}
+}  // namespace met
 
 namespace raster {
 

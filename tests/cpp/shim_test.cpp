@@ -256,6 +256,106 @@ int main() {
         CHECK(rel_err((obj(bp) - obj(bm)) / (2 * hc), d_base[5]) < 1e-4);
         CHECK(grads.d_local.w2.size() == 64 && grads.d_global.b3.size() == 4);
     }
+    {  // Stage-I densification: test_scene.cpp:175-245 restated on the shim
+        auto cloud = [](std::vector<Vec3> pts, double ls) {
+            GaussianScene s;
+            s.l_max = 0;
+            for (const Vec3& p : pts) {
+                s.positions.insert(s.positions.end(), {p.x, p.y, p.z});
+                s.log_scales.insert(s.log_scales.end(), {ls, ls, ls});
+                s.quaternions.insert(s.quaternions.end(), {1.0, 0.0, 0.0, 0.0});
+                s.tau_logits.push_back(std::log(0.1 / 0.9));
+            }
+            s.fle_coeffs.assign(static_cast<std::size_t>(s.count()) * s.coeff_stride(), 0.0);
+            return s;
+        };
+        {  // below threshold: no-op
+            auto s = cloud({{0, 0, 0}, {1, 0, 0}, {0, 1, 0}}, 0.0);
+            DensifyState st;
+            st.resize(3);
+            st.scene_extent = 10.0;
+            st.accumulate(std::vector<double>(9, 1e-9));
+            const auto before = s.positions;
+            const auto r = densify_and_prune(s, st, {}, 1, 0);
+            CHECK(s.count() == 3 && s.positions == before && r.cloned == 0 && r.split == 0 && r.pruned == 0);
+            CHECK((r.source_row == std::vector<int>{0, 1, 2}));
+        }
+        {  // small Gaussian cloned
+            auto s = cloud({{0, 0, 0}, {1, 0, 0}}, 0.0);
+            DensifyState st;
+            st.resize(2);
+            st.scene_extent = 1000.0;
+            st.accumulate({1.0, 0, 0, 0, 0, 0});
+            const auto r = densify_and_prune(s, st, {}, 1, 0);
+            CHECK(r.cloned == 1 && s.count() == 3);
+            CHECK(s.positions[6] == s.positions[0] && s.positions[7] == s.positions[1] && s.positions[8] == s.positions[2]);
+            CHECK((r.source_row == std::vector<int>{0, 1, -1}));
+            CHECK(st.grad_accum.size() == 3);
+        }
+        {  // large Gaussian splits: children 2 sigma apart, scales shrunk by 0.8
+            auto s = cloud({{0, 0, 0}, {1, 0, 0}}, 0.0);
+            s.log_scales[0] = s.log_scales[1] = s.log_scales[2] = std::log(0.5);
+            DensifyState st;
+            st.resize(2);
+            st.scene_extent = 10.0;
+            st.accumulate({1.0, 0, 0, 0, 0, 0});
+            const auto r = densify_and_prune(s, st, {}, 1, 0);
+            CHECK(r.split == 1 && s.count() == 3);
+            CHECK(rel_err(s.log_scales[0], std::log(0.5) + std::log(0.8)) < 1e-12);
+            const double dx = s.positions[0] - s.positions[6], dy = s.positions[1] - s.positions[7],
+                         dz = s.positions[2] - s.positions[8];
+            CHECK(rel_err(std::sqrt(dx * dx + dy * dy + dz * dz), 1.0) < 1e-12);
+        }
+        {  // oversized pruned
+            auto s = cloud({{0, 0, 0}, {1, 0, 0}, {0, 1, 0}}, std::log(5.0));
+            DensifyState st;
+            st.resize(3);
+            st.scene_extent = 10.0;
+            st.accumulate(std::vector<double>(9, 0.0));
+            const auto r = densify_and_prune(s, st, {}, 1, 0);
+            CHECK(r.pruned == 3 && s.count() == 0 && st.grad_accum.empty());
+        }
+        {  // reset_transmittance: tau = 0.01, idempotent (test_scene.cpp:164-173)
+            auto s = cloud({{0, 0, 0}, {1, 0, 0}, {0, 2, 0}}, 0.0);
+            reset_transmittance(s);
+            for (double v : s.tau_logits) CHECK(rel_err(1.0 / (1.0 + std::exp(-v)), 0.01) < 1e-12);
+            const auto once = s.tau_logits;
+            reset_transmittance(s);
+            CHECK(s.tau_logits == once);
+        }
+        bool threw = false;
+        try {
+            auto s = cloud({{0, 0, 0}, {1, 0, 0}}, 0.0);
+            DensifyState st;
+            st.resize(3);
+            densify_and_prune(s, st, {}, 1, 0);
+        } catch (const std::invalid_argument& e) {
+            threw = std::string(e.what()) == "densify_and_prune: state size mismatch";
+        }
+        CHECK(threw);
+    }
+    {  // metrics (test_metrics.cpp-style known answers)
+        std::vector<double> a = {1, 2, 3, 4}, b = {1, 2, 3, 6};
+        CHECK(rel_err(met::mae(a, b), 0.5) < 1e-15);
+        CHECK(rel_err(met::mse(a, b), 1.0) < 1e-15);
+        CHECK(rel_err(met::psnr(a, b, 2.0), 10.0 * std::log10(4.0)) < 1e-14);
+        CHECK(met::psnr(a, a, 1.0) == met::kDbSentinel);
+        std::vector<double> img(16 * 16), img2(16 * 16);
+        for (std::size_t i = 0; i < img.size(); ++i) {
+            img[i] = std::sin(0.1 * i);
+            img2[i] = img[i] + 0.05 * std::cos(0.7 * i);
+        }
+        CHECK(rel_err(met::ssim(img, img, 16, 16), 1.0) < 1e-14);
+        const double s1 = met::ssim(img, img2, 16, 16);
+        CHECK(s1 < 1.0 && s1 > 0.5);
+        bool threw = false;
+        try {
+            met::ssim(std::vector<double>(100, 0.0), std::vector<double>(100, 0.0), 10, 10);
+        } catch (const std::invalid_argument& e) {
+            threw = std::string(e.what()) == "ssim: image smaller than the window";
+        }
+        CHECK(threw);
+    }
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail ? 1 : 0;
 }
