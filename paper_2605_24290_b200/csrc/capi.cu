@@ -461,7 +461,7 @@ int rxgs_ctx_release_cache(rxgs_ctx ctx) {
     RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
     for (DevBuf* b : {&ctx->sort_tmp, &ctx->scratch_a, &ctx->scratch_b, &ctx->scratch_c, &ctx->scratch_d,
                       &ctx->signals, &ctx->ag, &ctx->partial, &ctx->host_in, &ctx->host_out, &ctx->ycache,
-                      &ctx->fle_a, &ctx->fle_b, &ctx->fle_m, &ctx->row_pos, &ctx->row_GB, &ctx->row_S}) {
+                      &ctx->fle_a, &ctx->fle_b, &ctx->fle_m, &ctx->probe_tr, &ctx->row_pos, &ctx->row_GB, &ctx->row_S}) {
         if (b->p) cudaFree(b->p);
         b->p = nullptr;
         b->bytes = 0;

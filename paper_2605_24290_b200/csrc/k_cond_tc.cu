@@ -329,13 +329,78 @@ __global__ void k_gather_rows(const int* __restrict__ n_rows, const int* __restr
 // YOUT: rows are all K Gaussians (Morton order) and the local-branch output
 // y = (alpha_L, beta_L) is written to ycache[k][j] instead of the signal (the
 // Tx-independent cache of the coverage workload).
+// RXGS_PROBE_SPLIT: the occupancy probe of every (needed row, receiver) in its
+// own kernel at full occupancy (the conditioning kernel runs 16 warps per SM,
+// too few to hide the cell-table loads), (T, rho) to probe_tr[j][row].  Same
+// arithmetic and the same warp grouping (32 rows, one receiver) as the fused
+// probe in k_cond_tc, so the features are bit-identical.  Measured slower
+// (3.08 vs 2.57 ms for the conditioning stage: at full occupancy the cell
+// table no longer stays in L1), so off.
+#ifndef RXGS_PROBE_SPLIT
+#define RXGS_PROBE_SPLIT 0
+#endif
+template <int ST, int RT>
+__global__ void __launch_bounds__(256) k_probe_rows(const __grid_constant__ LocalW W, CondDev c,
+                                                    const int* __restrict__ n_rows_dev, int cap,
+                                                    const float4* __restrict__ rpos, const double* __restrict__ rx,
+                                                    int n_rx, float2* __restrict__ out) {
+    const int n_rows = *n_rows_dev;
+    const int lane = threadIdx.x & 31;
+    const long long units = static_cast<long long>((n_rows + 31) >> 5) * n_rx;
+    const long long nw = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+    const int R = RT > 0 ? RT : c.R;
+    const float hiR = static_cast<float>(R);
+    const int S = ST > 0 ? ST : c.S;
+    const float tlast = S == 1 ? 0.5f : fmaf(static_cast<float>(S - 1), 0.9f / static_cast<float>(S - 1), 0.05f);
+    const float tfirst = S == 1 ? 0.5f : 0.05f;
+    constexpr bool kSplit = ST >= 2 && ST % 2 == 0 && RT > 0;
+    for (long long u = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); u < units;
+         u += nw) {
+        const int rb = static_cast<int>(u / n_rx), j = static_cast<int>(u - static_cast<long long>(rb) * n_rx);
+        const int r = rb * 32 + lane;
+        const bool active = r < n_rows;
+        const float4 pk = active ? rpos[r] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float qx = static_cast<float>(rx[3 * j]), qy = static_cast<float>(rx[3 * j + 1]),
+              qz = static_cast<float>(rx[3 * j + 2]);
+        const float px = active ? pk.x : 0.f, py = active ? pk.y : 0.f, pz = active ? pk.z : 0.f;
+        if (!active) {
+            qx = 1.f;
+            qy = qz = 0.f;
+        }
+        const float dx = qx - px, dy = qy - py, dz = qz - pz;
+        const float b0 = fmaf(px, W.icell[0], -W.blo[0]);
+        const float b1 = fmaf(py, W.icell[1], -W.blo[1]);
+        const float b2 = fmaf(pz, W.icell[2], -W.blo[2]);
+        const float s0 = dx * W.icell[0], s1 = dy * W.icell[1], s2 = dz * W.icell[2];
+        auto inside = [&](float t) {
+            const float u0 = fmaf(t, s0, b0), u1 = fmaf(t, s1, b1), u2 = fmaf(t, s2, b2);
+            return u0 >= -1.f && u0 <= hiR && u1 >= -1.f && u1 <= hiR && u2 >= -1.f && u2 <= hiR;
+        };
+        const bool ok = !active || (inside(tfirst) && inside(tlast));
+        float tr = 1.f, sum = 0.f;
+        if (__all_sync(0xffffffffu, ok)) {
+            if constexpr (kSplit) {
+                float2 tr2 = make_float2(1.f, 1.f), sum2 = make_float2(0.f, 0.f);
+                if (active) probe_pairs_cube<ST, RT, 0, ST / 2>(c.cube, b0, b1, b2, s0, s1, s2, tr2, sum2);
+                tr = tr2.x * tr2.y;
+                sum = sum2.x + sum2.y;
+            } else {
+                if (active) probe_seg_cube<ST, RT, false>(c.cube, R, S, b0, b1, b2, s0, s1, s2, tr, sum);
+            }
+        } else if (active) {
+            probe_seg_cube<ST, RT, true>(c.cube, R, S, b0, b1, b2, s0, s1, s2, tr, sum);
+        }
+        if (active) out[static_cast<size_t>(j) * cap + r] = make_float2(tr, sum * (1.f / static_cast<float>(S)));
+    }
+}
+
 template <int ST, int RT, bool YOUT>
 __global__ void __launch_bounds__(kThreads, 1)
     k_cond_tc(const __grid_constant__ LocalW W, CondDev c, const int* __restrict__ n_rows_dev, int n_rows_host,
               int cap, const int* __restrict__ rows, const float4* __restrict__ rpos, const double* __restrict__ rx,
               int n_rx, const float4* __restrict__ rGB, const float4* __restrict__ rS,
               const float* __restrict__ ag, const float2* __restrict__ Mpre, SigOut sig,
-              float4* __restrict__ ycache) {
+              float4* __restrict__ ycache, const float2* __restrict__ probe_in) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* w2hi = smem;
     uint8_t* w2lo = smem + kW2Bytes;
@@ -481,7 +546,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // half of the probe; feat_end the second half (it runs in the layer-2
     // MMA window) and writes [T, rho].  Clamped / generic probes run whole in
     // feat_begin.
-    auto feat_begin = [&](bool active, float4 pk, float qx, float qy, float qz, float* in, ProbeState& ps) {
+    auto feat_begin = [&](bool active, float4 pk, float qx, float qy, float qz, float* in, ProbeState& ps, int rr,
+                          int jj) {
         const float px = active ? pk.x : 0.f, py = active ? pk.y : 0.f, pz = active ? pk.z : 0.f;
         if (!active) {
             qx = 1.f;
@@ -499,7 +565,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         ps.split = false;
         ps.tr2 = make_float2(1.f, 1.f);
         ps.sum2 = make_float2(0.f, 0.f);
-        if (c.probe) {
+        if (c.probe && probe_in) {  // (T, rho) from k_probe_rows; consumed at the next A1 staging
+            const float2 v = active ? probe_in[static_cast<size_t>(jj) * cap + rr] : make_float2(1.f, 0.f);
+            in[4] = v.x;
+            in[5] = v.y;
+        } else if (c.probe) {
             ps.b0 = fmaf(px, W.icell[0], -W.blo[0]);
             ps.b1 = fmaf(py, W.icell[1], -W.blo[1]);
             ps.b2 = fmaf(pz, W.icell[2], -W.blo[2]);
@@ -554,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             qz = static_cast<float>(rx[3 * j + 2]);
         }
         ProbeState ps0;
-        feat_begin(act, pk, qx, qy, qz, in, ps0);
+        feat_begin(act, pk, qx, qy, qz, in, ps0, r, j);
         feat_end(act, in, ps0);
     }
 #if RXGS_AHEAD
@@ -687,7 +757,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         ProbeState ps;
         ps.split = false;
         if (ntile < tiles) {
-            feat_begin(nact, pkn, static_cast<float>(qxn), static_cast<float>(qyn), static_cast<float>(qzn), inn, ps);
+            feat_begin(nact, pkn, static_cast<float>(qxn), static_cast<float>(qyn), static_cast<float>(qzn), inn, ps, rn,
+                       jn);
             feat_end(nact, inn, ps);
         }
         fle();
@@ -721,7 +792,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         ProbeState ps;
         ps.split = false;
         if (ntile < tiles)
-            feat_begin(nact, pkn, static_cast<float>(qxn), static_cast<float>(qyn), static_cast<float>(qzn), inn, ps);
+            feat_begin(nact, pkn, static_cast<float>(qxn), static_cast<float>(qyn), static_cast<float>(qzn), inn, ps, rn,
+                       jn);
         if (RXGS_FLE_FIRST) fle();
         RXGS_MBAR_WAIT(&bars[g], phase);
         phase ^= 1u;
@@ -950,7 +1022,8 @@ namespace {
 template <bool YOUT>
 cudaError_t launch_tc(const rxgs_cond_s& cs, const int* n_rows_dev, long long rows_host, int cap, const int* rows,
                       const float4* rpos, const double* d_rx, int n_rx, const float4* rGB, const float4* rS,
-                      const float* d_ag, const float2* Mpre, SigOut d_sig, float4* ycache, cudaStream_t s) {
+                      const float* d_ag, const float2* Mpre, SigOut d_sig, float4* ycache, cudaStream_t s,
+                      float2* probe_buf = nullptr) {
     if (rows_host == 0 || n_rx == 0) return cudaSuccess;
     const CondDev d = make_dev(cs);
     LocalW w{};
@@ -977,8 +1050,15 @@ cudaError_t launch_tc(const rxgs_cond_s& cs, const int* n_rows_dev, long long ro
     auto kern = fast ? k_cond_tc<16, 32, YOUT> : k_cond_tc<0, 0, YOUT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
+    const float2* probe_in = nullptr;
+    if (!YOUT && probe_buf && d.probe && d.use_local && RXGS_PROBE_CUBE && n_rows_dev) {
+        auto pk = fast ? k_probe_rows<16, 32> : k_probe_rows<0, 0>;
+        pk<<<sms * 8, 256, 0, s>>>(w, d, n_rows_dev, cap, rpos, d_rx, n_rx, probe_buf);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        probe_in = probe_buf;
+    }
     kern<<<blocks, kThreads, smem, s>>>(w, d, n_rows_dev, static_cast<int>(rows_host), cap, rows, rpos, d_rx, n_rx,
-                                        rGB, rS, d_ag, Mpre, d_sig, ycache);
+                                        rGB, rS, d_ag, Mpre, d_sig, ycache, probe_in);
     return cudaGetLastError();
 }
 
@@ -1011,8 +1091,14 @@ cudaError_t launch_cond_signal_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc,
             return e;
         Mpre = ctx->fle_m.as<float2>();
     }
+    float2* probe_buf = nullptr;
+    if (RXGS_PROBE_SPLIT && cs.use_local() && cs.has_occ) {
+        if ((e = ctx->probe_tr.ensure(sizeof(float2) * static_cast<size_t>(cap) * n_rx)) != cudaSuccess) return e;
+        probe_buf = ctx->probe_tr.as<float2>();
+    }
     return launch_tc<false>(cs, n_rows, bound, cap, rows, ctx->row_pos.as<float4>(), d_rx, n_rx,
-                            ctx->row_GB.as<float4>(), ctx->row_S.as<float4>(), d_ag, Mpre, d_sig, nullptr, s);
+                            ctx->row_GB.as<float4>(), ctx->row_S.as<float4>(), d_ag, Mpre, d_sig, nullptr, s,
+                            probe_buf);
 }
 
 cudaError_t gather_rows(const rxgs_scene_s& sc, const rxgs_txstate_s& st, cudaStream_t s) {

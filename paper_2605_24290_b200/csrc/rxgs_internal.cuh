@@ -147,6 +147,7 @@ struct rxgs_ctx_s {
     rxgs_b200::DevBuf row_pos, row_GB, row_S;
     // FLE GEMM operands / result for high l_max (k_fle_gemm.cu)
     rxgs_b200::DevBuf fle_a, fle_b, fle_m;
+    rxgs_b200::DevBuf probe_tr;  // (T, rho) per (receiver, needed row) from k_probe_rows
     // version of the transmitter state whose receiver-independent row data
     // (row_pos / row_GB / row_S and the GEMM's A operand) the buffers hold,
     // so receiver chunks of one query batch gather and pack it once
