@@ -27,6 +27,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "cond_common.cuh"
+#include "f32x2.cuh"
 #include "rxgs_internal.cuh"
 
 namespace rxgs_b200 {
@@ -359,7 +360,9 @@ __host__ __device__ constexpr int local_grad_count(int H) { return H * 6 + H + H
 // gradient phase), where each thread owns fixed weight-gradient entries and
 // sums the tile's 128 rows in row order (deterministic).
 // smem per CTA: W2 (H*H) | h1 | h2 | dh2 | dh1 (4 x 128 x 65) | x (128 x 6) | dy (128 x 4)
-constexpr int kBwdPad = 65;
+// even row pitch: 8-byte aligned float2 rows; 33 float2 per row keeps the
+// per-thread row accesses bank-conflict free
+constexpr int kBwdPad = 66;
 __global__ void __launch_bounds__(kBwdThreads) k_cond_bwd(CondDev c, const int* __restrict__ n_rows,
                                                           const int* __restrict__ rows, const float4* __restrict__ pos32,
                                                           const double* __restrict__ rx, int n_rx,
@@ -369,7 +372,8 @@ __global__ void __launch_bounds__(kBwdThreads) k_cond_bwd(CondDev c, const int* 
     constexpr int H = 64;
     extern __shared__ __align__(16) float sm[];
     float* sW2 = sm;
-    float* sH1 = sW2 + H * H;
+    float2* sW2T2 = reinterpret_cast<float2*>(sW2 + H * H);  // [i][o/2] = (W2[o][i], W2[o+1][i])
+    float* sH1 = sW2 + 2 * H * H;
     float* sH2 = sH1 + kBwdThreads * kBwdPad;
     float* sDH2 = sH2 + kBwdThreads * kBwdPad;
     float* sDH1 = sDH2 + kBwdThreads * kBwdPad;
@@ -377,11 +381,17 @@ __global__ void __launch_bounds__(kBwdThreads) k_cond_bwd(CondDev c, const int* 
     float* sDY = sX + kBwdThreads * 6;
     const float* p = c.p32;
     for (int i = threadIdx.x; i < H * H; i += blockDim.x) sW2[i] = p[c.o_lw2 + i];
+    for (int i = threadIdx.x; i < H * H / 2; i += blockDim.x) {
+        const int ii = i / (H / 2), op = i % (H / 2);
+        sW2T2[i] = make_float2(p[c.o_lw2 + (2 * op) * H + ii], p[c.o_lw2 + (2 * op + 1) * H + ii]);
+    }
     __syncthreads();
     const int t = threadIdx.x;
-    // per-thread ownership of the weight-gradient accumulators
-    float gw2[32];  // dW2[o = t/2][i = (t%2)*32 .. +32)
-    for (int q = 0; q < 32; ++q) gw2[q] = 0.f;
+    // per-thread ownership of the weight-gradient accumulators; the 64x64
+    // loops run on FFMA2 (two lanes per instruction, each exactly fmaf, in
+    // the same order as the scalar code: bit-identical results)
+    float2 gw2[16];  // dW2[o = t/2][i = (t%2)*32 .. +32), pairs
+    for (int q = 0; q < 16; ++q) gw2[q] = make_float2(0.f, 0.f);
     float gw1[3] = {0.f, 0.f, 0.f};  // dW1 entries t*3 .. t*3+2 (of 384)
     float gw3[2] = {0.f, 0.f};        // dW3 entries t*2, t*2+1 (of 256)
     float gb1 = 0.f, gb2 = 0.f, gb3 = 0.f;  // b1[t], b2[t] (t < 64), b3[t] (t < 4)
@@ -395,9 +405,12 @@ __global__ void __launch_bounds__(kBwdThreads) k_cond_bwd(CondDev c, const int* 
         float* dh2s = sDH2 + t * kBwdPad;
         float x[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         float dy[4] = {0.f, 0.f, 0.f, 0.f};
-        float h1[H], dh1[H];
+        float h1[H];
+        float2 dh1[H / 2];
 #pragma unroll
-        for (int o = 0; o < H; ++o) h1[o] = dh1[o] = 0.f;
+        for (int o = 0; o < H; ++o) h1[o] = 0.f;
+#pragma unroll
+        for (int o = 0; o < H / 2; ++o) dh1[o] = make_float2(0.f, 0.f);
         if (active && !c.use_local) {  // global-only mode: no local branch, u = d_s
             const int k = rows[row / n_rx], j = static_cast<int>(row % n_rx);
             u_out[static_cast<size_t>(k) * n_rx + j] = d_s[static_cast<size_t>(k) * n_rx + j];
@@ -417,15 +430,18 @@ __global__ void __launch_bounds__(kBwdThreads) k_cond_bwd(CondDev c, const int* 
             }
             float y[4] = {p[c.o_lb3], p[c.o_lb3 + 1], p[c.o_lb3 + 2], p[c.o_lb3 + 3]};
 #pragma unroll 1
-            for (int o = 0; o < H; ++o) {
-                float a = p[c.o_lb2 + o];
-                const float* wr = sW2 + o * H;
+            for (int op = 0; op < H / 2; ++op) {  // outputs o = 2 op, 2 op + 1
+                const int o = 2 * op;
+                float2 a = make_float2(p[c.o_lb2 + o], p[c.o_lb2 + o + 1]);
 #pragma unroll
-                for (int i = 0; i < H; ++i) a = fmaf(wr[i], h1[i], a);
-                const float hv = fmaxf(a, 0.f);
-                h2s[o] = hv;
+                for (int i = 0; i < H; ++i) a = x2::fma(sW2T2[i * (H / 2) + op], x2::bc(h1[i]), a);
+                const float hv0 = fmaxf(a.x, 0.f), hv1 = fmaxf(a.y, 0.f);
+                h2s[o] = hv0;
+                h2s[o + 1] = hv1;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) y[q] = fmaf(p[c.o_lw3 + q * H + o], hv, y[q]);
+                for (int q = 0; q < 4; ++q) y[q] = fmaf(p[c.o_lw3 + q * H + o], hv0, y[q]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) y[q] = fmaf(p[c.o_lw3 + q * H + o + 1], hv1, y[q]);
             }
             // signal pieces M = sum_l mid_l B_l, Bs = sum_l B_l (k_cond signal math)
             float2 M = make_float2(0.f, 0.f), Bs = make_float2(0.f, 0.f);
@@ -456,19 +472,20 @@ __global__ void __launch_bounds__(kBwdThreads) k_cond_bwd(CondDev c, const int* 
                 const float g = h2s[o] > 0.f ? a : 0.f;
                 dh2s[o] = g;
                 if (g == 0.f) continue;
-                const float* wr = sW2 + o * H;
+                const float2* wr = reinterpret_cast<const float2*>(sW2 + o * H);
 #pragma unroll
-                for (int i = 0; i < H; ++i) dh1[i] = fmaf(wr[i], g, dh1[i]);
+                for (int i = 0; i < H / 2; ++i) dh1[i] = x2::fma(wr[i], x2::bc(g), dh1[i]);
             }
 #pragma unroll
-            for (int i = 0; i < H; ++i) dh1[i] = h1[i] > 0.f ? dh1[i] : 0.f;
+            for (int i = 0; i < H / 2; ++i)
+                dh1[i] = make_float2(h1[2 * i] > 0.f ? dh1[i].x : 0.f, h1[2 * i + 1] > 0.f ? dh1[i].y : 0.f);
         } else {
             for (int o = 0; o < H; ++o) h2s[o] = dh2s[o] = 0.f;
         }
 #pragma unroll
-        for (int i = 0; i < H; ++i) {
-            sH1[t * kBwdPad + i] = h1[i];
-            sDH1[t * kBwdPad + i] = dh1[i];
+        for (int i = 0; i < H / 2; ++i) {
+            reinterpret_cast<float2*>(sH1 + t * kBwdPad)[i] = make_float2(h1[2 * i], h1[2 * i + 1]);
+            reinterpret_cast<float2*>(sDH1 + t * kBwdPad)[i] = dh1[i];
         }
         for (int i = 0; i < 6; ++i) sX[t * 6 + i] = x[i];
         for (int q = 0; q < 4; ++q) sDY[t * 4 + q] = dy[q];
@@ -479,9 +496,9 @@ __global__ void __launch_bounds__(kBwdThreads) k_cond_bwd(CondDev c, const int* 
             for (int r = 0; r < kBwdThreads; ++r) {
                 const float g = sDH2[r * kBwdPad + o];
                 if (g == 0.f) continue;
-                const float* hr = sH1 + r * kBwdPad + i0;
+                const float2* hr = reinterpret_cast<const float2*>(sH1 + r * kBwdPad + i0);
 #pragma unroll
-                for (int q = 0; q < 32; ++q) gw2[q] = fmaf(g, hr[q], gw2[q]);
+                for (int q = 0; q < 16; ++q) gw2[q] = x2::fma(x2::bc(g), hr[q], gw2[q]);
             }
             for (int e = 0; e < 3; ++e) {
                 const int idx = t * 3 + e, oi = idx / 6, fi = idx % 6;
@@ -516,7 +533,10 @@ __global__ void __launch_bounds__(kBwdThreads) k_cond_bwd(CondDev c, const int* 
     constexpr int NG = local_grad_count(H);
     float* out = part + static_cast<size_t>(blockIdx.x) * NG;
     const int o_w1 = 0, o_b1 = H * 6, o_w2 = o_b1 + H, o_b2 = o_w2 + H * H, o_w3 = o_b2 + H, o_b3 = o_w3 + 4 * H;
-    for (int q = 0; q < 32; ++q) out[o_w2 + (t >> 1) * H + (t & 1) * 32 + q] = gw2[q];
+    for (int q = 0; q < 16; ++q) {
+        out[o_w2 + (t >> 1) * H + (t & 1) * 32 + 2 * q] = gw2[q].x;
+        out[o_w2 + (t >> 1) * H + (t & 1) * 32 + 2 * q + 1] = gw2[q].y;
+    }
     for (int e = 0; e < 3; ++e) out[o_w1 + t * 3 + e] = gw1[e];
     for (int e = 0; e < 2; ++e) out[o_w3 + t * 2 + e] = gw3[e];
     if (t < H) {
@@ -843,7 +863,7 @@ cudaError_t launch_render_adjoint(const rxgs_txstate_s& st, const float2* G, int
     return cudaGetLastError();
 }
 
-size_t cond_bwd_smem() { return sizeof(float) * (64 * 64 + 4 * kBwdThreads * kBwdPad + kBwdThreads * 10); }
+size_t cond_bwd_smem() { return sizeof(float) * (2 * 64 * 64 + 4 * kBwdThreads * kBwdPad + kBwdThreads * 10); }
 int cond_bwd_parts(int sms) { return sms * 2; }
 int local_grad_n() { return local_grad_count(64); }
 
