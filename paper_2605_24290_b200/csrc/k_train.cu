@@ -429,19 +429,34 @@ __global__ void __launch_bounds__(kBwdThreads) k_cond_bwd(CondDev c, const int* 
                 h1[o] = fmaxf(a, 0.f);
             }
             float y[4] = {p[c.o_lb3], p[c.o_lb3 + 1], p[c.o_lb3 + 2], p[c.o_lb3 + 3]};
+            // four output pairs per pass: independent FFMA2 chains (the 64-long
+            // dot products are latency-bound at one warp per SM sub-partition)
 #pragma unroll 1
-            for (int op = 0; op < H / 2; ++op) {  // outputs o = 2 op, 2 op + 1
-                const int o = 2 * op;
-                float2 a = make_float2(p[c.o_lb2 + o], p[c.o_lb2 + o + 1]);
+            for (int op0 = 0; op0 < H / 2; op0 += 4) {  // outputs o = 2 op0 .. 2 op0 + 7
+                float2 a[4];
 #pragma unroll
-                for (int i = 0; i < H; ++i) a = x2::fma(sW2T2[i * (H / 2) + op], x2::bc(h1[i]), a);
-                const float hv0 = fmaxf(a.x, 0.f), hv1 = fmaxf(a.y, 0.f);
-                h2s[o] = hv0;
-                h2s[o + 1] = hv1;
+                for (int u = 0; u < 4; ++u)
+                    a[u] = make_float2(p[c.o_lb2 + 2 * (op0 + u)], p[c.o_lb2 + 2 * (op0 + u) + 1]);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) y[q] = fmaf(p[c.o_lw3 + q * H + o], hv0, y[q]);
+                for (int i = 0; i < H; ++i) {
+                    const float4* wq = reinterpret_cast<const float4*>(sW2T2 + i * (H / 2) + op0);
+                    const float4 w01 = wq[0], w23 = wq[1];
+                    a[0] = x2::fma(make_float2(w01.x, w01.y), x2::bc(h1[i]), a[0]);
+                    a[1] = x2::fma(make_float2(w01.z, w01.w), x2::bc(h1[i]), a[1]);
+                    a[2] = x2::fma(make_float2(w23.x, w23.y), x2::bc(h1[i]), a[2]);
+                    a[3] = x2::fma(make_float2(w23.z, w23.w), x2::bc(h1[i]), a[3]);
+                }
 #pragma unroll
-                for (int q = 0; q < 4; ++q) y[q] = fmaf(p[c.o_lw3 + q * H + o + 1], hv1, y[q]);
+                for (int u = 0; u < 4; ++u) {
+                    const int o = 2 * (op0 + u);
+                    const float hv0 = fmaxf(a[u].x, 0.f), hv1 = fmaxf(a[u].y, 0.f);
+                    h2s[o] = hv0;
+                    h2s[o + 1] = hv1;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) y[q] = fmaf(p[c.o_lw3 + q * H + o], hv0, y[q]);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) y[q] = fmaf(p[c.o_lw3 + q * H + o + 1], hv1, y[q]);
+                }
             }
             // signal pieces M = sum_l mid_l B_l, Bs = sum_l B_l (k_cond signal math)
             float2 M = make_float2(0.f, 0.f), Bs = make_float2(0.f, 0.f);
