@@ -4,6 +4,7 @@
 // fused conditioning + FLE reduction of one (Gaussian, receiver) row.
 #pragma once
 
+#include "f32x2.cuh"
 #include "rxgs_internal.cuh"
 
 namespace rxgs_b200 {
@@ -309,6 +310,76 @@ __device__ __forceinline__ float2 fused_signal(const CondDev& c, int k, int j, i
     fle_reduce(k, j, ch, L, C, B, GB, ag, M, Bs);
     return local_affine(c, ch, M, Bs, y);
 }
+
+// ---- the same probes on the trilinear cell table (RXGS_PROBE_CUBE): one
+// 256-bit read-only load per sample (the cell's 8 polynomial coefficients,
+// k_occ_cubes) and v = (a + w0 b + w1 (c + w0 e)) + w2 (d + w0 f + w1 (g + w0 h))
+// in three FFMA2 + one FFMA, instead of 8 shared-memory corner loads and 7
+// lerps.  Cells are [-1, R]^3, i.e. exactly the padded grid's cell range.
+__device__ __forceinline__ float cube_eval(const float* cell, float w0, float w1, float w2) {
+    float c0, c1, c2, c3, c4, c5, c6, c7;
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(c0), "=f"(c1), "=f"(c2), "=f"(c3), "=f"(c4), "=f"(c5), "=f"(c6), "=f"(c7)
+        : "l"(cell));
+    const float2 x13 = x2::fma(x2::bc(w0), make_float2(c2, c3), make_float2(c0, c1));  // (a + w0 b, d + w0 f)
+    const float2 x24 = x2::fma(x2::bc(w0), make_float2(c6, c7), make_float2(c4, c5));  // (c + w0 e, g + w0 h)
+    const float2 y = x2::fma(x2::bc(w1), x24, x13);
+    return fmaf(w2, y.y, y.x);
+}
+
+template <int ST, int RT, int P0, int P1>
+__device__ __forceinline__ void probe_pairs_cube(const float* __restrict__ cube, float b0, float b1, float b2,
+                                                 float s0, float s1, float s2, float2& tr2, float2& sum2) {
+    static_assert(ST >= 2 && ST % 2 == 0 && RT > 0, "paired probe needs an even, static sample count");
+    constexpr int P = RT + 2;
+    constexpr float cidx = static_cast<float>(P * P + P + 1);
+    constexpr float dt = 0.9f / static_cast<float>(ST - 1);
+#pragma unroll
+    for (int sp = P0; sp < P1; ++sp) {
+        const float2 t = make_float2(fmaf(static_cast<float>(2 * sp), dt, 0.05f),
+                                     fmaf(static_cast<float>(2 * sp + 1), dt, 0.05f));
+        const float2 u0 = x2::fma(t, x2::bc(s0), x2::bc(b0));
+        const float2 u1 = x2::fma(t, x2::bc(s1), x2::bc(b1));
+        const float2 u2 = x2::fma(t, x2::bc(s2), x2::bc(b2));
+        const float2 f0 = make_float2(floorf(u0.x), floorf(u0.y));
+        const float2 f1 = make_float2(floorf(u1.x), floorf(u1.y));
+        const float2 f2 = make_float2(floorf(u2.x), floorf(u2.y));
+        const float2 w0 = x2::sub(u0, f0), w1 = x2::sub(u1, f1), w2 = x2::sub(u2, f2);
+        const float2 fi = x2::fma(f0, x2::bc(static_cast<float>(P * P)),
+                                  x2::fma(f1, x2::bc(static_cast<float>(P)), x2::add(f2, x2::bc(cidx))));
+        const float va = cube_eval(cube + 8 * static_cast<int>(fi.x), w0.x, w1.x, w2.x);
+        const float vb = cube_eval(cube + 8 * static_cast<int>(fi.y), w0.y, w1.y, w2.y);
+        const float2 v = make_float2(va, vb);
+        tr2 = x2::mul(tr2, x2::sub(x2::bc(1.f), v));
+        sum2 = x2::add(sum2, v);
+    }
+}
+
+template <int ST, int RT, bool CLAMP>
+__device__ __forceinline__ void probe_seg_cube(const float* __restrict__ cube, int R, int S, float b0, float b1,
+                                               float b2, float s0, float s1, float s2, float& tr, float& sum) {
+    const int P = (RT > 0 ? RT : R) + 2;
+    const float hi = static_cast<float>(RT > 0 ? RT : R);
+    const float cidx = static_cast<float>(P * P + P + 1);
+    const int NS = ST > 0 ? ST : S;
+    const float dt = NS == 1 ? 0.f : 0.9f / static_cast<float>(NS - 1);
+#pragma unroll 1
+    for (int si = 0; si < NS; ++si) {
+        const float t = NS == 1 ? 0.5f : fmaf(static_cast<float>(si), dt, 0.05f);
+        float u0 = fmaf(t, s0, b0), u1 = fmaf(t, s1, b1), u2 = fmaf(t, s2, b2);
+        if (CLAMP) {
+            u0 = fminf(fmaxf(u0, -1.f), hi);
+            u1 = fminf(fmaxf(u1, -1.f), hi);
+            u2 = fminf(fmaxf(u2, -1.f), hi);
+        }
+        const float f0 = floorf(u0), f1 = floorf(u1), f2 = floorf(u2);
+        const int idx = static_cast<int>(fmaf(f0, static_cast<float>(P * P), fmaf(f1, static_cast<float>(P), f2 + cidx)));
+        const float v = cube_eval(cube + 8 * idx, u0 - f0, u1 - f1, u2 - f2);
+        tr *= 1.f - v;
+        sum += v;
+    }
+}
+
 
 }  // namespace cond_dev
 }  // namespace rxgs_b200
