@@ -381,5 +381,66 @@ __device__ __forceinline__ void probe_seg_cube(const float* __restrict__ cube, i
 }
 
 
+// Local features [v_hat, d, T, rho] of one (Gaussian, receiver) with the
+// occupancy probe on the trilinear cell table (as the tcgen05 kernel: the
+// paired fast path when the whole warp's segments lie inside the grid); the
+// generic probe for nearest lookup.  Called by every lane (warp vote);
+// inactive lanes get dummy features.  Used by the training forward and
+// backward, so both see the same features.
+template <int ST, int RT>
+__device__ __forceinline__ void cube_features(const CondDev& c, bool active, float4 pk, float qx, float qy, float qz,
+                                             float* x) {
+    const bool cube = c.probe && !c.nearest && c.cube != nullptr;
+    if (!cube) {
+        if (active) local_features<false>(c, c.occ, pk.x, pk.y, pk.z, qx, qy, qz, x);
+        return;
+    }
+    const float px = active ? pk.x : 0.f, py = active ? pk.y : 0.f, pz = active ? pk.z : 0.f;
+    if (!active) {
+        qx = 1.f;
+        qy = qz = 0.f;
+    }
+    const float dx = qx - px, dy = qy - py, dz = qz - pz;
+    const float d = sqrtf(dx * dx + dy * dy + dz * dz);
+    const float inv = 1.f / d;
+    x[0] = dx * inv;
+    x[1] = dy * inv;
+    x[2] = dz * inv;
+    x[3] = d;
+    float ic[3], bl[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        ic[a] = 1.f / c.cell[a];
+        bl[a] = __fadd_rn(__fmul_rn(c.lo[a], ic[a]), 0.5f);
+    }
+    const float b0 = fmaf(px, ic[0], -bl[0]), b1 = fmaf(py, ic[1], -bl[1]), b2 = fmaf(pz, ic[2], -bl[2]);
+    const float s0 = dx * ic[0], s1 = dy * ic[1], s2 = dz * ic[2];
+    const int R = RT > 0 ? RT : c.R, S = ST > 0 ? ST : c.S;
+    const float hiR = static_cast<float>(R);
+    const float tlast = S == 1 ? 0.5f : fmaf(static_cast<float>(S - 1), 0.9f / static_cast<float>(S - 1), 0.05f);
+    const float tfirst = S == 1 ? 0.5f : 0.05f;
+    auto inside = [&](float t) {
+        const float u0 = fmaf(t, s0, b0), u1 = fmaf(t, s1, b1), u2 = fmaf(t, s2, b2);
+        return u0 >= -1.f && u0 <= hiR && u1 >= -1.f && u1 <= hiR && u2 >= -1.f && u2 <= hiR;
+    };
+    const bool ok = !active || (inside(tfirst) && inside(tlast));
+    float tr = 1.f, sum = 0.f;
+    if (__all_sync(0xffffffffu, ok)) {
+        if constexpr (ST >= 2 && ST % 2 == 0 && RT > 0) {
+            float2 tr2 = make_float2(1.f, 1.f), sum2 = make_float2(0.f, 0.f);
+            if (active) probe_pairs_cube<ST, RT, 0, ST / 2>(c.cube, b0, b1, b2, s0, s1, s2, tr2, sum2);
+            tr = tr2.x * tr2.y;
+            sum = sum2.x + sum2.y;
+        } else {
+            if (active) probe_seg_cube<ST, RT, false>(c.cube, R, S, b0, b1, b2, s0, s1, s2, tr, sum);
+        }
+    } else if (active) {
+        probe_seg_cube<ST, RT, true>(c.cube, R, S, b0, b1, b2, s0, s1, s2, tr, sum);
+    }
+    x[4] = tr;
+    x[5] = sum * (1.f / static_cast<float>(S));
+}
+
+
 }  // namespace cond_dev
 }  // namespace rxgs_b200

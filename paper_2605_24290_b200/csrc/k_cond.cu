@@ -142,7 +142,10 @@ __global__ void __launch_bounds__(512, 1)
     extern __shared__ __align__(16) float smem[];
     const int H = HT > 0 ? HT : c.H;
     const int C = CT > 0 ? CT : c.C;
-    const int R3 = c.probe ? c.R * c.R * c.R : 0;
+    // the specialised path probes the trilinear cell table (cube_features, the
+    // same features as the training backward); the generic one the smem grid
+    const bool cubep = HT > 0 && c.probe && !c.nearest && c.cube != nullptr;
+    const int R3 = c.probe && !cubep ? c.R * c.R * c.R : 0;
     // layout: w2 (H*H) | w1 (H*6) | b1 (H) | b2 (H) | w3 (4C*H) | b3 (4C) | occ (R^3)
     float* s_w2 = smem;
     float* s_w1 = s_w2 + H * H;
@@ -178,16 +181,24 @@ __global__ void __launch_bounds__(512, 1)
         const int vi = static_cast<int>(it / n_jc);
         const int jc = static_cast<int>(it % n_jc);
         const int j = jc * 32 + lane;
-        if (j >= n_rx) continue;
+        const bool act = j < n_rx;
         const int k = vis[vi];
         const float4 pk = pos32[k];
-        const float rxx = static_cast<float>(rx[3 * j]);
-        const float rxy = static_cast<float>(rx[3 * j + 1]);
-        const float rxz = static_cast<float>(rx[3 * j + 2]);
+        const int jr = act ? j : 0;
+        const float rxx = static_cast<float>(rx[3 * jr]);
+        const float rxy = static_cast<float>(rx[3 * jr + 1]);
+        const float rxz = static_cast<float>(rx[3 * jr + 2]);
         float y[YM];
+        float in[6];
+        if (c.use_local && cubep) {  // warp-uniform: the probe votes over all lanes
+            if (c.S == 16 && c.R == 32)
+                cube_features<16, 32>(c, act, pk, rxx, rxy, rxz, in);
+            else
+                cube_features<0, 0>(c, act, pk, rxx, rxy, rxz, in);
+        }
+        if (!act) continue;
         if (c.use_local) {
-            float in[6];
-            local_features<true>(c, s_occ, pk.x, pk.y, pk.z, rxx, rxy, rxz, in);
+            if (!cubep) local_features<true>(c, s_occ, pk.x, pk.y, pk.z, rxx, rxy, rxz, in);
             local_mlp<HT, CT>(c, w, in, y);
         } else {
 #pragma unroll
@@ -398,9 +409,11 @@ cudaError_t launch_cond_signal(const rxgs_cond_s* c, const rxgs_scene_s& sc,
     const int blocks = static_cast<int>(want < sms ? want : sms);
     const bool fast = d.use_local && d.H == 64 && d.C == 1;
     if (fast) {
+        const bool cubep = d.probe && !d.nearest && d.cube != nullptr;
+        const size_t smem_f = cubep ? local_smem_bytes(d, false) : smem;
         cudaFuncSetAttribute(k_cond_signal<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        k_cond_signal<64, 1><<<blocks, threads, smem, s>>>(
+                             static_cast<int>(smem_f));
+        k_cond_signal<64, 1><<<blocks, threads, smem_f, s>>>(
             d, st.needed_count.as<int>(), st.needed_order.as<int>(), sc.d_pos32.as<float4>(), d_rx, n_rx,
             st.basis32.as<float2>(), st.gb32.as<float2>(), d_ag, d_sig);
     } else {
