@@ -565,6 +565,210 @@ __global__ void __launch_bounds__(kBwdThreads) k_cond_bwd(CondDev c, const int* 
     if (t < 4) out[o_b3 + t] = gb3;
 }
 
+// ---- RXGS_BWD_SPLIT: the same backward in two kernels.  k_cond_bwd_rows
+// runs the per-row recompute + adjoint at three 4-warp CTAs per SM (no
+// per-row activation tiles in shared memory) and writes the activations
+// feature-major, act[f][row] (h1 64 | h2 64 | dh1 64 | dh2 64 | x 6 | dy 4);
+// k_cond_bwd_grads forms the weight gradients from them as fixed-order
+// per-CTA partial sums over contiguous row ranges (dW2 = dH2^T H1 on a 4x4
+// register tile per thread), in the k_cond_bwd partial layout.
+#ifndef RXGS_BWD_SPLIT
+#define RXGS_BWD_SPLIT 1
+#endif
+#ifndef RXGS_BWD_GRAD_CTAS
+#define RXGS_BWD_GRAD_CTAS 4
+#endif
+constexpr int kActF = 6 + 4 + 4 * 64;  // activation features per row
+constexpr int kAh1 = 0, kAh2 = 64, kAdh1 = 128, kAdh2 = 192, kAx = 256, kAdy = 262;  // 16-byte aligned blocks
+
+template <int ST, int RT>
+__global__ void __launch_bounds__(128, 3) k_cond_bwd_rows(CondDev c, const int* __restrict__ n_rows,
+                                                          const int* __restrict__ rows, const float4* __restrict__ pos32,
+                                                          const double* __restrict__ rx, int n_rx,
+                                                          const float2* __restrict__ Bm, const float2* __restrict__ GB,
+                                                          const float* __restrict__ ag, const float2* __restrict__ d_s,
+                                                          float2* __restrict__ u_out, float* __restrict__ act,
+                                                          long long rpad) {
+    constexpr int H = 64;
+    extern __shared__ __align__(16) float sm[];
+    float* sW2 = sm;
+    float2* sW2T2 = reinterpret_cast<float2*>(sW2 + H * H);
+    const float* p = c.p32;
+    for (int i = threadIdx.x; i < H * H; i += blockDim.x) sW2[i] = p[c.o_lw2 + i];
+    for (int i = threadIdx.x; i < H * H / 2; i += blockDim.x) {
+        const int ii = i / (H / 2), op = i % (H / 2);
+        sW2T2[i] = make_float2(p[c.o_lw2 + (2 * op) * H + ii], p[c.o_lw2 + (2 * op + 1) * H + ii]);
+    }
+    __syncthreads();
+    const long long rows_total = static_cast<long long>(*n_rows) * n_rx;
+    const int L = c.L;
+    for (long long base_row = static_cast<long long>(blockIdx.x) * blockDim.x; base_row < rows_total;
+         base_row += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long row = base_row + threadIdx.x;
+        const bool active = row < rows_total;
+        float x[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const int kk = active ? rows[row / n_rx] : 0, jj = active ? static_cast<int>(row % n_rx) : 0;
+        if (c.use_local)  // warp-uniform: every lane takes part in the probe's vote
+            cube_features<ST, RT>(c, active, active ? pos32[kk] : make_float4(0.f, 0.f, 0.f, 0.f),
+                                  static_cast<float>(rx[3 * jj]), static_cast<float>(rx[3 * jj + 1]),
+                                  static_cast<float>(rx[3 * jj + 2]), x);
+        if (!active) continue;
+        const int k = kk, j = jj;
+        if (!c.use_local) {  // global-only mode: no local branch, u = d_s
+            u_out[static_cast<size_t>(k) * n_rx + j] = d_s[static_cast<size_t>(k) * n_rx + j];
+            continue;
+        }
+        float* a = act + row;
+        float h1[H];
+#pragma unroll
+        for (int o = 0; o < H; ++o) {
+            float acc = p[c.o_lb1 + o];
+#pragma unroll
+            for (int i = 0; i < 6; ++i) acc = fmaf(p[c.o_lw1 + o * 6 + i], x[i], acc);
+            h1[o] = fmaxf(acc, 0.f);
+            a[(kAh1 + o) * rpad] = h1[o];
+        }
+        float y[4] = {p[c.o_lb3], p[c.o_lb3 + 1], p[c.o_lb3 + 2], p[c.o_lb3 + 3]};
+        uint32_t pos_lo = 0u, pos_hi = 0u;  // h2 > 0 mask (the ReLU of layer 2)
+#pragma unroll 1
+        for (int op0 = 0; op0 < H / 2; op0 += 4) {
+            float2 ac[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                ac[u] = make_float2(p[c.o_lb2 + 2 * (op0 + u)], p[c.o_lb2 + 2 * (op0 + u) + 1]);
+#pragma unroll
+            for (int i = 0; i < H; ++i) {
+                const float4* wq = reinterpret_cast<const float4*>(sW2T2 + i * (H / 2) + op0);
+                const float4 w01 = wq[0], w23 = wq[1];
+                ac[0] = x2::fma(make_float2(w01.x, w01.y), x2::bc(h1[i]), ac[0]);
+                ac[1] = x2::fma(make_float2(w01.z, w01.w), x2::bc(h1[i]), ac[1]);
+                ac[2] = x2::fma(make_float2(w23.x, w23.y), x2::bc(h1[i]), ac[2]);
+                ac[3] = x2::fma(make_float2(w23.z, w23.w), x2::bc(h1[i]), ac[3]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int o = 2 * (op0 + u);
+                const float hv0 = fmaxf(ac[u].x, 0.f), hv1 = fmaxf(ac[u].y, 0.f);
+                a[(kAh2 + o) * rpad] = hv0;
+                a[(kAh2 + o + 1) * rpad] = hv1;
+                const uint32_t bits = (hv0 > 0.f ? 1u : 0u) | (hv1 > 0.f ? 2u : 0u);
+                if (o < 32) pos_lo |= bits << o; else pos_hi |= bits << (o - 32);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) y[q] = fmaf(p[c.o_lw3 + q * H + o], hv0, y[q]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) y[q] = fmaf(p[c.o_lw3 + q * H + o + 1], hv1, y[q]);
+            }
+        }
+        float2 M = make_float2(0.f, 0.f), Bs = make_float2(0.f, 0.f);
+        const float4* a4 = reinterpret_cast<const float4*>(ag) + static_cast<size_t>(j) * L;
+        for (int l = 0; l < L; ++l) {
+            const float2 b = Bm[static_cast<size_t>(k) * L + l];
+            const float2 gb = GB[static_cast<size_t>(k) * L + l];
+            const float4 av = a4[l];
+            const float2 t0 = cmul(make_float2(1.f + av.x, av.y), gb), t1 = cmul(make_float2(av.z, av.w), b);
+            M = cadd(M, cadd(t0, t1));
+            Bs = cadd(Bs, b);
+        }
+        const float ar = c.additive ? 0.f : y[0], ai = c.additive ? 0.f : y[1];
+        const float2 ds = d_s[static_cast<size_t>(k) * n_rx + j];
+        const float2 da = cmul(ds, cconj(M)), db = cmul(ds, cconj(Bs));
+        float dy[4];
+        dy[0] = c.additive ? 0.f : da.x;
+        dy[1] = c.additive ? 0.f : da.y;
+        dy[2] = db.x;
+        dy[3] = db.y;
+        u_out[static_cast<size_t>(k) * n_rx + j] = cmul(make_float2(1.f + ar, -ai), ds);
+#pragma unroll
+        for (int f = 0; f < 6; ++f) a[(kAx + f) * rpad] = x[f];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) a[(kAdy + q) * rpad] = dy[q];
+        float2 dh1[H / 2];
+#pragma unroll
+        for (int i = 0; i < H / 2; ++i) dh1[i] = make_float2(0.f, 0.f);
+#pragma unroll 1
+        for (int o = 0; o < H; ++o) {
+            float gs = 0.f;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) gs = fmaf(p[c.o_lw3 + q * H + o], dy[q], gs);
+            const bool on = ((o < 32 ? pos_lo >> o : pos_hi >> (o - 32)) & 1u) != 0u;
+            const float g = on ? gs : 0.f;
+            a[(kAdh2 + o) * rpad] = g;
+            if (g == 0.f) continue;
+            const float2* wr = reinterpret_cast<const float2*>(sW2 + o * H);
+#pragma unroll
+            for (int i = 0; i < H / 2; ++i) dh1[i] = x2::fma(wr[i], x2::bc(g), dh1[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < H / 2; ++i) {
+            a[(kAdh1 + 2 * i) * rpad] = h1[2 * i] > 0.f ? dh1[i].x : 0.f;
+            a[(kAdh1 + 2 * i + 1) * rpad] = h1[2 * i + 1] > 0.f ? dh1[i].y : 0.f;
+        }
+    }
+}
+
+#ifndef RXGS_GRAD_ROWS
+#define RXGS_GRAD_ROWS 32
+#endif
+constexpr int kGradRows = RXGS_GRAD_ROWS;  // rows staged per step in k_cond_bwd_grads
+
+__global__ void __launch_bounds__(256) k_cond_bwd_grads(const float* __restrict__ act, long long rpad,
+                                                        const int* __restrict__ n_rows, int n_rx,
+                                                        float* __restrict__ part) {
+    constexpr int H = 64, PF = kActF + 2;  // row pitch 268 floats: 16-byte aligned rows
+    __shared__ __align__(16) float sA[kGradRows * PF];  // [row][feature]
+    const int t = threadIdx.x;
+    const long long rows_total = static_cast<long long>(*n_rows) * n_rx;
+    const long long per = ((rows_total + gridDim.x - 1) / gridDim.x + kGradRows - 1) / kGradRows * kGradRows;
+    const long long r_begin = static_cast<long long>(blockIdx.x) * per;
+    const long long r_end = r_begin + per < rows_total ? r_begin + per : rows_total;
+    const int o0 = (t >> 4) * 4, i0 = (t & 15) * 4;  // dW2 tile of this thread
+    float w2[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) w2[q] = 0.f;
+    float w1[2] = {0.f, 0.f}, w3 = 0.f, bsum = 0.f;
+    for (long long r0 = r_begin; r0 < r_end; r0 += kGradRows) {
+        const int nr = r_end - r0 < kGradRows ? static_cast<int>(r_end - r0) : kGradRows;
+        __syncthreads();
+        for (int e = t; e < kActF * kGradRows; e += blockDim.x) {
+            const int f = e / kGradRows, r = e % kGradRows;
+            sA[r * PF + f] = r < nr ? act[f * rpad + r0 + r] : 0.f;
+        }
+        __syncthreads();
+        for (int r = 0; r < kGradRows; ++r) {
+            const float* ar = sA + r * PF;
+            const float4 d4 = *reinterpret_cast<const float4*>(ar + kAdh2 + o0);
+            const float4 h4 = *reinterpret_cast<const float4*>(ar + kAh1 + i0);
+            const float dv[4] = {d4.x, d4.y, d4.z, d4.w}, hv[4] = {h4.x, h4.y, h4.z, h4.w};
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) w2[a * 4 + b] = fmaf(dv[a], hv[b], w2[a * 4 + b]);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int idx = t + 256 * e;  // dW1 entry (o, f) of 384
+                if (idx < H * 6) w1[e] = fmaf(ar[kAdh1 + idx / 6], ar[kAx + idx % 6], w1[e]);
+            }
+            w3 = fmaf(ar[kAdy + t / H], ar[kAh2 + t % H], w3);  // dW3 (q, o)
+            if (t < H) bsum += ar[kAdh1 + t];                    // db1
+            else if (t < 2 * H) bsum += ar[kAdh2 + t - H];       // db2
+            else if (t < 2 * H + 4) bsum += ar[kAdy + t - 2 * H]; // db3
+        }
+    }
+    constexpr int NG = local_grad_count(H);
+    float* out = part + static_cast<size_t>(blockIdx.x) * NG;
+    const int o_w1 = 0, o_b1 = H * 6, o_w2 = o_b1 + H, o_b2 = o_w2 + H * H, o_w3 = o_b2 + H, o_b3 = o_w3 + 4 * H;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) out[o_w2 + (o0 + a) * H + i0 + b] = w2[a * 4 + b];
+    for (int e = 0; e < 2; ++e)
+        if (t + 256 * e < H * 6) out[o_w1 + t + 256 * e] = w1[e];
+    out[o_w3 + t] = w3;
+    if (t < H) out[o_b1 + t] = bsum;
+    else if (t < 2 * H) out[o_b2 + t - H] = bsum;
+    else if (t < 2 * H + 4) out[o_b3 + t - 2 * H] = bsum;
+}
+
 // sum CTA partials in CTA order into the f64 gradient vector
 __global__ void k_reduce_parts(int n_parts, int n, const float* __restrict__ part, double* __restrict__ out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -883,13 +1087,35 @@ cudaError_t launch_render_adjoint(const rxgs_txstate_s& st, const float2* G, int
 }
 
 size_t cond_bwd_smem() { return sizeof(float) * (2 * 64 * 64 + 4 * kBwdThreads * kBwdPad + kBwdThreads * 10); }
-int cond_bwd_parts(int sms) { return sms * 2; }
+// partial-sum CTAs: the split backward's gradient kernel needs many CTAs in
+// flight to cover its staged loads
+int cond_bwd_parts(int sms) { return RXGS_BWD_SPLIT ? sms * RXGS_BWD_GRAD_CTAS : sms * 2; }
 int local_grad_n() { return local_grad_count(64); }
+
+size_t cond_bwd_act_bytes(long long rows) {
+    return RXGS_BWD_SPLIT ? sizeof(float) * kActF * static_cast<size_t>((rows + 31) / 32 * 32) : 0;
+}
 
 cudaError_t launch_cond_bwd(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
                             const double* d_rx, int n_rx, const float* d_ag, const float2* d_s, float2* u,
-                            float* part, int n_parts, cudaStream_t s) {
+                            float* part, int n_parts, cudaStream_t s, float* act) {
     const CondDev d = make_dev(cs);
+    if (RXGS_BWD_SPLIT && act) {
+        const long long rpad = (static_cast<long long>(st.visible) * n_rx + 31) / 32 * 32;
+        const size_t smem_r = sizeof(float) * 2 * 64 * 64;
+        auto kr = (d.S == 16 && d.R == 32) ? k_cond_bwd_rows<16, 32> : k_cond_bwd_rows<0, 0>;
+        cudaError_t e = cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_r));
+        if (e != cudaSuccess) return e;
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        kr<<<sms * 3, 128, smem_r, s>>>(d, st.needed_count.as<int>(), st.needed_order.as<int>(),
+                                        sc.d_pos32.as<float4>(), d_rx, n_rx, st.basis32.as<float2>(),
+                                        st.gb32.as<float2>(), d_ag, d_s, u, act, rpad);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if (d.use_local) k_cond_bwd_grads<<<n_parts, 256, 0, s>>>(act, rpad, st.needed_count.as<int>(), n_rx, part);
+        return cudaGetLastError();
+    }
     const size_t smem = cond_bwd_smem();
     auto kern = (d.S == 16 && d.R == 32) ? k_cond_bwd<16, 32> : k_cond_bwd<0, 0>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));

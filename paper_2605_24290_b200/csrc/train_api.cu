@@ -38,6 +38,7 @@ struct rxgs_trainer_s {
     double tau_lr = 1e-2, scale_lr = 5e-3, rot_lr = 1e-3;
     int64_t n_geo = 0;
     DevBuf co64, dv64, b_sig, b_eg, b_eds, b_rg, b_rds, geo_tmp;
+    DevBuf act;  // per-row activations of the split conditioning backward
     // DensifyState (scene.hpp:69-79) of the Stage-I loop, accumulated in apply
     DevBuf dens_acc, dens_cnt;
     // optimizer.reset("transmittance") restarts that group's Adam count
@@ -272,8 +273,13 @@ int rxgs_train_grads(rxgs_trainer t, rxgs_txstate st, const double* rx, int n_rx
         RXGS_CUDA(cudaMemcpyAsync(t->u.p, t->d_s.p, sizeof(float2) * static_cast<size_t>(sc->k) * n_rx,
                                   cudaMemcpyDeviceToDevice, s));
     else
-        RXGS_CUDA(launch_cond_bwd(*c, *sc, *st, d_rx, n_rx, ctx->ag.as<float>(), t->d_s.as<float2>(), t->u.as<float2>(),
-                              t->part.as<float>(), t->n_parts, s));
+    {
+            const size_t ab = cond_bwd_act_bytes(static_cast<long long>(st->visible) * n_rx);
+            if (ab) RXGS_CUDA(t->act.ensure(ab));
+            RXGS_CUDA(launch_cond_bwd(*c, *sc, *st, d_rx, n_rx, ctx->ag.as<float>(), t->d_s.as<float2>(),
+                                      t->u.as<float2>(), t->part.as<float>(), t->n_parts, s,
+                                      ab ? t->act.as<float>() : nullptr));
+        }
     if (c && c->use_local()) RXGS_CUDA(launch_reduce_parts(t->n_parts, nl, t->part.as<float>(), gpar + c->o_lw1, s));
     RXGS_CUDA(launch_dbase(c, *sc, *st, n_rx, ctx->ag.as<float>(), t->u.as<float2>(), gbase, s));
     if (c && c->use_global()) {
