@@ -722,27 +722,43 @@ __global__ void __launch_bounds__(256) k_cond_bwd_grads(const float* __restrict_
     const long long r_begin = static_cast<long long>(blockIdx.x) * per;
     const long long r_end = r_begin + per < rows_total ? r_begin + per : rows_total;
     const int o0 = (t >> 4) * 4, i0 = (t & 15) * 4;  // dW2 tile of this thread
-    float w2[16];
+    float2 w2[8];  // row a, column pair bp: w2[a * 2 + bp]
 #pragma unroll
-    for (int q = 0; q < 16; ++q) w2[q] = 0.f;
+    for (int q = 0; q < 8; ++q) w2[q] = make_float2(0.f, 0.f);
     float w1[2] = {0.f, 0.f}, w3 = 0.f, bsum = 0.f;
-    for (long long r0 = r_begin; r0 < r_end; r0 += kGradRows) {
+    // the next stage's activations are loaded into registers while this one
+    // is consumed from shared memory (one stage of software pipelining)
+    constexpr int kPer = (kActF * kGradRows + 255) / 256;
+    float nxt[kPer];
+    auto fetch = [&](long long r0) {
         const int nr = r_end - r0 < kGradRows ? static_cast<int>(r_end - r0) : kGradRows;
-        __syncthreads();
-        for (int e = t; e < kActF * kGradRows; e += blockDim.x) {
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int e = t + 256 * u;
             const int f = e / kGradRows, r = e % kGradRows;
-            sA[r * PF + f] = r < nr ? act[f * rpad + r0 + r] : 0.f;
+            nxt[u] = (e < kActF * kGradRows && r < nr) ? act[f * rpad + r0 + r] : 0.f;
+        }
+    };
+    if (r_begin < r_end) fetch(r_begin);
+    for (long long r0 = r_begin; r0 < r_end; r0 += kGradRows) {
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int e = t + 256 * u;
+            if (e < kActF * kGradRows) sA[(e % kGradRows) * PF + e / kGradRows] = nxt[u];
         }
         __syncthreads();
+        if (r0 + kGradRows < r_end) fetch(r0 + kGradRows);
         for (int r = 0; r < kGradRows; ++r) {
             const float* ar = sA + r * PF;
             const float4 d4 = *reinterpret_cast<const float4*>(ar + kAdh2 + o0);
             const float4 h4 = *reinterpret_cast<const float4*>(ar + kAh1 + i0);
-            const float dv[4] = {d4.x, d4.y, d4.z, d4.w}, hv[4] = {h4.x, h4.y, h4.z, h4.w};
+            const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-                for (int b = 0; b < 4; ++b) w2[a * 4 + b] = fmaf(dv[a], hv[b], w2[a * 4 + b]);
+            for (int a = 0; a < 4; ++a) {  // FFMA2 over column pairs (each lane exactly fmaf)
+                w2[2 * a] = x2::fma(x2::bc(dv[a]), make_float2(h4.x, h4.y), w2[2 * a]);
+                w2[2 * a + 1] = x2::fma(x2::bc(dv[a]), make_float2(h4.z, h4.w), w2[2 * a + 1]);
+            }
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int idx = t + 256 * e;  // dW1 entry (o, f) of 384
@@ -760,7 +776,10 @@ __global__ void __launch_bounds__(256) k_cond_bwd_grads(const float* __restrict_
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) out[o_w2 + (o0 + a) * H + i0 + b] = w2[a * 4 + b];
+        for (int b = 0; b < 4; ++b) {
+            const float2 v = w2[2 * a + b / 2];
+            out[o_w2 + (o0 + a) * H + i0 + b] = (b & 1) ? v.y : v.x;
+        }
     for (int e = 0; e < 2; ++e)
         if (t + 256 * e < H * 6) out[o_w1 + t + 256 * e] = w1[e];
     out[o_w3 + t] = w3;
