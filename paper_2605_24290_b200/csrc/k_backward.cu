@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(64) k_bwd_walk(DevGrid g, int cb, const int64_
             T = t_prev * (1.0 - w);
             if (!clamped) {
                 const double dm2 = dw * r.tau * (-0.5) * gg;
-                const double st = r.sin_theta, ct = cos(r.theta);
+                const double st = r.sin_theta, ct = r.cos_theta;  // = cos(theta), computed once in k_tx_prep
                 v[0] = dw * gg;
                 v[1] = dm2 * dt * dt;
                 v[2] = dm2 * dt * dp;

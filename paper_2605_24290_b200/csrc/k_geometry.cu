@@ -136,6 +136,7 @@ __global__ void k_tx_prep(int K, int l_max_rt, int C, const double* __restrict__
             r.theta = theta;
             r.phi = phi;
             r.sin_theta = st;
+            r.cos_theta = ct;
             r.pa = pa;
             r.pbc = pb + pc;
             r.pd = pd;

@@ -31,7 +31,7 @@ struct DevGrid {
 
 // Receiver-independent per-Gaussian record read by the FP64 blend walk.
 struct alignas(64) GaussRec {
-    double theta, phi, sin_theta, pa, pbc, pd, tau, pad;
+    double theta, phi, sin_theta, pa, pbc, pd, tau, cos_theta;  // cos_theta: for the adjoint re-walk
 };
 
 // Error capture: thread-local message + status.
