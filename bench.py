@@ -91,9 +91,47 @@ class ClockSampler:
     def __init__(self, device):
         self.device = device
         self.proc = None
+        self.thread = None
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{device}.csv")
 
     def start(self):
+        # NVML in a thread, ~1 ms period: the timed region is tens of ms, shorter
+        # than nvidia-smi's loop period (kept as the fallback)
+        self.samples = []
+        try:
+            import threading
+            import pynvml
+            pynvml.nvmlInit()
+            h = None
+            try:  # the CUDA device by PCI bus id (NVML indices ignore CUDA_VISIBLE_DEVICES)
+                import torch
+                pr = torch.cuda.get_device_properties(self.device)
+                bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+                h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self.stop_ev = threading.Event()
+            bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+
+            def run():
+                while not self.stop_ev.is_set():
+                    try:
+                        mhz = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((mhz, [n for n, b in bits.items() if r & b]))
+                    except Exception:
+                        pass
+                    self.stop_ev.wait(0.001)
+
+            self.thread = threading.Thread(target=run, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.thread = None
         try:
             os.makedirs(os.path.dirname(self.path), exist_ok=True)
             self.fh = open(self.path, "w")
@@ -104,6 +142,18 @@ class ClockSampler:
             self.proc = None
 
     def stop(self):
+        if getattr(self, "thread", None) is not None:
+            self.stop_ev.set()
+            self.thread.join(timeout=5)
+            if not self.samples:
+                return None
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            with open(self.path, "w") as fh:  # the raw samples, for the record
+                for mhz, rs in self.samples:
+                    fh.write(f"{mhz},{self.max_mhz},{'|'.join(rs)}\n")
+            reasons = sorted({n for _, rs in self.samples for n in rs})
+            return {"sm_mhz": statistics.median(m for m, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                    "reasons": reasons, "samples": len(self.samples), "source": "NVML, ~1 ms period"}
         if not self.proc:
             return None
         self.proc.terminate()
