@@ -367,6 +367,12 @@ static void ctx_free(rxgs_ctx ctx) {
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
     for (auto* t : ctx->spare_tx) delete t;
     for (auto e : ctx->chunk_events) cudaEventDestroy(e);
+    if (ctx->aux_ev) cudaEventDestroy(ctx->aux_ev);
+    if (ctx->aux_done) cudaEventDestroy(ctx->aux_done);
+    if (ctx->aux) {
+        ctx->aux->closed = true;
+        if (ctx->aux->refs == 0) ctx_free(ctx->aux);
+    }
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
@@ -1402,9 +1408,32 @@ int rxgs_coverage_table(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const rxgs_gri
         yc = ctx->ycache.as<float4>();
     }
     RXGS_CUDA(ctx->signals.ensure(std::max<size_t>(static_cast<size_t>(sc->k) * n_rx, 1) * sizeof(float2)));
+    // transmitter states are built one ahead on the helper context, so the
+    // next state's projection / sort / walk overlap this one's signals and
+    // compositing (the builder's host syncs block only its own stream)
+#ifndef RXGS_COV_PIPE
+#define RXGS_COV_PIPE 1
+#endif
+    rxgs_ctx bctx = ctx;
+    if (RXGS_COV_PIPE && n_tx > 1) {
+        if (!ctx->aux) {
+            RX_TRY(rxgs_ctx_create(ctx->device, &ctx->aux));
+            RXGS_CUDA(cudaEventCreateWithFlags(&ctx->aux_ev, cudaEventDisableTiming));
+            RXGS_CUDA(cudaEventCreateWithFlags(&ctx->aux_done, cudaEventDisableTiming));
+        }
+        bctx = ctx->aux;
+        bctx->profile = ctx->profile;
+    }
+    const int64_t aux_launches0 = bctx->launches;
+    rxgs_txstate st_next = nullptr;
+    RX_TRY(rxgs_tx_state_build(bctx, sc, txh.data(), grid, &st_next));
     for (int t = 0; t < n_tx; ++t) {
-        rxgs_txstate st = nullptr;
-        RX_TRY(rxgs_tx_state_build(ctx, sc, txh.data() + 3 * static_cast<size_t>(t), grid, &st));
+        rxgs_txstate st = st_next;
+        st_next = nullptr;
+        if (bctx != ctx) {  // this stream's work on st after the builder's
+            RXGS_CUDA(cudaEventRecord(ctx->aux_ev, bctx->stream));
+            RXGS_CUDA(cudaStreamWaitEvent(s, ctx->aux_ev, 0));
+        }
         const DevGrid& g = st->grid;
         const int n_tb = g.n_tiles * g.cell_blocks;
         int rc = RXGS_OK;
@@ -1438,8 +1467,30 @@ int rxgs_coverage_table(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const rxgs_gri
                                      nullptr, s);
         ctx->launches += 3;
         if (e != cudaSuccess) rc = cuda_fail(e, "coverage_table");
+        if (!rc && t + 1 < n_tx)
+            rc = rxgs_tx_state_build(bctx, sc, txh.data() + 3 * static_cast<size_t>(t + 1), grid, &st_next);
+        if (bctx != ctx) {  // st's buffers return to the builder's pool: wait for this stream's use
+            cudaEventRecord(ctx->aux_done, s);
+            cudaEventSynchronize(ctx->aux_done);
+        }
         rxgs_tx_state_destroy(st);
-        if (rc) return rc;
+        if (rc) {
+            if (st_next) rxgs_tx_state_destroy(st_next);
+            return rc;
+        }
+    }
+    if (bctx != ctx) {  // the builder's launches and phase timings count for this context
+        ctx->launches += bctx->launches - aux_launches0;
+        if (ctx->profile) {
+            resolve_timings(bctx);
+            for (const auto& kv : bctx->stats) {
+                KStat& d = ctx->stats[kv.first];
+                d.ms += kv.second.ms;
+                d.launches += kv.second.launches;
+                d.work += kv.second.work;
+            }
+            bctx->stats.clear();
+        }
     }
     if (c) {
         if (c->use_global()) c->global_calls += static_cast<int64_t>(n_rx) * sc->L;

@@ -159,6 +159,11 @@ struct rxgs_ctx_s {
     cudaStream_t copy_stream = nullptr;  // D2H of finished receiver chunks (host outputs)
     std::vector<cudaEvent_t> chunk_events;
     bool closed = false;  // rxgs_ctx_destroy called while handles were alive
+    // helper context (own stream and scratch) that builds the next
+    // transmitter's state while this one's stream renders the current one
+    // (rxgs_coverage_table); created on first use
+    rxgs_ctx_s* aux = nullptr;
+    cudaEvent_t aux_ev = nullptr, aux_done = nullptr;
 };
 
 struct rxgs_scene_s {
