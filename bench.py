@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-config3", action="store_true", help="skip the coverage-table (config 3) leg")
     ap.add_argument("--no-config5", action="store_true", help="skip the 2M / 180x720 (config 5) leg")
     ap.add_argument("--no-lmax9", action="store_true", help="skip the config-2 l_max = 9 (L = 100) leg")
+    ap.add_argument("--no-config1", action="store_true", help="skip the config-1 single-query latency leg")
     return ap.parse_args()
 
 
@@ -365,6 +366,7 @@ def run_b200(args):
     cov = None if args.no_config3 else bench_coverage(args, capi, ctx, stream, dev, rank, world)
     large = None if args.no_config5 else bench_large(args, capi, ctx, stream, dev, rank, world)
     lmax9 = None if args.no_lmax9 else bench_lmax9(args, capi, ctx, stream, dev, rank, world)
+    c1 = None if args.no_config1 or rank != 0 else bench_config1(args, capi, ctx, dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -387,7 +389,7 @@ def run_b200(args):
                 "config": workload(args), "e2e": e2e, "gpu_launches": int(launches),
                 "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
                 "tx_state": stats, "train_config4": train, "config3": cov, "config5": large,
-                "config2_lmax9": lmax9}
+                "config2_lmax9": lmax9, "config1": c1}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -648,6 +650,63 @@ def bench_large(args, capi, ctx, stream, dev, rank, world):
             "e2e": {"value": world * n / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": int(rx.nbytes + 24), "d2h_bytes_per_step": int(spec_h.nbytes + rssi_h.nbytes)},
             "phase_ms": phases, "gpu_launches": int(launches), "tx_state": stats, "cpu_baseline": cpu}
+
+
+def bench_config1(args, capi, ctx, dev):
+    """BASELINE config 1 (the reference's CPU-runnable case): 10k Gaussians,
+    1 Tx, 1 Rx = (1.1, 0.7, 0.2), 90x360 spectrum.  Latency of one query end
+    to end through the public API (build_tx_state + render_queries with host
+    input and output, conditioned), median of 20 after warm-up, wall clock
+    around the synchronous calls; rank 0 only (a single query does not shard)."""
+    import time
+    K = 10_000
+    scene = ctx.scene(capi.synth_scene(K, 2, 1, 7), "spectrum")
+    lo, hi = scene.bounds(0.0)
+    cfg = capi.cond_cfg()
+    cond = ctx.cond(cfg, capi.synth_cond(cfg, 2, 1, lo, hi, 3, True))
+    olo, ohi = scene.bounds(0.1)
+    cond.build_occupancy(scene, 32, olo, ohi)
+    grid = capi.Grid(args.n_theta, args.n_phi, 8, 1.0)
+    tx = np.array(TX)
+    rx = np.array([[1.1, 0.7, 0.2]])
+    spec = np.empty((1, args.n_theta, args.n_phi), np.float32)
+    rssi = np.empty(1, np.float32)
+
+    def query():
+        st = scene.tx_state(tx, grid)
+        scene.render_queries(cond, st, rx, spec, rssi)
+
+    for _ in range(5):
+        query()
+    ts = []
+    for _ in range(20):
+        t0 = time.perf_counter()
+        query()
+        ts.append((time.perf_counter() - t0) * 1e3)
+    ms = float(np.median(ts))
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import oracle as O  # cpu_baseline leg
+            chk = O.reference()
+            sc = chk.synth_scene(K, 2, 1, 7)
+            h = chk.scene(sc, "spectrum")
+            rlo, rhi = chk.scene_bounds(h, 0.0)
+            rcfg = O.cond_cfg()
+            params = chk.synth_cond(rcfg, 2, 1, rlo, rhi, 3, True)
+            rolo, rohi = chk.scene_bounds(h, 0.1)
+            rc = chk.cond(rcfg, params, chk.build_occupancy(h, 32, rolo, rohi), rolo, rohi)
+            threads = os.cpu_count() or 1
+            secs, _, _ = chk.bench_queries(h, rc, O.Grid(args.n_theta, args.n_phi, 8, 1.0), TX, rx, threads)
+            cpu = {"ms_per_query": secs * 1e3, "cores": threads, "kind": "reference",
+                   "sample": "the same query: build_tx_state + condition_forward + render_field + aggregation"}
+        except Exception as ex:
+            cpu = {"error": str(ex)}
+    del scene, cond
+    return {"workload": "config1: K=10k, 1 Tx, 1 Rx (1.1, 0.7, 0.2), 90x360 spectrum + RSSI, conditioned (full)",
+            "ms_per_query": ms, "queries_per_s": 1e3 / ms, "what": "wall clock of the synchronous public-API "
+            "calls with host buffers (latency-bound: one receiver)", "cpu_reference": cpu}
 
 
 def bench_lmax9(args, capi, ctx, stream, dev, rank, world):
