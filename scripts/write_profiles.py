@@ -13,7 +13,43 @@ if os.path.exists(lc):
     open(os.path.join(prof, f"{tag}_launches.txt"), "w").write(S.launches(lc) + "\n")
 traffic = {"source": "ncu --set full --clock-control none, one launch each; bench.py config 2 (K=100k, 1024 rx, 90x360); "
                      "k_cov_signal from the config-3 leg (K=500k)"}
-for k in ["k_cond_tc", "k_fle_gemm", "k_composite_tc", "k_walk", "k_tx_prep", "k_cov_signal"]:
+for name in ("train", "joint"):  # scripts/gpu_profiles_train.sh
+    lc = os.path.join(out, f"{tag}_{name}_launches.csv")
+    if os.path.exists(lc):
+        open(os.path.join(prof, f"{tag}_{name}_launches.txt"), "w").write(S.launches(lc) + "\n")
+
+
+def source_hotspots(rep, rows_per_launch=None, top=30):
+    """Per CUDA source line: warp instructions and stall-sample share (ncu source page, -lineinfo)."""
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                         capture_output=True, text=True).stdout
+    recs, fname = [], "?"
+    for r in csv.reader(txt.splitlines()):
+        if r and r[0] == "File Name":
+            fname = r[1].split("/")[-1]
+            continue
+        if len(r) > 8 and r[0].isdigit():
+            try:
+                recs.append((fname, int(r[0]), r[1].strip()[:88], int(r[4]), int(r[7])))
+            except ValueError:
+                pass
+    tot_s = sum(x[3] for x in recs) or 1
+    tot_i = sum(x[4] for x in recs) or 1
+    lines = [f"source-level hotspots of {os.path.basename(rep)} (ncu source page; instructions and stall samples "
+             f"attributed to CUDA lines via -lineinfo)",
+             f"attributed warp instructions: {tot_i}, stall samples: {tot_s}",
+             "   line  instr%  stall%  source"]
+    for x in sorted(recs, key=lambda x: -x[3])[:top]:
+        lines.append(f"  {x[1]:5d}  {100 * x[4] / tot_i:5.1f}  {100 * x[3] / tot_s:5.1f}   {x[2]}")
+    return "\n".join(lines) + "\n"
+
+
+rep = os.path.join(out, f"{tag}_k_cond_tc.ncu-rep")
+if os.path.exists(rep):
+    open(os.path.join(prof, f"{tag}_k_cond_tc_source.txt"), "w").write(source_hotspots(rep))
+
+for k in ["k_cond_tc", "k_fle_gemm", "k_composite_tc", "k_walk", "k_tx_prep", "k_cov_signal", "k_cond_bwd_rows",
+          "k_cond_bwd_grads"]:
     rep = os.path.join(out, f"{tag}_{k}.ncu-rep")
     if not os.path.exists(rep):
         continue
