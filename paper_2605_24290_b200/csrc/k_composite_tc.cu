@@ -44,6 +44,9 @@ __device__ __forceinline__ uint32_t mn_off(int mn, int k, uint32_t lbo) {
     return static_cast<uint32_t>((k >> 3) * lbo + (mn >> 3) * kSBO + (k & 7) * 16 + (mn & 7) * 2);
 }
 
+#ifndef RXGS_COMP_WAIT
+#define RXGS_COMP_WAIT tc::mbar_wait
+#endif
 #ifndef RXGS_COMP_RX_FAST
 #define RXGS_COMP_RX_FAST 1
 #endif
@@ -155,7 +158,7 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
         uint8_t* b_hi = base + 2 * kABytes;
         uint8_t* b_lo = base + 2 * kABytes + kBBytes;
         if (st >= 2) {  // the MMAs that read this buffer two stages ago must be done
-            tc::mbar_wait(&bars[buf], ph[buf]);
+            RXGS_COMP_WAIT(&bars[buf], ph[buf]);
             ph[buf] ^= 1u;
         }
 #pragma unroll
@@ -197,11 +200,11 @@ __global__ void __launch_bounds__(kThr) k_composite_tc(DevGrid g, const int64_t*
     // ---- wait for the last stage(s)
     if (n_stages >= 2) {
         const int b2 = (n_stages - 2) & 1;
-        tc::mbar_wait(&bars[b2], ph[b2]);
+        RXGS_COMP_WAIT(&bars[b2], ph[b2]);
     }
     if (n_stages >= 1) {
         const int b1 = (n_stages - 1) & 1;
-        tc::mbar_wait(&bars[b1], ph[b1]);
+        RXGS_COMP_WAIT(&bars[b1], ph[b1]);
     }
     tc::fence_after_sync();
 

@@ -88,6 +88,27 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
     } while (!done);
 }
 
+// try_wait without a hint, then a short __nanosleep between polls: the
+// waiting warp gives its issue slots to the other groups' SIMT work
+#ifndef RXGS_BACKOFF_NS
+#define RXGS_BACKOFF_NS 64
+#endif
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t done = 0;
+    for (;;) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (done) break;
+        __nanosleep(RXGS_BACKOFF_NS);
+    }
+}
+
 // ---- MMA: D[tmem] (+)= A[tmem] * B[smem]^T, bf16 x bf16 -> f32
 __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
     asm volatile(
