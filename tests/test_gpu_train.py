@@ -381,3 +381,42 @@ def test_stage1_densify_and_tau_reset(ctx, capi, ref):
     gtau = tr.get_geometry_grads()[3]
     tr.apply()
     assert rel_err(capi.scene_arrays(scene)["tau_logits"], _adam1(tau0, gtau, 1e-2)).max() < 1e-12
+
+
+def test_train_geometry_api_errors(ctx, capi, ref):
+    """Densification / transmittance reset need the geometry step; geometry must
+    be enabled before the first step (reference-style located messages)."""
+    sc, scene, grid, og = _stage1_setup(capi, ctx, ref, k=200)
+    tr = capi.Trainer(ctx, scene, None)
+    with pytest.raises(capi.InvalidArgument, match="densification needs rxgs_trainer_enable_geometry"):
+        tr.densify(10.0)
+    with pytest.raises(capi.InvalidArgument, match="transmittance reset needs rxgs_trainer_enable_geometry"):
+        tr.reset_transmittance()
+    with pytest.raises(capi.InvalidArgument, match="geometry gradients need rxgs_trainer_enable_geometry"):
+        tr.get_geometry_grads()
+    rx = capi.synth_points(1, 41, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
+    tr.grads(scene.tx_state(TX, grid), rx, _targets(1, grid.cells, 3))
+    tr.apply()
+    import ctypes
+    geo = np.asarray(capi.Trainer.GEOMETRY_DEFAULTS, np.float64)
+    assert capi._lib.rxgs_trainer_enable_geometry(tr.h, geo.ctypes.data) == capi.RXGS_ERR_INVALID
+    assert "enable geometry before the first step" in capi._lib.rxgs_last_error().decode()
+
+
+def test_train_unconditioned_stage2_matches_reference(ctx, capi, ref):
+    """cond == NULL without geometry: the base coefficients alone, d_base =
+    backward_render's d_coeffs summed over the batch."""
+    sc, scene, grid, og = _stage1_setup(capi, ctx, ref, k=300)
+    rx = capi.synth_points(2, 43, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
+    tg = _targets(2, grid.cells, 14)
+    tr = capi.Trainer(ctx, scene, None)
+    assert tr.n == tr.n_base
+    loss = tr.grads(scene.tx_state(TX, grid), rx, tg)
+    db, dp = tr.get_grads()
+    rs = ref.scene(sc, "spectrum")
+    want = 0.0
+    for j in range(2):
+        r = ref.train_sample(rs, None, og, TX, rx[j], tg[j].astype(np.float64))
+        assert rel_err(loss[j], r["loss"]) < TOL
+        want = want + r["d_base"]
+    assert rel_err(db, want).max() < TOL
