@@ -420,3 +420,25 @@ def test_train_unconditioned_stage2_matches_reference(ctx, capi, ref):
         assert rel_err(loss[j], r["loss"]) < TOL
         want = want + r["d_base"]
     assert rel_err(db, want).max() < TOL
+
+
+def test_joint_densify_keeps_conditioning(ctx, capi, ref):
+    """Densifying a conditioned (joint) trainer remaps the per-Gaussian groups
+    only: the conditioning parameters are untouched and training continues on
+    the new row set with the conditioning gradients still matching."""
+    sc, scene, cond, grid, og, rscene, rcond, params = _setup(capi, ctx, ref, k=400)
+    rx = capi.synth_points(1, 47, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
+    tg = _targets(1, grid.cells, 15)
+    tr = capi.Trainer(ctx, scene, cond, geometry=True)
+    tr.grads(scene.tx_state(TX, grid), rx, tg)
+    tr.apply()
+    par = capi.cond_params(cond)
+    k0 = scene.k
+    rep = tr.densify(40.0, (1e-6, 0.01, 0.1, 0.8), 3, 0)
+    assert sum(rep) > 0 and scene.k != k0
+    assert np.array_equal(capi.cond_params(cond), par)
+    assert tr.n == tr.n_base + cond.param_count + 11 * scene.k
+    loss = tr.grads(scene.tx_state(TX, grid), rx, tg)
+    assert np.isfinite(loss).all()
+    tr.apply()
+    assert np.isfinite(capi.scene_arrays(scene)["positions"]).all()
