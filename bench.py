@@ -183,13 +183,22 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU reference
-def cpu_reference_run(args, sample, threads):
-    """The reference's own CPU path (oracle/_ref: the unmodified reference
-    sources, see oracle/Makefile) on a bounded receiver sample."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_reference_setup(args):
+    """The reference model (oracle/_ref: the unmodified reference sources, see
+    oracle/Makefile) built once: scene, conditioning, occupancy."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O  # cpu_baseline leg: the one place bench.py executes oracle/
     chk = O.reference()
-    kind = "reference"
     if chk is None:
         raise RuntimeError("oracle/_ref/librxgs_ref.so missing (build() compiles it where /root/reference exists)")
     sc = chk.synth_scene(args.gaussians, 2, 1, 7)
@@ -200,10 +209,16 @@ def cpu_reference_run(args, sample, threads):
     olo, ohi = chk.scene_bounds(h, 0.1)
     occ = chk.build_occupancy(h, 32, olo, ohi)
     cond = chk.cond(cfg, params, occ, olo, ohi)
+    return chk, h, cond, O.Grid(args.n_theta, args.n_phi, 8, 1.0)
+
+
+def cpu_reference_run(args, sample, threads, setup=None):
+    """One bounded sample of the config-2 step on the reference's CPU path:
+    build_tx_state + `sample` receivers (conditioning, render, aggregation)."""
+    chk, h, cond, grid = setup if setup is not None else cpu_reference_setup(args)
     rx = chk.synth_points(sample, 11, "bench.rx", BOX_LO, BOX_HI, 0.05)
-    grid = O.Grid(args.n_theta, args.n_phi, 8, 1.0)
     secs, _, _ = chk.bench_queries(h, cond, grid, TX, rx, threads)
-    return secs, kind
+    return secs, "reference"
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -212,9 +227,25 @@ def run_b200(args):
     import torch.distributed as dist
 
     rank, world, local = dist_env()
+    if args.gpus != world and rank == 0:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; using {world} rank(s)", file=sys.stderr)
+    n_dev = torch.cuda.device_count()
+    shared = world > n_dev  # functional check only: ranks share GPUs, gloo plumbing
+    if shared:
+        print(f"bench: {world} ranks on {n_dev} GPU(s): ranks share devices over gloo (NOT a scaling "
+              f"measurement)", file=sys.stderr)
+        local = local % n_dev
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 and not shared:
+        # NCCL's communicator lines (rank / nranks / transport) on the record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        warm = torch.ones(1, device=torch.device("cuda", local))
+        dist.all_reduce(warm)  # communicator up before any timing
+        torch.cuda.synchronize()
+    elif world > 1:
+        dist.init_process_group("gloo")
     from paper_2605_24290_b200 import capi
 
     dev = torch.device("cuda", local)
@@ -371,10 +402,10 @@ def run_b200(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        sample = args.cpu_sample or 64
+        sample = args.cpu_sample or 256
         try:
             secs, kind = cpu_reference_run(args, sample, threads)
-            cpu = {"value": sample / secs, "unit": UNIT, "cores": threads, "kind": kind,
+            cpu = {"value": sample / secs, "unit": UNIT, "cores": threads, "kind": kind, "cpu_model": cpu_model(),
                    "sample": f"{sample} receivers of the same workload (K={args.gaussians}, "
                              f"{args.n_theta}x{args.n_phi}), build_tx_state + condition_forward (fanned over "
                              f"{threads} threads) + render_field (chunks of 16, {threads} threads) + "
@@ -388,8 +419,8 @@ def run_b200(args):
                 "vs_baseline": None, "dtype": "f32 (FP64 geometry/walk)", "data": "synthetic",
                 "config": workload(args), "e2e": e2e, "gpu_launches": int(launches),
                 "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
-                "tx_state": stats, "train_config4": train, "config3": cov, "config5": large,
-                "config2_lmax9": lmax9, "config1": c1}
+                "train_config4": train, "config1": c1, "config2_lmax9": lmax9, "config3": cov,
+                "config5": large, "tx_state": stats}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -441,11 +472,11 @@ def bench_train(args, capi, ctx, scene, cond, grid, stream, dev, rank, world):
         torch.cuda.synchronize(dev)
         return max_over_ranks(s0.elapsed_time(s1) / n_steps, dev), tr.n
 
-    ms, n_grad = time_trainer(None)  # spectrum L1 (lambda_ssim = lambda_fft = 0)
+    ms, n_grad = time_trainer(list(capi.Trainer.L1_ONLY))  # spectrum L1 (lambda_ssim = lambda_fft = 0)
     hp = list(capi.Trainer.DEFAULTS)
     hp[3], hp[4] = 0.2, 0.1  # the reference's default LossWeights (trainer.hpp:25-29)
     ms_full, _ = time_trainer(hp)
-    ms_joint, n_joint = time_trainer(None, geometry=True)
+    ms_joint, n_joint = time_trainer(list(capi.Trainer.L1_ONLY), geometry=True)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:  # reference CPU training sample (oracle/_ref), one sample, all host threads in render/backward
@@ -502,27 +533,28 @@ def _ref_model(O, chk, k):
 
 def bench_coverage(args, capi, ctx, stream, dev, rank, world):
     """BASELINE config 3: RSSI coverage table, K=500k, 64 Tx x 1024 Rx, 90x360.
-    Receivers sharded over ranks (1024 total), every rank does all 64 Tx
-    (strong scaling of the fixed table).  One step = the whole table through
-    rxgs_coverage_table: global + local conditioning once per receiver
-    (Tx-independent, cached in HBM), then per Tx build_tx_state + factorised
-    signal + RSSI compositing."""
+    The table is split over a gt x gr grid of ranks (dist.coverage_grid:
+    transmitter blocks x receiver blocks by a cost model), so per-Tx state
+    builds are not replicated on every rank (strong scaling of the fixed
+    table).  One step = this rank's block through rxgs_coverage_table:
+    global + local conditioning once per receiver (Tx-independent, cached in
+    HBM), then per Tx build_tx_state + factorised signal + RSSI compositing.
+    Timed with per-kernel profiling OFF; phases come from a separate pass."""
     import torch
-    from paper_2605_24290_b200.dist import max_over_ranks, shard_range
+    from paper_2605_24290_b200.dist import coverage_grid, coverage_shard, max_over_ranks
     K, n_tx, n_rx_total = 500_000, 64, 1024
-    b, e = shard_range(n_rx_total, rank, world)
-    rx = capi.synth_points(n_rx_total, 11, "bench.rx", BOX_LO, BOX_HI, 0.05)[b:e]
-    tx = capi.synth_points(n_tx, 13, "bench.tx", BOX_LO, BOX_HI, 0.05)
+    gt, gr = coverage_grid(n_tx, n_rx_total, world)
+    tb, te, rb, re_ = coverage_shard(n_tx, n_rx_total, rank, world, (gt, gr))
+    rx = capi.synth_points(n_rx_total, 11, "bench.rx", BOX_LO, BOX_HI, 0.05)[rb:re_]
+    tx = capi.synth_points(n_tx, 13, "bench.tx", BOX_LO, BOX_HI, 0.05)[tb:te]
     scene = ctx.scene(capi.synth_scene(K, 2, 1, 7), "rssi")
     cond = _cond_for(capi, ctx, scene)
     grid = capi.Grid(90, 360, 8, 1.0)
     rx_d, tx_d = torch.from_numpy(rx).to(dev), torch.from_numpy(tx).to(dev)
-    out_d = torch.empty((n_tx, rx.shape[0]), dtype=torch.float32, device=dev)
+    out_d = torch.empty((tx.shape[0], rx.shape[0]), dtype=torch.float32, device=dev)
     n_steps = max(2, min(args.steps, 3))
     scene.coverage_table(cond, grid, tx_d, rx_d, out_d)  # warm-up (pool, caches)
     torch.cuda.synchronize(dev)
-    ctx.reset_stats()
-    ctx.profile(True)
     l0 = ctx.launch_count()
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0.record(stream)
@@ -532,11 +564,16 @@ def bench_coverage(args, capi, ctx, stream, dev, rank, world):
     torch.cuda.synchronize(dev)
     ms = max_over_ranks(s0.elapsed_time(s1) / n_steps, dev)
     launches = (ctx.launch_count() - l0) // n_steps
-    phases = {n: ctx.kernel_stats(n)[0] / n_steps for n in ("cond_global", "local_cache", "tx_prep", "walk",
-                                                             "cov_signal", "composite")}
+    ctx.reset_stats()  # per-phase times: a separate profiled pass
+    ctx.profile(True)
+    scene.coverage_table(cond, grid, tx_d, rx_d, out_d)
+    torch.cuda.synchronize(dev)
+    phases = {n: ctx.kernel_stats(n)[0] for n in ("cond_global", "local_cache", "tx_prep", "sort", "walk",
+                                                   "cov_signal", "composite")}
     ctx.profile(False)
     # end to end with host buffers (tx/rx in, table out)
-    out_h = np.empty((n_tx, rx.shape[0]), np.float32)
+    out_h = np.empty((tx.shape[0], rx.shape[0]), np.float32)
+    torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     scene.coverage_table(cond, grid, tx, rx, out_h)
     e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3, dev)
@@ -562,7 +599,8 @@ def bench_coverage(args, capi, ctx, stream, dev, rank, world):
     ctx.release_cache()
     return {"workload": "config3: K=500k, 64 Tx x 1024 Rx RSSI coverage table, 90x360, conditioned (full)",
             "value": queries / (ms / 1e3), "unit": "queries/s", "ms_per_table": ms, "steps": n_steps,
-            "scaling": "strong (Rx sharded, all Tx per rank)", "n_gpus": world,
+            "scaling": "strong (fixed table split over ranks)", "n_gpus": world,
+            "rank_grid": {"tx_blocks": gt, "rx_blocks": gr, "rank0_block": [tb, te, rb, re_]},
             "e2e": {"value": queries / (e2e_ms / 1e3), "unit": "queries/s", "ms_per_table": e2e_ms,
                     "h2d_bytes_per_step": int(tx.nbytes + rx.nbytes), "d2h_bytes_per_step": int(out_h.nbytes)},
             "phase_ms": phases, "gpu_launches": int(launches), "cpu_baseline": cpu}
@@ -785,16 +823,20 @@ def bench_lmax9(args, capi, ctx, stream, dev, rank, world):
 
 
 def run_reference(args):
+    """The reference arm: the reference's own CPU implementation of the path
+    (oracle/_ref) on all host threads, rank 0 only.  Each step is a bounded
+    sample of the config-2 step: build_tx_state + 256 of its 1024 receivers."""
     rank, world, local = dist_env()
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    sample = args.cpu_sample or 32
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        cpu_reference_run(args, min(sample, 4), threads)
+    sample = args.cpu_sample or 256
+    setup = cpu_reference_setup(args)
+    for _ in range(min(args.warmup, 1)):
+        cpu_reference_run(args, min(sample, 4), threads, setup)
     t = []
     for _ in range(args.steps):
-        secs, kind = cpu_reference_run(args, sample, threads)
+        secs, kind = cpu_reference_run(args, sample, threads, setup)
         t.append(secs)
     v = sample / (sum(t) / len(t))
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -802,13 +844,32 @@ def run_reference(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload(args), "impl": "reference",
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": f"{sample} receivers per step of the same workload"},
+                             "cpu_model": cpu_model(),
+                             "sample": f"{sample} receivers per step of the same workload (build_tx_state once "
+                                       f"per step + condition_forward fanned over {threads} threads + "
+                                       f"render_field chunks of 16 with threads={threads} + aggregation)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+def spawn_ranks(n):
+    """`bench.py --gpus N` outside torchrun: re-launch this command under
+    torch.distributed.run, one rank (process) per GPU on 127.0.0.1; rank 0
+    prints the JSON line."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "b200":
+        sys.exit(spawn_ranks(args.gpus))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -292,12 +292,13 @@ int rxgs_predict(rxgs_ctx ctx, rxgs_scene scene, rxgs_cond c, const rxgs_grid* g
 /* ------------------------------------------------------------ training (config 4)
  * One step of the Stage-II chain of conditioned_training_loop
  * (trainer.cpp:410-466): condition_forward -> render_field -> spectrum
- * aggregate -> composite_loss (L1; lambda_ssim = lambda_fft = 0) ->
+ * aggregate -> composite_loss (L1 + SSIM + DFT2 terms) ->
  * aggregate_modality_backward -> backward_render (coefficient part) ->
  * condition_backward, for a batch of receivers sharing one transmitter.
  * hyper = {feature_lr, rest_lr_ratio, conditioning_lr, lambda_ssim,
- * lambda_fft, adam beta1, beta2, epsilon} (trainer.hpp:68-97 defaults
- * 5e-3, 0.2, 1e-3, 0, 0, 0.9, 0.999, 1e-8); NULL = defaults. */
+ * lambda_fft, adam beta1, beta2, epsilon}; NULL = the reference defaults
+ * 5e-3, 0.2, 1e-3 (TrainConfig, trainer.hpp:68-97), 0.2, 0.1 (LossWeights,
+ * trainer.hpp:25-29), 0.9, 0.999, 1e-8. */
 int rxgs_trainer_create(rxgs_ctx ctx, rxgs_scene scene, rxgs_cond c, const double hyper[8], rxgs_trainer* out);
 int rxgs_trainer_destroy(rxgs_trainer t);
 /* Sum over the n_rx samples of the per-sample gradients (the reference's
@@ -310,11 +311,16 @@ int rxgs_train_grads(rxgs_trainer t, rxgs_txstate st, const double* rx, int n_rx
  * data-parallel all-reduce (sum) before rxgs_train_apply. */
 int rxgs_train_grad_buffer(rxgs_trainer t, double** dev_ptr, int64_t* n, int64_t* n_base);
 int rxgs_train_get_grads(rxgs_trainer t, double* d_base, double* d_params);
+/* Copy of the whole flat buffer (n values of rxgs_train_grad_buffer) into a
+ * host or device array, after the trainer's stream has drained. */
+int rxgs_train_get_grad_buffer(rxgs_trainer t, double* out);
 /* In-place NCCL all-reduce (sum, ncclFloat64) of the flat gradient buffer
  * on the trainer's stream, over the caller's communicator (an ncclComm_t
  * passed as void*, one rank per GPU): the data-parallel exchange between
- * rxgs_train_grads and rxgs_train_apply. NCCL is resolved
- * at run time from the library the process already loaded. */
+ * rxgs_train_grads and rxgs_train_apply, over the whole
+ * buffer (n of rxgs_train_grad_buffer, geometry gradients included in joint
+ * and Stage-I trainers). NCCL is resolved at run time from the library the
+ * process already loaded (RXGS_NCCL_LIBRARY overrides the soname). */
 int rxgs_train_allreduce(rxgs_trainer t, void* nccl_comm);
 /* Optimizer::step on "features" (degree >= 1 scaled by rest_lr_ratio) and
  * every conditioning group (diffengine.cpp:50-58): throws the reference's

@@ -410,7 +410,8 @@ def cond_cfg(F=6, hidden=64, dc=16, S=16, R=32, nearest=0, mode="full", l_max=2,
                      l_max, C_], np.int32)
 
 
-def _train_sample(self, scene_h, cond_h, grid: Grid, tx, rx, target, lambda_ssim=0.0, lambda_fft=0.0, geometry=False):
+def _train_sample(self, scene_h, cond_h, grid: Grid, tx, rx, target, lambda_ssim=0.0, lambda_fft=0.0, geometry=False,
+                  threads=1):
     """Reference one-sample Stage-II gradient (ref_train_sample, reference build only)."""
     sc = scene_h.data
     k = len(sc["tau_logits"])
@@ -423,7 +424,7 @@ def _train_sample(self, scene_h, cond_h, grid: Grid, tx, rx, target, lambda_ssim
     err = C.create_string_buffer(512)
     rc = self._train_sample(scene_h.ptr, None if cond_h is None else cond_h.ptr, grid.gi, grid.gd, _d(np.asarray(tx, np.float64)),
                             _d(np.asarray(rx, np.float64)), _d(np.asarray(target, np.float64)), lambda_ssim,
-                            lambda_fft, 1, loss.ctypes.data_as(_dp), d_base.ctypes.data_as(_dp),
+                            lambda_fft, threads, loss.ctypes.data_as(_dp), d_base.ctypes.data_as(_dp),
                             d_par.ctypes.data_as(_dp), *[None if g is None else g.ctypes.data_as(_dp) for g in geo],
                             err, 512)
     if rc:

@@ -113,6 +113,7 @@ _SIG = {
     "rxgs_train_grads": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp, _vp, C.c_int]),
     "rxgs_train_grad_buffer": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_i64), C.POINTER(_i64)]),
     "rxgs_train_get_grads": (C.c_int, [_vp, _vp, _vp]),
+    "rxgs_train_get_grad_buffer": (C.c_int, [_vp, _vp]),
     "rxgs_train_allreduce": (C.c_int, [_vp, _vp]),
     "rxgs_trainer_enable_geometry": (C.c_int, [_vp, _vp]),
     "rxgs_train_densify": (C.c_int, [_vp, C.c_double, _vp, C.c_uint64, C.c_uint64, _vp]),
@@ -616,7 +617,9 @@ class _CudaArray:
 class Trainer:
     """Training step of the conditioned Stage-II chain (trainer.cpp:410-466)."""
 
-    DEFAULTS = (5e-3, 0.2, 1e-3, 0.0, 0.0, 0.9, 0.999, 1e-8)
+    DEFAULTS = (5e-3, 0.2, 1e-3, 0.2, 0.1, 0.9, 0.999, 1e-8)
+    # spectrum L1 only (lambda_ssim = lambda_fft = 0): the config-4 headline loss
+    L1_ONLY = (5e-3, 0.2, 1e-3, 0.0, 0.0, 0.9, 0.999, 1e-8)
 
     # TrainConfig geometry defaults (trainer.hpp:78-92): position lr schedule
     # (lr_init, lr_final, total_steps, delay_mult, delay_steps), transmittance,
@@ -682,6 +685,12 @@ class Trainer:
         dp = np.empty(self.cond.param_count if self.cond is not None else 0)
         _check(_lib.rxgs_train_get_grads(self.h, db.ctypes.data, dp.ctypes.data))
         return db, dp
+
+    def grad_buffer_host(self):
+        """The whole flat gradient buffer [d_base | d_cond | d_geometry] (host copy)."""
+        out = np.empty(self.n)
+        _check(_lib.rxgs_train_get_grad_buffer(self.h, out.ctypes.data))
+        return out
 
     def get_geometry_grads(self):
         """(d_positions K*3, d_log_scales K*3, d_quaternions K*4, d_tau_logits K)."""

@@ -613,6 +613,8 @@ int rxgs_tx_state_build(rxgs_ctx ctx, rxgs_scene sc, const double tx[3], const r
     st->needed_host = -1;
     st->regrouped = false;  // recycled buffers: per-state derived data must be rebuilt
     st->version = next_version();
+    st->coeff_version = sc->coeff_version;
+    st->geo_version = sc->geo_version;
     st->ctx = ctx;
     st->k = sc->k;
     st->l_max = sc->l_max;
@@ -1242,6 +1244,9 @@ int rxgs_render_queries(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, rxgs_txstate s
     if (!rx) return fail(RXGS_ERR_INVALID, "render_queries: null receivers");
     if (sc->k != st->k || sc->L != st->L || sc->channels != st->channels)
         return fail(RXGS_ERR_INVALID, "render_queries: scene / tx-state mismatch");
+    if (st->geo_version != sc->geo_version)
+        return fail(RXGS_ERR_INVALID,
+                    "render_queries: the scene geometry changed since this tx state was built; rebuild it");
     if (c && (sc->l_max != c->l_max || sc->channels != c->C))
         return fail(RXGS_ERR_INVALID, "condition_forward: scene/state shape mismatch");
     if (sc->channels != 1)
@@ -1251,6 +1256,10 @@ int rxgs_render_queries(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, rxgs_txstate s
     const double* d_rx = nullptr;
     RX_TRY(dev_in(ctx, rx, 3 * static_cast<size_t>(n_rx), ctx->scratch_c, &d_rx));
     if (c && c->use_local()) RX_TRY(check_receivers(ctx, sc, rx, n_rx));
+    if (st->coeff_version != sc->coeff_version) {  // optimizer stepped since build: basis*base is stale
+        RXGS_CUDA(launch_refresh_gb(*sc, *st, s));
+        st->coeff_version = sc->coeff_version;
+    }
     const DevGrid& g = st->grid;
     const size_t plane = static_cast<size_t>(g.nt) * g.np;
     const int n_tb = g.n_tiles * g.cell_blocks;

@@ -251,6 +251,8 @@ int densify_scene(rxgs_ctx ctx, rxgs_scene_s* sc, const double* d_accum, const i
     sc->d_tau = std::move(nt);
     sc->d_coeffs64 = std::move(nc);
     sc->k = K2;
+    sc->coeff_version += 1;
+    sc->geo_version += 1;
     report[0] = A - S;
     report[1] = S;
     report[2] = M - K2;
@@ -306,6 +308,7 @@ int rxgs_reset_transmittance(rxgs_scene scene) {
     const double v = std::log(0.01 / (1.0 - 0.01));  // logit(0.01) (scene.cpp:276-279, linalg logit)
     RXGS_CUDA(launch_fill64(scene->k, v, scene->d_tau.as<double>(), scene->ctx->stream));
     scene->geo_stale = true;
+    scene->geo_version += 1;  // tau enters the states' blend weights
     return RXGS_OK;
 }
 

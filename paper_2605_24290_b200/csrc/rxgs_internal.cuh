@@ -176,6 +176,10 @@ struct rxgs_scene_s {
     rxgs_b200::DevBuf d_morton, d_mpos32;
     bool host_stale = false;  // device coefficients updated by the optimizer
     bool geo_stale = false;   // device geometry updated by the joint optimizer
+    // bumped whenever the device FLE coefficients / geometry change (optimizer
+    // steps, densify): transmitter states remember the values they were built
+    // or refreshed at, so a reused state never renders stale basis*base rows
+    uint64_t coeff_version = 1, geo_version = 1;
     // exact position -> lowest Gaussian index (receiver-on-Gaussian check,
     // conditioning.cpp:380-382), built lazily on the host
     std::unordered_map<std::string, int> pos_index;
@@ -199,6 +203,9 @@ struct rxgs_txstate_s {
     int64_t needed_host = -1;
     // changes whenever the state's per-Gaussian data does (build, refresh_gb)
     uint64_t version = 0;
+    // the scene's coeff_version / geo_version this state's basis*base rows
+    // and geometry were computed from
+    uint64_t coeff_version = 0, geo_version = 0;
     // walked list entries regrouped by Gaussian (training adjoint), built lazily
     rxgs_b200::DevBuf gauss_off, gauss_ent;
     bool regrouped = false;

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -21,7 +22,7 @@ struct rxgs_trainer_s {
     rxgs_ctx ctx = nullptr;
     rxgs_scene sc = nullptr;
     rxgs_cond c = nullptr;
-    double feature_lr = 5e-3, rest_ratio = 0.2, cond_lr = 1e-3, lambda_ssim = 0.0, lambda_fft = 0.0;
+    double feature_lr = 5e-3, rest_ratio = 0.2, cond_lr = 1e-3, lambda_ssim = 0.2, lambda_fft = 0.1;  // LossWeights (trainer.hpp:25-29)
     double b1 = 0.9, b2 = 0.999, eps = 1e-8;
     int64_t step = 0;
     int64_t n_base = 0, n_par = 0;
@@ -222,6 +223,7 @@ int rxgs_train_grads(rxgs_trainer t, rxgs_txstate st, const double* rx, int n_rx
     if (!st->regrouped) TRY(train_regroup(ctx, *st, s));
     // ---- forward (coefficients may have changed since the state was built)
     RXGS_CUDA(launch_refresh_gb(*sc, *st, s));
+    st->coeff_version = sc->coeff_version;
     const size_t ag_n = static_cast<size_t>(n_rx) * sc->L * 4;
     RXGS_CUDA(ctx->ag.ensure(ag_n * sizeof(float)));
     if (c)
@@ -319,6 +321,14 @@ int rxgs_train_grad_buffer(rxgs_trainer t, double** dev_ptr, int64_t* n, int64_t
     return RXGS_OK;
 }
 
+int rxgs_train_get_grad_buffer(rxgs_trainer t, double* out) {
+    if (!t || !out) return fail(RXGS_ERR_INVALID, "null argument");
+    RXGS_CUDA(cudaSetDevice(t->ctx->device));
+    RXGS_CUDA(cudaStreamSynchronize(t->ctx->stream));
+    RXGS_CUDA(cudaMemcpy(out, t->grad.p, sizeof(double) * t->n_total(), cudaMemcpyDefault));
+    return RXGS_OK;
+}
+
 int rxgs_train_get_grads(rxgs_trainer t, double* d_base, double* d_params) {
     if (!t) return fail(RXGS_ERR_INVALID, "null trainer");
     RXGS_CUDA(cudaSetDevice(t->ctx->device));
@@ -347,7 +357,8 @@ struct NcclSyms {
 const NcclSyms& nccl_syms() {
     static NcclSyms s = [] {
         NcclSyms r;
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        const char* lib = std::getenv("RXGS_NCCL_LIBRARY");
+        void* h = dlopen(lib && *lib ? lib : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
         void* a = dlsym(h ? h : RTLD_DEFAULT, "ncclAllReduce");
         if (!a) a = dlsym(RTLD_DEFAULT, "ncclAllReduce");
         r.allreduce = reinterpret_cast<nccl_allreduce_fn>(a);
@@ -363,7 +374,8 @@ int rxgs_train_allreduce(rxgs_trainer t, void* nccl_comm) {
     const NcclSyms& n = nccl_syms();
     if (!n.allreduce) return fail(RXGS_ERR_RUNTIME, "train_allreduce: NCCL (libnccl.so.2) not found");
     RXGS_CUDA(cudaSetDevice(t->ctx->device));
-    const size_t count = static_cast<size_t>(t->n_base + t->n_par);
+    // the whole flat buffer: [d_base | d_cond | d_geometry] (rxgs_train_grad_buffer)
+    const size_t count = static_cast<size_t>(t->n_total());
     const int r = n.allreduce(t->grad.p, t->grad.p, count, kNcclFloat64, kNcclSum, nccl_comm, t->ctx->stream);
     if (r != 0)
         return fail(RXGS_ERR_CUDA, std::string("train_allreduce: ncclAllReduce failed: ") +
@@ -513,6 +525,7 @@ int rxgs_train_apply(rxgs_trainer t) {
                                   s));
         RXGS_CUDA(launch_geo_post(*sc, s));  // renormalize_quaternions + f32 position mirrors
         sc->geo_stale = true;
+        sc->geo_version += 1;
         ctx->launches += 5;
     }
     RXGS_CUDA(launch_adam(t->n_base, sc->d_coeffs64.as<double>(), g, m, v, t->feature_lr, t->step, t->b1, t->b2,
@@ -522,6 +535,7 @@ int rxgs_train_apply(rxgs_trainer t) {
                               t->b2, t->eps, 0, 1, 1.0, c->d_params32.as<float>(), s));
     ctx->launches += 3;
     sc->host_stale = true;
+    sc->coeff_version += 1;
     if (c) c->host_stale = true;
     return RXGS_OK;
 }

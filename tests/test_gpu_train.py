@@ -42,7 +42,7 @@ def test_train_grads_match_reference_sum(ctx, capi, ref, mode):
     rx = capi.synth_points(3, 11, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
     tg = _targets(3, grid.cells)
     st = scene.tx_state(TX, grid)
-    tr = capi.Trainer(ctx, scene, cond)
+    tr = capi.Trainer(ctx, scene, cond, capi.Trainer.L1_ONLY)
     loss = tr.grads(st, rx, tg)
     db, dp = tr.get_grads()
     want_b = np.zeros_like(db)
@@ -97,7 +97,7 @@ def test_train_deterministic_and_accumulate(ctx, capi, ref):
     rx = capi.synth_points(4, 13, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
     tg = _targets(4, grid.cells, 9)
     st = scene.tx_state(TX, grid)
-    tr = capi.Trainer(ctx, scene, cond)
+    tr = capi.Trainer(ctx, scene, cond, capi.Trainer.L1_ONLY)
     tr.grads(st, rx, tg)
     a = np.concatenate(tr.get_grads())
     tr.grads(st, rx, tg)
@@ -163,7 +163,7 @@ def test_train_allreduce_nccl(ctx, capi, ref):
     rx = capi.synth_points(2, 13, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
     tg = _targets(2, grid.cells)
     st = scene.tx_state(TX, grid)
-    tr = capi.Trainer(ctx, scene, cond)
+    tr = capi.Trainer(ctx, scene, cond, capi.Trainer.L1_ONLY)
     tr.grads(st, rx, tg)
     db0, dp0 = tr.get_grads()
     lib, comm = _nccl_one_rank_comm()
@@ -206,7 +206,7 @@ def test_train_joint_grads_match_reference_sum(ctx, capi, ref, mode):
     rx = capi.synth_points(3, 19, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
     tg = _targets(3, grid.cells, 4)
     st = scene.tx_state(TX, grid)
-    tr = capi.Trainer(ctx, scene, cond, geometry=True)
+    tr = capi.Trainer(ctx, scene, cond, capi.Trainer.L1_ONLY, geometry=True)
     assert tr.n == tr.n_base + cond.param_count + 11 * scene.k
     loss = tr.grads(st, rx, tg)
     db, dp = tr.get_grads()
@@ -239,7 +239,7 @@ def test_train_joint_apply(ctx, capi, ref):
     geo = (1.6e-4, 1.6e-6, 2000, 0.01, 200, 1e-2, 5e-3, 1e-3, 500)
     olo, ohi = scene.bounds(0.1)
     occ = cond.build_occupancy(scene, 32, olo, ohi)  # as in _setup; fixed for the run (trainer.cpp:395-397)
-    tr = capi.Trainer(ctx, scene, cond, geometry=geo)
+    tr = capi.Trainer(ctx, scene, cond, capi.Trainer.L1_ONLY, geometry=geo)
     a0 = capi.scene_arrays(scene)
     par0 = capi.cond_params(cond)
     st = scene.tx_state(TX, grid)
@@ -282,7 +282,7 @@ def test_train_nonfinite_group_names(ctx, capi, ref):
     rx = capi.synth_points(1, 29, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
     tg = _targets(1, grid.cells, 8)
     st = scene.tx_state(TX, grid)
-    tr = capi.Trainer(ctx, scene, cond, geometry=True)
+    tr = capi.Trainer(ctx, scene, cond, capi.Trainer.L1_ONLY, geometry=True)
     tr.grads(st, rx, tg)
     g = tr.grad_tensor()
     nb, npar, k = tr.n_base, cond.param_count, scene.k
@@ -324,7 +324,7 @@ def test_stage1_grads_match_reference(ctx, capi, ref):
     sc, scene, grid, og = _stage1_setup(capi, ctx, ref)
     rx = capi.synth_points(2, 31, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
     tg = _targets(2, grid.cells, 12)
-    tr = capi.Trainer(ctx, scene, None, geometry=True)
+    tr = capi.Trainer(ctx, scene, None, capi.Trainer.L1_ONLY, geometry=True)
     assert tr.n == tr.n_base + 11 * scene.k
     loss = tr.grads(scene.tx_state(TX, grid), rx, tg)
     db, dp = tr.get_grads()
@@ -350,7 +350,7 @@ def test_stage1_densify_and_tau_reset(ctx, capi, ref):
     sc, scene, grid, og = _stage1_setup(capi, ctx, ref, big=(3, 77))
     rx = capi.synth_points(1, 37, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
     tg = _targets(1, grid.cells, 13)
-    tr = capi.Trainer(ctx, scene, None, geometry=True)
+    tr = capi.Trainer(ctx, scene, None, capi.Trainer.L1_ONLY, geometry=True)
     d_pos = []
     for _ in range(2):
         tr.grads(scene.tx_state(TX, grid), rx, tg)
@@ -387,7 +387,7 @@ def test_train_geometry_api_errors(ctx, capi, ref):
     """Densification / transmittance reset need the geometry step; geometry must
     be enabled before the first step (reference-style located messages)."""
     sc, scene, grid, og = _stage1_setup(capi, ctx, ref, k=200)
-    tr = capi.Trainer(ctx, scene, None)
+    tr = capi.Trainer(ctx, scene, None, capi.Trainer.L1_ONLY)
     with pytest.raises(capi.InvalidArgument, match="densification needs rxgs_trainer_enable_geometry"):
         tr.densify(10.0)
     with pytest.raises(capi.InvalidArgument, match="transmittance reset needs rxgs_trainer_enable_geometry"):
@@ -409,7 +409,7 @@ def test_train_unconditioned_stage2_matches_reference(ctx, capi, ref):
     sc, scene, grid, og = _stage1_setup(capi, ctx, ref, k=300)
     rx = capi.synth_points(2, 43, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
     tg = _targets(2, grid.cells, 14)
-    tr = capi.Trainer(ctx, scene, None)
+    tr = capi.Trainer(ctx, scene, None, capi.Trainer.L1_ONLY)
     assert tr.n == tr.n_base
     loss = tr.grads(scene.tx_state(TX, grid), rx, tg)
     db, dp = tr.get_grads()
@@ -429,7 +429,7 @@ def test_joint_densify_keeps_conditioning(ctx, capi, ref):
     sc, scene, cond, grid, og, rscene, rcond, params = _setup(capi, ctx, ref, k=400)
     rx = capi.synth_points(1, 47, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
     tg = _targets(1, grid.cells, 15)
-    tr = capi.Trainer(ctx, scene, cond, geometry=True)
+    tr = capi.Trainer(ctx, scene, cond, capi.Trainer.L1_ONLY, geometry=True)
     tr.grads(scene.tx_state(TX, grid), rx, tg)
     tr.apply()
     par = capi.cond_params(cond)
@@ -442,3 +442,55 @@ def test_joint_densify_keeps_conditioning(ctx, capi, ref):
     assert np.isfinite(loss).all()
     tr.apply()
     assert np.isfinite(capi.scene_arrays(scene)["positions"]).all()
+
+
+_FAKE_NCCL_CHILD = r"""
+import ctypes, sys
+import numpy as np
+sys.path[:0] = [sys.argv[1], sys.argv[1] + "/tests"]
+from paper_2605_24290_b200 import capi
+fake = ctypes.CDLL(sys.argv[2])
+fake.fake_nccl_last_count.restype = ctypes.c_size_t
+ctx = capi.Context(0)
+sc = capi.synth_scene(500, 2, 1, 7)
+scene = ctx.scene(sc, "spectrum")
+lo, hi = scene.bounds(0.0)
+cfg = capi.cond_cfg()
+cond = ctx.cond(cfg, capi.synth_cond(cfg, 2, 1, lo, hi, 3, True))
+olo, ohi = scene.bounds(0.1)
+cond.build_occupancy(scene, 32, olo, ohi)
+grid = capi.Grid(18, 36, 8, 1.0)
+rx = capi.synth_points(2, 13, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
+tg = np.random.default_rng(5).uniform(0, 2, (2, grid.cells)).astype(np.float32)
+tr = capi.Trainer(ctx, scene, cond, capi.Trainer.L1_ONLY, geometry=True)
+tr.grads(scene.tx_state([0.3, -0.2, 0.1], grid), rx, tg)
+g0 = tr.grad_buffer_host()
+tr.allreduce(1)
+g1 = tr.grad_buffer_host()
+n = fake.fake_nccl_last_count()
+assert n == g0.size, (n, g0.size)
+geo = g0.size - 11 * 500
+assert np.abs(g0[geo:]).max() > 0
+assert np.array_equal(g1, 2.0 * g0), "not every segment was reduced"
+print("ok", n)
+"""
+
+
+def test_train_allreduce_covers_geometry_segment(tmp_path):
+    """ADVICE r1 (train_api.cu:366): the all-reduce must cover the whole flat
+    buffer, including the joint trainer's 11 K geometry gradients.  A fake
+    ncclAllReduce (tests/cpp/fake_nccl.c: a sum over two identical ranks)
+    stands in for a 2-GPU communicator; every value must double."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    so = str(tmp_path / "libfake_nccl.so")
+    subprocess.check_call(["gcc", "-O2", "-shared", "-fPIC", "-I/usr/local/cuda/include",
+                           os.path.join(root, "tests", "cpp", "fake_nccl.c"), "-o", so,
+                           "-L/usr/local/cuda/lib64/stubs", "-lcuda"])
+    env = dict(os.environ, RXGS_NCCL_LIBRARY=so)
+    out = subprocess.run([sys.executable, "-c", _FAKE_NCCL_CHILD, root, so], env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.strip().startswith("ok")
