@@ -150,6 +150,14 @@ class Checker:
                                            C.c_double, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
                                            C.c_char_p, C.c_int]),
             })
+        if prefix == "ref_" and hasattr(L, "ref_has_checkpoint") and L.ref_has_checkpoint():
+            sig.update({
+                "checkpoint_save": (C.c_int, [C.c_char_p, C.c_void_p, C.c_void_p, _ip, _dp, C.c_char_p, C.c_int]),
+                "checkpoint_load": (C.c_void_p, [C.c_char_p, C.POINTER(C.c_void_p), _ip, _dp, C.c_char_p, C.c_int]),
+                "scene_modality": (C.c_int, [C.c_void_p]),
+                "scene_shape": (None, [C.c_void_p, _ip]),
+                "cond_export": (None, [C.c_void_p, _ip, _dp, _dp, _dp, _dp]),
+            })
         for name, (res, args) in sig.items():
             fn = getattr(L, p + name)
             fn.restype = res
@@ -471,6 +479,53 @@ def _image_metrics(self, pred, gt, h, w, max_val=1.0, window=11, sigma=1.5, dyn=
                            float(sigma), float(dyn), out.ctypes.data_as(_dp), err, 512):
         raise ValueError(err.value.decode())
     return out
+
+
+def _checkpoint_save(self, path, scene_h, cond_h, grid: Grid):
+    """io::save_checkpoint (checkpoint.cpp:93-155) of Model{scene, grid, cond};
+    reference build only (needs checkpoint.cpp)."""
+    err = C.create_string_buffer(512)
+    rc = self._checkpoint_save(str(path).encode(), scene_h.ptr, None if cond_h is None else cond_h.ptr, grid.gi,
+                               grid.gd, err, 512)
+    if rc:
+        raise CheckerError(err.value.decode())
+
+
+def _checkpoint_load(self, path):
+    """io::load_checkpoint (checkpoint.cpp:157-231): a dict with the scene arrays,
+    modality, grid (n_theta, n_phi, tile_size, radius, theta_min, theta_max)
+    and the conditioning (cfg, packed params, occupancy, lo, hi) or None."""
+    cond = C.c_void_p()
+    gi = np.zeros(3, np.int32)
+    gd = np.zeros(3)
+    err = C.create_string_buffer(512)
+    ptr = self._checkpoint_load(str(path).encode(), C.byref(cond), _i(gi), _d(gd), err, 512)
+    if not ptr:
+        raise CheckerError(err.value.decode())
+    shp = np.zeros(3, np.int32)
+    self._scene_shape(ptr, _i(shp))
+    k, l_max, ch = (int(v) for v in shp)
+    h = _Handle(self, ptr, self._scene_free, dict(l_max=l_max, channels=ch))
+    arrays = _scene_arrays(self, h)
+    out = dict(scene=dict(arrays, l_max=l_max, channels=ch), handle=h,
+               modality={0: "rssi", 1: "csi", 2: "spectrum"}[self._scene_modality(ptr)],
+               grid=(int(gi[0]), int(gi[1]), int(gi[2]), float(gd[0]), float(gd[1]), float(gd[2])), cond=None)
+    if cond.value:
+        cfg = np.zeros(9, np.int32)
+        lo, hi = np.zeros(3), np.zeros(3)
+        self._cond_export(cond.value, _i(cfg), None, None, _d(lo), _d(hi))
+        n = self._cond_param_count(cond.value)
+        params = np.empty(n)
+        R = int(cfg[4])
+        occ = np.empty(R ** 3)
+        self._cond_export(cond.value, _i(cfg), _d(params), _d(occ) if R else None, _d(lo), _d(hi))
+        out["cond"] = dict(cfg=cfg, params=params, occupancy=occ, lo=lo, hi=hi)
+        self._cond_free(cond.value)
+    return out
+
+
+Checker.checkpoint_save = _checkpoint_save
+Checker.checkpoint_load = _checkpoint_load
 
 
 def _scene_arrays(self, h):

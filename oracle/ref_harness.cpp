@@ -35,6 +35,9 @@
 #include "rxgs/scene.hpp"
 #include "rxgs/sphraster.hpp"
 #include "rxgs/trainer.hpp"
+#ifdef RXGS_REF_CHECKPOINT
+#include "rxgs/checkpoint.hpp"
+#endif
 
 using namespace rxgs;
 
@@ -789,5 +792,73 @@ void ref_eval_basis(double theta, double phi, int l_max, double* out) {
         out[2 * i + 1] = b.b[i].imag();
     }
 }
+
+// ---------------------------------------------------------------- checkpoint (io::save/load_checkpoint)
+#ifdef RXGS_REF_CHECKPOINT
+int ref_has_checkpoint() { return 1; }
+int ref_checkpoint_save(const char* path, void* scene, void* cond, const int* gi, const double* gd, char* err,
+                        int errlen) {
+    try {
+        train::Model m;
+        m.scene = static_cast<Handle*>(scene)->scene;
+        m.grid = make_grid(gi, gd);
+        if (cond) {
+            m.has_conditioning = true;
+            m.conditioning = *static_cast<cond::ConditioningState*>(cond);
+        }
+        io::save_checkpoint(path, m);
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return 1;
+    }
+}
+// Returns the scene handle (NULL on error); *cond_out = conditioning or NULL;
+// gi = {n_theta, n_phi, tile_size}, gd = {radius, theta_min, theta_max}.
+void* ref_checkpoint_load(const char* path, void** cond_out, int* gi, double* gd, char* err, int errlen) {
+    try {
+        train::Model m = io::load_checkpoint(path);
+        auto* h = new Handle;
+        h->scene = std::move(m.scene);
+        *cond_out = m.has_conditioning ? new cond::ConditioningState(std::move(m.conditioning)) : nullptr;
+        gi[0] = m.grid.n_theta;
+        gi[1] = m.grid.n_phi;
+        gi[2] = m.grid.tile_size;
+        gd[0] = m.grid.radius;
+        gd[1] = m.grid.theta_min;
+        gd[2] = m.grid.theta_max;
+        return h;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return nullptr;
+    }
+}
+int ref_scene_modality(void* scene) { return static_cast<int>(static_cast<Handle*>(scene)->scene.modality); }
+void ref_scene_shape(void* scene, int* out) {
+    const GaussianScene& sc = static_cast<Handle*>(scene)->scene;
+    out[0] = sc.count();
+    out[1] = sc.l_max;
+    out[2] = sc.channels;
+}
+void ref_cond_export(void* cond, int* cfg, double* params, double* occ, double* lo, double* hi) {
+    auto* s = static_cast<cond::ConditioningState*>(cond);
+    const auto& c = s->config;
+    const int v[9] = {c.fourier_bands, c.hidden, c.embed_dim, c.probe_samples, s->occupancy.resolution,
+                      c.nearest_lookup ? 1 : 0, static_cast<int>(c.mode), s->l_max, s->channels};
+    std::memcpy(cfg, v, sizeof v);
+    std::size_t off = 0;
+    for_each_param(*s, [&](std::vector<double>& x) {
+        if (params) std::memcpy(params + off, x.data(), x.size() * sizeof(double));
+        off += x.size();
+    });
+    if (occ && !s->occupancy.densities.empty())
+        std::memcpy(occ, s->occupancy.densities.data(), s->occupancy.densities.size() * sizeof(double));
+    const auto& b = s->occupancy.bounds;
+    lo[0] = b.lo.x; lo[1] = b.lo.y; lo[2] = b.lo.z;
+    hi[0] = b.hi.x; hi[1] = b.hi.y; hi[2] = b.hi.z;
+}
+#else
+int ref_has_checkpoint() { return 0; }
+#endif
 
 }  // extern "C"

@@ -2,10 +2,11 @@
 of the reference's RXGS checkpoint container, io::save_checkpoint /
 io::load_checkpoint (/root/reference/proj/src/checkpoint.cpp:93-231, format
 include/rxgs/checkpoint.hpp:10-15).  The reference serialises its header with
-nlohmann::ordered_json::dump(), i.e. compact JSON in insertion order with
-shortest round-trip doubles -- json.dumps(separators=(',', ':')) writes the
-same text.  The reference's checkpoint.cpp cannot be compiled here (its
-nlohmann json.hpp is not shipped), so this restatement is the format oracle.
+nlohmann::ordered_json::dump(): compact JSON in insertion order, doubles as
+the shortest round-trip digits in nlohmann's layout (dtoa_impl::format_buffer,
+restated in _num).  Pinned against the reference itself: oracle/Makefile
+builds checkpoint.cpp into oracle/_ref against the nlohmann json.hpp shipped
+in this image, and tests/test_checkpoint.py compares bytes both ways.
 """
 import json
 import struct
@@ -49,6 +50,61 @@ def manifest(scene, cond):
     return [(n, s, np.ascontiguousarray(a, np.float64).reshape(-1)) for n, s, a in arrays]
 
 
+def _num(v: float) -> str:
+    """nlohmann::json's dump of a double: shortest round-trip digits d (k of
+    them) with value d * 10^(n-k); "digits[000].0" when k <= n <= 15,
+    "dig.its" when 0 < n <= 15, "0.[000]digits" when -4 < n <= 0, else
+    "d.igitse+XX" (at least two exponent digits); NaN/inf -> null."""
+    import math
+    if not math.isfinite(v):
+        return "null"
+    if v == 0.0:
+        return "-0.0" if math.copysign(1.0, v) < 0 else "0.0"
+    sign = "-" if v < 0 else ""
+    r = repr(abs(v))
+    if "e" in r:
+        m, e = r.split("e")
+        e = int(e)
+    else:
+        m, e = r, 0
+    if "." in m:
+        ip, fp = m.split(".")
+    else:
+        ip, fp = m, ""
+    digits = (ip + fp).lstrip("0")
+    lead = len(ip + fp) - len((ip + fp).lstrip("0"))
+    n = len(ip) + e - lead
+    digits = digits.rstrip("0") or "0"
+    k = len(digits)
+    if k <= n <= 15:
+        out = digits + "0" * (n - k) + ".0"
+    elif 0 < n <= 15:
+        out = digits[:n] + "." + digits[n:]
+    elif -4 < n <= 0:
+        out = "0." + "0" * (-n) + digits
+    else:
+        x = n - 1
+        out = digits[0] + ("." + digits[1:] if k > 1 else "") + f"e{'-' if x < 0 else '+'}{abs(x):02d}"
+    return sign + out
+
+
+def dump_json(o) -> str:
+    """nlohmann::ordered_json::dump() of the header (compact, insertion order)."""
+    if isinstance(o, bool):
+        return "true" if o else "false"
+    if isinstance(o, int):
+        return str(o)
+    if isinstance(o, float):
+        return _num(o)
+    if isinstance(o, str):
+        return json.dumps(o)
+    if isinstance(o, dict):
+        return "{" + ",".join(json.dumps(k) + ":" + dump_json(v) for k, v in o.items()) + "}"
+    if isinstance(o, (list, tuple)):
+        return "[" + ",".join(dump_json(v) for v in o) + "]"
+    raise TypeError(type(o))
+
+
 def write_checkpoint(path, scene, grid, cond=None, modality="spectrum"):
     """save_checkpoint (checkpoint.cpp:93-155).  grid: dict with n_theta,
     n_phi, tile_size, radius, theta_min, theta_max; cond: dict with cfg (9
@@ -71,7 +127,7 @@ def write_checkpoint(path, scene, grid, cond=None, modality="spectrum"):
         man.append({"name": name, "dtype": "f64", "shape": [int(s) for s in shape], "offset": off})
         off += a.size * 8
     header["arrays"] = man
-    text = json.dumps(header, separators=(",", ":")).encode()
+    text = dump_json(header).encode()
     with open(path, "wb") as f:
         f.write(MAGIC + struct.pack("<IQ", VERSION, len(text)) + text)
         for _, _, a in arrays:

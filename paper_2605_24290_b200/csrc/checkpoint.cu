@@ -228,16 +228,51 @@ struct Writer {
         out += c;
         first.pop_back();
     }
-    void num(double v) {  // shortest round-trip digits, as nlohmann's dump
+    // nlohmann::json's dump of a double (dtoa_impl::to_chars / format_buffer):
+    // the shortest round-trip digits d1..dk with the value d * 10^(n-k), written
+    // as "digits[000].0" for k <= n <= 15, "dig.its" for 0 < n <= 15,
+    // "0.[000]digits" for -4 < n <= 0, else "d.igitse+XX"; non-finite -> null
+    void num(double v) {
         sep();
-        char buf[40];
-        for (int prec = 1; prec <= 17; ++prec) {
-            std::snprintf(buf, sizeof buf, "%.*g", prec, v);
+        if (!std::isfinite(v)) {
+            out += "null";
+            return;
+        }
+        if (v == 0.0) {
+            out += std::signbit(v) ? "-0.0" : "0.0";
+            return;
+        }
+        char buf[48];
+        for (int prec = 0; prec <= 17; ++prec) {
+            std::snprintf(buf, sizeof buf, "%.*e", prec, v);
             if (std::strtod(buf, nullptr) == v) break;
         }
         std::string t(buf);
-        if (t.find_first_of(".eEn") == std::string::npos) t += ".0";  // a float stays a float
-        out += t;
+        if (t[0] == '-') {
+            out += '-';
+            t.erase(0, 1);
+        }
+        const size_t epos = t.find('e');
+        const int e10 = std::atoi(t.c_str() + epos + 1);
+        std::string dg;
+        for (size_t i = 0; i < epos; ++i)
+            if (t[i] != '.') dg += t[i];
+        while (dg.size() > 1 && dg.back() == '0') dg.pop_back();
+        const int k = static_cast<int>(dg.size()), n = e10 + 1;
+        if (k <= n && n <= 15) {
+            out += dg + std::string(static_cast<size_t>(n - k), '0') + ".0";
+        } else if (0 < n && n <= 15) {
+            out += dg.substr(0, static_cast<size_t>(n)) + "." + dg.substr(static_cast<size_t>(n));
+        } else if (-4 < n && n <= 0) {
+            out += "0." + std::string(static_cast<size_t>(-n), '0') + dg;
+        } else {
+            out += dg.substr(0, 1);
+            if (k > 1) out += "." + dg.substr(1);
+            const int x = n - 1;
+            char eb[8];
+            std::snprintf(eb, sizeof eb, "e%c%02d", x < 0 ? '-' : '+', x < 0 ? -x : x);
+            out += eb;
+        }
     }
     void integer(long long v) {
         sep();

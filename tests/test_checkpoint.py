@@ -1,9 +1,10 @@
 """Scene / model load: the RXGS checkpoint container (io::save_checkpoint /
-io::load_checkpoint, checkpoint.cpp:93-231).  The format oracle is the Python
-restatement oracle/rxgs_checkpoint.py (the reference's checkpoint.cpp needs an
-unshipped nlohmann json.hpp and cannot be built here); saved files must be
-byte-identical to it, and a loaded model must render exactly like the model
-it was saved from."""
+io::load_checkpoint, checkpoint.cpp:93-231).  The reference's checkpoint.cpp
+is built into oracle/_ref against the nlohmann json.hpp this image ships
+(oracle/Makefile); the Python restatement oracle/rxgs_checkpoint.py is pinned
+to it byte for byte, and rxgs_checkpoint_save must write exactly the
+reference's bytes (and each side loads the other's files).  A loaded model
+must render exactly like the model it was saved from."""
 import json
 import struct
 
@@ -149,3 +150,92 @@ def test_load_errors_match_reference(ctx, capi, tmp_path):
     bad.write_bytes(raw[:16] + text + raw[16 + hlen:])
     with pytest.raises(capi.IoError, match="load_checkpoint: unknown array 'tau_logitz'"):
         ctx.load_checkpoint(bad)
+
+
+# ---------------------------------------------------------------- pinned to the reference's checkpoint.cpp
+def _ref_model(ref, k=40, seed=7, mode="full", radius=1.0, pad=0.1, bounds=None):
+    import oracle as O
+    sc = ref.synth_scene(k, 2, 1, seed)
+    h = ref.scene(sc, "spectrum")
+    lo, hi = ref.scene_bounds(h, 0.0)
+    cfg = O.cond_cfg(mode=mode, R=8)
+    params = ref.synth_cond(cfg, 2, 1, lo, hi, 3, True)
+    olo, ohi = ref.scene_bounds(h, pad) if bounds is None else bounds
+    occ = ref.build_occupancy(h, 8, olo, ohi)
+    c = ref.cond(cfg, params, occ, olo, ohi)
+    cond = {"cfg": cfg, "params": params, "occupancy": occ, "lo": olo, "hi": ohi}
+    return sc, h, c, cond
+
+
+GRIDS = [GRID,
+         dict(n_theta=90, n_phi=360, tile_size=8, radius=10.0, theta_min=0.0, theta_max=3.141592653589793),
+         dict(n_theta=7, n_phi=13, tile_size=4, radius=0.123456789, theta_min=0.25, theta_max=2.0000001),
+         dict(n_theta=4, n_phi=4, tile_size=2, radius=12345.5, theta_min=1e-05, theta_max=0.0001)]
+
+
+@pytest.mark.parametrize("gi", range(len(GRIDS)))
+def test_restatement_bytes_equal_reference_save(ref, tmp_path, gi):
+    """The format oracle writes exactly the bytes of io::save_checkpoint
+    (checkpoint.cpp:93-155, nlohmann ordered_json dump): radius 10, integer
+    and tiny doubles in the grid, occupancy bounds of +-10."""
+    import oracle as O
+    if not hasattr(ref, "_checkpoint_save"):
+        pytest.skip("reference built without checkpoint.cpp (no json.hpp)")
+    g = GRIDS[gi]
+    og = O.Grid(g["n_theta"], g["n_phi"], g["tile_size"], g["radius"], g["theta_min"], g["theta_max"])
+    bounds = ([-10.0, -10.0, -10.0], [10.0, 10.0, 10.0]) if gi == 1 else None
+    sc, h, c, cond = _ref_model(ref, bounds=bounds)
+    for with_cond in (False, True):
+        a, b = tmp_path / f"ref{with_cond}.rxgs", tmp_path / f"ck{with_cond}.rxgs"
+        ref.checkpoint_save(a, h, c if with_cond else None, og)
+        CK.write_checkpoint(b, sc, g, cond if with_cond else None)
+        assert a.read_bytes() == b.read_bytes()
+
+
+def test_reference_load_reads_restatement_and_errors(ref, tmp_path):
+    import oracle as O
+    if not hasattr(ref, "_checkpoint_save"):
+        pytest.skip("reference built without checkpoint.cpp (no json.hpp)")
+    sc, h, c, cond = _ref_model(ref, mode="no_occlusion")
+    p = tmp_path / "m.rxgs"
+    CK.write_checkpoint(p, sc, GRIDS[2], cond)
+    got = ref.checkpoint_load(p)
+    g = GRIDS[2]
+    assert got["grid"] == (g["n_theta"], g["n_phi"], g["tile_size"], g["radius"], g["theta_min"], g["theta_max"])
+    for name in ("positions", "log_scales", "quaternions", "tau_logits", "fle_coeffs"):
+        assert np.array_equal(got["scene"][name].reshape(-1), np.asarray(sc[name]).reshape(-1))
+    assert np.array_equal(got["cond"]["params"], cond["params"])
+    assert np.array_equal(got["cond"]["occupancy"], np.asarray(cond["occupancy"]).reshape(-1))
+    assert np.array_equal(got["cond"]["cfg"], cond["cfg"])
+    bad = tmp_path / "bad.rxgs"
+    bad.write_bytes(b"XXXX" + p.read_bytes()[4:])
+    with pytest.raises(O.CheckerError, match="bad magic"):
+        ref.checkpoint_load(bad)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("gi", range(len(GRIDS)))
+def test_save_is_byte_identical_to_reference_save(ctx, capi, ref, tmp_path, gi):
+    """rxgs_checkpoint_save == io::save_checkpoint byte for byte (ADVICE r1:
+    radius 10, occupancy bounds +-10), and each side loads the other's file."""
+    import oracle as O
+    if not hasattr(ref, "_checkpoint_save"):
+        pytest.skip("reference built without checkpoint.cpp (no json.hpp)")
+    g = GRIDS[gi]
+    og = O.Grid(g["n_theta"], g["n_phi"], g["tile_size"], g["radius"], g["theta_min"], g["theta_max"])
+    bounds = ([-10.0, -10.0, -10.0], [10.0, 10.0, 10.0]) if gi == 1 else None
+    sc, h, c, cond = _ref_model(ref, bounds=bounds)
+    scene = ctx.scene(sc, "spectrum")
+    gcond = ctx.cond(cond["cfg"], cond["params"], cond["occupancy"], cond["lo"], cond["hi"])
+    grid = capi.Grid(**g)
+    ours, want = tmp_path / "ours.rxgs", tmp_path / "want.rxgs"
+    scene.save_checkpoint(ours, grid, gcond)
+    ref.checkpoint_save(want, h, c, og)
+    assert ours.read_bytes() == want.read_bytes()
+    # the reference loads ours; we load the reference's and save the same bytes back
+    back = ref.checkpoint_load(ours)
+    assert np.array_equal(back["cond"]["params"], cond["params"])
+    scene2, grid2, cond2 = ctx.load_checkpoint(want)
+    again = tmp_path / "again.rxgs"
+    scene2.save_checkpoint(again, grid2, cond2)
+    assert again.read_bytes() == want.read_bytes()
