@@ -360,6 +360,57 @@ int64_t rxgs_train_step_count(rxgs_trainer t);
 int rxgs_scene_get_coeffs(rxgs_scene scene, double* out);
 int rxgs_cond_get_params(rxgs_cond c, double* out);
 
+/* ------------------------------------------------------------ single-call reference API
+ * The reference's per-call helpers on the device in FP64 with the
+ * reference's operation order (k_geometry.cu / k_refapi.cu, -fmad=false);
+ * they back the link-level drop-in paper_2605_24290_b200/refapi and the
+ * header shim include/rxgs_b200.hpp.  Host or device buffers. */
+/* raster::project_gaussian (sphraster.hpp:46, sphraster.cpp:22-83) for n
+ * Gaussians: pos n*3, cov n*9 (row-major Mat3), tau n (activated); out geom
+ * n*12 = {theta, phi, depth, A (a, b, c, d), A^-1 (a, b, c, d), tau},
+ * culled n, spans n*4 = {t0, t1, p0, p1}. */
+int rxgs_project_gaussians(rxgs_ctx ctx, int n, const double* pos, const double* cov, const double* tau,
+                           const double tx[3], const rxgs_grid* grid, double* geom, int32_t* culled, int32_t* spans);
+/* fle:: (radiance.hpp:36-70): what = 0 eval_basis (a=theta, b=phi; out n*L
+ * complex), 1 eval_basis_jet (out n*3L complex: b, db/dtheta, db/dphi),
+ * 2 legendre_table (a=x; out n*NP, NP=(l_max+1)(l_max+2)/2), 3
+ * legendre_table_dtheta (a=theta; out n*2NP: P then dP), 4 normalization
+ * (a=l, b=m; out n), 5 eval_radiance (a=theta, b=phi, coeffs n*L complex;
+ * out n complex).  The reference's argument errors. */
+int rxgs_fle_eval(rxgs_ctx ctx, int what, int l_max, int n, const double* a, const double* b, const double* coeffs,
+                  double* out);
+/* raster::blend_ray (sphraster.hpp:82, sphraster.cpp:174-185): weights n,
+ * signals n complex; out = {re, im, transmittance}. */
+int rxgs_blend_ray(rxgs_ctx ctx, int n, const double* weights, const double* signals, double out[3]);
+/* OccupancyGrid::sample_trilinear / sample_nearest (conditioning.cpp:74-112)
+ * at n points; densities R^3 or NULL (empty grid -> 0). */
+int rxgs_occupancy_sample(rxgs_ctx ctx, int R, const double lo[3], const double hi[3], const double* densities, int n,
+                          const double* points, int nearest, double* out);
+/* cond::probe_segment (conditioning.hpp:50, conditioning.cpp:163-178) over an
+ * explicit grid (FP64): out n*2 = {transmittance, mean_density}. */
+int rxgs_probe_grid(rxgs_ctx ctx, int R, const double lo[3], const double hi[3], const double* densities, int n,
+                    const double* from, const double* to, int samples, int nearest, double* out);
+/* cond::fourier_encode (conditioning.cpp:255-265): freqs F*3, r n*3, out n*6F. */
+int rxgs_fourier_encode(rxgs_ctx ctx, int F, const double* freqs, int n, const double* r, double* out);
+/* cond::MlpLayer::forward (conditioning.cpp:12-19) on n input vectors. */
+int rxgs_mlp_layer_forward(rxgs_ctx ctx, int in, int out_dim, const double* w, const double* b, int n,
+                           const double* x, double* y);
+/* raster::SphericalGrid::validate (sphraster.cpp:14-20): the reference's errors. */
+int rxgs_grid_validate(const rxgs_grid* grid);
+/* cond::condition_forward with an explicit base (conditioning.hpp:114-117):
+ * base K*L*C*2 instead of the scene's coefficients; n_rx receivers, out
+ * n_rx*K*L*C*2; local_in K*6 of the first receiver or NULL. */
+int rxgs_condition_forward_base(rxgs_ctx ctx, rxgs_cond c, rxgs_scene scene, const double* base, const double* rx,
+                                int n_rx, double* out, double* local_in);
+/* A device transmitter state from a host raster::TxState (sphraster.hpp:52-61):
+ * the rows of rxgs_tx_state_get (culled, geom, spans, basis) and the per-tile
+ * lists as CSR (offsets n_tiles+1, indices); the blend walk and the needed-row
+ * compaction run on the device.  render_field / backward_render /
+ * render_queries accept it like a built state (no sort keys). */
+int rxgs_tx_state_import(rxgs_ctx ctx, rxgs_scene scene, const rxgs_grid* grid, const int32_t* culled,
+                         const double* geom, const int32_t* spans, const double* basis, const int64_t* offsets,
+                         const int32_t* indices, rxgs_txstate* out);
+
 #ifdef __cplusplus
 }
 #endif

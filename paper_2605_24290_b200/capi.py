@@ -108,6 +108,16 @@ _SIG = {
     "rxgs_render_queries": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp]),
     "rxgs_coverage_table": (C.c_int, [_vp, _vp, _vp, C.POINTER(Grid), _vp, C.c_int, _vp, C.c_int, _vp]),
     "rxgs_predict": (C.c_int, [_vp, _vp, _vp, C.POINTER(Grid), _vp, _vp, _vp]),
+    "rxgs_project_gaussians": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp, C.POINTER(Grid), _vp, _vp, _vp]),
+    "rxgs_fle_eval": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp]),
+    "rxgs_blend_ray": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp]),
+    "rxgs_occupancy_sample": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, C.c_int, _vp, C.c_int, _vp]),
+    "rxgs_probe_grid": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, C.c_int, _vp, _vp, C.c_int, C.c_int, _vp]),
+    "rxgs_fourier_encode": (C.c_int, [_vp, C.c_int, _vp, C.c_int, _vp, _vp]),
+    "rxgs_mlp_layer_forward": (C.c_int, [_vp, C.c_int, C.c_int, _vp, _vp, C.c_int, _vp, _vp]),
+    "rxgs_grid_validate": (C.c_int, [C.POINTER(Grid)]),
+    "rxgs_condition_forward_base": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp]),
+    "rxgs_tx_state_import": (C.c_int, [_vp, _vp, C.POINTER(Grid), _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "rxgs_trainer_create": (C.c_int, [_vp, _vp, _vp, _vp, C.POINTER(_vp)]),
     "rxgs_trainer_destroy": (C.c_int, [_vp]),
     "rxgs_train_grads": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp, _vp, C.c_int]),

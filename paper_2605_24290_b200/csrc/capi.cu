@@ -11,6 +11,7 @@
 #include <exception>
 #include <new>
 #include <string>
+#include <memory>
 #include <vector>
 
 #include "rxgs_internal.cuh"
@@ -380,6 +381,26 @@ static void ctx_free(rxgs_ctx ctx) {
 void ctx_release(rxgs_ctx ctx) {
     if (--ctx->refs == 0 && ctx->closed) ctx_free(ctx);
 }
+void scene_release(rxgs_scene_s* sc) {
+    if (--sc->refs > 0) return;
+    rxgs_ctx ctx = sc->ctx;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    delete sc;
+    ctx_release(ctx);
+}
+int ensure_tx_full(rxgs_txstate_s& st, cudaStream_t s) {
+    if (st.full) return RXGS_OK;
+    rxgs_scene_s* sc = st.sc;
+    if (!sc) return fail(RXGS_ERR_INVALID, "tx state: no scene to complete the FP64 geometry from");
+    if (sc->geo_version != st.geo_version || sc->k != st.k)
+        return fail(RXGS_ERR_INVALID, "tx state: the scene geometry changed since the state was built; rebuild it");
+    RXGS_CUDA(launch_tx_prep(*sc, st, s, true));  // same arithmetic: rec / spans / lists unchanged
+    st.ctx->launches += 1;
+    st.full = true;
+    st.coeff_version = sc->coeff_version;  // basis*base recomputed from the current coefficients
+    return RXGS_OK;
+}
 }  // namespace rxgs_b200
 
 namespace rxgs_b200 {
@@ -563,11 +584,7 @@ int rxgs_scene_create(rxgs_ctx ctx, int k, int l_max, int channels, int modality
 
 int rxgs_scene_destroy(rxgs_scene sc) {
     if (!sc) return RXGS_OK;
-    rxgs_ctx ctx = sc->ctx;
-    cudaSetDevice(ctx->device);
-    cudaStreamSynchronize(ctx->stream);
-    delete sc;
-    ctx_release(ctx);
+    scene_release(sc);
     return RXGS_OK;
 }
 
@@ -615,6 +632,7 @@ int rxgs_tx_state_build(rxgs_ctx ctx, rxgs_scene sc, const double tx[3], const r
     st->version = next_version();
     st->coeff_version = sc->coeff_version;
     st->geo_version = sc->geo_version;
+    st->full = false;
     st->ctx = ctx;
     st->k = sc->k;
     st->l_max = sc->l_max;
@@ -648,7 +666,7 @@ int rxgs_tx_state_build(rxgs_ctx ctx, rxgs_scene sc, const double tx[3], const r
     cudaEvent_t ev;
     timing_begin(ctx, "tx_prep", &ev);
     {
-        const cudaError_t e = launch_tx_prep(*sc, *st, s);
+        const cudaError_t e = launch_tx_prep(*sc, *st, s, false);
         if (e != cudaSuccess) return fail_st(cuda_fail(e, "tx_prep"));
     }
     timing_end(ctx, "tx_prep", ev, sc->k);
@@ -676,6 +694,8 @@ int rxgs_tx_state_build(rxgs_ctx ctx, rxgs_scene sc, const double tx[3], const r
     }
     ctx->launches += 1;
     ctx_retain(ctx);
+    st->sc = sc;
+    sc->refs += 1;
     *out = st;
     return RXGS_OK;
     API_END
@@ -685,6 +705,10 @@ int rxgs_tx_state_destroy(rxgs_txstate st) {
     if (!st) return RXGS_OK;
     rxgs_ctx ctx = st->ctx;
     cudaSetDevice(ctx->device);
+    if (st->sc) {
+        scene_release(st->sc);
+        st->sc = nullptr;
+    }
     if (ctx->spare_tx.size() < 2) {
         // Keep the buffers for the next build; stream order makes reuse safe
         // (later kernels on this stream run after every reader of st).
@@ -705,6 +729,7 @@ int rxgs_tx_state_get(rxgs_txstate st, int32_t* culled, double* geom, int32_t* s
     if (!st) return fail(RXGS_ERR_INVALID, "null tx state");
     rxgs_ctx ctx = st->ctx;
     RX_TRY(set_device(ctx));
+    if ((geom || basis) && st->k) RX_TRY(ensure_tx_full(*st, ctx->stream));
     RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
     const size_t K = st->k;
     if (culled && K) RXGS_CUDA(cudaMemcpy(culled, st->culled.p, K * sizeof(int), cudaMemcpyDefault));
@@ -800,7 +825,7 @@ int rxgs_bin_and_sort(rxgs_ctx ctx, int k, const int32_t* culled, const double* 
         uint64_t b;
         std::memcpy(&b, &dep[i], 8);
         dkey[i] = b;
-        cnt[i] = (sp[4 * i + 1] - sp[4 * i] + 1) * (sp[4 * i + 3] - sp[4 * i + 2] + 1);
+        cnt[i] = std::max(0, sp[4 * i + 1] - sp[4 * i] + 1) * std::max(0, sp[4 * i + 3] - sp[4 * i + 2] + 1);
     }
     RXGS_CUDA(st.depth_key.ensure(K * 8));
     RXGS_CUDA(st.tile_count.ensure(K * 4));
@@ -837,6 +862,7 @@ int rxgs_render_field(rxgs_ctx ctx, rxgs_txstate st, rxgs_scene sc, const double
     RXGS_CUDA(ctx->signals.ensure(std::max<size_t>(static_cast<size_t>(sc->k) * n_rx * sc->channels, 1) * sizeof(float2)));
     RX_TRY(reset_err_flag(ctx));
     if (nco) {
+        RX_TRY(ensure_tx_full(*st, s));
         RXGS_CUDA(launch_reduce_signals(*st, d_co, n_rx, ctx->signals.as<float2>(), ctx->err_flag.as<int>(), s));
         ctx->launches += 2;
     }
@@ -958,6 +984,7 @@ int rxgs_backward_render(rxgs_ctx ctx, rxgs_txstate st, rxgs_scene sc, const dou
     RXGS_CUDA(ctx->signals.ensure(std::max<size_t>(static_cast<size_t>(K) * n_jc, 1) * sizeof(float2)));
     RX_TRY(reset_err_flag(ctx));
     if (nco) {
+        RX_TRY(ensure_tx_full(*st, s));
         RXGS_CUDA(launch_reduce_signals(*st, d_co, n_rx, ctx->signals.as<float2>(), ctx->err_flag.as<int>(), s));
         ctx->launches += 2;
     }
@@ -989,6 +1016,7 @@ int rxgs_backward_render(rxgs_ctx ctx, rxgs_txstate st, rxgs_scene sc, const dou
     if (!dc) { RXGS_CUDA(o_co.ensure(std::max<size_t>(nco, 1) * sizeof(double))); dc = o_co.as<double>(); }
     cudaEvent_t ev;
     timing_begin(ctx, "backward_render", &ev);
+    RX_TRY(ensure_tx_full(*st, s));
     RXGS_CUDA(launch_backward_render(*st, *sc, d_co, n_rx, d_dv, b_sig.as<double2>(), b_eg.as<double>(),
                                      b_eds.as<double2>(), b_rg.as<double>(), b_rds.as<double2>(), dp, dl, dq, dt, dc,
                                      s));
@@ -1044,6 +1072,9 @@ int rxgs_cond_create(rxgs_ctx ctx, const int32_t cfg[9], const double* params, c
         if (e != cudaSuccess) return bad(e, "occ");
         e = cudaMemcpy(c->d_occ32.p, f.data(), n * sizeof(float), cudaMemcpyHostToDevice);
         if (e != cudaSuccess) return bad(e, "occ copy");
+        e = c->d_occ64.ensure(n * sizeof(double));
+        if (e == cudaSuccess) e = cudaMemcpy(c->d_occ64.p, h.data(), n * sizeof(double), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return bad(e, "occ64");
         std::vector<double> lo = to_host(occ_lo, 3), hi = to_host(occ_hi, 3);
         for (int a = 0; a < 3; ++a) {
             c->lo[a] = lo[a];
@@ -1113,6 +1144,8 @@ int rxgs_build_occupancy(rxgs_ctx ctx, rxgs_scene sc, int R, const double lo_[3]
         }
         attach->has_occ = true;
         RXGS_CUDA(launch_occ_cubes(*attach, ctx->stream));
+        RXGS_CUDA(attach->d_occ64.ensure(n * sizeof(double)));
+        RXGS_CUDA(cudaMemcpyAsync(attach->d_occ64.p, d64, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
         attach->h_occ.resize(n);
         RXGS_CUDA(cudaMemcpyAsync(attach->h_occ.data(), d64, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     }
@@ -1141,61 +1174,63 @@ int rxgs_probe_segments(rxgs_ctx ctx, rxgs_cond c, int n, const double* from, co
     API_END
 }
 
-int rxgs_condition_batch(rxgs_ctx ctx, rxgs_cond c, rxgs_scene sc, const double* rx, int n_rx,
-                         double* out) {
-    API_BEGIN
+// The materialised conditioning API runs the FP64 kernels (k_refapi.cu) in
+// the reference's operation order; the fused query path keeps its own
+// FP32 / tcgen05 pipeline.  base: the coefficients to condition (NULL = the
+// scene's own).
+namespace {
+int condition_fp64(rxgs_ctx ctx, rxgs_cond c, rxgs_scene sc, const double* rx, int n_rx, const double* base,
+                   double* out, double* local_in) {
     if (!ctx || !c || !sc || !rx) return fail(RXGS_ERR_INVALID, "condition_forward: null argument");
     if (sc->l_max != c->l_max || sc->channels != c->C)
         return fail(RXGS_ERR_INVALID, "condition_forward: scene/state shape mismatch");
     RX_TRY(set_device(ctx));
     cudaStream_t s = ctx->stream;
+    DevBuf t_rx, t_base, t_ag;
     const double* d_rx = nullptr;
-    RX_TRY(dev_in(ctx, rx, 3 * static_cast<size_t>(n_rx), ctx->scratch_c, &d_rx));
+    RX_TRY(dev_in(ctx, rx, 3 * static_cast<size_t>(n_rx), t_rx, &d_rx));
     if (c->use_local()) RX_TRY(check_receivers(ctx, sc, rx, n_rx));
     const size_t stride = static_cast<size_t>(sc->L) * sc->channels * 2;
-    const size_t no = static_cast<size_t>(n_rx) * sc->k * stride;
-    const size_t ag_n = static_cast<size_t>(n_rx) * sc->L * 4 * sc->channels;
-    RXGS_CUDA(ctx->ag.ensure(std::max<size_t>(ag_n, 1) * sizeof(float)));
-    RXGS_CUDA(launch_cond_global(*c, d_rx, n_rx, ctx->ag.as<float>(), s));
+    const size_t nb = static_cast<size_t>(sc->k) * stride;
+    const double* d_base = sc->d_coeffs64.as<double>();
+    if (base) RX_TRY(dev_in(ctx, base, nb, t_base, &d_base));
+    const size_t no = static_cast<size_t>(n_rx) * nb;
+    RXGS_CUDA(t_ag.ensure(std::max<size_t>(static_cast<size_t>(n_rx) * sc->L * 4 * sc->channels, 1) * sizeof(double)));
     double* d_out = nullptr;
     RX_TRY(dev_out(out, no, ctx->host_out, &d_out));
-    RXGS_CUDA(launch_cond_materialize(*c, *sc, d_rx, n_rx, ctx->ag.as<float>(), d_out, nullptr, nullptr, s));
+    double* d_li = nullptr;
+    DevBuf t_li;
+    if (local_in) RX_TRY(dev_out(local_in, static_cast<size_t>(sc->k) * 6, t_li, &d_li));
+    RXGS_CUDA(launch_cond_forward64(*c, *sc, d_rx, n_rx, d_base, t_ag.as<double>(), d_out, d_li, s));
     ctx->launches += 2;
     if (c->use_global()) c->global_calls += static_cast<int64_t>(n_rx) * sc->L;
     if (c->use_local()) c->local_calls += static_cast<int64_t>(n_rx) * sc->k;
     RX_TRY(finish_out(ctx, out, d_out, no));
+    if (local_in) RX_TRY(finish_out(ctx, local_in, d_li, static_cast<size_t>(sc->k) * 6));
     RXGS_CUDA(cudaStreamSynchronize(s));
     return RXGS_OK;
+}
+}  // namespace
+
+int rxgs_condition_batch(rxgs_ctx ctx, rxgs_cond c, rxgs_scene sc, const double* rx, int n_rx,
+                         double* out) {
+    API_BEGIN
+    return condition_fp64(ctx, c, sc, rx, n_rx, nullptr, out, nullptr);
     API_END
 }
 
 int rxgs_condition_forward(rxgs_ctx ctx, rxgs_cond c, rxgs_scene sc, const double rx[3], double* out,
                            double* local_in) {
     API_BEGIN
-    if (!local_in) return rxgs_condition_batch(ctx, c, sc, rx, 1, out);
-    if (!ctx || !c || !sc || !rx) return fail(RXGS_ERR_INVALID, "condition_forward: null argument");
-    if (sc->l_max != c->l_max || sc->channels != c->C)
-        return fail(RXGS_ERR_INVALID, "condition_forward: scene/state shape mismatch");
-    // Workspace variant: same pipeline, plus the local features.
-    RX_TRY(rxgs_condition_batch(ctx, c, sc, rx, 1, out));
-    c->global_calls -= c->use_global() ? sc->L : 0;  // counted once below
-    c->local_calls -= c->use_local() ? sc->k : 0;
-    cudaStream_t s = ctx->stream;
-    const double* d_rx = nullptr;
-    RX_TRY(dev_in(ctx, rx, 3, ctx->scratch_c, &d_rx));
-    const size_t stride = static_cast<size_t>(sc->L) * sc->channels * 2;
-    RXGS_CUDA(ctx->scratch_d.ensure(std::max<size_t>(static_cast<size_t>(sc->k) * stride, 1) * sizeof(double)));
-    double* d_li = nullptr;
-    RX_TRY(dev_out(local_in, static_cast<size_t>(sc->k) * 6, ctx->host_out, &d_li));
-    RXGS_CUDA(launch_cond_global(*c, d_rx, 1, ctx->ag.as<float>(), s));
-    RXGS_CUDA(launch_cond_materialize(*c, *sc, d_rx, 1, ctx->ag.as<float>(), ctx->scratch_d.as<double>(), d_li,
-                                      nullptr, s));
-    ctx->launches += 2;
-    if (c->use_global()) c->global_calls += sc->L;
-    if (c->use_local()) c->local_calls += sc->k;
-    RX_TRY(finish_out(ctx, local_in, d_li, static_cast<size_t>(sc->k) * 6));
-    RXGS_CUDA(cudaStreamSynchronize(s));
-    return RXGS_OK;
+    return condition_fp64(ctx, c, sc, rx, 1, nullptr, out, local_in);
+    API_END
+}
+
+int rxgs_condition_forward_base(rxgs_ctx ctx, rxgs_cond c, rxgs_scene sc, const double* base, const double* rx,
+                                int n_rx, double* out, double* local_in) {
+    API_BEGIN
+    if (!base) return fail(RXGS_ERR_INVALID, "condition_forward: null base");
+    return condition_fp64(ctx, c, sc, rx, n_rx, base, out, local_in);
     API_END
 }
 
@@ -1257,6 +1292,7 @@ int rxgs_render_queries(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, rxgs_txstate s
     RX_TRY(dev_in(ctx, rx, 3 * static_cast<size_t>(n_rx), ctx->scratch_c, &d_rx));
     if (c && c->use_local()) RX_TRY(check_receivers(ctx, sc, rx, n_rx));
     if (st->coeff_version != sc->coeff_version) {  // optimizer stepped since build: basis*base is stale
+        RX_TRY(ensure_tx_full(*st, s));
         RXGS_CUDA(launch_refresh_gb(*sc, *st, s));
         st->coeff_version = sc->coeff_version;
     }
@@ -1531,6 +1567,267 @@ int rxgs_predict(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const rxgs_grid* grid
     rxgs_tx_state_destroy(st);
     if (rc) return rc;
     return rxgs_aggregate_modality(ctx, grid, sc->modality, 1, sc->channels, vals.data(), out);
+    API_END
+}
+
+// ------------------------------------------------------------------ single-call reference API (FP64, device)
+int rxgs_project_gaussians(rxgs_ctx ctx, int n, const double* pos, const double* cov, const double* tau,
+                           const double tx[3], const rxgs_grid* grid, double* geom, int32_t* culled, int32_t* spans) {
+    API_BEGIN
+    if (!ctx || n < 0 || (n && (!pos || !cov || !tau)) || !tx) return fail(RXGS_ERR_INVALID, "project_gaussian: null argument");
+    RX_TRY(validate_grid(grid));
+    RX_TRY(set_device(ctx));
+    cudaStream_t s = ctx->stream;
+    DevBuf a, b, c, t, og, oc, os;
+    const double *dp = nullptr, *dc = nullptr, *dt = nullptr, *dtx = nullptr;
+    RX_TRY(dev_in(ctx, pos, 3 * static_cast<size_t>(n), a, &dp));
+    RX_TRY(dev_in(ctx, cov, 9 * static_cast<size_t>(n), b, &dc));
+    RX_TRY(dev_in(ctx, tau, static_cast<size_t>(n), c, &dt));
+    RX_TRY(dev_in(ctx, tx, 3, t, &dtx));
+    std::vector<double> txh = to_host(tx, 3);
+    double* d_g = nullptr;
+    int32_t* d_c = nullptr;
+    int32_t* d_s = nullptr;
+    RXGS_CUDA(og.ensure(std::max<size_t>(12 * static_cast<size_t>(n), 1) * 8));
+    RXGS_CUDA(oc.ensure(std::max<size_t>(n, 1) * 4));
+    RXGS_CUDA(os.ensure(std::max<size_t>(4 * static_cast<size_t>(n), 1) * 4));
+    d_g = og.as<double>();
+    d_c = oc.as<int32_t>();
+    d_s = os.as<int32_t>();
+    const DevGrid g = make_grid(grid);
+    RXGS_CUDA(launch_project(n, dp, dc, dt, txh.data(), g, d_g, d_c, reinterpret_cast<int4*>(d_s), s));
+    ctx->launches += 1;
+    RXGS_CUDA(cudaStreamSynchronize(s));
+    if (geom && n) RXGS_CUDA(cudaMemcpy(geom, d_g, 12 * sizeof(double) * n, cudaMemcpyDefault));
+    if (culled && n) RXGS_CUDA(cudaMemcpy(culled, d_c, sizeof(int32_t) * n, cudaMemcpyDefault));
+    if (spans && n) RXGS_CUDA(cudaMemcpy(spans, d_s, 4 * sizeof(int32_t) * n, cudaMemcpyDefault));
+    return RXGS_OK;
+    API_END
+}
+
+int rxgs_fle_eval(rxgs_ctx ctx, int what, int l_max, int n, const double* a, const double* b, const double* coeffs,
+                  double* out) {
+    API_BEGIN
+    static const char* kName[] = {"eval_basis", "eval_basis_jet", "legendre_table", "legendre_table_dtheta",
+                                  "normalization", "eval_radiance"};
+    if (!ctx || what < 0 || what > 5 || n < 0) return fail(RXGS_ERR_INVALID, "fle_eval: bad argument");
+    if (l_max < 0) return fail(RXGS_ERR_INVALID, std::string(kName[what]) + ": l_max < 0");
+    if (l_max > kApiMaxLmax) return fail(RXGS_ERR_INVALID, std::string(kName[what]) + ": l_max too large for the device");
+    if (n == 0) return RXGS_OK;
+    if (!a || !out || ((what == 0 || what == 1 || what == 4 || what == 5) && !b) || (what == 5 && !coeffs))
+        return fail(RXGS_ERR_INVALID, "fle_eval: null argument");
+    std::vector<double> ah = to_host(a, static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) {  // the reference's argument checks (radiance.cpp:17, 117)
+        if (what == 2 && std::abs(ah[i]) > 1.0 + 1e-12)
+            return fail(RXGS_ERR_INVALID, "legendre_table: |x| > 1");
+        if (what == 5 && (ah[i] < 0.0 || ah[i] > 3.14159265358979323846))
+            return fail(RXGS_ERR_INVALID, "eval_radiance: theta out of [0, pi]");
+    }
+    RX_TRY(set_device(ctx));
+    const int L = (l_max + 1) * (l_max + 1), NP = (l_max + 1) * (l_max + 2) / 2;
+    const size_t per = what == 0 ? 2 * L : what == 1 ? 6 * L : what == 2 ? NP : what == 3 ? 2 * NP : what == 4 ? 1 : 2;
+    DevBuf ta, tb, tc, to;
+    const double *da = nullptr, *db = nullptr, *dcf = nullptr;
+    RX_TRY(dev_in(ctx, a, static_cast<size_t>(n), ta, &da));
+    if (b) RX_TRY(dev_in(ctx, b, static_cast<size_t>(n), tb, &db));
+    if (what == 5) RX_TRY(dev_in(ctx, coeffs, static_cast<size_t>(n) * 2 * L, tc, &dcf));
+    double* d_out = nullptr;
+    RX_TRY(dev_out(out, per * n, to, &d_out));
+    RXGS_CUDA(launch_fle_eval(what, n, l_max, da, db, dcf, d_out, ctx->stream));
+    ctx->launches += 1;
+    RX_TRY(finish_out(ctx, out, d_out, per * n));
+    RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RXGS_OK;
+    API_END
+}
+
+int rxgs_blend_ray(rxgs_ctx ctx, int n, const double* weights, const double* signals, double out[3]) {
+    API_BEGIN
+    if (!ctx || n < 0 || !out || (n && (!weights || !signals))) return fail(RXGS_ERR_INVALID, "blend_ray: null argument");
+    RX_TRY(set_device(ctx));
+    DevBuf tw, ts, to;
+    const double *dw = nullptr, *ds = nullptr;
+    RX_TRY(dev_in(ctx, weights, std::max(n, 1), tw, &dw));
+    RX_TRY(dev_in(ctx, signals, 2 * static_cast<size_t>(std::max(n, 1)), ts, &ds));
+    double* d_out = nullptr;
+    RX_TRY(dev_out(out, 3, to, &d_out));
+    RXGS_CUDA(launch_blend_ray(n, dw, ds, d_out, ctx->stream));
+    ctx->launches += 1;
+    RX_TRY(finish_out(ctx, out, d_out, 3));
+    RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RXGS_OK;
+    API_END
+}
+
+int rxgs_occupancy_sample(rxgs_ctx ctx, int R, const double lo[3], const double hi[3], const double* densities, int n,
+                          const double* points, int nearest, double* out) {
+    API_BEGIN
+    if (!ctx || n < 0 || (n && (!points || !out))) return fail(RXGS_ERR_INVALID, "sample: null argument");
+    if (n == 0) return RXGS_OK;
+    RX_TRY(set_device(ctx));
+    DevBuf td, tp, to;
+    const double *dd = nullptr, *dp = nullptr;
+    std::vector<double> l(3, 0.0), h(3, 1.0);
+    if (densities && R > 0) {
+        RX_TRY(dev_in(ctx, densities, static_cast<size_t>(R) * R * R, td, &dd));
+        l = to_host(lo, 3);
+        h = to_host(hi, 3);
+    }
+    RX_TRY(dev_in(ctx, points, 3 * static_cast<size_t>(n), tp, &dp));
+    double* d_out = nullptr;
+    RX_TRY(dev_out(out, static_cast<size_t>(n), to, &d_out));
+    RXGS_CUDA(launch_occ_sample(R, l.data(), h.data(), dd, n, dp, nearest, d_out, ctx->stream));
+    ctx->launches += 1;
+    RX_TRY(finish_out(ctx, out, d_out, static_cast<size_t>(n)));
+    RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RXGS_OK;
+    API_END
+}
+
+int rxgs_probe_grid(rxgs_ctx ctx, int R, const double lo[3], const double hi[3], const double* densities, int n,
+                    const double* from, const double* to, int samples, int nearest, double* out) {
+    API_BEGIN
+    if (samples < 1) return fail(RXGS_ERR_INVALID, "probe_segment: samples must be >= 1");
+    if (!ctx || n < 0 || (n && (!from || !to || !out))) return fail(RXGS_ERR_INVALID, "probe_segment: null argument");
+    if (n == 0) return RXGS_OK;
+    RX_TRY(set_device(ctx));
+    DevBuf td, tf, tt, to_;
+    const double *dd = nullptr, *df = nullptr, *dt = nullptr;
+    std::vector<double> l(3, 0.0), h(3, 1.0);
+    if (densities && R > 0) {
+        RX_TRY(dev_in(ctx, densities, static_cast<size_t>(R) * R * R, td, &dd));
+        l = to_host(lo, 3);
+        h = to_host(hi, 3);
+    }
+    RX_TRY(dev_in(ctx, from, 3 * static_cast<size_t>(n), tf, &df));
+    RX_TRY(dev_in(ctx, to, 3 * static_cast<size_t>(n), tt, &dt));
+    double* d_out = nullptr;
+    RX_TRY(dev_out(out, 2 * static_cast<size_t>(n), to_, &d_out));
+    RXGS_CUDA(launch_probe64(R, l.data(), h.data(), dd, n, df, dt, samples, nearest, d_out, ctx->stream));
+    ctx->launches += 1;
+    RX_TRY(finish_out(ctx, out, d_out, 2 * static_cast<size_t>(n)));
+    RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RXGS_OK;
+    API_END
+}
+
+int rxgs_fourier_encode(rxgs_ctx ctx, int F, const double* freqs, int n, const double* r, double* out) {
+    API_BEGIN
+    if (!ctx || F < 0 || n < 0 || (n && (!r || !out)) || (F && !freqs))
+        return fail(RXGS_ERR_INVALID, "fourier_encode: null argument");
+    if (n == 0 || F == 0) return RXGS_OK;
+    RX_TRY(set_device(ctx));
+    DevBuf tf, tr, to;
+    const double *df = nullptr, *dr = nullptr;
+    RX_TRY(dev_in(ctx, freqs, 3 * static_cast<size_t>(F), tf, &df));
+    RX_TRY(dev_in(ctx, r, 3 * static_cast<size_t>(n), tr, &dr));
+    double* d_out = nullptr;
+    RX_TRY(dev_out(out, 6 * static_cast<size_t>(F) * n, to, &d_out));
+    RXGS_CUDA(launch_fourier64(F, df, n, dr, d_out, ctx->stream));
+    ctx->launches += 1;
+    RX_TRY(finish_out(ctx, out, d_out, 6 * static_cast<size_t>(F) * n));
+    RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RXGS_OK;
+    API_END
+}
+
+int rxgs_mlp_layer_forward(rxgs_ctx ctx, int in, int out_dim, const double* w, const double* b, int n,
+                           const double* x, double* y) {
+    API_BEGIN
+    if (!ctx || in < 0 || out_dim < 0 || n < 0) return fail(RXGS_ERR_INVALID, "MlpLayer::forward: bad argument");
+    if (!n || !out_dim) return RXGS_OK;
+    if (!b || !x || !y || (in && !w)) return fail(RXGS_ERR_INVALID, "MlpLayer::forward: null argument");
+    RX_TRY(set_device(ctx));
+    DevBuf tw, tb, tx, ty;
+    const double *dw = nullptr, *db = nullptr, *dx = nullptr;
+    RX_TRY(dev_in(ctx, w, std::max<size_t>(static_cast<size_t>(in) * out_dim, 1), tw, &dw));
+    RX_TRY(dev_in(ctx, b, static_cast<size_t>(out_dim), tb, &db));
+    RX_TRY(dev_in(ctx, x, std::max<size_t>(static_cast<size_t>(in) * n, 1), tx, &dx));
+    double* d_y = nullptr;
+    RX_TRY(dev_out(y, static_cast<size_t>(out_dim) * n, ty, &d_y));
+    RXGS_CUDA(launch_mlp_layer64(in, out_dim, dw, db, n, dx, d_y, ctx->stream));
+    ctx->launches += 1;
+    RX_TRY(finish_out(ctx, y, d_y, static_cast<size_t>(out_dim) * n));
+    RXGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RXGS_OK;
+    API_END
+}
+
+int rxgs_grid_validate(const rxgs_grid* grid) {
+    API_BEGIN
+    return validate_grid(grid);
+    API_END
+}
+
+// A device transmitter state from a host TxState (sphraster.hpp:52-61): the
+// FP64 rows, spans, basis and per-tile lists the caller holds; the walk and
+// the needed-row compaction run on the device as after a build.
+int rxgs_tx_state_import(rxgs_ctx ctx, rxgs_scene sc, const rxgs_grid* grid, const int32_t* culled,
+                         const double* geom, const int32_t* spans, const double* basis, const int64_t* offsets,
+                         const int32_t* indices, rxgs_txstate* out) {
+    API_BEGIN
+    if (!ctx || !sc || !out || (sc->k && (!culled || !geom || !spans || !basis)) || !offsets)
+        return fail(RXGS_ERR_INVALID, "tx_state_import: null argument");
+    RX_TRY(validate_grid(grid));
+    RX_TRY(set_device(ctx));
+    cudaStream_t s = ctx->stream;
+    auto* st = new rxgs_txstate_s;
+    std::unique_ptr<rxgs_txstate_s> guard(st);
+    st->ctx = ctx;
+    st->k = sc->k;
+    st->l_max = sc->l_max;
+    st->L = sc->L;
+    st->channels = sc->channels;
+    st->grid = make_grid(grid);
+    st->version = next_version();
+    st->coeff_version = 0;  // basis*base from the scene's coefficients on first query use
+    st->geo_version = sc->geo_version;
+    st->full = true;
+    const DevGrid& g = st->grid;
+    const size_t K = std::max(sc->k, 1);
+    std::vector<int64_t> off = to_host(offsets, static_cast<size_t>(g.n_tiles) + 1);
+    const int64_t E = off[g.n_tiles];
+    if (off[0] != 0 || E < 0) return fail(RXGS_ERR_INVALID, "tx_state_import: bad tile offsets");
+    if (E && !indices) return fail(RXGS_ERR_INVALID, "tx_state_import: null argument");
+    std::vector<int32_t> cul = to_host(culled, static_cast<size_t>(sc->k));
+    int64_t vis = 0;
+    for (int k = 0; k < sc->k; ++k) vis += cul[k] == 0;
+    st->entries = E;
+    st->visible = vis;
+    RXGS_CUDA(st->rec.ensure(K * sizeof(GaussRec)));
+    RXGS_CUDA(st->culled.ensure(K * sizeof(int)));
+    RXGS_CUDA(st->geom.ensure(K * 12 * sizeof(double)));
+    RXGS_CUDA(st->spans.ensure(K * sizeof(int4)));
+    RXGS_CUDA(st->basis64.ensure(K * sc->L * 2 * sizeof(double)));
+    RXGS_CUDA(st->basis32.ensure(K * sc->L * sizeof(float2)));
+    RXGS_CUDA(st->gb32.ensure(K * sc->L * sc->channels * sizeof(float2)));
+    RXGS_CUDA(st->tile_offsets.ensure((g.n_tiles + 1) * sizeof(int64_t)));
+    RXGS_CUDA(st->list.ensure(std::max<int64_t>(E, 1) * sizeof(int)));
+    RXGS_CUDA(st->keys.ensure(std::max<int64_t>(E, 1) * sizeof(uint64_t)));
+    if (sc->k) {
+        RXGS_CUDA(cudaMemcpy(st->culled.p, cul.data(), sc->k * sizeof(int), cudaMemcpyHostToDevice));
+        RXGS_CUDA(cudaMemcpy(st->geom.p, geom, sc->k * 12 * sizeof(double), cudaMemcpyDefault));
+        RXGS_CUDA(cudaMemcpy(st->spans.p, spans, sc->k * sizeof(int4), cudaMemcpyDefault));
+        RXGS_CUDA(cudaMemcpy(st->basis64.p, basis, sc->k * sc->L * 2 * sizeof(double), cudaMemcpyDefault));
+    }
+    RXGS_CUDA(cudaMemcpy(st->tile_offsets.p, off.data(), off.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    if (E) RXGS_CUDA(cudaMemcpy(st->list.p, indices, E * sizeof(int), cudaMemcpyDefault));
+    RXGS_CUDA(launch_rec_from_geom(sc->k, st->culled.as<int>(), st->geom.as<double>(), st->basis64.as<double>(),
+                                   sc->L, st->rec.as<GaussRec>(), st->basis32.as<float2>(), s));
+    const size_t cells = static_cast<size_t>(g.nt) * g.np;
+    RXGS_CUDA(st->tw.ensure(std::max<size_t>(E, 1) * g.cell_blocks * kMaxCellsPerBlock * sizeof(float)));
+    RXGS_CUDA(st->walk_len.ensure(static_cast<size_t>(g.n_tiles) * g.cell_blocks * sizeof(int)));
+    RXGS_CUDA(st->cell_T.ensure(cells * sizeof(double)));
+    RXGS_CUDA(st->cell_len.ensure(cells * sizeof(int)));
+    RXGS_CUDA(launch_walk(*st, s));
+    RX_TRY(compact_needed(ctx, *sc, *st, s));
+    ctx->launches += 3;
+    RXGS_CUDA(cudaStreamSynchronize(s));
+    ctx_retain(ctx);
+    st->sc = sc;
+    sc->refs += 1;
+    *out = guard.release();
+    return RXGS_OK;
     API_END
 }
 

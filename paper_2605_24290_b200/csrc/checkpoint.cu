@@ -269,7 +269,7 @@ struct Writer {
             out += dg.substr(0, 1);
             if (k > 1) out += "." + dg.substr(1);
             const int x = n - 1;
-            char eb[8];
+            char eb[16];
             std::snprintf(eb, sizeof eb, "e%c%02d", x < 0 ? '-' : '+', x < 0 ? -x : x);
             out += eb;
         }

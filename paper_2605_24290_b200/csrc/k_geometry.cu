@@ -55,33 +55,13 @@ __device__ __forceinline__ double normalization(int l, int am) {  // radiance.cp
     return sqrt((2.0 * l + 1.0) / (4.0 * kPi) * ratio);
 }
 
-template <int LMT>  // LMT > 0: l_max known at compile time (tables in registers)
-__global__ void k_tx_prep(int K, int l_max_rt, int C, const double* __restrict__ pos,
-                          const double* __restrict__ ls, const double* __restrict__ q,
-                          const double* __restrict__ tau_logit,
-                          const double* __restrict__ coeffs64, double tx0, double tx1, double tx2,
-                          DevGrid g, GaussRec* __restrict__ rec, int* __restrict__ culled,
-                          double* __restrict__ geom, int4* __restrict__ spans,
-                          double* __restrict__ basis64, float2* __restrict__ basis32,
-                          float2* __restrict__ gb32, uint64_t* __restrict__ depth_key,
-                          int* __restrict__ tile_count) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= K) return;
-    const int l_max = LMT > 0 ? LMT : l_max_rt;
-    const int L = (l_max + 1) * (l_max + 1);
-    double* gm = geom + 12 * static_cast<size_t>(k);
-    for (int i = 0; i < 12; ++i) gm[i] = 0.0;
-    int4 sp = make_int4(0, -1, 0, -1);
-    int is_culled = 1;
-    GaussRec r{};
-
-    double sig[9];
-    covariance(ls + 3 * static_cast<size_t>(k), q + 4 * static_cast<size_t>(k), sig);
-    const double tau = 1.0 / (1.0 + exp(-tau_logit[k]));  // linalg.hpp:157
-
-    const double u0 = pos[3 * static_cast<size_t>(k)] - tx0;
-    const double u1 = pos[3 * static_cast<size_t>(k) + 1] - tx1;
-    const double u2 = pos[3 * static_cast<size_t>(k) + 2] - tx2;
+// project_gaussian (sphraster.cpp:22-83) of one Gaussian at u = p - tx with
+// covariance sig and activated tau: gm = [theta, phi, depth, A (a, b, c, d),
+// A^-1 (4), tau], the inclusive tile span, the culled flag and the walk's
+// record.  Shared by k_tx_prep and the single-Gaussian API (k_project).
+__device__ __forceinline__ void project_core(double u0, double u1, double u2, const double* sig, double tau,
+                                             const DevGrid& g, double* gm, int4& sp, int& is_culled,
+                                             GaussRec& r) {
     const double d = sqrt(u0 * u0 + u1 * u1 + u2 * u2);
     double theta = 0.0, phi = 0.0;
     if ((d >= g.radius) && d != 0.0) {
@@ -143,6 +123,47 @@ __global__ void k_tx_prep(int K, int l_max_rt, int C, const double* __restrict__
             r.tau = tau;
         }
     }
+}
+
+// FULL: also the FP64 per-Gaussian geometry (geom) and basis (basis64) that
+// only the adjoint, the materialised render API and the state accessors
+// read; the query path builds lean states and completes them on demand
+// (ensure_tx_full, capi.cu) with the identical arithmetic.
+template <int LMT, bool FULL>  // LMT > 0: l_max known at compile time (tables in registers)
+__global__ void k_tx_prep(int K, int l_max_rt, int C, const double* __restrict__ pos,
+                          const double* __restrict__ ls, const double* __restrict__ q,
+                          const double* __restrict__ tau_logit,
+                          const double* __restrict__ coeffs64, double tx0, double tx1, double tx2,
+                          DevGrid g, GaussRec* __restrict__ rec, int* __restrict__ culled,
+                          double* __restrict__ geom, int4* __restrict__ spans,
+                          double* __restrict__ basis64, float2* __restrict__ basis32,
+                          float2* __restrict__ gb32, uint64_t* __restrict__ depth_key,
+                          int* __restrict__ tile_count) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    const int l_max = LMT > 0 ? LMT : l_max_rt;
+    const int L = (l_max + 1) * (l_max + 1);
+    double gm[12];
+#pragma unroll
+    for (int i = 0; i < 12; ++i) gm[i] = 0.0;
+    int4 sp = make_int4(0, -1, 0, -1);
+    int is_culled = 1;
+    GaussRec r{};
+
+    double sig[9];
+    covariance(ls + 3 * static_cast<size_t>(k), q + 4 * static_cast<size_t>(k), sig);
+    const double tau = 1.0 / (1.0 + exp(-tau_logit[k]));  // linalg.hpp:157
+
+    const double u0 = pos[3 * static_cast<size_t>(k)] - tx0;
+    const double u1 = pos[3 * static_cast<size_t>(k) + 1] - tx1;
+    const double u2 = pos[3 * static_cast<size_t>(k) + 2] - tx2;
+    project_core(u0, u1, u2, sig, tau, g, gm, sp, is_culled, r);
+    const double d = gm[2], theta = gm[0], phi = gm[1];
+    if (FULL) {
+        double* gout = geom + 12 * static_cast<size_t>(k);
+#pragma unroll
+        for (int i = 0; i < 12; ++i) gout[i] = gm[i];
+    }
     rec[k] = r;
     culled[k] = is_culled;
     spans[k] = sp;
@@ -156,8 +177,10 @@ __global__ void k_tx_prep(int K, int l_max_rt, int C, const double* __restrict__
     const double* cb = coeffs64 + static_cast<size_t>(k) * L * C * 2;
     if (is_culled) {
         for (int i = 0; i < L; ++i) {
-            b64[2 * i] = 0.0;
-            b64[2 * i + 1] = 0.0;
+            if (FULL) {
+                b64[2 * i] = 0.0;
+                b64[2 * i + 1] = 0.0;
+            }
             b32[i] = make_float2(0.f, 0.f);
             for (int c = 0; c < C; ++c) g32[i * C + c] = make_float2(0.f, 0.f);
         }
@@ -196,7 +219,7 @@ __global__ void k_tx_prep(int K, int l_max_rt, int C, const double* __restrict__
             const double np = normalization(l, am) * AT(l, am);
             const int idx = l * l + m + l;
             const double br = np * cm[m + LM], bi = np * sn[m + LM];
-            reinterpret_cast<double2*>(b64)[idx] = make_double2(br, bi);
+            if (FULL) reinterpret_cast<double2*>(b64)[idx] = make_double2(br, bi);
             b32[idx] = make_float2(static_cast<float>(br), static_cast<float>(bi));
             for (int c = 0; c < C; ++c) {
                 const double a_ = cb[(idx * C + c) * 2], b_ = cb[(idx * C + c) * 2 + 1];
@@ -206,6 +229,180 @@ __global__ void k_tx_prep(int K, int l_max_rt, int C, const double* __restrict__
         }
     }
 #undef AT
+}
+
+// ---------------------------------------------------------------- single-call API kernels
+// project_gaussian (sphraster.cpp:22-83) of n Gaussians given their
+// covariances and activated tau: the arithmetic of k_tx_prep (project_core).
+__global__ void k_project(int n, const double* __restrict__ pos, const double* __restrict__ cov,
+                          const double* __restrict__ tau, double tx0, double tx1, double tx2, DevGrid g,
+                          double* __restrict__ geom, int* __restrict__ culled, int4* __restrict__ spans) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double gm[12];
+#pragma unroll
+    for (int a = 0; a < 12; ++a) gm[a] = 0.0;
+    int4 sp = make_int4(0, -1, 0, -1);
+    int c = 1;
+    GaussRec r{};
+    project_core(pos[3 * static_cast<size_t>(i)] - tx0, pos[3 * static_cast<size_t>(i) + 1] - tx1,
+                 pos[3 * static_cast<size_t>(i) + 2] - tx2, cov + 9 * static_cast<size_t>(i), tau[i], g, gm, sp, c,
+                 r);
+    for (int a = 0; a < 12; ++a) geom[12 * static_cast<size_t>(i) + a] = gm[a];
+    culled[i] = c;
+    spans[i] = sp;
+}
+
+// The walk record of an imported state (rxgs_tx_state_import) from its FP64
+// geometry rows: the same values k_tx_prep writes (sin / cos of theta on the
+// device, p_b + p_c summed once), and the f32 basis.
+__global__ void k_rec_from_geom(int K, const int* __restrict__ culled, const double* __restrict__ geom,
+                                const double* __restrict__ basis64, int L, GaussRec* __restrict__ rec,
+                                float2* __restrict__ basis32) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    GaussRec r{};
+    if (!culled[k]) {
+        const double* gm = geom + 12 * static_cast<size_t>(k);
+        r.theta = gm[0];
+        r.phi = gm[1];
+        r.sin_theta = sin(gm[0]);
+        r.cos_theta = cos(gm[0]);
+        r.pa = gm[7];
+        r.pbc = gm[8] + gm[9];
+        r.pd = gm[10];
+        r.tau = gm[11];
+    }
+    rec[k] = r;
+    for (int l = 0; l < L; ++l) {
+        const double* b = basis64 + (static_cast<size_t>(k) * L + l) * 2;
+        basis32[static_cast<size_t>(k) * L + l] = make_float2(static_cast<float>(b[0]), static_cast<float>(b[1]));
+    }
+}
+
+constexpr int kApiLmax = 24;
+constexpr int kApiNP = (kApiLmax + 1) * (kApiLmax + 2) / 2;
+
+// legendre_table (radiance.cpp:16-37) after the |x| check / clamp
+__device__ void legendre_rt(double x, int l_max, double* P) {
+    x = x < -1.0 ? -1.0 : (x > 1.0 ? 1.0 : x);
+    const double s = sqrt(dmax(0.0, (1.0 - x) * (1.0 + x)));
+    for (int i = 0; i < (l_max + 1) * (l_max + 2) / 2; ++i) P[i] = 0.0;
+#define AT(l, m) P[(l) * ((l) + 1) / 2 + (m)]
+    AT(0, 0) = 1.0;
+    for (int m = 1; m <= l_max; ++m) AT(m, m) = AT(m - 1, m - 1) * (2.0 * m - 1.0) * s;
+    for (int m = 0; m < l_max; ++m) AT(m + 1, m) = x * (2.0 * m + 1.0) * AT(m, m);
+    for (int m = 0; m <= l_max; ++m)
+        for (int l = m + 2; l <= l_max; ++l)
+            AT(l, m) = (x * (2.0 * l - 1.0) * AT(l - 1, m) - (l + m - 1.0) * AT(l - 2, m)) / static_cast<double>(l - m);
+#undef AT
+}
+
+// legendre_table_dtheta (radiance.cpp:39-77)
+__device__ void legendre_dtheta_rt(double theta, int l_max, double* P, double* D) {
+    const double x = cos(theta), s = sin(theta);
+    for (int i = 0; i < (l_max + 1) * (l_max + 2) / 2; ++i) P[i] = D[i] = 0.0;
+#define AT(l, m) P[(l) * ((l) + 1) / 2 + (m)]
+#define DAT(l, m) D[(l) * ((l) + 1) / 2 + (m)]
+    AT(0, 0) = 1.0;
+    DAT(0, 0) = 0.0;
+    for (int m = 1; m <= l_max; ++m) {
+        const double c = 2.0 * m - 1.0;
+        AT(m, m) = AT(m - 1, m - 1) * c * s;
+        DAT(m, m) = c * (DAT(m - 1, m - 1) * s + AT(m - 1, m - 1) * x);
+    }
+    for (int m = 0; m < l_max; ++m) {
+        const double c = 2.0 * m + 1.0;
+        AT(m + 1, m) = x * c * AT(m, m);
+        DAT(m + 1, m) = c * (-s * AT(m, m) + x * DAT(m, m));
+    }
+    for (int m = 0; m <= l_max; ++m)
+        for (int l = m + 2; l <= l_max; ++l) {
+            const double a = 2.0 * l - 1.0, b = l + m - 1.0, inv = 1.0 / (l - m);
+            AT(l, m) = (x * a * AT(l - 1, m) - b * AT(l - 2, m)) * inv;
+            DAT(l, m) = (a * (-s * AT(l - 1, m) + x * DAT(l - 1, m)) - b * DAT(l - 2, m)) * inv;
+        }
+#undef AT
+#undef DAT
+}
+
+// The FLE basis API (radiance.hpp:36-70), one item per thread:
+//   0 eval_basis(theta, phi)            -> L complex
+//   1 eval_basis_jet(theta, phi)        -> b, db/dtheta, db/dphi (3 L complex)
+//   2 legendre_table(x)                 -> NP
+//   3 legendre_table_dtheta(theta)      -> P (NP), dP/dtheta (NP)
+//   4 normalization(l, m)               -> 1
+//   5 eval_radiance(coeffs, theta, phi) -> 1 complex
+__global__ void k_fle_eval(int what, int n, int l_max, const double* __restrict__ a, const double* __restrict__ b,
+                           const double* __restrict__ coeffs, double* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int L = (l_max + 1) * (l_max + 1), NP = (l_max + 1) * (l_max + 2) / 2;
+    double P[kApiNP], D[kApiNP];
+    if (what == 4) {
+        const int l = static_cast<int>(a[i]), m = static_cast<int>(b[i]);
+        out[i] = normalization(l, m < 0 ? -m : m);
+        return;
+    }
+    if (what == 2) {
+        legendre_rt(a[i], l_max, P);
+        for (int q = 0; q < NP; ++q) out[static_cast<size_t>(i) * NP + q] = P[q];
+        return;
+    }
+    if (what == 3) {
+        legendre_dtheta_rt(a[i], l_max, P, D);
+        for (int q = 0; q < NP; ++q) {
+            out[static_cast<size_t>(i) * 2 * NP + q] = P[q];
+            out[static_cast<size_t>(i) * 2 * NP + NP + q] = D[q];
+        }
+        return;
+    }
+    const double theta = a[i], phi = b[i];
+    if (what == 1) legendre_dtheta_rt(theta, l_max, P, D);
+    else legendre_rt(cos(theta), l_max, P);
+    double rr = 0.0, ri = 0.0;
+    for (int l = 0; l <= l_max; ++l)
+        for (int m = -l; m <= l; ++m) {
+            const int am = m < 0 ? -m : m;
+            const int idx = l * l + m + l;
+            const double c = cos(m * phi), sn = sin(m * phi);
+            if (what == 1) {
+                const double nrm = normalization(l, am);
+                const double pb = nrm * P[l * (l + 1) / 2 + am], pd = nrm * D[l * (l + 1) / 2 + am];
+                const double br = pb * c, bi = pb * sn;
+                double* o = out + static_cast<size_t>(i) * 6 * L;
+                o[2 * idx] = br;
+                o[2 * idx + 1] = bi;
+                o[2 * L + 2 * idx] = pd * c;
+                o[2 * L + 2 * idx + 1] = pd * sn;
+                o[4 * L + 2 * idx] = 0.0 * br - static_cast<double>(m) * bi;  // cplx{0, m} * b
+                o[4 * L + 2 * idx + 1] = 0.0 * bi + static_cast<double>(m) * br;
+            } else {
+                const double np = normalization(l, am) * P[l * (l + 1) / 2 + am];
+                const double br = np * c, bi = np * sn;
+                if (what == 0) {
+                    out[static_cast<size_t>(i) * 2 * L + 2 * idx] = br;
+                    out[static_cast<size_t>(i) * 2 * L + 2 * idx + 1] = bi;
+                } else {  // eval_radiance: r += cplx{coef} * basis, component order
+                    (void)0;
+                }
+            }
+        }
+    if (what == 5) {  // accumulate in component order (radiance.cpp:116-125)
+        for (int comp = 0; comp < L; ++comp) {
+            int l = 0;
+            while ((l + 1) * (l + 1) <= comp) ++l;
+            const int m = comp - l * l - l, am = m < 0 ? -m : m;
+            const double np = normalization(l, am) * P[l * (l + 1) / 2 + am];
+            const double br = np * cos(m * phi), bi = np * sin(m * phi);
+            const double cr = coeffs[static_cast<size_t>(i) * 2 * L + 2 * comp],
+                         ci = coeffs[static_cast<size_t>(i) * 2 * L + 2 * comp + 1];
+            rr += cr * br - ci * bi;
+            ri += cr * bi + ci * br;
+        }
+        out[2 * static_cast<size_t>(i)] = rr;
+        out[2 * static_cast<size_t>(i) + 1] = ri;
+    }
 }
 
 __global__ void k_occupancy(int K, int R, const double* __restrict__ pos,
@@ -267,17 +464,41 @@ __global__ void k_occ_finish(size_t n, const unsigned long long* __restrict__ bi
 
 }  // namespace
 
-cudaError_t launch_tx_prep(const rxgs_scene_s& sc, rxgs_txstate_s& st, cudaStream_t s) {
+cudaError_t launch_tx_prep(const rxgs_scene_s& sc, rxgs_txstate_s& st, cudaStream_t s, bool full) {
     if (sc.k == 0) return cudaSuccess;
     const int threads = 128;
     const int blocks = (sc.k + threads - 1) / threads;
-    auto kern = sc.l_max == 2 ? k_tx_prep<2> : (sc.l_max == 9 ? k_tx_prep<9> : k_tx_prep<0>);
+    auto kern = full ? (sc.l_max == 2 ? k_tx_prep<2, true> : (sc.l_max == 9 ? k_tx_prep<9, true> : k_tx_prep<0, true>))
+                     : (sc.l_max == 2 ? k_tx_prep<2, false>
+                                      : (sc.l_max == 9 ? k_tx_prep<9, false> : k_tx_prep<0, false>));
     kern<<<blocks, threads, 0, s>>>(
         sc.k, sc.l_max, sc.channels, sc.d_pos.as<double>(), sc.d_ls.as<double>(),
         sc.d_q.as<double>(), sc.d_tau.as<double>(), sc.d_coeffs64.as<double>(), st.tx[0], st.tx[1],
         st.tx[2], st.grid, st.rec.as<GaussRec>(), st.culled.as<int>(), st.geom.as<double>(),
         st.spans.as<int4>(), st.basis64.as<double>(), st.basis32.as<float2>(),
         st.gb32.as<float2>(), st.depth_key.as<uint64_t>(), st.tile_count.as<int>());
+    return cudaGetLastError();
+}
+
+cudaError_t launch_project(int n, const double* pos, const double* cov, const double* tau, const double* tx,
+                           const DevGrid& g, double* geom, int* culled, int4* spans, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    k_project<<<(n + 127) / 128, 128, 0, s>>>(n, pos, cov, tau, tx[0], tx[1], tx[2], g, geom, culled, spans);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fle_eval(int what, int n, int l_max, const double* a, const double* b, const double* coeffs,
+                            double* out, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    if (l_max > kApiLmax) return cudaErrorInvalidValue;
+    k_fle_eval<<<(n + 63) / 64, 64, 0, s>>>(what, n, l_max, a, b, coeffs, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rec_from_geom(int K, const int* culled, const double* geom, const double* basis64, int L,
+                                 GaussRec* rec, float2* basis32, cudaStream_t s) {
+    if (K == 0) return cudaSuccess;
+    k_rec_from_geom<<<(K + 127) / 128, 128, 0, s>>>(K, culled, geom, basis64, L, rec, basis32);
     return cudaGetLastError();
 }
 

@@ -180,6 +180,9 @@ struct rxgs_scene_s {
     // steps, densify): transmitter states remember the values they were built
     // or refreshed at, so a reused state never renders stale basis*base rows
     uint64_t coeff_version = 1, geo_version = 1;
+    // transmitter states built from this scene keep it alive (lean states are
+    // completed from it on demand); rxgs_scene_destroy drops the caller's ref
+    int refs = 1;
     // exact position -> lowest Gaussian index (receiver-on-Gaussian check,
     // conditioning.cpp:380-382), built lazily on the host
     std::unordered_map<std::string, int> pos_index;
@@ -206,6 +209,10 @@ struct rxgs_txstate_s {
     // the scene's coeff_version / geo_version this state's basis*base rows
     // and geometry were computed from
     uint64_t coeff_version = 0, geo_version = 0;
+    // the scene it was built from (retained), and whether geom / basis64 are
+    // filled (false after a lean build: the query path never reads them)
+    rxgs_scene_s* sc = nullptr;
+    bool full = false;
     // walked list entries regrouped by Gaussian (training adjoint), built lazily
     rxgs_b200::DevBuf gauss_off, gauss_ent;
     bool regrouped = false;
@@ -223,7 +230,7 @@ struct rxgs_cond_s {
     std::vector<double> h_occ;  // host f64 copy of the occupancy densities (checkpoint save)
     double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     int64_t global_calls = 0, local_calls = 0;
-    rxgs_b200::DevBuf d_params32, d_params64, d_occ32;
+    rxgs_b200::DevBuf d_params32, d_params64, d_occ32, d_occ64;  // d_occ64: the FP64 API kernels (k_refapi.cu)
     // trilinear cell table: per cell c in [-1, R]^3 the 8 polynomial
     // coefficients of its trilinear patch (k_occ_cubes, k_cond.cu)
     rxgs_b200::DevBuf d_occ_cube;
@@ -239,13 +246,35 @@ namespace rxgs_b200 {
 // ---- context lifetime (capi.cu)
 void ctx_retain(rxgs_ctx ctx);
 void ctx_release(rxgs_ctx ctx);
+void scene_release(rxgs_scene_s* sc);  // drops one reference, frees at zero
 
 // ---- timing helpers (capi.cu)
 void timing_begin(rxgs_ctx ctx, const char* name, cudaEvent_t* a);
 void timing_end(rxgs_ctx ctx, const char* name, cudaEvent_t a, double work);
 
 // ---- k_geometry.cu (FP64, compiled with -fmad=false)
-cudaError_t launch_tx_prep(const rxgs_scene_s& sc, rxgs_txstate_s& st, cudaStream_t s);
+cudaError_t launch_tx_prep(const rxgs_scene_s& sc, rxgs_txstate_s& st, cudaStream_t s, bool full);
+// Completes a lean state with its FP64 geometry / basis (capi.cu): the scene
+// must still have the geometry the state was built from.
+int ensure_tx_full(rxgs_txstate_s& st, cudaStream_t s);
+cudaError_t launch_project(int n, const double* pos, const double* cov, const double* tau, const double* tx,
+                           const DevGrid& g, double* geom, int* culled, int4* spans, cudaStream_t s);
+cudaError_t launch_fle_eval(int what, int n, int l_max, const double* a, const double* b, const double* coeffs,
+                            double* out, cudaStream_t s);
+constexpr int kApiMaxLmax = 24;
+// ---- k_refapi.cu (FP64 single-call API kernels)
+cudaError_t launch_blend_ray(int n, const double* w, const double* sig, double* out, cudaStream_t s);
+cudaError_t launch_occ_sample(int R, const double* lo, const double* hi, const double* dens, int n, const double* pts,
+                              int nearest, double* out, cudaStream_t s);
+cudaError_t launch_probe64(int R, const double* lo, const double* hi, const double* dens, int n, const double* from,
+                           const double* to, int samples, int nearest, double* out, cudaStream_t s);
+cudaError_t launch_fourier64(int F, const double* freqs, int n, const double* r, double* out, cudaStream_t s);
+cudaError_t launch_mlp_layer64(int in, int nout, const double* w, const double* b, int n, const double* x, double* y,
+                               cudaStream_t s);
+cudaError_t launch_cond_forward64(const rxgs_cond_s& c, const rxgs_scene_s& sc, const double* d_rx, int n_rx,
+                                  const double* base, double* ag64, double* out, double* local_in, cudaStream_t s);
+cudaError_t launch_rec_from_geom(int K, const int* culled, const double* geom, const double* basis64, int L,
+                                 GaussRec* rec, float2* basis32, cudaStream_t s);
 cudaError_t launch_occupancy(const rxgs_scene_s& sc, int R, const double* lo, const double* hi,
                              double* d_out64, float* d_out32, cudaStream_t s);
 

@@ -99,6 +99,7 @@ int geometry_grads(rxgs_trainer t, rxgs_txstate_s& st, const double* d_rx, int n
     RXGS_CUDA(t->b_rds.ensure(std::max<size_t>(K * n_jc, 1) * sizeof(double2)));
     RXGS_CUDA(t->geo_tmp.ensure(std::max<size_t>(t->n_geo, 1) * sizeof(double)));
     double* gt = t->geo_tmp.as<double>();  // [pos | tau | ls | q]
+    TRY(ensure_tx_full(st, s));
     RXGS_CUDA(launch_backward_render(st, *sc, t->co64.as<double>(), n_rx, t->dv64.as<double>(), t->b_sig.as<double2>(),
                                      t->b_eg.as<double>(), t->b_eds.as<double2>(), t->b_rg.as<double>(),
                                      t->b_rds.as<double2>(), gt, gt + 4 * static_cast<size_t>(K),
@@ -222,6 +223,7 @@ int rxgs_train_grads(rxgs_trainer t, rxgs_txstate st, const double* rx, int n_rx
     }
     if (!st->regrouped) TRY(train_regroup(ctx, *st, s));
     // ---- forward (coefficients may have changed since the state was built)
+    TRY(ensure_tx_full(*st, s));
     RXGS_CUDA(launch_refresh_gb(*sc, *st, s));
     st->coeff_version = sc->coeff_version;
     const size_t ag_n = static_cast<size_t>(n_rx) * sc->L * 4;

@@ -78,6 +78,50 @@ def test_bin_and_sort_on_reference_projections(ctx, capi, orc):
     assert np.array_equal(idx, d["indices"])
 
 
+def test_many_tiles_generic_path(ctx, capi, orc):
+    """More than 4096 tiles: the generic binning path ((tile, rank) pairs and
+    LSD passes on the tile id, k_sort.cu) instead of the fused pass."""
+    import oracle as O
+    sc = capi.synth_scene(6000, 2, 1, 11)
+    grid = capi.Grid(160, 720, 4, 1.0)  # 40 x 180 = 7200 tiles
+    st = ctx.scene(sc).tx_state(TX, grid)
+    og = O.Grid(160, 720, 4, 1.0)
+    otx = orc.tx_state(orc.scene(sc), TX, og)
+    got = st.get()
+    assert np.array_equal(got["offsets"], otx.data["offsets"])
+    assert np.array_equal(got["indices"], otx.data["indices"])
+    assert np.array_equal(st.keys(), _oracle_keys(og, otx))
+
+
+def test_bin_and_sort_depth_ties_and_near_ties(ctx, capi):
+    """Runs of equal or nearly equal FP64 depths (equal after the 32-bit key
+    truncation of the device depth rank) keep the (depth, index) order; a
+    non-culled Gaussian with an empty span contributes no entries."""
+    rng = np.random.default_rng(3)
+    n = 5000
+    depth = 1.0 + rng.integers(0, 40, n) * 0.25  # many exact ties
+    depth[::7] = 3.0 + rng.integers(0, 5, len(depth[::7])) * 1e-15  # near ties, distinct bits
+    depth[::11] = np.nextafter(2.0, 3.0)
+    culled = (rng.uniform(size=n) < 0.1).astype(np.int32)
+    t0 = rng.integers(0, 2, n)
+    p0 = rng.integers(0, 6, n)
+    spans = np.stack([t0, t0 + rng.integers(0, 2, n), p0, p0 + rng.integers(0, 3, n)], 1).astype(np.int32)
+    spans[5] = [1, 0, 0, -1]  # empty span, not culled
+    grid = capi.Grid(24, 48, 8, 0.25)  # 3 x 6 tiles; spans wrap past tiles_phi
+    offs, idx = ctx.bin_and_sort(culled, depth, spans, grid)
+    tp = 6
+    want = [[] for _ in range(18)]
+    for g in sorted(range(n), key=lambda i: (depth[i], i)):
+        if culled[g]:
+            continue
+        t0_, t1_, p0_, p1_ = spans[g]
+        for tt in range(t0_, t1_ + 1):
+            for pp in range(p0_, p1_ + 1):
+                want[tt * tp + pp % tp].append(g)
+    got = [list(idx[offs[t]:offs[t + 1]]) for t in range(18)]
+    assert got == want
+
+
 def test_bin_and_sort_tie_order_and_seam(ctx, capi):
     """Reference KATs: test_sphraster.cpp:96-119 ({1,0,2}) and :121-132 (seam)."""
     grid = capi.Grid(6, 12, 4, 0.25)  # 2 x 3 tiles
