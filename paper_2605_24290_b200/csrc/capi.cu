@@ -846,6 +846,11 @@ int rxgs_bin_and_sort(rxgs_ctx ctx, int k, const int32_t* culled, const double* 
 }
 
 // ------------------------------------------------------------------ render
+// raster::render_field (sphraster.cpp:255-315), materialised: FP64 signals
+// and the FP64 per-cell walk of the reference (k_refapi.cu), so the field
+// matches the reference to its rounding and finite differences of it agree
+// with backward_render.  The fused query path (rxgs_render_queries) is the
+// throughput path.
 int rxgs_render_field(rxgs_ctx ctx, rxgs_txstate st, rxgs_scene sc, const double* coeffs, int n_rx,
                       double* values, double* transmittance) {
     API_BEGIN
@@ -859,12 +864,13 @@ int rxgs_render_field(rxgs_ctx ctx, rxgs_txstate st, rxgs_scene sc, const double
     const size_t nco = static_cast<size_t>(n_rx) * sc->k * stride;
     const double* d_co = nullptr;
     RX_TRY(dev_in(ctx, coeffs, nco, ctx->host_in, &d_co));
-    RXGS_CUDA(ctx->signals.ensure(std::max<size_t>(static_cast<size_t>(sc->k) * n_rx * sc->channels, 1) * sizeof(float2)));
+    DevBuf sig;
+    RXGS_CUDA(sig.ensure(std::max<size_t>(static_cast<size_t>(sc->k) * n_rx * sc->channels, 1) * sizeof(double2)));
     RX_TRY(reset_err_flag(ctx));
     if (nco) {
         RX_TRY(ensure_tx_full(*st, s));
-        RXGS_CUDA(launch_reduce_signals(*st, d_co, n_rx, ctx->signals.as<float2>(), ctx->err_flag.as<int>(), s));
-        ctx->launches += 2;
+        const long long n = static_cast<long long>(nco);
+        RXGS_CUDA(launch_check_finite(n, static_cast<long long>(stride), d_co, ctx->err_flag.as<int>(), s));
     }
     int err = INT_MAX;
     RX_TRY(check_err_flag(ctx, ctx->err_flag.as<int>(), &err));
@@ -878,18 +884,17 @@ int rxgs_render_field(rxgs_ctx ctx, rxgs_txstate st, rxgs_scene sc, const double
     double* d_vals = nullptr;
     double* d_T = nullptr;
     RX_TRY(dev_out(values, nv, ctx->host_out, &d_vals));
-    RX_TRY(dev_out(transmittance, static_cast<size_t>(n_rx) * plane, ctx->scratch_c, &d_T));
-    CompositeOut co;
-    co.values = d_vals;
-    cudaEvent_t ev;
-    timing_begin(ctx, "composite", &ev);
-    RXGS_CUDA(launch_composite(*st, ctx->signals.as<float2>(), n_rx, co, s));
-    timing_end(ctx, "composite", ev, static_cast<double>(n_rx) * sc->channels);
-    ctx->launches += 1;
-    if (d_T) {
-        RXGS_CUDA(launch_fill_transmittance(*st, n_rx, d_T, s));
-        ctx->launches += 1;
+    DevBuf tT;
+    RX_TRY(dev_out(transmittance, static_cast<size_t>(n_rx) * plane, tT, &d_T));
+    if (!d_vals) {
+        RXGS_CUDA(ctx->host_out.ensure(std::max<size_t>(nv, 1) * sizeof(double)));
+        d_vals = ctx->host_out.as<double>();
     }
+    cudaEvent_t ev;
+    timing_begin(ctx, "render_field", &ev);
+    RXGS_CUDA(launch_render64(*st, d_co, n_rx, sig.as<double2>(), d_vals, d_T, s));
+    timing_end(ctx, "render_field", ev, static_cast<double>(n_rx) * sc->channels);
+    ctx->launches += 2;
     RX_TRY(finish_out(ctx, values, d_vals, nv));
     RX_TRY(finish_out(ctx, transmittance, d_T, static_cast<size_t>(n_rx) * plane));
     RXGS_CUDA(cudaStreamSynchronize(s));

@@ -489,6 +489,13 @@ cudaError_t launch_reduce_signals(const rxgs_txstate_s& st, const double* d_coef
     return cudaGetLastError();
 }
 
+cudaError_t launch_check_finite(long long n, long long per_row, const double* d_coeffs, int* d_err,
+                                cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    k_check_finite<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(n, per_row, d_coeffs, d_err);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_check_coincide(const rxgs_scene_s& sc, const double* d_rx, int n_rx, int* d_err,
                                   cudaStream_t s) {
     const long long rows = static_cast<long long>(sc.k) * n_rx;

@@ -243,6 +243,79 @@ __global__ void k_cond_forward64(CondDev c, Occ64 g, int K, const double* __rest
         }
 }
 
+// ---- materialised render_field in FP64 (sphraster.cpp:190-315)
+__device__ __forceinline__ double wrap_pm_pi64(double a) {  // linalg.hpp:152-157
+    a = fmod(a, kTwoPi);
+    if (a > kPi) a -= kTwoPi;
+    if (a <= -kPi) a += kTwoPi;
+    return a;
+}
+
+// s[(k * n_rx + j) * C + c] = sum_comp cplx{a, b} * basis (reduce_signals)
+__global__ void k_reduce_signals64(int K, int L, int C, int n_rx, const int* __restrict__ culled,
+                                   const double* __restrict__ basis64, const double* __restrict__ co,
+                                   double2* __restrict__ sig) {
+    const long long row = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (row >= static_cast<long long>(K) * n_rx) return;
+    const int k = static_cast<int>(row / n_rx), j = static_cast<int>(row % n_rx);
+    const size_t stride = static_cast<size_t>(L) * C * 2;
+    const double* cb = co + (static_cast<size_t>(j) * K + k) * stride;
+    const double* b = basis64 + static_cast<size_t>(k) * L * 2;
+    for (int ch = 0; ch < C; ++ch) {
+        double sr = 0.0, si = 0.0;
+        if (!culled[k])
+            for (int l = 0; l < L; ++l) {
+                const double a = cb[(l * C + ch) * 2], bb = cb[(l * C + ch) * 2 + 1];
+                sr += a * b[2 * l] - bb * b[2 * l + 1];
+                si += a * b[2 * l + 1] + bb * b[2 * l];
+            }
+        sig[(static_cast<size_t>(k) * n_rx + j) * C + ch] = make_double2(sr, si);
+    }
+}
+
+// One thread per (receiver, cell): the reference's per-cell front-to-back
+// walk (gaussian_weight, min(w, 0.999), contribute, update T, exit below 1e-4).
+__global__ void k_render64(DevGrid g, int n_rx, int C, const GaussRec* __restrict__ rec,
+                           const int64_t* __restrict__ offsets, const int* __restrict__ list,
+                           const double2* __restrict__ sig, double* __restrict__ values, double* __restrict__ tout) {
+    const size_t plane = static_cast<size_t>(g.nt) * g.np;
+    const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (t >= static_cast<long long>(n_rx) * plane) return;
+    const int j = static_cast<int>(t / plane);
+    const size_t cell = static_cast<size_t>(t % plane);
+    const int row = static_cast<int>(cell / g.np), col = static_cast<int>(cell % g.np);
+    const int tile = (row / g.ts) * g.tiles_p + col / g.ts;
+    const double theta_r = g.tmin + (row + 0.5) * g.dth;  // SphericalGrid::theta_at
+    const double phi_r = (col + 0.5) * g.dph;             // phi_at
+    double ar[kCMax], ai[kCMax];
+    for (int c = 0; c < C; ++c) ar[c] = ai[c] = 0.0;
+    double T = 1.0;
+    for (int64_t p = offsets[tile]; p < offsets[tile + 1]; ++p) {
+        const int k = list[p];
+        const GaussRec r = rec[k];
+        const double dt = theta_r - r.theta;
+        const double dpraw = wrap_pm_pi64(phi_r - r.phi);
+        const double dp = r.sin_theta * dpraw;
+        const double m2 = r.pa * dt * dt + r.pbc * dt * dp + r.pd * dp * dp;
+        double w = r.tau * exp(-0.5 * m2);
+        w = 0.999 < w ? 0.999 : w;  // std::min(w, kWeightClamp)
+        const double tw = T * w;
+        const double2* s = sig + (static_cast<size_t>(k) * n_rx + j) * C;
+        for (int c = 0; c < C; ++c) {
+            ar[c] += tw * s[c].x;
+            ai[c] += tw * s[c].y;
+        }
+        T *= 1.0 - w;
+        if (T < 1e-4) break;
+    }
+    for (int c = 0; c < C; ++c) {
+        const size_t base = (static_cast<size_t>(j) * C + c) * 2 * plane;
+        values[base + cell] = ar[c];
+        values[base + plane + cell] = ai[c];
+    }
+    if (tout) tout[static_cast<size_t>(j) * plane + cell] = T;
+}
+
 Occ64 make_occ64(const rxgs_cond_s* c, const double* dens, int R, const double* lo, const double* hi) {
     Occ64 g{};
     g.dens = dens;
@@ -256,6 +329,21 @@ Occ64 make_occ64(const rxgs_cond_s* c, const double* dens, int R, const double* 
 }
 
 }  // namespace
+
+cudaError_t launch_render64(const rxgs_txstate_s& st, const double* d_co, int n_rx, double2* d_sig, double* values,
+                            double* tout, cudaStream_t s) {
+    const long long rows = static_cast<long long>(st.k) * n_rx;
+    if (rows > 0)
+        k_reduce_signals64<<<static_cast<unsigned>((rows + 255) / 256), 256, 0, s>>>(
+            st.k, st.L, st.channels, n_rx, st.culled.as<int>(), st.basis64.as<double>(), d_co, d_sig);
+    const long long t = static_cast<long long>(n_rx) * st.grid.nt * st.grid.np;
+    if (t > 0)
+        k_render64<<<static_cast<unsigned>((t + 127) / 128), 128, 0, s>>>(st.grid, n_rx, st.channels,
+                                                                          st.rec.as<GaussRec>(),
+                                                                          st.tile_offsets.as<int64_t>(),
+                                                                          st.list.as<int>(), d_sig, values, tout);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_blend_ray(int n, const double* w, const double* sig, double* out, cudaStream_t s) {
     k_blend_ray<<<1, 1, 0, s>>>(n, w, sig, out);

@@ -492,68 +492,66 @@ __device__ __forceinline__ int entry_tile(int j, int4 sp, int tiles_p) {
     return tt * tiles_p + pp % tiles_p;
 }
 
-// hist[t * nb + b] = entries of block b in tile t.
-__global__ void __launch_bounds__(kTileThreads) k_tile_hist(int K, int64_t E, int nb, int n_tiles, int tiles_p,
-                                                             const int64_t* __restrict__ scan,
-                                                             const int* __restrict__ bfirst,
-                                                             const int* __restrict__ blast,
-                                                             const int4* __restrict__ spans_sorted,
-                                                             int* __restrict__ hist) {
+// (tile, rank) of every entry, in entry (= rank) order, coalesced; with
+// hist != nullptr also the block's tile histogram hist[t * nb + b] (the
+// fused counting-sort path, n_tiles <= kFusedTiles).
+__global__ void __launch_bounds__(kTileThreads) k_emit_entries(int64_t E, int nb, int n_tiles, int tiles_p,
+                                                                const int64_t* __restrict__ scan,
+                                                                const int* __restrict__ bfirst,
+                                                                const int* __restrict__ blast,
+                                                                const int4* __restrict__ spans_sorted,
+                                                                uint32_t* __restrict__ tkey, int* __restrict__ tval,
+                                                                int* __restrict__ hist) {
     extern __shared__ int sm[];
-    int* h = sm;                    // n_tiles
-    int* seg = sm + n_tiles;        // kTileM + 2
+    int* seg = sm;                  // kTileM + 2
     int* own = seg + kTileM + 2;    // kTileM
-    for (int t = threadIdx.x; t < n_tiles; t += kTileThreads) h[t] = 0;
+    int* h = own + kTileM;          // n_tiles (hist only)
+    if (hist)
+        for (int t = threadIdx.x; t < n_tiles; t += kTileThreads) h[t] = 0;
     const int64_t e0 = static_cast<int64_t>(blockIdx.x) * kTileM;
     const int n = static_cast<int>(E - e0 < kTileM ? E - e0 : int64_t{kTileM});
     const EntryMap m = map_entries(bfirst, blast, e0, n, scan, seg, own);
     for (int q = threadIdx.x; q < n; q += kTileThreads) {
         int j;
         const int i = entry_rank(q, e0, seg, own, scan, m, &j);
-        atomicAdd(&h[entry_tile(j, __ldg(spans_sorted + m.r0 + i), tiles_p)], 1);
+        const int t = entry_tile(j, __ldg(spans_sorted + m.r0 + i), tiles_p);
+        tkey[e0 + q] = static_cast<uint32_t>(t);
+        tval[e0 + q] = m.r0 + i;
+        if (hist) atomicAdd(&h[t], 1);
     }
+    if (!hist) return;
     __syncthreads();
     for (int t = threadIdx.x; t < n_tiles; t += kTileThreads) hist[t * nb + blockIdx.x] = h[t];
 }
 
-// Stable scatter of the entries by tile (rank order within a tile); writes
-// list[pos] = Gaussian, keys[pos] = (tile << 32) | rank, and the offsets.
-__global__ void __launch_bounds__(kTileThreads, 2) k_tile_scatter(int K, int64_t E, int nb, int n_tiles, int tiles_p,
-                                                                   const int64_t* __restrict__ scan,
-                                                                   const int* __restrict__ bfirst,
-                                                                   const int* __restrict__ blast,
-                                                                   const int4* __restrict__ spans_sorted,
-                                                                   const int* __restrict__ order,
-                                                                   const int* __restrict__ mat,
-                                                                   const int* __restrict__ base,
-                                                                   int* __restrict__ list,
-                                                                   uint64_t* __restrict__ keys,
-                                                                   int64_t* __restrict__ tile_offsets) {
+// Stable scatter of the entries by tile (rank order within a tile) from the
+// emitted (tile, rank) arrays; writes list[pos] = Gaussian, keys[pos] =
+// (tile << 32) | rank, and the tile offsets.
+__global__ void __launch_bounds__(kTileThreads) k_tile_scatter(int64_t E, int nb, int n_tiles,
+                                                                const uint32_t* __restrict__ tkey,
+                                                                const int* __restrict__ tval,
+                                                                const int* __restrict__ order,
+                                                                const int* __restrict__ mat,
+                                                                const int* __restrict__ base, int* __restrict__ list,
+                                                                uint64_t* __restrict__ keys,
+                                                                int64_t* __restrict__ tile_offsets) {
     extern __shared__ int sm[];
-    int* tb = sm;                                                   // n_tiles: block offset per tile
-    int* seg = tb + n_tiles;                                        // kTileM + 2
-    int* own = seg + kTileM + 2;                                    // kTileM
-    uint16_t* wc = reinterpret_cast<uint16_t*>(own + kTileM);       // kTileWarps x n_tiles (< 8192 each)
+    int* tb = sm;                                          // n_tiles: block offset per tile
+    uint16_t* wc = reinterpret_cast<uint16_t*>(tb + n_tiles);  // kTileWarps x n_tiles (< 8192 each)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < kTileWarps * n_tiles; i += kTileThreads) wc[i] = 0;
     if (blockIdx.x == 0)
         for (int t = threadIdx.x; t <= n_tiles; t += kTileThreads) tile_offsets[t] = base[t];
+    __syncthreads();
     const int64_t e0 = static_cast<int64_t>(blockIdx.x) * kTileM;
     const int n = static_cast<int>(E - e0 < kTileM ? E - e0 : int64_t{kTileM});
-    const EntryMap m = map_entries(bfirst, blast, e0, n, scan, seg, own);
     const int q0 = warp * (kTileM / kTileWarps);
     const unsigned lt = lanemask_lt();
     uint32_t pk[kTileRounds];  // tile, then tile << 12 | local rank (< 1024 per warp)
 #pragma unroll
-    for (int it = 0; it < kTileRounds; ++it) {  // tiles first: independent loads in flight
+    for (int it = 0; it < kTileRounds; ++it) {
         const int q = q0 + it * 32 + lane;
-        int t = 0;
-        if (q < n) {
-            int j;
-            const int i = entry_rank(q, e0, seg, own, scan, m, &j);
-            t = entry_tile(j, __ldg(spans_sorted + m.r0 + i), tiles_p);
-        }
-        pk[it] = static_cast<uint32_t>(t);
+        pk[it] = q < n ? __ldg(tkey + e0 + q) : 0u;
     }
 #pragma unroll
     for (int it = 0; it < kTileRounds; ++it) {
@@ -584,32 +582,9 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile_scatter(int K, int64_t
         if (q >= n) continue;
         const int t = static_cast<int>(pk[it] >> 12);
         const int pos = tb[t] + wc[warp * n_tiles + t] + static_cast<int>(pk[it] & 0xFFFu);
-        int j;
-        const int r = m.r0 + (m.glob ? entry_rank(q, e0, seg, own, scan, m, &j) : own[q]);
+        const int r = __ldg(tval + e0 + q);
         list[pos] = __ldg(order + r);
         keys[pos] = (static_cast<uint64_t>(t) << 32) | static_cast<uint32_t>(r);
-    }
-}
-
-// ---------------------------------------------------------------- generic tile path (many tiles)
-// (tile, rank) of every entry, in entry (= rank) order.
-__global__ void __launch_bounds__(kTileThreads) k_emit_pairs(int K, int64_t E, int tiles_p,
-                                                              const int64_t* __restrict__ scan,
-                                                              const int* __restrict__ bfirst,
-                                                              const int* __restrict__ blast,
-                                                              const int4* __restrict__ spans_sorted,
-                                                              uint32_t* __restrict__ tkey, int* __restrict__ tval) {
-    extern __shared__ int sm[];
-    int* seg = sm;
-    int* own = sm + kTileM + 2;
-    const int64_t e0 = static_cast<int64_t>(blockIdx.x) * kTileM;
-    const int n = static_cast<int>(E - e0 < kTileM ? E - e0 : int64_t{kTileM});
-    const EntryMap m = map_entries(bfirst, blast, e0, n, scan, seg, own);
-    for (int q = threadIdx.x; q < n; q += blockDim.x) {
-        int j;
-        const int i = entry_rank(q, e0, seg, own, scan, m, &j);
-        tkey[e0 + q] = static_cast<uint32_t>(entry_tile(j, spans_sorted[m.r0 + i], tiles_p));
-        tval[e0 + q] = m.r0 + i;
     }
 }
 
@@ -748,45 +723,41 @@ int bin_tiles(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
     int* bfirst = st.rank.as<int>();
     int* blast = bfirst + nbt + 1;
     k_block_ranks<<<(K + 255) / 256, 256, 0, s>>>(K, E, st.scan.as<int64_t>(), bfirst, blast);
-    if (n_tiles <= kFusedTiles) {
-        // (tile, block) count matrix | totals | base | counter in scratch_b
-        const size_t mat_ints = static_cast<size_t>(n_tiles) * nbt;
-        RXGS_CUDA(ctx->scratch_b.ensure(4 * (mat_ints + 2 * (n_tiles + 1) + 64)));
-        int* mat = ctx->scratch_b.as<int>();
-        int* tot = mat + mat_ints;
+    // entries (tile, rank) | pair temporaries | count matrix etc. in scratch_b
+    const size_t o_v = al256(4 * (E + 1)), o_kt = o_v + al256(4 * (E + 1)), o_vt = o_kt + al256(4 * (E + 1)),
+                 o_w = o_vt + al256(4 * (E + 1));
+    const bool fused = n_tiles <= kFusedTiles;
+    const size_t mat_ints = fused ? static_cast<size_t>(n_tiles) * nbt + 2 * (n_tiles + 1) + 64
+                                  : radix_sort_work_ints(static_cast<int>(E));
+    RXGS_CUDA(ctx->scratch_b.ensure(o_w + 4 * mat_ints));
+    char* pb = ctx->scratch_b.as<char>();
+    uint32_t* tk = reinterpret_cast<uint32_t*>(pb);
+    int* tv = reinterpret_cast<int*>(pb + o_v);
+    int* mat = reinterpret_cast<int*>(pb + o_w);
+    const size_t sm_e = 4 * (2 * static_cast<size_t>(kTileM) + 2 + (fused ? n_tiles : 0));
+    RXGS_CUDA(cudaFuncSetAttribute(k_emit_entries, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm_e)));
+    if (fused) {
+        int* tot = mat + static_cast<size_t>(n_tiles) * nbt;
         int* tbase = tot + n_tiles + 1;
         unsigned* counter = reinterpret_cast<unsigned*>(tbase + n_tiles + 1);
         RXGS_CUDA(cudaMemsetAsync(counter, 0, 4, s));
-        const size_t sm_h = 4 * (static_cast<size_t>(n_tiles) + 2 * kTileM + 2);
-        const size_t sm_s = 4 * (static_cast<size_t>(n_tiles) + 2 * kTileM + 2) + 2 * static_cast<size_t>(kTileWarps) * n_tiles;
-        RXGS_CUDA(cudaFuncSetAttribute(k_tile_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(sm_h)));
+        k_emit_entries<<<nbt, kTileThreads, sm_e, s>>>(E, nbt, n_tiles, st.grid.tiles_p, st.scan.as<int64_t>(), bfirst,
+                                                       blast, spans_sorted, tk, tv, mat);
+        k_matrix_scan<<<n_tiles, 256, 0, s>>>(n_tiles, nbt, mat, tot, tbase, counter);
+        const size_t sm_s = 4 * static_cast<size_t>(n_tiles) + 2 * static_cast<size_t>(kTileWarps) * n_tiles;
         RXGS_CUDA(cudaFuncSetAttribute(k_tile_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sm_s)));
-        k_tile_hist<<<nbt, kTileThreads, sm_h, s>>>(K, E, nbt, n_tiles, st.grid.tiles_p, st.scan.as<int64_t>(),
-                                                    bfirst, blast, spans_sorted, mat);
-        k_matrix_scan<<<n_tiles, 256, 0, s>>>(n_tiles, nbt, mat, tot, tbase, counter);
-        k_tile_scatter<<<nbt, kTileThreads, sm_s, s>>>(K, E, nbt, n_tiles, st.grid.tiles_p, st.scan.as<int64_t>(),
-                                                       bfirst, blast, spans_sorted, st.order.as<int>(), mat, tbase,
+        k_tile_scatter<<<nbt, kTileThreads, sm_s, s>>>(E, nbt, n_tiles, tk, tv, st.order.as<int>(), mat, tbase,
                                                        st.list.as<int>(), st.keys.as<uint64_t>(),
                                                        st.tile_offsets.as<int64_t>());
     } else {
-        // generic: (tile, rank) pairs, LSD passes on the tile id, then lists / keys / offsets
+        // generic: LSD passes on the tile id, then lists / keys / offsets
         const int En = static_cast<int>(E);
-        const size_t o_v = al256(4 * (E + 1)), o_kt = o_v + al256(4 * (E + 1)), o_vt = o_kt + al256(4 * (E + 1)),
-                     o_w = o_vt + al256(4 * (E + 1));
-        RXGS_CUDA(ctx->scratch_b.ensure(o_w + 4 * radix_sort_work_ints(En)));
-        char* pb = ctx->scratch_b.as<char>();
-        uint32_t* tk = reinterpret_cast<uint32_t*>(pb);
-        int* tv = reinterpret_cast<int*>(pb + o_v);
-        int* w2 = reinterpret_cast<int*>(pb + o_w);
-        RXGS_CUDA(cudaMemsetAsync(w2, 0, 4 * radix_sort_work_ints(En), s));
-        RXGS_CUDA(cudaFuncSetAttribute(k_emit_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       4 * (2 * kTileM + 2)));
-        k_emit_pairs<<<nbt, kTileThreads, 4 * (2 * kTileM + 2), s>>>(K, E, st.grid.tiles_p, st.scan.as<int64_t>(), bfirst,
-                                                                      blast, spans_sorted, tk, tv);
+        RXGS_CUDA(cudaMemsetAsync(mat, 0, 4 * mat_ints, s));
+        k_emit_entries<<<nbt, kTileThreads, sm_e, s>>>(E, nbt, n_tiles, st.grid.tiles_p, st.scan.as<int64_t>(), bfirst,
+                                                       blast, spans_sorted, tk, tv, nullptr);
         RXGS_CUDA(radix_sort_pairs(En, bits_for(n_tiles), tk, tv, reinterpret_cast<uint32_t*>(pb + o_kt),
-                                   reinterpret_cast<int*>(pb + o_vt), w2, false, s));
+                                   reinterpret_cast<int*>(pb + o_vt), mat, false, s));
         k_pairs_final<<<static_cast<unsigned>((E + 255) / 256), 256, 0, s>>>(E, tk, tv, st.order.as<int>(),
                                                                              st.list.as<int>(),
                                                                              st.keys.as<uint64_t>());

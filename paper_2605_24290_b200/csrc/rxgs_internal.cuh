@@ -263,6 +263,11 @@ cudaError_t launch_fle_eval(int what, int n, int l_max, const double* a, const d
                             double* out, cudaStream_t s);
 constexpr int kApiMaxLmax = 24;
 // ---- k_refapi.cu (FP64 single-call API kernels)
+// located non-finite check of n coefficients, rows of per_row (k_cond.cu)
+cudaError_t launch_check_finite(long long n, long long per_row, const double* d_coeffs, int* d_err, cudaStream_t s);
+// materialised render_field, FP64 signals and walk (k_refapi.cu)
+cudaError_t launch_render64(const rxgs_txstate_s& st, const double* d_co, int n_rx, double2* d_sig, double* values,
+                            double* tout, cudaStream_t s);
 cudaError_t launch_blend_ray(int n, const double* w, const double* sig, double* out, cudaStream_t s);
 cudaError_t launch_occ_sample(int R, const double* lo, const double* hi, const double* dens, int n, const double* pts,
                               int nearest, double* out, cudaStream_t s);
