@@ -8,9 +8,14 @@
 //   sphraster.hpp:15-133   SphericalGrid, ProjectedGaussian, TxState,
 //                          build_tx_state, bin_and_sort, RenderedField,
 //                          render_field (x2), Measurement, aggregate_modality
+//   sphraster.hpp:46,60,82 project_gaussian, TxState::hash, blend_ray
 //   conditioning.hpp:13-123 MlpLayer, Mlp, OccupancyGrid, ConditioningConfig,
-//                          ConditioningState, build_occupancy,
+//                          ConditioningState, init_conditioning,
+//                          probe_segment, fourier_encode, build_occupancy,
 //                          condition_forward, condition_batch
+//   radiance.hpp:66        fle::eval_basis (+ normalization, eval_radiance)
+// For a link-level drop-in that keeps the reference's own headers, see
+// paper_2605_24290_b200/refapi (librxgs_refapi.so).
 //   trainer.hpp:42-50      Model, predict
 // Usage: include this header instead of the reference headers and link
 // librxgs_b200.so.  Define RXGS_B200_AS_RXGS to expose everything as
@@ -198,6 +203,42 @@ inline double ssim(const std::vector<double>& pred, const std::vector<double>& g
 }
 }  // namespace met
 
+namespace fle {  // radiance.hpp:36-70, evaluated on the device in FP64
+
+struct BasisValues {
+    int l_max = 0;
+    std::vector<cplx> b;
+    const cplx& at(int comp) const { return b[static_cast<std::size_t>(comp)]; }
+};
+
+// eval_basis (radiance.hpp:66, radiance.cpp:79-92)
+inline BasisValues eval_basis(double theta, double phi, int l_max) {
+    const int L = component_count(l_max);
+    std::vector<double> o(2 * static_cast<std::size_t>(L));
+    detail::check(rxgs_fle_eval(detail::ctx(), 0, l_max, 1, &theta, &phi, nullptr, o.data()));
+    BasisValues r;
+    r.l_max = l_max;
+    for (int i = 0; i < L; ++i) r.b.push_back(cplx{o[2 * i], o[2 * i + 1]});
+    return r;
+}
+
+// normalization (radiance.cpp:9-14)
+inline double normalization(int l, int m) {
+    const double a = l, b = m;
+    double o = 0.0;
+    detail::check(rxgs_fle_eval(detail::ctx(), 4, 0, 1, &a, &b, nullptr, &o));
+    return o;
+}
+
+// eval_radiance (radiance.cpp:116-125): coeffs L complex
+inline cplx eval_radiance(const double* coeffs, double theta, double phi, int l_max) {
+    double o[2];
+    detail::check(rxgs_fle_eval(detail::ctx(), 5, l_max, 1, &theta, &phi, coeffs, o));
+    return cplx{o[0], o[1]};
+}
+
+}  // namespace fle
+
 namespace raster {
 
 inline constexpr double kWeightClamp = 0.999;
@@ -235,7 +276,90 @@ struct TxState {  // sphraster.hpp:52-61 (materialised from the device)
     std::vector<std::vector<int>> tile_lists;
     std::vector<cplx> basis;
     std::shared_ptr<detail::TxHandle> device;  // B200 state (lists, blend weights)
+    // TxState::hash (sphraster.hpp:60, sphraster.cpp:121-148): FNV-1a over the
+    // same fields in the same order and byte widths as the reference
+    uint64_t hash() const {
+        uint64_t h = 0xcbf29ce484222325ull;
+        auto bytes = [&h](const void* d, std::size_t n) {
+            const auto* p = static_cast<const unsigned char*>(d);
+            for (std::size_t i = 0; i < n; ++i) {
+                h ^= p[i];
+                h *= 0x100000001b3ull;
+            }
+        };
+        auto val = [&bytes](const auto& v) { bytes(&v, sizeof(v)); };
+        val(grid.n_theta);
+        val(grid.n_phi);
+        val(grid.tile_size);
+        val(grid.radius);
+        val(k);
+        val(l_max);
+        for (const auto& pg : proj) {
+            val(pg.culled);
+            if (pg.culled) continue;
+            val(pg.theta);
+            val(pg.phi);
+            val(pg.depth);
+            val(pg.angular_cov);
+            val(pg.weight_scale);
+            val(pg.t0);
+            val(pg.t1);
+            val(pg.p0);
+            val(pg.p1);
+        }
+        for (const auto& list : tile_lists) {
+            val(list.size());
+            for (const int idx : list) val(idx);
+        }
+        bytes(basis.data(), basis.size() * sizeof(cplx));
+        return h;
+    }
 };
+
+// project_gaussian (sphraster.hpp:46, sphraster.cpp:22-83) on the device
+// (FP64, the k_tx_prep arithmetic).  cov3: row-major 3x3.
+inline ProjectedGaussian project_gaussian(const Vec3& position, const std::array<double, 9>& cov3, double tau,
+                                          const Vec3& tx, const SphericalGrid& grid) {
+    const double p[3] = {position.x, position.y, position.z}, t[3] = {tx.x, tx.y, tx.z};
+    double g[12];
+    int32_t culled = 1, sp[4];
+    const rxgs_grid gc = grid.c();
+    detail::check(rxgs_project_gaussians(detail::ctx(), 1, p, cov3.data(), &tau, t, &gc, g, &culled, sp));
+    ProjectedGaussian o;
+    o.culled = culled != 0;
+    o.theta = g[0];
+    o.phi = g[1];
+    o.depth = g[2];
+    o.angular_cov = {g[3], g[4], g[5], g[6]};
+    o.angular_prec = {g[7], g[8], g[9], g[10]};
+    o.weight_scale = g[11];
+    o.t0 = sp[0];
+    o.t1 = sp[1];
+    o.p0 = sp[2];
+    o.p1 = sp[3];
+    return o;
+}
+
+struct BlendResult {  // sphraster.hpp:77-80
+    cplx c{0.0, 0.0};
+    double transmittance = 1.0;
+};
+
+// blend_ray (sphraster.hpp:82, sphraster.cpp:174-185) on the device
+inline BlendResult blend_ray(const std::vector<double>& weights, const std::vector<cplx>& signals) {
+    if (weights.size() != signals.size()) throw std::invalid_argument("blend_ray: weights/signals size mismatch");
+    std::vector<double> sg(2 * signals.size());
+    for (std::size_t i = 0; i < signals.size(); ++i) {
+        sg[2 * i] = signals[i].real();
+        sg[2 * i + 1] = signals[i].imag();
+    }
+    double o[3];
+    detail::check(rxgs_blend_ray(detail::ctx(), static_cast<int>(weights.size()), weights.data(), sg.data(), o));
+    BlendResult r;
+    r.c = cplx{o[0], o[1]};
+    r.transmittance = o[2];
+    return r;
+}
 
 inline TxState build_tx_state(const GaussianScene& scene, const Vec3& tx, const SphericalGrid& grid) {
     auto th = std::make_shared<detail::TxHandle>();
@@ -498,6 +622,74 @@ inline std::unique_ptr<CondHandle> upload(const ConditioningState& s) {
     return h;
 }
 }  // namespace detail_c
+
+struct ProbeResult {  // conditioning.hpp:44-47
+    double transmittance = 1.0;
+    double mean_density = 0.0;
+};
+
+// probe_segment (conditioning.hpp:50, conditioning.cpp:163-178) on the device, FP64
+inline ProbeResult probe_segment(const OccupancyGrid& grid, const Vec3& from, const Vec3& to, int samples,
+                                 bool nearest_lookup = false) {
+    if (samples < 1) throw std::invalid_argument("probe_segment: samples must be >= 1");
+    const double lo[3] = {grid.bounds.lo.x, grid.bounds.lo.y, grid.bounds.lo.z};
+    const double hi[3] = {grid.bounds.hi.x, grid.bounds.hi.y, grid.bounds.hi.z};
+    const double f[3] = {from.x, from.y, from.z}, t[3] = {to.x, to.y, to.z};
+    double o[2];
+    api::detail::check(rxgs_probe_grid(api::detail::ctx(), grid.resolution, lo, hi,
+                                       grid.empty() ? nullptr : grid.densities.data(), 1, f, t, samples,
+                                       nearest_lookup ? 1 : 0, o));
+    return {o[0], o[1]};
+}
+
+// init_conditioning (conditioning.hpp:93, conditioning.cpp:217-253): the
+// reference's derive_stream initialisation (rxgs_synth_cond, randomize = 0)
+inline ConditioningState init_conditioning(const ConditioningConfig& config, int l_max, int channels,
+                                           const Aabb& scene_bounds, uint64_t seed) {
+    if (config.fourier_bands < 1 || config.hidden < 1 || config.embed_dim < 1)
+        throw std::invalid_argument("init_conditioning: bad dimensions");
+    const int32_t cfg[9] = {config.fourier_bands, config.hidden, config.embed_dim, config.probe_samples,
+                            config.occupancy_resolution, config.nearest_lookup ? 1 : 0,
+                            static_cast<int32_t>(config.mode), l_max, channels};
+    const double lo[3] = {scene_bounds.lo.x, scene_bounds.lo.y, scene_bounds.lo.z};
+    const double hi[3] = {scene_bounds.hi.x, scene_bounds.hi.y, scene_bounds.hi.z};
+    std::vector<double> p(static_cast<std::size_t>(rxgs_synth_cond(cfg, l_max, channels, lo, hi, seed, 0, nullptr)));
+    rxgs_synth_cond(cfg, l_max, channels, lo, hi, seed, 0, p.data());
+    ConditioningState s;
+    s.config = config;
+    s.l_max = l_max;
+    s.channels = channels;
+    const int F = config.fourier_bands, d = config.hidden, dc = config.embed_dim;
+    const double* q = p.data();
+    auto take = [&q](std::vector<double>& v, std::size_t n) {
+        v.assign(q, q + n);
+        q += n;
+    };
+    auto layer = [&take](MlpLayer& l, int in, int out) {
+        l.in = in;
+        l.out = out;
+        take(l.w, static_cast<std::size_t>(in) * out);
+        take(l.b, static_cast<std::size_t>(out));
+    };
+    take(s.fourier_freqs, 3 * static_cast<std::size_t>(F));
+    layer(s.global_mlp.l1, 6 * F + 2 + dc, d);
+    layer(s.global_mlp.l2, d, d);
+    layer(s.global_mlp.l3, d, 4 * channels);
+    take(s.component_embed, static_cast<std::size_t>(api::component_count(l_max)) * dc);
+    layer(s.local_mlp.l1, 6, d);
+    layer(s.local_mlp.l2, d, d);
+    layer(s.local_mlp.l3, d, 4 * channels);
+    return s;
+}
+
+// fourier_encode (conditioning.cpp:255-265) on the device
+inline std::vector<double> fourier_encode(const Vec3& r, const std::vector<double>& freqs) {
+    const int F = static_cast<int>(freqs.size() / 3);
+    std::vector<double> out(6 * static_cast<std::size_t>(F));
+    const double rv[3] = {r.x, r.y, r.z};
+    api::detail::check(rxgs_fourier_encode(api::detail::ctx(), F, freqs.data(), 1, rv, out.data()));
+    return out;
+}
 
 inline OccupancyGrid build_occupancy(const GaussianScene& scene, int resolution, const Aabb& bounds) {
     auto sh = api::detail::upload(scene);

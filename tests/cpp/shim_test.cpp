@@ -356,6 +356,56 @@ int main() {
         }
         CHECK(threw);
     }
+    {  // project_gaussian: isotropic sigma^2/d^2 (test_sphraster.cpp:68-77), culling (:88-94)
+        const std::array<double, 9> cov = {0.04, 0, 0, 0, 0.04, 0, 0, 0, 0.04};
+        const auto pg = project_gaussian({0, 2, 0}, cov, 0.5, {0, 0, 0}, small_grid());
+        CHECK(!pg.culled);
+        CHECK(rel_err(pg.angular_cov.a, 0.04 / 4.0) < 1e-12);
+        CHECK(rel_err(pg.angular_cov.d, 0.04 / 4.0) < 1e-12);
+        CHECK(std::abs(pg.angular_cov.b) < 1e-15);
+        CHECK(project_gaussian({0.1, 0, 0}, cov, 0.5, {0, 0, 0}, small_grid()).culled);
+    }
+    {  // blend_ray closed forms (test_sphraster.cpp:134-142)
+        const auto one = blend_ray({0.5}, {cplx{1, 0}});
+        CHECK(one.c == cplx(0.5, 0.0) && one.transmittance == 0.5);
+        const auto two = blend_ray({0.5, 0.25}, {cplx{1, 0}, cplx{2, 0}});
+        CHECK(rel_err(two.c.real(), 0.75) < 1e-15 && rel_err(two.transmittance, 0.375) < 1e-15);
+    }
+    {  // TxState::hash is receiver-invariant (test_sphraster.cpp:225-237)
+        const auto scene = random_scene(47, 5, 2, 1);
+        const auto s1 = build_tx_state(scene, {0, 0, 0}, small_grid());
+        const auto s2 = build_tx_state(scene, {0, 0, 0}, small_grid());
+        CHECK(s1.hash() == s2.hash());
+        const auto s3 = build_tx_state(scene, {0.1, 0, 0}, small_grid());
+        CHECK(s1.hash() != s3.hash());
+    }
+    {  // probe_segment 0.9^16 (test_conditioning.cpp:114-133), init_conditioning ladder (:67-76)
+        cond::OccupancyGrid u;
+        u.resolution = 4;
+        u.bounds = {{-10, -10, -10}, {10, 10, 10}};
+        u.densities.assign(64, 0.1);
+        const auto pr = cond::probe_segment(u, {-5, 0, 0}, {5, 0, 0}, 16);
+        CHECK(rel_err(pr.transmittance, std::pow(0.9, 16)) < 1e-12);
+        CHECK(rel_err(pr.mean_density, 0.1) < 1e-12);
+        cond::ConditioningConfig cfg;
+        cfg.fourier_bands = 2;
+        cfg.hidden = 8;
+        cfg.embed_dim = 3;
+        const auto st = cond::init_conditioning(cfg, 1, 1, {{0, 0, 0}, {4, 2, 1}}, 5);
+        CHECK(rel_err(st.fourier_freqs[0], kTwoPi / 4.0) < 1e-15);
+        CHECK(rel_err(st.fourier_freqs[1], kTwoPi / 2.0) < 1e-15);
+        bool zero = true;
+        for (double w : st.local_mlp.l3.w) zero = zero && w == 0.0;
+        CHECK(zero);
+        const auto enc = cond::fourier_encode({0, 0, 0}, std::vector<double>(18, 1.7));
+        CHECK(enc.size() == 36 && enc[0] == 0.0 && enc[1] == 1.0);
+    }
+    {  // fle::eval_basis closed forms (test_radiance.cpp:99-126)
+        const auto b = fle::eval_basis(0.3, 1.1, 1);
+        CHECK(rel_err(b.at(0).real(), 0.2820947917738781) < 1e-15 && b.at(0).imag() == 0.0);
+        CHECK(rel_err(b.at(2).real(), 0.4886025119029199 * std::cos(0.3)) < 1e-14);
+        CHECK(rel_err(fle::normalization(1, 0), 0.4886025119029199) < 1e-15);
+    }
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail ? 1 : 0;
 }
