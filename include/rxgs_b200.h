@@ -198,6 +198,17 @@ int rxgs_reset_transmittance(rxgs_scene scene);
  * the 300 dB sentinel (kDbSentinel); errors carry the reference texts. */
 int rxgs_image_metrics(rxgs_ctx ctx, const void* pred, int pred_f32, const double* gt, int n_img, int h, int w,
                        double max_val, const double ssim_opts[3], double* out);
+/* met::snr_csi (metrics.hpp:33, metrics.cpp:114-125) for n_sets pairs of
+ * len complex values (pred / gt n_sets*len*2 f64): out_db n_sets; identical
+ * inputs give the 300 dB sentinel; the reference's errors. */
+int rxgs_snr_csi(rxgs_ctx ctx, int n_sets, int64_t len, const double* pred, const double* gt, double* out_db);
+/* met::per_receiver_aggregate (metrics.hpp:35-41, metrics.cpp:127-149) of n
+ * (rx, value) records: per receiver in ascending rx order the mean and the
+ * record count (outputs sized n, *n_unique filled), the mean of those means
+ * and their population stddev. */
+int rxgs_per_receiver_aggregate(rxgs_ctx ctx, int64_t n, const int32_t* rx, const double* values, int32_t* out_rx,
+                                double* out_mean, int64_t* out_count, int32_t* n_unique, double* mean,
+                                double* stddev);
 
 int rxgs_coverage_fraction(rxgs_ctx ctx, const double* table, int64_t tx_count, int64_t cand_count,
                            const int32_t* selected, int n_selected, double threshold_dbm, double* out);

@@ -146,6 +146,9 @@ class Checker:
                 "reset_transmittance": (None, [C.c_void_p]),
                 "image_metrics": (C.c_int, [_dp, _dp, C.c_int, C.c_int, C.c_double, C.c_int, C.c_double,
                                             C.c_double, _dp, C.c_char_p, C.c_int]),
+                "snr_csi": (C.c_int, [_dp, _dp, C.c_long, _dp, C.c_char_p, C.c_int]),
+                "per_receiver_aggregate": (C.c_int, [_ip, _dp, C.c_long, _ip, _dp, _lp, _ip, _dp, _dp, C.c_char_p,
+                                                     C.c_int]),
                 "train_sample": (C.c_int, [C.c_void_p, C.c_void_p, _ip, _dp, _dp, _dp, _dp, C.c_double,
                                            C.c_double, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
                                            C.c_char_p, C.c_int]),
@@ -557,5 +560,37 @@ def _densify(self, h, d_pos_list, extent, thresholds=(2e-4, 0.01, 0.1, 0.8), see
 Checker.scene_arrays = _scene_arrays
 Checker.densify = _densify
 Checker.image_metrics = _image_metrics
+
+
+def _snr_csi(self, pred, gt):
+    """met::snr_csi (metrics.cpp:114-125); pred / gt complex arrays; reference only."""
+    p = np.ascontiguousarray(np.asarray(pred, np.complex128)).view(np.float64)
+    g = np.ascontiguousarray(np.asarray(gt, np.complex128)).view(np.float64)
+    out = np.zeros(1)
+    err = C.create_string_buffer(512)
+    if self._snr_csi(_d(p), _d(g), len(p) // 2, out.ctypes.data_as(_dp), err, 512):
+        raise CheckerError(err.value.decode())
+    return float(out[0])
+
+
+def _per_receiver_aggregate(self, rx, values):
+    """met::per_receiver_aggregate (metrics.cpp:127-149); reference only.
+    Returns (rx ids, means, counts, mean, stddev)."""
+    rx = np.ascontiguousarray(rx, np.int32)
+    v = np.ascontiguousarray(values, np.float64)
+    n = len(rx)
+    o_rx, o_mean, o_cnt = np.zeros(max(n, 1), np.int32), np.zeros(max(n, 1)), np.zeros(max(n, 1), np.int64)
+    nu = np.zeros(1, np.int32)
+    mean, sd = np.zeros(1), np.zeros(1)
+    err = C.create_string_buffer(512)
+    if self._per_receiver_aggregate(_i(rx), _d(v), n, _i(o_rx), _d(o_mean), o_cnt.ctypes.data_as(_lp), _i(nu),
+                                    _d(mean), _d(sd), err, 512):
+        raise CheckerError(err.value.decode())
+    u = int(nu[0])
+    return o_rx[:u], o_mean[:u], o_cnt[:u], float(mean[0]), float(sd[0])
+
+
+Checker.snr_csi = _snr_csi
+Checker.per_receiver_aggregate = _per_receiver_aggregate
 Checker.coverage_fraction = _coverage_fraction
 Checker.greedy_plan = _greedy_plan

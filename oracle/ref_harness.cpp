@@ -784,6 +784,46 @@ int ref_image_metrics(const double* pred, const double* gt, int h, int w, double
     }
 }
 
+// met::snr_csi (metrics.cpp:114-125) of one (pred, gt) pair of n complex.
+int ref_snr_csi(const double* pred, const double* gt, long n, double* out, char* err, int errlen) {
+    try {
+        std::vector<cplx> p(static_cast<std::size_t>(n)), g(static_cast<std::size_t>(n));
+        for (long i = 0; i < n; ++i) {
+            p[i] = cplx{pred[2 * i], pred[2 * i + 1]};
+            g[i] = cplx{gt[2 * i], gt[2 * i + 1]};
+        }
+        *out = met::snr_csi(p, g);
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return 1;
+    }
+}
+
+// met::per_receiver_aggregate (metrics.cpp:127-149): per receiver (ascending
+// rx) the mean and count; *n_unique, *mean, *stddev.
+int ref_per_receiver_aggregate(const int* rx, const double* values, long n, int* out_rx, double* out_mean,
+                               long* out_count, int* n_unique, double* mean, double* stddev, char* err,
+                               int errlen) {
+    try {
+        std::vector<std::pair<int, double>> rec;
+        for (long i = 0; i < n; ++i) rec.emplace_back(rx[i], values[i]);
+        const auto a = met::per_receiver_aggregate(rec);
+        *n_unique = static_cast<int>(a.per_receiver.size());
+        for (std::size_t i = 0; i < a.per_receiver.size(); ++i) {
+            out_rx[i] = std::get<0>(a.per_receiver[i]);
+            out_mean[i] = std::get<1>(a.per_receiver[i]);
+            out_count[i] = static_cast<long>(std::get<2>(a.per_receiver[i]));
+        }
+        *mean = a.mean;
+        *stddev = a.stddev;
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return 1;
+    }
+}
+
 // FLE basis (radiance.cpp:79-92) at one direction, out L complex (2L f64).
 void ref_eval_basis(double theta, double phi, int l_max, double* out) {
     const auto b = fle::eval_basis(theta, phi, l_max);

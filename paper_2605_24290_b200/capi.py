@@ -108,6 +108,8 @@ _SIG = {
     "rxgs_render_queries": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp]),
     "rxgs_coverage_table": (C.c_int, [_vp, _vp, _vp, C.POINTER(Grid), _vp, C.c_int, _vp, C.c_int, _vp]),
     "rxgs_predict": (C.c_int, [_vp, _vp, _vp, C.POINTER(Grid), _vp, _vp, _vp]),
+    "rxgs_snr_csi": (C.c_int, [_vp, C.c_int, C.c_int64, _vp, _vp, _vp]),
+    "rxgs_per_receiver_aggregate": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "rxgs_project_gaussians": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp, C.POINTER(Grid), _vp, _vp, _vp]),
     "rxgs_fle_eval": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp]),
     "rxgs_blend_ray": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp]),
@@ -336,6 +338,30 @@ class Context:
         _check(_lib.rxgs_image_metrics(self.h, ptr(pred), int(f32), ptr(gt), n, int(h), int(w), float(max_val),
                                        opts.ctypes.data, out.ctypes.data))
         return out
+
+    def snr_csi(self, pred, gt):
+        """met::snr_csi (metrics.cpp:114-125) per row of complex (n_sets, len) arrays -> dB."""
+        p = np.ascontiguousarray(np.atleast_2d(np.asarray(pred, np.complex128)))
+        g = np.ascontiguousarray(np.atleast_2d(np.asarray(gt, np.complex128)))
+        if p.shape != g.shape:
+            raise InvalidArgument(RXGS_ERR_INVALID, "snr_csi: need equal non-empty inputs")
+        out = np.empty(p.shape[0])
+        _check(_lib.rxgs_snr_csi(self.h, p.shape[0], p.shape[1], p.ctypes.data, g.ctypes.data, out.ctypes.data))
+        return out
+
+    def per_receiver_aggregate(self, rx, values):
+        """met::per_receiver_aggregate (metrics.cpp:127-149) -> (rx, means, counts, mean, stddev)."""
+        rx = np.ascontiguousarray(rx, np.int32)
+        v = np.ascontiguousarray(values, np.float64)
+        n = len(rx)
+        o_rx, o_m, o_c = np.empty(max(n, 1), np.int32), np.empty(max(n, 1)), np.empty(max(n, 1), np.int64)
+        nu = C.c_int32(0)
+        mu, sd = C.c_double(0), C.c_double(0)
+        _check(_lib.rxgs_per_receiver_aggregate(self.h, n, rx.ctypes.data, v.ctypes.data, o_rx.ctypes.data,
+                                                o_m.ctypes.data, o_c.ctypes.data, C.byref(nu), C.byref(mu),
+                                                C.byref(sd)))
+        u = nu.value
+        return o_rx[:u], o_m[:u], o_c[:u], mu.value, sd.value
 
     def bin_and_sort(self, culled, depth, spans, grid: Grid):
         k = len(culled)

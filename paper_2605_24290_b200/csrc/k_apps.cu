@@ -8,6 +8,9 @@
 //   k_cover_count  transmitters covered by a selection (coverage_fraction)
 //   k_greedy       one CTA runs every round: gains = popcount(bits & ~covered),
 //                  argmax with the lowest index on ties, covered |= bits[best]
+#include <cmath>
+#include <climits>
+
 #include "rxgs_internal.cuh"
 
 namespace rxgs_b200 {
@@ -81,6 +84,75 @@ __global__ void __launch_bounds__(kGreedyThreads) k_greedy(int64_t cand, int wor
         for (int w = tid; w < words; w += blockDim.x) covered[w] |= bits[static_cast<int64_t>(pick) * words + w];
         __syncthreads();
     }
+}
+
+// met::snr_csi (metrics.cpp:114-125) per set: err = sum |p - g|^2, sig =
+// sum |g|^2 in a fixed order (per-thread strided sums, then a fixed tree).
+__global__ void k_snr_csi(int64_t len, const double* __restrict__ pred, const double* __restrict__ gt,
+                          double* __restrict__ es) {
+    __shared__ double se[256], ss[256];
+    const double* p = pred + static_cast<size_t>(blockIdx.x) * 2 * len;
+    const double* g = gt + static_cast<size_t>(blockIdx.x) * 2 * len;
+    double e = 0.0, sg = 0.0;
+    for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
+        const double dr = p[2 * i] - g[2 * i], di = p[2 * i + 1] - g[2 * i + 1];
+        e += dr * dr + di * di;  // std::norm
+        sg += g[2 * i] * g[2 * i] + g[2 * i + 1] * g[2 * i + 1];
+    }
+    se[threadIdx.x] = e;
+    ss[threadIdx.x] = sg;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            se[threadIdx.x] += se[threadIdx.x + o];
+            ss[threadIdx.x] += ss[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        es[2 * blockIdx.x] = se[0];
+        es[2 * blockIdx.x + 1] = ss[0];
+    }
+}
+
+// met::per_receiver_aggregate (metrics.cpp:127-149) on records sorted by
+// receiver (stable: input order within a receiver): head[i] marks the first
+// record of a receiver; its thread sums that receiver's values in input
+// order (as the reference's map slots do).
+__global__ void k_rx_heads(int64_t n, const uint32_t* __restrict__ key, int64_t* __restrict__ head) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) head[i] = (i == 0 || key[i] != key[i - 1]) ? 1 : 0;
+    else if (i == n) head[i] = 0;
+}
+
+__global__ void k_rx_segments(int64_t n, const uint32_t* __restrict__ key, const int* __restrict__ idx,
+                              const double* __restrict__ v, const int64_t* __restrict__ seg,
+                              int32_t* __restrict__ out_rx, double* __restrict__ out_mean,
+                              int64_t* __restrict__ out_count) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n || (i > 0 && key[i] == key[i - 1])) return;
+    double sum = 0.0;
+    int64_t c = 0;
+    for (int64_t q = i; q < n && key[q] == key[i]; ++q, ++c) sum += v[idx[q]];
+    const int64_t u = seg[i];
+    out_rx[u] = static_cast<int32_t>(key[i] ^ 0x80000000u);
+    out_mean[u] = sum / static_cast<double>(c);
+    out_count[u] = c;
+}
+
+// mean of the per-receiver means and their population stddev, in receiver order
+__global__ void k_rx_moments(int64_t m, const double* __restrict__ means, double* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double mu = 0.0;
+    for (int64_t i = 0; i < m; ++i) mu += means[i];
+    mu /= static_cast<double>(m);
+    double var = 0.0;
+    for (int64_t i = 0; i < m; ++i) {
+        const double d = means[i] - mu;
+        var += d * d;
+    }
+    out[0] = mu;
+    out[1] = sqrt(var / static_cast<double>(m));
 }
 
 }  // namespace
@@ -203,6 +275,103 @@ int rxgs_image_metrics(rxgs_ctx ctx, const void* pred, int pred_f32, const doubl
     RXGS_CUDA(cudaMemcpyAsync(out, t_out.p, sizeof(double) * 4 * n_img, cudaMemcpyDefault, s));
     RXGS_CUDA(cudaStreamSynchronize(s));
     ctx->launches += win > 0 ? 5 : 2;
+    return RXGS_OK;
+}
+
+int rxgs_snr_csi(rxgs_ctx ctx, int n_sets, int64_t len, const double* pred, const double* gt, double* out_db) {
+    if (!ctx || n_sets < 0 || (n_sets && (!pred || !gt || !out_db))) return fail(RXGS_ERR_INVALID, "snr_csi: null argument");
+    if (n_sets == 0) return RXGS_OK;
+    if (len < 1) return fail(RXGS_ERR_INVALID, "snr_csi: need equal non-empty inputs");
+    RXGS_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const size_t n = static_cast<size_t>(n_sets) * 2 * len;
+    DevBuf tp, tg, te;
+    const double* dp = pred;
+    const double* dg = gt;
+    if (!dev_ptr(pred)) {
+        RXGS_CUDA(tp.ensure(n * 8));
+        RXGS_CUDA(cudaMemcpyAsync(tp.p, pred, n * 8, cudaMemcpyHostToDevice, s));
+        dp = tp.as<double>();
+    }
+    if (!dev_ptr(gt)) {
+        RXGS_CUDA(tg.ensure(n * 8));
+        RXGS_CUDA(cudaMemcpyAsync(tg.p, gt, n * 8, cudaMemcpyHostToDevice, s));
+        dg = tg.as<double>();
+    }
+    RXGS_CUDA(te.ensure(16 * static_cast<size_t>(n_sets)));
+    k_snr_csi<<<n_sets, 256, 0, s>>>(len, dp, dg, te.as<double>());
+    std::vector<double> es(2 * static_cast<size_t>(n_sets));
+    RXGS_CUDA(cudaMemcpyAsync(es.data(), te.p, es.size() * 8, cudaMemcpyDeviceToHost, s));
+    RXGS_CUDA(cudaStreamSynchronize(s));
+    ctx->launches += 1;
+    std::vector<double> db(static_cast<size_t>(n_sets));
+    for (int i = 0; i < n_sets; ++i) {
+        const double err = es[2 * i], sig = es[2 * i + 1];
+        if (sig == 0.0) return fail(RXGS_ERR_INVALID, "snr_csi: zero ground-truth energy");
+        db[i] = err == 0.0 ? 300.0 : -10.0 * std::log10(err / sig);  // kDbSentinel
+    }
+    RXGS_CUDA(cudaMemcpy(out_db, db.data(), db.size() * 8, cudaMemcpyDefault));
+    return RXGS_OK;
+}
+
+int rxgs_per_receiver_aggregate(rxgs_ctx ctx, int64_t n, const int32_t* rx, const double* values, int32_t* out_rx,
+                                double* out_mean, int64_t* out_count, int32_t* n_unique, double* mean,
+                                double* stddev) {
+    if (!ctx) return fail(RXGS_ERR_INVALID, "per_receiver_aggregate: null argument");
+    if (n < 1) return fail(RXGS_ERR_INVALID, "per_receiver_aggregate: no records");
+    if (!rx || !values || n > INT32_MAX) return fail(RXGS_ERR_INVALID, "per_receiver_aggregate: bad argument");
+    RXGS_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const int nn = static_cast<int>(n);
+    std::vector<int32_t> hrx(static_cast<size_t>(n));
+    RXGS_CUDA(cudaMemcpy(hrx.data(), rx, 4 * n, cudaMemcpyDefault));
+    std::vector<uint32_t> key(static_cast<size_t>(n));
+    std::vector<int> idx(static_cast<size_t>(n));
+    for (int i = 0; i < nn; ++i) {
+        key[i] = static_cast<uint32_t>(hrx[i]) ^ 0x80000000u;  // signed order
+        idx[i] = i;
+    }
+    const size_t wi = radix_sort_work_ints(nn);
+    DevBuf buf;
+    const size_t o_k = 0, o_v = 4 * (n + 1), o_kt = o_v + 4 * (n + 1), o_vt = o_kt + 4 * (n + 1),
+                 o_w = o_vt + 4 * (n + 1), o_val = o_w + 4 * wi + 256, o_seg = o_val + 8 * (n + 1),
+                 o_bs = o_seg + 8 * (n + 2), o_rx = o_bs + 8 * (n / 2048 + 2), o_mean = o_rx + 4 * (n + 1),
+                 o_cnt = o_mean + 8 * (n + 1), o_mom = o_cnt + 8 * (n + 1);
+    RXGS_CUDA(buf.ensure(o_mom + 64));
+    char* b = buf.as<char>();
+    auto K = reinterpret_cast<uint32_t*>(b + o_k);
+    auto V = reinterpret_cast<int*>(b + o_v);
+    auto W = reinterpret_cast<int*>(b + o_w);
+    auto VAL = reinterpret_cast<double*>(b + o_val);
+    auto SEG = reinterpret_cast<int64_t*>(b + o_seg);
+    RXGS_CUDA(cudaMemcpyAsync(K, key.data(), 4 * n, cudaMemcpyHostToDevice, s));
+    RXGS_CUDA(cudaMemcpyAsync(V, idx.data(), 4 * n, cudaMemcpyHostToDevice, s));
+    RXGS_CUDA(cudaMemcpyAsync(VAL, values, 8 * n, cudaMemcpyDefault, s));
+    RXGS_CUDA(cudaMemsetAsync(W, 0, 4 * wi, s));
+    RXGS_CUDA(radix_sort_pairs(nn, 32, K, V, reinterpret_cast<uint32_t*>(b + o_kt), reinterpret_cast<int*>(b + o_vt),
+                               W, false, s));
+    const unsigned g = static_cast<unsigned>((n + 1 + 255) / 256);
+    k_rx_heads<<<g, 256, 0, s>>>(n, K, SEG);
+    RXGS_CUDA(scan_i64(n + 1, SEG, SEG, reinterpret_cast<int64_t*>(b + o_bs), s));
+    auto ORX = reinterpret_cast<int32_t*>(b + o_rx);
+    auto OM = reinterpret_cast<double*>(b + o_mean);
+    auto OC = reinterpret_cast<int64_t*>(b + o_cnt);
+    k_rx_segments<<<g, 256, 0, s>>>(n, K, V, VAL, SEG, ORX, OM, OC);
+    int64_t m = 0;
+    RXGS_CUDA(cudaMemcpyAsync(&m, SEG + n, 8, cudaMemcpyDeviceToHost, s));
+    RXGS_CUDA(cudaStreamSynchronize(s));
+    auto MOM = reinterpret_cast<double*>(b + o_mom);
+    k_rx_moments<<<1, 32, 0, s>>>(m, OM, MOM);
+    double mom[2];
+    RXGS_CUDA(cudaMemcpyAsync(mom, MOM, 16, cudaMemcpyDeviceToHost, s));
+    RXGS_CUDA(cudaStreamSynchronize(s));
+    ctx->launches += 12;
+    if (out_rx) RXGS_CUDA(cudaMemcpy(out_rx, ORX, 4 * m, cudaMemcpyDefault));
+    if (out_mean) RXGS_CUDA(cudaMemcpy(out_mean, OM, 8 * m, cudaMemcpyDefault));
+    if (out_count) RXGS_CUDA(cudaMemcpy(out_count, OC, 8 * m, cudaMemcpyDefault));
+    if (n_unique) *n_unique = static_cast<int32_t>(m);
+    if (mean) *mean = mom[0];
+    if (stddev) *stddev = mom[1];
     return RXGS_OK;
 }
 

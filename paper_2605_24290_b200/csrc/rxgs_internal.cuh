@@ -262,6 +262,13 @@ cudaError_t launch_project(int n, const double* pos, const double* cov, const do
 cudaError_t launch_fle_eval(int what, int n, int l_max, const double* a, const double* b, const double* coeffs,
                             double* out, cudaStream_t s);
 constexpr int kApiMaxLmax = 24;
+// ---- k_sort.cu helpers: stable LSD radix sort of (u32 key, int) pairs on the
+// low `bits` bits (work: radix_sort_work_ints(n) ints, zeroed), exclusive
+// int64 scan (bsum: n / 2048 + 2 int64)
+size_t radix_sort_work_ints(int n);
+cudaError_t radix_sort_pairs(int n, int bits, uint32_t* kin, int* vin, uint32_t* ktmp, int* vtmp, int* work,
+                             bool hist_ready, cudaStream_t s);
+cudaError_t scan_i64(int64_t n, const int64_t* in, int64_t* out, int64_t* bsum, cudaStream_t s);
 // ---- k_refapi.cu (FP64 single-call API kernels)
 // located non-finite check of n coefficients, rows of per_row (k_cond.cu)
 cudaError_t launch_check_finite(long long n, long long per_row, const double* d_coeffs, int* d_err, cudaStream_t s);

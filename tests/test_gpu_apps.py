@@ -115,3 +115,34 @@ def test_image_metrics_on_rendered_spectra(ctx, ref, capi):
         want = ref.image_metrics(spec[j].astype(np.float64), gt[j], 18, 72, 1.0)
         np.testing.assert_allclose(got[j], want, rtol=1e-12, atol=1e-14)
     assert (got[:, 3] > 0.999).all()  # the B200 render agrees with the reference render
+
+
+# ---------------------------------------------------------------- CSI evaluation metrics (metrics.cpp:114-149)
+def test_snr_csi_matches_reference(ctx, ref):
+    rng = np.random.default_rng(7)
+    for n in (1, 4, 1000):
+        g = rng.normal(size=(3, n)) + 1j * rng.normal(size=(3, n))
+        p = g + 0.1 * (rng.normal(size=(3, n)) + 1j * rng.normal(size=(3, n)))
+        got = ctx.snr_csi(p, g)
+        want = [ref.snr_csi(p[i], g[i]) for i in range(3)]
+        assert np.allclose(got, want, rtol=1e-12, atol=0)
+    assert ctx.snr_csi(g, g)[0] == 300.0  # kDbSentinel
+    import oracle as O
+    with pytest.raises(ValueError, match="snr_csi: zero ground-truth energy"):
+        ctx.snr_csi(np.ones((1, 3), complex), np.zeros((1, 3), complex))
+    with pytest.raises(O.CheckerError, match="snr_csi: zero ground-truth energy"):
+        ref.snr_csi(np.ones(3, complex), np.zeros(3, complex))
+
+
+def test_per_receiver_aggregate_matches_reference(ctx, ref):
+    rng = np.random.default_rng(11)
+    for n, n_rx in ((1, 1), (50, 7), (20000, 300)):
+        rx = rng.integers(-5, n_rx, n).astype(np.int32)
+        v = rng.normal(size=n)
+        g_rx, g_m, g_c, g_mu, g_sd = ctx.per_receiver_aggregate(rx, v)
+        w_rx, w_m, w_c, w_mu, w_sd = ref.per_receiver_aggregate(rx, v)
+        assert np.array_equal(g_rx, w_rx) and np.array_equal(g_c, w_c)
+        assert np.array_equal(g_m, w_m)  # per receiver: the same sums in the same order
+        assert abs(g_mu - w_mu) <= 1e-14 * max(1, abs(w_mu)) and abs(g_sd - w_sd) <= 1e-13 * max(1, w_sd)
+    with pytest.raises(ValueError, match="per_receiver_aggregate: no records"):
+        ctx.per_receiver_aggregate(np.zeros(0, np.int32), np.zeros(0))
