@@ -373,7 +373,8 @@ def run_b200(args):
         peak, peak_src = float(pk.get("bf16_tflops", 1590.0)), "measured bf16_tflops (MEASURED_PEAKS.json)"
     roofline = None
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r1_traffic.json")
+    tpath = next((os.path.join(ROOT, "profiles", f"{t}_traffic.json") for t in ("r2", "r1")
+                  if os.path.exists(os.path.join(ROOT, "profiles", f"{t}_traffic.json"))), "")
     if os.path.exists(tpath):  # dram bytes of the same kernel from the committed ncu --set full capture
         traffic = json.load(open(tpath)).get("k_cond_tc", {}).get("dram_bytes_per_launch")
     if cond_n:
@@ -384,7 +385,7 @@ def run_b200(args):
                     "frac": achieved / peak,
                     # with tcgen05 at 3 MMAs per product (bf16x3) the pipe's
                     # usable peak for the same algorithmic FLOP is peak / 3
-                    "frac_of_bf16x3_peak": achieved / (peak / 3.0), "traffic": traffic, "traffic_unit": "bytes per launch (profiles/r1_traffic.json)",
+                    "frac_of_bf16x3_peak": achieved / (peak / 3.0), "traffic": traffic, "traffic_unit": f"bytes per launch ({os.path.relpath(tpath, ROOT) if tpath else 'no capture'})",
                     "kernel": "cond_signal = k_fle_gemm (FLE reduction, tcgen05 GEMM) + k_cond_tc (probe + local MLP on tcgen05 + affine)",
                     "pipe": "tcgen05 bf16x3 (layers 1-2, FLE GEMM) + FP32 SIMT on FFMA2 (probe, layer 3, affine)", "peak_source": peak_src,
                     "flop_per_row": flop_row, "rows_per_launch": per_launch_rows,

@@ -1457,7 +1457,7 @@ int rxgs_coverage_table(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const rxgs_gri
         ctx->launches += 1;
         yc = ctx->ycache.as<float4>();
     }
-    RXGS_CUDA(ctx->signals.ensure(std::max<size_t>(static_cast<size_t>(sc->k) * n_rx, 1) * sizeof(float2)));
+    RXGS_CUDA(ctx->signals.ensure(std::max<size_t>(static_cast<size_t>(sc->k) * ((n_rx + 3) & ~3), 1) * sizeof(float2)));
     // transmitter states are built one ahead on the helper context, so the
     // next state's projection / sort / walk overlap this one's signals and
     // compositing (the builder's host syncs block only its own stream)

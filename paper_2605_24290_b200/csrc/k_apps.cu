@@ -333,10 +333,12 @@ int rxgs_per_receiver_aggregate(rxgs_ctx ctx, int64_t n, const int32_t* rx, cons
     }
     const size_t wi = radix_sort_work_ints(nn);
     DevBuf buf;
-    const size_t o_k = 0, o_v = 4 * (n + 1), o_kt = o_v + 4 * (n + 1), o_vt = o_kt + 4 * (n + 1),
-                 o_w = o_vt + 4 * (n + 1), o_val = o_w + 4 * wi + 256, o_seg = o_val + 8 * (n + 1),
-                 o_bs = o_seg + 8 * (n + 2), o_rx = o_bs + 8 * (n / 2048 + 2), o_mean = o_rx + 4 * (n + 1),
-                 o_cnt = o_mean + 8 * (n + 1), o_mom = o_cnt + 8 * (n + 1);
+    auto al = [](size_t x) { return (x + 255) & ~static_cast<size_t>(255); };
+    const size_t N1 = static_cast<size_t>(n) + 2;
+    const size_t o_k = 0, o_v = al(4 * N1), o_kt = o_v + al(4 * N1), o_vt = o_kt + al(4 * N1),
+                 o_w = o_vt + al(4 * N1), o_val = o_w + al(4 * wi), o_seg = o_val + al(8 * N1),
+                 o_bs = o_seg + al(8 * N1), o_rx = o_bs + al(8 * (N1 / 2048 + 2)), o_mean = o_rx + al(4 * N1),
+                 o_cnt = o_mean + al(8 * N1), o_mom = o_cnt + al(8 * N1);
     RXGS_CUDA(buf.ensure(o_mom + 64));
     char* b = buf.as<char>();
     auto K = reinterpret_cast<uint32_t*>(b + o_k);
