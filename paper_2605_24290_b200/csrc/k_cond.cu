@@ -29,22 +29,26 @@ using namespace cond_dev;
 
 // ------------------------------------------------------------------ global branch (FP64)
 // Persistent CTAs loop over receivers.  Per receiver the Fourier part of
-// layer 1 (the first 6F inputs, shared by all L components) is summed once
-// and each (component, unit) thread continues the same sequential sum over
-// [l/l_max, m/l_max, e_l] -- the reference's summation order
-// (mlp_forward, conditioning.cpp:23-29), so the result is unchanged; W2 is
-// staged transposed in shared memory once per CTA.
+// layer 1 (the first 6F inputs, shared by all L components) is summed once;
+// then the components go through the MLP CP at a time: thread (o, group)
+// carries FOUR components' dot products for output unit o (four independent
+// FP64 chains sharing each weight load -- the chains, not the FLOP count,
+// bound this kernel), and layer 3 splits each (component, output) sum over
+// a few lanes joined by shuffles.  W2 is staged transposed in shared memory
+// once per CTA.  The outputs are rounded to f32 (ag), so the summation order
+// only moves the FP64 rounding, far below that.
 constexpr int kGlobThreads = 256;
+constexpr int kGlobChains = 4;
 
 __global__ void __launch_bounds__(kGlobThreads) k_cond_global(CondDev c, const double* __restrict__ rx, int n_rx,
                                                               float* __restrict__ ag) {
     extern __shared__ double sm[];
-    const int H = c.H, F6 = 6 * c.F, CH = kGlobThreads / H > 0 ? kGlobThreads / H : 1;
-    double* w2t = sm;                  // [i][o]
-    double* gam = w2t + H * H;         // 6F
-    double* pre = gam + F6;            // H
-    double* h1 = pre + H;              // CH x H
-    double* h2 = h1 + CH * H;          // CH x H
+    const int H = c.H, F6 = 6 * c.F, G = kGlobThreads / H, CP = G * kGlobChains;
+    double* w2t = sm;            // [i][o]
+    double* gam = w2t + H * H;   // 6F
+    double* pre = gam + F6;      // H
+    double* h1 = pre + H;        // CP x H
+    double* h2 = h1 + CP * H;    // CP x H
     const double* p = c.p64;
     const int tid = threadIdx.x;
     for (int i = tid; i < H * H; i += blockDim.x) w2t[(i % H) * H + i / H] = p[c.o_gw2 + i];
@@ -52,6 +56,11 @@ __global__ void __launch_bounds__(kGlobThreads) k_cond_global(CondDev c, const d
     while ((l_max + 1) * (l_max + 1) < c.L) ++l_max;
     const double den = l_max > 0 ? static_cast<double>(l_max) : 1.0;  // conditioning.cpp:328
     const int NY = 4 * c.C;
+    const int o = tid % H, grp = tid / H;
+    // layer 3: (component, output) pairs of a pass, TP lanes each (power of two <= 32)
+    const int pairs = CP * NY;
+    int TP = 1;
+    while (TP * 2 <= 32 && pairs * TP * 2 <= kGlobThreads) TP *= 2;
     for (int j = blockIdx.x; j < n_rx; j += gridDim.x) {
         __syncthreads();
         for (int i = tid; i < F6; i += blockDim.x) {  // fourier_encode, conditioning.cpp:255-265
@@ -60,42 +69,58 @@ __global__ void __launch_bounds__(kGlobThreads) k_cond_global(CondDev c, const d
             gam[i] = (i % 2) ? cos(arg) : sin(arg);
         }
         __syncthreads();
-        for (int o = tid; o < H; o += blockDim.x) {
-            double acc = p[c.o_gb1 + o];
-            const double* w = p + c.o_gw1 + static_cast<size_t>(o) * c.gin;
+        for (int oo = tid; oo < H; oo += blockDim.x) {
+            double acc = p[c.o_gb1 + oo];
+            const double* w = p + c.o_gw1 + static_cast<size_t>(oo) * c.gin;
             for (int i = 0; i < F6; ++i) acc += w[i] * gam[i];
-            pre[o] = acc;
+            pre[oo] = acc;
         }
-        for (int c0 = 0; c0 < c.L; c0 += CH) {
+        for (int c0 = 0; c0 < c.L; c0 += CP) {
             __syncthreads();
-            const int cl = tid / H, o = tid % H, comp = c0 + cl;
-            const bool valid = cl < CH && comp < c.L;
-            if (valid) {
-                int l = 0;
-                while ((l + 1) * (l + 1) <= comp) ++l;
-                const int m = comp - l * l - l;
+            if (grp < G) {  // layer 1 tail: [l/l_max, m/l_max, e_l]
                 const double* w = p + c.o_gw1 + static_cast<size_t>(o) * c.gin + F6;
-                double acc = pre[o];
-                acc += w[0] * (l / den);
-                acc += w[1] * (m / den);
-                for (int e = 0; e < c.dc; ++e) acc += w[2 + e] * p[c.o_emb + comp * c.dc + e];
-                h1[cl * H + o] = acc > 0.0 ? acc : 0.0;
+#pragma unroll
+                for (int q = 0; q < kGlobChains; ++q) {
+                    const int cl = grp * kGlobChains + q, comp = c0 + cl;
+                    if (comp >= c.L) break;
+                    int l = 0;
+                    while ((l + 1) * (l + 1) <= comp) ++l;
+                    const int m = comp - l * l - l;
+                    double acc = pre[o];
+                    acc += w[0] * (l / den);
+                    acc += w[1] * (m / den);
+                    for (int e = 0; e < c.dc; ++e) acc += w[2 + e] * p[c.o_emb + comp * c.dc + e];
+                    h1[cl * H + o] = acc > 0.0 ? acc : 0.0;
+                }
             }
             __syncthreads();
-            if (valid) {
-                double acc = p[c.o_gb2 + o];
-                for (int i = 0; i < H; ++i) acc += w2t[i * H + o] * h1[cl * H + i];
-                h2[cl * H + o] = acc > 0.0 ? acc : 0.0;
+            if (grp < G) {  // layer 2: four chains per thread
+                double acc[kGlobChains];
+#pragma unroll
+                for (int q = 0; q < kGlobChains; ++q) acc[q] = p[c.o_gb2 + o];
+                const double* hb = h1 + grp * kGlobChains * H;
+                for (int i = 0; i < H; ++i) {
+                    const double w = w2t[i * H + o];
+#pragma unroll
+                    for (int q = 0; q < kGlobChains; ++q) acc[q] += w * hb[q * H + i];
+                }
+#pragma unroll
+                for (int q = 0; q < kGlobChains; ++q) h2[(grp * kGlobChains + q) * H + o] = acc[q] > 0.0 ? acc[q] : 0.0;
             }
             __syncthreads();
-            for (int t = tid; t < CH * NY; t += blockDim.x) {
-                const int cl3 = t / NY, oo = t % NY, comp3 = c0 + cl3;
-                if (comp3 >= c.L) continue;
-                double acc = p[c.o_gb3 + oo];
+            // layer 3: pair = (component cl, output oo), lanes sub = 0..TP-1 split the sum
+            for (int t = tid; t < pairs * TP; t += blockDim.x) {
+                const int pr = t / TP, sub = t % TP;
+                const int cl = pr / NY, oo = pr % NY, comp = c0 + cl;
                 const double* w = p + c.o_gw3 + static_cast<size_t>(oo) * H;
-                for (int i = 0; i < H; ++i) acc += w[i] * h2[cl3 * H + i];
-                if (c.additive && (oo % 4) < 2) acc = 0.0;
-                ag[(static_cast<size_t>(j) * c.L + comp3) * NY + oo] = static_cast<float>(acc);
+                double acc = 0.0;
+                for (int i = sub; i < H; i += TP) acc += w[i] * h2[cl * H + i];
+                for (int off = 1; off < TP; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, TP);
+                if (sub == 0 && comp < c.L) {
+                    acc += p[c.o_gb3 + oo];
+                    if (c.additive && (oo % 4) < 2) acc = 0.0;
+                    ag[(static_cast<size_t>(j) * c.L + comp) * NY + oo] = static_cast<float>(acc);
+                }
             }
         }
     }
@@ -370,9 +395,10 @@ cudaError_t launch_cond_global(const rxgs_cond_s& c, const double* d_rx, int n_r
     if (n_rx == 0) return cudaSuccess;
     if (!c.use_global()) return cudaMemsetAsync(d_ag, 0, sizeof(float) * n_rx * c.L * 4 * c.C, s);
     const CondDev d = make_dev(c);
-    const int H = c.hidden, CH = kGlobThreads / H > 0 ? kGlobThreads / H : 1;
+    const int H = c.hidden;
     if (H > kGlobThreads) return cudaErrorInvalidValue;
-    const size_t smem = sizeof(double) * (static_cast<size_t>(H) * H + 6 * c.F + H + 2 * CH * H);
+    const int CP = (kGlobThreads / H) * kGlobChains;
+    const size_t smem = sizeof(double) * (static_cast<size_t>(H) * H + 6 * c.F + H + 2 * static_cast<size_t>(CP) * H);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -48,7 +48,8 @@ rep = os.path.join(out, f"{tag}_k_cond_tc.ncu-rep")
 if os.path.exists(rep):
     open(os.path.join(prof, f"{tag}_k_cond_tc_source.txt"), "w").write(source_hotspots(rep))
 
-for k in ["k_cond_tc", "k_fle_gemm", "k_composite_tc", "k_walk", "k_tx_prep", "k_cov_signal", "k_cond_bwd_rows",
+for k in ["k_cond_tc", "k_fle_gemm", "k_composite_tc", "k_walk", "k_tx_prep", "k_cov_signal", "k_tile_scatter",
+          "k_emit_entries", "k_radix_scatter", "k_cond_bwd_rows",
           "k_cond_bwd_grads"]:
     rep = os.path.join(out, f"{tag}_{k}.ncu-rep")
     if not os.path.exists(rep):
