@@ -43,19 +43,34 @@ constexpr int kGlobChains = 4;
 __global__ void __launch_bounds__(kGlobThreads) k_cond_global(CondDev c, const double* __restrict__ rx, int n_rx,
                                                               float* __restrict__ ag) {
     extern __shared__ double sm[];
-    const int H = c.H, F6 = 6 * c.F, G = kGlobThreads / H, CP = G * kGlobChains;
-    double* w2t = sm;            // [i][o]
-    double* gam = w2t + H * H;   // 6F
-    double* pre = gam + F6;      // H
-    double* h1 = pre + H;        // CP x H
-    double* h2 = h1 + CP * H;    // CP x H
+    const int H = c.H, F6 = 6 * c.F, G = kGlobThreads / H, CP = G * kGlobChains, gin = c.gin, NY = 4 * c.C;
+    // every weight of the global MLP staged once per CTA, transposed so a
+    // warp's 32 output units read consecutive words
+    double* w1t = sm;                    // [i][o], gin x H
+    double* w2t = w1t + gin * H;         // [i][o], H x H
+    double* w3 = w2t + H * H;            // [oo][i], NY x H
+    double* emb = w3 + NY * H;           // L x dc
+    double* b1 = emb + c.L * c.dc;       // H
+    double* b2 = b1 + H;                 // H
+    double* b3 = b2 + H;                 // NY
+    double* gam = b3 + NY;               // 6F
+    double* pre = gam + F6;              // H
+    double* h1 = pre + H;                // CP x H
+    double* h2 = h1 + CP * H;            // CP x H
     const double* p = c.p64;
     const int tid = threadIdx.x;
+    for (int i = tid; i < gin * H; i += blockDim.x) w1t[(i % gin) * H + i / gin] = p[c.o_gw1 + i];
     for (int i = tid; i < H * H; i += blockDim.x) w2t[(i % H) * H + i / H] = p[c.o_gw2 + i];
+    for (int i = tid; i < NY * H; i += blockDim.x) w3[i] = p[c.o_gw3 + i];
+    for (int i = tid; i < c.L * c.dc; i += blockDim.x) emb[i] = p[c.o_emb + i];
+    for (int i = tid; i < H; i += blockDim.x) {
+        b1[i] = p[c.o_gb1 + i];
+        b2[i] = p[c.o_gb2 + i];
+    }
+    for (int i = tid; i < NY; i += blockDim.x) b3[i] = p[c.o_gb3 + i];
     int l_max = 0;
     while ((l_max + 1) * (l_max + 1) < c.L) ++l_max;
     const double den = l_max > 0 ? static_cast<double>(l_max) : 1.0;  // conditioning.cpp:328
-    const int NY = 4 * c.C;
     const int o = tid % H, grp = tid / H;
     // layer 3: (component, output) pairs of a pass, TP lanes each (power of two <= 32)
     const int pairs = CP * NY;
@@ -69,16 +84,14 @@ __global__ void __launch_bounds__(kGlobThreads) k_cond_global(CondDev c, const d
             gam[i] = (i % 2) ? cos(arg) : sin(arg);
         }
         __syncthreads();
-        for (int oo = tid; oo < H; oo += blockDim.x) {
-            double acc = p[c.o_gb1 + oo];
-            const double* w = p + c.o_gw1 + static_cast<size_t>(oo) * c.gin;
-            for (int i = 0; i < F6; ++i) acc += w[i] * gam[i];
-            pre[oo] = acc;
+        if (tid < H) {  // the Fourier part of layer 1, shared by every component
+            double acc = b1[tid];
+            for (int i = 0; i < F6; ++i) acc += w1t[i * H + tid] * gam[i];
+            pre[tid] = acc;
         }
         for (int c0 = 0; c0 < c.L; c0 += CP) {
             __syncthreads();
             if (grp < G) {  // layer 1 tail: [l/l_max, m/l_max, e_l]
-                const double* w = p + c.o_gw1 + static_cast<size_t>(o) * c.gin + F6;
 #pragma unroll
                 for (int q = 0; q < kGlobChains; ++q) {
                     const int cl = grp * kGlobChains + q, comp = c0 + cl;
@@ -87,9 +100,9 @@ __global__ void __launch_bounds__(kGlobThreads) k_cond_global(CondDev c, const d
                     while ((l + 1) * (l + 1) <= comp) ++l;
                     const int m = comp - l * l - l;
                     double acc = pre[o];
-                    acc += w[0] * (l / den);
-                    acc += w[1] * (m / den);
-                    for (int e = 0; e < c.dc; ++e) acc += w[2 + e] * p[c.o_emb + comp * c.dc + e];
+                    acc += w1t[F6 * H + o] * (l / den);
+                    acc += w1t[(F6 + 1) * H + o] * (m / den);
+                    for (int e = 0; e < c.dc; ++e) acc += w1t[(F6 + 2 + e) * H + o] * emb[comp * c.dc + e];
                     h1[cl * H + o] = acc > 0.0 ? acc : 0.0;
                 }
             }
@@ -97,7 +110,7 @@ __global__ void __launch_bounds__(kGlobThreads) k_cond_global(CondDev c, const d
             if (grp < G) {  // layer 2: four chains per thread
                 double acc[kGlobChains];
 #pragma unroll
-                for (int q = 0; q < kGlobChains; ++q) acc[q] = p[c.o_gb2 + o];
+                for (int q = 0; q < kGlobChains; ++q) acc[q] = b2[o];
                 const double* hb = h1 + grp * kGlobChains * H;
                 for (int i = 0; i < H; ++i) {
                     const double w = w2t[i * H + o];
@@ -112,12 +125,11 @@ __global__ void __launch_bounds__(kGlobThreads) k_cond_global(CondDev c, const d
             for (int t = tid; t < pairs * TP; t += blockDim.x) {
                 const int pr = t / TP, sub = t % TP;
                 const int cl = pr / NY, oo = pr % NY, comp = c0 + cl;
-                const double* w = p + c.o_gw3 + static_cast<size_t>(oo) * H;
                 double acc = 0.0;
-                for (int i = sub; i < H; i += TP) acc += w[i] * h2[cl * H + i];
+                for (int i = sub; i < H; i += TP) acc += w3[oo * H + i] * h2[cl * H + i];
                 for (int off = 1; off < TP; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, TP);
                 if (sub == 0 && comp < c.L) {
-                    acc += p[c.o_gb3 + oo];
+                    acc += b3[oo];
                     if (c.additive && (oo % 4) < 2) acc = 0.0;
                     ag[(static_cast<size_t>(j) * c.L + comp) * NY + oo] = static_cast<float>(acc);
                 }
@@ -397,15 +409,17 @@ cudaError_t launch_cond_global(const rxgs_cond_s& c, const double* d_rx, int n_r
     const CondDev d = make_dev(c);
     const int H = c.hidden;
     if (H > kGlobThreads) return cudaErrorInvalidValue;
-    const int CP = (kGlobThreads / H) * kGlobChains;
-    const size_t smem = sizeof(double) * (static_cast<size_t>(H) * H + 6 * c.F + H + 2 * static_cast<size_t>(CP) * H);
+    const int CP = (kGlobThreads / H) * kGlobChains, NY = 4 * c.C;
+    const size_t smem = sizeof(double) * (static_cast<size_t>(c.gin) * H + static_cast<size_t>(H) * H + NY * H +
+                                          static_cast<size_t>(c.L) * c.dc + 2 * H + NY + 6 * c.F + H +
+                                          2 * static_cast<size_t>(CP) * H);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaError_t e = cudaFuncSetAttribute(k_cond_global, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
 #ifndef RXGS_GLOB_CTAS_PER_SM
-#define RXGS_GLOB_CTAS_PER_SM 4  // A/B (2, 4, 8): 4 resident CTAs per SM hide the FP64 chains best
+#define RXGS_GLOB_CTAS_PER_SM 2  // weights staged in shared memory (~90 KB at L = 100): 2 CTAs per SM
 #endif
     k_cond_global<<<std::min(n_rx, RXGS_GLOB_CTAS_PER_SM * sms), kGlobThreads, smem, s>>>(d, d_rx, n_rx, d_ag);
     return cudaGetLastError();
