@@ -12,9 +12,14 @@
 // then M = D + sum_l GB_rl, written [j][row] for k_cond_tc's coalesced read
 // (or [row][j] for the coverage signal kernel).
 // tcgen05: 128 rows x 256 columns (128 receivers, re/im) per CTA, K in
-// steps of 16 staged by cp.async into the no-swizzle K-major canonical
-// layout, three shared-memory stages, bf16x3 (Ahi Bhi + Ahi Blo + Alo Bhi,
-// ~2^-17 relative, FP32-class) into a 256-column TMEM accumulator.
+// steps of 16, bf16x3 (Ahi Bhi + Ahi Blo + Alo Bhi, ~2^-17 relative,
+// FP32-class) into a 256-column TMEM accumulator.  The pack kernels write
+// the operands pre-tiled: every (128-row or 256-row block, 16-wide K step)
+// slab is the exact image of the no-swizzle K-major canonical layout, so
+// one thread moves a whole stage (A hi / lo 4 KB each, B hi / lo 8 KB each)
+// with four bulk copies on the TMA engine (cp.async.bulk, completion
+// counted in bytes on the stage's mbarrier) and the MMAs of a stage start
+// as soon as its bytes have landed; three stages in flight.
 #include "rxgs_internal.cuh"
 #include "tc_util.cuh"
 
@@ -30,8 +35,20 @@ constexpr uint32_t kIdesc = tc::idesc_bf16_f32(kTM, kTN);
 __device__ __forceinline__ uint32_t slab_off(int r, int k) {  // K = 16: LBO 128 B, SBO 256 B
     return static_cast<uint32_t>(((r >> 3) * 2 + (k >> 3)) * 128 + (r & 7) * 16 + (k & 7) * 2);
 }
-__device__ __forceinline__ void cp16(uint32_t dst, const void* src, int bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+// element index of (row r, k) in the pre-tiled operand: blocks of `rows`
+// rows, each a run of Kp / 16 slabs (rows x 16 bf16) in the canonical layout
+__device__ __forceinline__ size_t slab_elem(int r, int k, int rows, int Kp) {
+    const size_t slab = static_cast<size_t>(r / rows) * (Kp / kTK) + k / kTK;
+    return slab * rows * kTK + slab_off(r % rows, k % kTK) / 2;
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(bar)), "r"(bytes)
+                 : "memory");
 }
 __device__ __forceinline__ uint16_t bf16_bits(float x) { return static_cast<uint16_t>(tc::pack_bf16(x, 0.f) & 0xFFFFu); }
 __device__ __forceinline__ void split(float x, uint16_t& hi, uint16_t& lo) {
@@ -53,7 +70,7 @@ __global__ void k_fle_pack_a(const int* __restrict__ n_rows, int cap, int L, int
     uint16_t h[4], lo[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) split(v[q], h[q], lo[q]);
-    const size_t o = static_cast<size_t>(r) * Kp + 4 * l;
+    const size_t o = slab_elem(static_cast<int>(r), 4 * l, kTM, Kp);
     *reinterpret_cast<uint2*>(a_hi + o) = make_uint2(h[0] | (uint32_t(h[1]) << 16), h[2] | (uint32_t(h[3]) << 16));
     *reinterpret_cast<uint2*>(a_lo + o) = make_uint2(lo[0] | (uint32_t(lo[1]) << 16), lo[2] | (uint32_t(lo[3]) << 16));
 }
@@ -72,7 +89,7 @@ __global__ void k_fle_pack_b(int n_rx, int L, int Kp, const float4* __restrict__
     uint16_t h[4], lo[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) split(v[q], h[q], lo[q]);
-    const size_t o = static_cast<size_t>(n) * Kp + 4 * l;
+    const size_t o = slab_elem(static_cast<int>(n), 4 * l, kTN, Kp);
     *reinterpret_cast<uint2*>(b_hi + o) = make_uint2(h[0] | (uint32_t(h[1]) << 16), h[2] | (uint32_t(h[3]) << 16));
     *reinterpret_cast<uint2*>(b_lo + o) = make_uint2(lo[0] | (uint32_t(lo[1]) << 16), lo[2] | (uint32_t(lo[3]) << 16));
 }
@@ -83,20 +100,23 @@ __global__ void __launch_bounds__(kThr) k_fle_gemm(const int* __restrict__ n_row
                                                    const float4* __restrict__ rS, float2* __restrict__ Mout,
                                                    int row_major) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t bars[kStages];
+    __shared__ uint64_t bars[kStages];  // MMAs of the stage done (buffer free)
+    __shared__ uint64_t full[kStages];  // the stage's bytes landed
     __shared__ uint32_t tbase_s;
     const int n_rows = *n_rows_dev;
     const int r0 = blockIdx.x * kTM;
     if (r0 >= n_rows) return;
     const int n0 = blockIdx.y * kTN;  // first column (2 j0)
-    const int ncols = 2 * n_rx;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (warp == 0) {
         tc::tmem_alloc(&tbase_s, kTN);
         tc::tmem_relinquish();
     }
     if (tid == 0) {
-        for (int q = 0; q < kStages; ++q) tc::mbar_init(&bars[q], 1);
+        for (int q = 0; q < kStages; ++q) {
+            tc::mbar_init(&bars[q], 1);
+            tc::mbar_init(&full[q], 1);
+        }
         tc::fence_mbar_init();
     }
     tc::fence_before_sync();
@@ -106,67 +126,51 @@ __global__ void __launch_bounds__(kThr) k_fle_gemm(const int* __restrict__ n_row
     const uint32_t s0 = tc::smem_u32(smem);
     const int nk = Kp / kTK;
 
-    // stage st's copies: A slab 128 x 16 and B slab 256 x 16, hi and lo
-    auto issue = [&](int ks) {
-        if (ks < nk) {
-            const uint32_t base = s0 + (ks % kStages) * kStage;
-            // A: 256 chunks per plane (row r, half h) -> thread handles 2 per plane
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const int c = tid + q * kThr, r = c >> 1, h = c & 1;
-                const bool ok = r0 + r < n_rows;
-                const size_t src = static_cast<size_t>(ok ? r0 + r : 0) * Kp + ks * kTK + 8 * h;
-                const uint32_t off = slab_off(r, 8 * h);
-                cp16(base + off, a_hi + src, ok ? 16 : 0);
-                cp16(base + kASlab + off, a_lo + src, ok ? 16 : 0);
-            }
-            // B: 512 chunks per plane -> 4 per thread
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int c = tid + q * kThr, n = c >> 1, h = c & 1;
-                const bool ok = n0 + n < ncols;
-                const size_t src = static_cast<size_t>(ok ? n0 + n : 0) * Kp + ks * kTK + 8 * h;
-                const uint32_t off = slab_off(n, 8 * h);
-                cp16(base + 2 * kASlab + off, b_hi + src, ok ? 16 : 0);
-                cp16(base + 2 * kASlab + kBSlab + off, b_lo + src, ok ? 16 : 0);
-            }
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    uint32_t ph[kStages];
-#pragma unroll
-    for (int q = 0; q < kStages; ++q) ph[q] = 0u;
-#pragma unroll
-    for (int q = 0; q < kStages - 1; ++q) issue(q);
-    for (int ks = 0; ks < nk; ++ks) {
-        const int buf = ks % kStages;
-        asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 2) : "memory");
-        tc::fence_proxy_async_smem();
-        tc::fence_before_sync();
-        __syncthreads();
-        if (tid == 0) {
+    // one thread runs the whole pipeline: bulk copies of stage ks + kStages
+    // into the buffer stage ks used, once its MMAs are done (empty[b]); the
+    // MMAs of stage ks once its bytes have landed (full[b])
+    if (tid == 0) {
+        const uint16_t* pa_hi = a_hi + static_cast<size_t>(blockIdx.x) * nk * (kASlab / 2);
+        const uint16_t* pa_lo = a_lo + static_cast<size_t>(blockIdx.x) * nk * (kASlab / 2);
+        const uint16_t* pb_hi = b_hi + static_cast<size_t>(blockIdx.y) * nk * (kBSlab / 2);
+        const uint16_t* pb_lo = b_lo + static_cast<size_t>(blockIdx.y) * nk * (kBSlab / 2);
+        auto load = [&](int ks) {
+            const int b = ks % kStages;
+            const uint32_t base = s0 + b * kStage;
+            mbar_expect_tx(&full[b], kStage);
+            const uint32_t fb = tc::smem_u32(&full[b]);
+            bulk_g2s(base, pa_hi + static_cast<size_t>(ks) * (kASlab / 2), kASlab, fb);
+            bulk_g2s(base + kASlab, pa_lo + static_cast<size_t>(ks) * (kASlab / 2), kASlab, fb);
+            bulk_g2s(base + 2 * kASlab, pb_hi + static_cast<size_t>(ks) * (kBSlab / 2), kBSlab, fb);
+            bulk_g2s(base + 2 * kASlab + kBSlab, pb_lo + static_cast<size_t>(ks) * (kBSlab / 2), kBSlab, fb);
+        };
+        for (int ks = 0; ks < kStages && ks < nk; ++ks) load(ks);
+        for (int ks = 0; ks < nk; ++ks) {
+            const int b = ks % kStages;
+            tc::mbar_wait(&full[b], static_cast<uint32_t>((ks / kStages) & 1));
             tc::fence_after_sync();
-            const uint32_t ah = s0 + buf * kStage, al = ah + kASlab, bh = ah + 2 * kASlab, bl = bh + kBSlab;
+            const uint32_t ah = s0 + b * kStage, al = ah + kASlab, bh = ah + 2 * kASlab, bl = bh + kBSlab;
             const uint64_t dah = tc::sdesc_kmajor_noswizzle(ah, 128, 256), dal = tc::sdesc_kmajor_noswizzle(al, 128, 256);
             const uint64_t dbh = tc::sdesc_kmajor_noswizzle(bh, 128, 256), dbl = tc::sdesc_kmajor_noswizzle(bl, 128, 256);
             tc::mma_ss(tm, dah, dbh, kIdesc, ks > 0 ? 1u : 0u);
             tc::mma_ss(tm, dah, dbl, kIdesc, 1u);
             tc::mma_ss(tm, dal, dbh, kIdesc, 1u);
-            tc::mma_commit(&bars[buf]);
+            tc::mma_commit(&bars[b]);
+            if (ks + kStages < nk) {
+                tc::mbar_wait(&bars[b], static_cast<uint32_t>((ks / kStages) & 1));  // its MMAs read the buffer
+                load(ks + kStages);
+            }
         }
-        // the next copies reuse the buffer of stage ks - 1
-        if (ks >= 1) {
-            const int pb = (ks - 1) % kStages;
-            tc::mbar_wait(&bars[pb], ph[pb]);
-            ph[pb] ^= 1u;
-        }
-        issue(ks + kStages - 1);
     }
-    if (nk >= 1) {
+    // the last commit tracks every MMA before it.  Only thread 0 has seen
+    // every earlier phase of that barrier (a parity wait by the others could
+    // match an older phase), so it waits and releases the CTA.
+    if (tid == 0 && nk >= 1) {
         const int lb = (nk - 1) % kStages;
-        tc::mbar_wait(&bars[lb], ph[lb]);
+        tc::mbar_wait(&bars[lb], static_cast<uint32_t>(((nk - 1) / kStages) & 1));
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    tc::fence_before_sync();
+    __syncthreads();
     tc::fence_after_sync();
     // ---- epilogue: lane = row, column pairs = (Re, Im) of receiver j0 + c/2
     const int r = r0 + 32 * warp + lane;
@@ -206,12 +210,16 @@ cudaError_t launch_fle_gemm(rxgs_ctx ctx, const int* n_rows_dev, long long rows_
     if (rows_bound == 0 || n_rx == 0) return cudaSuccess;
     const int Kp = fle_gemm_kpad(L);
     cudaError_t e;
-    if ((e = ctx->fle_a.ensure(sizeof(uint16_t) * 2 * static_cast<size_t>(cap) * Kp)) != cudaSuccess) return e;
-    if ((e = ctx->fle_b.ensure(sizeof(uint16_t) * 4 * static_cast<size_t>(n_rx) * Kp)) != cudaSuccess) return e;
+    // pre-tiled operands: rows padded to the 128-row A blocks and the
+    // 256-column B blocks (the padding rows feed only unused outputs)
+    const size_t rows_p = (static_cast<size_t>(cap) + kTM - 1) / kTM * kTM;
+    const size_t cols_p = (2 * static_cast<size_t>(n_rx) + kTN - 1) / kTN * kTN;
+    if ((e = ctx->fle_a.ensure(sizeof(uint16_t) * 2 * rows_p * Kp)) != cudaSuccess) return e;
+    if ((e = ctx->fle_b.ensure(sizeof(uint16_t) * 2 * cols_p * Kp)) != cudaSuccess) return e;
     uint16_t* a_hi = ctx->fle_a.as<uint16_t>();
-    uint16_t* a_lo = a_hi + static_cast<size_t>(cap) * Kp;
+    uint16_t* a_lo = a_hi + rows_p * Kp;
     uint16_t* b_hi = ctx->fle_b.as<uint16_t>();
-    uint16_t* b_lo = b_hi + 2 * static_cast<size_t>(n_rx) * Kp;
+    uint16_t* b_lo = b_hi + cols_p * Kp;
     const long long na = rows_bound * (Kp / 4), nb = 2LL * n_rx * (Kp / 4);
     if (a_version == 0 || ctx->fle_a_version != a_version) {  // A depends on the state only
         k_fle_pack_a<<<static_cast<unsigned>((na + 255) / 256), 256, 0, s>>>(n_rows_dev, cap, L, Kp, rGB, a_hi, a_lo);

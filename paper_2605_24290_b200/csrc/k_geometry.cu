@@ -187,51 +187,48 @@ __global__ void k_tx_prep(int K, int l_max_rt, int C, const double* __restrict__
         return;
     }
     // legendre_table (radiance.cpp:16-37) on x = cos(theta), without the
-    // Condon-Shortley phase, walked order by order: for each m the diagonal
-    // P(m,m) from P(m-1,m-1), then P(m+1,m) and the upward recurrence in l,
-    // carrying two values -- every entry is the reference's formula on the
-    // same predecessors, so the values are the table's bit for bit, with O(1)
-    // live state instead of the (L_max+1)(L_max+2)/2 table (registers and
-    // occupancy at high l_max).
-    const int LB = LMT > 0 ? LMT : l_max;  // loop bound (constant when specialised)
+    // Condon-Shortley phase; entries packed l*(l+1)/2 + m.
+    constexpr int LM = LMT > 0 ? LMT : kMaxLmax;  // array bound
+    const int LB = LMT > 0 ? LMT : l_max;         // loop bound (constant when specialised)
+    double P[(LM + 1) * (LM + 2) / 2];
     double x = cos(theta);
     x = x < -1.0 ? -1.0 : (x > 1.0 ? 1.0 : x);
     const double s = sqrt(dmax(0.0, (1.0 - x) * (1.0 + x)));
-    auto emit = [&](int l, int m, double p_lm, double cm, double sm) {  // components (l, m): m may be < 0
-        const int am = m < 0 ? -m : m;
-        const double np = normalization(l, am) * p_lm;
-        const int idx = l * l + m + l;
-        const double br = np * cm, bi = np * sm;
-        if (FULL) reinterpret_cast<double2*>(b64)[idx] = make_double2(br, bi);
-        b32[idx] = make_float2(static_cast<float>(br), static_cast<float>(bi));
-        for (int c = 0; c < C; ++c) {
-            const double a_ = cb[(idx * C + c) * 2], b_ = cb[(idx * C + c) * 2 + 1];
-            g32[idx * C + c] = make_float2(static_cast<float>(a_ * br - b_ * bi), static_cast<float>(a_ * bi + b_ * br));
-        }
-    };
-    double pmm = 1.0;  // P(m, m)
+#define AT(l, m) P[(l) * ((l) + 1) / 2 + (m)]
+    AT(0, 0) = 1.0;
 #pragma unroll
-    for (int m = 0; m <= LB; ++m) {
-        if (m > 0) pmm = pmm * (2.0 * m - 1.0) * s;
-        // cos / sin of m phi and of -m phi, as eval_basis evaluates them per (l, m)
-        double cp, sp, cn, sn;
-        sincos(m * phi, &sp, &cp);
-        if (m > 0) sincos(-m * phi, &sn, &cn);
-        double p2 = 0.0, p1 = pmm;  // P(l-2, m), P(l-1, m) as l advances
+    for (int m = 1; m <= LB; ++m) AT(m, m) = AT(m - 1, m - 1) * (2.0 * m - 1.0) * s;
 #pragma unroll
-        for (int l = m; l <= LB; ++l) {
-            double plm;
-            if (l == m) plm = pmm;
-            else if (l == m + 1) plm = x * (2.0 * m + 1.0) * pmm;
-            else plm = (x * (2.0 * l - 1.0) * p1 - (l + m - 1.0) * p2) / static_cast<double>(l - m);
-            if (l > m) {
-                p2 = p1;
-                p1 = plm;
+    for (int m = 0; m < LB; ++m) AT(m + 1, m) = x * (2.0 * m + 1.0) * AT(m, m);
+#pragma unroll
+    for (int m = 0; m <= LB; ++m)
+#pragma unroll
+        for (int l = m + 2; l <= LB; ++l)
+            AT(l, m) = (x * (2.0 * l - 1.0) * AT(l - 1, m) - (l + m - 1.0) * AT(l - 2, m)) /
+                       static_cast<double>(l - m);
+    // cos(m phi), sin(m phi) once per distinct m (eval_basis evaluates them
+    // per (l, m); the same argument m * phi gives the same values)
+    double cm[2 * LM + 1], sn[2 * LM + 1];
+#pragma unroll
+    for (int m = -LB; m <= LB; ++m) sincos(m * phi, &sn[m + LM], &cm[m + LM]);
+#pragma unroll
+    for (int l = 0; l <= LB; ++l) {
+#pragma unroll
+        for (int m = -l; m <= l; ++m) {
+            const int am = m < 0 ? -m : m;
+            const double np = normalization(l, am) * AT(l, am);
+            const int idx = l * l + m + l;
+            const double br = np * cm[m + LM], bi = np * sn[m + LM];
+            if (FULL) reinterpret_cast<double2*>(b64)[idx] = make_double2(br, bi);
+            b32[idx] = make_float2(static_cast<float>(br), static_cast<float>(bi));
+            for (int c = 0; c < C; ++c) {
+                const double a_ = cb[(idx * C + c) * 2], b_ = cb[(idx * C + c) * 2 + 1];
+                g32[idx * C + c] = make_float2(static_cast<float>(a_ * br - b_ * bi),
+                                               static_cast<float>(a_ * bi + b_ * br));
             }
-            emit(l, m, plm, cp, sp);
-            if (m > 0) emit(l, -m, plm, cn, sn);
         }
     }
+#undef AT
 }
 
 // ---------------------------------------------------------------- single-call API kernels

@@ -31,7 +31,7 @@ namespace {
 #ifndef RXGS_WALK_CHUNK
 #define RXGS_WALK_CHUNK 128  // A/B: 128 > 64 > 32 (config-3 walk 17.5 / 18.6 / 21.1 ms)
 #endif
-constexpr int kChunk = RXGS_WALK_CHUNK;
+[[maybe_unused]] constexpr int kChunk = RXGS_WALK_CHUNK;
 constexpr int kWalkThreads = 512;
 constexpr int kLanesPerCell = kWalkThreads / kMaxCellsPerBlock;  // 4
 
@@ -44,6 +44,10 @@ __device__ __forceinline__ double wrap_pm_pi(double a) {  // linalg.hpp:152-157
     return a;
 }
 
+#ifndef RXGS_WALK_PIPE
+#define RXGS_WALK_PIPE 1
+#endif
+#if !RXGS_WALK_PIPE
 __global__ void __launch_bounds__(kWalkThreads) k_walk(DevGrid g, const int64_t* __restrict__ tile_offsets,
                                                        const int* __restrict__ list,
                                                        const GaussRec* __restrict__ rec, float* __restrict__ tw,
@@ -129,16 +133,134 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(DevGrid g, const int64_t*
     }
 }
 
+#endif  // !RXGS_WALK_PIPE
+
+// Pipelined variant (RXGS_WALK_PIPE, default): the two phases run
+// concurrently on different warps -- warps 0-1 (the 64 cell owners) run the
+// recurrence of chunk c while warps 2-15 stage the records of chunk c+1 and
+// evaluate its weights into the other half of a double buffer -- so a chunk
+// costs max(A, B) instead of A + B.  The producers skip cells that had
+// exited by the end of chunk c-1 (a cell exiting during chunk c costs at
+// most one chunk of unneeded weights).  Same arithmetic, same order: the
+// output is identical to the two-phase kernel.
+constexpr int kPipeChunk = 64;
+constexpr int kProducers = kWalkThreads - kMaxCellsPerBlock;  // 448
+
+__global__ void __launch_bounds__(kWalkThreads) k_walk_pipe(DevGrid g, const int64_t* __restrict__ tile_offsets,
+                                                            const int* __restrict__ list,
+                                                            const GaussRec* __restrict__ rec, float* __restrict__ tw,
+                                                            int* __restrict__ walk_len, double* __restrict__ cell_T,
+                                                            int* __restrict__ cell_len) {
+    extern __shared__ __align__(16) uint8_t walk_smem[];
+    GaussRec* srec = reinterpret_cast<GaussRec*>(walk_smem);  // [2][kPipeChunk]
+    double(*sw)[kMaxCellsPerBlock] =
+        reinterpret_cast<double(*)[kMaxCellsPerBlock]>(walk_smem + sizeof(GaussRec) * 2 * kPipeChunk);  // [2 * chunk][64]
+    __shared__ int s_alive[kMaxCellsPerBlock];
+    __shared__ int s_len[kMaxCellsPerBlock];
+    __shared__ int s_max, s_min;
+    const int tile = blockIdx.x;
+    const int cb = blockIdx.y;
+    const int tid = threadIdx.x;
+    const bool owner = tid < kMaxCellsPerBlock;
+    const int cl = tid % kMaxCellsPerBlock;  // owner: its cell; producer: the cell it evaluates
+    const int tt = tile / g.tiles_p, tp = tile % g.tiles_p;
+    const int lc = cb * kMaxCellsPerBlock + cl;
+    const int row = tt * g.ts + lc / g.ts;
+    const int col = tp * g.ts + lc % g.ts;
+    const bool valid = lc < g.cpt && (lc / g.ts) < g.ts && row < g.nt && col < g.np;
+    const int64_t begin = tile_offsets[tile];
+    const int n = static_cast<int>(tile_offsets[tile + 1] - begin);
+    const size_t stride = static_cast<size_t>(g.cell_blocks) * kMaxCellsPerBlock;
+    float* out = tw + static_cast<size_t>(begin) * stride + static_cast<size_t>(cb) * kMaxCellsPerBlock + cl;
+    const double theta_r = valid ? g.tmin + (row + 0.5) * g.dth : 0.0;
+    const double phi_r = valid ? (col + 0.5) * g.dph : 0.0;
+    double T = 1.0;
+    int len = valid ? n : 0;
+    bool alive = owner && valid && n > 0;
+    if (owner) s_alive[cl] = alive ? 1 : 0;
+    if (tid == 0) {
+        s_max = 0;
+        s_min = 0x7fffffff;
+    }
+    __syncthreads();
+    const int n_ch = (n + kPipeChunk - 1) / kPipeChunk;
+    const int ptid = tid - kMaxCellsPerBlock;  // producer index (owners: negative)
+    // producer step: records of chunk ch into half ch % 2, then its weights
+    auto produce = [&](int ch) {
+        const int h = ch & 1;
+        const int c0 = ch * kPipeChunk;
+        const int m = min(kPipeChunk, n - c0);
+        for (int q = ptid; q < m; q += kProducers) srec[h * kPipeChunk + q] = rec[list[begin + c0 + q]];
+        asm volatile("bar.sync 1, %0;" ::"n"(kProducers) : "memory");  // producers only
+        if (!*reinterpret_cast<volatile int*>(&s_alive[cl])) return;  // exited (by the end of the chunk before last)
+        for (int e = ptid / kMaxCellsPerBlock; e < m; e += kProducers / kMaxCellsPerBlock) {
+            const GaussRec& r = srec[h * kPipeChunk + e];
+            const double dt = theta_r - r.theta;
+            const double dpraw = wrap_pm_pi(phi_r - r.phi);
+            const double dp = r.sin_theta * dpraw;
+            const double m2 = r.pa * dt * dt + r.pbc * dt * dp + r.pd * dp * dp;
+            const double w = r.tau * exp(-0.5 * m2);
+            sw[h * kPipeChunk + e][cl] = kWeightClamp < w ? kWeightClamp : w;  // std::min(w, 0.999)
+        }
+    };
+    if (!owner && n_ch > 0) produce(0);
+    for (int ch = 0; ch < n_ch; ++ch) {
+        if (!__syncthreads_or(alive)) break;  // chunk ch's weights are ready; every cell exited -> stop
+        if (owner) {
+            if (alive) {  // the front-to-back recurrence (render_field :285-298)
+                const int h = ch & 1, c0 = ch * kPipeChunk, m = min(kPipeChunk, n - c0);
+                for (int e = 0; e < m; ++e) {
+                    const double w = sw[h * kPipeChunk + e][cl];
+                    out[static_cast<size_t>(c0 + e) * stride] = static_cast<float>(T * w);
+                    T *= 1.0 - w;
+                    if (T < kEarlyExitT) {
+                        len = c0 + e + 1;
+                        alive = false;
+                        break;
+                    }
+                }
+                s_alive[cl] = alive ? 1 : 0;
+            }
+        } else if (ch + 1 < n_ch) {
+            produce(ch + 1);
+        }
+    }
+    if (owner) {
+        s_len[cl] = len;
+        atomicMax(&s_max, len);
+        atomicMin(&s_min, len);
+    }
+    __syncthreads();
+    const int wmax = s_max;
+    // zero the rows past each cell's exit up to the tile's longest walk
+    for (int e = s_min + tid / kMaxCellsPerBlock; e < wmax; e += kLanesPerCell)
+        if (e >= s_len[cl]) out[static_cast<size_t>(e) * stride] = 0.0f;
+    if (tid == 0) walk_len[tile * g.cell_blocks + cb] = wmax;
+    if (owner && valid) {
+        const size_t cell = static_cast<size_t>(row) * g.np + col;
+        cell_T[cell] = T;
+        cell_len[cell] = len;
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_walk(rxgs_txstate_s& st, cudaStream_t s) {
     const DevGrid& g = st.grid;
     dim3 grid(g.n_tiles, g.cell_blocks);
+#if RXGS_WALK_PIPE
+    const size_t smem = 2 * (sizeof(GaussRec) * kPipeChunk + sizeof(double) * kPipeChunk * kMaxCellsPerBlock);
+    cudaFuncSetAttribute(k_walk_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_walk_pipe<<<grid, kWalkThreads, smem, s>>>(g, st.tile_offsets.as<int64_t>(), st.list.as<int>(),
+                                                  st.rec.as<GaussRec>(), st.tw.as<float>(), st.walk_len.as<int>(),
+                                                  st.cell_T.as<double>(), st.cell_len.as<int>());
+#else
     const size_t smem = sizeof(GaussRec) * kChunk + sizeof(double) * kChunk * kMaxCellsPerBlock;
     cudaFuncSetAttribute(k_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k_walk<<<grid, kWalkThreads, smem, s>>>(g, st.tile_offsets.as<int64_t>(), st.list.as<int>(),
                                st.rec.as<GaussRec>(), st.tw.as<float>(), st.walk_len.as<int>(),
                                st.cell_T.as<double>(), st.cell_len.as<int>());
+#endif
     return cudaGetLastError();
 }
 
