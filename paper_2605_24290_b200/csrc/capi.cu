@@ -7,6 +7,7 @@
 #include <atomic>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <new>
@@ -1319,23 +1320,22 @@ int rxgs_render_queries(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, rxgs_txstate s
     const bool pipelined = out_spectrum && d_spec != out_spectrum && n_rx >= 256;
     std::vector<int> bounds{0};
     if (pipelined) {
-#ifndef RXGS_E2E_SCHED
-#define RXGS_E2E_SCHED 1  // A/B: 5 shrinking chunks (last 1/32) beat 4 (last 1/8) by ~1% e2e and the
-                          // small-first schedules 3-5 by ~5% (per-chunk launch costs outweigh the earlier D2H start)
-#endif
-#if RXGS_E2E_SCHED == 1
-        const double frac[5] = {3.0 / 8, 3.0 / 8 + 5.0 / 16, 7.0 / 8, 7.0 / 8 + 3.0 / 32, 1.0};
-#elif RXGS_E2E_SCHED == 2
-        const double frac[3] = {1.0 / 2, 7.0 / 8, 1.0};
-#elif RXGS_E2E_SCHED == 3
-        const double frac[6] = {1.0 / 8, 3.0 / 8, 5.0 / 8, 7.0 / 8, 15.0 / 16, 1.0};
-#elif RXGS_E2E_SCHED == 4
-        const double frac[6] = {1.0 / 16, 1.0 / 4, 1.0 / 2, 3.0 / 4, 15.0 / 16, 1.0};
-#elif RXGS_E2E_SCHED == 5
-        const double frac[5] = {3.0 / 16, 1.0 / 2, 13.0 / 16, 15.0 / 16, 1.0};
-#else
-        const double frac[4] = {3.0 / 8, 3.0 / 8 + 5.0 / 16, 7.0 / 8, 1.0};
-#endif
+        // receiver-chunk schedules of the host-output pipeline (fractions of
+        // the batch at the chunk ends).  A/B on one B200, config 2 (e2e):
+        // schedule 0 is the default; RXGS_E2E_SCHED selects another at run time.
+        static const std::vector<std::vector<double>> kSched = {
+            {3.0 / 8, 3.0 / 8 + 5.0 / 16, 7.0 / 8, 7.0 / 8 + 3.0 / 32, 1.0},   // 0
+            {3.0 / 8, 3.0 / 8 + 5.0 / 16, 7.0 / 8, 1.0},                       // 1
+            {1.0 / 8, 3.0 / 8, 5.0 / 8, 27.0 / 32, 31.0 / 32, 1.0},            // 2
+            {1.0 / 4, 1.0 / 2, 3.0 / 4, 15.0 / 16, 1.0},                       // 3
+            {1.0 / 8, 1.0 / 2, 7.0 / 8, 31.0 / 32, 1.0},                       // 4
+        };
+        static const int sched = [] {
+            const char* e = std::getenv("RXGS_E2E_SCHED");
+            const int v = e ? std::atoi(e) : 0;
+            return v >= 0 && v < 5 ? v : 0;
+        }();
+        const std::vector<double>& frac = kSched[static_cast<size_t>(sched)];
         for (double f : frac) {
             int b = static_cast<int>(std::lround(f * n_rx / 32.0)) * 32;
             b = std::min(std::max(b, bounds.back() + 1), n_rx);
