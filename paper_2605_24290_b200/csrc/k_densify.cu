@@ -15,7 +15,6 @@
 //   k_dens_compact   survivors in merged order + their source rows
 // Compiled without FMA contraction (like the FP64 geometry) so positions and
 // scales follow the reference's rounding.
-#include <cub/device/device_scan.cuh>
 
 #include <cmath>
 
@@ -156,10 +155,8 @@ bool on_device(const void* p) {
 }
 
 int exclusive_sum(rxgs_ctx ctx, const int* in, int* out, int n, cudaStream_t s) {
-    size_t tmp = 0;
-    RXGS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, s));
-    RXGS_CUDA(ctx->sort_tmp.ensure(tmp));
-    RXGS_CUDA(cub::DeviceScan::ExclusiveSum(ctx->sort_tmp.p, tmp, in, out, n, s));
+    RXGS_CUDA(ctx->sort_tmp.ensure(sizeof(int64_t) * scan_bsum_count(n)));
+    RXGS_CUDA(scan_i32(n, in, out, ctx->sort_tmp.as<int64_t>(), s));
     return RXGS_OK;
 }
 

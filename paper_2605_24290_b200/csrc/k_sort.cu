@@ -341,8 +341,10 @@ __global__ void k_depth_final(int K, const uint32_t* __restrict__ ks, int* __res
 // Block-local exclusive scan of kScanChunk elements; block totals to bsum.
 // Warp w scans its contiguous chunk 32 elements at a time (coalesced,
 // register shuffles), then adds the totals of the earlier warps.
-__global__ void __launch_bounds__(256) k_scan_blocks(int64_t n, const int64_t* __restrict__ in,
-                                                     int64_t* __restrict__ out, int64_t* __restrict__ bsum) {
+// T = int64_t or int (int sums accumulate in int64 and are written back narrowed).
+template <typename T>
+__global__ void __launch_bounds__(256) k_scan_blocks(int64_t n, const T* __restrict__ in, T* __restrict__ out,
+                                                     int64_t* __restrict__ bsum) {
     __shared__ int64_t wt[8];
     constexpr int SEG = kScanChunk / 8;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -352,7 +354,7 @@ __global__ void __launch_bounds__(256) k_scan_blocks(int64_t n, const int64_t* _
 #pragma unroll
     for (int r = 0; r < SEG / 32; ++r) {
         const int64_t i = b0 + r * 32 + lane;
-        const int64_t x = i < n ? in[i] : 0;
+        const int64_t x = i < n ? static_cast<int64_t>(in[i]) : 0;
         int64_t inc = x;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -372,13 +374,14 @@ __global__ void __launch_bounds__(256) k_scan_blocks(int64_t n, const int64_t* _
 #pragma unroll
     for (int r = 0; r < SEG / 32; ++r) {
         const int64_t i = b0 + r * 32 + lane;
-        if (i < n) out[i] = v[r] + prev;
+        if (i < n) out[i] = static_cast<T>(v[r] + prev);
     }
     if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
 }
 
 // out += sum of the block totals before this block.
-__global__ void k_scan_add(int64_t n, int64_t* __restrict__ out, const int64_t* __restrict__ bsum) {
+template <typename T>
+__global__ void k_scan_add(int64_t n, T* __restrict__ out, const int64_t* __restrict__ bsum) {
     __shared__ int64_t ws[32];
     int64_t p = 0;
     for (int i = threadIdx.x; i < static_cast<int>(blockIdx.x); i += blockDim.x) p += bsum[i];
@@ -387,7 +390,7 @@ __global__ void k_scan_add(int64_t n, int64_t* __restrict__ out, const int64_t* 
     if (t == 0) return;
     const int64_t b0 = blockIdx.x * static_cast<int64_t>(kScanChunk);
     for (int i = threadIdx.x; i < kScanChunk; i += blockDim.x)
-        if (b0 + i < n) out[b0 + i] += t;
+        if (b0 + i < n) out[b0 + i] += static_cast<T>(t);
 }
 
 // ---------------------------------------------------------------- tile pass
@@ -652,14 +655,22 @@ cudaError_t radix_sort_pairs(int n, int bits, uint32_t* kin, int* vin, uint32_t*
     return cudaGetLastError();
 }
 
-// Exclusive scan of n int64 (in -> out, may alias); bsum: (n / kScanChunk + 1) int64.
-cudaError_t scan_i64(int64_t n, const int64_t* in, int64_t* out, int64_t* bsum, cudaStream_t s) {
+// Exclusive scan of n int64 / int (in -> out, may alias); bsum: scan_bsum_count(n) int64.
+template <typename T>
+static cudaError_t scan_any(int64_t n, const T* in, T* out, int64_t* bsum, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     const unsigned nb = static_cast<unsigned>((n + kScanChunk - 1) / kScanChunk);
-    k_scan_blocks<<<nb, 256, 0, s>>>(n, in, out, bsum);
-    if (nb > 1) k_scan_add<<<nb, 256, 0, s>>>(n, out, bsum);
+    k_scan_blocks<T><<<nb, 256, 0, s>>>(n, in, out, bsum);
+    if (nb > 1) k_scan_add<T><<<nb, 256, 0, s>>>(n, out, bsum);
     return cudaGetLastError();
 }
+cudaError_t scan_i64(int64_t n, const int64_t* in, int64_t* out, int64_t* bsum, cudaStream_t s) {
+    return scan_any(n, in, out, bsum, s);
+}
+cudaError_t scan_i32(int64_t n, const int* in, int* out, int64_t* bsum, cudaStream_t s) {
+    return scan_any(n, in, out, bsum, s);
+}
+size_t scan_bsum_count(int64_t n) { return static_cast<size_t>(n / kScanChunk + 2); }
 
 int bin_tiles(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
     const int K = st.k;

@@ -23,8 +23,6 @@
 //                                                               -> k_adam
 // Every reduction runs in a fixed order (no floating-point atomics), so a
 // step is bitwise reproducible, as the reference requires.
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
 
 #include "cond_common.cuh"
 #include "f32x2.cuh"
@@ -995,32 +993,32 @@ int train_regroup(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
     RXGS_CUDA(st.gauss_off.ensure(sizeof(int) * (K + 2)));
     RXGS_CUDA(st.gauss_ent.ensure(sizeof(int) * (E + 1)));
     auto al = [](size_t x) { return (x + 255) & ~static_cast<size_t>(255); };
+    const int En = static_cast<int>(E);
     const size_t o_vals = al(sizeof(int) * (E + 1)), o_ks = o_vals + al(sizeof(int) * (E + 1)),
-                 o_hist = o_ks + al(sizeof(int) * (E + 1));
-    RXGS_CUDA(ctx->scratch_b.ensure(o_hist + al(sizeof(int) * (K + 2))));
+                 o_hist = o_ks + al(sizeof(int) * (E + 1)), o_work = o_hist + al(sizeof(int) * (K + 2)),
+                 o_bsum = o_work + al(sizeof(int) * radix_sort_work_ints(En));
+    RXGS_CUDA(ctx->scratch_b.ensure(o_bsum + al(sizeof(int64_t) * scan_bsum_count(K + 1))));
     char* pb = ctx->scratch_b.as<char>();
-    int* keys = reinterpret_cast<int*>(pb);
+    uint32_t* keys = reinterpret_cast<uint32_t*>(pb);
     int* vals = reinterpret_cast<int*>(pb + o_vals);
-    int* ks = reinterpret_cast<int*>(pb + o_ks);
+    uint32_t* ks = reinterpret_cast<uint32_t*>(pb + o_ks);
     int* hist = reinterpret_cast<int*>(pb + o_hist);
+    int* work = reinterpret_cast<int*>(pb + o_work);
+    int64_t* bsum = reinterpret_cast<int64_t*>(pb + o_bsum);
     RXGS_CUDA(cudaMemsetAsync(hist, 0, sizeof(int) * (K + 2), s));
     if (E > 0) {
+        // entries (key = Gaussian, value = entry index) straight into gauss_ent;
+        // the stable radix sort leaves them grouped by Gaussian in entry order
         k_entry_keys<<<st.grid.n_tiles, 128, 0, s>>>(st.grid, K, st.tile_offsets.as<int64_t>(), st.list.as<int>(),
-                                                      st.walk_len.as<int>(), keys, vals);
+                                                      st.walk_len.as<int>(), reinterpret_cast<int*>(keys),
+                                                      st.gauss_ent.as<int>());
+        k_key_hist<<<static_cast<unsigned>((E + 255) / 256), 256, 0, s>>>(E, reinterpret_cast<int*>(keys), hist);
         int bits = 1;
         while ((1 << bits) <= K) ++bits;
-        size_t tmp = 0;
-        RXGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, ks, vals, st.gauss_ent.as<int>(),
-                                                  static_cast<int>(E), 0, bits, s));
-        RXGS_CUDA(ctx->sort_tmp.ensure(tmp));
-        RXGS_CUDA(cub::DeviceRadixSort::SortPairs(ctx->sort_tmp.p, tmp, keys, ks, vals, st.gauss_ent.as<int>(),
-                                                  static_cast<int>(E), 0, bits, s));
-        k_key_hist<<<static_cast<unsigned>((E + 255) / 256), 256, 0, s>>>(E, keys, hist);
+        RXGS_CUDA(cudaMemsetAsync(work, 0, sizeof(int) * radix_sort_work_ints(En), s));
+        RXGS_CUDA(radix_sort_pairs(En, bits, keys, st.gauss_ent.as<int>(), ks, vals, work, false, s));
     }
-    size_t tmp = 0;
-    RXGS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, hist, st.gauss_off.as<int>(), K + 1, s));
-    RXGS_CUDA(ctx->sort_tmp.ensure(tmp));
-    RXGS_CUDA(cub::DeviceScan::ExclusiveSum(ctx->sort_tmp.p, tmp, hist, st.gauss_off.as<int>(), K + 1, s));
+    RXGS_CUDA(scan_i32(K + 1, hist, st.gauss_off.as<int>(), bsum, s));
     st.regrouped = true;
     ctx->launches += 5;
     const cudaError_t e = cudaGetLastError();

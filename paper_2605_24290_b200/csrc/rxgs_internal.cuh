@@ -269,6 +269,8 @@ size_t radix_sort_work_ints(int n);
 cudaError_t radix_sort_pairs(int n, int bits, uint32_t* kin, int* vin, uint32_t* ktmp, int* vtmp, int* work,
                              bool hist_ready, cudaStream_t s);
 cudaError_t scan_i64(int64_t n, const int64_t* in, int64_t* out, int64_t* bsum, cudaStream_t s);
+cudaError_t scan_i32(int64_t n, const int* in, int* out, int64_t* bsum, cudaStream_t s);
+size_t scan_bsum_count(int64_t n);
 // ---- k_refapi.cu (FP64 single-call API kernels)
 // located non-finite check of n coefficients, rows of per_row (k_cond.cu)
 cudaError_t launch_check_finite(long long n, long long per_row, const double* d_coeffs, int* d_err, cudaStream_t s);
