@@ -34,6 +34,8 @@
 // TMEM: 512 columns per CTA = 4 groups x (64 accumulator + 32 A-hi + 32 A-lo).
 // Shared memory: W2 hi/lo (16 KB), W1 hi/lo (4 KB), b2 hi/lo + the constant
 // A tile (8 KB), the zero-bordered occupancy grid ((R+3)^3 FP32, 168 KB).
+#include <cstdlib>
+
 #include "cond_common.cuh"
 #include "rxgs_internal.cuh"
 #include "tc_util.cuh"
@@ -852,6 +854,385 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) tc::tmem_dealloc(tbase, 512);
 }
 
+// ------------------------------------------------------ warp-specialised form
+// k_cond_ws: the same rows, the same arithmetic and the same MMA sequence as
+// k_cond_tc (bit-identical signals), with the SIMT work split over two warp
+// roles so twice as many warps hide the latencies (k_cond_tc runs 16 warps
+// per SM, limited by TMEM and registers, at ~59% issue efficiency):
+//   * producer warps (warpgroups 4..7; warpgroup 4+g feeds MLP group g):
+//     local features, the occupancy probe and the FLE reduction of a tile's
+//     128 rows; they write the layer-1 A operand [x_hi, 1, 0, x_lo, 0, 0]
+//     (bf16, K-major canonical) and (M, sum_l B_l) into a shared-memory ring
+//     slot and arrive on the slot's `full` barrier;
+//   * MLP warps (warpgroups 0..3, TMEM owners): ReLU(h1) -> bf16 hi/lo split
+//     in place in TMEM, layer 2 on tcgen05, layer 3 and the affine epilogue.
+//     The next tile's layer-1 MMA (A from the ring) is issued as soon as this
+//     tile's layer 2 completes and runs under this tile's layer 3.
+// TMEM per group: 64 columns h1 -> A2 (split in place) + 64 columns h2.
+#ifndef RXGS_WS_SLOTS
+#define RXGS_WS_SLOTS 2
+#endif
+constexpr int kWsSlots = RXGS_WS_SLOTS;
+// register split between the roles (setmaxnreg; 0 = the launch's 64 for both)
+#ifndef RXGS_WS_REG_PROD
+#define RXGS_WS_REG_PROD 0
+#endif
+#ifndef RXGS_WS_REG_MLP
+#define RXGS_WS_REG_MLP 0
+#endif
+#ifndef RXGS_WS_MMA_WAIT
+#define RXGS_WS_MMA_WAIT tc::mbar_wait
+#endif
+#ifndef RXGS_WS_EMPTY_WAIT
+#define RXGS_WS_EMPTY_WAIT tc::mbar_wait_backoff
+#endif
+constexpr int kWsThreads = 256 * kGroups;
+constexpr int kSlotBytes = kA1Bytes + 128 * 16;  // A1 operand + float4 (M, Bs) per row
+constexpr int kWsSmem = kFixedSmem + kGroups * kWsSlots * kSlotBytes;
+
+template <int ST, int RT, bool YOUT>
+__global__ void __launch_bounds__(kWsThreads, 1)
+    k_cond_ws(const __grid_constant__ LocalW W, CondDev c, const int* __restrict__ n_rows_dev, int n_rows_host,
+              int cap, const int* __restrict__ rows, const float4* __restrict__ rpos, const double* __restrict__ rx,
+              int n_rx, const float4* __restrict__ rGB, const float4* __restrict__ rS, const float* __restrict__ ag,
+              const float2* __restrict__ Mpre, SigOut sig, float4* __restrict__ ycache) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* w2hi = smem;
+    uint8_t* w2lo = smem + kW2Bytes;
+    uint8_t* w1hi = smem + 2 * kW2Bytes;
+    uint8_t* w1lo = w1hi + kW1Bytes;
+    uint8_t* b2hi = w1lo + kW1Bytes;
+    uint8_t* aone = b2hi + 2 * kW1Bytes;
+    uint8_t* ring = smem + kFixedSmem;
+    __shared__ uint64_t full[kGroups][kWsSlots], empty[kGroups][kWsSlots], bar1[kGroups], bar2[kGroups];
+    __shared__ uint32_t arrivals[kGroups];
+    __shared__ uint32_t tbase_s;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int wg = warp >> 2, wl = warp & 3;
+    if (tid < kGroups) arrivals[tid] = 0u;
+    // ---- one-time setup (as k_cond_tc)
+    for (int i = tid; i < kH * kH; i += kWsThreads)
+        split_store(w2hi, w2lo, canon_off(i / kH, i % kH), c.p32[c.o_lw2 + i]);
+    for (int i = tid; i < kH * 16; i += kWsThreads) {
+        const int n = i / 16, k = i % 16;
+        const float w = k < 6 ? c.p32[c.o_lw1 + n * 6 + k] : (k == 6 ? c.p32[c.o_lb1 + n] : 0.f);
+        const float whi = tc::bf16_round(w);
+        const uint32_t off = canon_off16(n, k);
+        const float wa = k < 7 ? whi : ((k >= 8 && k < 14) ? tc::bf16_round(c.p32[c.o_lw1 + n * 6 + (k - 8)]) : 0.f);
+        const float wb = k < 7 ? w - whi : 0.f;
+        *reinterpret_cast<uint16_t*>(w1hi + off) = static_cast<uint16_t>(tc::pack_bf16(wa, 0.f) & 0xFFFFu);
+        *reinterpret_cast<uint16_t*>(w1lo + off) = static_cast<uint16_t>(tc::pack_bf16(wb, 0.f) & 0xFFFFu);
+        const float b2 = c.p32[c.o_lb2 + n], b2h = tc::bf16_round(b2);
+        const float bv = k == 0 ? b2h : (k == 1 ? b2 - b2h : 0.f);
+        *reinterpret_cast<uint16_t*>(b2hi + off) = static_cast<uint16_t>(tc::pack_bf16(bv, 0.f) & 0xFFFFu);
+    }
+    for (int i = tid; i < 128 * 16; i += kWsThreads) {
+        const int r = i / 16, k = i % 16;
+        *reinterpret_cast<uint16_t*>(aone + canon_off16(r, k)) = k < 2 ? 0x3F80u : 0u;  // bf16 1.0
+    }
+    if (warp == 0) {
+        tc::tmem_alloc(&tbase_s, 512);
+        tc::tmem_relinquish();
+    }
+    if (tid == 0) {
+        for (int q = 0; q < kGroups; ++q) {
+            for (int s = 0; s < kWsSlots; ++s) {
+                tc::mbar_init(&full[q][s], 128);  // every producer thread of the group
+                tc::mbar_init(&empty[q][s], 1);   // the layer-2 issuer of the consuming tile
+            }
+            tc::mbar_init(&bar1[q], 1);
+            tc::mbar_init(&bar2[q], 1);
+        }
+        tc::fence_mbar_init();
+    }
+    tc::fence_proxy_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+
+    const int n_rows = YOUT ? n_rows_host : *n_rows_dev;
+    const int nq = (n_rx + 3) >> 2;
+    const long long tiles = static_cast<long long>((n_rows + 31) >> 5) * nq;
+    const long long step = static_cast<long long>(gridDim.x) * kGroups;
+    const int step_gb = static_cast<int>(step / nq), step_jq = static_cast<int>(step % nq);
+    const int g = wg < kGroups ? wg : wg - kGroups;
+    const int arow = 32 * wl + lane;  // this thread's row of the 128-row tile (= TMEM lane)
+    int cur_gb = 0, cur_jq = 0;
+    long long tile = static_cast<long long>(blockIdx.x) * kGroups + g;
+    if (tile < tiles) {
+        cur_gb = static_cast<int>(tile / nq);
+        cur_jq = static_cast<int>(tile - static_cast<long long>(cur_gb) * nq);
+    }
+    auto advance = [&]() {
+        cur_gb += step_gb;
+        cur_jq += step_jq;
+        if (cur_jq >= nq) {
+            cur_jq -= nq;
+            ++cur_gb;
+        }
+    };
+    auto slot_a1 = [&](int s) { return ring + static_cast<size_t>(g * kWsSlots + s) * kSlotBytes; };
+    auto slot_mb = [&](int s) { return reinterpret_cast<float4*>(slot_a1(s) + kA1Bytes); };
+
+    if (wg >= kGroups) {
+        // =================================================== producer warps
+#if RXGS_WS_REG_PROD
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(RXGS_WS_REG_PROD));
+#endif
+        const int R = RT > 0 ? RT : c.R;
+        const float hiR = static_cast<float>(R);
+        const int S = ST > 0 ? ST : c.S;
+        const float tlast = S == 1 ? 0.5f : fmaf(static_cast<float>(S - 1), 0.9f / static_cast<float>(S - 1), 0.05f);
+        const float tfirst = S == 1 ? 0.5f : 0.05f;
+        constexpr bool kPairs = ST >= 2 && ST % 2 == 0 && RT > 0;
+        const int L = c.L;
+        int s = 0;
+        uint32_t eph = 0;  // parity of the next empty[s] phase to wait for
+        for (long long t = 0; tile < tiles; tile += step, ++t) {
+            const int r = cur_gb * 32 + lane, j = cur_jq * 4 + wl;
+            const bool active = r < n_rows && j < n_rx;
+            float4 pk = make_float4(0.f, 0.f, 0.f, 0.f);
+            float qx = 1.f, qy = 0.f, qz = 0.f;
+            if (active) {
+                pk = rpos[r];
+                qx = static_cast<float>(rx[3 * j]);
+                qy = static_cast<float>(rx[3 * j + 1]);
+                qz = static_cast<float>(rx[3 * j + 2]);
+            }
+            // ---- local features [v_hat, d, T, rho] (as k_cond_tc's feat_begin / feat_end)
+            float in[6];
+            {
+                const float px = active ? pk.x : 0.f, py = active ? pk.y : 0.f, pz = active ? pk.z : 0.f;
+                const float dx = qx - px, dy = qy - py, dz = qz - pz;
+                const float d = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+                const float inv = 1.f / d;
+                in[0] = dx * inv;
+                in[1] = dy * inv;
+                in[2] = dz * inv;
+                in[3] = d;
+                in[4] = 1.f;
+                in[5] = 0.f;
+                if (c.probe) {
+                    const float b0 = fmaf(px, W.icell[0], -W.blo[0]);
+                    const float b1 = fmaf(py, W.icell[1], -W.blo[1]);
+                    const float b2 = fmaf(pz, W.icell[2], -W.blo[2]);
+                    const float s0 = dx * W.icell[0], s1 = dy * W.icell[1], s2 = dz * W.icell[2];
+                    auto inside = [&](float tt) {
+                        const float u0 = fmaf(tt, s0, b0), u1 = fmaf(tt, s1, b1), u2 = fmaf(tt, s2, b2);
+                        return u0 >= -1.f && u0 <= hiR && u1 >= -1.f && u1 <= hiR && u2 >= -1.f && u2 <= hiR;
+                    };
+                    const bool ok = !active || (inside(tfirst) && inside(tlast));
+                    float tr = 1.f, sum = 0.f;
+                    if (__all_sync(0xffffffffu, ok)) {
+                        if constexpr (kPairs) {
+                            float2 tr2 = make_float2(1.f, 1.f), sum2 = make_float2(0.f, 0.f);
+                            if (active) probe_pairs_cube<ST, RT, 0, ST / 2>(c.cube, b0, b1, b2, s0, s1, s2, tr2, sum2);
+                            tr = tr2.x * tr2.y;
+                            sum = sum2.x + sum2.y;
+                        } else {
+                            if (active) probe_seg_cube<ST, RT, false>(c.cube, R, S, b0, b1, b2, s0, s1, s2, tr, sum);
+                        }
+                    } else if (active) {
+                        probe_seg_cube<ST, RT, true>(c.cube, R, S, b0, b1, b2, s0, s1, s2, tr, sum);
+                    }
+                    in[4] = tr;
+                    in[5] = sum * (1.f / static_cast<float>(S));
+                }
+            }
+            // ---- FLE reduction M = sum_l [(1+aG_l) GB_l + bG_l B_l], Bs = sum_l B_l
+            float2 M = make_float2(0.f, 0.f), Bs = make_float2(0.f, 0.f);
+            if (!YOUT && active) {
+                const float4 sums = rS[r];
+                Bs = make_float2(sums.z, sums.w);
+                if (Mpre) {
+                    M = Mpre[static_cast<size_t>(j) * cap + r];
+                } else {
+                    M = make_float2(sums.x, sums.y);
+                    const float4* a4 = reinterpret_cast<const float4*>(ag) + static_cast<size_t>(j) * L;
+                    const float4* e4 = rGB + r;
+                    float2 M1 = make_float2(0.f, 0.f);
+                    auto acc = [](float2 m, float4 e, float4 a) {
+                        m = x2::fma(x2::bc(a.x), make_float2(e.x, e.y), m);
+                        m = x2::fma(make_float2(-e.y, e.x), x2::bc(a.y), m);
+                        m = x2::fma(x2::bc(a.z), make_float2(e.z, e.w), m);
+                        return x2::fma(make_float2(-e.w, e.z), x2::bc(a.w), m);
+                    };
+                    int l = 0;
+                    for (; l + 4 <= L; l += 4) {
+                        float4 e[4], a[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            e[u] = e4[static_cast<size_t>(l + u) * cap];
+                            a[u] = a4[l + u];
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; u += 2) {
+                            M = acc(M, e[u], a[u]);
+                            M1 = acc(M1, e[u + 1], a[u + 1]);
+                        }
+                    }
+                    for (; l < L; ++l) M = acc(M, e4[static_cast<size_t>(l) * cap], a4[l]);
+                    M = x2::add(M, M1);
+                }
+            }
+            // ---- hand the tile to the MLP group: A1 = [x_hi, 1, 0, x_lo, 0, 0] + (M, Bs)
+            uint32_t a[8];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) x2::split_bf16(in[2 * q], in[2 * q + 1], a[q], a[4 + q]);
+            a[3] = 0x3F80u;  // (1, 0): the bias feature
+            a[7] = 0u;
+            if (t >= kWsSlots) {
+                RXGS_WS_EMPTY_WAIT(&empty[g][s], eph);
+                if (s == kWsSlots - 1) eph ^= 1u;
+            }
+            uint8_t* a1s = slot_a1(s);
+            *reinterpret_cast<uint4*>(a1s + canon_off16(arow, 0)) = make_uint4(a[0], a[1], a[2], a[3]);
+            *reinterpret_cast<uint4*>(a1s + canon_off16(arow, 8)) = make_uint4(a[4], a[5], a[6], a[7]);
+            if (!YOUT) slot_mb(s)[arow] = make_float4(M.x, M.y, Bs.x, Bs.y);
+            tc::fence_proxy_async_smem();  // generic-proxy stores -> the MMA's async-proxy reads
+            tc::mbar_arrive(&full[g][s]);
+            if (++s == kWsSlots) s = 0;
+            advance();
+        }
+        return;
+    }
+
+    // ======================================================== MLP warps
+#if RXGS_WS_REG_MLP
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(RXGS_WS_REG_MLP));
+#endif
+    const uint32_t tbase = tbase_s;
+    const uint32_t lane_off = static_cast<uint32_t>(32 * wl) << 16;
+    const uint32_t tm_a = tbase + 128 * g;  // h1 accumulator, split in place into the layer-2 A operand
+    const uint32_t tm_d = tm_a + 64;        // h2 accumulator
+    const uint32_t w2hi_a = tc::smem_u32(w2hi), w2lo_a = tc::smem_u32(w2lo);
+    const uint32_t w1hi_a = tc::smem_u32(w1hi), w1lo_a = tc::smem_u32(w1lo);
+    const uint32_t b2hi_a = tc::smem_u32(b2hi), aone_a = tc::smem_u32(aone);
+    // layer 1: two K=16 MMAs (hi.hi + lo.hi + bias, hi.lo) from ring slot s -> tm_a
+    auto issue_l1 = [&](int s, uint32_t fph) {
+        tc::mbar_wait(&full[g][s], fph);
+        tc::fence_after_sync();
+        const uint64_t ad = tc::sdesc_kmajor_noswizzle(tc::smem_u32(slot_a1(s)), 128, 256);
+        tc::mma_ss(tm_a, ad, tc::sdesc_kmajor_noswizzle(w1hi_a, 128, 256), kIdesc, 0u);
+        tc::mma_ss(tm_a, ad, tc::sdesc_kmajor_noswizzle(w1lo_a, 128, 256), kIdesc, 1u);
+        tc::mma_commit(&bar1[g]);
+    };
+    const bool leader = wl == 0 && lane == 0;
+    if (leader && tile < tiles) issue_l1(0, 0u);
+    __syncwarp();
+    uint32_t ph1 = 0, ph2 = 0, fph = 0;
+    int s = 0;
+    for (; tile < tiles; tile += step) {
+        const int r = cur_gb * 32 + lane, j = cur_jq * 4 + wl;
+        const bool active = r < n_rows && j < n_rx;
+        const int k = active ? rows[r] : 0;
+        // ---- h1 ready: ReLU -> bf16 hi/lo written back in place (chunk ch's 16
+        // f32 columns become its 8 hi + 8 lo columns: the layer-2 A operand)
+        RXGS_WS_MMA_WAIT(&bar1[g], ph1);
+        ph1 ^= 1u;
+        tc::fence_after_sync();
+        float4 mb = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (!YOUT) {
+            tc::mbar_wait(&full[g][s], fph);  // completed already (the MMA consumed the slot): visibility
+            mb = slot_mb(s)[arow];
+        }
+        {
+            uint32_t vb[2][16];
+            tc::tmem_ld16(tm_a + lane_off, vb[0]);
+            tc::wait_ld_regs(vb[0]);
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) {
+                uint32_t(&v)[16] = vb[ch & 1];
+                uint32_t hi[8], lo[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    x2::relu_split_bf16(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]), hi[q], lo[q]);
+                tc::tmem_st8(tm_a + lane_off + 16 * ch, hi);
+                tc::tmem_st8(tm_a + lane_off + 16 * ch + 8, lo);
+                if (ch + 1 < 4) {
+                    tc::tmem_ld16(tm_a + lane_off + 16 * (ch + 1), vb[(ch + 1) & 1]);
+                    tc::wait_ld_regs(vb[(ch + 1) & 1]);
+                }
+            }
+        }
+        tc::wait_st();
+        tc::fence_before_sync();
+        // ---- layer 2: D = 1 b2 + Ahi Bhi + Ahi Blo + Alo Bhi; the slot is free after it
+        if (arrive_last(&arrivals[g], lane) && lane == 0) {
+            tc::fence_after_sync();
+            tc::mma_ss(tm_d, tc::sdesc_kmajor_noswizzle(aone_a, 128, 256), tc::sdesc_kmajor_noswizzle(b2hi_a, 128, 256),
+                       kIdesc, 0u);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint64_t bh = tc::sdesc_kmajor_noswizzle(w2hi_a + 256 * q, 128, 1024);
+                const uint64_t bl = tc::sdesc_kmajor_noswizzle(w2lo_a + 256 * q, 128, 1024);
+                tc::mma_ts(tm_d, tm_a + 16 * q, bh, kIdesc, 1u);
+                tc::mma_ts(tm_d, tm_a + 16 * q, bl, kIdesc, 1u);
+                tc::mma_ts(tm_d, tm_a + 16 * q + 8, bh, kIdesc, 1u);
+            }
+            tc::mma_commit(&bar2[g]);
+            tc::mbar_arrive(&empty[g][s]);  // A1 consumed by layer 1, (M, Bs) read by all 128 threads
+        }
+        const int sn = s + 1 == kWsSlots ? 0 : s + 1;
+        const uint32_t fphn = sn == 0 ? fph ^ 1u : fph;
+        RXGS_WS_MMA_WAIT(&bar2[g], ph2);
+        ph2 ^= 1u;
+        tc::fence_after_sync();
+        // ---- the next tile's layer 1 (tm_a is free: layer 2 has read it) runs under layer 3
+        if (leader && tile + step < tiles) issue_l1(sn, fphn);
+        __syncwarp();
+        float2 ya = make_float2(W.b3[0], W.b3[1]), yb = make_float2(W.b3[2], W.b3[3]);
+        float2 ya1 = make_float2(0.f, 0.f), yb1 = make_float2(0.f, 0.f);
+        {
+            uint32_t vb[2][16];
+            tc::tmem_ld16(tm_d + lane_off, vb[0]);
+            tc::wait_ld_regs(vb[0]);
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) {
+                uint32_t(&v)[16] = vb[ch & 1];
+#pragma unroll
+                for (int q = 0; q < 16; q += 2) {
+                    const float4 w3 = W.w3[16 * ch + q], w3b = W.w3[16 * ch + q + 1];
+                    const float2 h2 = x2::bc(fmaxf(__uint_as_float(v[q]), 0.f));
+                    const float2 h2b = x2::bc(fmaxf(__uint_as_float(v[q + 1]), 0.f));
+                    ya = x2::fma(h2, make_float2(w3.x, w3.y), ya);
+                    yb = x2::fma(h2, make_float2(w3.z, w3.w), yb);
+                    ya1 = x2::fma(h2b, make_float2(w3b.x, w3b.y), ya1);
+                    yb1 = x2::fma(h2b, make_float2(w3b.z, w3b.w), yb1);
+                }
+                if (ch + 1 < 4) {
+                    tc::tmem_ld16(tm_d + lane_off + 16 * (ch + 1), vb[(ch + 1) & 1]);
+                    tc::wait_ld_regs(vb[(ch + 1) & 1]);
+                }
+            }
+        }
+        ya = x2::add(ya, ya1);
+        yb = x2::add(yb, yb1);
+        tc::fence_before_sync();  // the next layer-2 MMA overwrites tm_d after the group rendezvous
+        if (active) {
+            if (YOUT) {
+                ycache[static_cast<size_t>(k) * n_rx + j] = make_float4(ya.x, ya.y, yb.x, yb.y);
+            } else {
+                const float2 M = make_float2(mb.x, mb.y), Bs = make_float2(mb.z, mb.w);
+                const float2 al = c.additive ? make_float2(0.f, 0.f) : ya;
+                float2 sg = x2::fma(x2::bc(al.x), M, M);
+                sg = x2::fma(make_float2(-M.y, M.x), x2::bc(al.y), sg);
+                sg = x2::fma(x2::bc(yb.x), Bs, sg);
+                sg = x2::fma(make_float2(-Bs.y, Bs.x), x2::bc(yb.y), sg);
+                store_sig(sig, k, n_rx, j, 1, 0, sg);
+            }
+        }
+        s = sn;
+        fph = fphn;
+        advance();
+    }
+    tc::fence_before_sync();
+    tc::named_bar_sync(1, 128 * kGroups);
+    if (warp == 0) tc::tmem_dealloc(tbase, 512);
+}
+
 // ------------------------------------------------------------------ self test
 // 128x64x64 bf16 GEMM through both operand paths (A in TMEM and A in shared
 // memory) against FP32 FMA of the same bf16 values.
@@ -948,6 +1329,21 @@ bool cond_tc_eligible(const rxgs_cond_s* c) {
            (RXGS_PROBE_CUBE || kFixedSmem + padded_dim(c->R) * padded_dim(c->R) * padded_dim(c->R) * 4 <= 227 * 1024);
 }
 
+// RXGS_COND_WS=1 selects the warp-specialised k_cond_ws (A/B, bit-identical
+// signals).  Measured on config 2: 2.60 ms against 2.43 ms for k_cond_tc
+// (producers at 64 registers keep ~2 cube loads in flight; setmaxnreg
+// splits and a 3-slot ring were slower still), so k_cond_tc is the default.
+bool cond_ws_enabled() {
+#ifdef RXGS_FORCE_TC
+    return false;
+#endif
+    static const bool on = [] {
+        const char* v = std::getenv("RXGS_COND_WS");
+        return v && v[0] == '1';
+    }();
+    return on;
+}
+
 namespace {
 
 template <bool YOUT>
@@ -987,6 +1383,14 @@ cudaError_t launch_tc(const rxgs_cond_s& cs, const int* n_rows_dev, long long ro
         pk<<<sms * 8, 256, 0, s>>>(w, d, n_rows_dev, cap, rpos, d_rx, n_rx, probe_buf);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         probe_in = probe_buf;
+    }
+    if (!probe_in && cond_ws_enabled()) {
+        auto wk = fast ? k_cond_ws<16, 32, YOUT> : k_cond_ws<0, 0, YOUT>;
+        if ((e = cudaFuncSetAttribute(wk, cudaFuncAttributeMaxDynamicSharedMemorySize, kWsSmem)) != cudaSuccess)
+            return e;
+        wk<<<blocks, kWsThreads, kWsSmem, s>>>(w, d, n_rows_dev, static_cast<int>(rows_host), cap, rows, rpos, d_rx,
+                                               n_rx, rGB, rS, d_ag, Mpre, d_sig, ycache);
+        return cudaGetLastError();
     }
     kern<<<blocks, kThreads, smem, s>>>(w, d, n_rows_dev, static_cast<int>(rows_host), cap, rows, rpos, d_rx, n_rx,
                                         rGB, rS, d_ag, Mpre, d_sig, ycache, probe_in);

@@ -326,6 +326,7 @@ cudaError_t launch_check_coincide(const rxgs_scene_s& sc, const double* d_rx, in
                                   cudaStream_t s);
 // tcgen05 variant of the hot kernel (k_cond_tc.cu): hidden 64, C == 1.
 bool cond_tc_eligible(const rxgs_cond_s* c);
+bool cond_ws_enabled();
 cudaError_t launch_cond_signal_tc(const rxgs_cond_s& c, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
                                   const double* d_rx, int n_rx, const float* d_ag, SigOut d_sig,
                                   cudaStream_t s);
