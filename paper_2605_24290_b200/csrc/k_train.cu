@@ -24,9 +24,12 @@
 // Every reduction runs in a fixed order (no floating-point atomics), so a
 // step is bitwise reproducible, as the reference requires.
 
+#include <cuda.h>
+
 #include "cond_common.cuh"
 #include "f32x2.cuh"
 #include "rxgs_internal.cuh"
+#include "tc_util.cuh"
 
 namespace rxgs_b200 {
 namespace {
@@ -576,8 +579,24 @@ __global__ void __launch_bounds__(kBwdThreads) k_cond_bwd(CondDev c, const int* 
 #ifndef RXGS_BWD_GRAD_CTAS
 #define RXGS_BWD_GRAD_CTAS 4
 #endif
-constexpr int kActF = 6 + 4 + 4 * 64;  // activation features per row
-constexpr int kAh1 = 0, kAh2 = 64, kAdh1 = 128, kAdh2 = 192, kAx = 256, kAdy = 262;  // 16-byte aligned blocks
+// activations per row as bf16 hi/lo feature planes act[plane][f][row]
+// (hi = bf16(v), lo = bf16(v - hi)); the feature order groups the operands
+// of k_cond_grads_tc's two GEMMs over rows: [dh2 | dh1] (A of GEMM 1),
+// [h1 | x] (B of GEMM 1), h2 (A of GEMM 2), dy (B of GEMM 2)
+constexpr int kActF = 4 * 64 + 6 + 4;  // activation features per row
+constexpr int kAdh2 = 0, kAdh1 = 64, kAh1 = 128, kAx = 192, kAh2 = 198, kAdy = 262;
+constexpr int kActRowAlign = 64;       // rows padded to the grads kernel's K chunk
+
+struct ActOut {
+    uint16_t* p;
+    long long rpad;
+    __device__ __forceinline__ void put(long long row, int f, float v) const {
+        const uint32_t h = tc::pack_bf16(v, 0.f) & 0xFFFFu;
+        const uint32_t l = tc::pack_bf16(v - __uint_as_float(h << 16), 0.f) & 0xFFFFu;
+        p[static_cast<size_t>(f) * rpad + row] = static_cast<uint16_t>(h);
+        p[static_cast<size_t>(kActF + f) * rpad + row] = static_cast<uint16_t>(l);
+    }
+};
 
 template <int ST, int RT>
 __global__ void __launch_bounds__(128, 3) k_cond_bwd_rows(CondDev c, const int* __restrict__ n_rows,
@@ -585,8 +604,7 @@ __global__ void __launch_bounds__(128, 3) k_cond_bwd_rows(CondDev c, const int* 
                                                           const double* __restrict__ rx, int n_rx,
                                                           const float2* __restrict__ Bm, const float2* __restrict__ GB,
                                                           const float* __restrict__ ag, const float2* __restrict__ d_s,
-                                                          float2* __restrict__ u_out, float* __restrict__ act,
-                                                          long long rpad) {
+                                                          float2* __restrict__ u_out, ActOut act) {
     constexpr int H = 64;
     extern __shared__ __align__(16) float sm[];
     float* sW2 = sm;
@@ -600,6 +618,12 @@ __global__ void __launch_bounds__(128, 3) k_cond_bwd_rows(CondDev c, const int* 
     __syncthreads();
     const long long rows_total = static_cast<long long>(*n_rows) * n_rx;
     const int L = c.L;
+    if (blockIdx.x == 0) {  // zero the last 64-row chunk's tail: k_cond_grads_tc reads whole chunks
+        const long long tail_end = (rows_total + kActRowAlign - 1) / kActRowAlign * kActRowAlign;
+        for (long long e = threadIdx.x; e < (tail_end - rows_total) * 2 * kActF; e += blockDim.x)
+            act.p[static_cast<size_t>(e / (tail_end - rows_total)) * act.rpad + rows_total +
+                  e % (tail_end - rows_total)] = 0;
+    }
     for (long long base_row = static_cast<long long>(blockIdx.x) * blockDim.x; base_row < rows_total;
          base_row += static_cast<long long>(gridDim.x) * blockDim.x) {
         const long long row = base_row + threadIdx.x;
@@ -616,7 +640,6 @@ __global__ void __launch_bounds__(128, 3) k_cond_bwd_rows(CondDev c, const int* 
             u_out[static_cast<size_t>(k) * n_rx + j] = d_s[static_cast<size_t>(k) * n_rx + j];
             continue;
         }
-        float* a = act + row;
         float h1[H];
 #pragma unroll
         for (int o = 0; o < H; ++o) {
@@ -624,7 +647,7 @@ __global__ void __launch_bounds__(128, 3) k_cond_bwd_rows(CondDev c, const int* 
 #pragma unroll
             for (int i = 0; i < 6; ++i) acc = fmaf(p[c.o_lw1 + o * 6 + i], x[i], acc);
             h1[o] = fmaxf(acc, 0.f);
-            a[(kAh1 + o) * rpad] = h1[o];
+            act.put(row, kAh1 + o, h1[o]);
         }
         float y[4] = {p[c.o_lb3], p[c.o_lb3 + 1], p[c.o_lb3 + 2], p[c.o_lb3 + 3]};
         uint32_t pos_lo = 0u, pos_hi = 0u;  // h2 > 0 mask (the ReLU of layer 2)
@@ -647,8 +670,8 @@ __global__ void __launch_bounds__(128, 3) k_cond_bwd_rows(CondDev c, const int* 
             for (int u = 0; u < 4; ++u) {
                 const int o = 2 * (op0 + u);
                 const float hv0 = fmaxf(ac[u].x, 0.f), hv1 = fmaxf(ac[u].y, 0.f);
-                a[(kAh2 + o) * rpad] = hv0;
-                a[(kAh2 + o + 1) * rpad] = hv1;
+                act.put(row, kAh2 + o, hv0);
+                act.put(row, kAh2 + o + 1, hv1);
                 const uint32_t bits = (hv0 > 0.f ? 1u : 0u) | (hv1 > 0.f ? 2u : 0u);
                 if (o < 32) pos_lo |= bits << o; else pos_hi |= bits << (o - 32);
 #pragma unroll
@@ -677,9 +700,9 @@ __global__ void __launch_bounds__(128, 3) k_cond_bwd_rows(CondDev c, const int* 
         dy[3] = db.y;
         u_out[static_cast<size_t>(k) * n_rx + j] = cmul(make_float2(1.f + ar, -ai), ds);
 #pragma unroll
-        for (int f = 0; f < 6; ++f) a[(kAx + f) * rpad] = x[f];
+        for (int f = 0; f < 6; ++f) act.put(row, kAx + f, x[f]);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) a[(kAdy + q) * rpad] = dy[q];
+        for (int q = 0; q < 4; ++q) act.put(row, kAdy + q, dy[q]);
         float2 dh1[H / 2];
 #pragma unroll
         for (int i = 0; i < H / 2; ++i) dh1[i] = make_float2(0.f, 0.f);
@@ -690,7 +713,7 @@ __global__ void __launch_bounds__(128, 3) k_cond_bwd_rows(CondDev c, const int* 
             for (int q = 0; q < 4; ++q) gs = fmaf(p[c.o_lw3 + q * H + o], dy[q], gs);
             const bool on = ((o < 32 ? pos_lo >> o : pos_hi >> (o - 32)) & 1u) != 0u;
             const float g = on ? gs : 0.f;
-            a[(kAdh2 + o) * rpad] = g;
+            act.put(row, kAdh2 + o, g);
             if (g == 0.f) continue;
             const float2* wr = reinterpret_cast<const float2*>(sW2 + o * H);
 #pragma unroll
@@ -698,92 +721,194 @@ __global__ void __launch_bounds__(128, 3) k_cond_bwd_rows(CondDev c, const int* 
         }
 #pragma unroll
         for (int i = 0; i < H / 2; ++i) {
-            a[(kAdh1 + 2 * i) * rpad] = h1[2 * i] > 0.f ? dh1[i].x : 0.f;
-            a[(kAdh1 + 2 * i + 1) * rpad] = h1[2 * i + 1] > 0.f ? dh1[i].y : 0.f;
+            act.put(row, kAdh1 + 2 * i, h1[2 * i] > 0.f ? dh1[i].x : 0.f);
+            act.put(row, kAdh1 + 2 * i + 1, h1[2 * i + 1] > 0.f ? dh1[i].y : 0.f);
         }
     }
 }
 
-#ifndef RXGS_GRAD_ROWS
-#define RXGS_GRAD_ROWS 32
-#endif
-constexpr int kGradRows = RXGS_GRAD_ROWS;  // rows staged per step in k_cond_bwd_grads
+// Weight gradients of the local MLP as two GEMMs over rows on tcgen05
+// (conditioning.cpp:472-587, mlp_backward: g.w += dy x h summed over the
+// batch), K = rows, fed by the TMA engine from the bf16 hi/lo feature planes:
+//   GEMM 1: D1[128 x 80] += A1 B1^T,  A1 = [dh2 | dh1] (M 128),
+//           B1 = [h1 | x | 1 | 0..] (N 80)  ->  dW2 | db2 (rows 0-63),
+//                                              dW1 | db1 (rows 64-127);
+//   GEMM 2: D2[128 x 16] += A2 B2^T,  A2 = [h2 | 1 ..] (M 128),
+//           B2 = [dy | 0..] (N 16)       ->  dW3^T (rows 0-63), db3 (row 64).
+// bf16x3 (Ahi Bhi + Ahi Blo + Alo Bhi, ~2^-17), f32 accumulation in TMEM over
+// a contiguous row range per CTA, partials in CTA order (k_reduce_parts):
+// deterministic.  Operand tiles are K-major, 128-byte swizzled (64 rows =
+// one 128 B line per feature); the constant rows (the bias "1" features and
+// the zero padding) are written once per stage buffer and never by the TMA.
+// Per 64-row chunk: 8 tiled TMA loads (68 KB), 24 MMAs; 2-stage ring.
+constexpr int kGradK = 64;                              // rows per chunk (one SW128 line)
+constexpr int kG1N = 80, kG2N = 16;
+constexpr int kGA1 = 128 * 128, kGB1 = kG1N * 128, kGA2 = 128 * 128, kGB2 = kG2N * 128;  // bytes per plane
+constexpr int kGOffA1 = 0, kGOffB1 = 2 * kGA1, kGOffA2 = kGOffB1 + 2 * kGB1, kGOffB2 = kGOffA2 + 2 * kGA2;
+constexpr int kGStage = kGOffB2 + 2 * kGB2;             // 90112 B
+constexpr int kGStages = 2;
+constexpr uint32_t kGTx = 2u * (128 + 70 + 64 + 4) * 128;  // bytes the TMA brings per chunk
+constexpr uint32_t kGIdesc1 = tc::idesc_bf16_f32(128, kG1N), kGIdesc2 = tc::idesc_bf16_f32(128, kG2N);
 
-__global__ void __launch_bounds__(256) k_cond_bwd_grads(const float* __restrict__ act, long long rpad,
-                                                        const int* __restrict__ n_rows, int n_rx,
-                                                        float* __restrict__ part) {
-    constexpr int H = 64, PF = kActF + 2;  // row pitch 268 floats: 16-byte aligned rows
-    __shared__ __align__(16) float sA[kGradRows * PF];  // [row][feature]
-    const int t = threadIdx.x;
+__device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t saddr) {  // K-major, 128 B swizzle, 8-row groups 1 KB
+    return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (1ull << 16) | (static_cast<uint64_t>(1024 >> 4) << 32) |
+           (1ull << 46) | (2ull << 61);
+}
+__device__ __forceinline__ void g_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void g_tma_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(tc::smem_u32(bar))
+        : "memory");
+}
+
+__global__ void __launch_bounds__(128, 1) k_cond_grads_tc(const __grid_constant__ CUtensorMap tm_a1,
+                                                          const __grid_constant__ CUtensorMap tm_b1,
+                                                          const __grid_constant__ CUtensorMap tm_a2,
+                                                          const __grid_constant__ CUtensorMap tm_b2,
+                                                          const int* __restrict__ n_rows, int n_rx,
+                                                          float* __restrict__ part) {
+    constexpr int H = 64;
+    extern __shared__ uint8_t g_smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(g_smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t full[kGStages], empty[kGStages], done;
+    __shared__ uint32_t tbase_s;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const long long rows_total = static_cast<long long>(*n_rows) * n_rx;
-    const long long per = ((rows_total + gridDim.x - 1) / gridDim.x + kGradRows - 1) / kGradRows * kGradRows;
-    const long long r_begin = static_cast<long long>(blockIdx.x) * per;
-    const long long r_end = r_begin + per < rows_total ? r_begin + per : rows_total;
-    const int o0 = (t >> 4) * 4, i0 = (t & 15) * 4;  // dW2 tile of this thread
-    float2 w2[8];  // row a, column pair bp: w2[a * 2 + bp]
-#pragma unroll
-    for (int q = 0; q < 8; ++q) w2[q] = make_float2(0.f, 0.f);
-    float w1[2] = {0.f, 0.f}, w3 = 0.f, bsum = 0.f;
-    // the next stage's activations are loaded into registers while this one
-    // is consumed from shared memory (one stage of software pipelining)
-    constexpr int kPer = (kActF * kGradRows + 255) / 256;
-    float nxt[kPer];
-    auto fetch = [&](long long r0) {
-        const int nr = r_end - r0 < kGradRows ? static_cast<int>(r_end - r0) : kGradRows;
-#pragma unroll
-        for (int u = 0; u < kPer; ++u) {
-            const int e = t + 256 * u;
-            const int f = e / kGradRows, r = e % kGradRows;
-            nxt[u] = (e < kActF * kGradRows && r < nr) ? act[f * rpad + r0 + r] : 0.f;
+    const long long chunks = (rows_total + kGradK - 1) / kGradK;
+    const long long per = (chunks + gridDim.x - 1) / gridDim.x;
+    const long long c_begin = static_cast<long long>(blockIdx.x) * per;
+    const long long c_end = c_begin + per < chunks ? c_begin + per : chunks;
+    const int n_chunks = c_begin < c_end ? static_cast<int>(c_end - c_begin) : 0;
+
+    // constant rows of every stage: B1 row 70 = 1 (hi) / 0 (lo), rows 71-79 =
+    // 0; A2 rows 64-127 = 1 (hi) / 0 (lo); B2 rows 4-15 = 0.  Each row is one
+    // 128 B line of a swizzle atom; uniform rows are swizzle-invariant.
+    for (int i = tid; i < kGStages * 2 * 10 * 32; i += blockDim.x) {  // B1 rows 70..79
+        const int st = i / (2 * 10 * 32), pl = (i / (10 * 32)) % 2, row = 70 + (i / 32) % 10, w = i % 32;
+        reinterpret_cast<uint32_t*>(smem + st * kGStage + kGOffB1 + pl * kGB1 + row * 128)[w] =
+            (row == 70 && pl == 0) ? 0x3F803F80u : 0u;
+    }
+    for (int i = tid; i < kGStages * 2 * 64 * 32; i += blockDim.x) {  // A2 rows 64..127
+        const int st = i / (2 * 64 * 32), pl = (i / (64 * 32)) % 2, row = 64 + (i / 32) % 64, w = i % 32;
+        reinterpret_cast<uint32_t*>(smem + st * kGStage + kGOffA2 + pl * kGA2 + row * 128)[w] =
+            pl == 0 ? 0x3F803F80u : 0u;
+    }
+    for (int i = tid; i < kGStages * 2 * 12 * 32; i += blockDim.x) {  // B2 rows 4..15
+        const int st = i / (2 * 12 * 32), pl = (i / (12 * 32)) % 2, row = 4 + (i / 32) % 12, w = i % 32;
+        reinterpret_cast<uint32_t*>(smem + st * kGStage + kGOffB2 + pl * kGB2 + row * 128)[w] = 0u;
+    }
+    if (warp == 0) {
+        tc::tmem_alloc(&tbase_s, 128);
+        tc::tmem_relinquish();
+    }
+    if (tid == 0) {
+        for (int q = 0; q < kGStages; ++q) {
+            tc::mbar_init(&full[q], 1);
+            tc::mbar_init(&empty[q], 1);
         }
-    };
-    if (r_begin < r_end) fetch(r_begin);
-    for (long long r0 = r_begin; r0 < r_end; r0 += kGradRows) {
-        __syncthreads();
+        tc::mbar_init(&done, 1);
+        tc::fence_mbar_init();
+    }
+    tc::fence_proxy_async_smem();  // the constant rows -> the MMA's async-proxy reads
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tm_d1 = tbase_s, tm_d2 = tbase_s + 96;
+    const uint32_t sbase = tc::smem_u32(smem);
+
+    if (warp == 0 && lane == 0) {  // TMA producer
+        for (int i = 0; i < n_chunks; ++i) {
+            const int s = i % kGStages;
+            if (i >= kGStages) tc::mbar_wait(&empty[s], ((i / kGStages) - 1) & 1);
+            const int x = static_cast<int>((c_begin + i) * kGradK);
+            const uint32_t st = sbase + s * kGStage;
+            g_expect_tx(&full[s], kGTx);
 #pragma unroll
-        for (int u = 0; u < kPer; ++u) {
-            const int e = t + 256 * u;
-            if (e < kActF * kGradRows) sA[(e % kGradRows) * PF + e / kGradRows] = nxt[u];
+            for (int pl = 0; pl < 2; ++pl) {  // feature planes hi, lo
+                g_tma_2d(st + kGOffA1 + pl * kGA1, &tm_a1, x, pl * kActF + kAdh2, &full[s]);
+                g_tma_2d(st + kGOffB1 + pl * kGB1, &tm_b1, x, pl * kActF + kAh1, &full[s]);
+                g_tma_2d(st + kGOffA2 + pl * kGA2, &tm_a2, x, pl * kActF + kAh2, &full[s]);
+                g_tma_2d(st + kGOffB2 + pl * kGB2, &tm_b2, x, pl * kActF + kAdy, &full[s]);
+            }
         }
-        __syncthreads();
-        if (r0 + kGradRows < r_end) fetch(r0 + kGradRows);
-        for (int r = 0; r < kGradRows; ++r) {
-            const float* ar = sA + r * PF;
-            const float4 d4 = *reinterpret_cast<const float4*>(ar + kAdh2 + o0);
-            const float4 h4 = *reinterpret_cast<const float4*>(ar + kAh1 + i0);
-            const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+    } else if (warp == 1 && lane == 0) {  // MMA issuer
+        for (int i = 0; i < n_chunks; ++i) {
+            const int s = i % kGStages;
+            tc::mbar_wait(&full[s], (i / kGStages) & 1);
+            tc::fence_after_sync();
+            const uint32_t st = sbase + s * kGStage;
 #pragma unroll
-            for (int a = 0; a < 4; ++a) {  // FFMA2 over column pairs (each lane exactly fmaf)
-                w2[2 * a] = x2::fma(x2::bc(dv[a]), make_float2(h4.x, h4.y), w2[2 * a]);
-                w2[2 * a + 1] = x2::fma(x2::bc(dv[a]), make_float2(h4.z, h4.w), w2[2 * a + 1]);
+            for (int ks = 0; ks < kGradK / 16; ++ks) {
+                const uint32_t ko = 32 * ks;  // 16 K elements within the swizzled 128 B line
+                const uint32_t acc0 = (i > 0 || ks > 0) ? 1u : 0u;
+                const uint64_t a1h = sdesc_k_sw128(st + kGOffA1 + ko), a1l = sdesc_k_sw128(st + kGOffA1 + kGA1 + ko);
+                const uint64_t b1h = sdesc_k_sw128(st + kGOffB1 + ko), b1l = sdesc_k_sw128(st + kGOffB1 + kGB1 + ko);
+                tc::mma_ss(tm_d1, a1h, b1h, kGIdesc1, acc0);
+                tc::mma_ss(tm_d1, a1h, b1l, kGIdesc1, 1u);
+                tc::mma_ss(tm_d1, a1l, b1h, kGIdesc1, 1u);
+                const uint64_t a2h = sdesc_k_sw128(st + kGOffA2 + ko), a2l = sdesc_k_sw128(st + kGOffA2 + kGA2 + ko);
+                const uint64_t b2h = sdesc_k_sw128(st + kGOffB2 + ko), b2l = sdesc_k_sw128(st + kGOffB2 + kGB2 + ko);
+                tc::mma_ss(tm_d2, a2h, b2h, kGIdesc2, acc0);
+                tc::mma_ss(tm_d2, a2h, b2l, kGIdesc2, 1u);
+                tc::mma_ss(tm_d2, a2l, b2h, kGIdesc2, 1u);
             }
+            tc::mma_commit(&empty[s]);
+        }
+        tc::mma_commit(&done);
+    }
+    __syncwarp();
+    if (n_chunks > 0) tc::mbar_wait_backoff(&done, 0);
+    tc::fence_after_sync();
+    // ---- epilogue: TMEM lane m = 32 warp + lane = row m of D1 / D2
+    constexpr int NG = local_grad_count(H);
+    constexpr int o_w1 = 0, o_b1 = H * 6, o_w2 = o_b1 + H, o_b2 = o_w2 + H * H, o_w3 = o_b2 + H, o_b3 = o_w3 + 4 * H;
+    float* out = part + static_cast<size_t>(blockIdx.x) * NG;
+    const int m = 32 * warp + lane;
+    const uint32_t lo = static_cast<uint32_t>(32 * warp) << 16;
+    uint32_t r[16];
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int idx = t + 256 * e;  // dW1 entry (o, f) of 384
-                if (idx < H * 6) w1[e] = fmaf(ar[kAdh1 + idx / 6], ar[kAx + idx % 6], w1[e]);
+    for (int cb = 0; cb < 5; ++cb) {  // D1 columns 16 cb ..
+        if (n_chunks > 0) {
+            tc::tmem_ld16(tm_d1 + lo + 16 * cb, r);
+            tc::wait_ld();
+        } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) r[q] = 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int col = 16 * cb + q;
+            const float v = __uint_as_float(r[q]);
+            if (m < H) {  // dh2 row o = m
+                if (col < H) out[o_w2 + m * H + col] = v;
+                else if (col == 70) out[o_b2 + m] = v;
+            } else {      // dh1 row o = m - 64
+                if (col >= 64 && col < 70) out[o_w1 + (m - H) * 6 + (col - 64)] = v;
+                else if (col == 70) out[o_b1 + (m - H)] = v;
             }
-            w3 = fmaf(ar[kAdy + t / H], ar[kAh2 + t % H], w3);  // dW3 (q, o)
-            if (t < H) bsum += ar[kAdh1 + t];                    // db1
-            else if (t < 2 * H) bsum += ar[kAdh2 + t - H];       // db2
-            else if (t < 2 * H + 4) bsum += ar[kAdy + t - 2 * H]; // db3
         }
     }
-    constexpr int NG = local_grad_count(H);
-    float* out = part + static_cast<size_t>(blockIdx.x) * NG;
-    const int o_w1 = 0, o_b1 = H * 6, o_w2 = o_b1 + H, o_b2 = o_w2 + H * H, o_w3 = o_b2 + H, o_b3 = o_w3 + 4 * H;
+    if (n_chunks > 0) {
+        tc::tmem_ld16(tm_d2 + lo, r);
+        tc::wait_ld();
+    } else {
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+        for (int q = 0; q < 16; ++q) r[q] = 0u;
+    }
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const float2 v = w2[2 * a + b / 2];
-            out[o_w2 + (o0 + a) * H + i0 + b] = (b & 1) ? v.y : v.x;
-        }
-    for (int e = 0; e < 2; ++e)
-        if (t + 256 * e < H * 6) out[o_w1 + t + 256 * e] = w1[e];
-    out[o_w3 + t] = w3;
-    if (t < H) out[o_b1 + t] = bsum;
-    else if (t < 2 * H) out[o_b2 + t - H] = bsum;
-    else if (t < 2 * H + 4) out[o_b3 + t - 2 * H] = bsum;
+    for (int q = 0; q < 4; ++q) {
+        const float v = __uint_as_float(r[q]);
+        if (m < H) out[o_w3 + q * H + m] = v;  // dW3[q][o] from row o = h2 feature
+        else if (m == H) out[o_b3 + q] = v;    // the "1" row: sum of dy
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(tbase_s, 128);
 }
 
 // sum CTA partials in CTA order into the f64 gradient vector
@@ -1106,19 +1231,53 @@ cudaError_t launch_render_adjoint(const rxgs_txstate_s& st, const float2* G, int
 size_t cond_bwd_smem() { return sizeof(float) * (2 * 64 * 64 + 4 * kBwdThreads * kBwdPad + kBwdThreads * 10); }
 // partial-sum CTAs: the split backward's gradient kernel needs many CTAs in
 // flight to cover its staged loads
-int cond_bwd_parts(int sms) { return RXGS_BWD_SPLIT ? sms * RXGS_BWD_GRAD_CTAS : sms * 2; }
+int cond_bwd_parts(int sms) { return RXGS_BWD_SPLIT ? sms : sms * 2; }  // split: one k_cond_grads_tc CTA per SM
 int local_grad_n() { return local_grad_count(64); }
 
 size_t cond_bwd_act_bytes(long long rows) {
-    return RXGS_BWD_SPLIT ? sizeof(float) * kActF * static_cast<size_t>((rows + 31) / 32 * 32) : 0;
+    return RXGS_BWD_SPLIT ? 2 * sizeof(uint16_t) * kActF *
+                                static_cast<size_t>((rows + kActRowAlign - 1) / kActRowAlign * kActRowAlign)
+                          : 0;
 }
+
+namespace {
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiled encode_tiled() {
+    static EncodeTiled fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiled>(p);
+    }();
+    return fn;
+}
+// the activation planes as a 2D bf16 tensor {rows (inner), 2 kActF features},
+// box {64 rows, box_f features}, 128-byte swizzle; rows past `rows` read as 0
+cudaError_t make_act_map(CUtensorMap* m, const void* base, uint64_t rows, long long rpad, uint32_t box_f) {
+    EncodeTiled enc = encode_tiled();
+    if (!enc) return cudaErrorNotSupported;
+    const cuuint64_t dims[2] = {rows, static_cast<cuuint64_t>(2 * kActF)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(rpad) * 2};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kGradK), box_f};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+}  // namespace
 
 cudaError_t launch_cond_bwd(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
                             const double* d_rx, int n_rx, const float* d_ag, const float2* d_s, float2* u,
                             float* part, int n_parts, cudaStream_t s, float* act) {
     const CondDev d = make_dev(cs);
     if (RXGS_BWD_SPLIT && act) {
-        const long long rpad = (static_cast<long long>(st.visible) * n_rx + 31) / 32 * 32;
+        const long long rows_bound = static_cast<long long>(st.visible) * n_rx;
+        const long long rpad = (rows_bound + kActRowAlign - 1) / kActRowAlign * kActRowAlign;
         const size_t smem_r = sizeof(float) * 2 * 64 * 64;
         auto kr = (d.S == 16 && d.R == 32) ? k_cond_bwd_rows<16, 32> : k_cond_bwd_rows<0, 0>;
         cudaError_t e = cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_r));
@@ -1126,11 +1285,25 @@ cudaError_t launch_cond_bwd(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        ActOut ao{reinterpret_cast<uint16_t*>(act), rpad};
         kr<<<sms * 3, 128, smem_r, s>>>(d, st.needed_count.as<int>(), st.needed_order.as<int>(),
                                         sc.d_pos32.as<float4>(), d_rx, n_rx, st.basis32.as<float2>(),
-                                        st.gb32.as<float2>(), d_ag, d_s, u, act, rpad);
+                                        st.gb32.as<float2>(), d_ag, d_s, u, ao);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        if (d.use_local) k_cond_bwd_grads<<<n_parts, 256, 0, s>>>(act, rpad, st.needed_count.as<int>(), n_rx, part);
+        if (!d.use_local) return cudaSuccess;
+        // the row extent of the tensor maps is the host bound (rows past the
+        // needed ones are never read: each CTA stops at needed x n_rx)
+        CUtensorMap ma1, mb1, ma2, mb2;
+        const uint64_t rows = static_cast<uint64_t>(rows_bound > 0 ? rows_bound : 1);
+        if ((e = make_act_map(&ma1, act, rows, rpad, 128)) != cudaSuccess) return e;
+        if ((e = make_act_map(&mb1, act, rows, rpad, 70)) != cudaSuccess) return e;
+        if ((e = make_act_map(&ma2, act, rows, rpad, 64)) != cudaSuccess) return e;
+        if ((e = make_act_map(&mb2, act, rows, rpad, 4)) != cudaSuccess) return e;
+        const size_t smem_g = static_cast<size_t>(kGStages) * kGStage + 1024;
+        if ((e = cudaFuncSetAttribute(k_cond_grads_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem_g))) != cudaSuccess)
+            return e;
+        k_cond_grads_tc<<<n_parts, 128, smem_g, s>>>(ma1, mb1, ma2, mb2, st.needed_count.as<int>(), n_rx, part);
         return cudaGetLastError();
     }
     const size_t smem = cond_bwd_smem();
