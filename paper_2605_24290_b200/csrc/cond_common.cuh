@@ -452,5 +452,38 @@ __device__ __forceinline__ void cube_features(const CondDev& c, bool active, flo
 }
 
 
+// activations per row as bf16 hi/lo feature planes act[plane][f][row]
+// (hi = bf16(v), lo = bf16(v - hi)); the feature order groups the operands
+// of k_cond_grads_tc's two GEMMs over rows: [dh2 | dh1] (A of GEMM 1),
+// [h1 | x] (B of GEMM 1), h2 (A of GEMM 2), dy (B of GEMM 2)
+constexpr int kActF = 4 * 64 + 6 + 4;  // activation features per row
+constexpr int kAdh2 = 0, kAdh1 = 64, kAh1 = 128, kAx = 192, kAh2 = 198, kAdy = 262;
+constexpr int kActRowAlign = 64;       // rows padded to the grads kernel's K chunk
+
+__device__ __forceinline__ uint32_t act_bf16(float v) {  // bf16 round to nearest, in the low half
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(0.f), "f"(v));
+    return r;
+}
+struct ActOut {
+    uint16_t* p;
+    long long rpad;
+    __device__ __forceinline__ void put(long long row, int f, float v) const {
+#ifdef RXGS_ACT_NOSTORE  // timing experiment only (wrong gradients)
+        if (v != 12345.f) return;
+#endif
+        const uint32_t h = act_bf16(v) & 0xFFFFu;
+        const uint32_t l = act_bf16(v - __uint_as_float(h << 16)) & 0xFFFFu;
+        p[static_cast<size_t>(f) * rpad + row] = static_cast<uint16_t>(h);
+        p[static_cast<size_t>(kActF + f) * rpad + row] = static_cast<uint16_t>(l);
+    }
+    // a value already split into bf16 hi / lo
+    __device__ __forceinline__ void put_bits(long long row, int f, uint32_t hi16, uint32_t lo16) const {
+        p[static_cast<size_t>(f) * rpad + row] = static_cast<uint16_t>(hi16);
+        p[static_cast<size_t>(kActF + f) * rpad + row] = static_cast<uint16_t>(lo16);
+    }
+};
+
+
 }  // namespace cond_dev
 }  // namespace rxgs_b200

@@ -1233,6 +1233,284 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     if (warp == 0) tc::tmem_dealloc(tbase, 512);
 }
 
+// ------------------------------------------------- training backward (rows)
+// k_cond_bwd_tc: the per-row half of condition_backward's local branch
+// (conditioning.cpp:472-587, mlp_backward :33-74) for the spectrum-L1
+// training step, on the same rows / tile mapping / TMEM layout as
+// k_cond_tc, with three MMA rounds per 128-row tile:
+//   layer 1 (A1 = [x_hi, 1, 0, x_lo, 0, 0])  -> h1 -> ReLU, bf16 hi/lo split
+//   layer 2 (1 b2 + A2 W2, bf16x3)          -> h2 -> ReLU, layer 3 (FFMA2), dy
+//   dh1 = W2^T dh2  (A = dh2 split, B = W2^T hi/lo in shared memory, bf16x3)
+// dh2 = (W3^T dy) * [h2 > 0] and the ReLU masks stay on the FP32 pipe.  The
+// activations go to the bf16 hi/lo feature planes read by k_cond_grads_tc
+// (the split values of h1 are the layer-2 operand itself).  The SIMT
+// k_cond_bwd_rows stays for the SSIM / DFT losses (train_api.cu).
+template <int ST, int RT>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_cond_bwd_tc(const __grid_constant__ LocalW W, CondDev c, const int* __restrict__ n_rows_dev,
+                  const int* __restrict__ rows, const float4* __restrict__ pos32, const double* __restrict__ rx,
+                  int n_rx, const float2* __restrict__ Bm, const float2* __restrict__ GB, const float* __restrict__ ag,
+                  const float2* __restrict__ d_s, float2* __restrict__ u_out, ActOut act) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* w2hi = smem;
+    uint8_t* w2lo = smem + kW2Bytes;
+    uint8_t* w1hi = smem + 2 * kW2Bytes;
+    uint8_t* w1lo = w1hi + kW1Bytes;
+    uint8_t* b2hi = w1lo + kW1Bytes;
+    uint8_t* aone = b2hi + 2 * kW1Bytes;
+    uint8_t* w2thi = smem + kFixedSmem;  // B[n = input i][k = output o] = W2[o][i]
+    uint8_t* w2tlo = w2thi + kW2Bytes;
+    __shared__ uint64_t bars[kGroups];
+    __shared__ uint32_t arrivals[kGroups];
+    __shared__ uint32_t tbase_s;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int g = warp >> 2, wl = warp & 3;
+    const int n_rows = *n_rows_dev;
+    const long long rows_total = static_cast<long long>(n_rows) * n_rx;
+    if (blockIdx.x == 0) {  // zero the last 64-row chunk's tail: k_cond_grads_tc reads whole chunks
+        const long long tail = (rows_total + kActRowAlign - 1) / kActRowAlign * kActRowAlign - rows_total;
+        for (long long e = tid; e < tail * 2 * kActF; e += kThreads)
+            act.p[static_cast<size_t>(e / tail) * act.rpad + rows_total + e % tail] = 0;
+    }
+    if (tid < kGroups) arrivals[tid] = 0u;
+    for (int i = tid; i < kH * kH; i += kThreads) {
+        const int a = i / kH, b = i % kH;
+        split_store(w2hi, w2lo, canon_off(a, b), c.p32[c.o_lw2 + i]);              // (n = o, k = i)
+        split_store(w2thi, w2tlo, canon_off(b, a), c.p32[c.o_lw2 + i]);            // (n = i, k = o)
+    }
+    for (int i = tid; i < kH * 16; i += kThreads) {
+        const int n = i / 16, k = i % 16;
+        const float w = k < 6 ? c.p32[c.o_lw1 + n * 6 + k] : (k == 6 ? c.p32[c.o_lb1 + n] : 0.f);
+        const float whi = tc::bf16_round(w);
+        const uint32_t off = canon_off16(n, k);
+        const float wa = k < 7 ? whi : ((k >= 8 && k < 14) ? tc::bf16_round(c.p32[c.o_lw1 + n * 6 + (k - 8)]) : 0.f);
+        const float wb = k < 7 ? w - whi : 0.f;
+        *reinterpret_cast<uint16_t*>(w1hi + off) = static_cast<uint16_t>(tc::pack_bf16(wa, 0.f) & 0xFFFFu);
+        *reinterpret_cast<uint16_t*>(w1lo + off) = static_cast<uint16_t>(tc::pack_bf16(wb, 0.f) & 0xFFFFu);
+        const float b2 = c.p32[c.o_lb2 + n], b2h = tc::bf16_round(b2);
+        const float bv = k == 0 ? b2h : (k == 1 ? b2 - b2h : 0.f);
+        *reinterpret_cast<uint16_t*>(b2hi + off) = static_cast<uint16_t>(tc::pack_bf16(bv, 0.f) & 0xFFFFu);
+    }
+    for (int i = tid; i < 128 * 16; i += kThreads) {
+        const int r = i / 16, k = i % 16;
+        *reinterpret_cast<uint16_t*>(aone + canon_off16(r, k)) = k < 2 ? 0x3F80u : 0u;
+    }
+    if (warp == 0) {
+        tc::tmem_alloc(&tbase_s, 512);
+        tc::tmem_relinquish();
+    }
+    if (tid == 0) {
+        for (int q = 0; q < kGroups; ++q) tc::mbar_init(&bars[q], 1);
+        tc::fence_mbar_init();
+    }
+    tc::fence_proxy_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+
+    const uint32_t tbase = tbase_s;
+    const uint32_t lane_off = static_cast<uint32_t>(32 * wl) << 16;
+    const uint32_t tm_d = tbase + 128 * g;
+    const uint32_t tm_ahi = tm_d + 64, tm_alo = tm_d + 96;
+    const uint32_t w2hi_a = tc::smem_u32(w2hi), w2lo_a = tc::smem_u32(w2lo);
+    const uint32_t w2thi_a = tc::smem_u32(w2thi), w2tlo_a = tc::smem_u32(w2tlo);
+    const uint32_t w1hi_a = tc::smem_u32(w1hi), w1lo_a = tc::smem_u32(w1lo);
+    const uint32_t b2hi_a = tc::smem_u32(b2hi), aone_a = tc::smem_u32(aone);
+    const int nq = (n_rx + 3) >> 2;
+    const long long tiles = static_cast<long long>((n_rows + 31) >> 5) * nq;
+    const long long step = static_cast<long long>(gridDim.x) * kGroups;
+    const int L = c.L;
+    uint32_t phase = 0;
+    auto wait_mma = [&]() {
+        RXGS_MBAR_WAIT(&bars[g], phase);
+        phase ^= 1u;
+        tc::fence_after_sync();
+    };
+    for (long long tile = static_cast<long long>(blockIdx.x) * kGroups + g; tile < tiles; tile += step) {
+        const int gb = static_cast<int>(tile / nq), jq = static_cast<int>(tile - static_cast<long long>(gb) * nq);
+        const int r = gb * 32 + lane, j = jq * 4 + wl;
+        const bool active = r < n_rows && j < n_rx;
+        const int k = active ? rows[r] : 0;
+        // activation row id, receiver-major: a warp's 32 lanes (consecutive
+        // needed rows, one receiver) store 64 contiguous bytes per feature
+        // plane (k_cond_grads_tc sums over rows in any order)
+        const long long row = static_cast<long long>(j) * n_rows + r;
+        // ---- local features (the same function as the SIMT kernels)
+        float x[6];
+        cube_features<ST, RT>(c, active, active ? pos32[k] : make_float4(0.f, 0.f, 0.f, 0.f),
+                              active ? static_cast<float>(rx[3 * j]) : 1.f, active ? static_cast<float>(rx[3 * j + 1]) : 0.f,
+                              active ? static_cast<float>(rx[3 * j + 2]) : 0.f, x);
+        if (!active) {
+#pragma unroll
+            for (int f = 0; f < 6; ++f) x[f] = 0.f;
+        }
+        if (active) {
+#pragma unroll
+            for (int f = 0; f < 6; ++f) act.put(row, kAx + f, x[f]);
+        }
+        // ---- layer 1
+        {
+            uint32_t a[8];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) x2::split_bf16(x[2 * q], x[2 * q + 1], a[q], a[4 + q]);
+            a[3] = 0x3F80u;
+            a[7] = 0u;
+            tc::tmem_st8(tm_ahi + lane_off, a);
+        }
+        tc::wait_st();
+        tc::fence_before_sync();
+        if (arrive_last(&arrivals[g], lane) && lane == 0) {
+            tc::fence_after_sync();
+            tc::mma_ts(tm_d, tm_ahi, tc::sdesc_kmajor_noswizzle(w1hi_a, 128, 256), kIdesc, 0u);
+            tc::mma_ts(tm_d, tm_ahi, tc::sdesc_kmajor_noswizzle(w1lo_a, 128, 256), kIdesc, 1u);
+            tc::mma_commit(&bars[g]);
+        }
+        wait_mma();
+        // ---- ReLU(h1) -> bf16 hi/lo (the layer-2 operand and the h1 activations)
+        uint32_t m1lo = 0u, m1hi = 0u;  // h1 > 0
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+            uint32_t v[16], hi[8], lo[8];
+            tc::tmem_ld16(tm_d + lane_off + 16 * ch, v);
+            tc::wait_ld_regs(v);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const float h0 = __uint_as_float(v[2 * q]), h1v = __uint_as_float(v[2 * q + 1]);
+                x2::relu_split_bf16(h0, h1v, hi[q], lo[q]);
+                const int i = 16 * ch + 2 * q;
+                const uint32_t bits = (h0 > 0.f ? 1u : 0u) | (h1v > 0.f ? 2u : 0u);
+                if (i < 32) m1lo |= bits << i; else m1hi |= bits << (i - 32);
+                if (active) {
+                    act.put_bits(row, kAh1 + i, hi[q] & 0xFFFFu, lo[q] & 0xFFFFu);
+                    act.put_bits(row, kAh1 + i + 1, hi[q] >> 16, lo[q] >> 16);
+                }
+            }
+            tc::tmem_st8(tm_ahi + lane_off + 8 * ch, hi);
+            tc::tmem_st8(tm_alo + lane_off + 8 * ch, lo);
+        }
+        tc::wait_st();
+        tc::fence_before_sync();
+        // ---- layer 2
+        if (arrive_last(&arrivals[g], lane) && lane == 0) {
+            tc::fence_after_sync();
+            tc::mma_ss(tm_d, tc::sdesc_kmajor_noswizzle(aone_a, 128, 256), tc::sdesc_kmajor_noswizzle(b2hi_a, 128, 256),
+                       kIdesc, 0u);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint64_t bh = tc::sdesc_kmajor_noswizzle(w2hi_a + 256 * q, 128, 1024);
+                const uint64_t bl = tc::sdesc_kmajor_noswizzle(w2lo_a + 256 * q, 128, 1024);
+                tc::mma_ts(tm_d, tm_ahi + 8 * q, bh, kIdesc, 1u);
+                tc::mma_ts(tm_d, tm_ahi + 8 * q, bl, kIdesc, 1u);
+                tc::mma_ts(tm_d, tm_alo + 8 * q, bh, kIdesc, 1u);
+            }
+            tc::mma_commit(&bars[g]);
+        }
+        wait_mma();
+        // ---- ReLU(h2), layer 3, the h2 activations and mask
+        float2 ya = make_float2(W.b3[0], W.b3[1]), yb = make_float2(W.b3[2], W.b3[3]);
+        uint32_t m2lo = 0u, m2hi = 0u;  // h2 > 0
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+            uint32_t v[16];
+            tc::tmem_ld16(tm_d + lane_off + 16 * ch, v);
+            tc::wait_ld_regs(v);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int o = 16 * ch + q;
+                const float h2 = fmaxf(__uint_as_float(v[q]), 0.f);
+                if (h2 > 0.f) {
+                    if (o < 32) m2lo |= 1u << o; else m2hi |= 1u << (o - 32);
+                }
+                if (active) act.put(row, kAh2 + o, h2);
+                const float4 w3 = W.w3[o];
+                ya = x2::fma(x2::bc(h2), make_float2(w3.x, w3.y), ya);
+                yb = x2::fma(x2::bc(h2), make_float2(w3.z, w3.w), yb);
+            }
+        }
+        // ---- the affine adjoint: dy = (ds conj(M), ds conj(Bs)), u = conj(1 + aL) ds
+        float dy[4] = {0.f, 0.f, 0.f, 0.f};
+        if (active) {
+            float2 M = make_float2(0.f, 0.f), Bs = make_float2(0.f, 0.f);
+            const float4* a4 = reinterpret_cast<const float4*>(ag) + static_cast<size_t>(j) * L;
+            for (int l = 0; l < L; ++l) {
+                const float2 b = Bm[static_cast<size_t>(k) * L + l];
+                const float2 gbv = GB[static_cast<size_t>(k) * L + l];
+                const float4 av = a4[l];
+                const float2 t0 = cmul(make_float2(1.f + av.x, av.y), gbv), t1 = cmul(make_float2(av.z, av.w), b);
+                M = make_float2(M.x + (t0.x + t1.x), M.y + (t0.y + t1.y));
+                Bs = make_float2(Bs.x + b.x, Bs.y + b.y);
+            }
+            const float ar = c.additive ? 0.f : ya.x, ai = c.additive ? 0.f : ya.y;
+            const float2 ds = d_s[static_cast<size_t>(k) * n_rx + j];
+            const float2 da = cmul(ds, make_float2(M.x, -M.y)), db = cmul(ds, make_float2(Bs.x, -Bs.y));
+            dy[0] = c.additive ? 0.f : da.x;
+            dy[1] = c.additive ? 0.f : da.y;
+            dy[2] = db.x;
+            dy[3] = db.y;
+            u_out[static_cast<size_t>(k) * n_rx + j] = cmul(make_float2(1.f + ar, -ai), ds);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) act.put(row, kAdy + q, dy[q]);
+        }
+        // ---- dh2 = (W3^T dy) [h2 > 0] -> activations and the dh1 MMA's A operand
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+            uint32_t hi[8], lo[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int o = 16 * ch + 2 * q;
+                const float4 wa = W.w3[o], wb = W.w3[o + 1];
+                float g0 = fmaf(wa.x, dy[0], fmaf(wa.y, dy[1], fmaf(wa.z, dy[2], wa.w * dy[3])));
+                float g1 = fmaf(wb.x, dy[0], fmaf(wb.y, dy[1], fmaf(wb.z, dy[2], wb.w * dy[3])));
+                const uint32_t mk = o < 32 ? m2lo >> o : m2hi >> (o - 32);
+                g0 = (mk & 1u) ? g0 : 0.f;
+                g1 = (mk & 2u) ? g1 : 0.f;
+                if (active) {
+                    act.put(row, kAdh2 + o, g0);
+                    act.put(row, kAdh2 + o + 1, g1);
+                }
+                x2::split_bf16(g0, g1, hi[q], lo[q]);
+            }
+            tc::tmem_st8(tm_ahi + lane_off + 8 * ch, hi);
+            tc::tmem_st8(tm_alo + lane_off + 8 * ch, lo);
+        }
+        tc::wait_st();
+        tc::fence_before_sync();
+        // ---- dh1 = W2^T dh2 (bf16x3) into the h2 columns (read above)
+        if (arrive_last(&arrivals[g], lane) && lane == 0) {
+            tc::fence_after_sync();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint64_t bh = tc::sdesc_kmajor_noswizzle(w2thi_a + 256 * q, 128, 1024);
+                const uint64_t bl = tc::sdesc_kmajor_noswizzle(w2tlo_a + 256 * q, 128, 1024);
+                tc::mma_ts(tm_d, tm_ahi + 8 * q, bh, kIdesc, q > 0 ? 1u : 0u);
+                tc::mma_ts(tm_d, tm_ahi + 8 * q, bl, kIdesc, 1u);
+                tc::mma_ts(tm_d, tm_alo + 8 * q, bh, kIdesc, 1u);
+            }
+            tc::mma_commit(&bars[g]);
+        }
+        wait_mma();
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+            uint32_t v[16];
+            tc::tmem_ld16(tm_d + lane_off + 16 * ch, v);
+            tc::wait_ld_regs(v);
+            if (active) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const int i = 16 * ch + q;
+                    const uint32_t mk = i < 32 ? m1lo >> i : m1hi >> (i - 32);
+                    act.put(row, kAdh1 + i, (mk & 1u) ? __uint_as_float(v[q]) : 0.f);
+                }
+            }
+        }
+        tc::fence_before_sync();  // the next tile's layer 1 overwrites these columns after the rendezvous
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(tbase, 512);
+}
+
 // ------------------------------------------------------------------ self test
 // 128x64x64 bf16 GEMM through both operand paths (A in TMEM and A in shared
 // memory) against FP32 FMA of the same bf16 values.
@@ -1462,6 +1740,34 @@ cudaError_t launch_local_cache_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc,
                                   float4* ycache, cudaStream_t s) {
     return launch_tc<true>(cs, nullptr, sc.k, sc.k, sc.d_morton.as<int>(), sc.d_mpos32.as<float4>(), d_rx, n_rx,
                            nullptr, nullptr, nullptr, nullptr, SigOut(), ycache, s);
+}
+
+cudaError_t launch_cond_bwd_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
+                               const double* d_rx, int n_rx, const float* d_ag, const float2* d_s, float2* u,
+                               uint16_t* act, long long rpad, cudaStream_t s) {
+    const CondDev d = make_dev(cs);
+    LocalW w{};
+    const std::vector<double>& p = cs.h_params;
+    for (int o = 0; o < kH; ++o)
+        w.w3[o] = make_float4(static_cast<float>(p[cs.o_lw3 + o]), static_cast<float>(p[cs.o_lw3 + kH + o]),
+                              static_cast<float>(p[cs.o_lw3 + 2 * kH + o]), static_cast<float>(p[cs.o_lw3 + 3 * kH + o]));
+    for (int i = 0; i < 4; ++i) w.b3[i] = static_cast<float>(p[cs.o_lb3 + i]);
+    const long long bound = st.needed_host >= 0 ? st.needed_host : st.visible;
+    const long long tiles = ((bound + 31) / 32) * ((n_rx + 3) / 4);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long want = (tiles + kGroups - 1) / kGroups;
+    const int blocks = static_cast<int>(want < sms ? (want > 0 ? want : 1) : sms);
+    const size_t smem = kFixedSmem + 2 * kW2Bytes;
+    const bool fast = d.S == 16 && d.R == 32;
+    auto kern = fast ? k_cond_bwd_tc<16, 32> : k_cond_bwd_tc<0, 0>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<blocks, kThreads, smem, s>>>(w, d, st.needed_count.as<int>(), st.needed_order.as<int>(),
+                                        sc.d_pos32.as<float4>(), d_rx, n_rx, st.basis32.as<float2>(),
+                                        st.gb32.as<float2>(), d_ag, d_s, u, ActOut{act, rpad});
+    return cudaGetLastError();
 }
 
 cudaError_t launch_tc_selftest(float* d_err, cudaStream_t s) {

@@ -579,25 +579,6 @@ __global__ void __launch_bounds__(kBwdThreads) k_cond_bwd(CondDev c, const int* 
 #ifndef RXGS_BWD_GRAD_CTAS
 #define RXGS_BWD_GRAD_CTAS 4
 #endif
-// activations per row as bf16 hi/lo feature planes act[plane][f][row]
-// (hi = bf16(v), lo = bf16(v - hi)); the feature order groups the operands
-// of k_cond_grads_tc's two GEMMs over rows: [dh2 | dh1] (A of GEMM 1),
-// [h1 | x] (B of GEMM 1), h2 (A of GEMM 2), dy (B of GEMM 2)
-constexpr int kActF = 4 * 64 + 6 + 4;  // activation features per row
-constexpr int kAdh2 = 0, kAdh1 = 64, kAh1 = 128, kAx = 192, kAh2 = 198, kAdy = 262;
-constexpr int kActRowAlign = 64;       // rows padded to the grads kernel's K chunk
-
-struct ActOut {
-    uint16_t* p;
-    long long rpad;
-    __device__ __forceinline__ void put(long long row, int f, float v) const {
-        const uint32_t h = tc::pack_bf16(v, 0.f) & 0xFFFFu;
-        const uint32_t l = tc::pack_bf16(v - __uint_as_float(h << 16), 0.f) & 0xFFFFu;
-        p[static_cast<size_t>(f) * rpad + row] = static_cast<uint16_t>(h);
-        p[static_cast<size_t>(kActF + f) * rpad + row] = static_cast<uint16_t>(l);
-    }
-};
-
 template <int ST, int RT>
 __global__ void __launch_bounds__(128, 3) k_cond_bwd_rows(CondDev c, const int* __restrict__ n_rows,
                                                           const int* __restrict__ rows, const float4* __restrict__ pos32,
@@ -1273,7 +1254,7 @@ cudaError_t make_act_map(CUtensorMap* m, const void* base, uint64_t rows, long l
 
 cudaError_t launch_cond_bwd(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
                             const double* d_rx, int n_rx, const float* d_ag, const float2* d_s, float2* u,
-                            float* part, int n_parts, cudaStream_t s, float* act) {
+                            float* part, int n_parts, cudaStream_t s, float* act, bool tc_rows) {
     const CondDev d = make_dev(cs);
     if (RXGS_BWD_SPLIT && act) {
         const long long rows_bound = static_cast<long long>(st.visible) * n_rx;
@@ -1286,10 +1267,14 @@ cudaError_t launch_cond_bwd(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         ActOut ao{reinterpret_cast<uint16_t*>(act), rpad};
-        kr<<<sms * 3, 128, smem_r, s>>>(d, st.needed_count.as<int>(), st.needed_order.as<int>(),
-                                        sc.d_pos32.as<float4>(), d_rx, n_rx, st.basis32.as<float2>(),
-                                        st.gb32.as<float2>(), d_ag, d_s, u, ao);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if (tc_rows && d.use_local) {
+            if ((e = launch_cond_bwd_tc(cs, sc, st, d_rx, n_rx, d_ag, d_s, u, ao.p, rpad, s)) != cudaSuccess) return e;
+        } else {
+            kr<<<sms * 3, 128, smem_r, s>>>(d, st.needed_count.as<int>(), st.needed_order.as<int>(),
+                                            sc.d_pos32.as<float4>(), d_rx, n_rx, st.basis32.as<float2>(),
+                                            st.gb32.as<float2>(), d_ag, d_s, u, ao);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        }
         if (!d.use_local) return cudaSuccess;
         // the row extent of the tensor maps is the host bound (rows past the
         // needed ones are never read: each CTA stops at needed x n_rx)

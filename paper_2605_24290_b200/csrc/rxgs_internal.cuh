@@ -409,7 +409,11 @@ int cond_bwd_parts(int sms);
 int local_grad_n();
 cudaError_t launch_cond_bwd(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
                             const double* d_rx, int n_rx, const float* d_ag, const float2* d_s, float2* u,
-                            float* part, int n_parts, cudaStream_t s, float* act = nullptr);
+                            float* part, int n_parts, cudaStream_t s, float* act = nullptr, bool tc_rows = false);
+// the per-row half of the split backward on tcgen05 (spectrum-L1 training)
+cudaError_t launch_cond_bwd_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
+                               const double* d_rx, int n_rx, const float* d_ag, const float2* d_s, float2* u,
+                               uint16_t* act, long long rpad, cudaStream_t s);
 // scratch of the split backward (0 when the fused kernel is used)
 size_t cond_bwd_act_bytes(long long rows);
 cudaError_t launch_reduce_parts(int n_parts, int n, const float* part, double* out, cudaStream_t s);

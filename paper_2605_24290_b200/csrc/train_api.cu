@@ -247,7 +247,8 @@ int rxgs_train_grads(rxgs_trainer t, rxgs_txstate st, const double* rx, int n_rx
     const bool l1_only = t->lambda_ssim == 0.0 && t->lambda_fft == 0.0;
     const int saved = ctx->cond_kernel;
     ctx->cond_kernel = train_cond >= 0 ? train_cond : (l1_only ? 0 : 1);
-    if (c && c->host_stale && ctx->cond_kernel == 0 && cond_tc_eligible(c)) {
+    const bool tc_cond = ctx->cond_kernel == 0 && c && cond_tc_eligible(c);
+    if (tc_cond && c->host_stale) {
         // the tcgen05 kernel takes the local layer 3 as a kernel parameter
         // built from the host copy: refresh those values after an optimizer step
         RXGS_CUDA(cudaStreamSynchronize(s));
@@ -301,7 +302,7 @@ int rxgs_train_grads(rxgs_trainer t, rxgs_txstate st, const double* rx, int n_rx
             if (ab) RXGS_CUDA(t->act.ensure(ab));
             RXGS_CUDA(launch_cond_bwd(*c, *sc, *st, d_rx, n_rx, ctx->ag.as<float>(), t->d_s.as<float2>(),
                                       t->u.as<float2>(), t->part.as<float>(), t->n_parts, s,
-                                      ab ? t->act.as<float>() : nullptr));
+                                      ab ? t->act.as<float>() : nullptr, tc_cond));
         }
     if (c && c->use_local()) RXGS_CUDA(launch_reduce_parts(t->n_parts, nl, t->part.as<float>(), gpar + c->o_lw1, s));
     RXGS_CUDA(launch_dbase(c, *sc, *st, n_rx, ctx->ag.as<float>(), t->u.as<float2>(), gbase, s));

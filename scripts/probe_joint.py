@@ -17,7 +17,9 @@ cond.build_occupancy(scene, 32, olo, ohi)
 grid = capi.Grid(90, 360, 8, 1.0)
 rx = capi.synth_points(16, 23, "bench.train.rx", [-4, -3, -1.5], [4, 3, 1.5], 0.05)
 tg = np.random.default_rng(29).uniform(0, 2, (16, grid.cells)).astype(np.float32)
-tr = capi.Trainer(ctx, scene, cond, geometry=(len(sys.argv) < 2 or sys.argv[1] != "stage2") or None)
+stage2 = len(sys.argv) > 1 and sys.argv[1].startswith("stage2")
+hyper = capi.Trainer.L1_ONLY if len(sys.argv) > 1 and sys.argv[1] == "stage2l1" else None
+tr = capi.Trainer(ctx, scene, cond, hyper, geometry=(not stage2) or None)
 for _ in range(3):
     st = scene.tx_state(np.array([0.3, -0.2, 0.1]), grid)
     tr.grads(st, rx, tg)
