@@ -285,7 +285,13 @@ __global__ void k_loss_total(int n_rx, int nb, int P, double l_w, double lambda_
 
 // ------------------------------------------------------------------ composite transpose
 // d_entry[e][j] = sum_cells tw[e][cell] * G_j[cell] for the first W rows of a tile.
-__global__ void __launch_bounds__(256) k_composite_T(DevGrid g, const int64_t* __restrict__ tile_offsets,
+// One thread per walked list position: its weight row (ncell floats) is
+// read once as float4s and multiplied against every receiver's cell adjoint
+// (shared memory, warp-broadcast reads), JB receivers per pass held as
+// complex accumulators (FFMA2 on (re, im)).  Per (pos, j) the sum runs over
+// the cells in ascending order, exactly as a scalar fmaf chain.
+constexpr int kCTJ = 16;  // receivers per pass
+__global__ void __launch_bounds__(128) k_composite_T(DevGrid g, const int64_t* __restrict__ tile_offsets,
                                                      const float* __restrict__ tw, const int* __restrict__ walk_len,
                                                      const float2* __restrict__ G, int n_rx,
                                                      float2* __restrict__ d_entry) {
@@ -295,27 +301,45 @@ __global__ void __launch_bounds__(256) k_composite_T(DevGrid g, const int64_t* _
     const int ncell = g.cell_blocks * kMaxCellsPerBlock;
     const size_t plane = static_cast<size_t>(g.nt) * g.np;
     for (int i = threadIdx.x; i < ncell * n_rx; i += blockDim.x) {
-        const int lc = i / n_rx, j = i % n_rx;
+        const int j = i / ncell, lc = i % ncell;  // coalesced over cells of one receiver plane
         const int row = tt * g.ts + lc / g.ts, col = tp * g.ts + lc % g.ts;
         const bool valid = lc < g.cpt && row < g.nt && col < g.np;
-        sG[i] = valid ? G[static_cast<size_t>(j) * plane + static_cast<size_t>(row) * g.np + col] : make_float2(0.f, 0.f);
+        sG[lc * n_rx + j] = valid ? G[static_cast<size_t>(j) * plane + static_cast<size_t>(row) * g.np + col]
+                                  : make_float2(0.f, 0.f);
     }
     __syncthreads();
     int W = 0;
     for (int b = 0; b < g.cell_blocks; ++b) W = max(W, walk_len[tile * g.cell_blocks + b]);
     const int64_t begin = tile_offsets[tile];
-    const size_t stride = static_cast<size_t>(g.cell_blocks) * kMaxCellsPerBlock;
-    for (int i = threadIdx.x; i < W * n_rx; i += blockDim.x) {
-        const int pos = i / n_rx, j = i % n_rx;
-        const float* t = tw + static_cast<size_t>(begin + pos) * stride;
-        float ar = 0.f, ai = 0.f;
-        for (int c = 0; c < ncell; ++c) {
-            const float w = t[c];
-            const float2 gv = sG[c * n_rx + j];
-            ar = fmaf(w, gv.x, ar);
-            ai = fmaf(w, gv.y, ai);
+    const size_t stride = static_cast<size_t>(ncell);
+    for (int pos = threadIdx.x; pos < W; pos += blockDim.x) {
+        const float4* t4 = reinterpret_cast<const float4*>(tw + static_cast<size_t>(begin + pos) * stride);
+        float2* out = d_entry + static_cast<size_t>(begin + pos) * n_rx;
+        for (int j0 = 0; j0 < n_rx; j0 += kCTJ) {
+            const int nj = n_rx - j0 < kCTJ ? n_rx - j0 : kCTJ;
+            float2 acc[kCTJ];
+#pragma unroll
+            for (int q = 0; q < kCTJ; ++q) acc[q] = make_float2(0.f, 0.f);
+            for (int c4 = 0; c4 < ncell / 4; ++c4) {
+                const float4 w4 = t4[c4];
+                const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float2* gr = sG + (4 * c4 + u) * n_rx + j0;
+                    if (nj == kCTJ) {
+#pragma unroll
+                        for (int q = 0; q < kCTJ; ++q) acc[q] = x2::fma(x2::bc(wv[u]), gr[q], acc[q]);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < kCTJ; ++q)
+                            if (q < nj) acc[q] = x2::fma(x2::bc(wv[u]), gr[q], acc[q]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kCTJ; ++q)
+                if (q < nj) out[j0 + q] = acc[q];
         }
-        d_entry[static_cast<size_t>(begin + pos) * n_rx + j] = make_float2(ar, ai);
     }
 }
 
@@ -1198,7 +1222,7 @@ cudaError_t launch_render_adjoint(const rxgs_txstate_s& st, const float2* G, int
     if (st.entries > 0) {
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(k_composite_T, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        k_composite_T<<<g.n_tiles, 256, smem, s>>>(g, st.tile_offsets.as<int64_t>(), st.tw.as<float>(),
+        k_composite_T<<<g.n_tiles, 128, smem, s>>>(g, st.tile_offsets.as<int64_t>(), st.tw.as<float>(),
                                                    st.walk_len.as<int>(), G, n_rx, d_entry);
     }
     const long long rows = static_cast<long long>(st.visible) * n_rx;
