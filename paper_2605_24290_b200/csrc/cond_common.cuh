@@ -327,23 +327,13 @@ __device__ __forceinline__ float cube_eval(const float* cell, float w0, float w1
     return fmaf(w2, y.y, y.x);
 }
 
-// Paired fast path (all of the warp's segments inside the grid, u in [-1, R]
-// on every axis).  floor(u) without FRND / F2I: u +rm 1.5*2^23 is exactly
-// floor(u) + 1.5*2^23 (|u| < 2^22), so f = (u +rm M) - M is floor(u) on the
-// FP32 pipe (FADD2.RM + FADD2), and the cell index computed as the exact
-// integer float idx + M carries idx in its low mantissa bits: the cell
-// address is one IMAD.WIDE of those bits on a base pointer shifted by
-// -32 * bits(M) bytes.  Same f, w and idx as floorf / F2I: bit-identical.
 template <int ST, int RT, int P0, int P1>
 __device__ __forceinline__ void probe_pairs_cube(const float* __restrict__ cube, float b0, float b1, float b2,
                                                  float s0, float s1, float s2, float2& tr2, float2& sum2) {
     static_assert(ST >= 2 && ST % 2 == 0 && RT > 0, "paired probe needs an even, static sample count");
     constexpr int P = RT + 2;
-    constexpr float kM = 12582912.f;  // 1.5 * 2^23
-    constexpr float cidxM = static_cast<float>(P * P + P + 1) + kM;  // exact (< 2^24)
+    constexpr float cidx = static_cast<float>(P * P + P + 1);
     constexpr float dt = 0.9f / static_cast<float>(ST - 1);
-    static_assert(P * P * P + P * P + P + 1 < (1 << 22), "cell index must stay exact in FP32");
-    const char* cb = reinterpret_cast<const char*>(cube) - 32ull * 0x4B400000ull;  // 0x4B400000 = bits(kM)
 #pragma unroll
     for (int sp = P0; sp < P1; ++sp) {
         const float2 t = make_float2(fmaf(static_cast<float>(2 * sp), dt, 0.05f),
@@ -351,14 +341,14 @@ __device__ __forceinline__ void probe_pairs_cube(const float* __restrict__ cube,
         const float2 u0 = x2::fma(t, x2::bc(s0), x2::bc(b0));
         const float2 u1 = x2::fma(t, x2::bc(s1), x2::bc(b1));
         const float2 u2 = x2::fma(t, x2::bc(s2), x2::bc(b2));
-        const float2 f0 = x2::sub(x2::add_rm(u0, x2::bc(kM)), x2::bc(kM));
-        const float2 f1 = x2::sub(x2::add_rm(u1, x2::bc(kM)), x2::bc(kM));
-        const float2 f2 = x2::sub(x2::add_rm(u2, x2::bc(kM)), x2::bc(kM));
+        const float2 f0 = make_float2(floorf(u0.x), floorf(u0.y));
+        const float2 f1 = make_float2(floorf(u1.x), floorf(u1.y));
+        const float2 f2 = make_float2(floorf(u2.x), floorf(u2.y));
         const float2 w0 = x2::sub(u0, f0), w1 = x2::sub(u1, f1), w2 = x2::sub(u2, f2);
         const float2 fi = x2::fma(f0, x2::bc(static_cast<float>(P * P)),
-                                  x2::fma(f1, x2::bc(static_cast<float>(P)), x2::add(f2, x2::bc(cidxM))));
-        const float va = cube_eval(reinterpret_cast<const float*>(cb + 32ull * __float_as_uint(fi.x)), w0.x, w1.x, w2.x);
-        const float vb = cube_eval(reinterpret_cast<const float*>(cb + 32ull * __float_as_uint(fi.y)), w0.y, w1.y, w2.y);
+                                  x2::fma(f1, x2::bc(static_cast<float>(P)), x2::add(f2, x2::bc(cidx))));
+        const float va = cube_eval(cube + 8 * static_cast<int>(fi.x), w0.x, w1.x, w2.x);
+        const float vb = cube_eval(cube + 8 * static_cast<int>(fi.y), w0.y, w1.y, w2.y);
         const float2 v = make_float2(va, vb);
         tr2 = x2::mul(tr2, x2::sub(x2::bc(1.f), v));
         sum2 = x2::add(sum2, v);
@@ -469,9 +459,6 @@ struct ActOut {
     uint16_t* p;
     long long rpad;
     __device__ __forceinline__ void put(long long row, int f, float v) const {
-#ifdef RXGS_ACT_NOSTORE  // timing experiment only (wrong gradients)
-        if (v != 12345.f) return;
-#endif
         const uint32_t h = act_bf16(v) & 0xFFFFu;
         const uint32_t l = act_bf16(v - __uint_as_float(h << 16)) & 0xFFFFu;
         p[static_cast<size_t>(f) * rpad + row] = static_cast<uint16_t>(h);

@@ -34,12 +34,6 @@ __device__ __forceinline__ float2 add(float2 a, float2 b) {
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(u64(a)), "l"(u64(b)));
     return f2(r);
 }
-// a + b rounded toward -infinity (FADD2.RM)
-__device__ __forceinline__ float2 add_rm(float2 a, float2 b) {
-    unsigned long long r;
-    asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(u64(a)), "l"(u64(b)));
-    return f2(r);
-}
 __device__ __forceinline__ float2 sub(float2 a, float2 b) {
     unsigned long long r;
     asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(u64(a)), "l"(u64(b)));
