@@ -2,7 +2,7 @@
 # Profiling artefacts for profiles/ (round tag $1, default r1): the launch list
 # of the config-2 bench step and one ncu --set full capture per hot kernel.
 # Run under gpurun; then `python scripts/write_profiles.py $1` here.
-TAG=${1:-r1}
+TAG=${1:-r2}
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv

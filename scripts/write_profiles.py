@@ -13,7 +13,7 @@ if os.path.exists(lc):
     open(os.path.join(prof, f"{tag}_launches.txt"), "w").write(S.launches(lc) + "\n")
 traffic = {"source": "ncu --set full --clock-control none, one launch each; bench.py config 2 (K=100k, 1024 rx, 90x360); "
                      "k_cov_signal from the config-3 leg (K=500k)"}
-for name in ("train", "joint"):  # scripts/gpu_profiles_train.sh
+for name in ("train", "train_l1", "joint"):  # scripts/gpu_profiles_train.sh
     lc = os.path.join(out, f"{tag}_{name}_launches.csv")
     if os.path.exists(lc):
         open(os.path.join(prof, f"{tag}_{name}_launches.txt"), "w").write(S.launches(lc) + "\n")
@@ -49,8 +49,8 @@ if os.path.exists(rep):
     open(os.path.join(prof, f"{tag}_k_cond_tc_source.txt"), "w").write(source_hotspots(rep))
 
 for k in ["k_cond_tc", "k_fle_gemm", "k_composite_tc", "k_walk", "k_tx_prep", "k_cov_signal", "k_tile_scatter",
-          "k_emit_entries", "k_radix_scatter", "k_cond_bwd_rows",
-          "k_cond_bwd_grads"]:
+          "k_emit_entries", "k_radix_scatter", "k_cond_bwd_rows", "k_cond_bwd_grads", "k_cond_bwd_tc",
+          "k_cond_grads_tc", "k_composite_T"]:
     rep = os.path.join(out, f"{tag}_{k}.ncu-rep")
     if not os.path.exists(rep):
         continue
