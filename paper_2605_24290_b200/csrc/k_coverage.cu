@@ -55,7 +55,7 @@ constexpr int kCovThreads = 256;
 // LT > 0: L == LT, the receiver's (alpha_G, beta_G) held in registers;
 // LT == 0 (other l_max): re-read per row from the transposed cache.
 template <int LT>
-__global__ void __launch_bounds__(kCovThreads, 3) k_cov_signal(CondDev c, const int* __restrict__ n_rows,
+__global__ void __launch_bounds__(kCovThreads, 2) k_cov_signal(CondDev c, const int* __restrict__ n_rows,
                                                             const int* __restrict__ rows, int n_rx, int L,
                                                             const float2* __restrict__ B, const float2* __restrict__ GB,
                                                             const float4* __restrict__ agT,
@@ -103,13 +103,23 @@ __global__ void __launch_bounds__(kCovThreads, 3) k_cov_signal(CondDev c, const 
         const int k = rr < kCovRows ? s_k[rr] : -1;
         return (ycache && k >= 0) ? ycache[static_cast<size_t>(k) * n_rx + j] : make_float4(0.f, 0.f, 0.f, 0.f);
     };
-    float4 ynext = load_y(0);
+    // the receiver's (alpha_G, beta_G) for all l in registers for the 32 rows
+    float4 areg[LT > 0 ? LT : 1];
+#pragma unroll
+    for (int l = 0; l < LT; ++l) areg[l] = s_a[l * kCovThreads + tid];
+    constexpr int kAhead = 4;  // y-cache rows in flight per thread
+    float4 yq[kAhead];
+#pragma unroll
+    for (int q = 0; q < kAhead; ++q) yq[q] = load_y(q);
 #pragma unroll 1
-    for (int rr = 0; rr < kCovRows; ++rr) {
+    for (int rr0 = 0; rr0 < kCovRows; rr0 += kAhead) {
+#pragma unroll
+    for (int q = 0; q < kAhead; ++q) {
+        const int rr = rr0 + q;
         const int k = s_k[rr];
-        if (k < 0) break;
-        const float4 y = ynext;
-        ynext = load_y(rr + 1);  // one row ahead
+        if (k < 0) return;
+        const float4 y = yq[q];
+        yq[q] = load_y(rr + kAhead);  // kAhead rows ahead
         const float4 sm = s_sum[rr];
         // M = sum_l [(1 + aG_l) GB_l + bG_l B_l] = sum_l GB_l + sum_l [aG_l GB_l + bG_l B_l]
         float2 M = make_float2(sm.x, sm.y), M1 = make_float2(0.f, 0.f);
@@ -122,9 +132,8 @@ __global__ void __launch_bounds__(kCovThreads, 3) k_cov_signal(CondDev c, const 
         if constexpr (LT > 0) {
 #pragma unroll
             for (int l = 0; l < LT; ++l) {
-                const float4 al = s_a[l * kCovThreads + tid];
-                if (l & 1) M1 = term(M1, s_e_dyn[rr * LT + l], al);
-                else M = term(M, s_e_dyn[rr * LT + l], al);
+                if (l & 1) M1 = term(M1, s_e_dyn[rr * LT + l], areg[l]);
+                else M = term(M, s_e_dyn[rr * LT + l], areg[l]);
             }
         } else {
             for (int l = 0; l < L; ++l) {
@@ -141,6 +150,7 @@ __global__ void __launch_bounds__(kCovThreads, 3) k_cov_signal(CondDev c, const 
         sg = x2::fma(x2::bc(y.z), make_float2(sm.z, sm.w), sg);
         sg = x2::fma(make_float2(-sm.w, sm.z), x2::bc(y.w), sg);
         store_sig(sig, k, n_rx, j, 1, 0, sg);
+    }
     }
 }
 

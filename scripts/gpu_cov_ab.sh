@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_render.py tests/test_gpu_fullscale.py tests/test_gpu_apps.py -m gpu -q -p no:cacheprovider -k "cover or config3" 2>&1 | tail -2
+timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-train --no-config5 --no-lmax9 --no-config1 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); c=d['config3']; print('config3', c['value'], c['ms_per_table'], c['phase_ms'])"
