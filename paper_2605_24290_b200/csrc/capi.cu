@@ -693,7 +693,11 @@ int rxgs_tx_state_build(rxgs_ctx ctx, rxgs_scene sc, const double tx[3], const r
         const int rc = compact_needed(ctx, *sc, *st, s);
         if (rc) return fail_st(rc);
     }
-    ctx->launches += 1;
+    {
+        const cudaError_t e = launch_basis_rows(*sc, *st, s);
+        if (e != cudaSuccess) return fail_st(cuda_fail(e, "basis_rows"));
+    }
+    ctx->launches += 2;
     ctx_retain(ctx);
     st->sc = sc;
     sc->refs += 1;

@@ -129,48 +129,14 @@ __device__ __forceinline__ void project_core(double u0, double u1, double u2, co
 // only the adjoint, the materialised render API and the state accessors
 // read; the query path builds lean states and completes them on demand
 // (ensure_tx_full, capi.cu) with the identical arithmetic.
-template <int LMT, bool FULL>  // LMT > 0: l_max known at compile time (tables in registers)
-__global__ void k_tx_prep(int K, int l_max_rt, int C, const double* __restrict__ pos,
-                          const double* __restrict__ ls, const double* __restrict__ q,
-                          const double* __restrict__ tau_logit,
-                          const double* __restrict__ coeffs64, double tx0, double tx1, double tx2,
-                          DevGrid g, GaussRec* __restrict__ rec, int* __restrict__ culled,
-                          double* __restrict__ geom, int4* __restrict__ spans,
-                          double* __restrict__ basis64, float2* __restrict__ basis32,
-                          float2* __restrict__ gb32, uint64_t* __restrict__ depth_key,
-                          int* __restrict__ tile_count) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= K) return;
-    const int l_max = LMT > 0 ? LMT : l_max_rt;
+// FLE basis of Gaussian k at the centre direction (theta, phi) into the
+// FP64 / f32 basis rows and the f32 basis*base rows (eval_basis,
+// radiance.cpp:79-92); zeros for a culled Gaussian.
+template <int LMT, bool FULL>
+__device__ __forceinline__ void fle_basis_row(int k, int l_max, int C, int is_culled, double theta, double phi,
+                                              const double* __restrict__ coeffs64, double* __restrict__ basis64,
+                                              float2* __restrict__ basis32, float2* __restrict__ gb32) {
     const int L = (l_max + 1) * (l_max + 1);
-    double gm[12];
-#pragma unroll
-    for (int i = 0; i < 12; ++i) gm[i] = 0.0;
-    int4 sp = make_int4(0, -1, 0, -1);
-    int is_culled = 1;
-    GaussRec r{};
-
-    double sig[9];
-    covariance(ls + 3 * static_cast<size_t>(k), q + 4 * static_cast<size_t>(k), sig);
-    const double tau = 1.0 / (1.0 + exp(-tau_logit[k]));  // linalg.hpp:157
-
-    const double u0 = pos[3 * static_cast<size_t>(k)] - tx0;
-    const double u1 = pos[3 * static_cast<size_t>(k) + 1] - tx1;
-    const double u2 = pos[3 * static_cast<size_t>(k) + 2] - tx2;
-    project_core(u0, u1, u2, sig, tau, g, gm, sp, is_culled, r);
-    const double d = gm[2], theta = gm[0], phi = gm[1];
-    if (FULL) {
-        double* gout = geom + 12 * static_cast<size_t>(k);
-#pragma unroll
-        for (int i = 0; i < 12; ++i) gout[i] = gm[i];
-    }
-    rec[k] = r;
-    culled[k] = is_culled;
-    spans[k] = sp;
-    tile_count[k] = is_culled ? 0 : (sp.y - sp.x + 1) * (sp.w - sp.z + 1);
-    depth_key[k] = is_culled ? ~0ull : static_cast<uint64_t>(__double_as_longlong(d));
-
-    // FLE basis at the centre direction (zero for culled Gaussians).
     double* b64 = basis64 + static_cast<size_t>(k) * L * 2;
     float2* b32 = basis32 + static_cast<size_t>(k) * L;
     float2* g32 = gb32 + static_cast<size_t>(k) * L * C;
@@ -229,6 +195,66 @@ __global__ void k_tx_prep(int K, int l_max_rt, int C, const double* __restrict__
         }
     }
 #undef AT
+}
+
+
+template <int LMT, bool FULL, bool BASIS>  // LMT > 0: l_max known at compile time (tables in registers)
+__global__ void k_tx_prep(int K, int l_max_rt, int C, const double* __restrict__ pos,
+                          const double* __restrict__ ls, const double* __restrict__ q,
+                          const double* __restrict__ tau_logit,
+                          const double* __restrict__ coeffs64, double tx0, double tx1, double tx2,
+                          DevGrid g, GaussRec* __restrict__ rec, int* __restrict__ culled,
+                          double* __restrict__ geom, int4* __restrict__ spans,
+                          double* __restrict__ basis64, float2* __restrict__ basis32,
+                          float2* __restrict__ gb32, uint64_t* __restrict__ depth_key,
+                          int* __restrict__ tile_count) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    const int l_max = LMT > 0 ? LMT : l_max_rt;
+    double gm[12];
+#pragma unroll
+    for (int i = 0; i < 12; ++i) gm[i] = 0.0;
+    int4 sp = make_int4(0, -1, 0, -1);
+    int is_culled = 1;
+    GaussRec r{};
+
+    double sig[9];
+    covariance(ls + 3 * static_cast<size_t>(k), q + 4 * static_cast<size_t>(k), sig);
+    const double tau = 1.0 / (1.0 + exp(-tau_logit[k]));  // linalg.hpp:157
+
+    const double u0 = pos[3 * static_cast<size_t>(k)] - tx0;
+    const double u1 = pos[3 * static_cast<size_t>(k) + 1] - tx1;
+    const double u2 = pos[3 * static_cast<size_t>(k) + 2] - tx2;
+    project_core(u0, u1, u2, sig, tau, g, gm, sp, is_culled, r);
+    const double d = gm[2], theta = gm[0], phi = gm[1];
+    if (FULL) {
+        double* gout = geom + 12 * static_cast<size_t>(k);
+#pragma unroll
+        for (int i = 0; i < 12; ++i) gout[i] = gm[i];
+    }
+    rec[k] = r;
+    culled[k] = is_culled;
+    spans[k] = sp;
+    tile_count[k] = is_culled ? 0 : (sp.y - sp.x + 1) * (sp.w - sp.z + 1);
+    depth_key[k] = is_culled ? ~0ull : static_cast<uint64_t>(__double_as_longlong(d));
+
+    // FLE basis at the centre direction (zero for culled Gaussians).  A lean
+    // build (BASIS = false) defers it to k_basis_rows for the Gaussians the
+    // walk reaches (compact_needed): the only rows the query path reads.
+    if (BASIS) fle_basis_row<LMT, FULL>(k, l_max, C, is_culled, theta, phi, coeffs64, basis64, basis32, gb32);
+}
+
+// The needed rows' f32 basis and basis*base of a lean build, from the walk
+// records' theta / phi: the same arithmetic as k_tx_prep's basis.
+template <int LMT>
+__global__ void k_basis_rows(const int* __restrict__ n_rows, const int* __restrict__ rows, int l_max_rt, int C,
+                             const GaussRec* __restrict__ rec, const double* __restrict__ coeffs64,
+                             float2* __restrict__ basis32, float2* __restrict__ gb32) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= *n_rows) return;
+    const int k = rows[r];
+    const int l_max = LMT > 0 ? LMT : l_max_rt;
+    fle_basis_row<LMT, false>(k, l_max, C, 0, rec[k].theta, rec[k].phi, coeffs64, nullptr, basis32, gb32);
 }
 
 // ---------------------------------------------------------------- single-call API kernels
@@ -468,15 +494,27 @@ cudaError_t launch_tx_prep(const rxgs_scene_s& sc, rxgs_txstate_s& st, cudaStrea
     if (sc.k == 0) return cudaSuccess;
     const int threads = 128;
     const int blocks = (sc.k + threads - 1) / threads;
-    auto kern = full ? (sc.l_max == 2 ? k_tx_prep<2, true> : (sc.l_max == 9 ? k_tx_prep<9, true> : k_tx_prep<0, true>))
-                     : (sc.l_max == 2 ? k_tx_prep<2, false>
-                                      : (sc.l_max == 9 ? k_tx_prep<9, false> : k_tx_prep<0, false>));
+    auto kern = full ? (sc.l_max == 2 ? k_tx_prep<2, true, true>
+                                      : (sc.l_max == 9 ? k_tx_prep<9, true, true> : k_tx_prep<0, true, true>))
+                     : (sc.l_max == 2 ? k_tx_prep<2, false, false>
+                                      : (sc.l_max == 9 ? k_tx_prep<9, false, false> : k_tx_prep<0, false, false>));
     kern<<<blocks, threads, 0, s>>>(
         sc.k, sc.l_max, sc.channels, sc.d_pos.as<double>(), sc.d_ls.as<double>(),
         sc.d_q.as<double>(), sc.d_tau.as<double>(), sc.d_coeffs64.as<double>(), st.tx[0], st.tx[1],
         st.tx[2], st.grid, st.rec.as<GaussRec>(), st.culled.as<int>(), st.geom.as<double>(),
         st.spans.as<int4>(), st.basis64.as<double>(), st.basis32.as<float2>(),
         st.gb32.as<float2>(), st.depth_key.as<uint64_t>(), st.tile_count.as<int>());
+    return cudaGetLastError();
+}
+
+cudaError_t launch_basis_rows(const rxgs_scene_s& sc, rxgs_txstate_s& st, cudaStream_t s) {
+    if (st.visible <= 0) return cudaSuccess;
+    const int threads = 128;
+    const unsigned blocks = static_cast<unsigned>((st.visible + threads - 1) / threads);
+    auto kern = sc.l_max == 2 ? k_basis_rows<2> : (sc.l_max == 9 ? k_basis_rows<9> : k_basis_rows<0>);
+    kern<<<blocks, threads, 0, s>>>(st.needed_count.as<int>(), st.needed_order.as<int>(), sc.l_max, sc.channels,
+                                    st.rec.as<GaussRec>(), sc.d_coeffs64.as<double>(), st.basis32.as<float2>(),
+                                    st.gb32.as<float2>());
     return cudaGetLastError();
 }
 

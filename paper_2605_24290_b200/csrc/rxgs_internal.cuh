@@ -254,6 +254,8 @@ void timing_end(rxgs_ctx ctx, const char* name, cudaEvent_t a, double work);
 
 // ---- k_geometry.cu (FP64, compiled with -fmad=false)
 cudaError_t launch_tx_prep(const rxgs_scene_s& sc, rxgs_txstate_s& st, cudaStream_t s, bool full);
+// the lean build's basis rows for the needed Gaussians (after compact_needed)
+cudaError_t launch_basis_rows(const rxgs_scene_s& sc, rxgs_txstate_s& st, cudaStream_t s);
 // Completes a lean state with its FP64 geometry / basis (capi.cu): the scene
 // must still have the geometry the state was built from.
 int ensure_tx_full(rxgs_txstate_s& st, cudaStream_t s);
