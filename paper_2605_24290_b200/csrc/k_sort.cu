@@ -33,6 +33,8 @@
 // digit carries the count across rounds; an exclusive prefix over the warps
 // plus the block's offset from the (digit, block) scan gives each item its
 // output position.
+#include <algorithm>
+
 #include "rxgs_internal.cuh"
 
 namespace rxgs_b200 {
@@ -159,13 +161,19 @@ __global__ void k_matrix_scan(int rows, int nb, int* __restrict__ mat, int* __re
     }
 }
 
-// Stable scatter of one LSD pass (see the file header).
+// Stable scatter of one LSD pass (see the file header).  The block's items
+// are staged in shared memory in (digit, input) order and written out with
+// consecutive threads on consecutive output positions (runs of one digit).
 __global__ void __launch_bounds__(kPassThreads) k_radix_scatter(int n, int nb, const uint32_t* __restrict__ kin,
                                                                  const int* __restrict__ vin, uint32_t* __restrict__ kout,
                                                                  int* __restrict__ vout, int shift,
                                                                  const int* __restrict__ mat,
                                                                  const int* __restrict__ base) {
     __shared__ int wc[kPassWarps][kBins];
+    __shared__ int gb[kBins], lb[kBins];  // global / local start of the block's run of each digit
+    __shared__ uint32_t sk[kPassM];
+    __shared__ int sv[kPassM];
+    __shared__ int wsum[kPassWarps];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < kPassWarps * kBins; i += kPassThreads) (&wc[0][0])[i] = 0;
     __syncthreads();
@@ -192,24 +200,38 @@ __global__ void __launch_bounds__(kPassThreads) k_radix_scatter(int n, int nb, c
         loc[it] = c + __popc(peers & lt);
     }
     __syncthreads();
-    for (int d = threadIdx.x; d < kBins; d += kPassThreads) {
-        int s = base[d] + mat[d * nb + b];
+    static_assert(kBins == kPassThreads, "one digit per thread");
+    {
+        const int d = threadIdx.x;
+        gb[d] = base[d] + mat[d * nb + b];
+        int s = 0;
 #pragma unroll
         for (int w = 0; w < kPassWarps; ++w) {
             const int t = wc[w][d];
             wc[w][d] = s;
             s += t;
         }
+        int tot = 0;
+        const int inc = block_incl_scan<int>(s, wsum, &tot);  // over digits
+        lb[d] = inc - s;
     }
     __syncthreads();
+    const int n_blk = n - b * kPassM < kPassM ? n - b * kPassM : kPassM;
 #pragma unroll
     for (int it = 0; it < kPassRounds; ++it) {
-        const int i = i0 + it * 32 + lane;
-        if (i >= n) continue;
+        if (i0 + it * 32 + lane >= n) continue;
         const int d = static_cast<int>((kk[it] >> shift) & (kBins - 1));
-        const int pos = wc[warp][d] + loc[it];
-        kout[pos] = kk[it];
-        vout[pos] = vv[it];
+        const int lp = lb[d] + wc[warp][d] + loc[it];
+        sk[lp] = kk[it];
+        sv[lp] = vv[it];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_blk; i += kPassThreads) {
+        const uint32_t k = sk[i];
+        const int d = static_cast<int>((k >> shift) & (kBins - 1));
+        const int pos = gb[d] + (i - lb[d]);
+        kout[pos] = k;
+        vout[pos] = sv[i];
     }
 }
 
@@ -530,6 +552,12 @@ __global__ void __launch_bounds__(kTileThreads) k_emit_entries(int64_t E, int nb
 // Stable scatter of the entries by tile (rank order within a tile) from the
 // emitted (tile, rank) arrays; writes list[pos] = Gaussian, keys[pos] =
 // (tile << 32) | rank, and the tile offsets.
+// Stable counting-sort pass by tile of one block's kTileM entries.  The
+// ranking (warp ballots, warp-private counters) gives every entry its output
+// position; the entries are then staged in shared memory in (tile, rank)
+// order, aliased over the consumed per-warp counters, and written out so
+// that consecutive threads write consecutive list / key positions (runs of
+// one tile) instead of 32 scattered tiles per warp store.
 __global__ void __launch_bounds__(kTileThreads) k_tile_scatter(int64_t E, int nb, int n_tiles,
                                                                 const uint32_t* __restrict__ tkey,
                                                                 const int* __restrict__ tval,
@@ -539,8 +567,12 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_scatter(int64_t E, int nb
                                                                 uint64_t* __restrict__ keys,
                                                                 int64_t* __restrict__ tile_offsets) {
     extern __shared__ int sm[];
-    int* tb = sm;                                          // n_tiles: block offset per tile
-    uint16_t* wc = reinterpret_cast<uint16_t*>(tb + n_tiles);  // kTileWarps x n_tiles (< 8192 each)
+    int* tb = sm;                          // n_tiles: global offset of this block's run of each tile
+    int* ls = tb + n_tiles;                // n_tiles: local (block) start of each tile's run
+    int* s_tot = ls + n_tiles;             // kTileThreads: scan scratch
+    uint16_t* wc = reinterpret_cast<uint16_t*>(s_tot + kTileThreads);  // kTileWarps x n_tiles (< 8192 each)
+    int* st_r = reinterpret_cast<int*>(wc);                                // staged ranks (aliases wc)
+    uint16_t* st_t = reinterpret_cast<uint16_t*>(st_r + kTileM);           // staged tiles
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < kTileWarps * n_tiles; i += kTileThreads) wc[i] = 0;
     if (blockIdx.x == 0)
@@ -556,6 +588,12 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_scatter(int64_t E, int nb
         const int q = q0 + it * 32 + lane;
         pk[it] = q < n ? __ldg(tkey + e0 + q) : 0u;
     }
+    int rv[kTileRounds];
+#pragma unroll
+    for (int it = 0; it < kTileRounds; ++it) {
+        const int q = q0 + it * 32 + lane;
+        rv[it] = q < n ? __ldg(tval + e0 + q) : 0;
+    }
 #pragma unroll
     for (int it = 0; it < kTileRounds; ++it) {
         const bool ok = q0 + it * 32 + lane < n;
@@ -568,24 +606,64 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_scatter(int64_t E, int nb
         pk[it] = (static_cast<uint32_t>(t) << 12) | static_cast<uint32_t>(c + __popc(peers & lt));
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < n_tiles; t += kTileThreads) {
+    // per tile: global base, exclusive prefix over warps, and the block count;
+    // the block counts' exclusive scan over tiles -> local starts
+    const int per = (n_tiles + kTileThreads - 1) / kTileThreads;  // tiles per thread (contiguous)
+    int my_sum = 0;
+    for (int u = 0; u < per; ++u) {
+        const int t = threadIdx.x * per + u;
+        if (t >= n_tiles) break;
         tb[t] = base[t] + mat[t * nb + blockIdx.x];
-        int s = 0;
+        int acc = 0;
 #pragma unroll
         for (int w = 0; w < kTileWarps; ++w) {
             const int v = wc[w * n_tiles + t];
-            wc[w * n_tiles + t] = static_cast<uint16_t>(s);
-            s += v;
+            wc[w * n_tiles + t] = static_cast<uint16_t>(acc);
+            acc += v;
         }
+        ls[t] = acc;  // block count for now
+        my_sum += acc;
+    }
+    s_tot[threadIdx.x] = my_sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {  // exclusive scan of the thread sums (kTileThreads values)
+        int a = 0;
+        for (int i = 0; i < kTileThreads; ++i) {
+            const int v = s_tot[i];
+            s_tot[i] = a;
+            a += v;
+        }
+    }
+    __syncthreads();
+    {
+        int a = s_tot[threadIdx.x];
+        for (int u = 0; u < per; ++u) {
+            const int t = threadIdx.x * per + u;
+            if (t >= n_tiles) break;
+            const int v = ls[t];
+            ls[t] = a;
+            a += v;
+        }
+    }
+    __syncthreads();
+    // local position of every entry (reads wc), then stage over wc
+    int lp[kTileRounds];
+#pragma unroll
+    for (int it = 0; it < kTileRounds; ++it) {
+        const int t = static_cast<int>(pk[it] >> 12);
+        lp[it] = ls[t] + wc[warp * n_tiles + t] + static_cast<int>(pk[it] & 0xFFFu);
     }
     __syncthreads();
 #pragma unroll
     for (int it = 0; it < kTileRounds; ++it) {
-        const int q = q0 + it * 32 + lane;
-        if (q >= n) continue;
-        const int t = static_cast<int>(pk[it] >> 12);
-        const int pos = tb[t] + wc[warp * n_tiles + t] + static_cast<int>(pk[it] & 0xFFFu);
-        const int r = __ldg(tval + e0 + q);
+        if (q0 + it * 32 + lane >= n) continue;
+        st_r[lp[it]] = rv[it];
+        st_t[lp[it]] = static_cast<uint16_t>(pk[it] >> 12);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += kTileThreads) {
+        const int t = st_t[i], r = st_r[i];
+        const int pos = tb[t] + (i - ls[t]);
         list[pos] = __ldg(order + r);
         keys[pos] = (static_cast<uint64_t>(t) << 32) | static_cast<uint32_t>(r);
     }
@@ -755,7 +833,8 @@ int bin_tiles(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
         k_emit_entries<<<nbt, kTileThreads, sm_e, s>>>(E, nbt, n_tiles, st.grid.tiles_p, st.scan.as<int64_t>(), bfirst,
                                                        blast, spans_sorted, tk, tv, mat);
         k_matrix_scan<<<n_tiles, 256, 0, s>>>(n_tiles, nbt, mat, tot, tbase, counter);
-        const size_t sm_s = 4 * static_cast<size_t>(n_tiles) + 2 * static_cast<size_t>(kTileWarps) * n_tiles;
+        const size_t sm_s = 4 * (2 * static_cast<size_t>(n_tiles) + kTileThreads) +
+                            std::max(2 * static_cast<size_t>(kTileWarps) * n_tiles, 6 * static_cast<size_t>(kTileM));
         RXGS_CUDA(cudaFuncSetAttribute(k_tile_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sm_s)));
         k_tile_scatter<<<nbt, kTileThreads, sm_s, s>>>(E, nbt, n_tiles, tk, tv, st.order.as<int>(), mat, tbase,
