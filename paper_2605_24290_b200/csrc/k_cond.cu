@@ -341,6 +341,43 @@ __global__ void k_cond_materialize(CondDev c, int K, const float4* __restrict__ 
         }
 }
 
+// condition_forward's materialised output (conditioning.cpp:340-421) of the
+// needed rows from the local branch's (alpha_L, beta_L) y[k][j] (tcgen05,
+// launch_local_y_rows): out = affine_L(affine_G(base)) in FP64, the
+// reference's operation order; C == 1.
+__global__ void k_materialize_y(CondDev c, int K, int L, int n_rx, const int* __restrict__ rows,
+                                const int* __restrict__ n_rows, const double* __restrict__ base,
+                                const float* __restrict__ ag, const float4* __restrict__ y,
+                                double* __restrict__ out) {
+    const long long row = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    const int n = *n_rows;
+    if (row >= static_cast<long long>(n) * n_rx) return;
+    const int j = static_cast<int>(row / n);
+    const int k = rows[row % n];
+    const float4 yl = c.use_local ? y[static_cast<size_t>(k) * n_rx + j] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const double ar = c.additive ? 0.0 : yl.x, ai = c.additive ? 0.0 : yl.y, br = yl.z, bi = yl.w;
+    const size_t stride = static_cast<size_t>(L) * 2;
+    for (int l = 0; l < L; ++l) {
+        const size_t idx = static_cast<size_t>(k) * stride + static_cast<size_t>(l) * 2;
+        const double zr = base[idx], zi = base[idx + 1];
+        double mr = zr, mi = zi;
+        if (c.use_global) {
+            const float* a = ag + (static_cast<size_t>(j) * L + l) * 4;
+            const double gar = a[0], gai = a[1], gbr = a[2], gbi = a[3];
+            mr = zr + (gar * zr - gai * zi + gbr);
+            mi = zi + (gai * zr + gar * zi + gbi);
+        }
+        double orr = mr, oi = mi;
+        if (c.use_local) {
+            orr = mr + (ar * mr - ai * mi + br);
+            oi = mi + (ai * mr + ar * mi + bi);
+        }
+        const size_t o = static_cast<size_t>(j) * K * stride + idx;
+        out[o] = orr;
+        out[o + 1] = oi;
+    }
+}
+
 __global__ void k_probe(CondDev c, int n, const double* __restrict__ from,
                         const double* __restrict__ to, double* __restrict__ out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -481,6 +518,16 @@ cudaError_t launch_cond_materialize(const rxgs_cond_s& c, const rxgs_scene_s& sc
     k_cond_materialize<<<static_cast<unsigned>((rows + 255) / 256), 256, smem, s>>>(
         d, sc.k, sc.d_pos32.as<float4>(), d_rx, n_rx, sc.d_coeffs64.as<double>(), d_ag, d_out,
         d_local_in);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_materialize_y(const rxgs_cond_s& c, const rxgs_scene_s& sc, const rxgs_txstate_s& st, int n_rx,
+                                 const float* d_ag, const float4* y, double* d_out, cudaStream_t s) {
+    if (st.visible == 0 || n_rx == 0) return cudaSuccess;
+    const long long bound = static_cast<long long>(st.visible) * n_rx;
+    k_materialize_y<<<static_cast<unsigned>((bound + 255) / 256), 256, 0, s>>>(
+        make_dev(c), sc.k, sc.L, n_rx, st.needed_order.as<int>(), st.needed_count.as<int>(),
+        sc.d_coeffs64.as<double>(), d_ag, y, d_out);
     return cudaGetLastError();
 }
 

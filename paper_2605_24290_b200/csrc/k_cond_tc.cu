@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t w1hi_a = tc::smem_u32(w1hi), w1lo_a = tc::smem_u32(w1lo);
     const uint32_t b2hi_a = tc::smem_u32(b2hi), aone_a = tc::smem_u32(aone);
 
-    const int n_rows = YOUT ? n_rows_host : *n_rows_dev;
+    const int n_rows = (YOUT && !n_rows_dev) ? n_rows_host : *n_rows_dev;
     const int nq = (n_rx + 3) >> 2;
     const long long tiles = static_cast<long long>((n_rows + 31) >> 5) * nq;
     const long long step = static_cast<long long>(gridDim.x) * kGroups;
@@ -952,7 +952,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     __syncthreads();
     tc::fence_after_sync();
 
-    const int n_rows = YOUT ? n_rows_host : *n_rows_dev;
+    const int n_rows = (YOUT && !n_rows_dev) ? n_rows_host : *n_rows_dev;
     const int nq = (n_rx + 3) >> 2;
     const long long tiles = static_cast<long long>((n_rows + 31) >> 5) * nq;
     const long long step = static_cast<long long>(gridDim.x) * kGroups;
@@ -1734,6 +1734,19 @@ cudaError_t gather_rows(const rxgs_scene_s& sc, const rxgs_txstate_s& st, cudaSt
     ctx->rows_version = st.version;
     ctx->fle_a_version = 0;
     return cudaSuccess;
+}
+
+// Local-branch outputs y = (alpha_L, beta_L) of a state's needed rows,
+// y[k * n_rx + j] (the joint step's materialised conditioning)
+cudaError_t launch_local_y_rows(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
+                                const double* d_rx, int n_rx, float4* y, cudaStream_t s) {
+    if (st.visible == 0 || n_rx == 0) return cudaSuccess;
+    rxgs_ctx ctx = sc.ctx;
+    cudaError_t e;
+    if ((e = gather_rows(sc, st, s)) != cudaSuccess) return e;
+    const long long bound = st.needed_host >= 0 ? st.needed_host : st.visible;
+    return launch_tc<true>(cs, st.needed_count.as<int>(), bound, st.k, st.needed_order.as<int>(),
+                           ctx->row_pos.as<float4>(), d_rx, n_rx, nullptr, nullptr, nullptr, nullptr, SigOut(), y, s);
 }
 
 cudaError_t launch_local_cache_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const double* d_rx, int n_rx,

@@ -317,6 +317,12 @@ cudaError_t launch_cond_materialize(const rxgs_cond_s& c, const rxgs_scene_s& sc
                                     const double* d_rx, int n_rx, const float* d_ag, double* d_out,
                                     double* d_local_in, int* d_err, cudaStream_t s);
 // the same, only for the TxState's needed Gaussians (other rows untouched)
+// the joint step's materialised conditioning on tcgen05: y = (alpha_L, beta_L)
+// of the needed rows, then both affines in FP64 (C == 1)
+cudaError_t launch_local_y_rows(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
+                                const double* d_rx, int n_rx, float4* y, cudaStream_t s);
+cudaError_t launch_materialize_y(const rxgs_cond_s& c, const rxgs_scene_s& sc, const rxgs_txstate_s& st, int n_rx,
+                                 const float* d_ag, const float4* y, double* d_out, cudaStream_t s);
 cudaError_t launch_cond_materialize_needed(const rxgs_cond_s& c, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
                                            const double* d_rx, int n_rx, const float* d_ag, double* d_out,
                                            cudaStream_t s);

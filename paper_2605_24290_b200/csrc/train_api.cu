@@ -40,6 +40,7 @@ struct rxgs_trainer_s {
     int64_t n_geo = 0;
     DevBuf co64, dv64, b_sig, b_eg, b_eds, b_rg, b_rds, geo_tmp;
     DevBuf act;  // per-row activations of the split conditioning backward
+    DevBuf ylocal;  // joint step: (alpha_L, beta_L) of the needed rows, K x n_rx
     // DensifyState (scene.hpp:69-79) of the Stage-I loop, accumulated in apply
     DevBuf dens_acc, dens_cnt;
     // optimizer.reset("transmittance") restarts that group's Adam count
@@ -69,6 +70,20 @@ bool is_dev(const void* p) {
 
 namespace {
 
+// The tcgen05 conditioning kernels take the local layer 3 as a kernel
+// parameter built from the host copy of the parameters: refresh those values
+// after an optimizer step (the rest of the host copy stays stale until a
+// query path needs it).
+int refresh_local_w3(rxgs_cond c, cudaStream_t s) {
+    if (!c || !c->host_stale) return RXGS_OK;
+    RXGS_CUDA(cudaStreamSynchronize(s));
+    const double* dp = c->d_params64.as<double>();
+    RXGS_CUDA(cudaMemcpy(c->h_params.data() + c->o_lw3, dp + c->o_lw3, sizeof(double) * 4 * c->hidden,
+                         cudaMemcpyDeviceToHost));
+    RXGS_CUDA(cudaMemcpy(c->h_params.data() + c->o_lb3, dp + c->o_lb3, sizeof(double) * 4, cudaMemcpyDeviceToHost));
+    return RXGS_OK;
+}
+
 int geometry_grads(rxgs_trainer t, rxgs_txstate_s& st, const double* d_rx, int n_rx, int P, bool accumulate,
                    cudaStream_t s) {
     rxgs_ctx ctx = t->ctx;
@@ -80,8 +95,16 @@ int geometry_grads(rxgs_trainer t, rxgs_txstate_s& st, const double* d_rx, int n
         // only the needed rows: the re-walk reads signals of walked entries, and
         // the basis-jet term only rows with a non-zero signal adjoint
         RXGS_CUDA(cudaMemsetAsync(t->co64.p, 0, nco * sizeof(double), s));
-        RXGS_CUDA(launch_cond_materialize_needed(*t->c, *sc, st, d_rx, n_rx, ctx->ag.as<float>(), t->co64.as<double>(),
-                                                 s));
+        if (cond_tc_eligible(t->c)) {  // local branch on tcgen05, the affines in FP64
+            TRY(refresh_local_w3(t->c, s));
+            RXGS_CUDA(t->ylocal.ensure(std::max<size_t>(static_cast<size_t>(K) * n_rx, 1) * sizeof(float4)));
+            RXGS_CUDA(launch_local_y_rows(*t->c, *sc, st, d_rx, n_rx, t->ylocal.as<float4>(), s));
+            RXGS_CUDA(launch_materialize_y(*t->c, *sc, st, n_rx, ctx->ag.as<float>(), t->ylocal.as<float4>(),
+                                           t->co64.as<double>(), s));
+        } else {
+            RXGS_CUDA(launch_cond_materialize_needed(*t->c, *sc, st, d_rx, n_rx, ctx->ag.as<float>(),
+                                                     t->co64.as<double>(), s));
+        }
     } else {  // Stage I: every receiver sees the scene's own coefficients
         const size_t one = nco / std::max(n_rx, 1);
         for (int j = 0; j < n_rx; ++j)
@@ -248,16 +271,7 @@ int rxgs_train_grads(rxgs_trainer t, rxgs_txstate st, const double* rx, int n_rx
     const int saved = ctx->cond_kernel;
     ctx->cond_kernel = train_cond >= 0 ? train_cond : (l1_only ? 0 : 1);
     const bool tc_cond = ctx->cond_kernel == 0 && c && cond_tc_eligible(c);
-    if (tc_cond && c->host_stale) {
-        // the tcgen05 kernel takes the local layer 3 as a kernel parameter
-        // built from the host copy: refresh those values after an optimizer step
-        RXGS_CUDA(cudaStreamSynchronize(s));
-        const double* dp = c->d_params64.as<double>();
-        RXGS_CUDA(cudaMemcpy(c->h_params.data() + c->o_lw3, dp + c->o_lw3, sizeof(double) * 4 * c->hidden,
-                             cudaMemcpyDeviceToHost));
-        RXGS_CUDA(cudaMemcpy(c->h_params.data() + c->o_lb3, dp + c->o_lb3, sizeof(double) * 4,
-                             cudaMemcpyDeviceToHost));
-    }
+    if (tc_cond) TRY(refresh_local_w3(c, s));
     const cudaError_t ef = launch_cond_signal(c, *sc, *st, d_rx, n_rx, ctx->ag.as<float>(),
                                               ctx->signals.as<float2>(), nullptr, s);
     ctx->cond_kernel = saved;
