@@ -111,7 +111,11 @@ __global__ void __launch_bounds__(64) k_bwd_walk(DevGrid g, int cb, const int64_
                                                  const int* __restrict__ walk_len, const double2* __restrict__ sig,
                                                  int n_jc, const double* __restrict__ dvals, int64_t n_ent,
                                                  double* __restrict__ ent_geo, double2* __restrict__ ent_ds) {
-    __shared__ double red[2][7 + 2 * kNC];
+    constexpr int kV = 7 + 2 * kNC;
+    // per-warp block sums of the last 32 positions, flushed to the entry
+    // records 32 positions at a time by all threads (red[0] + red[1], then
+    // accumulated: the order of the former per-position flush)
+    __shared__ double ring[2][32][kV];
     const int tile = blockIdx.x, lane = threadIdx.x;
     // receiver chunk blockIdx.y: its own slice of the per-entry geometry sums
     const int jc0 = blockIdx.y * kNC, nc = n_jc - jc0 < kNC ? n_jc - jc0 : kNC;
@@ -214,27 +218,60 @@ __global__ void __launch_bounds__(64) k_bwd_walk(DevGrid g, int cb, const int64_
                 v[6] = -d_dp * st;
             }
         }
+        if constexpr (kV <= 16) {
+            // reduce-scatter by recursive halving (8 + 4 + 2 + 1 exchanges, then a
+            // final pair add): lane l ends with the warp sum of value
+            // 8 b4 + 4 b3 + 2 b2 + b1 (b_i = bit i of l); fixed order
+            double h8[8];
+            const bool up16 = (wl & 16) != 0;
 #pragma unroll
-        for (int i = 0; i < 7 + 2 * kNC; ++i) {
-            if (i >= 7 + 2 * nc) break;
-            double x = v[i];
+            for (int i = 0; i < 8; ++i) {
+                const double lo = v[i], hi = (i + 8 < kV) ? v[i + 8] : 0.0;
+                const double send = up16 ? lo : hi, keep = up16 ? hi : lo;
+                h8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+            }
+            double h4[4];
+            const bool up8 = (wl & 8) != 0;
 #pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-            if (wl == 0) red[warp][i] = x;
-        }
-        __syncthreads();
-        if (lane == 0) {
-            const int64_t e = begin + p;
-            double* og = ent_geo + e * 7;
-            for (int i = 0; i < 7; ++i) og[i] += red[0][i] + red[1][i];
-            for (int q = 0; q < nc; ++q) {
-                double2 a = ent_ds[e * n_jc + jc0 + q];
-                a.x += red[0][7 + 2 * q] + red[1][7 + 2 * q];
-                a.y += red[0][8 + 2 * q] + red[1][8 + 2 * q];
-                ent_ds[e * n_jc + jc0 + q] = a;
+            for (int i = 0; i < 4; ++i) {
+                const double send = up8 ? h8[i] : h8[i + 4], keep = up8 ? h8[i + 4] : h8[i];
+                h4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+            }
+            double h2[2];
+            const bool up4 = (wl & 4) != 0;
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const double send = up4 ? h4[i] : h4[i + 2], keep = up4 ? h4[i + 2] : h4[i];
+                h2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+            }
+            const bool up2 = (wl & 2) != 0;
+            double h1 = (up2 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, up2 ? h2[0] : h2[1], 2);
+            h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+            const int idx = 8 * ((wl >> 4) & 1) + 4 * ((wl >> 3) & 1) + 2 * ((wl >> 2) & 1) + ((wl >> 1) & 1);
+            if ((wl & 1) == 0 && idx < 7 + 2 * nc) ring[warp][p & 31][idx] = h1;
+        } else {
+#pragma unroll
+            for (int i = 0; i < kV; ++i) {
+                if (i >= 7 + 2 * nc) break;
+                double x = v[i];
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+                if (wl == 0) ring[warp][p & 31][i] = x;
             }
         }
-        __syncthreads();
+        if ((p & 31) == 31 || p == W - 1) {
+            __syncthreads();
+            const int p0 = p & ~31, np = p - p0 + 1, nv = 7 + 2 * nc;
+            for (int idx = lane; idx < np * nv; idx += 64) {
+                const int pp = idx / nv, i = idx % nv;
+                const int64_t e = begin + p0 + pp;
+                const double x = ring[0][pp][i] + ring[1][pp][i];
+                double* dst = i < 7 ? ent_geo + e * 7 + i
+                                    : reinterpret_cast<double*>(ent_ds) + (e * n_jc + jc0 + (i - 7) / 2) * 2 + (i - 7) % 2;
+                *dst += x;
+            }
+            __syncthreads();
+        }
     }
 }
 
