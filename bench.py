@@ -572,12 +572,17 @@ def bench_coverage(args, capi, ctx, stream, dev, rank, world):
     phases = {n: ctx.kernel_stats(n)[0] for n in ("cond_global", "local_cache", "tx_prep", "sort", "walk",
                                                    "cov_signal", "composite")}
     ctx.profile(False)
-    # end to end with host buffers (tx/rx in, table out)
+    # end to end with host buffers (tx/rx in, table out): one untimed call
+    # (first use of the host-buffer path: lazy module loads, staging buffers),
+    # then the mean of two timed calls
     out_h = np.empty((tx.shape[0], rx.shape[0]), np.float32)
-    torch.cuda.synchronize(dev)
-    t0 = time.perf_counter()
     scene.coverage_table(cond, grid, tx, rx, out_h)
-    e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3, dev)
+    torch.cuda.synchronize(dev)
+    n_e2e = 2
+    t0 = time.perf_counter()
+    for _ in range(n_e2e):
+        scene.coverage_table(cond, grid, tx, rx, out_h)
+    e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / n_e2e, dev)
     queries = n_tx * n_rx_total
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
