@@ -1318,26 +1318,29 @@ int rxgs_render_queries(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, rxgs_txstate s
     // overlap the conditioning of chunk i+1
     const size_t per_rx = std::max<size_t>(static_cast<size_t>(sc->k), 1) * sizeof(float2);
     int chunk = static_cast<int>(std::min<size_t>(static_cast<size_t>(n_rx), (size_t{4} << 30) / per_rx));
-    // host spectra: four shrinking receiver chunks (3/8, 5/16, 3/16, 1/8 of
-    // the batch, multiples of 32): the D2H of each overlaps the next chunk's
-    // compute and only the smallest, last one is exposed
+    // host spectra: receiver chunks (multiples of 32) whose D2H overlaps the
+    // next chunk's compute; only the last, small one is exposed
     const bool pipelined = out_spectrum && d_spec != out_spectrum && n_rx >= 256;
     std::vector<int> bounds{0};
     if (pipelined) {
         // receiver-chunk schedules of the host-output pipeline (fractions of
-        // the batch at the chunk ends).  A/B on one B200, config 2 (e2e):
-        // schedule 0 is the default; RXGS_E2E_SCHED selects another at run time.
+        // the batch at the chunk ends).  A/B on one B200, config 2 (e2e, the
+        // global branch and FLE GEMM batched once; scripts/probe_e2e_sched.py,
+        // median of 15): 6 = 3.59-3.62 ms, 3 = 3.63-3.67, 2 = 3.67-3.68,
+        // 0 = 3.71-3.74; 6 is the default, RXGS_E2E_SCHED selects another.
         static const std::vector<std::vector<double>> kSched = {
             {3.0 / 8, 3.0 / 8 + 5.0 / 16, 7.0 / 8, 7.0 / 8 + 3.0 / 32, 1.0},   // 0
             {3.0 / 8, 3.0 / 8 + 5.0 / 16, 7.0 / 8, 1.0},                       // 1
             {1.0 / 8, 3.0 / 8, 5.0 / 8, 27.0 / 32, 31.0 / 32, 1.0},            // 2
             {1.0 / 4, 1.0 / 2, 3.0 / 4, 15.0 / 16, 1.0},                       // 3
             {1.0 / 8, 1.0 / 2, 7.0 / 8, 31.0 / 32, 1.0},                       // 4
+            {1.0 / 8, 3.0 / 8, 5.0 / 8, 13.0 / 16, 15.0 / 16, 1.0},            // 5
+            {3.0 / 16, 7.0 / 16, 11.0 / 16, 7.0 / 8, 1.0},                     // 6
         };
         static const int sched = [] {
             const char* e = std::getenv("RXGS_E2E_SCHED");
-            const int v = e ? std::atoi(e) : 0;
-            return v >= 0 && v < 5 ? v : 0;
+            const int v = e ? std::atoi(e) : 6;
+            return v >= 0 && v < static_cast<int>(kSched.size()) ? v : 6;
         }();
         const std::vector<double>& frac = kSched[static_cast<size_t>(sched)];
         for (double f : frac) {
@@ -1363,9 +1366,56 @@ int rxgs_render_queries(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, rxgs_txstate s
     // the tcgen05 compositor reads the signals pre-split into bf16 hi/lo
     const bool tc_comp = ctx->composite_kernel != 1 && composite_tc_eligible(*st);
     const SigOut so = tc_comp ? SigOut::presplit(ctx->signals.p) : SigOut(ctx->signals.as<float2>());
+    // several chunks: the receiver-independent and whole-batch work once --
+    // the global branch for all receivers and, on the tensor-core path, the
+    // row gather and the FLE GEMM -- so each chunk launches only the
+    // conditioning kernel (per-chunk global branch / GEMM measured +0.5 ms
+    // over five chunks at config 2)
+    const bool batched = c && bounds.size() > 2;
+    const bool tc_cond = batched && ctx->cond_kernel != 1 && cond_tc_eligible(c);
+    const float2* mpre_all = nullptr;
+    const size_t ag_row = static_cast<size_t>(sc->L) * 4 * sc->channels;  // floats per receiver
+    if (batched) {
+        if (c->host_stale) {  // the tcgen05 kernel takes layers 1/3 from the host copy
+            RXGS_CUDA(cudaStreamSynchronize(s));
+            RXGS_CUDA(cudaMemcpy(c->h_params.data(), c->d_params64.p, c->h_params.size() * sizeof(double),
+                                 cudaMemcpyDeviceToHost));
+            c->host_stale = false;
+        }
+        RXGS_CUDA(ctx->ag.ensure(std::max<size_t>(ag_row * n_rx, 1) * sizeof(float)));
+        cudaEvent_t evg;
+        if (c->use_global()) {
+            timing_begin(ctx, "cond_global", &evg);
+            RXGS_CUDA(launch_cond_global(*c, d_rx, n_rx, ctx->ag.as<float>(), s));
+            timing_end(ctx, "cond_global", evg, static_cast<double>(n_rx) * sc->L);
+        } else {
+            RXGS_CUDA(cudaMemsetAsync(ctx->ag.p, 0, ag_row * n_rx * sizeof(float), s));
+        }
+        if (tc_cond) {
+            timing_begin(ctx, "cond_signal", &evg);
+            RXGS_CUDA(launch_cond_signal_tc_prep(*c, *sc, *st, n_rx, ctx->ag.as<float>(), s, &mpre_all));
+            timing_end(ctx, "cond_signal", evg, 0.0);
+        }
+        ctx->launches += 2;
+    }
     for (size_t ci = 0; ci + 1 < bounds.size(); ++ci) {
         const int j0 = bounds[ci], nj = bounds[ci + 1] - bounds[ci];
-        RX_TRY(compute_signals(ctx, sc, c, st, d_rx + 3 * static_cast<size_t>(j0), nj, so));
+        if (batched) {
+            const double* rxc = d_rx + 3 * static_cast<size_t>(j0);
+            const float* agc = ctx->ag.as<float>() + ag_row * j0;
+            cudaEvent_t evc;
+            timing_begin(ctx, "cond_signal", &evc);
+            if (tc_cond)
+                RXGS_CUDA(launch_cond_signal_tc(*c, *sc, *st, rxc, nj, agc, so, s,
+                                                mpre_all ? mpre_all + static_cast<size_t>(st->k) * j0 : nullptr));
+            else
+                RXGS_CUDA(launch_cond_signal(c, *sc, *st, rxc, nj, agc, so, nullptr, s));
+            timing_end(ctx, "cond_signal", evc,
+                       static_cast<double>(st->needed_host >= 0 ? st->needed_host : st->visible) * nj);
+            ctx->launches += 1;
+        } else {
+            RX_TRY(compute_signals(ctx, sc, c, st, d_rx + 3 * static_cast<size_t>(j0), nj, so));
+        }
         CompositeOut co;
         co.spectrum = d_spec ? d_spec + static_cast<size_t>(j0) * plane : nullptr;
         co.rssi_partial = d_rssi ? ctx->partial.as<float>() : nullptr;

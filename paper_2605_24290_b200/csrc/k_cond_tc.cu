@@ -1677,9 +1677,36 @@ cudaError_t launch_tc(const rxgs_cond_s& cs, const int* n_rows_dev, long long ro
 
 }  // namespace
 
+#ifndef RXGS_FLE_GEMM_MIN_L
+#define RXGS_FLE_GEMM_MIN_L 4  // A/B at L=9: GEMM 2.70 ms vs per-row loop 2.95 ms
+#endif
+
+// Receiver-independent and whole-batch work of a chunked render
+// (rxgs_render_queries with host spectra): the row gather and, at high
+// l_max, the FLE GEMM for ALL receivers, so the chunks only launch the
+// conditioning kernel.  *mpre = M[j][row] (cap rows per receiver) or null.
+cudaError_t launch_cond_signal_tc_prep(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
+                                       int n_rx, const float* d_ag, cudaStream_t s, const float2** mpre) {
+    (void)cs;
+    *mpre = nullptr;
+    if (st.visible == 0 || n_rx == 0) return cudaSuccess;
+    rxgs_ctx ctx = sc.ctx;
+    cudaError_t e;
+    if ((e = gather_rows(sc, st, s)) != cudaSuccess) return e;
+    if (st.L < RXGS_FLE_GEMM_MIN_L) return cudaSuccess;
+    const int cap = st.k;
+    const long long bound = st.needed_host >= 0 ? st.needed_host : st.visible;
+    if ((e = ctx->fle_m.ensure(sizeof(float2) * static_cast<size_t>(cap) * n_rx)) != cudaSuccess) return e;
+    if ((e = launch_fle_gemm(ctx, st.needed_count.as<int>(), bound, cap, st.L, n_rx, ctx->row_GB.as<float4>(),
+                             ctx->row_S.as<float4>(), d_ag, ctx->fle_m.as<float2>(), s, st.version)) != cudaSuccess)
+        return e;
+    *mpre = ctx->fle_m.as<float2>();
+    return cudaSuccess;
+}
+
 cudaError_t launch_cond_signal_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
                                   const double* d_rx, int n_rx, const float* d_ag, SigOut d_sig,
-                                  cudaStream_t s) {
+                                  cudaStream_t s, const float2* mpre_given) {
     if (st.visible == 0 || n_rx == 0) return cudaSuccess;
     rxgs_ctx ctx = sc.ctx;
     const int cap = st.k;
@@ -1693,11 +1720,8 @@ cudaError_t launch_cond_signal_tc(const rxgs_cond_s& cs, const rxgs_scene_s& sc,
     const long long bound = st.needed_host >= 0 ? st.needed_host : st.visible;
     if ((e = gather_rows(sc, st, s)) != cudaSuccess) return e;
     // high l_max: the FLE reduction as one tensor-core GEMM instead of the per-row loop
-#ifndef RXGS_FLE_GEMM_MIN_L
-#define RXGS_FLE_GEMM_MIN_L 4  // A/B at L=9: GEMM 2.70 ms vs per-row loop 2.95 ms
-#endif
-    const float2* Mpre = nullptr;
-    if (L >= RXGS_FLE_GEMM_MIN_L) {
+    const float2* Mpre = mpre_given;
+    if (!Mpre && L >= RXGS_FLE_GEMM_MIN_L) {
         if ((e = ctx->fle_m.ensure(sizeof(float2) * static_cast<size_t>(cap) * n_rx)) != cudaSuccess) return e;
         if ((e = launch_fle_gemm(ctx, n_rows, bound, cap, L, n_rx, ctx->row_GB.as<float4>(), ctx->row_S.as<float4>(),
                                  d_ag, ctx->fle_m.as<float2>(), s, st.version)) != cudaSuccess)

@@ -337,7 +337,9 @@ bool cond_tc_eligible(const rxgs_cond_s* c);
 bool cond_ws_enabled();
 cudaError_t launch_cond_signal_tc(const rxgs_cond_s& c, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
                                   const double* d_rx, int n_rx, const float* d_ag, SigOut d_sig,
-                                  cudaStream_t s);
+                                  cudaStream_t s, const float2* mpre_given = nullptr);
+cudaError_t launch_cond_signal_tc_prep(const rxgs_cond_s& cs, const rxgs_scene_s& sc, const rxgs_txstate_s& st,
+                                       int n_rx, const float* d_ag, cudaStream_t s, const float2** mpre);
 cudaError_t launch_tc_selftest(float* d_err, cudaStream_t s);
 // FLE reduction of the query path as a tensor-core GEMM: Mout[j][row] (k_fle_gemm.cu)
 int fle_gemm_kpad(int L);

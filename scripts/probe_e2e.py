@@ -31,3 +31,10 @@ scene.render_queries(cond, st, rxd, sd, rd); st2 = scene.tx_state(tx, grid); ctx
 for k in ("tx_prep", "walk", "cond_global", "cond_signal", "composite"):
     print(k, ctx.kernel_stats(k))
 print("stats", st.stats())
+# kernel-time totals of one device-output vs one pinned-host-output render
+for name, out in (("device", (sd, rd)), ("pinned", (sp.numpy(), rp.numpy()))):
+    ctx.profile(True); ctx.reset_stats()
+    scene.render_queries(cond, st, rxd if name == "device" else rx, *out); ctx.synchronize()
+    tot = {k: ctx.kernel_stats(k) for k in ("cond_global", "cond_signal", "composite")}
+    print(name, {k: (round(v[0], 4), v[1]) for k, v in tot.items()}, "sum", round(sum(v[0] for v in tot.values()), 4))
+    ctx.profile(False)
