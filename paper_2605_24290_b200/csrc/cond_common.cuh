@@ -255,6 +255,49 @@ __device__ __forceinline__ void local_mlp(const CondDev& c, const LocalSmem& w, 
     }
 }
 
+// local_mlp<64, 1> on W2 transposed into output pairs, w2t2[i][o / 2] =
+// (W2[o][i], W2[o + 1][i]): eight outputs at a time as four independent
+// FFMA2 chains (the row kernel's pattern); per output the sum still runs
+// over i in ascending order with fmaf, so the result is bit-identical.
+__device__ __forceinline__ void local_mlp64_t(const LocalSmem& w, const float2* __restrict__ w2t2, const float* in,
+                                              float* y) {
+    constexpr int H = 64;
+    float h1[H];
+#pragma unroll
+    for (int o = 0; o < H; ++o) {
+        float acc = w.b1[o];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) acc = fmaf(w.w1[o * 6 + i], in[i], acc);
+        h1[o] = fmaxf(acc, 0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) y[q] = w.b3[q];
+#pragma unroll 1
+    for (int op0 = 0; op0 < H / 2; op0 += 4) {  // output pairs op0 .. op0 + 3 (outputs 2 op0 .. 2 op0 + 7)
+        float2 ac[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) ac[u] = make_float2(w.b2[2 * (op0 + u)], w.b2[2 * (op0 + u) + 1]);
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+            const float4* wq = reinterpret_cast<const float4*>(w2t2 + i * (H / 2) + op0);
+            const float4 w01 = wq[0], w23 = wq[1];
+            ac[0] = x2::fma(make_float2(w01.x, w01.y), x2::bc(h1[i]), ac[0]);
+            ac[1] = x2::fma(make_float2(w01.z, w01.w), x2::bc(h1[i]), ac[1]);
+            ac[2] = x2::fma(make_float2(w23.x, w23.y), x2::bc(h1[i]), ac[2]);
+            ac[3] = x2::fma(make_float2(w23.z, w23.w), x2::bc(h1[i]), ac[3]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int o = 2 * (op0 + u);
+            const float hv0 = fmaxf(ac[u].x, 0.f), hv1 = fmaxf(ac[u].y, 0.f);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) y[q] = fmaf(w.w3[q * H + o], hv0, y[q]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) y[q] = fmaf(w.w3[q * H + o + 1], hv1, y[q]);
+        }
+    }
+}
+
 // Store one signal value (k, j, channel ch) in the requested format.
 __device__ __forceinline__ void store_sig(const SigOut& o, int k, int n_rx, int j, int C, int ch, float2 v) {
     const size_t i = (static_cast<size_t>(k) * n_rx + j) * C + ch;

@@ -191,8 +191,16 @@ __global__ void __launch_bounds__(512, 1)
     float* s_w3 = s_b2 + H;
     float* s_b3 = s_w3 + 4 * C * H;
     float* s_occ = s_b3 + ((4 * C + 3) & ~3);
+    // HT == 64, CT == 1: W2 as output pairs, transposed (local_mlp64_t), after the grid
+    const int occ_floats = R3 ? padded_dim(c.R) * padded_dim(c.R) * padded_dim(c.R) : 0;
+    float2* s_w2t2 = reinterpret_cast<float2*>(s_occ + ((occ_floats + 3) & ~3));
     const float* p = c.p32;
     if (c.use_local) {
+        if (HT == 64 && CT == 1)
+            for (int i = threadIdx.x; i < H * H / 2; i += blockDim.x) {
+                const int ii = i / (H / 2), op = i % (H / 2);
+                s_w2t2[i] = make_float2(p[c.o_lw2 + (2 * op) * H + ii], p[c.o_lw2 + (2 * op + 1) * H + ii]);
+            }
         for (int i = threadIdx.x; i < H * H; i += blockDim.x) s_w2[i] = p[c.o_lw2 + i];
         for (int i = threadIdx.x; i < H * 6; i += blockDim.x) s_w1[i] = p[c.o_lw1 + i];
         for (int i = threadIdx.x; i < H; i += blockDim.x) {
@@ -236,7 +244,10 @@ __global__ void __launch_bounds__(512, 1)
         if (!act) continue;
         if (c.use_local) {
             if (!cubep) local_features<true>(c, s_occ, pk.x, pk.y, pk.z, rxx, rxy, rxz, in);
-            local_mlp<HT, CT>(c, w, in, y);
+            if constexpr (HT == 64 && CT == 1)
+                local_mlp64_t(w, s_w2t2, in, y);
+            else
+                local_mlp<HT, CT>(c, w, in, y);
         } else {
 #pragma unroll
             for (int q = 0; q < YM; ++q) y[q] = 0.f;
@@ -487,7 +498,7 @@ cudaError_t launch_cond_signal(const rxgs_cond_s* c, const rxgs_scene_s& sc,
     const bool fast = d.use_local && d.H == 64 && d.C == 1;
     if (fast) {
         const bool cubep = d.probe && !d.nearest && d.cube != nullptr;
-        const size_t smem_f = cubep ? local_smem_bytes(d, false) : smem;
+        const size_t smem_f = (cubep ? local_smem_bytes(d, false) : smem) + sizeof(float) * (64 * 64 + 4);
         cudaFuncSetAttribute(k_cond_signal<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem_f));
         k_cond_signal<64, 1><<<blocks, threads, smem_f, s>>>(
