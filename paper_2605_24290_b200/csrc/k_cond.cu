@@ -216,17 +216,21 @@ __global__ void __launch_bounds__(512, 1)
 
     const int lane = threadIdx.x & 31;
     const int warps_per_block = blockDim.x >> 5;
-    const int n_jc = (n_rx + 31) >> 5;
-    const long long items = static_cast<long long>(*n_rows) * n_jc;
+    // a warp takes 32 consecutive rows of the (needed Gaussian, receiver)
+    // space, receivers fastest: no idle lanes when n_rx is not a multiple
+    // of 32 (training batches of 16)
+    const long long rows_total = static_cast<long long>(*n_rows) * n_rx;
+    const long long items = (rows_total + 31) >> 5;
     const long long stride = static_cast<long long>(gridDim.x) * warps_per_block;
     const int L = c.L;
     constexpr int YM = CT > 0 ? 4 * CT : 4 * kCMax;
     for (long long it = static_cast<long long>(blockIdx.x) * warps_per_block + (threadIdx.x >> 5);
          it < items; it += stride) {
-        const int vi = static_cast<int>(it / n_jc);
-        const int jc = static_cast<int>(it % n_jc);
-        const int j = jc * 32 + lane;
-        const bool act = j < n_rx;
+        const long long row = it * 32 + lane;
+        const bool act = row < rows_total;
+        const long long rowc = act ? row : rows_total - 1;
+        const int vi = static_cast<int>(rowc / n_rx);
+        const int j = static_cast<int>(rowc - static_cast<long long>(vi) * n_rx);
         const int k = vis[vi];
         const float4 pk = pos32[k];
         const int jr = act ? j : 0;
