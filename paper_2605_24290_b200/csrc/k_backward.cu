@@ -18,7 +18,7 @@ namespace rxgs_b200 {
 namespace {
 
 #ifndef RXGS_BWD_NC
-#define RXGS_BWD_NC 4  // A/B (2, 4, 8) on the joint step: 4
+#define RXGS_BWD_NC 4  // A/B (2, 4, 8) on the joint step: 4 (with the reduce-scatter: 4 = 5.8 ms, 8 = 6.4 ms, 195 registers)
 #endif
 constexpr int kNC = RXGS_BWD_NC;  // (receiver, channel) pairs per walk pass (one receiver chunk)
 
@@ -97,6 +97,47 @@ __global__ void k_signals64(int K, int L, int C, int n_rx, const int* __restrict
             }
         sig[(static_cast<size_t>(k) * n_rx + j) * C + ch] = make_double2(sr, si);
     }
+}
+
+// One halving step of a warp reduce-scatter: lanes with bit `off` clear keep
+// the low half of the N values, the others the high half, each adding its
+// partner's copy of the half it keeps.
+template <int N>
+__device__ __forceinline__ void rs_step(const double (&in)[N], double (&out)[N / 2], int wl, int off) {
+    const bool up = (wl & off) != 0;
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+        const double lo = in[i], hi = in[i + N / 2];
+        out[i] = (up ? hi : lo) + __shfl_xor_sync(0xffffffffu, up ? lo : hi, off);
+    }
+}
+// kV <= 16 values: 8 + 4 + 2 + 1 exchanges, then lanes l and l^1 add (both
+// hold value 8 b4 + 4 b3 + 2 b2 + b1 of their lane index)
+template <int kV>
+__device__ __forceinline__ double reduce_scatter16(const double* v, int wl) {
+    double a[16], b[8], c[4], d[2];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = i < kV ? v[i] : 0.0;
+    rs_step<16>(a, b, wl, 16);
+    rs_step<8>(b, c, wl, 8);
+    rs_step<4>(c, d, wl, 4);
+    const bool up2 = (wl & 2) != 0;
+    double h = (up2 ? d[1] : d[0]) + __shfl_xor_sync(0xffffffffu, up2 ? d[0] : d[1], 2);
+    return h + __shfl_xor_sync(0xffffffffu, h, 1);
+}
+// kV <= 32 values: 16 + 8 + 4 + 2 + 1 exchanges; lane l holds value
+// 16 b4 + 8 b3 + 4 b2 + 2 b1 + b0
+template <int kV>
+__device__ __forceinline__ double reduce_scatter32(const double* v, int wl) {
+    double a[32], b[16], c[8], d[4], e[2];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) a[i] = i < kV ? v[i] : 0.0;
+    rs_step<32>(a, b, wl, 16);
+    rs_step<16>(b, c, wl, 8);
+    rs_step<8>(c, d, wl, 4);
+    rs_step<4>(d, e, wl, 2);
+    const bool up1 = (wl & 1) != 0;
+    return (up1 ? e[1] : e[0]) + __shfl_xor_sync(0xffffffffu, up1 ? e[0] : e[1], 1);
 }
 
 // ------------------------------------------------------------------ per-cell walks
@@ -218,46 +259,18 @@ __global__ void __launch_bounds__(64) k_bwd_walk(DevGrid g, int cb, const int64_
                 v[6] = -d_dp * st;
             }
         }
+        // reduce-scatter of the kV values by recursive halving (VP/2 + ... + 1
+        // exchanges; for VP = 16 a final pair add): lane l ends with the warp sum
+        // of value rs_index(l); fixed order
         if constexpr (kV <= 16) {
-            // reduce-scatter by recursive halving (8 + 4 + 2 + 1 exchanges, then a
-            // final pair add): lane l ends with the warp sum of value
-            // 8 b4 + 4 b3 + 2 b2 + b1 (b_i = bit i of l); fixed order
-            double h8[8];
-            const bool up16 = (wl & 16) != 0;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const double lo = v[i], hi = (i + 8 < kV) ? v[i + 8] : 0.0;
-                const double send = up16 ? lo : hi, keep = up16 ? hi : lo;
-                h8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-            }
-            double h4[4];
-            const bool up8 = (wl & 8) != 0;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const double send = up8 ? h8[i] : h8[i + 4], keep = up8 ? h8[i + 4] : h8[i];
-                h4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-            }
-            double h2[2];
-            const bool up4 = (wl & 4) != 0;
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                const double send = up4 ? h4[i] : h4[i + 2], keep = up4 ? h4[i + 2] : h4[i];
-                h2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-            }
-            const bool up2 = (wl & 2) != 0;
-            double h1 = (up2 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, up2 ? h2[0] : h2[1], 2);
-            h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+            const double h1 = reduce_scatter16<kV>(v, wl);
             const int idx = 8 * ((wl >> 4) & 1) + 4 * ((wl >> 3) & 1) + 2 * ((wl >> 2) & 1) + ((wl >> 1) & 1);
             if ((wl & 1) == 0 && idx < 7 + 2 * nc) ring[warp][p & 31][idx] = h1;
         } else {
-#pragma unroll
-            for (int i = 0; i < kV; ++i) {
-                if (i >= 7 + 2 * nc) break;
-                double x = v[i];
-#pragma unroll
-                for (int off = 16; off >= 1; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-                if (wl == 0) ring[warp][p & 31][i] = x;
-            }
+            const double h1 = reduce_scatter32<kV>(v, wl);
+            const int idx = 16 * ((wl >> 4) & 1) + 8 * ((wl >> 3) & 1) + 4 * ((wl >> 2) & 1) + 2 * ((wl >> 1) & 1) +
+                            (wl & 1);
+            if (idx < 7 + 2 * nc) ring[warp][p & 31][idx] = h1;
         }
         if ((p & 31) == 31 || p == W - 1) {
             __syncthreads();
