@@ -157,6 +157,11 @@ __global__ void __launch_bounds__(64) k_bwd_walk(DevGrid g, int cb, const int64_
     // records 32 positions at a time by all threads (red[0] + red[1], then
     // accumulated: the order of the former per-position flush)
     __shared__ double ring[2][32][kV];
+    // the walk records and this chunk's signals of 64 list positions, staged
+    // cooperatively (every cell of the block reads the same entries)
+    constexpr int kStage = 64;
+    __shared__ GaussRec srec[kStage];
+    __shared__ double2 ssig[kStage][kNC];
     const int tile = blockIdx.x, lane = threadIdx.x;
     // receiver chunk blockIdx.y: its own slice of the per-entry geometry sums
     const int jc0 = blockIdx.y * kNC, nc = n_jc - jc0 < kNC ? n_jc - jc0 : kNC;
@@ -181,30 +186,46 @@ __global__ void __launch_bounds__(64) k_bwd_walk(DevGrid g, int cb, const int64_
             gim[q] = dvals[static_cast<size_t>(jc) * 2 * plane + plane + cell];
         }
     }
-    // pass 1: C_total (forward walk, identical exit)
-    int len = 0;
-    if (valid) {
-        double T = 1.0;
-        for (int p = 0; p < W; ++p) {
-            const int k = list[begin + p];
-            const GaussRec r = rec[k];
-            const double dt = theta_r - r.theta;
-            const double dpraw = wrap_pm_pi(phi_r - r.phi);
-            const double dp = r.sin_theta * dpraw;
-            const double m2 = r.pa * dt * dt + r.pbc * dt * dp + r.pd * dp * dp;
-            double w = r.tau * exp(-0.5 * m2);
-            w = kWeightClamp < w ? kWeightClamp : w;
-            const double tw = T * w;
+    auto stage_chunk = [&](int c0) {  // positions c0 .. c0 + 63 -> srec / ssig
+        __syncthreads();  // the previous chunk has been consumed
+        if (c0 + lane < W) {
+            const int k = list[begin + c0 + lane];
+            srec[lane] = rec[k];
 #pragma unroll
             for (int q = 0; q < kNC; ++q)
-                if (q < nc) {
-                    const double2 s = sig[static_cast<size_t>(k) * n_jc + jc0 + q];
-                    Cr[q] += tw * s.x;
-                    Ci[q] += tw * s.y;
-                }
-            T *= 1.0 - w;
-            len = p + 1;
-            if (T < kEarlyExitT) break;
+                ssig[lane][q] = q < nc ? sig[static_cast<size_t>(k) * n_jc + jc0 + q] : make_double2(0.0, 0.0);
+        }
+        __syncthreads();
+    };
+    // pass 1: C_total (forward walk, identical exit)
+    int len = 0;
+    {
+        double T = 1.0;
+        bool alive = valid;
+        for (int c0 = 0; c0 < W; c0 += kStage) {
+            if (!__syncthreads_or(alive)) break;
+            stage_chunk(c0);
+            const int m = W - c0 < kStage ? W - c0 : kStage;
+            for (int e = 0; e < m && alive; ++e) {
+                const GaussRec& r = srec[e];
+                const double dt = theta_r - r.theta;
+                const double dpraw = wrap_pm_pi(phi_r - r.phi);
+                const double dp = r.sin_theta * dpraw;
+                const double m2 = r.pa * dt * dt + r.pbc * dt * dp + r.pd * dp * dp;
+                double w = r.tau * exp(-0.5 * m2);
+                w = kWeightClamp < w ? kWeightClamp : w;
+                const double tw = T * w;
+#pragma unroll
+                for (int q = 0; q < kNC; ++q)
+                    if (q < nc) {
+                        const double2 sv = ssig[e][q];
+                        Cr[q] += tw * sv.x;
+                        Ci[q] += tw * sv.y;
+                    }
+                T *= 1.0 - w;
+                len = c0 + e + 1;
+                if (T < kEarlyExitT) alive = false;
+            }
         }
     }
     // pass 2: per-entry adjoints with suffix = C_total - C_upto(p), reduced
@@ -214,13 +235,16 @@ __global__ void __launch_bounds__(64) k_bwd_walk(DevGrid g, int cb, const int64_
 #pragma unroll
     for (int q = 0; q < kNC; ++q) Ur[q] = Ui[q] = 0.0;
     const int warp = lane >> 5, wl = lane & 31;
-    for (int p = 0; p < W; ++p) {
+    for (int c0 = 0; c0 < W; c0 += kStage) {
+    stage_chunk(c0);
+    const int m_ch = W - c0 < kStage ? W - c0 : kStage;
+    for (int e = 0; e < m_ch; ++e) {
+        const int p = c0 + e;
         double v[7 + 2 * kNC];
 #pragma unroll
         for (int i = 0; i < 7 + 2 * kNC; ++i) v[i] = 0.0;
-        const int k = list[begin + p];
         if (p < len) {
-            const GaussRec r = rec[k];
+            const GaussRec& r = srec[e];
             const double dt = theta_r - r.theta;
             const double dpraw = wrap_pm_pi(phi_r - r.phi);
             const double dp = r.sin_theta * dpraw;
@@ -235,7 +259,7 @@ __global__ void __launch_bounds__(64) k_bwd_walk(DevGrid g, int cb, const int64_
 #pragma unroll
             for (int q = 0; q < kNC; ++q)
                 if (q < nc) {
-                    const double2 s = sig[static_cast<size_t>(k) * n_jc + jc0 + q];
+                    const double2 s = ssig[e][q];
                     v[7 + 2 * q] = gre[q] * t_prev * w;
                     v[8 + 2 * q] = gim[q] * t_prev * w;
                     Ur[q] += t_prev * w * s.x;
@@ -285,6 +309,7 @@ __global__ void __launch_bounds__(64) k_bwd_walk(DevGrid g, int cb, const int64_
             }
             __syncthreads();
         }
+    }
     }
 }
 
