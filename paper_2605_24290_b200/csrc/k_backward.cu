@@ -314,23 +314,32 @@ __global__ void __launch_bounds__(64) k_bwd_walk(DevGrid g, int cb, const int64_
 }
 
 // per-Gaussian sums of the walked entries, in tile order
+// One thread per (Gaussian, output value): the 7 geometry terms (receiver
+// chunks summed in order per entry) and the n_jc signal adjoints, each summed
+// over the Gaussian's entries in tile order -- the same per-value order as one
+// thread per Gaussian, with 7 + n_jc times the parallelism for the gathers.
 __global__ void k_bwd_gauss_reduce(int K, int n_jc, int n_chunks, int64_t n_ent, const int* __restrict__ goff,
                                    const int* __restrict__ gent, const double* __restrict__ ent_geo,
                                    const double2* __restrict__ ent_ds, double* __restrict__ raw_geo,
                                    double2* __restrict__ raw_ds) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= K) return;
-    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
-    for (int e = goff[k]; e < goff[k + 1]; ++e)
-        for (int i = 0; i < 7; ++i) {
-            double v = ent_geo[static_cast<size_t>(gent[e]) * 7 + i];  // receiver chunks in order
-            for (int ch = 1; ch < n_chunks; ++ch) v += ent_geo[(static_cast<size_t>(ch) * n_ent + gent[e]) * 7 + i];
-            acc[i] += v;
+    const int nv = 7 + n_jc;
+    const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (t >= static_cast<long long>(K) * nv) return;
+    const int k = static_cast<int>(t / nv), i = static_cast<int>(t - static_cast<long long>(k) * nv);
+    const int e0 = goff[k], e1 = goff[k + 1];
+    if (i < 7) {
+        double acc = 0.0;
+        for (int e = e0; e < e1; ++e) {
+            const int ge = gent[e];
+            double v = ent_geo[static_cast<size_t>(ge) * 7 + i];  // receiver chunks in order
+            for (int ch = 1; ch < n_chunks; ++ch) v += ent_geo[(static_cast<size_t>(ch) * n_ent + ge) * 7 + i];
+            acc += v;
         }
-    for (int i = 0; i < 7; ++i) raw_geo[static_cast<size_t>(k) * 7 + i] = acc[i];
-    for (int q = 0; q < n_jc; ++q) {
+        raw_geo[static_cast<size_t>(k) * 7 + i] = acc;
+    } else {
+        const int q = i - 7;
         double2 a = make_double2(0.0, 0.0);
-        for (int e = goff[k]; e < goff[k + 1]; ++e) {
+        for (int e = e0; e < e1; ++e) {
             const double2 v = ent_ds[static_cast<size_t>(gent[e]) * n_jc + q];
             a.x += v.x;
             a.y += v.y;
@@ -564,7 +573,9 @@ cudaError_t launch_backward_render(const rxgs_txstate_s& st, const rxgs_scene_s&
                                                                  st.entries, ent_geo, ent_ds);
     }
     if (K > 0) {
-        k_bwd_gauss_reduce<<<(K + 127) / 128, 128, 0, s>>>(K, n_jc, n_chunks, st.entries, st.gauss_off.as<int>(),
+        const long long nt = static_cast<long long>(K) * (7 + n_jc);
+        k_bwd_gauss_reduce<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, s>>>(K, n_jc, n_chunks, st.entries,
+                                                                                  st.gauss_off.as<int>(),
                                                           st.gauss_ent.as<int>(), ent_geo, ent_ds, raw_geo, raw_ds);
         k_bwd_finalize<<<(K + 63) / 64, 64, 0, s>>>(K, st.l_max, C, n_rx, st.culled.as<int>(), st.geom.as<double>(),
                                                     st.basis64.as<double>(), d_coeffs_in, raw_geo, raw_ds,
