@@ -13,4 +13,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 for k in k_cond_bwd_tc k_cond_grads_tc k_composite_T; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -c 1 -o gpurun_out/${TAG}_$k -f python scripts/probe_joint.py stage2l1 > /dev/null 2>&1
 done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_bwd_walk -c 1 -o gpurun_out/${TAG}_k_bwd_walk -f python scripts/probe_joint.py > /dev/null 2>&1
 ls gpurun_out/${TAG}_*train* gpurun_out/${TAG}_*joint* gpurun_out/${TAG}_k_c*

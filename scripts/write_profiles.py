@@ -50,7 +50,7 @@ if os.path.exists(rep):
 
 for k in ["k_cond_tc", "k_fle_gemm", "k_composite_tc", "k_walk", "k_tx_prep", "k_cov_signal", "k_tile_scatter",
           "k_emit_entries", "k_radix_scatter", "k_cond_bwd_rows", "k_cond_bwd_grads", "k_cond_bwd_tc",
-          "k_cond_grads_tc", "k_composite_T"]:
+          "k_cond_grads_tc", "k_composite_T", "k_bwd_walk"]:
     rep = os.path.join(out, f"{tag}_{k}.ncu-rep")
     if not os.path.exists(rep):
         continue
