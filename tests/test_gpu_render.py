@@ -194,6 +194,33 @@ def test_render_queries_high_lmax_fle_gemm(ctx, capi, orc, l_max, n_rx):
         assert rel_err(rssi[j], wr) < TOL
 
 
+@pytest.mark.parametrize("l_max,mode", [(0, "full"), (1, "full"), (2, "global_only"), (2, "local_only")])
+def test_render_queries_host_chunks_equal_device_batch(ctx, capi, orc, l_max, mode):
+    """Host-output render of >= 256 receivers runs in receiver chunks with
+    the global branch and (tensor-core path, l_max >= 1) the FLE GEMM
+    computed once for the whole batch: spectra and RSSI identical, bit for
+    bit, to the one-chunk device-resident render; spot-checked against the
+    oracle."""
+    import torch
+    import oracle as O
+    sc = capi.synth_scene(3000, l_max, 1, 7)
+    scene, cond, oscene, ocond = _setup_cond(capi, ctx, orc, sc, mode=mode)
+    grid, og = capi.Grid(30, 60, 8, 1.0), O.Grid(30, 60, 8, 1.0)
+    n_rx = 300
+    rx = capi.synth_points(n_rx, 11, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
+    st = scene.tx_state(TX, grid)
+    spec, rssi = scene.render_queries(cond, st, rx)
+    dev = torch.device("cuda", 0)
+    sd = torch.empty((n_rx, 30, 60), dtype=torch.float32, device=dev)
+    rd = torch.empty(n_rx, dtype=torch.float32, device=dev)
+    scene.render_queries(cond, st, torch.from_numpy(rx).to(dev), sd, rd)
+    torch.cuda.synchronize()
+    assert np.array_equal(sd.cpu().numpy(), spec) and np.array_equal(rd.cpu().numpy(), rssi)
+    for j in (0, n_rx // 2, n_rx - 1):
+        want = orc.predict(oscene, ocond, og, TX, rx[j], "spectrum").reshape(30, 60)
+        assert rel_err(spec[j], want).max() <= TOL
+
+
 def test_render_queries_unconditioned_and_batch_invariance(ctx, capi, orc):
     import oracle as O
     sc = capi.synth_scene(3000, 2, 1, 8)
