@@ -55,7 +55,13 @@ constexpr int kCovThreads = 256;
 // LT > 0: L == LT, the receiver's (alpha_G, beta_G) held in registers;
 // LT == 0 (other l_max): re-read per row from the transposed cache.
 template <int LT>
-__global__ void __launch_bounds__(kCovThreads, 2) k_cov_signal(CondDev c, const int* __restrict__ n_rows,
+#ifndef RXGS_COV_MINB
+#define RXGS_COV_MINB 3  // A/B (config 3, cov_signal phase per table): 2 CTAs + 4 ahead 43.7 ms, 3 CTAs + 8 ahead 36.1 ms
+#endif
+#ifndef RXGS_COV_AHEAD
+#define RXGS_COV_AHEAD 8
+#endif
+__global__ void __launch_bounds__(kCovThreads, RXGS_COV_MINB) k_cov_signal(CondDev c, const int* __restrict__ n_rows,
                                                             const int* __restrict__ rows, int n_rx, int L,
                                                             const float2* __restrict__ B, const float2* __restrict__ GB,
                                                             const float4* __restrict__ agT,
@@ -107,7 +113,7 @@ __global__ void __launch_bounds__(kCovThreads, 2) k_cov_signal(CondDev c, const 
     float4 areg[LT > 0 ? LT : 1];
 #pragma unroll
     for (int l = 0; l < LT; ++l) areg[l] = s_a[l * kCovThreads + tid];
-    constexpr int kAhead = 4;  // y-cache rows in flight per thread
+    constexpr int kAhead = RXGS_COV_AHEAD;  // y-cache rows in flight per thread
     float4 yq[kAhead];
 #pragma unroll
     for (int q = 0; q < kAhead; ++q) yq[q] = load_y(q);
