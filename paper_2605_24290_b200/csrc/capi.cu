@@ -12,6 +12,9 @@
 #include <exception>
 #include <new>
 #include <string>
+#include <thread>
+#include <mutex>
+#include <condition_variable>
 #include <memory>
 #include <vector>
 
@@ -369,11 +372,13 @@ static void ctx_free(rxgs_ctx ctx) {
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
     for (auto* t : ctx->spare_tx) delete t;
     for (auto e : ctx->chunk_events) cudaEventDestroy(e);
-    if (ctx->aux_ev) cudaEventDestroy(ctx->aux_ev);
-    if (ctx->aux_done) cudaEventDestroy(ctx->aux_done);
-    if (ctx->aux) {
-        ctx->aux->closed = true;
-        if (ctx->aux->refs == 0) ctx_free(ctx->aux);
+    for (int i = 0; i < rxgs_ctx_s::kAuxMax; ++i) {
+        if (ctx->aux_ev[i]) cudaEventDestroy(ctx->aux_ev[i]);
+        if (ctx->aux_done[i]) cudaEventDestroy(ctx->aux_done[i]);
+        if (ctx->aux[i]) {
+            ctx->aux[i]->closed = true;
+            if (ctx->aux[i]->refs == 0) ctx_free(ctx->aux[i]);
+        }
     }
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
@@ -1512,35 +1517,10 @@ int rxgs_coverage_table(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const rxgs_gri
         yc = ctx->ycache.as<float4>();
     }
     RXGS_CUDA(ctx->signals.ensure(std::max<size_t>(static_cast<size_t>(sc->k) * ((n_rx + 3) & ~3), 1) * sizeof(float2)));
-    // transmitter states are built one ahead on the helper context, so the
-    // next state's projection / sort / walk overlap this one's signals and
-    // compositing (the builder's host syncs block only its own stream)
-#ifndef RXGS_COV_PIPE
-#define RXGS_COV_PIPE 1
-#endif
-    rxgs_ctx bctx = ctx;
-    if (RXGS_COV_PIPE && n_tx > 1) {
-        if (!ctx->aux) {
-            RX_TRY(rxgs_ctx_create(ctx->device, &ctx->aux));
-            RXGS_CUDA(cudaEventCreateWithFlags(&ctx->aux_ev, cudaEventDisableTiming));
-            RXGS_CUDA(cudaEventCreateWithFlags(&ctx->aux_done, cudaEventDisableTiming));
-        }
-        bctx = ctx->aux;
-        bctx->profile = ctx->profile;
-    }
-    const int64_t aux_launches0 = bctx->launches;
-    rxgs_txstate st_next = nullptr;
-    RX_TRY(rxgs_tx_state_build(bctx, sc, txh.data(), grid, &st_next));
-    for (int t = 0; t < n_tx; ++t) {
-        rxgs_txstate st = st_next;
-        st_next = nullptr;
-        if (bctx != ctx) {  // this stream's work on st after the builder's
-            RXGS_CUDA(cudaEventRecord(ctx->aux_ev, bctx->stream));
-            RXGS_CUDA(cudaStreamWaitEvent(s, ctx->aux_ev, 0));
-        }
+    // Render of one transmitter state (this context's stream)
+    auto render_tx = [&](int t, rxgs_txstate st) -> int {
         const DevGrid& g = st->grid;
         const int n_tb = g.n_tiles * g.cell_blocks;
-        int rc = RXGS_OK;
         bool tc_comp = false;
         cudaError_t e = ctx->partial.ensure(std::max<size_t>(static_cast<size_t>(n_tb) * n_rx, 1) * sizeof(float));
         if (e == cudaSuccess) {
@@ -1554,7 +1534,7 @@ int rxgs_coverage_table(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const rxgs_gri
                                            s);
             else
                 e = launch_cov_signal(c, *st, n_rx, t_agT.as<float>(), yc,
-                                  tc_comp ? SigOut::presplit(ctx->signals.p) : SigOut(ctx->signals.as<float2>()), s);
+                                      tc_comp ? SigOut::presplit(ctx->signals.p) : SigOut(ctx->signals.as<float2>()), s);
             timing_end(ctx, "cov_signal", ev,
                        static_cast<double>(st->needed_host >= 0 ? st->needed_host : st->visible) * n_rx);
         }
@@ -1570,31 +1550,122 @@ int rxgs_coverage_table(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const rxgs_gri
             e = launch_rssi_finalize(ctx->partial.as<float>(), n_tb, n_rx, d_out + static_cast<size_t>(t) * n_rx,
                                      nullptr, s);
         ctx->launches += 3;
-        if (e != cudaSuccess) rc = cuda_fail(e, "coverage_table");
-        if (!rc && t + 1 < n_tx)
-            rc = rxgs_tx_state_build(bctx, sc, txh.data() + 3 * static_cast<size_t>(t + 1), grid, &st_next);
-        if (bctx != ctx) {  // st's buffers return to the builder's pool: wait for this stream's use
-            cudaEventRecord(ctx->aux_done, s);
-            cudaEventSynchronize(ctx->aux_done);
+        return e == cudaSuccess ? RXGS_OK : cuda_fail(e, "coverage_table");
+    };
+    // Transmitter states are built by D builder threads, each on its own
+    // helper context (stream, scratch, buffer pool): builder i builds the
+    // states t = i, i + D, ... while this thread renders.  A build is a chain
+    // of short kernels with host syncs (entry counts), latency- rather than
+    // throughput-bound, so D builders in flight keep the render stream fed.
+    // Stream order: the render of t waits on the builder's event; builder i
+    // recycles state t's buffers for t + D only after the render of t is
+    // done on the device.
+#ifndef RXGS_COV_BUILDERS
+#define RXGS_COV_BUILDERS 4  // A/B (config 3, ms per table): serial 128.3, D=1 129.1, 2 116.5, 3 113.4, 4 110.8
+#endif
+    int D = std::min(RXGS_COV_BUILDERS, rxgs_ctx_s::kAuxMax);
+    if (const char* v = std::getenv("RXGS_COV_BUILDERS")) D = std::max(0, std::min(std::atoi(v), rxgs_ctx_s::kAuxMax));
+    if (n_tx < 2) D = 0;
+    D = std::min(D, n_tx);
+    if (D == 0) {  // one transmitter: build and render in turn on this context
+        for (int t = 0; t < n_tx; ++t) {
+            rxgs_txstate st = nullptr;
+            RX_TRY(rxgs_tx_state_build(ctx, sc, txh.data() + 3 * static_cast<size_t>(t), grid, &st));
+            const int rc = render_tx(t, st);
+            rxgs_tx_state_destroy(st);
+            if (rc) return rc;
         }
-        rxgs_tx_state_destroy(st);
-        if (rc) {
-            if (st_next) rxgs_tx_state_destroy(st_next);
-            return rc;
-        }
-    }
-    if (bctx != ctx) {  // the builder's launches and phase timings count for this context
-        ctx->launches += bctx->launches - aux_launches0;
-        if (ctx->profile) {
-            resolve_timings(bctx);
-            for (const auto& kv : bctx->stats) {
-                KStat& d = ctx->stats[kv.first];
-                d.ms += kv.second.ms;
-                d.launches += kv.second.launches;
-                d.work += kv.second.work;
+    } else {
+        int64_t launches0[rxgs_ctx_s::kAuxMax];
+        for (int i = 0; i < D; ++i) {
+            if (!ctx->aux[i]) {
+                RX_TRY(rxgs_ctx_create(ctx->device, &ctx->aux[i]));
+                RXGS_CUDA(cudaEventCreateWithFlags(&ctx->aux_ev[i], cudaEventDisableTiming));
+                RXGS_CUDA(cudaEventCreateWithFlags(&ctx->aux_done[i], cudaEventDisableTiming));
             }
-            bctx->stats.clear();
+            ctx->aux[i]->profile = ctx->profile;
+            launches0[i] = ctx->aux[i]->launches;
         }
+        std::mutex mu;
+        std::condition_variable cv;
+        std::vector<rxgs_txstate> states(n_tx, nullptr);
+        std::vector<signed char> built(n_tx, 0);  // 1 built, -1 failed
+        std::vector<char> issued(n_tx, 0), dead(n_tx, 0);
+        bool abort = false;
+        int b_rc = RXGS_OK;
+        std::string b_err;
+        auto builder = [&](int i) {
+            rxgs_ctx b = ctx->aux[i];
+            cudaSetDevice(b->device);
+            for (int t = i; t < n_tx; t += D) {
+                if (t >= D) {  // state t - D: recycle once its render is done on the device
+                    {
+                        std::unique_lock<std::mutex> lk(mu);
+                        cv.wait(lk, [&] { return issued[t - D] || abort; });
+                        if (abort) return;
+                    }
+                    cudaEventSynchronize(ctx->aux_done[i]);
+                    rxgs_tx_state_destroy(states[t - D]);
+                    std::lock_guard<std::mutex> lk(mu);
+                    dead[t - D] = 1;
+                }
+                rxgs_txstate st = nullptr;
+                int rc = rxgs_tx_state_build(b, sc, txh.data() + 3 * static_cast<size_t>(t), grid, &st);
+                if (!rc) {
+                    const cudaError_t e = cudaEventRecord(ctx->aux_ev[i], b->stream);
+                    if (e != cudaSuccess) rc = cuda_fail(e, "coverage_table builder");
+                }
+                std::lock_guard<std::mutex> lk(mu);
+                states[t] = st;
+                built[t] = rc ? -1 : 1;
+                if (rc && !b_rc) {
+                    b_rc = rc;
+                    b_err = rxgs_last_error();
+                }
+                cv.notify_all();
+                if (rc) return;
+            }
+        };
+        std::vector<std::thread> workers;
+        for (int i = 0; i < D; ++i) workers.emplace_back(builder, i);
+        int rc = RXGS_OK;
+        for (int t = 0; t < n_tx && !rc; ++t) {
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return built[t] != 0; });
+                if (built[t] < 0) {
+                    rc = fail(b_rc, b_err);
+                    break;
+                }
+            }
+            const int i = t % D;
+            cudaError_t e = cudaStreamWaitEvent(s, ctx->aux_ev[i], 0);
+            rc = e == cudaSuccess ? render_tx(t, states[t]) : cuda_fail(e, "coverage_table");
+            if (!rc && (e = cudaEventRecord(ctx->aux_done[i], s)) != cudaSuccess) rc = cuda_fail(e, "coverage_table");
+            std::lock_guard<std::mutex> lk(mu);
+            if (rc) abort = true;
+            else issued[t] = 1;
+            cv.notify_all();
+        }
+        for (auto& w : workers) w.join();
+        cudaStreamSynchronize(s);  // the states still alive: no reader left
+        for (int t = 0; t < n_tx; ++t)
+            if (states[t] && !dead[t]) rxgs_tx_state_destroy(states[t]);
+        for (int i = 0; i < D; ++i) {  // the builders' launches and phase timings count for this context
+            rxgs_ctx b = ctx->aux[i];
+            ctx->launches += b->launches - launches0[i];
+            if (ctx->profile) {
+                resolve_timings(b);
+                for (const auto& kv : b->stats) {
+                    KStat& d = ctx->stats[kv.first];
+                    d.ms += kv.second.ms;
+                    d.launches += kv.second.launches;
+                    d.work += kv.second.work;
+                }
+                b->stats.clear();
+            }
+        }
+        if (rc) return rc;
     }
     if (c) {
         if (c->use_global()) c->global_calls += static_cast<int64_t>(n_rx) * sc->L;

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <map>
 #include <string>
@@ -155,15 +156,16 @@ struct rxgs_ctx_s {
     int sm_count = 148;
     int cond_kernel = 0;  // 0 auto (tcgen05 when eligible), 1 force SIMT
     int composite_kernel = 0;  // 0 auto (tcgen05 when eligible), 1 force SIMT
-    int refs = 0;         // live handles on this context
+    std::atomic<int> refs{0};  // live handles on this context (builder threads retain / release)
     cudaStream_t copy_stream = nullptr;  // D2H of finished receiver chunks (host outputs)
     std::vector<cudaEvent_t> chunk_events;
     bool closed = false;  // rxgs_ctx_destroy called while handles were alive
     // helper context (own stream and scratch) that builds the next
     // transmitter's state while this one's stream renders the current one
     // (rxgs_coverage_table); created on first use
-    rxgs_ctx_s* aux = nullptr;
-    cudaEvent_t aux_ev = nullptr, aux_done = nullptr;
+    static constexpr int kAuxMax = 4;
+    rxgs_ctx_s* aux[kAuxMax] = {};
+    cudaEvent_t aux_ev[kAuxMax] = {}, aux_done[kAuxMax] = {};
 };
 
 struct rxgs_scene_s {
@@ -182,7 +184,7 @@ struct rxgs_scene_s {
     uint64_t coeff_version = 1, geo_version = 1;
     // transmitter states built from this scene keep it alive (lean states are
     // completed from it on demand); rxgs_scene_destroy drops the caller's ref
-    int refs = 1;
+    std::atomic<int> refs{1};
     // exact position -> lowest Gaussian index (receiver-on-Gaussian check,
     // conditioning.cpp:380-382), built lazily on the host
     std::unordered_map<std::string, int> pos_index;
