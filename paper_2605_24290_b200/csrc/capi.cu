@@ -7,6 +7,7 @@
 #include <atomic>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
@@ -1561,7 +1562,8 @@ int rxgs_coverage_table(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const rxgs_gri
     // recycles state t's buffers for t + D only after the render of t is
     // done on the device.
 #ifndef RXGS_COV_BUILDERS
-#define RXGS_COV_BUILDERS 4  // A/B (config 3, ms per table): serial 128.3, D=1 129.1, 2 116.5, 3 113.4, 4 110.8
+#define RXGS_COV_BUILDERS 4  // A/B (config 3, ms per table): serial 128.3, D=1 129.1, 2 116.5, 3 113.4, 4 110.8;
+                             // 6 / 8 and high-priority builder streams within noise (109-112)
 #endif
     int D = std::min(RXGS_COV_BUILDERS, rxgs_ctx_s::kAuxMax);
     if (const char* v = std::getenv("RXGS_COV_BUILDERS")) D = std::max(0, std::min(std::atoi(v), rxgs_ctx_s::kAuxMax));
@@ -1594,6 +1596,11 @@ int rxgs_coverage_table(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const rxgs_gri
         bool abort = false;
         int b_rc = RXGS_OK;
         std::string b_err;
+        // RXGS_COV_TRACE=1: per-transmitter build / render timeline on stderr (diagnostics)
+        const bool trace = std::getenv("RXGS_COV_TRACE") != nullptr;
+        std::vector<cudaEvent_t> tev(trace ? 4 * static_cast<size_t>(n_tx) + 1 : 0);
+        for (auto& e : tev) cudaEventCreate(&e);
+        if (trace) cudaEventRecord(tev[4 * n_tx], s);
         auto builder = [&](int i) {
             rxgs_ctx b = ctx->aux[i];
             cudaSetDevice(b->device);
@@ -1610,7 +1617,9 @@ int rxgs_coverage_table(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const rxgs_gri
                     dead[t - D] = 1;
                 }
                 rxgs_txstate st = nullptr;
+                if (trace) cudaEventRecord(tev[4 * t], b->stream);
                 int rc = rxgs_tx_state_build(b, sc, txh.data() + 3 * static_cast<size_t>(t), grid, &st);
+                if (trace) cudaEventRecord(tev[4 * t + 1], b->stream);
                 if (!rc) {
                     const cudaError_t e = cudaEventRecord(ctx->aux_ev[i], b->stream);
                     if (e != cudaSuccess) rc = cuda_fail(e, "coverage_table builder");
@@ -1640,7 +1649,9 @@ int rxgs_coverage_table(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const rxgs_gri
             }
             const int i = t % D;
             cudaError_t e = cudaStreamWaitEvent(s, ctx->aux_ev[i], 0);
+            if (trace) cudaEventRecord(tev[4 * t + 2], s);
             rc = e == cudaSuccess ? render_tx(t, states[t]) : cuda_fail(e, "coverage_table");
+            if (trace) cudaEventRecord(tev[4 * t + 3], s);
             if (!rc && (e = cudaEventRecord(ctx->aux_done[i], s)) != cudaSuccess) rc = cuda_fail(e, "coverage_table");
             std::lock_guard<std::mutex> lk(mu);
             if (rc) abort = true;
@@ -1649,6 +1660,22 @@ int rxgs_coverage_table(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const rxgs_gri
         }
         for (auto& w : workers) w.join();
         cudaStreamSynchronize(s);  // the states still alive: no reader left
+        if (trace) {
+            cudaDeviceSynchronize();
+            double busy = 0, wait_build = 0, prev_end = 0;
+            for (int t = 0; t < n_tx; ++t) {
+                float v[4];
+                for (int q = 0; q < 4; ++q) cudaEventElapsedTime(&v[q], tev[4 * n_tx], tev[4 * t + q]);
+                busy += v[3] - v[2];
+                if (t > 0) wait_build += std::max(0.0, static_cast<double>(v[2]) - prev_end);
+                prev_end = v[3];
+                std::fprintf(stderr, "tx %2d build %8.3f %8.3f (%.3f)  render %8.3f %8.3f (%.3f)\n", t, v[0], v[1],
+                             v[1] - v[0], v[2], v[3], v[3] - v[2]);
+            }
+            std::fprintf(stderr, "render busy %.3f ms, gaps between renders %.3f ms, end %.3f ms\n", busy,
+                         wait_build, prev_end);
+            for (auto& e : tev) cudaEventDestroy(e);
+        }
         for (int t = 0; t < n_tx; ++t)
             if (states[t] && !dead[t]) rxgs_tx_state_destroy(states[t]);
         for (int i = 0; i < D; ++i) {  // the builders' launches and phase timings count for this context

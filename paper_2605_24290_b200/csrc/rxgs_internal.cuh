@@ -163,7 +163,7 @@ struct rxgs_ctx_s {
     // helper context (own stream and scratch) that builds the next
     // transmitter's state while this one's stream renders the current one
     // (rxgs_coverage_table); created on first use
-    static constexpr int kAuxMax = 4;
+    static constexpr int kAuxMax = 8;
     rxgs_ctx_s* aux[kAuxMax] = {};
     cudaEvent_t aux_ev[kAuxMax] = {}, aux_done[kAuxMax] = {};
 };
