@@ -32,8 +32,11 @@ namespace {
 #define RXGS_WALK_CHUNK 128  // A/B: 128 > 64 > 32 (config-3 walk 17.5 / 18.6 / 21.1 ms)
 #endif
 [[maybe_unused]] constexpr int kChunk = RXGS_WALK_CHUNK;
-constexpr int kWalkThreads = 512;
-constexpr int kLanesPerCell = kWalkThreads / kMaxCellsPerBlock;  // 4
+#ifndef RXGS_WALK_THREADS
+#define RXGS_WALK_THREADS 384  // A/B (walk ms, config 2 / config 5): 512: 0.118 / 0.377, 384: 0.114 / 0.336, 256: 0.131 / 0.357
+#endif
+constexpr int kWalkThreads = RXGS_WALK_THREADS;
+constexpr int kLanesPerCell = kWalkThreads / kMaxCellsPerBlock;
 
 __device__ __forceinline__ double wrap_pm_pi(double a) {  // linalg.hpp:152-157
     // fmod(a, 2 pi) is exact and returns a itself when |a| < 2 pi -- always
@@ -143,8 +146,11 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(DevGrid g, const int64_t*
 // exited by the end of chunk c-1 (a cell exiting during chunk c costs at
 // most one chunk of unneeded weights).  Same arithmetic, same order: the
 // output is identical to the two-phase kernel.
-constexpr int kPipeChunk = 64;
-constexpr int kProducers = kWalkThreads - kMaxCellsPerBlock;  // 448
+#ifndef RXGS_WALK_PCHUNK
+#define RXGS_WALK_PCHUNK 64
+#endif
+constexpr int kPipeChunk = RXGS_WALK_PCHUNK;
+constexpr int kProducers = kWalkThreads - kMaxCellsPerBlock;  // 320
 
 __global__ void __launch_bounds__(kWalkThreads) k_walk_pipe(DevGrid g, const int64_t* __restrict__ tile_offsets,
                                                             const int* __restrict__ list,
