@@ -1636,8 +1636,20 @@ int rxgs_coverage_table(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const rxgs_gri
             }
         };
         std::vector<std::thread> workers;
-        for (int i = 0; i < D; ++i) workers.emplace_back(builder, i);
         int rc = RXGS_OK;
+        try {
+            for (int i = 0; i < D; ++i) workers.emplace_back(builder, i);
+        } catch (const std::exception& ex) {  // no thread left joinable on the way out
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                abort = true;
+                cv.notify_all();
+            }
+            for (auto& w : workers) w.join();
+            for (int t = 0; t < n_tx; ++t)
+                if (states[t]) rxgs_tx_state_destroy(states[t]);
+            return fail(RXGS_ERR_CUDA, std::string("coverage_table: builder thread: ") + ex.what());
+        }
         for (int t = 0; t < n_tx && !rc; ++t) {
             {
                 std::unique_lock<std::mutex> lk(mu);
@@ -1656,6 +1668,11 @@ int rxgs_coverage_table(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const rxgs_gri
             std::lock_guard<std::mutex> lk(mu);
             if (rc) abort = true;
             else issued[t] = 1;
+            cv.notify_all();
+        }
+        {  // a failed build or render: builders waiting for a render that will not come stop
+            std::lock_guard<std::mutex> lk(mu);
+            if (rc) abort = true;
             cv.notify_all();
         }
         for (auto& w : workers) w.join();
