@@ -375,8 +375,27 @@ def run_b200(args):
     traffic = None
     tpath = next((os.path.join(ROOT, "profiles", f"{t}_traffic.json") for t in ("r2", "r1")
                   if os.path.exists(os.path.join(ROOT, "profiles", f"{t}_traffic.json"))), "")
+    ncu_pipes = None
     if os.path.exists(tpath):  # dram bytes of the same kernel from the committed ncu --set full capture
-        traffic = json.load(open(tpath)).get("k_cond_tc", {}).get("dram_bytes_per_launch")
+        tj = json.load(open(tpath))
+        traffic = tj.get("k_cond_tc", {}).get("dram_bytes_per_launch")
+        # ncu pipe evidence of the config-2 kernels (same capture): FP32 / tensor pipe
+        # and issue utilisation, achieved DRAM GB/s and its fraction of the measured HBM peak
+        hbm = 6548.2
+        if os.path.exists(peaks_path):
+            hbm = float(json.load(open(peaks_path)).get("hbm_gbs", hbm))
+        ncu_pipes = {}
+        for kn in ("k_cond_tc", "k_fle_gemm", "k_composite_tc", "k_walk"):
+            r = tj.get(kn)
+            if not r or r.get("fp32_pipe_pct") is None:
+                continue
+            ncu_pipes[kn] = {"fp32_pipe_pct": round(r["fp32_pipe_pct"], 1),
+                             "tensor_pipe_pct": round(r["tensor_pipe_pct"], 1),
+                             "fp64_pipe_pct": round(r["fp64_pipe_pct"], 1),
+                             "issue_active_pct": round(r["issue_active_pct"], 1),
+                             "dram_gbps": round(r["dram_gbps"], 1),
+                             "hbm_frac": round(r["dram_gbps"] / hbm, 3)}
+        ncu_pipes = ncu_pipes or None
     if cond_n:
         per_launch_rows = cond_rows / cond_n
         avg_ms = cond_ms / cond_n
@@ -391,7 +410,10 @@ def run_b200(args):
                     "flop_per_row": flop_row, "rows_per_launch": per_launch_rows,
                     "kernel_ms": avg_ms,
                     "share_of_step": (cond_ms / cond_n) / ms_local,
-                    "composite_ms": comp_ms / max(comp_n, 1), "walk_ms": walk_ms / max(comp_n, 1)}
+                    "composite_ms": comp_ms / max(comp_n, 1), "walk_ms": walk_ms / max(comp_n, 1),
+                    "ncu_pipes": ncu_pipes,
+                    "ncu_pipes_source": f"{os.path.relpath(tpath, ROOT) if tpath else 'no capture'} "
+                                        "(ncu --set full, one launch each, cold cache)"}
 
     train = None if args.no_train else bench_train(args, capi, ctx, scene, cond, grid, stream, dev, rank, world)
     del scene, cond

@@ -68,7 +68,15 @@ for k in ["k_cond_tc", "k_fle_gemm", "k_composite_tc", "k_walk", "k_tx_prep", "k
         return float(v[i].replace(",", "")) * scale.get(u[i], 1.0)
 
     rd, wr = get("dram__bytes_read.sum"), get("dram__bytes_write.sum")
+    dur = get("gpu__time_duration.sum")
     traffic[k] = {"dram_bytes_per_launch": (rd + wr) if rd is not None else None,
-                  "duration_us": get("gpu__time_duration.sum")}
+                  "duration_us": dur,
+                  # pipe evidence of the same launch (percent of peak sustained, active cycles)
+                  "dram_gbps": (rd + wr) / (dur * 1e3) if rd is not None and dur else None,
+                  "fp32_pipe_pct": get("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+                  "fp32_inst_pct": get("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+                  "tensor_pipe_pct": get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
+                  "fp64_pipe_pct": get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                  "issue_active_pct": get("smsp__issue_active.avg.pct_of_peak_sustained_active")}
 json.dump(traffic, open(os.path.join(prof, f"{tag}_traffic.json"), "w"), indent=1)
 print(json.dumps(traffic, indent=1))
