@@ -1681,7 +1681,7 @@ int rxgs_coverage_table(rxgs_ctx ctx, rxgs_scene sc, rxgs_cond c, const rxgs_gri
             cudaDeviceSynchronize();
             double busy = 0, wait_build = 0, prev_end = 0;
             for (int t = 0; t < n_tx; ++t) {
-                float v[4];
+                float v[4] = {0.f, 0.f, 0.f, 0.f};  // stays 0 for a transmitter never reached (failed table)
                 for (int q = 0; q < 4; ++q) cudaEventElapsedTime(&v[q], tev[4 * n_tx], tev[4 * t + q]);
                 busy += v[3] - v[2];
                 if (t > 0) wait_build += std::max(0.0, static_cast<double>(v[2]) - prev_end);
