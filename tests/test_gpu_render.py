@@ -338,3 +338,29 @@ def test_coverage_table_matches_oracle_predict(ctx, capi, orc, mode, hidden, l_m
     st = scene.tx_state(tx[1], grid)
     _, r = scene.render_queries(cond, st, rx, want=("rssi",))
     assert rel_err(table[1], r).max() < 1e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n_tx", [1, 2, 7])
+def test_coverage_table_builder_count_invariant(ctx, capi, orc, n_tx, monkeypatch):
+    """The transmitter states of a coverage table are built by builder threads
+    on helper contexts while the calling thread renders; the table is bitwise
+    the same for a serial build (0), one builder and more builders than
+    transmitters, and matches the oracle."""
+    import oracle as O
+    sc = capi.synth_scene(3000, 2, 1, 5)
+    scene, cond, _, ocond = _setup_cond(capi, ctx, orc, sc)
+    oscene = orc.scene(sc, "rssi")
+    grid, og = capi.Grid(18, 36, 6, 1.0), O.Grid(18, 36, 6, 1.0)
+    tx = capi.synth_points(n_tx, 17, "bench.tx", [-4, -3, -1.5], [4, 3, 1.5])
+    rx = capi.synth_points(45, 19, "bench.rx", [-4, -3, -1.5], [4, 3, 1.5])
+    tables = {}
+    for d in (0, 1, 2, 3, 8):
+        monkeypatch.setenv("RXGS_COV_BUILDERS", str(d))
+        tables[d] = scene.coverage_table(cond, grid, tx, rx)
+    for d, tb in tables.items():
+        assert np.array_equal(tb, tables[0]), d
+    for t in range(n_tx):
+        j = (7 * t) % 45
+        want = orc.predict(oscene, ocond, og, tx[t], rx[j], "rssi")[0]
+        assert rel_err(tables[8][t, j], want) < TOL, (t, j)
