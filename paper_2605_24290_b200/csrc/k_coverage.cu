@@ -56,10 +56,11 @@ constexpr int kCovThreads = 256;
 // LT == 0 (other l_max): re-read per row from the transposed cache.
 template <int LT>
 #ifndef RXGS_COV_MINB
-#define RXGS_COV_MINB 3  // A/B (config 3, cov_signal phase per table): 2 CTAs + 4 ahead 43.7 ms, 3 CTAs + 8 ahead 36.1 ms
+#define RXGS_COV_MINB 4  // A/B (config 3, ms per table / cov_signal phase): 3 CTAs + 8 ahead 111.2 / 42,
+                          // 4 + 4 107.3 / 36, 4 + 8 (spills) 115.2 / 46, 5 + 4 125 / 55; 2 + 4 (earlier) 43.7 phase
 #endif
 #ifndef RXGS_COV_AHEAD
-#define RXGS_COV_AHEAD 8
+#define RXGS_COV_AHEAD 4
 #endif
 __global__ void __launch_bounds__(kCovThreads, RXGS_COV_MINB) k_cov_signal(CondDev c, const int* __restrict__ n_rows,
                                                             const int* __restrict__ rows, int n_rx, int L,
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(kCovThreads, RXGS_COV_MINB) k_cov_signal(CondD
 #pragma unroll
     for (int l = 0; l < LT; ++l) areg[l] = s_a[l * kCovThreads + tid];
     constexpr int kAhead = RXGS_COV_AHEAD;  // y-cache rows in flight per thread
+    static_assert(kCovRows % kAhead == 0, "the y-cache ring walks whole 32-row blocks");
     float4 yq[kAhead];
 #pragma unroll
     for (int q = 0; q < kAhead; ++q) yq[q] = load_y(q);
