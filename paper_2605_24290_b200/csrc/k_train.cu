@@ -356,9 +356,15 @@ __global__ void k_entry_keys(DevGrid g, int K, const int64_t* __restrict__ tile_
     }
 }
 
-__global__ void k_key_hist(int64_t n, const int* __restrict__ keys, int* __restrict__ hist) {
+// entries per Gaussian; the unwalked entries' sentinel key K is not counted
+// (the exclusive scan of hist[0..K] never reads hist[K], and those entries
+// would otherwise serialise on one counter)
+__global__ void k_key_hist(int64_t n, int K, const int* __restrict__ keys, int* __restrict__ hist) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (i < n) atomicAdd(hist + keys[i], 1);
+    if (i < n) {
+        const int k = keys[i];
+        if (k < K) atomicAdd(hist + k, 1);
+    }
 }
 
 // d_s[k][j] = sum of the k's walked entries, in tile order.
@@ -1142,7 +1148,7 @@ int train_regroup(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
         k_entry_keys<<<st.grid.n_tiles, 128, 0, s>>>(st.grid, K, st.tile_offsets.as<int64_t>(), st.list.as<int>(),
                                                       st.walk_len.as<int>(), reinterpret_cast<int*>(keys),
                                                       st.gauss_ent.as<int>());
-        k_key_hist<<<static_cast<unsigned>((E + 255) / 256), 256, 0, s>>>(E, reinterpret_cast<int*>(keys), hist);
+        k_key_hist<<<static_cast<unsigned>((E + 255) / 256), 256, 0, s>>>(E, K, reinterpret_cast<int*>(keys), hist);
         int bits = 1;
         while ((1 << bits) <= K) ++bits;
         RXGS_CUDA(cudaMemsetAsync(work, 0, sizeof(int) * radix_sort_work_ints(En), s));
