@@ -2,7 +2,8 @@
 # Training-step evidence for profiles/: launch lists of the Stage-II step
 # (spectrum L1: tcgen05 conditioning forward / backward; default loss: FP32
 # SIMT conditioning for SSIM parity) and of the joint step
-# (scripts/probe_joint.py, K=100k, 16 samples, TxState rebuilt per step),
+# (scripts/probe_joint.py, K=100k, 16 samples, as bench.py: Stage II reuses
+# one TxState built before the 3 profiled steps, the joint step rebuilds it),
 # and one ncu --set full capture of each training kernel.  Run under
 # gpurun; then `python scripts/write_profiles.py <tag>` here.
 TAG=${1:-r2}

@@ -17,11 +17,23 @@ cond.build_occupancy(scene, 32, olo, ohi)
 grid = capi.Grid(90, 360, 8, 1.0)
 rx = capi.synth_points(16, 23, "bench.train.rx", [-4, -3, -1.5], [4, 3, 1.5], 0.05)
 tg = np.random.default_rng(29).uniform(0, 2, (16, grid.cells)).astype(np.float32)
-stage2 = len(sys.argv) > 1 and sys.argv[1].startswith("stage2")
-hyper = capi.Trainer.L1_ONLY if len(sys.argv) > 1 and sys.argv[1] == "stage2l1" else None
+# as bench.py's config-4 legs: stage2l1 (spectrum L1), stage2 (the reference's
+# default loss), joint (L1, geometry on).  Stage II caches the transmitter
+# state (trainer.cpp:417-427: built once, before the profiled steps); the
+# joint step rebuilds it from the moving geometry every step.
+mode = sys.argv[1] if len(sys.argv) > 1 else "joint"
+stage2 = mode.startswith("stage2")
+if mode == "stage2":
+    hyper = list(capi.Trainer.DEFAULTS)
+    hyper[3], hyper[4] = 0.2, 0.1
+else:
+    hyper = list(capi.Trainer.L1_ONLY)
 tr = capi.Trainer(ctx, scene, cond, hyper, geometry=(not stage2) or None)
+tx = np.array([0.3, -0.2, 0.1])
+st = scene.tx_state(tx, grid)
 for _ in range(3):
-    st = scene.tx_state(np.array([0.3, -0.2, 0.1]), grid)
+    if not stage2:
+        st = scene.tx_state(tx, grid)
     tr.grads(st, rx, tg)
     tr.apply()
 torch.cuda.synchronize()
