@@ -354,8 +354,13 @@ __device__ __forceinline__ double normalization(int l, int am) {  // radiance.cp
     return sqrt((2.0 * l + 1.0) / (4.0 * kPi) * ratio);
 }
 
-// Per-Gaussian finalisation (sphraster.cpp:615-731).
-__global__ void k_bwd_finalize(int K, int l_max, int C, int n_rx, const int* __restrict__ culled,
+// Per-Gaussian finalisation (sphraster.cpp:615-731).  LT > 0: l_max == LT
+// at compile time -- the Legendre tables stay in registers and each
+// component's basis derivatives (normalization, cos / sin of m phi) are
+// formed once per Gaussian instead of once per receiver; the same
+// expressions in the same order, so the results are bit-identical.
+template <int LT>
+__global__ void k_bwd_finalize(int K, int l_max_rt, int C, int n_rx, const int* __restrict__ culled,
                                const double* __restrict__ geom, const double* __restrict__ basis64,
                                const double* __restrict__ coeffs, const double* __restrict__ raw_geo,
                                const double2* __restrict__ raw_ds, const double* __restrict__ ls,
@@ -363,6 +368,7 @@ __global__ void k_bwd_finalize(int K, int l_max, int C, int n_rx, const int* __r
                                double* __restrict__ d_q, double* __restrict__ d_tau, double* __restrict__ d_coeffs) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= K) return;
+    const int l_max = LT > 0 ? LT : l_max_rt;
     const int L = (l_max + 1) * (l_max + 1);
     for (int a = 0; a < 3; ++a) d_pos[3 * k + a] = d_ls[3 * k + a] = 0.0;
     for (int a = 0; a < 4; ++a) d_q[4 * k + a] = 0.0;
@@ -378,7 +384,8 @@ __global__ void k_bwd_finalize(int K, int l_max, int C, int n_rx, const int* __r
     double d_theta = rg[5], d_phi = rg[6];
 
     // ---- basis jet (radiance.cpp:39-77, 94-114) and coefficient gradients
-    double P[(kMaxLmax + 1) * (kMaxLmax + 2) / 2], D[(kMaxLmax + 1) * (kMaxLmax + 2) / 2];
+    constexpr int kPT = LT > 0 ? (LT + 1) * (LT + 2) / 2 : (kMaxLmax + 1) * (kMaxLmax + 2) / 2;
+    double P[kPT], D[kPT];
     {
         const double x = cos(theta), s = sin(theta);
 #define AT(l, m) P[(l) * ((l) + 1) / 2 + (m)]
@@ -403,6 +410,44 @@ __global__ void k_bwd_finalize(int K, int l_max, int C, int n_rx, const int* __r
             }
     }
     const double* B = basis64 + static_cast<size_t>(k) * L * 2;
+    if constexpr (LT > 0) {
+        constexpr int LL = (LT + 1) * (LT + 1);
+        double tb[LL][4];  // per component: d/dtheta (re, im) and d/dphi (re, im) of the basis
+#pragma unroll
+        for (int l = 0; l <= LT; ++l)
+#pragma unroll
+            for (int m = -l; m <= l; ++m) {
+                const int comp = l * l + m + l, am = m < 0 ? -m : m;
+                const double nrm = normalization(l, am);
+                const double cm = cos(m * phi), sm = sin(m * phi);
+                const double dth = nrm * DAT(l, am);
+                const double bre = nrm * AT(l, am) * cm, bim = nrm * AT(l, am) * sm;
+                tb[comp][0] = dth * cm;
+                tb[comp][1] = dth * sm;
+                tb[comp][2] = -m * bim;
+                tb[comp][3] = m * bre;
+            }
+        for (int j = 0; j < n_rx; ++j)
+            for (int c = 0; c < C; ++c) {
+                const double2 ds = raw_ds[(static_cast<size_t>(k) * n_rx + j) * C + c];
+                if (ds.x == 0.0 && ds.y == 0.0) continue;
+                const size_t cbase = (static_cast<size_t>(j) * K + k) * stride;
+#pragma unroll
+                for (int comp = 0; comp < LL; ++comp) {
+                    const size_t ci = cbase + (static_cast<size_t>(comp) * C + c) * 2;
+                    const double br = B[2 * comp], bi = B[2 * comp + 1];
+                    if (d_coeffs) {
+                        d_coeffs[ci] += ds.x * br + ds.y * bi;
+                        d_coeffs[ci + 1] += -ds.x * bi + ds.y * br;
+                    }
+                    const double a_co = coeffs[ci], b_co = coeffs[ci + 1];
+                    const double db_re = ds.x * a_co + ds.y * b_co;
+                    const double db_im = -ds.x * b_co + ds.y * a_co;
+                    d_theta += db_re * tb[comp][0] + db_im * tb[comp][1];
+                    d_phi += db_re * tb[comp][2] + db_im * tb[comp][3];
+                }
+            }
+    } else
     for (int j = 0; j < n_rx; ++j)
         for (int c = 0; c < C; ++c) {
             const double2 ds = raw_ds[(static_cast<size_t>(k) * n_rx + j) * C + c];
@@ -577,7 +622,8 @@ cudaError_t launch_backward_render(const rxgs_txstate_s& st, const rxgs_scene_s&
         k_bwd_gauss_reduce<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, s>>>(K, n_jc, n_chunks, st.entries,
                                                                                   st.gauss_off.as<int>(),
                                                           st.gauss_ent.as<int>(), ent_geo, ent_ds, raw_geo, raw_ds);
-        k_bwd_finalize<<<(K + 63) / 64, 64, 0, s>>>(K, st.l_max, C, n_rx, st.culled.as<int>(), st.geom.as<double>(),
+        auto fin = st.l_max == 2 ? k_bwd_finalize<2> : k_bwd_finalize<0>;
+        fin<<<(K + 63) / 64, 64, 0, s>>>(K, st.l_max, C, n_rx, st.culled.as<int>(), st.geom.as<double>(),
                                                     st.basis64.as<double>(), d_coeffs_in, raw_geo, raw_ds,
                                                     sc.d_ls.as<double>(), sc.d_q.as<double>(), d_pos, d_ls, d_q,
                                                     d_tau, d_coeffs);
