@@ -1022,10 +1022,16 @@ __global__ void k_global_bwd(CondDev c, int n_rx, const double* __restrict__ rx,
         }
         in[i] = v;
     }
-    if (threadIdx.x < 4) {
-        double s = 0.0;
-        for (int b = 0; b < n_red; ++b) s += red_part[(static_cast<size_t>(b) * n_rx * L + row) * 4 + threadIdx.x];
-        dy[threadIdx.x] = (c.additive && threadIdx.x < 2) ? 0.0 : s;
+    {  // dy[q] = sum of the n_red k_global_red partials: warp q, lane l sums
+       // b = l, l + 32, ... in order, then a fixed shuffle tree (deterministic)
+        const int q = threadIdx.x >> 5, ln = threadIdx.x & 31;
+        if (q < 4) {
+            double s = 0.0;
+            for (int b = ln; b < n_red; b += 32) s += red_part[(static_cast<size_t>(b) * n_rx * L + row) * 4 + q];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+            if (ln == 0) dy[q] = (c.additive && q < 2) ? 0.0 : s;
+        }
     }
     __syncthreads();
     for (int o = threadIdx.x; o < H; o += blockDim.x) {
