@@ -1357,7 +1357,9 @@ cudaError_t launch_global_bwd(const rxgs_cond_s& cs, const rxgs_scene_s& sc, con
                               double* gslice, double* grad, cudaStream_t s) {
     const CondDev d = make_dev(cs);
     const int npair = n_rx * cs.L;
-    k_global_red<<<n_red, 128, 0, s>>>(st.needed_count.as<int>(), st.needed_order.as<int>(), cs.L, n_rx,
+    // one pass over the pairs per thread (a 128-thread block ran 144 pairs as two passes)
+    const int red_threads = std::min(1024, (npair + 31) / 32 * 32);
+    k_global_red<<<n_red, red_threads, 0, s>>>(st.needed_count.as<int>(), st.needed_order.as<int>(), cs.L, n_rx,
                                        st.basis32.as<float2>(), st.gb32.as<float2>(), u, red_part);
     const int n_gpar = static_cast<int>(cs.F * 3 + (cs.o_emb - cs.o_gw1) + cs.L * cs.dc);
     const size_t smem = sizeof(double) * (2 * cs.gin + 4 * cs.hidden + 4);
