@@ -272,14 +272,26 @@ int rxgs_train_grads(rxgs_trainer t, rxgs_txstate st, const double* rx, int n_rx
     ctx->cond_kernel = train_cond >= 0 ? train_cond : (l1_only ? 0 : 1);
     const bool tc_cond = ctx->cond_kernel == 0 && c && cond_tc_eligible(c);
     if (tc_cond) TRY(refresh_local_w3(c, s));
+    // the forward compositor on tcgen05 with the f32 field output where the
+    // conditioning forward is (the L1 loss; RXGS_TRAIN_COMP=0: FP32 SIMT)
+    static const bool train_comp = [] {
+        const char* v = std::getenv("RXGS_TRAIN_COMP");
+        return !(v && v[0] == '0');
+    }();
+    const bool tc_comp = tc_cond && train_comp && ctx->composite_kernel != 1 && composite_tc_eligible(*st);
     const cudaError_t ef = launch_cond_signal(c, *sc, *st, d_rx, n_rx, ctx->ag.as<float>(),
-                                              ctx->signals.as<float2>(), nullptr, s);
+                                              tc_comp ? SigOut::presplit(ctx->signals.p)
+                                                      : SigOut(ctx->signals.as<float2>()),
+                                              nullptr, s);
     ctx->cond_kernel = saved;
     RXGS_CUDA(ef);
     RXGS_CUDA(t->field32.ensure(sizeof(float) * 2 * static_cast<size_t>(n_rx) * P));
     CompositeOut co;
     co.field32 = t->field32.as<float>();
-    RXGS_CUDA(launch_composite(*st, ctx->signals.as<float2>(), n_rx, co, s));
+    if (tc_comp)
+        RXGS_CUDA(launch_composite_tc(*st, ctx->signals.as<uint2>(), n_rx, co, s));
+    else
+        RXGS_CUDA(launch_composite(*st, ctx->signals.as<float2>(), n_rx, co, s));
     // ---- loss + aggregate adjoint
     RXGS_CUDA(t->G.ensure(sizeof(float2) * static_cast<size_t>(n_rx) * P));
     RXGS_CUDA(t->loss_part.ensure(sizeof(double) * 16 * n_rx));
