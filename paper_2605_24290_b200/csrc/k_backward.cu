@@ -79,11 +79,15 @@ __global__ void k_aggregate_bwd(DevGrid g, int modality, int n_rx, int C, const 
 }
 
 // ------------------------------------------------------------------ signals in FP64
+// rows: all K x n_rx (rows == nullptr) or the state's needed Gaussians only
+// (the re-walk reads the signals of walked entries, all among them)
 __global__ void k_signals64(int K, int L, int C, int n_rx, const int* __restrict__ culled,
-                            const double* __restrict__ basis64, const double* __restrict__ co, double2* __restrict__ sig) {
+                            const double* __restrict__ basis64, const double* __restrict__ co, double2* __restrict__ sig,
+                            const int* __restrict__ rows, const int* __restrict__ n_rows) {
     const long long row = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-    if (row >= static_cast<long long>(K) * n_rx) return;
-    const int k = static_cast<int>(row / n_rx), j = static_cast<int>(row % n_rx);
+    const long long n_k = rows ? *n_rows : K;
+    if (row >= n_k * n_rx) return;
+    const int k = rows ? rows[row / n_rx] : static_cast<int>(row / n_rx), j = static_cast<int>(row % n_rx);
     const size_t stride = static_cast<size_t>(L) * C * 2;
     const double* cb = co + (static_cast<size_t>(j) * K + k) * stride;
     const double* b = basis64 + static_cast<size_t>(k) * L * 2;
@@ -598,14 +602,16 @@ cudaError_t launch_aggregate_bwd(const DevGrid& g, int modality, int n_rx, int c
 cudaError_t launch_backward_render(const rxgs_txstate_s& st, const rxgs_scene_s& sc, const double* d_coeffs_in,
                                    int n_rx, const double* d_values, double2* sig64, double* ent_geo,
                                    double2* ent_ds, double* raw_geo, double2* raw_ds, double* d_pos, double* d_ls,
-                                   double* d_q, double* d_tau, double* d_coeffs, cudaStream_t s) {
+                                   double* d_q, double* d_tau, double* d_coeffs, cudaStream_t s, bool needed_only) {
     const DevGrid& g = st.grid;
     const int K = st.k, C = st.channels, L = st.L;
     const int n_jc = n_rx * C;
-    const long long rows = static_cast<long long>(K) * n_rx;
+    const long long n_k = needed_only ? (st.needed_host >= 0 ? st.needed_host : st.visible) : K;
+    const long long rows = n_k * n_rx;
     if (rows > 0)
-        k_signals64<<<static_cast<unsigned>((rows + 255) / 256), 256, 0, s>>>(K, L, C, n_rx, st.culled.as<int>(),
-                                                                             st.basis64.as<double>(), d_coeffs_in, sig64);
+        k_signals64<<<static_cast<unsigned>((rows + 255) / 256), 256, 0, s>>>(
+            K, L, C, n_rx, st.culled.as<int>(), st.basis64.as<double>(), d_coeffs_in, sig64,
+            needed_only ? st.needed_order.as<int>() : nullptr, needed_only ? st.needed_count.as<int>() : nullptr);
     const int n_chunks = (n_jc + kNC - 1) / kNC;
     if (st.entries > 0) {
         cudaMemsetAsync(ent_geo, 0, sizeof(double) * 7 * st.entries * n_chunks, s);

@@ -404,7 +404,8 @@ size_t bwd_geo_bytes(int64_t entries, int n_jc);
 cudaError_t launch_backward_render(const rxgs_txstate_s& st, const rxgs_scene_s& sc, const double* d_coeffs_in,
                                    int n_rx, const double* d_values, double2* sig64, double* ent_geo,
                                    double2* ent_ds, double* raw_geo, double2* raw_ds, double* d_pos, double* d_ls,
-                                   double* d_q, double* d_tau, double* d_coeffs, cudaStream_t s);
+                                   double* d_q, double* d_tau, double* d_coeffs, cudaStream_t s,
+                                   bool needed_only = false);  // coefficients valid for the needed rows only
 
 cudaError_t launch_refresh_gb(const rxgs_scene_s& sc, rxgs_txstate_s& st, cudaStream_t s);
 cudaError_t launch_loss_spectrum(int n_rx, int P, const float* field, const float* target, double l_weight,

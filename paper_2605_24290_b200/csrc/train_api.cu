@@ -93,8 +93,8 @@ int geometry_grads(rxgs_trainer t, rxgs_txstate_s& st, const double* d_rx, int n
     RXGS_CUDA(t->co64.ensure(std::max<size_t>(nco, 1) * sizeof(double)));
     if (t->c) {
         // only the needed rows: the re-walk reads signals of walked entries, and
-        // the basis-jet term only rows with a non-zero signal adjoint
-        RXGS_CUDA(cudaMemsetAsync(t->co64.p, 0, nco * sizeof(double), s));
+        // the basis-jet term only rows with a non-zero signal adjoint (the
+        // other rows are never read: no clearing)
         if (cond_tc_eligible(t->c)) {  // local branch on tcgen05, the affines in FP64
             TRY(refresh_local_w3(t->c, s));
             RXGS_CUDA(t->ylocal.ensure(std::max<size_t>(static_cast<size_t>(K) * n_rx, 1) * sizeof(float4)));
@@ -126,7 +126,8 @@ int geometry_grads(rxgs_trainer t, rxgs_txstate_s& st, const double* d_rx, int n
     RXGS_CUDA(launch_backward_render(st, *sc, t->co64.as<double>(), n_rx, t->dv64.as<double>(), t->b_sig.as<double2>(),
                                      t->b_eg.as<double>(), t->b_eds.as<double2>(), t->b_rg.as<double>(),
                                      t->b_rds.as<double2>(), gt, gt + 4 * static_cast<size_t>(K),
-                                     gt + 7 * static_cast<size_t>(K), gt + 3 * static_cast<size_t>(K), nullptr, s));
+                                     gt + 7 * static_cast<size_t>(K), gt + 3 * static_cast<size_t>(K), nullptr, s,
+                                     t->c != nullptr));
     double* dst = t->grad.as<double>() + t->n_base + t->n_par;
     if (accumulate) {
         RXGS_CUDA(launch_add64(t->n_geo, gt, dst, s));
