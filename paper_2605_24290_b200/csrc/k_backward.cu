@@ -22,8 +22,10 @@ namespace {
 #endif
 constexpr int kNC = RXGS_BWD_NC;  // (receiver, channel) pairs per walk pass (one receiver chunk)
 
-__device__ __forceinline__ double wrap_pm_pi(double a) {
-    a = fmod(a, kTwoPi);
+__device__ __forceinline__ double wrap_pm_pi(double a) {  // linalg.hpp:152-157
+    // fmod(a, 2 pi) returns a exactly when |a| < 2 pi (always, for two
+    // azimuths in [0, 2 pi)): the software FP64 fmod is skipped there
+    if (!(fabs(a) < kTwoPi)) a = fmod(a, kTwoPi);
     if (a > kPi) a -= kTwoPi;
     if (a <= -kPi) a += kTwoPi;
     return a;

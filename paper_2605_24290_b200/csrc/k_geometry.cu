@@ -17,7 +17,9 @@ namespace rxgs_b200 {
 namespace {
 
 __device__ __forceinline__ double wrap_two_pi(double a) {  // linalg.hpp:160-164
-    a = fmod(a, kTwoPi);
+    // fmod(a, 2 pi) is exact and returns a itself when |a| < 2 pi (an atan2
+    // result always): the software FP64 fmod is skipped there
+    if (!(fabs(a) < kTwoPi)) a = fmod(a, kTwoPi);
     if (a < 0.0) a += kTwoPi;
     return a;
 }

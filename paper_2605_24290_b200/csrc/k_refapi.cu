@@ -245,7 +245,7 @@ __global__ void k_cond_forward64(CondDev c, Occ64 g, int K, const double* __rest
 
 // ---- materialised render_field in FP64 (sphraster.cpp:190-315)
 __device__ __forceinline__ double wrap_pm_pi64(double a) {  // linalg.hpp:152-157
-    a = fmod(a, kTwoPi);
+    if (!(fabs(a) < kTwoPi)) a = fmod(a, kTwoPi);  // fmod returns a exactly below 2 pi
     if (a > kPi) a -= kTwoPi;
     if (a <= -kPi) a += kTwoPi;
     return a;
