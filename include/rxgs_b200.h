@@ -291,7 +291,12 @@ int rxgs_render_queries(rxgs_ctx ctx, rxgs_scene scene, rxgs_cond c, rxgs_txstat
  * rssi_table[t*candidates + c]).  The Tx-independent conditioning (local
  * branch per (Gaussian, rx), global branch per rx) is computed once and
  * reused for every transmitter.  cond may be NULL (unconditioned scene).
- * Requires channels == 1. */
+ * Requires channels == 1.  With two or more transmitters the per-Tx states
+ * are built by up to 4 host threads (RXGS_COV_BUILDERS, 0 = serial), each on
+ * a helper context of ctx (own stream and buffer pool, created on first use
+ * and freed with ctx) while the calling thread renders on ctx's stream; the
+ * table is bitwise the same for any builder count.  The call returns after
+ * ctx's stream has finished the table. */
 int rxgs_coverage_table(rxgs_ctx ctx, rxgs_scene scene, rxgs_cond cond, const rxgs_grid* grid,
                         const double* tx, int n_tx, const double* rx, int n_rx, float* out_rssi);
 
