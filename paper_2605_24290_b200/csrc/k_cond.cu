@@ -59,9 +59,15 @@ __global__ void __launch_bounds__(kGlobThreads) k_cond_global(CondDev c, const d
     double* h2 = h1 + CP * H;            // CP x H
     const double* p = c.p64;
     const int tid = threadIdx.x;
+    // staging: several loads in flight per thread (a one-receiver call is
+    // one CTA, latency-bound on this)
+#pragma unroll 8
     for (int i = tid; i < gin * H; i += blockDim.x) w1t[(i % gin) * H + i / gin] = p[c.o_gw1 + i];
+#pragma unroll 8
     for (int i = tid; i < H * H; i += blockDim.x) w2t[(i % H) * H + i / H] = p[c.o_gw2 + i];
+#pragma unroll 4
     for (int i = tid; i < NY * H; i += blockDim.x) w3[i] = p[c.o_gw3 + i];
+#pragma unroll 4
     for (int i = tid; i < c.L * c.dc; i += blockDim.x) emb[i] = p[c.o_emb + i];
     for (int i = tid; i < H; i += blockDim.x) {
         b1[i] = p[c.o_gb1 + i];
