@@ -34,6 +34,7 @@
 // plus the block's offset from the (digit, block) scan gives each item its
 // output position.
 #include <algorithm>
+#include <type_traits>
 
 #include "rxgs_internal.cuh"
 
@@ -49,8 +50,8 @@ constexpr int kPassM = kPassWarps * 32 * kPassRounds;  // items per block (2048)
 
 constexpr int kTileWarps = 8;
 constexpr int kTileThreads = kTileWarps * 32;
-constexpr int kTileRounds = 32;
-constexpr int kTileM = kTileWarps * 32 * kTileRounds;  // entries per block (8192)
+// entries per block of the emit / tile-scatter passes: the template
+// parameter M (2048 or 8192, by entry count; bin_tiles)
 constexpr int kFusedTiles = 4096;                      // tile ids of the fused pass: 12 bits
 
 constexpr int kScanItems = 8;
@@ -422,12 +423,13 @@ struct EntryMap {
 };
 
 // Block-wide inclusive max-scan of own[0..n) in place (kTileThreads threads,
-// n <= kTileM): warp w scans its contiguous kTileM / kTileWarps elements 32 at
+// n <= M): warp w scans its contiguous M / kTileWarps elements 32 at
 // a time (lane-contiguous, conflict-free), then applies the max of the
 // earlier warps' totals.
+template <int M>
 __device__ __forceinline__ void block_max_scan(int* own, int n) {
     __shared__ int wm[kTileWarps];
-    constexpr int SEG = kTileM / kTileWarps;
+    constexpr int SEG = M / kTileWarps;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int* seg = own + warp * SEG;
     const int len = min(SEG, max(0, n - warp * SEG));
@@ -453,39 +455,41 @@ __device__ __forceinline__ void block_max_scan(int* own, int n) {
 // per entry: the scan values of ranks r0 .. r0 + nseg - 1 (relative to e0)
 // go to seg[], every rank marks its first entry in own[], and a max-scan
 // spreads the marks -- own[q] = rank index (from r0) of entry q.  Every rank
-// with tiles has >= 1 entry, so kTileM + 2 ranks cover a block unless
+// with tiles has >= 1 entry, so M + 2 ranks cover a block unless
 // zero-count ranks sit between them (only possible through the host-span
 // API); then the entries binary-search the scan in global memory instead.
+template <int M>
 __device__ __forceinline__ EntryMap map_entries(const int* __restrict__ bfirst, const int* __restrict__ blast,
                                                 int64_t e0, int n, const int64_t* __restrict__ scan, int* seg,
                                                 int* own) {
     const int r0 = bfirst[blockIdx.x];
     const int need = blast[blockIdx.x] - r0 + 1;
-    if (need > kTileM + 2) return {r0, need, true};
+    if (need > M + 2) return {r0, need, true};
     for (int i = threadIdx.x; i < need; i += blockDim.x) seg[i] = static_cast<int>(scan[r0 + i] - e0);
     for (int q = threadIdx.x; q < n; q += blockDim.x) own[q] = 0;
     __syncthreads();
     for (int i = threadIdx.x + 1; i < need; i += blockDim.x)
         if (seg[i] < n) atomicMax(&own[seg[i]], i);
     __syncthreads();
-    block_max_scan(own, n);
+    block_max_scan<M>(own, n);
     return {r0, need, false};
 }
 
 // bfirst[b] / blast[b]: the ranks holding the first and the last entry of
-// block b (blocks of kTileM entries), from the scan in one pass over the
+// block b (blocks of M entries), from the scan in one pass over the
 // ranks -- no per-block binary search.
+template <int M>
 __global__ void k_block_ranks(int K, int64_t E, const int64_t* __restrict__ scan, int* __restrict__ bfirst,
                               int* __restrict__ blast) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= K) return;
     const int64_t a = scan[r], c = scan[r + 1];
     if (c <= a) return;
-    const int64_t nb = (E + kTileM - 1) / kTileM;
-    for (int64_t b = (a + kTileM - 1) / kTileM; b * kTileM < c; ++b) bfirst[b] = r;
+    const int64_t nb = (E + M - 1) / M;
+    for (int64_t b = (a + M - 1) / M; b * M < c; ++b) bfirst[b] = r;
     // block b ends at entry min(E, (b + 1) M) - 1
-    for (int64_t b = a / kTileM; b < nb; ++b) {
-        const int64_t last = min(E, (b + 1) * kTileM) - 1;
+    for (int64_t b = a / M; b < nb; ++b) {
+        const int64_t last = min(E, (b + 1) * M) - 1;
         if (last >= c) break;
         if (last >= a) blast[b] = r;
     }
@@ -520,6 +524,7 @@ __device__ __forceinline__ int entry_tile(int j, int4 sp, int tiles_p) {
 // (tile, rank) of every entry, in entry (= rank) order, coalesced; with
 // hist != nullptr also the block's tile histogram hist[t * nb + b] (the
 // fused counting-sort path, n_tiles <= kFusedTiles).
+template <int M>
 __global__ void __launch_bounds__(kTileThreads) k_emit_entries(int64_t E, int nb, int n_tiles, int tiles_p,
                                                                 const int64_t* __restrict__ scan,
                                                                 const int* __restrict__ bfirst,
@@ -528,14 +533,14 @@ __global__ void __launch_bounds__(kTileThreads) k_emit_entries(int64_t E, int nb
                                                                 uint32_t* __restrict__ tkey, int* __restrict__ tval,
                                                                 int* __restrict__ hist) {
     extern __shared__ int sm[];
-    int* seg = sm;                  // kTileM + 2
-    int* own = seg + kTileM + 2;    // kTileM
-    int* h = own + kTileM;          // n_tiles (hist only)
+    int* seg = sm;                  // M + 2
+    int* own = seg + M + 2;         // M
+    int* h = own + M;               // n_tiles (hist only)
     if (hist)
         for (int t = threadIdx.x; t < n_tiles; t += kTileThreads) h[t] = 0;
-    const int64_t e0 = static_cast<int64_t>(blockIdx.x) * kTileM;
-    const int n = static_cast<int>(E - e0 < kTileM ? E - e0 : int64_t{kTileM});
-    const EntryMap m = map_entries(bfirst, blast, e0, n, scan, seg, own);
+    const int64_t e0 = static_cast<int64_t>(blockIdx.x) * M;
+    const int n = static_cast<int>(E - e0 < M ? E - e0 : int64_t{M});
+    const EntryMap m = map_entries<M>(bfirst, blast, e0, n, scan, seg, own);
     for (int q = threadIdx.x; q < n; q += kTileThreads) {
         int j;
         const int i = entry_rank(q, e0, seg, own, scan, m, &j);
@@ -552,12 +557,13 @@ __global__ void __launch_bounds__(kTileThreads) k_emit_entries(int64_t E, int nb
 // Stable scatter of the entries by tile (rank order within a tile) from the
 // emitted (tile, rank) arrays; writes list[pos] = Gaussian, keys[pos] =
 // (tile << 32) | rank, and the tile offsets.
-// Stable counting-sort pass by tile of one block's kTileM entries.  The
+// Stable counting-sort pass by tile of one block's M entries.  The
 // ranking (warp ballots, warp-private counters) gives every entry its output
 // position; the entries are then staged in shared memory in (tile, rank)
 // order, aliased over the consumed per-warp counters, and written out so
 // that consecutive threads write consecutive list / key positions (runs of
 // one tile) instead of 32 scattered tiles per warp store.
+template <int M>
 __global__ void __launch_bounds__(kTileThreads) k_tile_scatter(int64_t E, int nb, int n_tiles,
                                                                 const uint32_t* __restrict__ tkey,
                                                                 const int* __restrict__ tval,
@@ -572,30 +578,31 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_scatter(int64_t E, int nb
     int* s_tot = ls + n_tiles;             // kTileThreads: scan scratch
     uint16_t* wc = reinterpret_cast<uint16_t*>(s_tot + kTileThreads);  // kTileWarps x n_tiles (< 8192 each)
     int* st_r = reinterpret_cast<int*>(wc);                                // staged ranks (aliases wc)
-    uint16_t* st_t = reinterpret_cast<uint16_t*>(st_r + kTileM);           // staged tiles
+    uint16_t* st_t = reinterpret_cast<uint16_t*>(st_r + M);                // staged tiles
+    constexpr int kRounds = M / kTileThreads;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < kTileWarps * n_tiles; i += kTileThreads) wc[i] = 0;
     if (blockIdx.x == 0)
         for (int t = threadIdx.x; t <= n_tiles; t += kTileThreads) tile_offsets[t] = base[t];
     __syncthreads();
-    const int64_t e0 = static_cast<int64_t>(blockIdx.x) * kTileM;
-    const int n = static_cast<int>(E - e0 < kTileM ? E - e0 : int64_t{kTileM});
-    const int q0 = warp * (kTileM / kTileWarps);
+    const int64_t e0 = static_cast<int64_t>(blockIdx.x) * M;
+    const int n = static_cast<int>(E - e0 < M ? E - e0 : int64_t{M});
+    const int q0 = warp * (M / kTileWarps);
     const unsigned lt = lanemask_lt();
-    uint32_t pk[kTileRounds];  // tile, then tile << 12 | local rank (< 1024 per warp)
+    uint32_t pk[kRounds];  // tile, then tile << 12 | local rank (< 1024 per warp)
 #pragma unroll
-    for (int it = 0; it < kTileRounds; ++it) {
+    for (int it = 0; it < kRounds; ++it) {
         const int q = q0 + it * 32 + lane;
         pk[it] = q < n ? __ldg(tkey + e0 + q) : 0u;
     }
-    int rv[kTileRounds];
+    int rv[kRounds];
 #pragma unroll
-    for (int it = 0; it < kTileRounds; ++it) {
+    for (int it = 0; it < kRounds; ++it) {
         const int q = q0 + it * 32 + lane;
         rv[it] = q < n ? __ldg(tval + e0 + q) : 0;
     }
 #pragma unroll
-    for (int it = 0; it < kTileRounds; ++it) {
+    for (int it = 0; it < kRounds; ++it) {
         const bool ok = q0 + it * 32 + lane < n;
         const int t = static_cast<int>(pk[it]);
         const unsigned peers = match_digit<12>(static_cast<unsigned>(t), ok);
@@ -647,15 +654,15 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_scatter(int64_t E, int nb
     }
     __syncthreads();
     // local position of every entry (reads wc), then stage over wc
-    int lp[kTileRounds];
+    int lp[kRounds];
 #pragma unroll
-    for (int it = 0; it < kTileRounds; ++it) {
+    for (int it = 0; it < kRounds; ++it) {
         const int t = static_cast<int>(pk[it] >> 12);
         lp[it] = ls[t] + wc[warp * n_tiles + t] + static_cast<int>(pk[it] & 0xFFFu);
     }
     __syncthreads();
 #pragma unroll
-    for (int it = 0; it < kTileRounds; ++it) {
+    for (int it = 0; it < kRounds; ++it) {
         if (q0 + it * 32 + lane >= n) continue;
         st_r[lp[it]] = rv[it];
         st_t[lp[it]] = static_cast<uint16_t>(pk[it] >> 12);
@@ -807,52 +814,64 @@ int bin_tiles(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
         RXGS_CUDA(cudaMemsetAsync(st.tile_offsets.p, 0, sizeof(int64_t) * (n_tiles + 1), s));
         return RXGS_OK;
     }
-    const int nbt = static_cast<int>((E + kTileM - 1) / kTileM);
-    RXGS_CUDA(st.rank.ensure(sizeof(int) * 2 * (nbt + 1)));  // per-block first / last ranks
-    int* bfirst = st.rank.as<int>();
-    int* blast = bfirst + nbt + 1;
-    k_block_ranks<<<(K + 255) / 256, 256, 0, s>>>(K, E, st.scan.as<int64_t>(), bfirst, blast);
-    // entries (tile, rank) | pair temporaries | count matrix etc. in scratch_b
-    const size_t o_v = al256(4 * (E + 1)), o_kt = o_v + al256(4 * (E + 1)), o_vt = o_kt + al256(4 * (E + 1)),
-                 o_w = o_vt + al256(4 * (E + 1));
-    const bool fused = n_tiles <= kFusedTiles;
-    const size_t mat_ints = fused ? static_cast<size_t>(n_tiles) * nbt + 2 * (n_tiles + 1) + 64
-                                  : radix_sort_work_ints(static_cast<int>(E));
-    RXGS_CUDA(ctx->scratch_b.ensure(o_w + 4 * mat_ints));
-    char* pb = ctx->scratch_b.as<char>();
-    uint32_t* tk = reinterpret_cast<uint32_t*>(pb);
-    int* tv = reinterpret_cast<int*>(pb + o_v);
-    int* mat = reinterpret_cast<int*>(pb + o_w);
-    const size_t sm_e = 4 * (2 * static_cast<size_t>(kTileM) + 2 + (fused ? n_tiles : 0));
-    RXGS_CUDA(cudaFuncSetAttribute(k_emit_entries, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm_e)));
-    if (fused) {
-        int* tot = mat + static_cast<size_t>(n_tiles) * nbt;
-        int* tbase = tot + n_tiles + 1;
-        unsigned* counter = reinterpret_cast<unsigned*>(tbase + n_tiles + 1);
-        RXGS_CUDA(cudaMemsetAsync(counter, 0, 4, s));
-        k_emit_entries<<<nbt, kTileThreads, sm_e, s>>>(E, nbt, n_tiles, st.grid.tiles_p, st.scan.as<int64_t>(), bfirst,
-                                                       blast, spans_sorted, tk, tv, mat);
-        k_matrix_scan<<<n_tiles, 256, 0, s>>>(n_tiles, nbt, mat, tot, tbase, counter);
-        const size_t sm_s = 4 * (2 * static_cast<size_t>(n_tiles) + kTileThreads) +
-                            std::max(2 * static_cast<size_t>(kTileWarps) * n_tiles, 6 * static_cast<size_t>(kTileM));
-        RXGS_CUDA(cudaFuncSetAttribute(k_tile_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(sm_s)));
-        k_tile_scatter<<<nbt, kTileThreads, sm_s, s>>>(E, nbt, n_tiles, tk, tv, st.order.as<int>(), mat, tbase,
-                                                       st.list.as<int>(), st.keys.as<uint64_t>(),
-                                                       st.tile_offsets.as<int64_t>());
-    } else {
-        // generic: LSD passes on the tile id, then lists / keys / offsets
-        const int En = static_cast<int>(E);
-        RXGS_CUDA(cudaMemsetAsync(mat, 0, 4 * mat_ints, s));
-        k_emit_entries<<<nbt, kTileThreads, sm_e, s>>>(E, nbt, n_tiles, st.grid.tiles_p, st.scan.as<int64_t>(), bfirst,
-                                                       blast, spans_sorted, tk, tv, nullptr);
-        RXGS_CUDA(radix_sort_pairs(En, bits_for(n_tiles), tk, tv, reinterpret_cast<uint32_t*>(pb + o_kt),
-                                   reinterpret_cast<int*>(pb + o_vt), mat, false, s));
-        k_pairs_final<<<static_cast<unsigned>((E + 255) / 256), 256, 0, s>>>(E, tk, tv, st.order.as<int>(),
-                                                                             st.list.as<int>(),
-                                                                             st.keys.as<uint64_t>());
-        k_offsets<<<static_cast<unsigned>((E + 1 + 255) / 256), 256, 0, s>>>(E, n_tiles, tk,
-                                                                              st.tile_offsets.as<int64_t>());
+    // entries per block of the emit / tile-scatter passes: 2048 below ~1.2M
+    // entries (config 2: 169 blocks instead of 43 on 148 SMs), else 8192; the
+    // stable counting sort gives the same lists and keys for either
+    auto bin_entries = [&](auto m_c) -> int {
+        constexpr int M = decltype(m_c)::value;
+        const int nbt = static_cast<int>((E + M - 1) / M);
+        RXGS_CUDA(st.rank.ensure(sizeof(int) * 2 * (nbt + 1)));  // per-block first / last ranks
+        int* bfirst = st.rank.as<int>();
+        int* blast = bfirst + nbt + 1;
+        k_block_ranks<M><<<(K + 255) / 256, 256, 0, s>>>(K, E, st.scan.as<int64_t>(), bfirst, blast);
+        // entries (tile, rank) | pair temporaries | count matrix etc. in scratch_b
+        const size_t o_v = al256(4 * (E + 1)), o_kt = o_v + al256(4 * (E + 1)), o_vt = o_kt + al256(4 * (E + 1)),
+                     o_w = o_vt + al256(4 * (E + 1));
+        const bool fused = n_tiles <= kFusedTiles;
+        const size_t mat_ints = fused ? static_cast<size_t>(n_tiles) * nbt + 2 * (n_tiles + 1) + 64
+                                      : radix_sort_work_ints(static_cast<int>(E));
+        RXGS_CUDA(ctx->scratch_b.ensure(o_w + 4 * mat_ints));
+        char* pb = ctx->scratch_b.as<char>();
+        uint32_t* tk = reinterpret_cast<uint32_t*>(pb);
+        int* tv = reinterpret_cast<int*>(pb + o_v);
+        int* mat = reinterpret_cast<int*>(pb + o_w);
+        const size_t sm_e = 4 * (2 * static_cast<size_t>(M) + 2 + (fused ? n_tiles : 0));
+        RXGS_CUDA(cudaFuncSetAttribute(k_emit_entries<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm_e)));
+        if (fused) {
+            int* tot = mat + static_cast<size_t>(n_tiles) * nbt;
+            int* tbase = tot + n_tiles + 1;
+            unsigned* counter = reinterpret_cast<unsigned*>(tbase + n_tiles + 1);
+            RXGS_CUDA(cudaMemsetAsync(counter, 0, 4, s));
+            k_emit_entries<M><<<nbt, kTileThreads, sm_e, s>>>(E, nbt, n_tiles, st.grid.tiles_p, st.scan.as<int64_t>(), bfirst,
+                                                           blast, spans_sorted, tk, tv, mat);
+            k_matrix_scan<<<n_tiles, 256, 0, s>>>(n_tiles, nbt, mat, tot, tbase, counter);
+            const size_t sm_s = 4 * (2 * static_cast<size_t>(n_tiles) + kTileThreads) +
+                                std::max(2 * static_cast<size_t>(kTileWarps) * n_tiles, 6 * static_cast<size_t>(M));
+            RXGS_CUDA(cudaFuncSetAttribute(k_tile_scatter<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(sm_s)));
+            k_tile_scatter<M><<<nbt, kTileThreads, sm_s, s>>>(E, nbt, n_tiles, tk, tv, st.order.as<int>(), mat, tbase,
+                                                           st.list.as<int>(), st.keys.as<uint64_t>(),
+                                                           st.tile_offsets.as<int64_t>());
+        } else {
+            // generic: LSD passes on the tile id, then lists / keys / offsets
+            const int En = static_cast<int>(E);
+            RXGS_CUDA(cudaMemsetAsync(mat, 0, 4 * mat_ints, s));
+            k_emit_entries<M><<<nbt, kTileThreads, sm_e, s>>>(E, nbt, n_tiles, st.grid.tiles_p, st.scan.as<int64_t>(), bfirst,
+                                                           blast, spans_sorted, tk, tv, nullptr);
+            RXGS_CUDA(radix_sort_pairs(En, bits_for(n_tiles), tk, tv, reinterpret_cast<uint32_t*>(pb + o_kt),
+                                       reinterpret_cast<int*>(pb + o_vt), mat, false, s));
+            k_pairs_final<<<static_cast<unsigned>((E + 255) / 256), 256, 0, s>>>(E, tk, tv, st.order.as<int>(),
+                                                                                 st.list.as<int>(),
+                                                                                 st.keys.as<uint64_t>());
+            k_offsets<<<static_cast<unsigned>((E + 1 + 255) / 256), 256, 0, s>>>(E, n_tiles, tk,
+                                                                                  st.tile_offsets.as<int64_t>());
+        }
+        return RXGS_OK;
+    };
+    {
+        const int rc = E < (int64_t{1} << 20) + (int64_t{1} << 18) ? bin_entries(std::integral_constant<int, 2048>{})
+                                                                  : bin_entries(std::integral_constant<int, 8192>{});
+        if (rc) return rc;
     }
     ctx->launches += 20;
     const cudaError_t e = cudaGetLastError();
