@@ -34,6 +34,7 @@
 // plus the block's offset from the (digit, block) scan gives each item its
 // output position.
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "rxgs_internal.cuh"
@@ -45,8 +46,12 @@ constexpr int kRadixBits = 8;
 constexpr int kBins = 1 << kRadixBits;
 constexpr int kPassWarps = 8;
 constexpr int kPassThreads = kPassWarps * 32;
-constexpr int kPassRounds = 8;
-constexpr int kPassM = kPassWarps * 32 * kPassRounds;  // items per block (2048)
+#ifndef RXGS_PASS_SMALL_N
+#define RXGS_PASS_SMALL_N 400000
+#endif
+#ifndef RXGS_PASS_SMALL_M
+#define RXGS_PASS_SMALL_M 512  // A/B at K = 100k (config-2 step): 2048 3.285 ms, 1024 3.291, 512 3.260
+#endif
 
 constexpr int kTileWarps = 8;
 constexpr int kTileThreads = kTileWarps * 32;
@@ -108,14 +113,15 @@ __device__ __forceinline__ T block_incl_scan(T v, T* warp_sums, T* total) {
 
 // ---------------------------------------------------------------- generic LSD pass
 // hist[d * nb + b] = number of items of block b with digit d.
+template <int M>
 __global__ void __launch_bounds__(kPassThreads) k_radix_hist(int n, int nb, const uint32_t* __restrict__ kin,
                                                               int shift, int* __restrict__ hist) {
     __shared__ int h[kBins];
     for (int d = threadIdx.x; d < kBins; d += kPassThreads) h[d] = 0;
     __syncthreads();
     const int b = blockIdx.x;
-    const int i1 = min(n, (b + 1) * kPassM);
-    for (int i = b * kPassM + threadIdx.x; i < i1; i += kPassThreads)
+    const int i1 = min(n, (b + 1) * M);
+    for (int i = b * M + threadIdx.x; i < i1; i += kPassThreads)
         atomicAdd(&h[(kin[i] >> shift) & (kBins - 1)], 1);
     __syncthreads();
     for (int d = threadIdx.x; d < kBins; d += kPassThreads) hist[d * nb + b] = h[d];
@@ -165,6 +171,7 @@ __global__ void k_matrix_scan(int rows, int nb, int* __restrict__ mat, int* __re
 // Stable scatter of one LSD pass (see the file header).  The block's items
 // are staged in shared memory in (digit, input) order and written out with
 // consecutive threads on consecutive output positions (runs of one digit).
+template <int M>
 __global__ void __launch_bounds__(kPassThreads) k_radix_scatter(int n, int nb, const uint32_t* __restrict__ kin,
                                                                  const int* __restrict__ vin, uint32_t* __restrict__ kout,
                                                                  int* __restrict__ vout, int shift,
@@ -172,25 +179,26 @@ __global__ void __launch_bounds__(kPassThreads) k_radix_scatter(int n, int nb, c
                                                                  const int* __restrict__ base) {
     __shared__ int wc[kPassWarps][kBins];
     __shared__ int gb[kBins], lb[kBins];  // global / local start of the block's run of each digit
-    __shared__ uint32_t sk[kPassM];
-    __shared__ int sv[kPassM];
+    constexpr int kRounds = M / kPassThreads;
+    __shared__ uint32_t sk[M];
+    __shared__ int sv[M];
     __shared__ int wsum[kPassWarps];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < kPassWarps * kBins; i += kPassThreads) (&wc[0][0])[i] = 0;
     __syncthreads();
     const int b = blockIdx.x;
-    const int i0 = b * kPassM + warp * (kPassM / kPassWarps);
+    const int i0 = b * M + warp * (M / kPassWarps);
     const unsigned lt = lanemask_lt();
-    uint32_t kk[kPassRounds];
-    int vv[kPassRounds], loc[kPassRounds];
+    uint32_t kk[kRounds];
+    int vv[kRounds], loc[kRounds];
 #pragma unroll
-    for (int it = 0; it < kPassRounds; ++it) {  // all loads in flight before the ranking
+    for (int it = 0; it < kRounds; ++it) {  // all loads in flight before the ranking
         const int i = i0 + it * 32 + lane;
         kk[it] = i < n ? __ldg(kin + i) : 0u;
         vv[it] = i < n ? __ldg(vin + i) : 0;
     }
 #pragma unroll
-    for (int it = 0; it < kPassRounds; ++it) {
+    for (int it = 0; it < kRounds; ++it) {
         const bool ok = i0 + it * 32 + lane < n;
         const int d = static_cast<int>((kk[it] >> shift) & (kBins - 1));
         const unsigned peers = match_digit<kRadixBits>(static_cast<unsigned>(d), ok);
@@ -217,9 +225,9 @@ __global__ void __launch_bounds__(kPassThreads) k_radix_scatter(int n, int nb, c
         lb[d] = inc - s;
     }
     __syncthreads();
-    const int n_blk = n - b * kPassM < kPassM ? n - b * kPassM : kPassM;
+    const int n_blk = n - b * M < M ? n - b * M : M;
 #pragma unroll
-    for (int it = 0; it < kPassRounds; ++it) {
+    for (int it = 0; it < kRounds; ++it) {
         if (i0 + it * 32 + lane >= n) continue;
         const int d = static_cast<int>((kk[it] >> shift) & (kBins - 1));
         const int lp = lb[d] + wc[warp][d] + loc[it];
@@ -278,6 +286,7 @@ __device__ __forceinline__ int depth_shift(unsigned long long lo, unsigned long 
 
 // 32-bit order-preserving depth keys (index-ordered input) + the first
 // pass's histogram.
+template <int M>
 __global__ void __launch_bounds__(kPassThreads) k_depth_keys(int K, int nb, const uint64_t* __restrict__ dk,
                                                               const unsigned long long* __restrict__ mm,
                                                               uint32_t* __restrict__ key, int* __restrict__ val,
@@ -288,8 +297,8 @@ __global__ void __launch_bounds__(kPassThreads) k_depth_keys(int K, int nb, cons
     const unsigned long long lo = mm[0], hi = mm[1];
     const int sh = depth_shift(lo, hi);
     const int b = blockIdx.x;
-    const int i1 = min(K, (b + 1) * kPassM);
-    for (int i = b * kPassM + threadIdx.x; i < i1; i += kPassThreads) {
+    const int i1 = min(K, (b + 1) * M);
+    for (int i = b * M + threadIdx.x; i < i1; i += kPassThreads) {
         const unsigned long long v = dk[i];
         const uint32_t k = v == ~0ull ? 0xFFFFFFFFu : static_cast<uint32_t>((v - lo) >> sh);
         key[i] = k;
@@ -707,15 +716,29 @@ size_t al256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 // Stable LSD radix sort of (u32 key, int value) pairs on the low `bits` key
 // bits: kin/vin -> kin/vin (ping-ponging through ktmp/vtmp).  work: int
 // scratch of radix_sort_work_ints(n) (count matrix, totals, base, counter).
+// items per block of the LSD passes: blocks enough for the SMs at small n
+// (RXGS_PASS_SMALL_M below RXGS_PASS_SMALL_N items); RXGS_PASS_M overrides (512 / 1024 / 2048)
+static int pass_m(int n) {
+    static const int forced = [] {
+        const char* v = std::getenv("RXGS_PASS_M");
+        return v ? std::atoi(v) : 0;
+    }();
+    if (forced == 512 || forced == 1024 || forced == 2048) return forced;
+    return n <= RXGS_PASS_SMALL_N ? RXGS_PASS_SMALL_M : 2048;
+}
+
 size_t radix_sort_work_ints(int n) {
-    const int nb = (n + kPassM - 1) / kPassM;
+    const int nb = (n + pass_m(n) - 1) / pass_m(n);
     return static_cast<size_t>(kBins) * std::max(nb, 1) + 2 * (kBins + 1) + 64;
 }
 
 cudaError_t radix_sort_pairs(int n, int bits, uint32_t* kin, int* vin, uint32_t* ktmp, int* vtmp, int* work,
                              bool hist_ready, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
-    const int nb = (n + kPassM - 1) / kPassM;
+    const int M = pass_m(n);
+    const int nb = (n + M - 1) / M;
+    auto hist_k = M == 512 ? k_radix_hist<512> : (M == 1024 ? k_radix_hist<1024> : k_radix_hist<2048>);
+    auto scat_k = M == 512 ? k_radix_scatter<512> : (M == 1024 ? k_radix_scatter<1024> : k_radix_scatter<2048>);
     int* mat = work;
     int* tot = mat + static_cast<size_t>(kBins) * nb;
     int* base = tot + kBins + 1;
@@ -727,9 +750,9 @@ cudaError_t radix_sort_pairs(int n, int bits, uint32_t* kin, int* vin, uint32_t*
     int* vb = vtmp;
     for (int p = 0; p < passes; ++p) {
         const int shift = p * kRadixBits;
-        if (!(p == 0 && hist_ready)) k_radix_hist<<<nb, kPassThreads, 0, s>>>(n, nb, ka, shift, mat);
+        if (!(p == 0 && hist_ready)) hist_k<<<nb, kPassThreads, 0, s>>>(n, nb, ka, shift, mat);
         k_matrix_scan<<<kBins, 256, 0, s>>>(kBins, nb, mat, tot, base, counter);
-        k_radix_scatter<<<nb, kPassThreads, 0, s>>>(n, nb, ka, va, kb, vb, shift, mat, base);
+        scat_k<<<nb, kPassThreads, 0, s>>>(n, nb, ka, va, kb, vb, shift, mat, base);
         std::swap(ka, kb);
         std::swap(va, vb);
     }
@@ -765,7 +788,8 @@ int bin_tiles(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
     RXGS_CUDA(st.tile_offsets.ensure(sizeof(int64_t) * (n_tiles + 1)));
 
     // scratch_a: keys/values x2 | cnt_sorted | spans_sorted | radix work | block sums | [minmax, visible]
-    const int nbk = (K + kPassM - 1) / kPassM;
+    const int pm = pass_m(K);  // the same blocks as radix_sort_pairs (the first pass's histogram)
+    const int nbk = (K + pm - 1) / pm;
     const size_t o_k1 = 0, o_v1 = al256(4 * (K + 1)), o_k2 = o_v1 + al256(4 * (K + 1)),
                  o_v2 = o_k2 + al256(4 * (K + 1)), o_cnt = o_v2 + al256(4 * (K + 1)),
                  o_sp = o_cnt + al256(8 * (K + 2)), o_work = o_sp + al256(16 * (K + 1)),
@@ -791,7 +815,8 @@ int bin_tiles(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
         RXGS_CUDA(cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, s));
         k_depth_minmax<<<std::min((K + 255) / 256, 2 * ctx->sm_count), 256, 0, s>>>(K, st.depth_key.as<uint64_t>(),
                                                                                       mm);
-        k_depth_keys<<<nbk, kPassThreads, 0, s>>>(K, nbk, st.depth_key.as<uint64_t>(), mm, k1, v1, work);
+        auto dk_k = pm == 512 ? k_depth_keys<512> : (pm == 1024 ? k_depth_keys<1024> : k_depth_keys<2048>);
+        dk_k<<<nbk, kPassThreads, 0, s>>>(K, nbk, st.depth_key.as<uint64_t>(), mm, k1, v1, work);
         RXGS_CUDA(radix_sort_pairs(K, 32, k1, v1, k2, v2, work, true, s));
         k_depth_final<<<(K + 1 + 255) / 256, 256, 0, s>>>(K, k1, v1, st.depth_key.as<uint64_t>(),
                                                           st.spans.as<int4>(), st.order.as<int>(), cnt_sorted,
