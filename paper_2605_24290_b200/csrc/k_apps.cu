@@ -337,7 +337,7 @@ int rxgs_per_receiver_aggregate(rxgs_ctx ctx, int64_t n, const int32_t* rx, cons
     const size_t N1 = static_cast<size_t>(n) + 2;
     const size_t o_k = 0, o_v = al(4 * N1), o_kt = o_v + al(4 * N1), o_vt = o_kt + al(4 * N1),
                  o_w = o_vt + al(4 * N1), o_val = o_w + al(4 * wi), o_seg = o_val + al(8 * N1),
-                 o_bs = o_seg + al(8 * N1), o_rx = o_bs + al(8 * (N1 / 2048 + 2)), o_mean = o_rx + al(4 * N1),
+                 o_bs = o_seg + al(8 * N1), o_rx = o_bs + al(8 * scan_bsum_count(static_cast<int64_t>(n) + 1)), o_mean = o_rx + al(4 * N1),
                  o_cnt = o_mean + al(8 * N1), o_mom = o_cnt + al(8 * N1);
     RXGS_CUDA(buf.ensure(o_mom + 64));
     char* b = buf.as<char>();

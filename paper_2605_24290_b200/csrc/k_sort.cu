@@ -59,8 +59,8 @@ constexpr int kTileThreads = kTileWarps * 32;
 // parameter M (2048 or 8192, by entry count; bin_tiles)
 constexpr int kFusedTiles = 4096;                      // tile ids of the fused pass: 12 bits
 
-constexpr int kScanItems = 8;
-constexpr int kScanChunk = 256 * kScanItems;  // elements per block of the K scans
+// elements per block of the K scans: the template parameter CH, 2048, or
+// 512 up to RXGS_PASS_SMALL_N elements (scan_chunk)
 
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
@@ -370,17 +370,17 @@ __global__ void k_depth_final(int K, const uint32_t* __restrict__ ks, int* __res
 }
 
 // ---------------------------------------------------------------- K scans (int64)
-// Block-local exclusive scan of kScanChunk elements; block totals to bsum.
+// Block-local exclusive scan of CH elements; block totals to bsum.
 // Warp w scans its contiguous chunk 32 elements at a time (coalesced,
 // register shuffles), then adds the totals of the earlier warps.
 // T = int64_t or int (int sums accumulate in int64 and are written back narrowed).
-template <typename T>
+template <typename T, int CH>
 __global__ void __launch_bounds__(256) k_scan_blocks(int64_t n, const T* __restrict__ in, T* __restrict__ out,
                                                      int64_t* __restrict__ bsum) {
     __shared__ int64_t wt[8];
-    constexpr int SEG = kScanChunk / 8;
+    constexpr int SEG = CH / 8;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t b0 = blockIdx.x * static_cast<int64_t>(kScanChunk) + warp * SEG;
+    const int64_t b0 = blockIdx.x * static_cast<int64_t>(CH) + warp * SEG;
     int64_t v[SEG / 32];
     int64_t carry = 0;
 #pragma unroll
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(256) k_scan_blocks(int64_t n, const T* __restr
 }
 
 // out += sum of the block totals before this block.
-template <typename T>
+template <typename T, int CH>
 __global__ void k_scan_add(int64_t n, T* __restrict__ out, const int64_t* __restrict__ bsum) {
     __shared__ int64_t ws[32];
     int64_t p = 0;
@@ -420,8 +420,8 @@ __global__ void k_scan_add(int64_t n, T* __restrict__ out, const int64_t* __rest
     int64_t t;
     block_incl_scan(p, ws, &t);
     if (t == 0) return;
-    const int64_t b0 = blockIdx.x * static_cast<int64_t>(kScanChunk);
-    for (int i = threadIdx.x; i < kScanChunk; i += blockDim.x)
+    const int64_t b0 = blockIdx.x * static_cast<int64_t>(CH);
+    for (int i = threadIdx.x; i < CH; i += blockDim.x)
         if (b0 + i < n) out[b0 + i] += static_cast<T>(t);
 }
 
@@ -764,13 +764,20 @@ cudaError_t radix_sort_pairs(int n, int bits, uint32_t* kin, int* vin, uint32_t*
 }
 
 // Exclusive scan of n int64 / int (in -> out, may alias); bsum: scan_bsum_count(n) int64.
+static int scan_chunk(int64_t n) { return n <= RXGS_PASS_SMALL_N ? 512 : 2048; }
+
+template <typename T, int CH>
+static cudaError_t scan_chunks(int64_t n, const T* in, T* out, int64_t* bsum, cudaStream_t s) {
+    const unsigned nb = static_cast<unsigned>((n + CH - 1) / CH);
+    k_scan_blocks<T, CH><<<nb, 256, 0, s>>>(n, in, out, bsum);
+    if (nb > 1) k_scan_add<T, CH><<<nb, 256, 0, s>>>(n, out, bsum);
+    return cudaGetLastError();
+}
+
 template <typename T>
 static cudaError_t scan_any(int64_t n, const T* in, T* out, int64_t* bsum, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
-    const unsigned nb = static_cast<unsigned>((n + kScanChunk - 1) / kScanChunk);
-    k_scan_blocks<T><<<nb, 256, 0, s>>>(n, in, out, bsum);
-    if (nb > 1) k_scan_add<T><<<nb, 256, 0, s>>>(n, out, bsum);
-    return cudaGetLastError();
+    return scan_chunk(n) == 512 ? scan_chunks<T, 512>(n, in, out, bsum, s) : scan_chunks<T, 2048>(n, in, out, bsum, s);
 }
 cudaError_t scan_i64(int64_t n, const int64_t* in, int64_t* out, int64_t* bsum, cudaStream_t s) {
     return scan_any(n, in, out, bsum, s);
@@ -778,7 +785,7 @@ cudaError_t scan_i64(int64_t n, const int64_t* in, int64_t* out, int64_t* bsum, 
 cudaError_t scan_i32(int64_t n, const int* in, int* out, int64_t* bsum, cudaStream_t s) {
     return scan_any(n, in, out, bsum, s);
 }
-size_t scan_bsum_count(int64_t n) { return static_cast<size_t>(n / kScanChunk + 2); }
+size_t scan_bsum_count(int64_t n) { return static_cast<size_t>(n / scan_chunk(n) + 2); }
 
 int bin_tiles(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
     const int K = st.k;
@@ -794,7 +801,7 @@ int bin_tiles(rxgs_ctx ctx, rxgs_txstate_s& st, cudaStream_t s) {
                  o_v2 = o_k2 + al256(4 * (K + 1)), o_cnt = o_v2 + al256(4 * (K + 1)),
                  o_sp = o_cnt + al256(8 * (K + 2)), o_work = o_sp + al256(16 * (K + 1)),
                  o_bs = o_work + al256(4 * radix_sort_work_ints(K)),
-                 o_red = o_bs + al256(8 * ((K + 1) / kScanChunk + 2));
+                 o_red = o_bs + al256(8 * scan_bsum_count(K + 1));
     RXGS_CUDA(ctx->scratch_a.ensure(o_red + 256));
     char* base = ctx->scratch_a.as<char>();
     uint32_t* k1 = reinterpret_cast<uint32_t*>(base + o_k1);
@@ -941,7 +948,7 @@ int compact_needed(rxgs_ctx ctx, const rxgs_scene_s& sc, rxgs_txstate_s& st, cud
     RXGS_CUDA(st.needed_order.ensure(sizeof(int) * (K + 1)));
     RXGS_CUDA(st.needed_count.ensure(sizeof(int) * 4));
     RXGS_CUDA(st.scan.ensure(sizeof(int64_t) * (K + 2)));  // free after binning: the flag scan
-    RXGS_CUDA(ctx->scratch_b.ensure(sizeof(int64_t) * ((K + 1) / 2048 + 2)));
+    RXGS_CUDA(ctx->scratch_b.ensure(sizeof(int64_t) * scan_bsum_count(K + 1)));
     unsigned char* needed = st.needed.as<unsigned char>();
     RXGS_CUDA(cudaMemsetAsync(needed, 0, static_cast<size_t>(K + 1), s));
     RXGS_CUDA(cudaMemsetAsync(st.needed_count.p, 0, sizeof(int), s));
